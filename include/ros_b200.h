@@ -1,0 +1,180 @@
+/* ros_b200.h -- C ABI of the B200-native ROS (Reference-Oriented Storage)
+ * read path.  Plain pointers and sizes; no torch or C++ types.
+ *
+ * Every entry point returns an int status whose values are exactly the
+ * reference's refstore::Status codes
+ * (/root/reference/proj/include/refstore/types.hpp:22-41): 0 = ok,
+ * 1 invalid_argument, 2 invalid_state, 3 already_exists, 4 not_found,
+ * 5 version_regression, 6 manifest_conflict, 7 mutability_violation,
+ * 8 version_unavailable, 9 group_aborted, 10 server_unavailable,
+ * 11 transfer_failed, 12 checksum_mismatch, 13 not_serving, 14 timeout,
+ * 15 offload_failed, 16 protocol_error, 17 closed.
+ *
+ * Which reference interface each group replaces is cited per function; the
+ * bindings a maintainer would add on the reference side are in
+ * INTEGRATION.md.  Threading: one caller per rs_handle; a
+ * rs_cluster may be shared by handles on different threads.
+ */
+#ifndef ROS_B200_H
+#define ROS_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RS_ABI_VERSION 1
+
+typedef struct rs_cluster rs_cluster; /* ServerCore + ServeRegistry of this process */
+typedef struct rs_handle rs_handle;   /* ClientCore: one replica's shard handles   */
+
+/* ClientConfig (reference config.hpp:23-47) restricted to the knobs that shape
+ * the read path, plus the digest chunk size of the device path. */
+typedef struct {
+  uint64_t chunk_bytes;    /* digest/watermark unit, multiple of 16 (default 4096)   */
+  uint64_t tiny_threshold; /* ManifestLimits.tiny_threshold (default 2 MiB)          */
+  uint64_t group_target;   /* ManifestLimits.group_target (default 64 MiB)           */
+  int pipeline;            /* serve partially landed fills (default 1)               */
+  int checksum_retries;    /* failure reports per fill before giving up (default 3) */
+  double pull_timeout_s;   /* upstream silence before a failure report (default 4)  */
+  char datacenter[32];     /* ClientConfig.datacenter (default "dc0")                */
+} rs_config;
+
+/* Assignment (reference messages.hpp:40-52) minus the manifest bytes, which
+ * are read with rs_assignment_manifest / rs_manifest. */
+typedef struct {
+  uint64_t version;
+  char source_replica[128];
+  char source_endpoint[128];
+  int source_complete;
+  int cross_dc;
+  int seeding;
+  int local_seed_consume;
+} rs_assignment;
+
+/* ClientCore::Stats (client_core.hpp:44-52) + device-path timing. */
+typedef struct {
+  uint64_t bytes_pulled;
+  uint64_t bytes_pulled_cross_dc;
+  uint64_t bytes_copied_local;
+  uint64_t items_verified;
+  uint64_t checksum_failures;
+  uint64_t failure_reports;
+  uint64_t failovers;
+  float last_pull_ms;       /* CUDA-event time of the last fill's pull kernel     */
+  float last_publish_ms;    /* CUDA-event time of the last publish (digests+pack) */
+  uint64_t last_pull_bytes; /* bytes landed+verified by that kernel               */
+  uint32_t last_pull_launches;
+  uint64_t h2d_bytes;       /* descriptor uploads, cumulative                     */
+  uint64_t d2h_bytes;       /* status / digest read-backs, cumulative             */
+} rs_stats;
+
+/* ---- process-level objects ------------------------------------------------ */
+int rs_abi_version(void);
+const char* rs_status_name(int status);                     /* types.cpp:7-29  */
+void rs_config_default(rs_config* cfg);
+
+/* ServerCore (server_core.hpp:30-52) + ServeRegistry (transport.hpp:72-85).
+ * ServerConfig.pipeline / smart_skipping (config.hpp:15-21). */
+int rs_cluster_create(int pipeline, int smart_skipping, rs_cluster** out);
+void rs_cluster_destroy(rs_cluster* c);
+/* Planner trace: one event per line "<seq> <kind> k=v ..." (kinds as the
+ * reference's trace: assign, replicate_resolved, reassign, ...). */
+int rs_cluster_trace(rs_cluster* c, char* buf, size_t cap, size_t* len);
+/* ServerCore::listing (server_core.cpp:1276-1286) as "v:rep,rep;v:rep". */
+int rs_cluster_listing(rs_cluster* c, const char* model, char* buf, size_t cap, size_t* len);
+/* ServerCore::replica_view (server_core.hpp:42-50). lifecycle buffer >= 16. */
+int rs_cluster_view(rs_cluster* c, const char* model, const char* replica, char* lifecycle,
+                    uint64_t* version, uint32_t* serving, int* visible);
+/* Fault hook (MemNetwork::set_data_silent, transport_mem.hpp:33-46): a
+ * silent replica's data plane never answers, so its readers time out. */
+int rs_cluster_set_silent(rs_cluster* c, const char* model, const char* replica, int silent);
+
+/* ---- ClientCore API (paper Table 2; client_core.hpp:63-93) -------------- */
+int rs_open(rs_cluster* c, const char* model, const char* replica, uint32_t num_shards,
+            const rs_config* cfg, rs_handle** out);
+/* register_tensor (client_core.hpp:72-73): dev_ptr is caller-owned device
+ * memory that must outlive the handle (weights live in place). */
+int rs_register(rs_handle* h, uint32_t shard, const char* name, void* dev_ptr, uint64_t bytes);
+int rs_set_endpoint(rs_handle* h, uint32_t shard, const char* endpoint);
+/* Launch the shard's device work on this cudaStream_t (default: a private
+ * non-blocking stream). */
+int rs_set_stream(rs_handle* h, uint32_t shard, void* cuda_stream);
+int rs_publish(rs_handle* h, uint64_t version);              /* publish()   */
+int rs_unpublish(rs_handle* h);                              /* unpublish() */
+/* replicate(spec) / update(spec) -- spec "17" | "latest" | "latest-k".
+ * Blocking; a parked replicate waits up to wait_s for a version to appear. */
+int rs_replicate(rs_handle* h, const char* spec, double wait_s, uint64_t* out_version);
+int rs_update(rs_handle* h, const char* spec, double wait_s, int* changed, uint64_t* out_version);
+int rs_close(rs_handle* h);                                  /* close(); frees h */
+/* Plan view without side effects: the source `replica` would pull `shard`
+ * of `spec` from right now. */
+int rs_locate(rs_cluster* c, const char* model, const char* replica, const char* spec,
+              uint32_t shard, rs_assignment* out);
+int rs_current_version(rs_handle* h, uint64_t* out); /* not_found if none held */
+int rs_is_published(rs_handle* h);
+int rs_stats_get(rs_handle* h, rs_stats* out);
+/* Canonical manifest bytes of the shard's held version
+ * (TensorManifest::encode, manifest.cpp:103-139). */
+int rs_manifest(rs_handle* h, uint32_t shard, char* buf, size_t cap, size_t* len);
+/* The shard's per-chunk XXH64 table (device path integrity metadata). */
+int rs_chunk_digests(rs_handle* h, uint32_t shard, uint64_t* out, size_t cap, size_t* n);
+/* Drop the landed watermark so the next fill re-pulls every byte. */
+int rs_invalidate(rs_handle* h);
+
+/* ---- split phase: the caller drives the registry (replicated across
+ *      processes: every rank applies the same rs_server_* sequence) ------- */
+int rs_server_open(rs_cluster* c, const char* model, const char* replica, uint32_t num_shards,
+                   const char* datacenter, const char* const* endpoints);
+int rs_server_publish(rs_cluster* c, const char* model, const char* replica, uint64_t version,
+                      uint32_t num_shards, const char* const* manifests, const size_t* lens);
+int rs_server_unpublish(rs_cluster* c, const char* model, const char* replica);
+int rs_server_replicate(rs_cluster* c, const char* model, const char* replica, const char* spec);
+int rs_server_update(rs_cluster* c, const char* model, const char* replica, const char* spec,
+                     int has_current, uint64_t current);
+/* Outcome of the replica's latest op: done=0 while parked. */
+int rs_server_result(rs_cluster* c, const char* model, const char* replica, int* done,
+                     int* status, uint64_t* version, int* changed);
+int rs_server_complete(rs_cluster* c, const char* model, const char* replica, uint32_t shard,
+                       int outcome);
+int rs_server_failure_report(rs_cluster* c, const char* model, const char* replica,
+                             uint32_t shard, const char* failed_replica, int reason);
+int rs_server_close(rs_cluster* c, const char* model, const char* replica);
+/* Client half. */
+int rs_prepare_publish(rs_handle* h, uint64_t version);  /* digests+pack+manifest */
+int rs_commit_publish(rs_handle* h, uint64_t version, int status);
+/* Bind every shard to the registry's current assignment and start serving
+ * the empty fill (so downstream readers can chase it). */
+int rs_transfer_bind(rs_handle* h, uint64_t version);
+/* One fill attempt of every shard still pending; statuses/reasons per shard
+ * (reason 0 timeout/not serving, 1 checksum). */
+int rs_transfer_fill(rs_handle* h, int* statuses, int* reasons);
+int rs_transfer_finish(rs_handle* h, uint64_t version, int ok);
+/* Cross-process serve state (CUDA IPC handles + watermarks). */
+int rs_serve_export(rs_handle* h, uint32_t shard, void* buf, size_t cap, size_t* len);
+int rs_serve_import(rs_cluster* c, const void* blob, size_t len);
+
+/* ---- device primitives (kernel boundary) --------------------------------- */
+/* digest64 (digest.cpp:79-106) of n device spans; out is host memory. */
+int rs_digest_spans(const uint64_t* dev_ptrs, const uint64_t* lens, int n, uint64_t* out,
+                    int device);
+/* Synthetic bf16 weights into device memory. */
+int rs_synth_bf16(void* dev_dst, uint64_t n_elems, uint64_t seed, uint64_t first_elem,
+                  void* cuda_stream);
+/* Saturating RNE bf16 -> fp8 e4m3 on device. */
+int rs_bf16_to_e4m3(const void* dev_src, void* dev_dst, uint64_t n_elems, void* cuda_stream);
+/* copy_slice_locked (transport.cpp:51-69) + chunk verification, standalone:
+ * copy n_items (src -> dst, len) spans cut into chunk_bytes chunks, verify
+ * against expect (device, may be NULL) and write the computed chunk digests
+ * to out_digests (device, may be NULL).  Reports the kernel status. */
+int rs_pull_spans(const uint64_t* src_ptrs, const uint64_t* dst_ptrs, const uint64_t* lens,
+                  int n_items, uint64_t chunk_bytes, const uint64_t* expect_dev,
+                  uint64_t* out_digests_dev, int device, void* cuda_stream, int* kernel_code,
+                  float* kernel_ms);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ROS_B200_H */

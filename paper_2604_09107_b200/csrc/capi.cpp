@@ -1,0 +1,514 @@
+// extern "C" boundary of libros_b200.so (declared in include/ros_b200.h).
+#include "../../include/ros_b200.h"
+
+#include <cuda_runtime.h>
+
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "client.hpp"
+#include "device.hpp"
+#include "registry.hpp"
+
+struct rs_cluster {
+  rsb::Registry reg;
+  rsb::ServeRegistry serves;
+  explicit rs_cluster(rsb::Registry::Config c) : reg(c) {}
+};
+
+struct rs_handle {
+  rs_cluster* cluster = nullptr;
+  std::unique_ptr<rsb::Client> client;
+  std::vector<std::uint32_t> pending;  // split-phase fill: shards still to land
+};
+
+namespace {
+
+int st(rsb::Status s) { return static_cast<int>(s); }
+
+int put_bytes(const std::string& s, char* buf, size_t cap, size_t* len) {
+  if (len) *len = s.size();
+  if (buf && cap >= s.size()) std::memcpy(buf, s.data(), s.size());
+  else if (buf && cap < s.size()) return st(rsb::Status::invalid_argument);
+  return 0;
+}
+
+void fill_assignment(const rsb::Assignment& a, rs_assignment* out) {
+  std::memset(out, 0, sizeof(*out));
+  out->version = a.version;
+  std::strncpy(out->source_replica, a.source_replica.c_str(), sizeof(out->source_replica) - 1);
+  std::strncpy(out->source_endpoint, a.source_endpoint.c_str(), sizeof(out->source_endpoint) - 1);
+  out->source_complete = a.source_complete;
+  out->cross_dc = a.cross_dc;
+  out->seeding = a.seeding;
+  out->local_seed_consume = a.local_seed_consume;
+}
+
+rsb::ClientConfig to_cfg(const rs_config* c) {
+  rsb::ClientConfig cfg;
+  if (!c) return cfg;
+  if (c->chunk_bytes) cfg.chunk_bytes = c->chunk_bytes;
+  if (c->tiny_threshold) cfg.limits.tiny_threshold = c->tiny_threshold;
+  if (c->group_target) cfg.limits.group_target = c->group_target;
+  cfg.pipeline = c->pipeline != 0;
+  cfg.checksum_retries = c->checksum_retries;
+  if (c->pull_timeout_s > 0) cfg.pull_timeout_s = c->pull_timeout_s;
+  if (c->datacenter[0]) cfg.dc = std::string(c->datacenter, strnlen(c->datacenter, 32));
+  return cfg;
+}
+
+bool parse_spec(const char* spec, rsb::VersionSpec* out) {
+  if (!spec) return false;
+  auto r = rsb::VersionSpec::parse(spec);
+  if (!r) return false;
+  *out = *r;
+  return true;
+}
+
+}  // namespace
+
+extern "C" {
+
+int rs_abi_version(void) { return RS_ABI_VERSION; }
+
+const char* rs_status_name(int status) {
+  return rsb::status_name(static_cast<rsb::Status>(status));
+}
+
+void rs_config_default(rs_config* cfg) {
+  std::memset(cfg, 0, sizeof(*cfg));
+  rsb::ClientConfig d;
+  cfg->chunk_bytes = d.chunk_bytes;
+  cfg->tiny_threshold = d.limits.tiny_threshold;
+  cfg->group_target = d.limits.group_target;
+  cfg->pipeline = d.pipeline;
+  cfg->checksum_retries = d.checksum_retries;
+  cfg->pull_timeout_s = d.pull_timeout_s;
+  std::strncpy(cfg->datacenter, d.dc.c_str(), sizeof(cfg->datacenter) - 1);
+}
+
+int rs_cluster_create(int pipeline, int smart_skipping, rs_cluster** out) {
+  if (!out) return st(rsb::Status::invalid_argument);
+  rsb::Registry::Config c;
+  c.pipeline = pipeline != 0;
+  c.smart_skipping = smart_skipping != 0;
+  *out = new rs_cluster(c);
+  return 0;
+}
+
+void rs_cluster_destroy(rs_cluster* c) { delete c; }
+
+int rs_cluster_trace(rs_cluster* c, char* buf, size_t cap, size_t* len) {
+  if (!c) return st(rsb::Status::invalid_argument);
+  return put_bytes(c->reg.trace_text(), buf, cap, len);
+}
+
+int rs_cluster_listing(rs_cluster* c, const char* model, char* buf, size_t cap, size_t* len) {
+  if (!c || !model) return st(rsb::Status::invalid_argument);
+  std::string out;
+  for (const auto& [v, reps] : c->reg.listing(model)) {
+    if (!out.empty()) out += ';';
+    out += std::to_string(v) + ':';
+    bool first = true;
+    for (const auto& r : reps) {
+      if (!first) out += ',';
+      out += r;
+      first = false;
+    }
+  }
+  return put_bytes(out, buf, cap, len);
+}
+
+int rs_cluster_view(rs_cluster* c, const char* model, const char* replica, char* lifecycle,
+                    uint64_t* version, uint32_t* serving, int* visible) {
+  if (!c || !model || !replica) return st(rsb::Status::invalid_argument);
+  auto v = c->reg.view(model, replica);
+  if (!v) return st(rsb::Status::not_found);
+  if (lifecycle) std::strncpy(lifecycle, v->lifecycle.c_str(), 15), lifecycle[15] = 0;
+  if (version) *version = v->version.value_or(0);
+  if (serving) *serving = v->serving;
+  if (visible) *visible = v->visible;
+  return 0;
+}
+
+int rs_cluster_set_silent(rs_cluster* c, const char* model, const char* replica, int silent) {
+  if (!c || !model || !replica) return st(rsb::Status::invalid_argument);
+  c->serves.set_silent(model, replica, silent != 0);
+  return 0;
+}
+
+// ------------------------------------------------------------ ClientCore
+
+int rs_open(rs_cluster* c, const char* model, const char* replica, uint32_t num_shards,
+            const rs_config* cfg, rs_handle** out) {
+  if (!c || !model || !replica || !out || num_shards == 0 || !*model || !*replica)
+    return st(rsb::Status::invalid_argument);
+  auto* h = new rs_handle;
+  h->cluster = c;
+  h->client = std::make_unique<rsb::Client>(&c->reg, &c->serves, model, replica, num_shards,
+                                            to_cfg(cfg));
+  *out = h;
+  return 0;
+}
+
+int rs_register(rs_handle* h, uint32_t shard, const char* name, void* dev_ptr, uint64_t bytes) {
+  if (!h || !name) return st(rsb::Status::invalid_argument);
+  return st(h->client->register_tensor(shard, name, dev_ptr, bytes));
+}
+
+int rs_set_endpoint(rs_handle* h, uint32_t shard, const char* endpoint) {
+  if (!h || !endpoint || shard >= h->client->num_shards()) return st(rsb::Status::invalid_argument);
+  h->client->set_shard_endpoint(shard, endpoint);
+  return 0;
+}
+
+int rs_set_stream(rs_handle* h, uint32_t shard, void* cuda_stream) {
+  if (!h || shard >= h->client->num_shards()) return st(rsb::Status::invalid_argument);
+  h->client->set_stream(shard, static_cast<cudaStream_t>(cuda_stream));
+  return 0;
+}
+
+int rs_publish(rs_handle* h, uint64_t version) {
+  if (!h) return st(rsb::Status::invalid_argument);
+  return st(h->client->publish(version));
+}
+
+int rs_unpublish(rs_handle* h) {
+  if (!h) return st(rsb::Status::invalid_argument);
+  return st(h->client->unpublish());
+}
+
+int rs_replicate(rs_handle* h, const char* spec, double wait_s, uint64_t* out_version) {
+  rsb::VersionSpec vs;
+  if (!h || !parse_spec(spec, &vs)) return st(rsb::Status::invalid_argument);
+  rsb::VersionId v = 0;
+  auto s = h->client->replicate(vs, &v, wait_s > 0 ? wait_s : 0.0);
+  if (out_version) *out_version = v;
+  return st(s);
+}
+
+int rs_update(rs_handle* h, const char* spec, double wait_s, int* changed, uint64_t* out_version) {
+  rsb::VersionSpec vs;
+  if (!h || !parse_spec(spec, &vs)) return st(rsb::Status::invalid_argument);
+  bool ch = false;
+  rsb::VersionId v = 0;
+  auto s = h->client->update(vs, &ch, &v, wait_s > 0 ? wait_s : 0.0);
+  if (changed) *changed = ch;
+  if (out_version) *out_version = v;
+  return st(s);
+}
+
+int rs_close(rs_handle* h) {
+  if (!h) return st(rsb::Status::invalid_argument);
+  auto s = h->client->close();
+  delete h;
+  return st(s);
+}
+
+int rs_locate(rs_cluster* c, const char* model, const char* replica, const char* spec,
+              uint32_t shard, rs_assignment* out) {
+  rsb::VersionSpec vs;
+  if (!c || !model || !replica || !out || !parse_spec(spec, &vs))
+    return st(rsb::Status::invalid_argument);
+  auto r = c->reg.locate(model, replica, vs, shard);
+  if (!r) return st(r.status());
+  fill_assignment(*r, out);
+  return 0;
+}
+
+int rs_current_version(rs_handle* h, uint64_t* out) {
+  if (!h || !out) return st(rsb::Status::invalid_argument);
+  auto v = h->client->current_version();
+  if (!v) return st(rsb::Status::not_found);
+  *out = *v;
+  return 0;
+}
+
+int rs_is_published(rs_handle* h) { return h && h->client->is_published() ? 1 : 0; }
+
+int rs_stats_get(rs_handle* h, rs_stats* out) {
+  if (!h || !out) return st(rsb::Status::invalid_argument);
+  const auto& s = h->client->stats();
+  out->bytes_pulled = s.bytes_pulled;
+  out->bytes_pulled_cross_dc = s.bytes_pulled_cross_dc;
+  out->bytes_copied_local = s.bytes_copied_local;
+  out->items_verified = s.items_verified;
+  out->checksum_failures = s.checksum_failures;
+  out->failure_reports = s.failure_reports;
+  out->failovers = s.failovers;
+  out->last_pull_ms = s.last_pull_ms;
+  out->last_publish_ms = s.last_publish_ms;
+  out->last_pull_bytes = s.last_pull_bytes;
+  out->last_pull_launches = s.last_pull_launches;
+  out->h2d_bytes = s.h2d_bytes;
+  out->d2h_bytes = s.d2h_bytes;
+  return 0;
+}
+
+int rs_manifest(rs_handle* h, uint32_t shard, char* buf, size_t cap, size_t* len) {
+  if (!h) return st(rsb::Status::invalid_argument);
+  auto m = h->client->manifest_bytes(shard);
+  if (!m) return st(m.status());
+  return put_bytes(*m, buf, cap, len);
+}
+
+int rs_chunk_digests(rs_handle* h, uint32_t shard, uint64_t* out, size_t cap, size_t* n) {
+  if (!h) return st(rsb::Status::invalid_argument);
+  std::vector<std::uint64_t> d;
+  auto s = h->client->chunk_digests(shard, &d);
+  if (!rsb::ok(s)) return st(s);
+  if (n) *n = d.size();
+  if (out) {
+    if (cap < d.size()) return st(rsb::Status::invalid_argument);
+    std::memcpy(out, d.data(), d.size() * 8);
+  }
+  return 0;
+}
+
+int rs_invalidate(rs_handle* h) {
+  if (!h) return st(rsb::Status::invalid_argument);
+  h->client->invalidate();
+  return 0;
+}
+
+// ------------------------------------------------------------ split phase
+
+int rs_server_open(rs_cluster* c, const char* model, const char* replica, uint32_t num_shards,
+                   const char* datacenter, const char* const* endpoints) {
+  if (!c || !model || !replica || !endpoints) return st(rsb::Status::invalid_argument);
+  std::vector<std::string> eps;
+  for (uint32_t i = 0; i < num_shards; ++i) eps.emplace_back(endpoints[i] ? endpoints[i] : "");
+  return st(c->reg.open(model, replica, num_shards, datacenter ? datacenter : "dc0", eps));
+}
+
+int rs_server_publish(rs_cluster* c, const char* model, const char* replica, uint64_t version,
+                      uint32_t num_shards, const char* const* manifests, const size_t* lens) {
+  if (!c || !model || !replica || !manifests || !lens) return st(rsb::Status::invalid_argument);
+  std::vector<std::string> ms;
+  for (uint32_t i = 0; i < num_shards; ++i) ms.emplace_back(manifests[i], lens[i]);
+  rsb::OpOutcome o;
+  auto s = c->reg.publish(model, replica, version, ms, &o);
+  return st(rsb::ok(s) ? o.status : s);
+}
+
+int rs_server_unpublish(rs_cluster* c, const char* model, const char* replica) {
+  if (!c || !model || !replica) return st(rsb::Status::invalid_argument);
+  return st(c->reg.unpublish(model, replica, nullptr));
+}
+
+int rs_server_replicate(rs_cluster* c, const char* model, const char* replica, const char* spec) {
+  rsb::VersionSpec vs;
+  if (!c || !model || !replica || !parse_spec(spec, &vs)) return st(rsb::Status::invalid_argument);
+  return st(c->reg.replicate(model, replica, vs, nullptr));
+}
+
+int rs_server_update(rs_cluster* c, const char* model, const char* replica, const char* spec,
+                     int has_current, uint64_t current) {
+  rsb::VersionSpec vs;
+  if (!c || !model || !replica || !parse_spec(spec, &vs)) return st(rsb::Status::invalid_argument);
+  std::optional<rsb::VersionId> cur;
+  if (has_current) cur = current;
+  return st(c->reg.update(model, replica, vs, cur, nullptr));
+}
+
+int rs_server_result(rs_cluster* c, const char* model, const char* replica, int* done, int* status,
+                     uint64_t* version, int* changed) {
+  if (!c || !model || !replica) return st(rsb::Status::invalid_argument);
+  auto o = c->reg.op_result(model, replica);
+  if (done) *done = o.done;
+  if (status) *status = st(o.status);
+  if (version) *version = o.version.value_or(0);
+  if (changed) *changed = o.changed;
+  return 0;
+}
+
+int rs_server_complete(rs_cluster* c, const char* model, const char* replica, uint32_t shard,
+                       int outcome) {
+  if (!c || !model || !replica) return st(rsb::Status::invalid_argument);
+  c->reg.complete(model, replica, shard, static_cast<rsb::Status>(outcome));
+  return 0;
+}
+
+int rs_server_failure_report(rs_cluster* c, const char* model, const char* replica,
+                             uint32_t shard, const char* failed_replica, int reason) {
+  if (!c || !model || !replica || !failed_replica) return st(rsb::Status::invalid_argument);
+  auto r = c->reg.failure_report(model, replica, shard, failed_replica, reason);
+  return st(r.status());
+}
+
+int rs_server_close(rs_cluster* c, const char* model, const char* replica) {
+  if (!c || !model || !replica) return st(rsb::Status::invalid_argument);
+  return st(c->reg.close(model, replica));
+}
+
+int rs_prepare_publish(rs_handle* h, uint64_t version) {
+  if (!h) return st(rsb::Status::invalid_argument);
+  std::vector<std::string> ms;
+  return st(h->client->prepare_publish(version, &ms));
+}
+
+int rs_commit_publish(rs_handle* h, uint64_t version, int status) {
+  if (!h) return st(rsb::Status::invalid_argument);
+  h->client->commit_publish(version, static_cast<rsb::Status>(status));
+  return 0;
+}
+
+int rs_transfer_bind(rs_handle* h, uint64_t version) {
+  if (!h) return st(rsb::Status::invalid_argument);
+  auto& cl = *h->client;
+  std::vector<rsb::Assignment> as;
+  for (std::uint32_t i = 0; i < cl.num_shards(); ++i) {
+    auto a = h->cluster->reg.current_assignment(cl.model(), cl.replica(), i);
+    if (!a) return st(a.status());
+    as.push_back(std::move(*a));
+  }
+  auto s = cl.bind_all(as, version);
+  h->pending.clear();
+  if (rsb::ok(s))
+    for (std::uint32_t i = 0; i < cl.num_shards(); ++i) h->pending.push_back(i);
+  return st(s);
+}
+
+int rs_transfer_fill(rs_handle* h, int* statuses, int* reasons) {
+  if (!h) return st(rsb::Status::invalid_argument);
+  auto& cl = *h->client;
+  std::vector<rsb::Assignment> as(cl.num_shards());
+  for (std::uint32_t i : h->pending) {
+    auto a = h->cluster->reg.current_assignment(cl.model(), cl.replica(), i);
+    if (!a) return st(a.status());
+    as[i] = std::move(*a);
+  }
+  auto res = cl.fill_shards(as, h->pending);
+  std::vector<std::uint32_t> still;
+  int worst = 0;
+  for (std::uint32_t i = 0; i < cl.num_shards(); ++i) {
+    int s = st(res[i].status);
+    if (statuses) statuses[i] = s;
+    if (reasons) reasons[i] = res[i].reason;
+    bool was_pending = false;
+    for (auto p : h->pending) was_pending |= p == i;
+    if (was_pending && s != 0) {
+      still.push_back(i);
+      worst = s;
+    }
+  }
+  h->pending = std::move(still);
+  return worst;
+}
+
+int rs_transfer_finish(rs_handle* h, uint64_t version, int good) {
+  if (!h) return st(rsb::Status::invalid_argument);
+  h->client->finish_transfers(version, good != 0);
+  return 0;
+}
+
+int rs_serve_export(rs_handle* h, uint32_t shard, void* buf, size_t cap, size_t* len) {
+  if (!h) return st(rsb::Status::invalid_argument);
+  auto b = h->client->export_serve(shard);
+  if (!b) return st(b.status());
+  return put_bytes(*b, static_cast<char*>(buf), cap, len);
+}
+
+int rs_serve_import(rs_cluster* c, const void* blob, size_t len) {
+  if (!c || !blob) return st(rsb::Status::invalid_argument);
+  return st(c->serves.import_state(std::string(static_cast<const char*>(blob), len)));
+}
+
+// ------------------------------------------------------- device primitives
+
+int rs_digest_spans(const uint64_t* dev_ptrs, const uint64_t* lens, int n, uint64_t* out,
+                    int device) {
+  if (n < 0 || (n > 0 && (!dev_ptrs || !lens || !out))) return st(rsb::Status::invalid_argument);
+  if (n == 0) return 0;
+  int prev = 0;
+  cudaGetDevice(&prev);
+  cudaSetDevice(device);
+  rsb::DevBuf t;
+  int rc = 0;
+  if (!rsb::ok(t.alloc(device, 3 * std::size_t(n) * 8))) rc = st(rsb::Status::transfer_failed);
+  auto* d = static_cast<std::uint64_t*>(t.p);
+  if (!rc && (cudaMemcpy(d, dev_ptrs, n * 8, cudaMemcpyHostToDevice) != cudaSuccess ||
+              cudaMemcpy(d + n, lens, n * 8, cudaMemcpyHostToDevice) != cudaSuccess ||
+              rsb::dev::launch_span_digests(d, d + n, d + 2 * n, n, nullptr) != cudaSuccess ||
+              cudaMemcpy(out, d + 2 * n, n * 8, cudaMemcpyDeviceToHost) != cudaSuccess))
+    rc = st(rsb::Status::transfer_failed);
+  cudaSetDevice(prev);
+  return rc;
+}
+
+int rs_synth_bf16(void* dev_dst, uint64_t n_elems, uint64_t seed, uint64_t first_elem,
+                  void* cuda_stream) {
+  if (!dev_dst && n_elems) return st(rsb::Status::invalid_argument);
+  auto e = rsb::dev::launch_synth_bf16(static_cast<std::uint16_t*>(dev_dst), n_elems, seed,
+                                       first_elem, static_cast<cudaStream_t>(cuda_stream));
+  return e == cudaSuccess ? 0 : st(rsb::Status::transfer_failed);
+}
+
+int rs_bf16_to_e4m3(const void* dev_src, void* dev_dst, uint64_t n_elems, void* cuda_stream) {
+  if ((!dev_src || !dev_dst) && n_elems) return st(rsb::Status::invalid_argument);
+  auto e = rsb::dev::launch_bf16_to_e4m3(static_cast<const std::uint16_t*>(dev_src),
+                                         static_cast<std::uint8_t*>(dev_dst), n_elems,
+                                         static_cast<cudaStream_t>(cuda_stream));
+  return e == cudaSuccess ? 0 : st(rsb::Status::transfer_failed);
+}
+
+int rs_pull_spans(const uint64_t* src_ptrs, const uint64_t* dst_ptrs, const uint64_t* lens,
+                  int n_items, uint64_t chunk_bytes, const uint64_t* expect_dev,
+                  uint64_t* out_digests_dev, int device, void* cuda_stream, int* kernel_code,
+                  float* kernel_ms) {
+  if (n_items < 0 || chunk_bytes == 0 || chunk_bytes % 16 || chunk_bytes > (1u << 30))
+    return st(rsb::Status::invalid_argument);
+  int prev = 0;
+  cudaGetDevice(&prev);
+  cudaSetDevice(device);
+  auto stream = static_cast<cudaStream_t>(cuda_stream);
+  std::vector<rsb::dev::ItemDesc> descs(n_items);
+  std::uint32_t chunk = 0;
+  for (int i = 0; i < n_items; ++i) {
+    descs[i] = {src_ptrs[i], dst_ptrs ? dst_ptrs[i] : 0, lens[i], chunk,
+                static_cast<std::uint32_t>(chunk_bytes)};
+    chunk += static_cast<std::uint32_t>((lens[i] + chunk_bytes - 1) / chunk_bytes);
+  }
+  const std::size_t dbytes = descs.size() * sizeof(rsb::dev::ItemDesc);
+  rsb::DevBuf t;
+  int rc = 0;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  rsb::dev::PullStatus ps{};
+  if (!rsb::ok(t.alloc(device, dbytes + 128))) rc = st(rsb::Status::transfer_failed);
+  if (!rc) {
+    auto* base = static_cast<std::uint8_t*>(t.p);
+    rsb::dev::PullParams p{};
+    p.items = reinterpret_cast<const rsb::dev::ItemDesc*>(base);
+    p.n_items = static_cast<std::uint32_t>(n_items);
+    p.n_chunks = chunk;
+    p.n_batches = (chunk + rsb::dev::kBatchChunks - 1) / rsb::dev::kBatchChunks;
+    p.src_digests = expect_dev;
+    p.dst_digests = out_digests_dev;
+    p.work = reinterpret_cast<std::uint32_t*>(base + dbytes);
+    p.status = reinterpret_cast<rsb::dev::PullStatus*>(base + dbytes + 64);
+    p.timeout_ns = 4000000000ull;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    if ((dbytes && cudaMemcpyAsync(base, descs.data(), dbytes, cudaMemcpyHostToDevice, stream) !=
+                       cudaSuccess) ||
+        cudaMemsetAsync(base + dbytes, 0, 128, stream) != cudaSuccess ||
+        cudaEventRecord(e0, stream) != cudaSuccess ||
+        rsb::dev::launch_pull(p, rsb::dev::pull_grid(device), stream) != cudaSuccess ||
+        cudaEventRecord(e1, stream) != cudaSuccess ||
+        cudaMemcpyAsync(&ps, p.status, sizeof(ps), cudaMemcpyDeviceToHost, stream) != cudaSuccess ||
+        cudaStreamSynchronize(stream) != cudaSuccess)
+      rc = st(rsb::Status::transfer_failed);
+    float ms = 0;
+    if (!rc) cudaEventElapsedTime(&ms, e0, e1);
+    if (kernel_ms) *kernel_ms = ms;
+    if (kernel_code) *kernel_code = static_cast<int>(ps.code);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+  }
+  cudaSetDevice(prev);
+  return rc;
+}
+
+}  // extern "C"

@@ -1,0 +1,978 @@
+#include "client.hpp"
+
+#include <cuda.h>
+#include <unistd.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cstring>
+#include <thread>
+
+namespace rsb {
+
+namespace {
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (dev >= 0 && dev != prev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
+Status cuda_status(cudaError_t e) {
+  return e == cudaSuccess ? Status::ok : Status::transfer_failed;
+}
+
+#define RS_CUDA(expr)                              \
+  do {                                             \
+    cudaError_t _e = (expr);                       \
+    if (_e != cudaSuccess) return cuda_status(_e); \
+  } while (0)
+
+// cuMemGetAddressRange through the runtime's driver entry point (no libcuda
+// link dependency, so the library still loads on a GPU-less host).
+using GetRangeFn = CUresult (*)(CUdeviceptr*, size_t*, CUdeviceptr);
+GetRangeFn get_range_fn() {
+  static GetRangeFn fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return static_cast<GetRangeFn>(nullptr);
+    return reinterpret_cast<GetRangeFn>(p);
+  }();
+  return fn;
+}
+
+// Binary writer/reader for serve-state export blobs.
+struct W {
+  std::string s;
+  template <class T>
+  void pod(const T& v) {
+    s.append(reinterpret_cast<const char*>(&v), sizeof(T));
+  }
+  void str(const std::string& v) {
+    pod(static_cast<std::uint32_t>(v.size()));
+    s.append(v);
+  }
+  template <class T>
+  void vec(const std::vector<T>& v) {
+    pod(static_cast<std::uint32_t>(v.size()));
+    s.append(reinterpret_cast<const char*>(v.data()), v.size() * sizeof(T));
+  }
+};
+struct R {
+  const char* p;
+  std::size_t n, i = 0;
+  bool ok = true;
+  template <class T>
+  T pod() {
+    T v{};
+    if (i + sizeof(T) > n) {
+      ok = false;
+      return v;
+    }
+    std::memcpy(static_cast<void*>(&v), p + i, sizeof(T));
+    i += sizeof(T);
+    return v;
+  }
+  std::string str() {
+    auto len = pod<std::uint32_t>();
+    if (!ok || i + len > n) {
+      ok = false;
+      return {};
+    }
+    std::string v(p + i, len);
+    i += len;
+    return v;
+  }
+  template <class T>
+  std::vector<T> vec() {
+    auto len = pod<std::uint32_t>();
+    std::vector<T> v;
+    if (!ok || i + std::size_t(len) * sizeof(T) > n) {
+      ok = false;
+      return v;
+    }
+    v.resize(len);
+    std::memcpy(static_cast<void*>(v.data()), p + i, std::size_t(len) * sizeof(T));
+    i += std::size_t(len) * sizeof(T);
+    return v;
+  }
+};
+
+constexpr std::uint32_t kBlobMagic = 0x31425352;  // "RSB1"
+
+// IPC mappings opened in this process, keyed by (handle bytes, device).
+std::mutex g_ipc_mu;
+std::map<std::pair<std::string, int>, void*> g_ipc_open;
+
+Result<std::uint64_t> open_ipc(const cudaIpcMemHandle_t& h, int device) {
+  std::string key(reinterpret_cast<const char*>(&h), sizeof(h));
+  std::lock_guard lk(g_ipc_mu);
+  auto it = g_ipc_open.find({key, device});
+  if (it != g_ipc_open.end()) return reinterpret_cast<std::uint64_t>(it->second);
+  DeviceGuard g(device);
+  void* p = nullptr;
+  if (cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess)
+    return Status::not_serving;
+  g_ipc_open[{key, device}] = p;
+  return reinterpret_cast<std::uint64_t>(p);
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ DevBuf
+
+DevBuf::~DevBuf() {
+  if (p) {
+    DeviceGuard g(dev);
+    cudaFree(p);
+  }
+}
+
+Status DevBuf::alloc(int device, std::size_t bytes) {
+  if (p && n >= bytes && dev == device) return Status::ok;
+  if (p) {
+    DeviceGuard g(dev);
+    cudaFree(p);
+    p = nullptr;
+  }
+  DeviceGuard g(device);
+  dev = device;
+  n = bytes ? bytes : 16;
+  if (cudaMalloc(&p, n) != cudaSuccess) {
+    p = nullptr;
+    n = 0;
+    return Status::transfer_failed;
+  }
+  return Status::ok;
+}
+
+// ---------------------------------------------------------------- ChunkMap
+
+ChunkMap ChunkMap::uniform(const Manifest& m, std::uint64_t chunk_bytes) {
+  ChunkMap c;
+  c.chunk0.push_back(0);
+  for (const auto& it : m.items()) {
+    std::uint64_t n = (it.length + chunk_bytes - 1) / chunk_bytes;
+    c.chunk_len.push_back(static_cast<std::uint32_t>(chunk_bytes));
+    c.chunk0.push_back(c.chunk0.back() + static_cast<std::uint32_t>(n));
+  }
+  return c;
+}
+
+// ----------------------------------------------------------- ServeRegistry
+
+std::string ServeRegistry::key(const std::string& model, const std::string& replica,
+                               std::uint32_t shard) {
+  return model + "|" + replica + "|" + std::to_string(shard);
+}
+
+std::shared_ptr<ServeState> ServeRegistry::ensure(const std::string& k) {
+  std::lock_guard lk(m_);
+  auto& slot = map_[k];
+  if (!slot) slot = std::make_shared<ServeState>();
+  return slot;
+}
+
+std::shared_ptr<ServeState> ServeRegistry::find(const std::string& k) const {
+  std::lock_guard lk(m_);
+  auto it = map_.find(k);
+  return it == map_.end() ? nullptr : it->second;
+}
+
+void ServeRegistry::erase(const std::string& k) {
+  std::lock_guard lk(m_);
+  map_.erase(k);
+}
+
+void ServeRegistry::set_silent(const std::string& model, const std::string& replica, bool on) {
+  std::lock_guard lk(m_);
+  const std::string prefix = model + "|" + replica + "|";
+  if (on) silent_.insert(prefix);
+  else silent_.erase(prefix);
+}
+
+bool ServeRegistry::is_silent(const std::string& k) const {
+  std::lock_guard lk(m_);
+  for (const auto& p : silent_)
+    if (k.compare(0, p.size(), p) == 0) return true;
+  return false;
+}
+
+Result<std::string> ServeRegistry::export_state(const std::string& k) {
+  auto st = find(k);
+  if (!st) return Status::not_found;
+  std::lock_guard lk(st->m);
+  if (st->imported) return Status::invalid_state;
+  auto range = get_range_fn();
+  if (!range) return Status::transfer_failed;
+  DeviceGuard g(st->device);
+  std::vector<ServeState::Alloc> allocs;
+  std::map<std::uint64_t, std::uint32_t> by_base;
+  auto locate = [&](std::uint64_t ptr, std::pair<std::uint32_t, std::uint64_t>* loc) -> Status {
+    CUdeviceptr base = 0;
+    size_t size = 0;
+    if (range(&base, &size, static_cast<CUdeviceptr>(ptr)) != CUDA_SUCCESS)
+      return Status::invalid_argument;
+    auto it = by_base.find(base);
+    if (it == by_base.end()) {
+      ServeState::Alloc a{};
+      if (cudaIpcGetMemHandle(&a.handle, reinterpret_cast<void*>(base)) != cudaSuccess)
+        return Status::invalid_argument;
+      a.size = size;
+      it = by_base.emplace(base, static_cast<std::uint32_t>(allocs.size())).first;
+      allocs.push_back(a);
+    }
+    *loc = {it->second, ptr - base};
+    return Status::ok;
+  };
+  std::vector<std::pair<std::uint32_t, std::uint64_t>> item_loc(st->item_ptrs.size());
+  for (std::size_t i = 0; i < st->item_ptrs.size(); ++i)
+    if (Status s = locate(st->item_ptrs[i], &item_loc[i]); !ok(s)) return s;
+  std::pair<std::uint32_t, std::uint64_t> dl{0, 0}, fl{0, 0};
+  if (Status s = locate(st->digests, &dl); !ok(s)) return s;
+  if (Status s = locate(st->flags, &fl); !ok(s)) return s;
+  W w;
+  w.pod(kBlobMagic);
+  w.str(k);
+  w.pod(st->version);
+  w.pod(static_cast<std::uint8_t>(st->serving));
+  w.pod(static_cast<std::uint8_t>(st->complete));
+  w.pod(st->progress);
+  w.pod(st->epoch);
+  w.pod(st->device);
+  w.pod(static_cast<std::int32_t>(getpid()));
+  w.vec(st->item_ends);
+  w.vec(st->cmap.chunk0);
+  w.vec(st->cmap.chunk_len);
+  w.vec(allocs);
+  w.vec(item_loc);
+  w.pod(dl);
+  w.pod(fl);
+  return w.s;
+}
+
+Status ServeRegistry::import_state(const std::string& blob) {
+  R r{blob.data(), blob.size()};
+  if (r.pod<std::uint32_t>() != kBlobMagic) return Status::protocol_error;
+  std::string k = r.str();
+  auto version = r.pod<VersionId>();
+  bool serving = r.pod<std::uint8_t>() != 0;
+  bool complete = r.pod<std::uint8_t>() != 0;
+  auto progress = r.pod<std::uint64_t>();
+  auto epoch = r.pod<std::uint32_t>();
+  auto device = r.pod<int>();
+  auto pid = r.pod<std::int32_t>();
+  auto ends = r.vec<std::uint64_t>();
+  auto c0 = r.vec<std::uint32_t>();
+  auto cl = r.vec<std::uint32_t>();
+  auto allocs = r.vec<ServeState::Alloc>();
+  auto item_loc = r.vec<std::pair<std::uint32_t, std::uint64_t>>();
+  auto dl = r.pod<std::pair<std::uint32_t, std::uint64_t>>();
+  auto fl = r.pod<std::pair<std::uint32_t, std::uint64_t>>();
+  if (!r.ok) return Status::protocol_error;
+  if (pid == getpid()) return Status::ok;  // our own state: nothing to import
+  auto st = ensure(k);
+  std::lock_guard lk(st->m);
+  st->imported = true;
+  st->serving = serving;
+  st->complete = complete;
+  st->version = version;
+  st->progress = progress;
+  st->epoch = epoch;
+  st->device = device;
+  st->pid = pid;
+  st->item_ends = std::move(ends);
+  st->cmap.chunk0 = std::move(c0);
+  st->cmap.chunk_len = std::move(cl);
+  st->allocs = std::move(allocs);
+  st->item_loc = std::move(item_loc);
+  st->digests_loc = dl;
+  st->flags_loc = fl;
+  return Status::ok;
+}
+
+// --------------------------------------------------------- address mapping
+
+Status enable_peer(int reader_device, int owner_device) {
+  if (reader_device == owner_device) return Status::ok;
+  static std::mutex mu;
+  static std::set<std::pair<int, int>> done;
+  std::lock_guard lk(mu);
+  if (done.count({reader_device, owner_device})) return Status::ok;
+  int can = 0;
+  cudaDeviceCanAccessPeer(&can, reader_device, owner_device);
+  if (!can) return Status::not_serving;
+  DeviceGuard g(reader_device);
+  cudaError_t e = cudaDeviceEnablePeerAccess(owner_device, 0);
+  if (e == cudaErrorPeerAccessAlreadyEnabled) {
+    cudaGetLastError();
+    e = cudaSuccess;
+  }
+  if (e != cudaSuccess) return Status::not_serving;
+  done.insert({reader_device, owner_device});
+  return Status::ok;
+}
+
+Status map_source(const std::shared_ptr<ServeState>& st, int reader_device, SourceView* out) {
+  std::lock_guard lk(st->m);
+  out->cmap = st->cmap;
+  out->epoch = st->epoch;
+  out->total = st->item_ends.empty() ? 0 : st->item_ends.back();
+  if (!st->imported) {
+    if (Status s = enable_peer(reader_device, st->device); !ok(s)) return s;
+    out->item_ptrs = st->item_ptrs;
+    out->digests = st->digests;
+    out->flags = st->flags;
+    return Status::ok;
+  }
+  std::vector<std::uint64_t> bases(st->allocs.size());
+  for (std::size_t a = 0; a < st->allocs.size(); ++a) {
+    auto b = open_ipc(st->allocs[a].handle, reader_device);
+    if (!b) return b.status();
+    bases[a] = *b;
+  }
+  out->item_ptrs.resize(st->item_loc.size());
+  for (std::size_t i = 0; i < st->item_loc.size(); ++i)
+    out->item_ptrs[i] = bases[st->item_loc[i].first] + st->item_loc[i].second;
+  out->digests = bases[st->digests_loc.first] + st->digests_loc.second;
+  out->flags = bases[st->flags_loc.first] + st->flags_loc.second;
+  return Status::ok;
+}
+
+// ------------------------------------------------------------------ Client
+
+Client::Client(Registry* reg, ServeRegistry* serves, std::string model, std::string replica,
+               std::uint32_t num_shards, ClientConfig cfg)
+    : reg_(reg),
+      serves_(serves),
+      model_(std::move(model)),
+      replica_(std::move(replica)),
+      num_shards_(num_shards),
+      cfg_(std::move(cfg)) {
+  shards_.resize(num_shards_);
+  for (std::uint32_t i = 0; i < num_shards_; ++i) shards_[i].idx = i;
+}
+
+Client::~Client() {
+  stop_serving();
+  for (auto& sh : shards_) {
+    if (sh.device < 0) continue;
+    DeviceGuard g(sh.device);
+    if (sh.ev0) cudaEventDestroy(sh.ev0);
+    if (sh.ev1) cudaEventDestroy(sh.ev1);
+    if (sh.own_stream && sh.stream) cudaStreamDestroy(sh.stream);
+  }
+}
+
+Status Client::register_tensor(std::uint32_t shard, const std::string& name, void* ptr,
+                               std::uint64_t len) {
+  if (shard >= num_shards_ || name.empty() || !ptr || len == 0) return Status::invalid_argument;
+  Shard& sh = shards_[shard];
+  if (sh.by_name.count(name)) return Status::already_exists;
+  if (published_ || current_) return Status::invalid_state;
+  cudaPointerAttributes attr{};
+  if (cudaPointerGetAttributes(&attr, ptr) != cudaSuccess || attr.type != cudaMemoryTypeDevice) {
+    cudaGetLastError();
+    return Status::invalid_argument;  // registered regions live in device memory
+  }
+  if (sh.device < 0) sh.device = attr.device;
+  if (sh.device != attr.device) return Status::invalid_argument;  // one device per shard
+  if (sh.endpoint.empty()) sh.endpoint = "cuda:" + std::to_string(sh.device);
+  sh.by_name[name] = static_cast<std::uint32_t>(sh.regs.size());
+  sh.regs.push_back({name, static_cast<std::uint8_t*>(ptr), len});
+  return Status::ok;
+}
+
+void Client::set_shard_endpoint(std::uint32_t shard, std::string ep) {
+  if (shard < num_shards_) shards_[shard].endpoint = std::move(ep);
+}
+
+void Client::set_stream(std::uint32_t shard, cudaStream_t s) {
+  if (shard >= num_shards_) return;
+  Shard& sh = shards_[shard];
+  if (sh.own_stream && sh.stream) {
+    DeviceGuard g(sh.device);
+    cudaStreamDestroy(sh.stream);
+  }
+  sh.stream = s;
+  sh.own_stream = false;
+}
+
+Status Client::ensure_stream(Shard& sh) {
+  if (sh.device < 0) return Status::invalid_state;
+  DeviceGuard g(sh.device);
+  if (!sh.stream) {
+    RS_CUDA(cudaStreamCreateWithFlags(&sh.stream, cudaStreamNonBlocking));
+    sh.own_stream = true;
+  }
+  if (!sh.ev0) RS_CUDA(cudaEventCreate(&sh.ev0));
+  if (!sh.ev1) RS_CUDA(cudaEventCreate(&sh.ev1));
+  return Status::ok;
+}
+
+Status Client::open() {
+  std::vector<std::string> eps;
+  for (auto& sh : shards_) {
+    if (sh.device < 0) return Status::invalid_state;  // nothing registered on a shard
+    eps.push_back(sh.endpoint);
+  }
+  Status s = reg_->open(model_, replica_, num_shards_, cfg_.dc, eps);
+  if (ok(s)) opened_ = true;
+  return s;
+}
+
+// ---- publish --------------------------------------------------------------
+
+Status Client::build_payload(Shard& sh, VersionId v, std::shared_ptr<Payload>* out) {
+  if (Status s = ensure_stream(sh); !ok(s)) return s;
+  DeviceGuard g(sh.device);
+  const std::size_t n = sh.regs.size();
+  auto p = std::make_shared<Payload>();
+  RS_CUDA(cudaEventRecord(sh.ev0, sh.stream));
+
+  // Entry digests (K6).
+  std::vector<std::uint64_t> ptrs(n), lens(n), dig(n);
+  for (std::size_t i = 0; i < n; ++i) {
+    ptrs[i] = reinterpret_cast<std::uint64_t>(sh.regs[i].ptr);
+    lens[i] = sh.regs[i].len;
+  }
+  DevBuf tab;
+  if (Status s = tab.alloc(sh.device, std::max<std::size_t>(3 * n, 1) * 8); !ok(s)) return s;
+  auto* d = static_cast<std::uint64_t*>(tab.p);
+  if (n) {
+    RS_CUDA(cudaMemcpyAsync(d, ptrs.data(), n * 8, cudaMemcpyHostToDevice, sh.stream));
+    RS_CUDA(cudaMemcpyAsync(d + n, lens.data(), n * 8, cudaMemcpyHostToDevice, sh.stream));
+    RS_CUDA(dev::launch_span_digests(d, d + n, d + 2 * n, static_cast<int>(n), sh.stream));
+    RS_CUDA(cudaMemcpyAsync(dig.data(), d + 2 * n, n * 8, cudaMemcpyDeviceToHost, sh.stream));
+    RS_CUDA(cudaStreamSynchronize(sh.stream));
+    stats_.h2d_bytes += 16 * n;
+    stats_.d2h_bytes += 8 * n;
+  }
+  std::vector<EntryInfo> infos(n);
+  for (std::size_t i = 0; i < n; ++i) infos[i] = {sh.regs[i].name, lens[i], dig[i]};
+  auto mr = assemble(infos, cfg_.limits);
+  if (!mr) return mr.status();
+  p->manifest = std::move(*mr);
+
+  // Tiny-tensor groups: pack (K3) then digest (K6) the staging buffer.
+  const std::size_t ng = p->manifest.groups.size();
+  if (ng) {
+    std::vector<std::uint64_t> srcs, dsts, ls, gp(ng), gl(ng), gd(ng);
+    for (std::size_t gi = 0; gi < ng; ++gi) {
+      const auto& grp = p->manifest.groups[gi];
+      auto buf = std::make_unique<DevBuf>();
+      if (Status s = buf->alloc(sh.device, grp.packed_length); !ok(s)) return s;
+      for (const auto& mem : grp.members) {
+        srcs.push_back(ptrs[mem.entry]);
+        dsts.push_back(reinterpret_cast<std::uint64_t>(buf->p) + mem.offset);
+        ls.push_back(lens[mem.entry]);
+      }
+      gp[gi] = reinterpret_cast<std::uint64_t>(buf->p);
+      gl[gi] = grp.packed_length;
+      p->group_bufs.push_back(std::move(buf));
+    }
+    const std::size_t nm = srcs.size();
+    DevBuf gt;
+    if (Status s = gt.alloc(sh.device, (3 * nm + 3 * ng) * 8); !ok(s)) return s;
+    auto* t = static_cast<std::uint64_t*>(gt.p);
+    RS_CUDA(cudaMemcpyAsync(t, srcs.data(), nm * 8, cudaMemcpyHostToDevice, sh.stream));
+    RS_CUDA(cudaMemcpyAsync(t + nm, dsts.data(), nm * 8, cudaMemcpyHostToDevice, sh.stream));
+    RS_CUDA(cudaMemcpyAsync(t + 2 * nm, ls.data(), nm * 8, cudaMemcpyHostToDevice, sh.stream));
+    RS_CUDA(dev::launch_copy_spans(t, t + nm, t + 2 * nm, static_cast<int>(nm), sh.stream));
+    auto* g2 = t + 3 * nm;
+    RS_CUDA(cudaMemcpyAsync(g2, gp.data(), ng * 8, cudaMemcpyHostToDevice, sh.stream));
+    RS_CUDA(cudaMemcpyAsync(g2 + ng, gl.data(), ng * 8, cudaMemcpyHostToDevice, sh.stream));
+    RS_CUDA(dev::launch_span_digests(g2, g2 + ng, g2 + 2 * ng, static_cast<int>(ng), sh.stream));
+    RS_CUDA(cudaMemcpyAsync(gd.data(), g2 + 2 * ng, ng * 8, cudaMemcpyDeviceToHost, sh.stream));
+    RS_CUDA(cudaStreamSynchronize(sh.stream));
+    stats_.h2d_bytes += 24 * nm + 16 * ng;
+    stats_.d2h_bytes += 8 * ng;
+    for (std::size_t gi = 0; gi < ng; ++gi)
+      p->manifest.set_group_digest(static_cast<std::uint32_t>(gi), gd[gi]);
+  }
+
+  // Serving addresses per item, chunk map, chunk digest table + watermarks.
+  const auto& items = p->manifest.items();
+  p->item_ptrs.resize(items.size());
+  for (std::size_t i = 0; i < items.size(); ++i)
+    p->item_ptrs[i] = items[i].is_group
+                          ? reinterpret_cast<std::uint64_t>(p->group_bufs[items[i].index]->p)
+                          : ptrs[items[i].index];
+  p->cmap = ChunkMap::uniform(p->manifest, cfg_.chunk_bytes);
+  const std::uint32_t nc = p->cmap.n_chunks(), nb = p->cmap.n_batches();
+  if (Status s = p->digests.alloc(sh.device, std::size_t(nc) * 8); !ok(s)) return s;
+  if (Status s = p->flags.alloc(sh.device, std::size_t(nb) * 4); !ok(s)) return s;
+  RS_CUDA(cudaMemsetAsync(p->flags.p, 0, std::size_t(nb) * 4, sh.stream));
+  p->epoch = ++sh.epoch_ctr;
+  if (nc) {
+    std::vector<dev::ItemDesc> descs(items.size());
+    for (std::size_t i = 0; i < items.size(); ++i)
+      descs[i] = {p->item_ptrs[i], 0, items[i].length, p->cmap.chunk0[i], p->cmap.chunk_len[i]};
+    const std::size_t dbytes = descs.size() * sizeof(dev::ItemDesc);
+    if (Status s = sh.scratch.alloc(sh.device, dbytes + 128); !ok(s)) return s;
+    auto* base = static_cast<std::uint8_t*>(sh.scratch.p);
+    auto* work = reinterpret_cast<std::uint32_t*>(base + dbytes);
+    auto* status = reinterpret_cast<dev::PullStatus*>(base + dbytes + 64);
+    RS_CUDA(cudaMemcpyAsync(base, descs.data(), dbytes, cudaMemcpyHostToDevice, sh.stream));
+    RS_CUDA(cudaMemsetAsync(work, 0, 128, sh.stream));
+    dev::PullParams pp{};
+    pp.items = reinterpret_cast<const dev::ItemDesc*>(base);
+    pp.n_items = static_cast<std::uint32_t>(descs.size());
+    pp.n_chunks = nc;
+    pp.n_batches = nb;
+    pp.dst_digests = static_cast<std::uint64_t*>(p->digests.p);
+    pp.dst_flags = static_cast<std::uint32_t*>(p->flags.p);
+    pp.dst_epoch = p->epoch;
+    pp.work = work;
+    pp.status = status;
+    pp.timeout_ns = static_cast<std::uint64_t>(cfg_.pull_timeout_s * 1e9);
+    RS_CUDA(dev::launch_pull(pp, dev::pull_grid(sh.device), sh.stream));
+    stats_.h2d_bytes += dbytes;
+  }
+  RS_CUDA(cudaEventRecord(sh.ev1, sh.stream));
+  RS_CUDA(cudaStreamSynchronize(sh.stream));
+  float ms = 0;
+  cudaEventElapsedTime(&ms, sh.ev0, sh.ev1);
+  stats_.last_publish_ms = ms;
+  p->encoded = p->manifest.encode();
+  *out = std::move(p);
+  return Status::ok;
+}
+
+Status Client::prepare_publish(VersionId v, std::vector<std::string>* manifests) {
+  manifests->clear();
+  for (auto& sh : shards_) {
+    std::shared_ptr<Payload> p;
+    if (Status s = build_payload(sh, v, &p); !ok(s)) return s;
+    sh.holding = std::move(p);
+    manifests->push_back(sh.holding->encoded);
+  }
+  return Status::ok;
+}
+
+void Client::commit_publish(VersionId v, Status st) {
+  if (!ok(st)) return;
+  for (auto& sh : shards_) {
+    sh.partial_version.reset();
+    serve(sh, v, true);
+  }
+  current_ = v;
+  published_ = true;
+}
+
+Status Client::publish(VersionId v) {
+  if (!opened_) {
+    if (Status s = open(); !ok(s)) return s;
+  }
+  if (published_) return Status::mutability_violation;
+  std::vector<std::string> manifests;
+  if (Status s = prepare_publish(v, &manifests); !ok(s)) return s;
+  OpOutcome o;
+  Status s = reg_->publish(model_, replica_, v, manifests, &o);
+  if (ok(s)) s = o.status;
+  commit_publish(v, s);
+  return s;
+}
+
+Status Client::unpublish() {
+  if (!opened_) return Status::invalid_state;
+  OpOutcome o;
+  Status s = reg_->unpublish(model_, replica_, &o);
+  if (!ok(s)) return s;
+  if (!o.done) o = reg_->wait_op(model_, replica_, 600.0);
+  if (!o.done) return Status::timeout;
+  if (ok(o.status)) {
+    published_ = false;
+    stop_serving();
+  }
+  return o.status;
+}
+
+// ---- serve state ----------------------------------------------------------
+
+void Client::serve(Shard& sh, VersionId v, bool complete) {
+  if (!sh.serve) sh.serve = serves_->ensure(ServeRegistry::key(model_, replica_, sh.idx));
+  const auto& p = *sh.holding;
+  std::vector<std::uint64_t> ends;
+  for (const auto& it : p.manifest.items()) ends.push_back(it.stream_offset + it.length);
+  std::lock_guard lk(sh.serve->m);
+  sh.serve->serving = true;
+  sh.serve->imported = false;
+  sh.serve->version = v;
+  sh.serve->complete = complete;
+  sh.serve->progress = complete ? p.manifest.items().size() : 0;
+  sh.serve->device = sh.device;
+  sh.serve->pid = static_cast<int>(getpid());
+  sh.serve->item_ends = std::move(ends);
+  sh.serve->item_ptrs = p.item_ptrs;
+  sh.serve->cmap = p.cmap;
+  sh.serve->digests = reinterpret_cast<std::uint64_t>(p.digests.p);
+  sh.serve->flags = reinterpret_cast<std::uint64_t>(p.flags.p);
+  sh.serve->epoch = p.epoch;
+}
+
+void Client::invalidate() {
+  for (auto& sh : shards_) {
+    if (sh.holding) sh.holding->epoch = ++sh.epoch_ctr;
+    sh.partial_version.reset();
+  }
+  current_.reset();
+}
+
+void Client::stop_serving() {
+  for (auto& sh : shards_) {
+    if (!sh.serve) continue;
+    std::lock_guard lk(sh.serve->m);
+    sh.serve->serving = false;
+  }
+}
+
+// ---- receive --------------------------------------------------------------
+
+Status Client::resolve_source(Shard& sh, const Assignment& a, VersionId v, SourceView* out,
+                              double wait_s) {
+  // An assigned upstream that is not serving yet is waited for, not
+  // condemned (the reference's threaded race).
+  auto deadline = std::chrono::steady_clock::now() + std::chrono::duration<double>(wait_s);
+  const std::string k = ServeRegistry::key(model_, a.source_replica, sh.idx);
+  for (;;) {
+    auto st = serves_->is_silent(k) ? nullptr : serves_->find(k);
+    if (st) {
+      bool ready;
+      {
+        std::lock_guard lk(st->m);
+        ready = st->serving && st->version == v && !st->cmap.chunk0.empty();
+      }
+      if (ready) return map_source(st, sh.device, out);
+    }
+    if (std::chrono::steady_clock::now() > deadline) return Status::not_serving;
+    std::this_thread::sleep_for(std::chrono::microseconds(200));
+  }
+}
+
+Status Client::bind(Shard& sh, const Assignment& a, VersionId v) {
+  if (Status s = ensure_stream(sh); !ok(s)) return s;
+  if (sh.holding && sh.holding->encoded == a.manifest) {
+    // Identical manifest: resume.  Keeping the fill epoch keeps every batch
+    // already landed for this version (flag == epoch) out of the pull.
+    bool resume = (current_ && *current_ == v) || (sh.partial_version && *sh.partial_version == v);
+    if (!resume) sh.holding->epoch = ++sh.epoch_ctr;
+    sh.partial_version = v;
+    return Status::ok;
+  }
+  auto mr = Manifest::decode(a.manifest);
+  if (!mr) return Status::protocol_error;
+  if (mr->entries.size() != sh.regs.size()) return Status::invalid_argument;
+  for (const auto& e : mr->entries) {
+    auto it = sh.by_name.find(e.name);
+    if (it == sh.by_name.end() || sh.regs[it->second].len != e.length)
+      return Status::invalid_argument;
+  }
+  DeviceGuard g(sh.device);
+  auto p = std::make_shared<Payload>();
+  p->manifest = std::move(*mr);
+  p->encoded = a.manifest;
+  for (const auto& grp : p->manifest.groups) {
+    auto buf = std::make_unique<DevBuf>();
+    if (Status s = buf->alloc(sh.device, grp.packed_length); !ok(s)) return s;
+    p->group_bufs.push_back(std::move(buf));
+  }
+  const auto& items = p->manifest.items();
+  // The chunk map is a pure function of (manifest, chunk_bytes), so a reader
+  // can start serving its own fill before its source is even reachable.
+  p->cmap = ChunkMap::uniform(p->manifest, cfg_.chunk_bytes);
+  p->item_ptrs.resize(items.size());
+  for (std::size_t i = 0; i < items.size(); ++i) {
+    const auto& it = items[i];
+    p->item_ptrs[i] =
+        it.is_group ? reinterpret_cast<std::uint64_t>(p->group_bufs[it.index]->p)
+                    : reinterpret_cast<std::uint64_t>(
+                          sh.regs[sh.by_name.at(p->manifest.entries[it.index].name)].ptr);
+  }
+  const std::uint32_t nc = p->cmap.n_chunks(), nb = p->cmap.n_batches();
+  if (Status s = p->digests.alloc(sh.device, std::size_t(nc) * 8); !ok(s)) return s;
+  if (Status s = p->flags.alloc(sh.device, std::size_t(nb) * 4); !ok(s)) return s;
+  RS_CUDA(cudaMemsetAsync(p->flags.p, 0, std::size_t(nb) * 4, sh.stream));
+  RS_CUDA(cudaStreamSynchronize(sh.stream));
+  p->epoch = ++sh.epoch_ctr;
+  sh.holding = std::move(p);
+  sh.partial_version = v;
+  return Status::ok;
+}
+
+Status Client::bind_all(const std::vector<Assignment>& as, VersionId v) {
+  if (as.size() != num_shards_) return Status::protocol_error;
+  for (std::uint32_t i = 0; i < num_shards_; ++i) {
+    if (as[i].version != v) return Status::protocol_error;
+    if (Status s = bind(shards_[i], as[i], v); !ok(s)) return s;
+  }
+  // The incoming version overwrites registered regions in place: until every
+  // shard verifies, this replica holds no coherent version.
+  current_.reset();
+  published_ = false;
+  for (auto& sh : shards_) serve(sh, v, false);
+  return Status::ok;
+}
+
+Status Client::launch_fill(Shard& sh, const SourceView& src, bool src_complete) {
+  DeviceGuard g(sh.device);
+  const auto& p = *sh.holding;
+  const auto& items = p.manifest.items();
+  std::vector<dev::ItemDesc> descs(items.size());
+  for (std::size_t i = 0; i < items.size(); ++i)
+    descs[i] = {src.item_ptrs[i], p.item_ptrs[i], items[i].length, p.cmap.chunk0[i],
+                p.cmap.chunk_len[i]};
+  const std::size_t dbytes = descs.size() * sizeof(dev::ItemDesc);
+  if (Status s = sh.scratch.alloc(sh.device, dbytes + 128); !ok(s)) return s;
+  auto* base = static_cast<std::uint8_t*>(sh.scratch.p);
+  auto* work = reinterpret_cast<std::uint32_t*>(base + dbytes);
+  auto* status = reinterpret_cast<dev::PullStatus*>(base + dbytes + 64);
+  if (dbytes) RS_CUDA(cudaMemcpyAsync(base, descs.data(), dbytes, cudaMemcpyHostToDevice, sh.stream));
+  RS_CUDA(cudaMemsetAsync(work, 0, 128, sh.stream));
+  stats_.h2d_bytes += dbytes;
+  dev::PullParams pp{};
+  pp.items = reinterpret_cast<const dev::ItemDesc*>(base);
+  pp.n_items = static_cast<std::uint32_t>(descs.size());
+  pp.n_chunks = p.cmap.n_chunks();
+  pp.n_batches = p.cmap.n_batches();
+  pp.src_digests = reinterpret_cast<const std::uint64_t*>(src.digests);
+  pp.dst_digests = static_cast<std::uint64_t*>(p.digests.p);
+  pp.src_flags = src_complete ? nullptr : reinterpret_cast<const std::uint32_t*>(src.flags);
+  pp.src_epoch = src.epoch;
+  pp.dst_flags = static_cast<std::uint32_t*>(p.flags.p);
+  pp.dst_epoch = p.epoch;
+  pp.work = work;
+  pp.status = status;
+  pp.timeout_ns = static_cast<std::uint64_t>(cfg_.pull_timeout_s * 1e9);
+  RS_CUDA(cudaEventRecord(sh.ev0, sh.stream));
+  RS_CUDA(dev::launch_pull(pp, dev::pull_grid(sh.device), sh.stream));
+  RS_CUDA(cudaEventRecord(sh.ev1, sh.stream));
+  return Status::ok;
+}
+
+std::vector<Client::FillOutcome> Client::fill_shards(const std::vector<Assignment>& as,
+                                                     const std::vector<std::uint32_t>& which) {
+  std::vector<FillOutcome> out(num_shards_);
+  std::vector<dev::PullStatus> st(num_shards_);
+  std::vector<bool> launched(num_shards_, false);
+  for (std::uint32_t i : which) {
+    Shard& sh = shards_[i];
+    const Assignment& a = as[i];
+    SourceView view;
+    Status s = resolve_source(sh, a, a.version, &view, cfg_.pull_timeout_s);
+    // Every replica of a cluster digests with the same chunk size; a source
+    // cut differently cannot be verified chunk-by-chunk.
+    if (ok(s) && !(view.cmap == sh.holding->cmap)) s = Status::protocol_error;
+    if (!ok(s)) {
+      out[i] = {s, 0, 0};
+      continue;
+    }
+    s = launch_fill(sh, view, a.source_complete);
+    if (!ok(s)) {
+      out[i] = {s, 0, 0};
+      continue;
+    }
+    launched[i] = true;
+  }
+  for (std::uint32_t i : which) {
+    if (!launched[i]) continue;
+    Shard& sh = shards_[i];
+    DeviceGuard g(sh.device);
+    const std::size_t dbytes = sh.holding->manifest.items().size() * sizeof(dev::ItemDesc);
+    auto* status = reinterpret_cast<dev::PullStatus*>(static_cast<std::uint8_t*>(sh.scratch.p) +
+                                                      dbytes + 64);
+    cudaMemcpyAsync(&st[i], status, sizeof(dev::PullStatus), cudaMemcpyDeviceToHost, sh.stream);
+    cudaError_t e = cudaStreamSynchronize(sh.stream);
+    stats_.d2h_bytes += sizeof(dev::PullStatus);
+    if (e != cudaSuccess) {
+      out[i] = {Status::transfer_failed, 0, 0};
+      continue;
+    }
+    float ms = 0;
+    cudaEventElapsedTime(&ms, sh.ev0, sh.ev1);
+    stats_.last_pull_ms = ms;
+    stats_.last_pull_bytes = st[i].bytes;
+    stats_.last_pull_launches = 1;
+    stats_.bytes_pulled += st[i].bytes;
+    stats_.checksum_failures += st[i].retried_batches;
+    switch (st[i].code) {
+      case dev::kPullOk:
+        out[i] = {Status::ok, 0, 0};
+        break;
+      case dev::kPullChecksum:
+        stats_.checksum_failures += 1;
+        out[i] = {Status::checksum_mismatch, 1, st[i].bad_chunk};
+        break;
+      case dev::kPullTimeout:
+        out[i] = {Status::timeout, 0, st[i].bad_chunk};
+        break;
+      default:
+        out[i] = {Status::not_serving, 0, st[i].bad_chunk};
+        break;
+    }
+  }
+  // Unpack verified groups into their members (K3, unpack_group).
+  for (std::uint32_t i : which) {
+    if (!ok(out[i].status)) continue;
+    Shard& sh = shards_[i];
+    const auto& p = *sh.holding;
+    std::vector<std::uint64_t> srcs, dsts, ls;
+    for (std::size_t gi = 0; gi < p.manifest.groups.size(); ++gi)
+      for (const auto& mem : p.manifest.groups[gi].members) {
+        srcs.push_back(reinterpret_cast<std::uint64_t>(p.group_bufs[gi]->p) + mem.offset);
+        dsts.push_back(reinterpret_cast<std::uint64_t>(
+            sh.regs[sh.by_name.at(p.manifest.entries[mem.entry].name)].ptr));
+        ls.push_back(p.manifest.entries[mem.entry].length);
+      }
+    if (srcs.empty()) continue;
+    DeviceGuard g(sh.device);
+    DevBuf t;
+    const std::size_t nm = srcs.size();
+    if (!ok(t.alloc(sh.device, 3 * nm * 8))) {
+      out[i] = {Status::transfer_failed, 0, 0};
+      continue;
+    }
+    auto* d = static_cast<std::uint64_t*>(t.p);
+    cudaMemcpyAsync(d, srcs.data(), nm * 8, cudaMemcpyHostToDevice, sh.stream);
+    cudaMemcpyAsync(d + nm, dsts.data(), nm * 8, cudaMemcpyHostToDevice, sh.stream);
+    cudaMemcpyAsync(d + 2 * nm, ls.data(), nm * 8, cudaMemcpyHostToDevice, sh.stream);
+    dev::launch_copy_spans(d, d + nm, d + 2 * nm, static_cast<int>(nm), sh.stream);
+    if (cudaStreamSynchronize(sh.stream) != cudaSuccess) out[i] = {Status::transfer_failed, 0, 0};
+    stats_.h2d_bytes += 24 * nm;
+  }
+  return out;
+}
+
+void Client::finish_transfers(VersionId v, bool good) {
+  if (good) {
+    for (auto& sh : shards_) {
+      sh.partial_version.reset();
+      {
+        std::lock_guard lk(sh.serve->m);
+        sh.serve->complete = true;
+        sh.serve->progress = sh.holding->manifest.items().size();
+      }
+      stats_.items_verified += sh.holding->manifest.items().size();
+    }
+    current_ = v;
+    published_ = true;
+  } else {
+    stop_serving();
+    current_.reset();
+    published_ = false;
+  }
+}
+
+Status Client::run_replicate_loop(const OpOutcome& o, VersionId v) {
+  std::vector<Assignment> as = o.assignments;
+  if (Status s = bind_all(as, v); !ok(s)) {
+    for (std::uint32_t i = 0; i < num_shards_; ++i) reg_->complete(model_, replica_, i, s);
+    finish_transfers(v, false);
+    return s;
+  }
+  std::vector<int> reports_left(num_shards_, cfg_.checksum_retries);
+  std::vector<std::uint32_t> pending;
+  for (std::uint32_t i = 0; i < num_shards_; ++i) pending.push_back(i);
+  while (!pending.empty()) {
+    auto res = fill_shards(as, pending);
+    std::vector<std::uint32_t> next;
+    for (std::uint32_t i : pending) {
+      if (ok(res[i].status)) {
+        reg_->progress(model_, replica_, i, shards_[i].holding->manifest.items().size());
+        continue;
+      }
+      Status fail = res[i].status;
+      if (res[i].reason == 1 && reports_left[i]-- <= 0) fail = Status::checksum_mismatch;
+      else {
+        stats_.failure_reports++;
+        auto r = reg_->failure_report(model_, replica_, i, as[i].source_replica, res[i].reason);
+        if (r) {
+          as[i] = *r;
+          next.push_back(i);
+          continue;
+        }
+        fail = r.status();
+      }
+      for (std::uint32_t j = 0; j < num_shards_; ++j) reg_->complete(model_, replica_, j, fail);
+      finish_transfers(v, false);
+      return fail;
+    }
+    pending = std::move(next);
+  }
+  finish_transfers(v, true);
+  for (std::uint32_t i = 0; i < num_shards_; ++i) reg_->complete(model_, replica_, i, Status::ok);
+  return Status::ok;
+}
+
+Status Client::replicate(const VersionSpec& spec, VersionId* out, double wait_s) {
+  if (!opened_) {
+    if (Status s = open(); !ok(s)) return s;
+  }
+  OpOutcome o;
+  Status s = reg_->replicate(model_, replica_, spec, &o);
+  if (!ok(s)) return s;
+  if (!o.done) o = reg_->wait_op(model_, replica_, wait_s);
+  if (!o.done) return Status::timeout;
+  if (!ok(o.status)) return o.status;
+  s = run_replicate_loop(o, *o.version);
+  if (ok(s) && out) *out = *o.version;
+  return s;
+}
+
+Status Client::update(const VersionSpec& spec, bool* changed, VersionId* out, double wait_s) {
+  if (!opened_) {
+    if (Status s = open(); !ok(s)) return s;
+  }
+  OpOutcome o;
+  Status s = reg_->update(model_, replica_, spec, current_, &o);
+  if (!ok(s)) return s;
+  if (!o.done) o = reg_->wait_op(model_, replica_, wait_s);
+  if (!o.done) return Status::timeout;
+  if (!ok(o.status)) return o.status;
+  if (changed) *changed = o.changed;
+  if (!o.changed) {
+    if (out && o.version) *out = *o.version;
+    return Status::ok;
+  }
+  s = run_replicate_loop(o, *o.version);
+  if (ok(s) && out) *out = *o.version;
+  return s;
+}
+
+Status Client::close() {
+  stop_serving();
+  for (auto& sh : shards_) serves_->erase(ServeRegistry::key(model_, replica_, sh.idx));
+  if (opened_) reg_->close(model_, replica_);
+  opened_ = false;
+  published_ = false;
+  return Status::ok;
+}
+
+Result<std::string> Client::manifest_bytes(std::uint32_t shard) const {
+  if (shard >= num_shards_ || !shards_[shard].holding) return Status::not_found;
+  return shards_[shard].holding->encoded;
+}
+
+Status Client::chunk_digests(std::uint32_t shard, std::vector<std::uint64_t>* out) {
+  if (shard >= num_shards_ || !shards_[shard].holding) return Status::not_found;
+  Shard& sh = shards_[shard];
+  DeviceGuard g(sh.device);
+  out->resize(sh.holding->cmap.n_chunks());
+  if (out->empty()) return Status::ok;
+  RS_CUDA(cudaMemcpy(out->data(), sh.holding->digests.p, out->size() * 8, cudaMemcpyDeviceToHost));
+  return Status::ok;
+}
+
+Result<std::string> Client::export_serve(std::uint32_t shard) {
+  if (shard >= num_shards_) return Status::invalid_argument;
+  return serves_->export_state(ServeRegistry::key(model_, replica_, shard));
+}
+
+}  // namespace rsb

@@ -1,0 +1,262 @@
+// Reader/publisher side of the B200 ROS read path: one replica's shard
+// handles, their registered device regions, the serve state peers chase, and
+// the device transfer loop.
+//
+// Mirrors the data-path parts of the reference ClientCore
+// (/root/reference/proj/include/refstore/client_core.hpp:35-104):
+//   register_tensor            client_core.hpp:72-73
+//   build_publish_payload      client_core.cpp:1547-1579  -> prepare_publish
+//   bind_receive_payload       client_core.cpp:1581-1622  -> bind()
+//   serve_payload/payload_spans client_core.cpp:1624-1670 -> serve()
+//   TransferTask (step/issue_pull/verify_ready/item_failed/retarget)
+//                              client_core.cpp:47-492     -> fill_shards()
+//   task_progress / task_done  client_core.cpp:1414-1542
+// and of the transport boundary (transport.hpp:53-156): ServeRegistry,
+// PeerServeState, compute_slice / copy_slice_locked (the latter two become
+// the device pull kernel over peer-mapped source spans).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdint>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <optional>
+#include <set>
+#include <string>
+#include <vector>
+
+#include "common.hpp"
+#include "device.hpp"
+#include "manifest.hpp"
+#include "registry.hpp"
+
+namespace rsb {
+
+struct ClientConfig {
+  std::uint64_t chunk_bytes = 4096;  // digest + watermark unit (multiple of 16)
+  PackLimits limits;                 // tiny-tensor packing (config.hpp:46)
+  bool pipeline = true;              // serve partially landed fills
+  int checksum_retries = 3;          // failure reports per fill (config.hpp:42)
+  double pull_timeout_s = 4.0;       // upstream silence before reporting
+  std::string dc = "dc0";
+};
+
+// Owned device allocation.
+struct DevBuf {
+  void* p = nullptr;
+  std::size_t n = 0;
+  int dev = -1;
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  DevBuf(DevBuf&& o) noexcept : p(o.p), n(o.n), dev(o.dev) { o.p = nullptr; o.n = 0; }
+  ~DevBuf();
+  Status alloc(int device, std::size_t bytes);
+};
+
+// Item -> digest chunks.  Chunks are item-relative; chunk j of item i covers
+// [j*len_i, min((j+1)*len_i, item_len)).  Batches of 32 chunks carry one
+// watermark flag.
+struct ChunkMap {
+  std::vector<std::uint32_t> chunk0;     // n_items + 1 prefix
+  std::vector<std::uint32_t> chunk_len;  // per item
+  std::uint32_t n_chunks() const { return chunk0.empty() ? 0 : chunk0.back(); }
+  std::uint32_t n_batches() const {
+    return (n_chunks() + dev::kBatchChunks - 1) / dev::kBatchChunks;
+  }
+  static ChunkMap uniform(const Manifest& m, std::uint64_t chunk_bytes);
+  bool operator==(const ChunkMap& o) const {
+    return chunk0 == o.chunk0 && chunk_len == o.chunk_len;
+  }
+};
+
+// PeerServeState (transport.hpp:53-69) with device-resident watermarks.
+// Host fields are guarded by `m`; the device watermark words are the
+// authoritative progress for chasing readers.
+struct ServeState {
+  std::mutex m;
+  bool serving = false;
+  VersionId version = 0;
+  std::uint64_t progress = 0;  // verified items (host view)
+  bool complete = false;
+  int device = -1;
+  int pid = 0;
+  std::vector<std::uint64_t> item_ends;  // stream end offset per item
+  std::vector<std::uint64_t> item_ptrs;  // device address per item (owner VA)
+  ChunkMap cmap;
+  std::uint64_t digests = 0;  // device u64[n_chunks]
+  std::uint64_t flags = 0;    // device u32[n_batches]
+  std::uint32_t epoch = 0;    // current fill epoch (flags == epoch: landed)
+  // Imported (other process) state: IPC handles per allocation.
+  bool imported = false;
+  struct Alloc {
+    cudaIpcMemHandle_t handle;
+    std::uint64_t size = 0;
+  };
+  std::vector<Alloc> allocs;
+  std::vector<std::pair<std::uint32_t, std::uint64_t>> item_loc;  // (alloc, offset)
+  std::pair<std::uint32_t, std::uint64_t> digests_loc{0, 0}, flags_loc{0, 0};
+};
+
+// (model, replica, shard) -> serve state, process-wide (transport.hpp:72-85).
+class ServeRegistry {
+ public:
+  static std::string key(const std::string& model, const std::string& replica,
+                         std::uint32_t shard);
+  std::shared_ptr<ServeState> ensure(const std::string& k);
+  std::shared_ptr<ServeState> find(const std::string& k) const;
+  void erase(const std::string& k);
+  // Cross-process: serialize a local state / install a remote one.
+  Result<std::string> export_state(const std::string& k);
+  Status import_state(const std::string& blob);
+  // Fault hook: a silent replica's serve states never answer
+  // (MemNetwork::set_data_silent, transport_mem.hpp:33-46).
+  void set_silent(const std::string& model, const std::string& replica, bool on);
+  bool is_silent(const std::string& k) const;
+
+ private:
+  mutable std::mutex m_;
+  std::map<std::string, std::shared_ptr<ServeState>> map_;
+  std::set<std::string> silent_;  // "model|replica|" prefixes
+};
+
+// Source addresses as the reader's device sees them.
+struct SourceView {
+  std::vector<std::uint64_t> item_ptrs;
+  std::uint64_t digests = 0;
+  std::uint64_t flags = 0;
+  std::uint32_t epoch = 0;
+  ChunkMap cmap;
+  std::uint64_t total = 0;
+};
+
+struct ClientStats {
+  std::uint64_t bytes_pulled = 0;
+  std::uint64_t bytes_pulled_cross_dc = 0;
+  std::uint64_t bytes_copied_local = 0;
+  std::uint64_t items_verified = 0;
+  std::uint64_t checksum_failures = 0;
+  std::uint64_t failure_reports = 0;
+  std::uint64_t failovers = 0;
+  // device timing of the most recent fill / publish (CUDA events)
+  float last_pull_ms = 0;
+  float last_publish_ms = 0;
+  std::uint64_t last_pull_bytes = 0;
+  std::uint32_t last_pull_launches = 0;
+  std::uint64_t h2d_bytes = 0;  // descriptor uploads (cumulative)
+  std::uint64_t d2h_bytes = 0;  // status / digest read-backs (cumulative)
+};
+
+class Client {
+ public:
+  Client(Registry* reg, ServeRegistry* serves, std::string model, std::string replica,
+         std::uint32_t num_shards, ClientConfig cfg);
+  ~Client();
+
+  Status register_tensor(std::uint32_t shard, const std::string& name, void* ptr,
+                         std::uint64_t len);
+  void set_shard_endpoint(std::uint32_t shard, std::string ep);
+  void set_stream(std::uint32_t shard, cudaStream_t s);
+
+  // --- blocking ops (in-process registry) ---------------------------------
+  Status open();
+  Status publish(VersionId v);
+  Status unpublish();
+  Status replicate(const VersionSpec& spec, VersionId* out, double wait_s);
+  Status update(const VersionSpec& spec, bool* changed, VersionId* out, double wait_s);
+  Status close();
+
+  // --- split phase (caller drives the registry, e.g. replicated across
+  //     processes) -----------------------------------------------------------
+  Status prepare_publish(VersionId v, std::vector<std::string>* manifests);
+  void commit_publish(VersionId v, Status st);
+  // Binds every shard to its assignment and starts serving the (empty)
+  // fill so downstream readers can chase it.
+  Status bind_all(const std::vector<Assignment>& a, VersionId v);
+  // One attempt of every shard's fill.  Per-shard status; reason: 0 timeout
+  // / not serving, 1 checksum.
+  struct FillOutcome {
+    Status status = Status::ok;
+    int reason = 0;
+    std::uint32_t bad_chunk = 0;
+  };
+  std::vector<FillOutcome> fill_shards(const std::vector<Assignment>& a,
+                                       const std::vector<std::uint32_t>& which);
+  void finish_transfers(VersionId v, bool ok);
+  void stop_serving();
+  // Forget held bytes: the next fill of any version re-pulls everything
+  // (a new fill epoch invalidates every landed watermark).
+  void invalidate();
+
+  std::optional<VersionId> current_version() const { return current_; }
+  bool is_published() const { return published_; }
+  const ClientStats& stats() const { return stats_; }
+  const std::string& model() const { return model_; }
+  const std::string& replica() const { return replica_; }
+  std::uint32_t num_shards() const { return num_shards_; }
+  Result<std::string> manifest_bytes(std::uint32_t shard) const;
+  Status chunk_digests(std::uint32_t shard, std::vector<std::uint64_t>* out);
+  Result<std::string> export_serve(std::uint32_t shard);
+  std::string endpoint(std::uint32_t shard) const { return shards_[shard].endpoint; }
+
+ private:
+  struct Reg {
+    std::string name;
+    std::uint8_t* ptr = nullptr;
+    std::uint64_t len = 0;
+  };
+  struct Payload {
+    Manifest manifest;
+    std::string encoded;
+    std::vector<std::unique_ptr<DevBuf>> group_bufs;
+    ChunkMap cmap;
+    DevBuf digests;
+    DevBuf flags;
+    std::uint32_t epoch = 0;
+    std::vector<std::uint64_t> item_ptrs;  // own landing/serving address per item
+  };
+  struct Shard {
+    std::uint32_t idx = 0;
+    int device = -1;
+    std::string endpoint;
+    std::vector<Reg> regs;
+    std::map<std::string, std::uint32_t> by_name;
+    std::shared_ptr<Payload> holding;
+    std::optional<VersionId> partial_version;
+    std::shared_ptr<ServeState> serve;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    DevBuf scratch;  // descriptor tables + work/status words
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    std::uint32_t epoch_ctr = 0;
+  };
+
+  Status ensure_stream(Shard& sh);
+  Status build_payload(Shard& sh, VersionId v, std::shared_ptr<Payload>* out);
+  Status bind(Shard& sh, const Assignment& a, VersionId v);
+  void serve(Shard& sh, VersionId v, bool complete);
+  Status resolve_source(Shard& sh, const Assignment& a, VersionId v, SourceView* out,
+                        double wait_s);
+  Status launch_fill(Shard& sh, const SourceView& src, bool src_complete);
+  Status run_replicate_loop(const OpOutcome& o, VersionId v);
+
+  Registry* reg_;
+  ServeRegistry* serves_;
+  std::string model_, replica_;
+  std::uint32_t num_shards_;
+  ClientConfig cfg_;
+  std::vector<Shard> shards_;
+  std::optional<VersionId> current_;
+  bool published_ = false;
+  bool opened_ = false;
+  ClientStats stats_;
+};
+
+// Peer / IPC address translation for the reader's device.
+Status map_source(const std::shared_ptr<ServeState>& st, int reader_device, SourceView* out);
+Status enable_peer(int reader_device, int owner_device);
+
+}  // namespace rsb

@@ -1,0 +1,230 @@
+// Version registry + transfer planner: the metadata half of ROS.
+//
+// This is the subset of the reference ServerCore
+// (/root/reference/proj/src/server_core.cpp) that decides WHERE a reader
+// pulls from: replica lifecycle, version availability with smart skipping
+// (available_versions 1487-1515), source choice (pick_source 1517-1543),
+// settle-time re-validation (settle_source 1007-1037), assignment building
+// (make_assignment 1545-1557), parked-replicate wake order (wake_blocked
+// 1565-1587), completion/drain (on_complete 1142-1175, finish_replication
+// 1177-1204, release_source 1206-1216, check_drain 1218-1226) and failure
+// reassignment (on_failure_report 1291-1382, fail_replica 1682-1711).
+//
+// Differences by design (B200 in-box path):
+//  * Group transactions arrive whole: one call carries every shard of a
+//    replica, so there is no straggler assembly / txn timeout machinery.
+//  * Calls are synchronous and deterministic.  A caller whose op parks
+//    (replicate before a version exists, unpublish/update waiting for readers
+//    to drain) gets Status::ok with `pending` set and later reads the outcome
+//    with op_result(); with several threads it may block in wait_op().  The
+//    same call sequence applied on every rank (replicated state machine,
+//    paper_2604_09107_b200/ros.py Cluster) yields the same plan everywhere.
+//  * Offload / seed / retention lanes are not modelled.
+//  * pick_source's key gains a topology cost between dc and serving; on a
+//    uniform NVSwitch box every cost is equal and the order is exactly the
+//    reference's (own_seed, same_dc, serving, last_assigned, name).
+#pragma once
+
+#include <condition_variable>
+#include <cstdint>
+#include <functional>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <optional>
+#include <set>
+#include <string>
+#include <vector>
+
+#include "common.hpp"
+
+namespace rsb {
+
+// messages.hpp:40-52.
+struct Assignment {
+  VersionId version = 0;
+  std::string source_replica;
+  std::string source_endpoint;
+  bool source_complete = false;
+  bool cross_dc = false;
+  bool seeding = false;
+  bool local_seed_consume = false;
+  std::string manifest;  // encoded Manifest of this shard
+};
+
+enum class OpKind : std::uint8_t { none, publish, unpublish, replicate, update };
+
+struct OpOutcome {
+  bool done = false;
+  Status status = Status::ok;
+  std::optional<VersionId> version;
+  bool changed = false;                 // update
+  std::vector<Assignment> assignments;  // replicate/update(change): per shard
+};
+
+struct ReplicaView {
+  std::string lifecycle;  // registered|replicating|published|failed
+  std::optional<VersionId> version;
+  std::uint32_t serving = 0;
+  bool visible = false;
+  bool seeding = false;
+  std::uint64_t min_progress = 0;
+  std::string source;
+};
+
+struct TraceLine {
+  std::uint64_t seq = 0;
+  std::string kind;
+  std::vector<std::pair<std::string, std::string>> kv;
+  std::string format() const;
+};
+
+class Registry {
+ public:
+  struct Config {
+    bool pipeline = true;
+    bool smart_skipping = true;
+  };
+  // Returns a topology cost (lower = closer) between two data endpoints;
+  // default: every pair costs 0.
+  using TopoFn = std::function<int(const std::string& reader_ep,
+                                   const std::string& source_ep)>;
+
+  explicit Registry(Config cfg);
+
+  void set_topology(TopoFn fn);
+
+  Status open(const std::string& model, const std::string& replica,
+              std::uint32_t num_shards, const std::string& dc,
+              const std::vector<std::string>& endpoints);
+  Status close(const std::string& model, const std::string& replica);
+
+  // Each returns the immediate status; if ok and the op is parked,
+  // *pending = true and the outcome arrives through op_result().
+  Status publish(const std::string& model, const std::string& replica,
+                 VersionId v, const std::vector<std::string>& manifests,
+                 OpOutcome* out);
+  Status unpublish(const std::string& model, const std::string& replica,
+                   OpOutcome* out);
+  Status replicate(const std::string& model, const std::string& replica,
+                   const VersionSpec& spec, OpOutcome* out);
+  Status update(const std::string& model, const std::string& replica,
+                const VersionSpec& spec, std::optional<VersionId> current,
+                OpOutcome* out);
+
+  // Transfer lifecycle reports from the reader (ProgressMsg / CompleteMsg).
+  void progress(const std::string& model, const std::string& replica,
+                std::uint32_t shard, std::uint64_t items);
+  void complete(const std::string& model, const std::string& replica,
+                std::uint32_t shard, Status outcome);
+  // FailureReportMsg: reason 0 = timeout, 1 = checksum.  On success returns
+  // the replacement assignment for `shard`.
+  Result<Assignment> failure_report(const std::string& model,
+                                    const std::string& replica,
+                                    std::uint32_t shard,
+                                    const std::string& failed_replica,
+                                    int reason);
+
+  // Dry-run plan view: which source `replica` would be assigned for `spec`
+  // right now (no counters move).
+  Result<Assignment> locate(const std::string& model, const std::string& replica,
+                            const VersionSpec& spec, std::uint32_t shard);
+  // The replicating replica's current assignment for `shard` (after
+  // failure_report retargets it).
+  Result<Assignment> current_assignment(const std::string& model,
+                                        const std::string& replica, std::uint32_t shard);
+
+  // Outcome of the replica's most recent op (done=false while parked).
+  OpOutcome op_result(const std::string& model, const std::string& replica);
+  // Blocks until that op is done or `timeout_s` passes (multi-threaded use).
+  OpOutcome wait_op(const std::string& model, const std::string& replica,
+                    double timeout_s);
+
+  std::map<VersionId, std::set<std::string>> listing(const std::string& model);
+  std::optional<ReplicaView> view(const std::string& model,
+                                  const std::string& replica);
+  std::vector<TraceLine> trace();
+  std::string trace_text();
+
+ private:
+  enum class Life { registered, replicating, published, failed };
+  struct Txn {
+    OpKind kind = OpKind::none;
+    std::uint64_t order = 0;
+    VersionSpec spec;
+    std::optional<VersionId> current;  // update: caller's held version
+    bool blocked = false, resolved = false, settled = false, changed = false;
+    bool was_visible = false;
+    std::optional<VersionId> target;
+    std::string source;
+  };
+  struct ShardState {
+    std::uint64_t progress = 0;
+    bool complete = false;
+  };
+  struct Rep {
+    std::string model, name, dc;
+    std::uint32_t num_shards = 1;
+    std::vector<std::string> endpoints;
+    Life life = Life::registered;
+    bool visible = false, seeding = false;
+    std::optional<VersionId> version, last_published;
+    std::string source;
+    std::uint32_t serving = 0;
+    std::uint64_t last_assigned = 0;
+    std::vector<ShardState> shards;
+    std::optional<Txn> txn;  // in-flight op (one per replica)
+    OpOutcome last;          // outcome of the latest op
+    bool complete_all() const {
+      for (const auto& s : shards)
+        if (!s.complete) return false;
+      return true;
+    }
+  };
+  struct VersionInfo {
+    std::uint32_t num_shards = 0;
+    std::vector<std::string> manifests;
+  };
+  struct ModelState {
+    std::map<std::string, std::unique_ptr<Rep>> reps;
+    std::map<VersionId, VersionInfo> versions;
+    std::optional<VersionId> max_published;
+  };
+
+  ModelState& ms(const std::string& model) { return models_[model]; }
+  Rep* find(const std::string& model, const std::string& replica);
+  void trace(std::string kind,
+             std::vector<std::pair<std::string, std::string>> kv);
+  static const char* life_name(Life l);
+
+  std::set<VersionId> available(ModelState& m, const std::string& dc);
+  Rep* pick_source(ModelState& m, VersionId v, const Rep& reader);
+  bool still_good(const Rep& cand, const Rep& reader, VersionId v) const;
+  Rep* settle_source(Rep& r, Txn& t);
+  Assignment make_assignment(ModelState& m, Rep& src, VersionId v,
+                             std::uint32_t shard, const std::string& dc);
+  void start_replicate(Rep& r);
+  void start_update(Rep& r);
+  void try_settle(Rep& r);
+  void apply_settle(Rep& r);
+  void finish_op(Rep& r, Status st);
+  void settle_ok(Rep& r);
+  void wake_blocked(const std::string& model);
+  void release_source(Rep& r);
+  void check_drain(Rep& src);
+  void finish_replication(Rep& r);
+  void void_replication(Rep& r, const std::string& reason);
+  void fail_replica(Rep& r, const std::string& reason);
+  void prune_version(ModelState& m, VersionId v);
+
+  Config cfg_;
+  TopoFn topo_;
+  std::mutex mu_;
+  std::condition_variable cv_;
+  std::map<std::string, ModelState> models_;
+  std::vector<TraceLine> trace_;
+  std::uint64_t tick_ = 0;   // assign tick (last_assigned)
+  std::uint64_t order_ = 0;  // op arrival order (wake_blocked)
+};
+
+}  // namespace rsb

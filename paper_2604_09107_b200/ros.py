@@ -1,0 +1,332 @@
+"""Python host mirror of the ROS API over the C ABI (include/ros_b200.h).
+
+Names, argument meaning and status values follow the reference ClientCore /
+ServerCore (/root/reference/proj/include/refstore/client_core.hpp:63-93,
+server_core.hpp:37-52) so tests read like the reference's own
+(tests/unit/test_client_core.cpp).  Two deployments:
+
+* ``Cluster`` -- one process: a registry ("server A") shared by any number of
+  handles, which may sit on different GPUs (peer access over NVLink).
+* ``DistCluster`` -- one process per GPU (torchrun): every rank holds a
+  replica of the registry and applies the same operation log in the same
+  order (a replicated state machine over ``torch.distributed``), so every
+  rank computes the same plan; serve states cross processes as CUDA IPC
+  handles.  No NCCL collective touches the data path.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+import re
+from dataclasses import dataclass, field
+from typing import Optional
+
+from ._lib import RsAssignment, RsConfig, RsStats, lib
+
+
+class Status(enum.IntEnum):
+    """refstore::Status (types.hpp:22-41)."""
+    ok = 0
+    invalid_argument = 1
+    invalid_state = 2
+    already_exists = 3
+    not_found = 4
+    version_regression = 5
+    manifest_conflict = 6
+    mutability_violation = 7
+    version_unavailable = 8
+    group_aborted = 9
+    server_unavailable = 10
+    transfer_failed = 11
+    checksum_mismatch = 12
+    not_serving = 13
+    timeout = 14
+    offload_failed = 15
+    protocol_error = 16
+    closed = 17
+
+
+class ROSError(RuntimeError):
+    def __init__(self, status: int, what: str = ""):
+        self.status = Status(status)
+        super().__init__(f"{what}: {self.status.name}" if what else self.status.name)
+
+
+def check(rc: int, what: str = "") -> None:
+    if rc != 0:
+        raise ROSError(rc, what)
+
+
+@dataclass
+class OpResult:
+    """ClientCore::OpResult (client_core.hpp:37-42)."""
+    status: Status
+    version: Optional[int] = None
+    changed: bool = False
+
+
+@dataclass
+class Stats:
+    bytes_pulled: int = 0
+    bytes_pulled_cross_dc: int = 0
+    bytes_copied_local: int = 0
+    items_verified: int = 0
+    checksum_failures: int = 0
+    failure_reports: int = 0
+    failovers: int = 0
+    last_pull_ms: float = 0.0
+    last_publish_ms: float = 0.0
+    last_pull_bytes: int = 0
+    last_pull_launches: int = 0
+    h2d_bytes: int = 0
+    d2h_bytes: int = 0
+
+
+@dataclass
+class Assign:
+    replica: str
+    version: int
+    src: str
+    src_serving: int
+
+
+def _b(s: str) -> bytes:
+    return s.encode()
+
+
+def _read_bytes(fn, *args) -> bytes:
+    n = C.c_size_t(0)
+    check(fn(*args, None, 0, C.byref(n)))
+    buf = C.create_string_buffer(max(n.value, 1))
+    check(fn(*args, buf, n.value, C.byref(n)))
+    return buf.raw[:n.value]
+
+
+def make_config(chunk_bytes=4096, tiny_threshold=2 << 20, group_target=64 << 20, pipeline=True,
+                checksum_retries=3, pull_timeout_s=4.0, datacenter="dc0") -> RsConfig:
+    cfg = RsConfig()
+    lib.rs_config_default(C.byref(cfg))
+    cfg.chunk_bytes = chunk_bytes
+    cfg.tiny_threshold = tiny_threshold
+    cfg.group_target = group_target
+    cfg.pipeline = int(pipeline)
+    cfg.checksum_retries = checksum_retries
+    cfg.pull_timeout_s = pull_timeout_s
+    cfg.datacenter = datacenter.encode()
+    return cfg
+
+
+_ASSIGN = re.compile(r"^\d+ assign (.*)$")
+
+
+class Cluster:
+    """ServerCore + ServeRegistry of this process (rs_cluster)."""
+
+    def __init__(self, pipeline: bool = True, smart_skipping: bool = True):
+        h = C.c_void_p()
+        check(lib.rs_cluster_create(int(pipeline), int(smart_skipping), C.byref(h)))
+        self.h = h
+        self.handles: list[Handle] = []
+
+    def close(self):
+        for hd in list(self.handles):
+            hd.close()
+        if self.h:
+            lib.rs_cluster_destroy(self.h)
+            self.h = None
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def open(self, model: str, replica: str, num_shards: int = 1, **cfg) -> "Handle":
+        out = C.c_void_p()
+        c = make_config(**cfg)
+        check(lib.rs_open(self.h, _b(model), _b(replica), num_shards, C.byref(c), C.byref(out)),
+              "rs_open")
+        hd = Handle(self, out, model, replica, num_shards)
+        self.handles.append(hd)
+        return hd
+
+    # ---- introspection -------------------------------------------------
+    def trace(self) -> str:
+        return _read_bytes(lib.rs_cluster_trace, self.h).decode()
+
+    def assigns(self) -> list[Assign]:
+        out = []
+        for line in self.trace().splitlines():
+            m = _ASSIGN.match(line)
+            if m:
+                kv = dict(f.split("=", 1) for f in m.group(1).split())
+                out.append(Assign(kv["replica"], int(kv["v"]), kv["src"], int(kv["src_serving"])))
+        return out
+
+    def listing(self, model: str = "m") -> dict[int, set[str]]:
+        text = _read_bytes(lib.rs_cluster_listing, self.h, _b(model)).decode()
+        out: dict[int, set[str]] = {}
+        for part in filter(None, text.split(";")):
+            v, reps = part.split(":", 1)
+            out[int(v)] = set(filter(None, reps.split(",")))
+        return out
+
+    def view(self, model: str, replica: str) -> Optional[dict]:
+        life = C.create_string_buffer(16)
+        v, s, vis = C.c_uint64(), C.c_uint32(), C.c_int()
+        rc = lib.rs_cluster_view(self.h, _b(model), _b(replica), life, C.byref(v), C.byref(s),
+                                 C.byref(vis))
+        if rc == Status.not_found:
+            return None
+        check(rc)
+        return {"lifecycle": life.value.decode(), "version": v.value, "serving": s.value,
+                "visible": bool(vis.value)}
+
+    def locate(self, model: str, replica: str, spec: str = "latest", shard: int = 0) -> dict:
+        a = RsAssignment()
+        check(lib.rs_locate(self.h, _b(model), _b(replica), _b(spec), shard, C.byref(a)), "rs_locate")
+        return _assignment(a)
+
+    def set_silent(self, model: str, replica: str, silent: bool = True):
+        check(lib.rs_cluster_set_silent(self.h, _b(model), _b(replica), int(silent)))
+
+
+def _assignment(a: RsAssignment) -> dict:
+    return {"version": a.version, "source_replica": a.source_replica.decode(),
+            "source_endpoint": a.source_endpoint.decode(), "source_complete": bool(a.source_complete),
+            "cross_dc": bool(a.cross_dc), "seeding": bool(a.seeding),
+            "local_seed_consume": bool(a.local_seed_consume)}
+
+
+class Handle:
+    """ClientCore for one replica (rs_handle).  Registered tensors are
+    caller-owned CUDA memory that must outlive the handle."""
+
+    def __init__(self, cluster: Cluster, h, model: str, replica: str, num_shards: int):
+        self.cluster = cluster
+        self.h = h
+        self.model = model
+        self.replica = replica
+        self.num_shards = num_shards
+        self._keep = []
+
+    # ---- setup ------------------------------------------------------------
+    def register_tensor(self, shard: int, name: str, tensor=None, *, ptr: int = 0,
+                        nbytes: int = 0) -> Status:
+        if tensor is not None:
+            if not tensor.is_cuda or not tensor.is_contiguous():
+                return Status.invalid_argument
+            ptr, nbytes = tensor.data_ptr(), tensor.numel() * tensor.element_size()
+            self._keep.append(tensor)
+        return Status(lib.rs_register(self.h, shard, _b(name), C.c_void_p(ptr), nbytes))
+
+    def set_endpoint(self, shard: int, endpoint: str):
+        check(lib.rs_set_endpoint(self.h, shard, _b(endpoint)))
+
+    def set_stream(self, shard: int, stream) -> None:
+        raw = stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+        check(lib.rs_set_stream(self.h, shard, C.c_void_p(raw)))
+
+    # ---- ops --------------------------------------------------------------
+    def publish(self, version: int) -> OpResult:
+        st = Status(lib.rs_publish(self.h, version))
+        return OpResult(st, version if st == Status.ok else None)
+
+    def unpublish(self) -> OpResult:
+        return OpResult(Status(lib.rs_unpublish(self.h)))
+
+    def replicate(self, spec: str = "latest", wait_s: float = 60.0) -> OpResult:
+        v = C.c_uint64()
+        st = Status(lib.rs_replicate(self.h, _b(spec), wait_s, C.byref(v)))
+        return OpResult(st, v.value if st == Status.ok else None)
+
+    def update(self, spec: str = "latest", wait_s: float = 60.0) -> OpResult:
+        v, ch = C.c_uint64(), C.c_int()
+        st = Status(lib.rs_update(self.h, _b(spec), wait_s, C.byref(ch), C.byref(v)))
+        return OpResult(st, v.value if st == Status.ok and v.value else None, bool(ch.value))
+
+    def close(self) -> OpResult:
+        if not self.h:
+            return OpResult(Status.closed)
+        st = Status(lib.rs_close(self.h))
+        self.h = None
+        if self in self.cluster.handles:
+            self.cluster.handles.remove(self)
+        return OpResult(st)
+
+    def invalidate(self):
+        check(lib.rs_invalidate(self.h))
+
+    # ---- introspection ----------------------------------------------------
+    @property
+    def current_version(self) -> Optional[int]:
+        v = C.c_uint64()
+        return v.value if lib.rs_current_version(self.h, C.byref(v)) == 0 else None
+
+    @property
+    def is_published(self) -> bool:
+        return bool(lib.rs_is_published(self.h))
+
+    def stats(self) -> Stats:
+        s = RsStats()
+        check(lib.rs_stats_get(self.h, C.byref(s)))
+        return Stats(**{f: getattr(s, f) for f, _ in RsStats._fields_})
+
+    def manifest(self, shard: int = 0) -> bytes:
+        return _read_bytes(lib.rs_manifest, self.h, shard)
+
+    def chunk_digests(self, shard: int = 0):
+        import numpy as np
+        n = C.c_size_t(0)
+        check(lib.rs_chunk_digests(self.h, shard, None, 0, C.byref(n)))
+        out = np.zeros(n.value, np.uint64)
+        check(lib.rs_chunk_digests(self.h, shard, out.ctypes.data, n.value, C.byref(n)))
+        return out
+
+    def serve_export(self, shard: int = 0) -> bytes:
+        return _read_bytes(lib.rs_serve_export, self.h, shard)
+
+
+# ----------------------------------------------------------------------------
+# Device primitives
+def digest_spans(ptrs, lens, device: int = 0) -> list[int]:
+    import numpy as np
+    p = np.asarray(ptrs, np.uint64)
+    n = np.asarray(lens, np.uint64)
+    out = np.zeros(len(p), np.uint64)
+    check(lib.rs_digest_spans(p.ctypes.data, n.ctypes.data, len(p), out.ctypes.data, device),
+          "rs_digest_spans")
+    return [int(x) for x in out]
+
+
+def synth_bf16(tensor, seed: int, first: int = 0, stream=None):
+    """Fill a contiguous CUDA tensor (any dtype; viewed as bf16 words) with
+    the synthetic weights of SURVEY.md §8d."""
+    n = tensor.numel() * tensor.element_size() // 2
+    raw = 0 if stream is None else stream.cuda_stream
+    check(lib.rs_synth_bf16(C.c_void_p(tensor.data_ptr()), n, seed, first, C.c_void_p(raw)),
+          "rs_synth_bf16")
+
+
+def bf16_to_e4m3(src, dst, stream=None):
+    raw = 0 if stream is None else stream.cuda_stream
+    check(lib.rs_bf16_to_e4m3(C.c_void_p(src.data_ptr()), C.c_void_p(dst.data_ptr()), src.numel(),
+                              C.c_void_p(raw)), "rs_bf16_to_e4m3")
+
+
+def pull_spans(srcs, dsts, lens, chunk_bytes=4096, expect=None, out_digests=None, device=0,
+               stream=None):
+    """Standalone fused copy+verify over explicit device spans.  Returns
+    (kernel_code, kernel_ms)."""
+    import numpy as np
+    s = np.asarray(srcs, np.uint64)
+    d = np.asarray(dsts, np.uint64) if dsts is not None else None
+    n = np.asarray(lens, np.uint64)
+    code, ms = C.c_int(), C.c_float()
+    raw = 0 if stream is None else stream.cuda_stream
+    check(lib.rs_pull_spans(s.ctypes.data, None if d is None else d.ctypes.data, n.ctypes.data,
+                            len(s), chunk_bytes,
+                            None if expect is None else C.c_void_p(expect.data_ptr()),
+                            None if out_digests is None else C.c_void_p(out_digests.data_ptr()),
+                            device, C.c_void_p(raw), C.byref(code), C.byref(ms)), "rs_pull_spans")
+    return code.value, ms.value
