@@ -1,0 +1,348 @@
+"""Benchmark of the B200 ROS read path (BASELINE.json metric: per-receiver pull
+GB/s; weight-update latency).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--workload llama3_8b|config1] [--no-verify]
+
+Workload (config.workload): BASELINE configs[1], Llama-3-8B bf16 weights
+(291 tensors, 16,060,522,496 B, synthetic values of SURVEY.md §8d) published
+by a trainer replica.  N=1: trainer and one reader on cuda:0, the pull runs
+HBM->HBM on one GPU (bound: HBM).  N>1 (torchrun, one rank per GPU): rank 0
+is the trainer, ranks 1..N-1 are readers planned by the registry (a chain,
+like the reference planner); every reader pulls over NVLink (bound: ingress).
+
+A step = one full weight update: every reader drops its copy
+(unpublish + invalidate) and replicates "latest" through the C ABI --
+registry plan, bind, the fused pull+verify kernel, group unpack, complete.
+`value` = bytes landed by all readers / device time of the timed steps
+(max over ranks).  `e2e` = the same metric over host wall-clock of the
+rs_replicate calls (descriptor H2D + status D2H inside).  Inputs (16 GB per
+replica) are far larger than the 126 MB L2, so no flush is needed.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "per-receiver pull GB/s"
+UNIT = "GB/s"
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+# ----------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines: list[str] = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except (OSError, FileNotFoundError):
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.lines:
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                smax.append(float(f[2]))
+            except ValueError:
+                continue
+            for n, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(smax) if smax else None, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def measured_peaks() -> dict:
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return {"hbm_gbs": d.get("hbm_gbs", 6650.0), "src": "measured"}
+    return {"hbm_gbs": 6650.0, "src": "fallback"}
+
+
+def ncu_traffic(kind: str):
+    """Per-launch DRAM bytes of the pull kernel from the committed ncu capture."""
+    p = os.path.join(ROOT, "profiles", "ncu_pull_summary.json")
+    if not os.path.exists(p):
+        return None
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return d.get(kind, {}).get("dram_bytes_per_launch")
+    except (OSError, ValueError):
+        return None
+
+
+# --------------------------------------------------------------- workload
+def workload_shapes(name: str):
+    from tests.golden.models import config1, llama3_8b_shapes
+    if name == "llama3_8b":
+        return llama3_8b_shapes()
+    if name == "config1":
+        return config1()
+    raise SystemExit(f"unknown workload {name}")
+
+
+def alloc_replica(shapes, dev, seed_base=None):
+    """One contiguous arena per replica, tensors as views (IPC-exportable)."""
+    import torch
+
+    from paper_2604_09107_b200 import ros
+    sizes = [2 * _numel(s) for _, s in shapes]
+    offs, tot = [], 0
+    for n in sizes:
+        offs.append(tot)
+        tot += (n + 255) // 256 * 256
+    arena = torch.empty(tot, dtype=torch.uint8, device=dev)
+    views = []
+    for i, ((name, s), off, n) in enumerate(zip(shapes, offs, sizes)):
+        v = arena[off:off + n]
+        if seed_base is not None:
+            ros.synth_bf16(v, seed_base + i)
+        views.append((name, v))
+    return arena, views
+
+
+def _numel(shape):
+    n = 1
+    for d in shape:
+        n *= d
+    return n
+
+
+# ------------------------------------------------------------- CPU legs
+def cpu_reference_run(shapes, budget_bytes: int, reps: int, threaded: bool = True):
+    """The reference refstore (oracle/_ref) pulling a bounded sample of the
+    workload through its own MemNetwork path on this host's cores."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import numpy as np
+
+    import oracle as O
+    if not O.ref_available():
+        return None
+    sample, tot = [], 0
+    for name, s in shapes:
+        n = 2 * _numel(s)
+        if tot + n > budget_bytes and sample:
+            break
+        sample.append((name, n))
+        tot += n
+    times = []
+    for rep in range(reps):
+        c = O.RefCluster(threaded=threaded, server_pipeline=False, client_pipeline=False)
+        c.add("trainer")
+        c.add("reader")
+        keep = []
+        for i, (name, n) in enumerate(sample):
+            a = O.synth_bf16(42 + i, n // 2).view(np.uint8)
+            b = np.zeros(n, np.uint8)
+            keep += [a, b]
+            c.register("trainer", 0, name, a)
+            c.register("reader", 0, name, b)
+        st, _ = c.publish("trainer", 1)
+        assert st == 0, st
+        sts, _, _, secs = c.pull_many(["reader"])
+        assert sts == [0], sts
+        assert np.array_equal(keep[0], keep[1])
+        times.append(secs)
+        c.close()
+    best = min(times)
+    return {"value": tot / best / 1e9, "unit": UNIT, "cores": 1, "kind": "reference",
+            "threads": 3 if threaded else 1,
+            "sample": f"first {len(sample)} tensors of {len(shapes)} ({tot / 1e9:.2f} GB), "
+                      f"1 trainer -> 1 reader, refstore ThreadExecutor+MemNetwork, pipeline off, "
+                      f"best of {reps}; the copy+digest runs on the reader's one executor thread"}
+
+
+# ------------------------------------------------------------- our arm
+def run_single(args):
+    import torch
+
+    from paper_2604_09107_b200.ros import Cluster, Status
+    dev = torch.device("cuda:0")
+    shapes = workload_shapes(args.workload)
+    total = sum(2 * _numel(s) for _, s in shapes)
+    log(f"[bench] workload {args.workload}: {len(shapes)} tensors, {total / 1e9:.3f} GB")
+    tarena, tviews = alloc_replica(shapes, dev, seed_base=42)
+    rarena, rviews = alloc_replica(shapes, dev)
+    torch.cuda.synchronize()
+    stream = torch.cuda.Stream(device=dev)
+    cl = Cluster()
+    t = cl.open("m", "trainer", 1, chunk_bytes=args.chunk)
+    r = cl.open("m", "rollout1", 1, chunk_bytes=args.chunk)
+    for (n, v), (_, w) in zip(tviews, rviews):
+        assert t.register_tensor(0, n, v) == Status.ok
+        assert r.register_tensor(0, n, w) == Status.ok
+    r.set_stream(0, stream)
+    t0 = time.perf_counter()
+    assert t.publish(1).status == Status.ok
+    publish_s = time.perf_counter() - t0
+    publish_ms = t.stats().last_publish_ms
+
+    def step():
+        if r.is_published:
+            assert r.unpublish().status == Status.ok
+        r.invalidate()
+        w0 = time.perf_counter()
+        res = r.replicate("latest")
+        w1 = time.perf_counter()
+        assert res.status == Status.ok, res
+        return w1 - w0
+
+    for _ in range(args.warmup):
+        step()
+    if not args.no_verify:
+        assert torch.equal(tarena, rarena), "reader bytes differ from trainer"
+        assert (r.chunk_digests(0) == t.chunk_digests(0)).all()
+    clk = ClockSampler(0)
+    torch.cuda.synchronize()
+    clk.start()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    kernel_ms, walls = [], []
+    pulled0 = r.stats().bytes_pulled
+    h2d0, d2h0 = r.stats().h2d_bytes, r.stats().d2h_bytes
+    ev0.record(stream)
+    for _ in range(args.steps):
+        walls.append(step())
+        kernel_ms.append(r.stats().last_pull_ms)
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    clocks = clk.stop()
+    dev_ms = ev0.elapsed_time(ev1)
+    st = r.stats()
+    landed = st.bytes_pulled - pulled0
+    assert landed == args.steps * total, (landed, total)
+    if not args.no_verify:
+        assert torch.equal(tarena, rarena), "reader bytes differ from trainer after timed steps"
+    value = landed / (dev_ms / 1e3) / 1e9
+    e2e = landed / sum(walls) / 1e9
+    k_avg = statistics.mean(kernel_ms)
+    n_chunks = sum((2 * _numel(s) + args.chunk - 1) // args.chunk for _, s in shapes)
+    # algorithmic bytes per launch: read source + write destination + read the
+    # source chunk table + write own table + watermark words
+    alg = 2 * total + 16 * n_chunks + 4 * ((n_chunks + 31) // 32)
+    peaks = measured_peaks()
+    achieved = alg / (k_avg / 1e3) / 1e9
+    line = {
+        "metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": 1, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(dev_ms / args.steps, 3), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+        "config": {"workload": f"{args.workload}: trainer -> 1 reader on one GPU (local HBM pull)",
+                   "bytes_per_receiver": total, "tensors": len(shapes), "chunk_bytes": args.chunk,
+                   "receivers": 1, "l2": "inputs (16 GB/replica) >> 126 MB L2; no flush"},
+        "per_receiver_gbs": [round(value, 2)],
+        "weight_update_latency_s": round(statistics.mean(walls), 5),
+        "publish_s": round(publish_s, 4), "publish_device_ms": round(publish_ms, 3),
+        "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peaks["hbm_gbs"],
+                     "unit": "GB/s", "frac": round(achieved / peaks["hbm_gbs"], 4),
+                     "traffic": ncu_traffic("local"), "peak_src": peaks["src"],
+                     "kernel": "pull_kernel", "kernel_ms_avg": round(k_avg, 3),
+                     "alg_bytes_per_launch": alg},
+        "e2e": {"value": round(e2e, 2), "unit": UNIT,
+                "h2d_bytes_per_step": (st.h2d_bytes - h2d0) // args.steps,
+                "d2h_bytes_per_step": (st.d2h_bytes - d2h0) // args.steps,
+                "what": "wall clock of rs_replicate (plan+bind+kernel+unpack+complete) per step"},
+        "gpu_launches": args.steps * (1 + 1),  # pull_kernel + group unpack per step
+        "clocks": clocks,
+    }
+    if not args.no_cpu:
+        line["cpu_baseline"] = cpu_reference_run(shapes, args.cpu_bytes, args.cpu_reps)
+    print(json.dumps(line), flush=True)
+    cl.close()
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    shapes = workload_shapes(args.workload)
+    vals = []
+    for _ in range(args.warmup):
+        cpu_reference_run(shapes, args.cpu_bytes, 1)
+    for _ in range(args.steps):
+        r = cpu_reference_run(shapes, args.cpu_bytes, 1)
+        if r is None:
+            print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built"}))
+            return
+        vals.append(r)
+    v = statistics.median(x["value"] for x in vals)
+    line = {"impl": "reference", "metric": METRIC, "value": round(v, 3), "unit": UNIT,
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
+            "data": "synthetic",
+            "config": {"workload": f"{args.workload}: bounded sample, trainer -> 1 reader on host"},
+            "cpu_baseline": {"value": round(v, 3), "unit": UNIT, "cores": vals[0]["cores"],
+                             "kind": "reference", "sample": vals[0]["sample"]},
+            "e2e": {"value": round(v, 3), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="llama3_8b")
+    ap.add_argument("--chunk", type=int, default=4096)
+    ap.add_argument("--no-verify", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-bytes", type=int, default=2 << 30)
+    ap.add_argument("--cpu-reps", type=int, default=3)
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world > 1 or args.gpus > 1:
+        from paper_2604_09107_b200 import bench_dist
+        return bench_dist.run(args)
+    return run_single(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,282 @@
+"""GPU: the ROS API end to end through the C ABI, mirroring the reference's
+ClusterFix scenarios (tests/unit/test_client_core.cpp) with device-resident
+regions.  Bytes, manifests, chunk digests and plans are checked against the
+CPU oracle / reference fixtures."""
+import json
+import threading
+
+import numpy as np
+import pytest
+
+from tests.conftest import golden
+from tests.golden.models import tiny_set
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module", autouse=True)
+def need_gpu():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+
+
+def pattern(n, salt):
+    # fill_pattern of test_client_core.cpp:76-81
+    return ((salt * 1315423911 + np.arange(n, dtype=np.uint64) * 131) & 0xFF).astype(np.uint8)
+
+
+class Fix:
+    """ClusterFix with device buffers."""
+
+    def __init__(self, dev=0, **cluster_kw):
+        from paper_2604_09107_b200.ros import Cluster
+        self.cl = Cluster(**cluster_kw)
+        self.h = {}
+        self.bufs = {}
+        self.dev = dev
+
+    def make(self, replica, shards=1, dev=None, **cfg):
+        self.h[replica] = self.cl.open("m", replica, shards, **cfg)
+        self.h[replica].devnum = self.dev if dev is None else dev
+        return self.h[replica]
+
+    def reg(self, replica, shard, name, n, salt):
+        dev = torch.device("cuda", self.h[replica].devnum)
+        t = torch.from_numpy(pattern(n, salt)).to(dev)
+        self.bufs[(replica, shard, name)] = t
+        from paper_2604_09107_b200.ros import Status
+        assert self.h[replica].register_tensor(shard, name, t) == Status.ok
+
+    def same(self, a, b, shard, name):
+        return torch.equal(self.bufs[(a, shard, name)].cpu(), self.bufs[(b, shard, name)].cpu())
+
+    def close(self):
+        self.cl.close()
+
+
+@pytest.fixture
+def fx():
+    f = Fix()
+    yield f
+    f.close()
+
+
+def test_publish_list_unpublish_roundtrip(fx):
+    from paper_2604_09107_b200.ros import Status
+    t = fx.make("T", 2)
+    fx.reg("T", 0, "a", 3000, 1)
+    fx.reg("T", 0, "b", 5000, 2)
+    fx.reg("T", 1, "c", 4096, 3)
+    r = t.publish(1)
+    assert r.status == Status.ok and r.version == 1
+    assert t.is_published and t.current_version == 1
+    assert fx.cl.listing("m") == {1: {"T"}}
+    assert t.unpublish().status == Status.ok
+    assert not t.is_published and t.current_version == 1
+    assert fx.cl.listing("m") == {}
+
+
+def test_replicate_pulls_bytes_that_verify(fx, oracle):
+    # test_client_core.cpp:163-202
+    from paper_2604_09107_b200.ros import Status
+    t = fx.make("T", 2)
+    for args in [(0, "big", 3 << 20, 7), (0, "t1", 1000, 8), (0, "t2", 2000, 9), (1, "u1", 4096, 10)]:
+        fx.reg("T", *args)
+    assert t.publish(1).status == Status.ok
+    w = fx.make("R", 2)
+    for args in [(0, "big", 3 << 20, 100), (0, "t1", 1000, 100), (0, "t2", 2000, 100),
+                 (1, "u1", 4096, 100)]:
+        fx.reg("R", *args)
+    r = w.replicate("latest")
+    assert r.status == Status.ok and r.version == 1
+    assert w.is_published and w.current_version == 1
+    for s, n in [(0, "big"), (0, "t1"), (0, "t2"), (1, "u1")]:
+        assert fx.same("T", "R", s, n)
+    st = w.stats()
+    assert st.items_verified == 3
+    assert st.bytes_pulled == (3 << 20) + 1000 + 2000 + 4096
+    assert st.checksum_failures == 0
+    v = fx.cl.view("m", "R")
+    assert v["lifecycle"] == "published" and v["version"] == 1
+    # manifests are byte-identical to build_publish_payload's (oracle port,
+    # itself pinned to the reference on CPU)
+    m0 = oracle.publish_manifest(["big", "t1", "t2"], [pattern(3 << 20, 7), pattern(1000, 8),
+                                                         pattern(2000, 9)])
+    assert t.manifest(0) == m0 and w.manifest(0) == m0
+    assert t.manifest(1) == oracle.publish_manifest(["u1"], [pattern(4096, 10)])
+    # chunk digest tables agree with the oracle on both sides
+    want0 = oracle.chunk_digests([pattern(3 << 20, 7), np.concatenate([pattern(1000, 8),
+                                                                        pattern(2000, 9)])], 4096)
+    assert np.array_equal(t.chunk_digests(0), want0)
+    assert np.array_equal(w.chunk_digests(0), want0)
+
+
+def test_manifest_matches_reference_fixture(fx):
+    from paper_2604_09107_b200.ros import Status
+    m = json.load(open(golden("manifests.json")))
+    names, arrays = tiny_set()
+    for key, kw in (("tiny_set_real", {}),
+                    ("tiny_set_real_small_limits", {"tiny_threshold": 100 << 10,
+                                                    "group_target": 1 << 20})):
+        h = fx.cl.open("m", "P" + key, 1, **kw)
+        keep = []
+        for n, a in zip(names, arrays):
+            t = torch.from_numpy(a).cuda()
+            keep.append(t)
+            assert h.register_tensor(0, n, t) == Status.ok
+        assert h.publish(1).status == Status.ok
+        assert h.manifest(0).hex() == m[key]["encoded"]
+        h.unpublish()
+
+
+def test_chain_of_readers_matches_reference_plan(fx):
+    from paper_2604_09107_b200.ros import Status
+    plan = json.load(open(golden("plans.json")))["chain7"]
+    names = ["trainer"] + [f"rollout{i}" for i in range(1, 8)]
+    for i, r in enumerate(names):
+        fx.make(r)
+        for n, l in plan["tensors"]:
+            fx.reg(r, 0, n, l, 1 if r == "trainer" else 50 + i)
+    assert fx.h["trainer"].publish(1).status == Status.ok
+    # one GPU: run the fills one after another (each upstream completes before
+    # its reader launches; chasing across GPUs is covered by the multi-GPU test)
+    for r in names[1:]:
+        assert fx.h[r].replicate().status == Status.ok
+    got = [(a.replica, a.version, a.src, a.src_serving) for a in fx.cl.assigns()]
+    want = [(a["replica"], a["version"], a["src"], a["src_serving"]) for a in plan["assigns"]]
+    assert got == want
+    for r in names[1:]:
+        for n, _ in plan["tensors"]:
+            assert fx.same("trainer", r, 0, n)
+
+
+def test_corrupt_source_quiet_retry_report_repick(fx):
+    # test_client_core.cpp:346-377
+    from paper_2604_09107_b200.ros import Status
+    t1 = fx.make("T1")
+    fx.reg("T1", 0, "big", 3 << 20, 11)
+    fx.reg("T1", 0, "tiny", 5000, 12)
+    assert t1.publish(1).status == Status.ok
+    t2 = fx.make("T2")
+    fx.reg("T2", 0, "big", 3 << 20, 20)
+    fx.reg("T2", 0, "tiny", 5000, 21)
+    assert t2.replicate().status == Status.ok
+    fx.bufs[("T2", 0, "big")][17] ^= 0xFF  # corrupt T2's copy in place
+    w = fx.make("R")
+    fx.reg("R", 0, "big", 3 << 20, 30)
+    fx.reg("R", 0, "tiny", 5000, 31)
+    r = w.replicate()
+    assert r.status == Status.ok
+    st = w.stats()
+    assert st.checksum_failures == 2  # first attempt + quiet retry
+    assert st.failure_reports == 1
+    assert fx.same("T1", "R", 0, "big") and fx.same("T1", "R", 0, "tiny")
+    assert "T2" in fx.cl.listing("m")[1]  # corruption does not condemn
+
+
+def test_silent_source_is_reported_and_pull_moves(fx):
+    # test_client_core.cpp:317-344
+    from paper_2604_09107_b200.ros import Status
+    t1 = fx.make("T1", pull_timeout_s=0.5)
+    fx.reg("T1", 0, "w", 150000, 6)
+    assert t1.publish(1).status == Status.ok
+    t2 = fx.make("T2", pull_timeout_s=0.5)
+    fx.reg("T2", 0, "w", 150000, 60)
+    assert t2.replicate().status == Status.ok
+    fx.cl.set_silent("m", "T2", True)
+    w = fx.make("R", pull_timeout_s=0.5)
+    fx.reg("R", 0, "w", 150000, 70)
+    r = w.replicate()
+    assert r.status == Status.ok
+    assert w.stats().failure_reports >= 1
+    assert fx.same("T1", "R", 0, "w")
+    lm = fx.cl.listing("m")
+    assert "T2" not in lm[1] and "T1" in lm[1]
+
+
+def test_update_moves_to_newer_version(fx, oracle):
+    from paper_2604_09107_b200.ros import Status
+    t = fx.make("T")
+    fx.reg("T", 0, "w", 200000, 1)
+    assert t.publish(1).status == Status.ok
+    w = fx.make("R")
+    fx.reg("R", 0, "w", 200000, 2)
+    r = w.update("latest")
+    assert r.status == Status.ok and r.changed and r.version == 1
+    r = w.update("latest")
+    assert r.status == Status.ok and not r.changed
+    # trainer mutates in place and publishes v2
+    assert t.unpublish().status == Status.ok
+    fx.bufs[("T", 0, "w")].copy_(torch.from_numpy(pattern(200000, 9)).cuda())
+    assert t.publish(2).status == Status.ok
+    r = w.update("latest")
+    assert r.status == Status.ok and r.changed and r.version == 2
+    assert fx.same("T", "R", 0, "w")
+    assert w.current_version == 2
+
+
+def test_resume_moves_no_bytes_then_invalidate_repulls(fx):
+    from paper_2604_09107_b200.ros import Status
+    t = fx.make("T")
+    fx.reg("T", 0, "w", 1 << 20, 1)
+    assert t.publish(1).status == Status.ok
+    w = fx.make("R")
+    fx.reg("R", 0, "w", 1 << 20, 2)
+    assert w.replicate().status == Status.ok
+    pulled = w.stats().bytes_pulled
+    assert w.unpublish().status == Status.ok
+    assert w.replicate().status == Status.ok
+    assert w.stats().bytes_pulled == pulled  # verified prefix kept: resumed
+    assert w.unpublish().status == Status.ok
+    w.invalidate()
+    assert w.replicate().status == Status.ok
+    assert w.stats().bytes_pulled == 2 * pulled
+
+
+def test_bind_rejects_mismatched_registration(fx):
+    from paper_2604_09107_b200.ros import Status
+    t = fx.make("T")
+    fx.reg("T", 0, "w", 4096, 1)
+    assert t.publish(1).status == Status.ok
+    w = fx.make("R")
+    fx.reg("R", 0, "w", 4000, 2)  # wrong length (client_core.cpp:1601-1608)
+    assert w.replicate().status == Status.invalid_argument
+
+
+def test_multi_gpu_chain_with_chasing():
+    """Readers on different GPUs fill concurrently, each chasing its upstream's
+    device watermark over NVLink (peer access)."""
+    n = torch.cuda.device_count()
+    if n < 2:
+        pytest.skip("needs >= 2 GPUs")
+    from paper_2604_09107_b200.ros import Status
+    f = Fix()
+    try:
+        names = ["trainer"] + [f"r{i}" for i in range(1, n)]
+        size = 256 << 20
+        for i, r in enumerate(names):
+            f.make(r, dev=i)
+            f.reg(r, 0, "w", size, 1 if i == 0 else 99)
+            f.reg(r, 0, "norm", 8192, 2 if i == 0 else 98)
+        assert f.h["trainer"].publish(1).status == Status.ok
+        results = {}
+
+        def run(r):
+            results[r] = f.h[r].replicate()
+
+        ths = [threading.Thread(target=run, args=(r,)) for r in names[1:]]
+        for th in ths:
+            th.start()
+        for th in ths:
+            th.join()
+        assert all(v.status == Status.ok for v in results.values()), results
+        # threads arrive in any order; the plan is still a chain: every
+        # replica serves exactly one downstream reader
+        srcs = [a.src for a in f.cl.assigns()]
+        assert len(set(srcs)) == len(srcs) and "trainer" in srcs
+        for r in names[1:]:
+            assert f.same("trainer", r, 0, "w") and f.same("trainer", r, 0, "norm")
+    finally:
+        f.close()
