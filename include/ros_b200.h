@@ -88,6 +88,9 @@ int rs_cluster_listing(rs_cluster* c, const char* model, char* buf, size_t cap, 
 /* ServerCore::replica_view (server_core.hpp:42-50). lifecycle buffer >= 16. */
 int rs_cluster_view(rs_cluster* c, const char* model, const char* replica, char* lifecycle,
                     uint64_t* version, uint32_t* serving, int* visible);
+/* The source replica a replicating replica currently pulls from ("" if none). */
+int rs_cluster_source(rs_cluster* c, const char* model, const char* replica, char* buf,
+                      size_t cap, size_t* len);
 /* Fault hook (MemNetwork::set_data_silent, transport_mem.hpp:33-46): a
  * silent replica's data plane never answers, so its readers time out. */
 int rs_cluster_set_silent(rs_cluster* c, const char* model, const char* replica, int silent);
@@ -168,7 +171,9 @@ int rs_bf16_to_e4m3(const void* dev_src, void* dev_dst, uint64_t n_elems, void* 
 /* copy_slice_locked (transport.cpp:51-69) + chunk verification, standalone:
  * copy n_items (src -> dst, len) spans cut into chunk_bytes chunks, verify
  * against expect (device, may be NULL) and write the computed chunk digests
- * to out_digests (device, may be NULL).  Reports the kernel status. */
+ * to out_digests (device, may be NULL).  Both tables are indexed batch
+ * aligned: item i's chunks start at round_up(end of item i-1, 32); entries
+ * in between are unused.  Reports the kernel status. */
 int rs_pull_spans(const uint64_t* src_ptrs, const uint64_t* dst_ptrs, const uint64_t* lens,
                   int n_items, uint64_t chunk_bytes, const uint64_t* expect_dev,
                   uint64_t* out_digests_dev, int device, void* cuda_stream, int* kernel_code,

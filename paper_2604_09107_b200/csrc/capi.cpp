@@ -133,6 +133,14 @@ int rs_cluster_view(rs_cluster* c, const char* model, const char* replica, char*
   return 0;
 }
 
+int rs_cluster_source(rs_cluster* c, const char* model, const char* replica, char* buf,
+                      size_t cap, size_t* len) {
+  if (!c || !model || !replica) return st(rsb::Status::invalid_argument);
+  auto v = c->reg.view(model, replica);
+  if (!v) return st(rsb::Status::not_found);
+  return put_bytes(v->source, buf, cap, len);
+}
+
 int rs_cluster_set_silent(rs_cluster* c, const char* model, const char* replica, int silent) {
   if (!c || !model || !replica) return st(rsb::Status::invalid_argument);
   c->serves.set_silent(model, replica, silent != 0);
@@ -464,37 +472,33 @@ int rs_pull_spans(const uint64_t* src_ptrs, const uint64_t* dst_ptrs, const uint
   cudaGetDevice(&prev);
   cudaSetDevice(device);
   auto stream = static_cast<cudaStream_t>(cuda_stream);
+  // Item i's chunks start at a multiple of 32 (batch aligned, as in
+  // ChunkMap::uniform); indices in between are holes of expect/out tables.
   std::vector<rsb::dev::ItemDesc> descs(n_items);
   std::uint32_t chunk = 0;
   for (int i = 0; i < n_items; ++i) {
     descs[i] = {src_ptrs[i], dst_ptrs ? dst_ptrs[i] : 0, lens[i], chunk,
                 static_cast<std::uint32_t>(chunk_bytes)};
-    chunk += static_cast<std::uint32_t>((lens[i] + chunk_bytes - 1) / chunk_bytes);
+    const auto n = static_cast<std::uint32_t>((lens[i] + chunk_bytes - 1) / chunk_bytes);
+    chunk += (n + rsb::dev::kBatchChunks - 1) / rsb::dev::kBatchChunks * rsb::dev::kBatchChunks;
   }
-  const std::size_t dbytes = descs.size() * sizeof(rsb::dev::ItemDesc);
-  rsb::DevBuf t;
+  rsb::dev::PlanUpload plan;
   int rc = 0;
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   rsb::dev::PullStatus ps{};
-  if (!rsb::ok(t.alloc(device, dbytes + 128))) rc = st(rsb::Status::transfer_failed);
+  rsb::dev::PullParams p{};
+  if (rsb::dev::upload_pull_plan(device, stream, descs.data(), static_cast<std::uint32_t>(n_items),
+                                 &plan, &p) != cudaSuccess)
+    rc = st(rsb::Status::transfer_failed);
   if (!rc) {
-    auto* base = static_cast<std::uint8_t*>(t.p);
-    rsb::dev::PullParams p{};
-    p.items = reinterpret_cast<const rsb::dev::ItemDesc*>(base);
-    p.n_items = static_cast<std::uint32_t>(n_items);
     p.n_chunks = chunk;
     p.n_batches = (chunk + rsb::dev::kBatchChunks - 1) / rsb::dev::kBatchChunks;
     p.src_digests = expect_dev;
     p.dst_digests = out_digests_dev;
-    p.work = reinterpret_cast<std::uint32_t*>(base + dbytes);
-    p.status = reinterpret_cast<rsb::dev::PullStatus*>(base + dbytes + 64);
     p.timeout_ns = 4000000000ull;
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
-    if ((dbytes && cudaMemcpyAsync(base, descs.data(), dbytes, cudaMemcpyHostToDevice, stream) !=
-                       cudaSuccess) ||
-        cudaMemsetAsync(base + dbytes, 0, 128, stream) != cudaSuccess ||
-        cudaEventRecord(e0, stream) != cudaSuccess ||
+    if (cudaEventRecord(e0, stream) != cudaSuccess ||
         rsb::dev::launch_pull(p, rsb::dev::pull_grid(device), stream) != cudaSuccess ||
         cudaEventRecord(e1, stream) != cudaSuccess ||
         cudaMemcpyAsync(&ps, p.status, sizeof(ps), cudaMemcpyDeviceToHost, stream) != cudaSuccess ||
@@ -507,6 +511,7 @@ int rs_pull_spans(const uint64_t* src_ptrs, const uint64_t* dst_ptrs, const uint
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
   }
+  rsb::dev::free_pull_plan(device, &plan);
   cudaSetDevice(prev);
   return rc;
 }

@@ -157,12 +157,15 @@ Status DevBuf::alloc(int device, std::size_t bytes) {
 
 ChunkMap ChunkMap::uniform(const Manifest& m, std::uint64_t chunk_bytes) {
   ChunkMap c;
-  c.chunk0.push_back(0);
+  std::uint32_t next = 0;
   for (const auto& it : m.items()) {
-    std::uint64_t n = (it.length + chunk_bytes - 1) / chunk_bytes;
+    const auto n = static_cast<std::uint32_t>((it.length + chunk_bytes - 1) / chunk_bytes);
+    c.chunk0.push_back(next);
     c.chunk_len.push_back(static_cast<std::uint32_t>(chunk_bytes));
-    c.chunk0.push_back(c.chunk0.back() + static_cast<std::uint32_t>(n));
+    c.count.push_back(n);
+    next += (n + dev::kBatchChunks - 1) / dev::kBatchChunks * dev::kBatchChunks;
   }
+  c.chunk0.push_back(next);
   return c;
 }
 
@@ -251,6 +254,7 @@ Result<std::string> ServeRegistry::export_state(const std::string& k) {
   w.vec(st->item_ends);
   w.vec(st->cmap.chunk0);
   w.vec(st->cmap.chunk_len);
+  w.vec(st->cmap.count);
   w.vec(allocs);
   w.vec(item_loc);
   w.pod(dl);
@@ -272,6 +276,7 @@ Status ServeRegistry::import_state(const std::string& blob) {
   auto ends = r.vec<std::uint64_t>();
   auto c0 = r.vec<std::uint32_t>();
   auto cl = r.vec<std::uint32_t>();
+  auto cc = r.vec<std::uint32_t>();
   auto allocs = r.vec<ServeState::Alloc>();
   auto item_loc = r.vec<std::pair<std::uint32_t, std::uint64_t>>();
   auto dl = r.pod<std::pair<std::uint32_t, std::uint64_t>>();
@@ -291,6 +296,7 @@ Status ServeRegistry::import_state(const std::string& blob) {
   st->item_ends = std::move(ends);
   st->cmap.chunk0 = std::move(c0);
   st->cmap.chunk_len = std::move(cl);
+  st->cmap.count = std::move(cc);
   st->allocs = std::move(allocs);
   st->item_loc = std::move(item_loc);
   st->digests_loc = dl;
@@ -368,6 +374,7 @@ Client::~Client() {
     if (sh.ev0) cudaEventDestroy(sh.ev0);
     if (sh.ev1) cudaEventDestroy(sh.ev1);
     if (sh.own_stream && sh.stream) cudaStreamDestroy(sh.stream);
+    dev::free_pull_plan(sh.device, &sh.plan);
   }
 }
 
@@ -510,31 +517,25 @@ Status Client::build_payload(Shard& sh, VersionId v, std::shared_ptr<Payload>* o
   if (Status s = p->digests.alloc(sh.device, std::size_t(nc) * 8); !ok(s)) return s;
   if (Status s = p->flags.alloc(sh.device, std::size_t(nb) * 4); !ok(s)) return s;
   RS_CUDA(cudaMemsetAsync(p->flags.p, 0, std::size_t(nb) * 4, sh.stream));
+  RS_CUDA(cudaMemsetAsync(p->digests.p, 0, std::size_t(nc) * 8, sh.stream));
   p->epoch = ++sh.epoch_ctr;
   if (nc) {
+    // Chunk digest table of the published bytes (hash-only pull), and every
+    // watermark set: a complete source.
     std::vector<dev::ItemDesc> descs(items.size());
     for (std::size_t i = 0; i < items.size(); ++i)
       descs[i] = {p->item_ptrs[i], 0, items[i].length, p->cmap.chunk0[i], p->cmap.chunk_len[i]};
-    const std::size_t dbytes = descs.size() * sizeof(dev::ItemDesc);
-    if (Status s = sh.scratch.alloc(sh.device, dbytes + 128); !ok(s)) return s;
-    auto* base = static_cast<std::uint8_t*>(sh.scratch.p);
-    auto* work = reinterpret_cast<std::uint32_t*>(base + dbytes);
-    auto* status = reinterpret_cast<dev::PullStatus*>(base + dbytes + 64);
-    RS_CUDA(cudaMemcpyAsync(base, descs.data(), dbytes, cudaMemcpyHostToDevice, sh.stream));
-    RS_CUDA(cudaMemsetAsync(work, 0, 128, sh.stream));
     dev::PullParams pp{};
-    pp.items = reinterpret_cast<const dev::ItemDesc*>(base);
-    pp.n_items = static_cast<std::uint32_t>(descs.size());
+    RS_CUDA(dev::upload_pull_plan(sh.device, sh.stream, descs.data(),
+                                  static_cast<std::uint32_t>(descs.size()), &sh.plan, &pp));
     pp.n_chunks = nc;
     pp.n_batches = nb;
     pp.dst_digests = static_cast<std::uint64_t*>(p->digests.p);
     pp.dst_flags = static_cast<std::uint32_t*>(p->flags.p);
     pp.dst_epoch = p->epoch;
-    pp.work = work;
-    pp.status = status;
     pp.timeout_ns = static_cast<std::uint64_t>(cfg_.pull_timeout_s * 1e9);
     RS_CUDA(dev::launch_pull(pp, dev::pull_grid(sh.device), sh.stream));
-    stats_.h2d_bytes += dbytes;
+    stats_.h2d_bytes += sh.plan.h2d_bytes;
   }
   RS_CUDA(cudaEventRecord(sh.ev1, sh.stream));
   RS_CUDA(cudaStreamSynchronize(sh.stream));
@@ -620,7 +621,10 @@ void Client::serve(Shard& sh, VersionId v, bool complete) {
 
 void Client::invalidate() {
   for (auto& sh : shards_) {
-    if (sh.holding) sh.holding->epoch = ++sh.epoch_ctr;
+    if (sh.holding) {
+      sh.holding->epoch = ++sh.epoch_ctr;
+      sh.holding->landed_some = false;
+    }
     sh.partial_version.reset();
   }
   current_.reset();
@@ -663,7 +667,10 @@ Status Client::bind(Shard& sh, const Assignment& a, VersionId v) {
     // Identical manifest: resume.  Keeping the fill epoch keeps every batch
     // already landed for this version (flag == epoch) out of the pull.
     bool resume = (current_ && *current_ == v) || (sh.partial_version && *sh.partial_version == v);
-    if (!resume) sh.holding->epoch = ++sh.epoch_ctr;
+    if (!resume) {
+      sh.holding->epoch = ++sh.epoch_ctr;
+      sh.holding->landed_some = false;
+    }
     sh.partial_version = v;
     return Status::ok;
   }
@@ -700,6 +707,7 @@ Status Client::bind(Shard& sh, const Assignment& a, VersionId v) {
   if (Status s = p->digests.alloc(sh.device, std::size_t(nc) * 8); !ok(s)) return s;
   if (Status s = p->flags.alloc(sh.device, std::size_t(nb) * 4); !ok(s)) return s;
   RS_CUDA(cudaMemsetAsync(p->flags.p, 0, std::size_t(nb) * 4, sh.stream));
+  RS_CUDA(cudaMemsetAsync(p->digests.p, 0, std::size_t(nc) * 8, sh.stream));
   RS_CUDA(cudaStreamSynchronize(sh.stream));
   p->epoch = ++sh.epoch_ctr;
   sh.holding = std::move(p);
@@ -729,17 +737,10 @@ Status Client::launch_fill(Shard& sh, const SourceView& src, bool src_complete) 
   for (std::size_t i = 0; i < items.size(); ++i)
     descs[i] = {src.item_ptrs[i], p.item_ptrs[i], items[i].length, p.cmap.chunk0[i],
                 p.cmap.chunk_len[i]};
-  const std::size_t dbytes = descs.size() * sizeof(dev::ItemDesc);
-  if (Status s = sh.scratch.alloc(sh.device, dbytes + 128); !ok(s)) return s;
-  auto* base = static_cast<std::uint8_t*>(sh.scratch.p);
-  auto* work = reinterpret_cast<std::uint32_t*>(base + dbytes);
-  auto* status = reinterpret_cast<dev::PullStatus*>(base + dbytes + 64);
-  if (dbytes) RS_CUDA(cudaMemcpyAsync(base, descs.data(), dbytes, cudaMemcpyHostToDevice, sh.stream));
-  RS_CUDA(cudaMemsetAsync(work, 0, 128, sh.stream));
-  stats_.h2d_bytes += dbytes;
   dev::PullParams pp{};
-  pp.items = reinterpret_cast<const dev::ItemDesc*>(base);
-  pp.n_items = static_cast<std::uint32_t>(descs.size());
+  RS_CUDA(dev::upload_pull_plan(sh.device, sh.stream, descs.data(),
+                                static_cast<std::uint32_t>(descs.size()), &sh.plan, &pp));
+  stats_.h2d_bytes += sh.plan.h2d_bytes;
   pp.n_chunks = p.cmap.n_chunks();
   pp.n_batches = p.cmap.n_batches();
   pp.src_digests = reinterpret_cast<const std::uint64_t*>(src.digests);
@@ -748,12 +749,12 @@ Status Client::launch_fill(Shard& sh, const SourceView& src, bool src_complete) 
   pp.src_epoch = src.epoch;
   pp.dst_flags = static_cast<std::uint32_t*>(p.flags.p);
   pp.dst_epoch = p.epoch;
-  pp.work = work;
-  pp.status = status;
   pp.timeout_ns = static_cast<std::uint64_t>(cfg_.pull_timeout_s * 1e9);
+  pp.resume = p.landed_some ? 1u : 0u;
   RS_CUDA(cudaEventRecord(sh.ev0, sh.stream));
   RS_CUDA(dev::launch_pull(pp, dev::pull_grid(sh.device), sh.stream));
   RS_CUDA(cudaEventRecord(sh.ev1, sh.stream));
+  sh.holding->landed_some = true;
   return Status::ok;
 }
 
@@ -785,9 +786,7 @@ std::vector<Client::FillOutcome> Client::fill_shards(const std::vector<Assignmen
     if (!launched[i]) continue;
     Shard& sh = shards_[i];
     DeviceGuard g(sh.device);
-    const std::size_t dbytes = sh.holding->manifest.items().size() * sizeof(dev::ItemDesc);
-    auto* status = reinterpret_cast<dev::PullStatus*>(static_cast<std::uint8_t*>(sh.scratch.p) +
-                                                      dbytes + 64);
+    auto* status = reinterpret_cast<dev::PullStatus*>(static_cast<std::uint8_t*>(sh.plan.scratch) + 64);
     cudaMemcpyAsync(&st[i], status, sizeof(dev::PullStatus), cudaMemcpyDeviceToHost, sh.stream);
     cudaError_t e = cudaStreamSynchronize(sh.stream);
     stats_.d2h_bytes += sizeof(dev::PullStatus);
@@ -964,9 +963,15 @@ Status Client::chunk_digests(std::uint32_t shard, std::vector<std::uint64_t>* ou
   if (shard >= num_shards_ || !shards_[shard].holding) return Status::not_found;
   Shard& sh = shards_[shard];
   DeviceGuard g(sh.device);
-  out->resize(sh.holding->cmap.n_chunks());
-  if (out->empty()) return Status::ok;
-  RS_CUDA(cudaMemcpy(out->data(), sh.holding->digests.p, out->size() * 8, cudaMemcpyDeviceToHost));
+  const ChunkMap& cm = sh.holding->cmap;
+  std::vector<std::uint64_t> raw(cm.n_chunks());
+  out->clear();
+  if (raw.empty()) return Status::ok;
+  RS_CUDA(cudaMemcpy(raw.data(), sh.holding->digests.p, raw.size() * 8, cudaMemcpyDeviceToHost));
+  // dense, in item order: the holes between batch-aligned items are skipped
+  out->reserve(cm.n_real());
+  for (std::size_t i = 0; i < cm.count.size(); ++i)
+    out->insert(out->end(), raw.begin() + cm.chunk0[i], raw.begin() + cm.chunk0[i] + cm.count[i]);
   return Status::ok;
 }
 

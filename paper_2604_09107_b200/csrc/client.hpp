@@ -59,17 +59,25 @@ struct DevBuf {
 
 // Item -> digest chunks.  Chunks are item-relative; chunk j of item i covers
 // [j*len_i, min((j+1)*len_i, item_len)).  Batches of 32 chunks carry one
-// watermark flag.
+// watermark flag.  Every item starts a new batch (its first chunk index is a
+// multiple of 32), so a batch never spans items; the unused indices between
+// items are holes (no bytes, no digest).
 struct ChunkMap {
-  std::vector<std::uint32_t> chunk0;     // n_items + 1 prefix
+  std::vector<std::uint32_t> chunk0;     // n_items + 1 prefix (batch aligned)
   std::vector<std::uint32_t> chunk_len;  // per item
+  std::vector<std::uint32_t> count;      // real chunks per item
   std::uint32_t n_chunks() const { return chunk0.empty() ? 0 : chunk0.back(); }
   std::uint32_t n_batches() const {
     return (n_chunks() + dev::kBatchChunks - 1) / dev::kBatchChunks;
   }
+  std::uint64_t n_real() const {
+    std::uint64_t n = 0;
+    for (auto c : count) n += c;
+    return n;
+  }
   static ChunkMap uniform(const Manifest& m, std::uint64_t chunk_bytes);
   bool operator==(const ChunkMap& o) const {
-    return chunk0 == o.chunk0 && chunk_len == o.chunk_len;
+    return chunk0 == o.chunk0 && chunk_len == o.chunk_len && count == o.count;
   }
 };
 
@@ -216,6 +224,7 @@ class Client {
     DevBuf digests;
     DevBuf flags;
     std::uint32_t epoch = 0;
+    bool landed_some = false;  // a fill ran in this epoch: flags may be set
     std::vector<std::uint64_t> item_ptrs;  // own landing/serving address per item
   };
   struct Shard {
@@ -229,7 +238,7 @@ class Client {
     std::shared_ptr<ServeState> serve;
     cudaStream_t stream = nullptr;
     bool own_stream = false;
-    DevBuf scratch;  // descriptor tables + work/status words
+    dev::PlanUpload plan;  // item table + tensor maps + work/status words
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     std::uint32_t epoch_ctr = 0;
   };

@@ -1,0 +1,221 @@
+// Device helpers shared by the sm_100a kernels: XXH64 pieces (reference
+// digest.cpp:13-75 restated for the device), PTX wrappers for cp.async,
+// TMA bulk copies, mbarriers and system-scope acquire/release.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "device.hpp"
+
+namespace rsb::dev::detail {
+
+constexpr std::uint64_t kP1 = 0x9E3779B185EBCA87ULL;
+constexpr std::uint64_t kP2 = 0xC2B2AE3D27D4EB4FULL;
+constexpr std::uint64_t kP3 = 0x165667B19E3779F9ULL;
+constexpr std::uint64_t kP4 = 0x85EBCA77C2B2AE63ULL;
+constexpr std::uint64_t kP5 = 0x27D4EB2F165667C5ULL;
+
+__device__ __forceinline__ std::uint64_t rotl64(std::uint64_t x, int r) {
+  return (x << r) | (x >> (64 - r));
+}
+// One accumulator step of the 32-byte stripe loop (round64).
+__device__ __forceinline__ std::uint64_t xround(std::uint64_t acc, std::uint64_t w) {
+  return rotl64(acc + w * kP2, 31) * kP1;
+}
+__device__ __forceinline__ std::uint64_t avalanche(std::uint64_t h) {
+  h ^= h >> 33;
+  h *= kP2;
+  h ^= h >> 29;
+  h *= kP3;
+  h ^= h >> 32;
+  return h;
+}
+// Fold of the four accumulators (merge_round x4).
+__device__ __forceinline__ std::uint64_t merge4(std::uint64_t a, std::uint64_t b,
+                                                std::uint64_t c, std::uint64_t d) {
+  std::uint64_t h = rotl64(a, 1) + rotl64(b, 7) + rotl64(c, 12) + rotl64(d, 18);
+  h = (h ^ xround(0, a)) * kP1 + kP4;
+  h = (h ^ xround(0, b)) * kP1 + kP4;
+  h = (h ^ xround(0, c)) * kP1 + kP4;
+  h = (h ^ xround(0, d)) * kP1 + kP4;
+  return h;
+}
+// Tail (< 32 bytes), then avalanche (finalize).
+static __device__ __noinline__ std::uint64_t finish_tail(std::uint64_t h, const std::uint8_t* p, int n) {
+  while (n >= 8) {
+    std::uint64_t w = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) w |= std::uint64_t(p[k]) << (8 * k);
+    h ^= xround(0, w);
+    h = rotl64(h, 27) * kP1 + kP4;
+    p += 8;
+    n -= 8;
+  }
+  if (n >= 4) {
+    std::uint32_t w = std::uint32_t(p[0]) | (std::uint32_t(p[1]) << 8) |
+                      (std::uint32_t(p[2]) << 16) | (std::uint32_t(p[3]) << 24);
+    h ^= std::uint64_t(w) * kP1;
+    h = rotl64(h, 23) * kP2 + kP3;
+    p += 4;
+    n -= 4;
+  }
+  while (n > 0) {
+    h ^= std::uint64_t(*p) * kP5;
+    h = rotl64(h, 11) * kP1;
+    ++p;
+    --n;
+  }
+  return avalanche(h);
+}
+
+__device__ __forceinline__ std::uint32_t smem_u32(const void* p) {
+  return static_cast<std::uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(smem)), "l"(gmem)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() {
+  asm volatile("cp.async.commit_group;\n" ::: "memory");
+}
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ std::uint32_t ld_acquire_sys(const std::uint32_t* p) {
+  std::uint32_t v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_sys(std::uint32_t* p, std::uint32_t v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ std::uint64_t globaltimer() {
+  std::uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;\n" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ std::uint32_t ld_volatile(const std::uint32_t* p) {
+  return *reinterpret_cast<const volatile std::uint32_t*>(p);
+}
+
+// Waits until the upstream watermark of a batch reaches `epoch`.
+static __device__ __noinline__ std::uint32_t wait_flag(const std::uint32_t* flag, std::uint32_t epoch,
+                                                std::uint64_t timeout_ns,
+                                                const std::uint32_t* abort) {
+  std::uint64_t t0 = 0;
+  unsigned ns = 32;
+  for (;;) {
+    std::uint32_t v = ld_acquire_sys(flag);
+    if (v == epoch) return kPullOk;
+    if (v > epoch) return kPullNotServing;  // newer fill or abort bit
+    if (ld_volatile(abort)) return kPullAborted;
+    std::uint64_t now = globaltimer();
+    if (t0 == 0) t0 = now;
+    if (now - t0 > timeout_ns) return kPullTimeout;
+    __nanosleep(ns);
+    if (ns < 1024) ns <<= 1;
+  }
+}
+
+// ---- mbarrier / TMA bulk ---------------------------------------------------
+__device__ __forceinline__ void mbar_init(unsigned long long* b, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(b)), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive_tx(unsigned long long* b, unsigned tx) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(b)),
+               "r"(tx)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(unsigned long long* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(b)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* smem, const void* gmem, unsigned bytes,
+                                         unsigned long long* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, "
+      "[%3];\n" ::"r"(smem_u32(smem)),
+      "l"(gmem), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void bulk_s2g(void* gmem, const void* smem, unsigned bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(gmem),
+               "r"(smem_u32(smem)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() {
+  asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+}
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;\n" ::"n"(N) : "memory");
+}
+template <int N>
+__device__ __forceinline__ void bulk_wait() {
+  asm volatile("cp.async.bulk.wait_group %0;\n" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_global() {
+  asm volatile("fence.proxy.async.global;\n" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+}
+
+// XXH64 of one chunk straight from (possibly peer) global memory, optionally
+// storing it to dst: the quiet same-source retry after a mismatch
+// (client_core.cpp:336-357).  Rare path.
+static __device__ __noinline__ std::uint64_t repull_chunk(const std::uint8_t* src, std::uint8_t* dst,
+                                                   std::uint32_t len) {
+  std::uint64_t v1 = kP1 + kP2, v2 = kP2, v3 = 0, v4 = 0 - kP1;
+  std::uint32_t i = 0;
+  std::uint8_t tail[32];
+  for (; i + 32 <= len; i += 32) {
+    std::uint64_t w[4];
+    for (int k = 0; k < 4; ++k) {
+      std::uint64_t x = 0;
+      for (int b = 0; b < 8; ++b) x |= std::uint64_t(__ldcg(src + i + 8 * k + b)) << (8 * b);
+      w[k] = x;
+    }
+    v1 = xround(v1, w[0]);
+    v2 = xround(v2, w[1]);
+    v3 = xround(v3, w[2]);
+    v4 = xround(v4, w[3]);
+    if (dst)
+      for (int b = 0; b < 32; ++b) dst[i + b] = static_cast<std::uint8_t>(w[b >> 3] >> (8 * (b & 7)));
+  }
+  const int t = static_cast<int>(len - i);
+  for (int b = 0; b < t; ++b) {
+    tail[b] = __ldcg(src + i + b);
+    if (dst) dst[i + b] = tail[b];
+  }
+  std::uint64_t h = len >= 32 ? merge4(v1, v2, v3, v4) : kP5;
+  h += len;
+  return finish_tail(h, tail, t);
+}
+
+// Last item whose first chunk is <= c (items sorted by chunk0).
+__device__ __forceinline__ std::uint32_t find_item(const ItemDesc* items, std::uint32_t n,
+                                                   std::uint32_t c) {
+  std::uint32_t lo = 0, hi = n;
+  while (hi - lo > 1) {
+    const std::uint32_t mid = (lo + hi) >> 1;
+    if (items[mid].chunk0 <= c) lo = mid;
+    else hi = mid;
+  }
+  return lo;
+}
+
+}  // namespace rsb::dev::detail

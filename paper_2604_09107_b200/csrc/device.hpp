@@ -4,6 +4,7 @@
 
 #include <cuda_runtime.h>
 
+#include <cstddef>
 #include <cstdint>
 
 namespace rsb::dev {
@@ -26,8 +27,14 @@ struct ItemDesc {
   std::uint64_t dst;        // landing address (0: hash-only)
   std::uint64_t len;        // bytes
   std::uint32_t chunk0;     // global index of the item's first chunk
-  std::uint32_t chunk_len;  // uniform chunk length inside the item
+  std::uint32_t chunk_len;  // uniform chunk length inside the item | kHasMap
 };
+// ItemDesc.chunk_len flag: the item has TMA tensor maps (2-D view
+// [len / chunk_len rows][chunk_len bytes]) at PullParams.maps + 256*i
+// (source) and + 256*i + 128 (destination).
+constexpr std::uint32_t kHasMap = 0x80000000u;
+constexpr std::uint32_t kChunkLenMask = 0x7fffffffu;
+constexpr int kMapBoxCols = 128;  // TMA box: 128 bytes x 32 rows, 128B swizzle
 
 enum PullCode : std::uint32_t {
   kPullOk = 0,
@@ -61,11 +68,29 @@ struct PullParams {
   std::uint32_t* work;               // [0] batch ticket, [1] abort
   PullStatus* status;
   std::uint64_t timeout_ns;
+  std::uint32_t resume;              // dst_flags may already hold dst_epoch
+  std::uint32_t pad;
+  const void* maps;                  // CUtensorMap pairs per item (or null)
 };
 
-// Fused mover: copy + per-chunk XXH64 verify + watermark publish.
-cudaError_t launch_pull(const PullParams& p, int grid, cudaStream_t s);
-int pull_grid(int device);  // persistent grid size for the device
+// Uploads a pull plan (item table + TMA tensor maps + work/status words)
+// into `scratch` on `device` and points `p` at it.  Items whose source (and
+// destination) are 16-byte aligned get tensor maps (kHasMap).  Declared
+// here, implemented in pullplan.cpp.
+struct PlanUpload {
+  void* scratch = nullptr;       // device buffer (grown by the callee)
+  std::size_t scratch_bytes = 0;
+  std::size_t h2d_bytes = 0;     // bytes uploaded by the last call
+};
+cudaError_t upload_pull_plan(int device, cudaStream_t s, ItemDesc* items, std::uint32_t n_items,
+                             PlanUpload* up, PullParams* p);
+void free_pull_plan(int device, PlanUpload* up);
+
+// Fused mover: copy + per-chunk XXH64 verify + watermark publish.  `sms` is
+// the device's SM count (pull_grid); the persistent grid is sized from it.
+cudaError_t launch_pull(const PullParams& p, int sms, cudaStream_t s);
+int pull_grid(int device);  // SM count of the device
+const char* pull_kernel_name();
 
 // XXH64 (reference digest64) of n spans, one warp per span.
 cudaError_t launch_span_digests(const std::uint64_t* ptrs, const std::uint64_t* lens,

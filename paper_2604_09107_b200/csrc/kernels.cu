@@ -1,151 +1,44 @@
-// sm_100a kernels of the ROS read path.
+// sm_100a kernels of the ROS read path (besides the TMA pull in pull_tma.cu).
 //
-//   pull_kernel        K1+K2: SM-driven copy of the item stream from a source
-//                      GPU (local HBM, NVLink peer, or IPC-mapped peer) into
-//                      the reader's regions, fused with per-chunk XXH64
-//                      verification and a per-batch release watermark that
-//                      downstream readers chase (replaces copy_slice_locked,
-//                      transport.cpp:51-69, and the per-item digest64 check
-//                      of TransferTask::verify_ready, client_core.cpp:306-334).
+//   pull_kernel        K1+K2 on the LDGSTS path (RSB_PULL_KERNEL=ldg): the
+//                      same contract as pull_tma_kernel with cp.async 16-byte
+//                      copies issued by every lane; kept as the variant for
+//                      comparisons and as a fallback.
 //   span_digest_kernel K6: reference-identical XXH64 of whole items/groups
 //                      (digest64, digest.cpp:79-106) for the manifest.
 //   copy_spans_kernel  K3: pack/unpack of tiny-tensor groups
 //                      (pack_group / unpack_group, manifest.cpp:204-225).
 //   synth_bf16_kernel  synthetic weights.
 //   e4m3_kernel        K5: saturating RNE bf16 -> fp8 e4m3.
-//
-// Layout and scheduling: work is cut into item-relative
-// chunks (digest units) and chunks into warp batches of 32; a warp owns one
-// batch at a time (lane l hashes chunk 32b+l), taken from a global ticket so
-// the landed prefix advances front-to-back.  Each step the warp stages the
-// next 256 B of all 32 chunks in shared memory with cp.async (16 B per lane,
-// 256 B contiguous per half-warp), writes the stage to the destination with
-// 128-bit stores and hashes its own slot.  Grid = 2 CTAs x 4 warps per SM.
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
+#include <cstring>
 
+#include "dev_common.cuh"
 #include "device.hpp"
 
 namespace rsb::dev {
 
+using namespace detail;
+
+cudaError_t launch_pull_tma(const PullParams& p, int sms, cudaStream_t s);
+
 namespace {
 
-constexpr std::uint64_t kP1 = 0x9E3779B185EBCA87ULL;
-constexpr std::uint64_t kP2 = 0xC2B2AE3D27D4EB4FULL;
-constexpr std::uint64_t kP3 = 0x165667B19E3779F9ULL;
-constexpr std::uint64_t kP4 = 0x85EBCA77C2B2AE63ULL;
-constexpr std::uint64_t kP5 = 0x27D4EB2F165667C5ULL;
-
-constexpr int kWarps = 4;                   // warps per CTA
+// ------------------------------------------------------- K1+K2, LDGSTS ----
+// A warp owns one batch (lane l hashes chunk 32b+l); each step it stages the
+// next 256 B of all 32 chunks with cp.async (16 B per lane, 256 B contiguous
+// per half-warp), writes the stage to the destination with 128-bit stores
+// and hashes its own slot.
+constexpr int kWarps = 4;
 constexpr int kThreads = kWarps * 32;
-constexpr int kSlot = kPiece + 16;          // padded per-lane slot (bank skew)
-constexpr int kStageBytes = 32 * kSlot;     // one step of one warp
-constexpr int kStages = 3;                  // cp.async pipeline depth
+constexpr int kSlot = kPiece + 16;
+constexpr int kStageBytes = 32 * kSlot;
+constexpr int kStages = 3;
 constexpr int kSmemBytes = kWarps * kStages * kStageBytes;
-constexpr int kUnits = 32 * kPiece / 16 / 32;  // 16-byte units per lane per step
-
-__device__ __forceinline__ std::uint64_t rotl64(std::uint64_t x, int r) {
-  return (x << r) | (x >> (64 - r));
-}
-__device__ __forceinline__ std::uint64_t xround(std::uint64_t acc, std::uint64_t w) {
-  return rotl64(acc + w * kP2, 31) * kP1;
-}
-__device__ __forceinline__ std::uint64_t avalanche(std::uint64_t h) {
-  h ^= h >> 33;
-  h *= kP2;
-  h ^= h >> 29;
-  h *= kP3;
-  h ^= h >> 32;
-  return h;
-}
-// h after the 32-byte stripes (or kP5 if len < 32), plus len.
-__device__ __forceinline__ std::uint64_t merge4(std::uint64_t a, std::uint64_t b,
-                                                std::uint64_t c, std::uint64_t d) {
-  std::uint64_t h = rotl64(a, 1) + rotl64(b, 7) + rotl64(c, 12) + rotl64(d, 18);
-  h = (h ^ xround(0, a)) * kP1 + kP4;
-  h = (h ^ xround(0, b)) * kP1 + kP4;
-  h = (h ^ xround(0, c)) * kP1 + kP4;
-  h = (h ^ xround(0, d)) * kP1 + kP4;
-  return h;
-}
-// Tail (< 32 bytes) from shared memory, then avalanche (digest.cpp:54-75).
-__device__ std::uint64_t finish_tail(std::uint64_t h, const std::uint8_t* p, int n) {
-  while (n >= 8) {
-    std::uint64_t w = 0;
-#pragma unroll
-    for (int k = 0; k < 8; ++k) w |= std::uint64_t(p[k]) << (8 * k);
-    h ^= xround(0, w);
-    h = rotl64(h, 27) * kP1 + kP4;
-    p += 8;
-    n -= 8;
-  }
-  if (n >= 4) {
-    std::uint32_t w = std::uint32_t(p[0]) | (std::uint32_t(p[1]) << 8) |
-                      (std::uint32_t(p[2]) << 16) | (std::uint32_t(p[3]) << 24);
-    h ^= std::uint64_t(w) * kP1;
-    h = rotl64(h, 23) * kP2 + kP3;
-    p += 4;
-    n -= 4;
-  }
-  while (n > 0) {
-    h ^= std::uint64_t(*p) * kP5;
-    h = rotl64(h, 11) * kP1;
-    ++p;
-    --n;
-  }
-  return avalanche(h);
-}
-
-__device__ __forceinline__ std::uint32_t smem_u32(const void* p) {
-  return static_cast<std::uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(smem)),
-               "l"(gmem)
-               : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() {
-  asm volatile("cp.async.commit_group;\n" ::: "memory");
-}
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
-}
-__device__ __forceinline__ std::uint32_t ld_acquire_sys(const std::uint32_t* p) {
-  std::uint32_t v;
-  asm volatile("ld.acquire.sys.global.u32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void st_release_sys(std::uint32_t* p, std::uint32_t v) {
-  asm volatile("st.release.sys.global.u32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
-}
-__device__ __forceinline__ std::uint64_t globaltimer() {
-  std::uint64_t t;
-  asm volatile("mov.u64 %0, %%globaltimer;\n" : "=l"(t));
-  return t;
-}
-__device__ __forceinline__ std::uint32_t ld_volatile(const std::uint32_t* p) {
-  return *reinterpret_cast<const volatile std::uint32_t*>(p);
-}
-
-// Waits until the upstream watermark of a batch reaches `epoch`.
-__device__ std::uint32_t wait_flag(const std::uint32_t* flag, std::uint32_t epoch,
-                                   std::uint64_t timeout_ns, const std::uint32_t* abort) {
-  std::uint64_t t0 = 0;
-  unsigned ns = 32;
-  for (;;) {
-    std::uint32_t v = ld_acquire_sys(flag);
-    if (v == epoch) return kPullOk;
-    if (v > epoch) return kPullNotServing;  // newer fill or abort bit
-    if (ld_volatile(abort)) return kPullAborted;
-    std::uint64_t now = globaltimer();
-    if (t0 == 0) t0 = now;
-    if (now - t0 > timeout_ns) return kPullTimeout;
-    __nanosleep(ns);
-    if (ns < 1024) ns <<= 1;
-  }
-}
+constexpr int kUnits = 32 * kPiece / 16 / 32;
 
 struct LaneChunk {
   const std::uint8_t* src;
@@ -154,7 +47,6 @@ struct LaneChunk {
   std::uint32_t pad;
 };
 
-// Issues the cp.async loads of step `s` of the current batch into `stage`.
 __device__ __forceinline__ void load_step(const LaneChunk* refs, std::uint8_t* stage, int s,
                                           int lane) {
   const int half = lane >> 4;
@@ -177,7 +69,6 @@ __device__ __forceinline__ void load_step(const LaneChunk* refs, std::uint8_t* s
   }
 }
 
-// Writes step `s` of the stage to the destination regions.
 __device__ __forceinline__ void store_step(const LaneChunk* refs, const std::uint8_t* stage,
                                            int s, int lane) {
   const int half = lane >> 4;
@@ -215,11 +106,7 @@ __global__ void __launch_bounds__(kThreads, 2) pull_kernel(const PullParams p) {
     b = __shfl_sync(full, b, 0);
     if (b >= p.n_batches) break;
     if (ld_volatile(&p.work[1])) break;
-
-    // Resume: the batch already landed and verified in this fill.
-    if (p.dst_flags && ld_volatile(&p.dst_flags[b]) == p.dst_epoch) continue;
-
-    // Chase the upstream watermark (pipelined source still filling).
+    if (p.dst_flags && ld_volatile(&p.dst_flags[b]) == p.dst_epoch) continue;  // resume
     if (p.src_flags) {
       std::uint32_t code = 0;
       if (lane == 0) code = wait_flag(&p.src_flags[b], p.src_epoch, p.timeout_ns, &p.work[1]);
@@ -236,24 +123,19 @@ __global__ void __launch_bounds__(kThreads, 2) pull_kernel(const PullParams p) {
         break;
       }
     }
-
-    // Locate this lane's chunk: binary search over item chunk starts.
     const std::uint32_t c = b * kBatchChunks + lane;
     LaneChunk mine{nullptr, nullptr, 0u, 0u};
     std::uint64_t expect = 0;
     if (c < p.n_chunks) {
-      std::uint32_t lo = 0, hi = p.n_items;  // first item with chunk0 > c, minus 1
-      while (hi - lo > 1) {
-        std::uint32_t mid = (lo + hi) >> 1;
-        if (__ldg(&p.items[mid].chunk0) <= c) lo = mid;
-        else hi = mid;
+      const ItemDesc it = p.items[find_item(p.items, p.n_items, c)];
+      const std::uint32_t cunit = it.chunk_len & kChunkLenMask;
+      const std::uint64_t off = std::uint64_t(c - it.chunk0) * cunit;
+      if (off < it.len) {  // else: a hole between batch-aligned items
+        const std::uint64_t rem = it.len - off;
+        mine.len = static_cast<std::uint32_t>(rem < cunit ? rem : cunit);
+        mine.src = reinterpret_cast<const std::uint8_t*>(it.src) + off;
+        mine.dst = it.dst ? reinterpret_cast<std::uint8_t*>(it.dst) + off : nullptr;
       }
-      const ItemDesc it = p.items[lo];
-      const std::uint64_t off = std::uint64_t(c - it.chunk0) * it.chunk_len;
-      const std::uint64_t rem = it.len - off;
-      mine.len = static_cast<std::uint32_t>(rem < it.chunk_len ? rem : it.chunk_len);
-      mine.src = reinterpret_cast<const std::uint8_t*>(it.src) + off;
-      mine.dst = it.dst ? reinterpret_cast<std::uint8_t*>(it.dst) + off : nullptr;
       if (p.src_digests) expect = __ldcg(&p.src_digests[c]);
     }
     refs[lane] = mine;
@@ -267,7 +149,6 @@ __global__ void __launch_bounds__(kThreads, 2) pull_kernel(const PullParams p) {
     bool good = false;
     for (int attempt = 0; attempt < 2 && !good; ++attempt) {
       std::uint64_t v1 = kP1 + kP2, v2 = kP2, v3 = 0, v4 = 0 - kP1;
-      std::uint64_t h = 0;
 #pragma unroll
       for (int s = 0; s < kStages - 1; ++s) {
         if (s < nsteps) load_step(refs, wbuf + s * kStageBytes, s, lane);
@@ -281,7 +162,6 @@ __global__ void __launch_bounds__(kThreads, 2) pull_kernel(const PullParams p) {
         __syncwarp();
         const std::uint8_t* st = wbuf + (s % kStages) * kStageBytes;
         store_step(refs, st, s, lane);
-        // Hash this lane's piece.
         const std::uint32_t g = static_cast<std::uint32_t>(s) * kPiece;
         if (g < mine.len) {
           const std::uint32_t n = min(static_cast<std::uint32_t>(kPiece), mine.len - g);
@@ -295,8 +175,8 @@ __global__ void __launch_bounds__(kThreads, 2) pull_kernel(const PullParams p) {
             v3 = xround(v3, (std::uint64_t(bq.y) << 32) | bq.x);
             v4 = xround(v4, (std::uint64_t(bq.w) << 32) | bq.z);
           }
-          if (g + n == mine.len) {  // last piece of this chunk: finalize
-            h = mine.len >= 32 ? merge4(v1, v2, v3, v4) : kP5;
+          if (g + n == mine.len) {
+            std::uint64_t h = mine.len >= 32 ? merge4(v1, v2, v3, v4) : kP5;
             h += mine.len;
             digest = finish_tail(h, slot + (n & ~31u), static_cast<int>(n & 31u));
           }
@@ -321,8 +201,6 @@ __global__ void __launch_bounds__(kThreads, 2) pull_kernel(const PullParams p) {
       break;
     }
     if (p.dst_digests && mine.len) p.dst_digests[c] = digest;
-    // Publish: every lane's stores are made visible system-wide before lane 0
-    // releases the watermark that downstream readers acquire.
     __threadfence_system();
     __syncwarp();
     if (lane == 0) {
@@ -332,8 +210,9 @@ __global__ void __launch_bounds__(kThreads, 2) pull_kernel(const PullParams p) {
     std::uint64_t landed = mine.len;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) landed += __shfl_xor_sync(full, landed, o);
-    if (lane == 0) atomicAdd(reinterpret_cast<unsigned long long*>(&p.status->bytes),
-                             static_cast<unsigned long long>(landed));
+    if (lane == 0)
+      atomicAdd(reinterpret_cast<unsigned long long*>(&p.status->bytes),
+                static_cast<unsigned long long>(landed));
   }
 }
 
@@ -403,15 +282,12 @@ __global__ void __launch_bounds__(kDigWarps * 32)
   if (lane == 0) {
     std::uint64_t h = len >= 32 ? merge4(a, b, c, d) : kP5;
     h += len;
-    // The tail (< 32 bytes) sits at the end of the last staged step.
     const std::uint64_t tail_at = full_stripes * 32;
     const int tail = static_cast<int>(len - tail_at);
-    const std::uint8_t* tp;
+    const std::uint8_t* tp = ring;
     if (tail > 0) {
       const std::uint64_t s = tail_at / kDigStep;
       tp = ring + (s % kDigRing) * kDigStep + (tail_at - s * kDigStep);
-    } else {
-      tp = ring;
     }
     out[span] = finish_tail(h, tp, tail);
   }
@@ -419,25 +295,23 @@ __global__ void __launch_bounds__(kDigWarps * 32)
 
 // ---------------------------------------------------------------- K3 -----
 __global__ void copy_spans_kernel(const std::uint64_t* srcs, const std::uint64_t* dsts,
-                                  const std::uint64_t* lens, int n) {
-  // blockIdx.y = span, blockIdx.x strides the span in 16-byte units.
-  const int span = blockIdx.y;
+                                  const std::uint64_t* lens, int n, int span0) {
+  const int span = span0 + static_cast<int>(blockIdx.y);
   if (span >= n) return;
   const std::uint8_t* src = reinterpret_cast<const std::uint8_t*>(srcs[span]);
   std::uint8_t* dst = reinterpret_cast<std::uint8_t*>(dsts[span]);
   const std::uint64_t len = lens[span];
-  const bool vec = ((reinterpret_cast<std::uintptr_t>(src) | reinterpret_cast<std::uintptr_t>(dst)) & 15) == 0;
+  const bool vec =
+      ((reinterpret_cast<std::uintptr_t>(src) | reinterpret_cast<std::uintptr_t>(dst)) & 15) == 0;
   const std::uint64_t stride = std::uint64_t(gridDim.x) * blockDim.x;
+  const std::uint64_t tid = std::uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (vec) {
     const std::uint64_t units = len / 16;
-    for (std::uint64_t i = std::uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < units; i += stride)
+    for (std::uint64_t i = tid; i < units; i += stride)
       reinterpret_cast<uint4*>(dst)[i] = reinterpret_cast<const uint4*>(src)[i];
-    for (std::uint64_t i = units * 16 + std::uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < len;
-         i += stride)
-      dst[i] = src[i];
+    for (std::uint64_t i = units * 16 + tid; i < len; i += stride) dst[i] = src[i];
   } else {
-    for (std::uint64_t i = std::uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < len; i += stride)
-      dst[i] = src[i];
+    for (std::uint64_t i = tid; i < len; i += stride) dst[i] = src[i];
   }
 }
 
@@ -459,7 +333,8 @@ __device__ __forceinline__ std::uint16_t synth_one(std::uint64_t seed, std::uint
 __global__ void synth_bf16_kernel(std::uint16_t* dst, std::uint64_t n, std::uint64_t seed,
                                   std::uint64_t first) {
   const std::uint64_t stride = std::uint64_t(gridDim.x) * blockDim.x * 8;
-  for (std::uint64_t i = (std::uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) * 8; i < n; i += stride) {
+  for (std::uint64_t i = (std::uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) * 8; i < n;
+       i += stride) {
     if (i + 8 <= n && (reinterpret_cast<std::uintptr_t>(dst + i) & 15) == 0) {
       std::uint32_t w[4];
 #pragma unroll
@@ -477,7 +352,7 @@ __global__ void synth_bf16_kernel(std::uint16_t* dst, std::uint64_t n, std::uint
 __device__ __forceinline__ std::uint8_t bf16_to_e4m3(std::uint16_t x) {
   const float f = __uint_as_float(std::uint32_t(x) << 16);
   std::uint16_t r;
-  // cvt.rn.satfinite.e4m3x2.f32 d, a, b  packs (a -> hi byte, b -> lo byte).
+  // cvt.rn.satfinite.e4m3x2.f32 d, a, b packs a -> high byte, b -> low byte.
   asm("cvt.rn.satfinite.e4m3x2.f32 %0, %1, %2;\n" : "=h"(r) : "f"(0.0f), "f"(f));
   return static_cast<std::uint8_t>(r & 0xFF);
 }
@@ -488,6 +363,14 @@ __global__ void e4m3_kernel(const std::uint16_t* src, std::uint8_t* dst, std::ui
     dst[i] = bf16_to_e4m3(src[i]);
 }
 
+bool use_ldg_kernel() {
+  static const bool v = [] {
+    const char* e = std::getenv("RSB_PULL_KERNEL");
+    return e && std::strcmp(e, "ldg") == 0;
+  }();
+  return v;
+}
+
 }  // namespace
 
 // ------------------------------------------------------------ launchers --
@@ -495,10 +378,14 @@ __global__ void e4m3_kernel(const std::uint16_t* src, std::uint8_t* dst, std::ui
 int pull_grid(int device) {
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
-  return 2 * sms;
+  return sms;
 }
 
-cudaError_t launch_pull(const PullParams& p, int grid, cudaStream_t s) {
+const char* pull_kernel_name() { return use_ldg_kernel() ? "pull_kernel" : "pull_tma_kernel"; }
+
+cudaError_t launch_pull(const PullParams& p, int sms, cudaStream_t s) {
+  if (p.n_batches <= p.first_batch) return cudaSuccess;
+  if (!use_ldg_kernel()) return launch_pull_tma(p, sms, s);
   static bool attr_done[64] = {};
   int dev = 0;
   cudaGetDevice(&dev);
@@ -508,9 +395,9 @@ cudaError_t launch_pull(const PullParams& p, int grid, cudaStream_t s) {
     if (e != cudaSuccess) return e;
     attr_done[dev] = true;
   }
-  if (p.n_batches <= p.first_batch) return cudaSuccess;
   const std::uint32_t todo = p.n_batches - p.first_batch;
   const std::uint32_t need = (todo + kWarps - 1) / kWarps;
+  int grid = 2 * sms;
   if (static_cast<std::uint32_t>(grid) > need) grid = static_cast<int>(need);
   pull_kernel<<<grid, kThreads, kSmemBytes, s>>>(p);
   return cudaGetLastError();
@@ -524,22 +411,26 @@ cudaError_t launch_span_digests(const std::uint64_t* ptrs, const std::uint64_t* 
   int dev = 0;
   cudaGetDevice(&dev);
   if (dev < 64 && !attr_done[dev]) {
-    cudaError_t e = cudaFuncSetAttribute(span_digest_kernel,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaError_t e =
+        cudaFuncSetAttribute(span_digest_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
     attr_done[dev] = true;
   }
-  span_digest_kernel<<<(n + kDigWarps - 1) / kDigWarps, kDigWarps * 32, smem, s>>>(ptrs, lens, out,
-                                                                                   n);
+  span_digest_kernel<<<(n + kDigWarps - 1) / kDigWarps, kDigWarps * 32, smem, s>>>(ptrs, lens,
+                                                                                   out, n);
   return cudaGetLastError();
 }
 
 cudaError_t launch_copy_spans(const std::uint64_t* srcs, const std::uint64_t* dsts,
                               const std::uint64_t* lens, int n, cudaStream_t s) {
-  if (n <= 0) return cudaSuccess;
-  dim3 grid(64, static_cast<unsigned>(n));
-  copy_spans_kernel<<<grid, 256, 0, s>>>(srcs, dsts, lens, n);
-  return cudaGetLastError();
+  for (int span0 = 0; span0 < n; span0 += 65535) {
+    const int cnt = n - span0 < 65535 ? n - span0 : 65535;
+    dim3 grid(64, static_cast<unsigned>(cnt));
+    copy_spans_kernel<<<grid, 256, 0, s>>>(srcs, dsts, lens, n, span0);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
 }
 
 cudaError_t launch_synth_bf16(std::uint16_t* dst, std::uint64_t n, std::uint64_t seed,

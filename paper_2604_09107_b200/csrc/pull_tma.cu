@@ -1,0 +1,448 @@
+// K1+K2 on the TMA path: the fused pull + per-chunk XXH64 verify + watermark
+// kernel (replaces copy_slice_locked, transport.cpp:51-69, and the per-item
+// digest64 check of TransferTask::verify_ready, client_core.cpp:306-334).
+//
+// Warp-specialized, persistent: each CTA is one producer warp and one
+// consumer warp sharing a ring of S stages in shared memory.  A stage holds
+// the next P bytes of each of the 32 chunks of one watermark batch; lane l
+// of the consumer hashes chunk 32b+l.
+//
+// Two stage layouts:
+//  * box (the common case: all 32 chunks of the batch are full-length rows
+//    of one item that has TMA tensor maps).  The item is viewed as a 2-D
+//    tensor [len/chunk_len rows][chunk_len bytes]; a stage is P/128 boxes of
+//    [32 rows x 128 B] with 128-byte swizzle, each moved by ONE
+//    cp.async.bulk.tensor load (and landed by ONE tensor store) issued by a
+//    single lane.  The swizzle keeps the per-row 128-bit reads of the hash
+//    lanes bank-conflict free.
+//  * slot (batches with a short last chunk, item holes, unaligned regions):
+//    one padded slot of P+16 bytes per chunk, every lane issuing its own
+//    cp.async.bulk copy (plain loads/stores for unaligned bytes and tails).
+//
+//   producer  walks its batches (static schedule b = blockIdx.x + k*grid, so
+//             the landed prefix advances front to back), waits the upstream
+//             watermark when the source is still filling, fills stages.
+//   consumer  per stage: lands the stage (tensor store / bulk stores), hashes
+//             (XXH64 32-byte stripes), frees the stage once the stores have
+//             read it.  After a batch's last step it verifies the 32 chunk
+//             digests against the source's table (one quiet re-pull of a bad
+//             chunk), writes its own digest table, and one stage later --
+//             when the batch's stores have completed -- publishes the batch
+//             watermark (fence.proxy.async + st.release.sys, cumulative over
+//             the warp through __syncwarp).
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdlib>
+
+#include "dev_common.cuh"
+#include "device.hpp"
+
+namespace rsb::dev {
+
+using namespace detail;
+
+namespace {
+
+constexpr std::uint32_t kPill = 0xffffffffu;
+
+__device__ __forceinline__ void tensor_load_2d(void* smem, const void* map, int x, int y,
+                                               unsigned long long* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes "
+      "[%0], [%1, {%2, %3}], [%4];\n" ::"r"(smem_u32(smem)),
+      "l"(map), "r"(x), "r"(y), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tensor_store_2d(const void* map, int x, int y, const void* smem) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.global.shared::cta.tile.bulk_group [%0, {%1, %2}], [%3];\n" ::"l"(map),
+      "r"(x), "r"(y), "r"(smem_u32(smem))
+      : "memory");
+}
+
+template <int P, int S, int CTAS, int ITEMS>
+struct Cfg {
+  static constexpr int kP = P;
+  static constexpr int kSlot = P + 16;
+  static constexpr int kStage = (32 * kSlot + 1023) / 1024 * 1024;  // box layout needs 1 KiB
+  static constexpr int kStages = S;
+  static constexpr int kCtas = CTAS;
+  static constexpr int kItems = ITEMS;
+  static_assert(P % kMapBoxCols == 0, "piece must be whole boxes");
+
+  struct Meta {
+    std::uint32_t batch;
+    std::uint32_t step;
+    std::uint32_t last;
+    std::uint32_t box;   // 1: box layout
+    std::uint32_t item;  // box layout: item index
+    std::uint32_t y0;    // box layout: first row (chunk) of the batch in the item
+    std::uint32_t g;     // box layout: byte offset of the step within the chunk
+    std::uint32_t bpiece;
+    std::uint64_t dst[32];
+    std::uint32_t piece[32];
+    std::uint32_t clen[32];
+    std::uint64_t expect[32];
+  };
+  struct Smem {
+    std::uint8_t stage[S][kStage];
+    Meta meta[S];
+    ItemDesc items[ITEMS];
+    unsigned long long full[S];
+    unsigned long long empty[S];
+  };
+  static constexpr int kSmemBytes = static_cast<int>(sizeof(Smem)) + 1024;
+};
+
+template <class C>
+__global__ void __launch_bounds__(64, C::kCtas) pull_tma_kernel(const PullParams p) {
+  using Smem = typename C::Smem;
+  using Meta = typename C::Meta;
+  constexpr int kP = C::kP;
+  constexpr int kStages = C::kStages;
+  extern __shared__ __align__(1024) std::uint8_t smraw[];
+  // 1 KiB-align the stages (128B-swizzled boxes)
+  const std::uint32_t mis = smem_u32(smraw) & 1023u;
+  Smem& sm = *reinterpret_cast<Smem*>(smraw + (mis ? 1024 - mis : 0));
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const unsigned full = 0xffffffffu;
+  const std::uint8_t* maps = static_cast<const std::uint8_t*>(p.maps);
+  auto advance = [](int& stage, unsigned& phase) {
+    if (++stage == kStages) {
+      stage = 0;
+      phase ^= 1;
+    }
+  };
+
+  const bool smem_items = p.n_items <= static_cast<std::uint32_t>(C::kItems);
+  if (smem_items) {
+    const uint4* s = reinterpret_cast<const uint4*>(p.items);
+    uint4* d = reinterpret_cast<uint4*>(sm.items);
+    for (std::uint32_t i = threadIdx.x; i < p.n_items * 2; i += blockDim.x) d[i] = s[i];
+  }
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&sm.full[s], 1);
+      mbar_init(&sm.empty[s], 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  const ItemDesc* items = smem_items ? sm.items : p.items;
+
+  if (warp == 0) {
+    // ================================ producer ==============================
+    int stage = 0;
+    unsigned phase = 0;
+    std::uint32_t abort_seen = 0;
+    for (std::uint32_t b = p.first_batch + blockIdx.x; b < p.n_batches; b += gridDim.x) {
+      if (abort_seen) break;
+      const std::uint32_t abort_next = ld_volatile(&p.work[1]);  // acted on next batch
+      if (p.resume && ld_volatile(&p.dst_flags[b]) == p.dst_epoch) {  // landed already
+        abort_seen = abort_next;
+        continue;
+      }
+      if (p.src_flags) {
+        std::uint32_t code = 0;
+        if (lane == 0) code = wait_flag(&p.src_flags[b], p.src_epoch, p.timeout_ns, &p.work[1]);
+        code = __shfl_sync(full, code, 0);
+        if (code != kPullOk) {
+          if (lane == 0) {
+            if (code != kPullAborted) {
+              atomicCAS(&p.status->code, 0u, code);
+              atomicExch(&p.status->bad_chunk, b * kBatchChunks);
+            }
+            atomicExch(&p.work[1], 1u);
+            if (p.dst_flags) st_release_sys(&p.dst_flags[b], p.dst_epoch | kAbort);
+          }
+          break;
+        }
+        fence_proxy_async_global();  // upstream bytes are read by the async proxy
+      }
+      const std::uint32_t c = b * kBatchChunks + lane;
+      const std::uint8_t* src = nullptr;
+      std::uint8_t* dst = nullptr;
+      std::uint32_t clen = 0, cunit = 0, item = 0xffffffffu, itflags = 0, row = 0;
+      std::uint64_t expect = 0;
+      if (c < p.n_chunks) {
+        if (p.src_digests) expect = __ldcg(&p.src_digests[c]);  // consumed at the last step
+        item = find_item(items, p.n_items, c);
+        const ItemDesc d = items[item];
+        cunit = d.chunk_len & kChunkLenMask;
+        itflags = d.chunk_len & kHasMap;
+        row = c - d.chunk0;
+        const std::uint64_t off = std::uint64_t(row) * cunit;
+        if (off < d.len) {
+          const std::uint64_t rem = d.len - off;
+          clen = static_cast<std::uint32_t>(rem < cunit ? rem : cunit);
+          src = reinterpret_cast<const std::uint8_t*>(d.src) + off;
+          dst = d.dst ? reinterpret_cast<std::uint8_t*>(d.dst) + off : nullptr;
+        }  // else: a hole between batch-aligned items
+      }
+      const std::uint32_t item0 = __shfl_sync(full, item, 0);
+      const std::uint32_t y0 = __shfl_sync(full, row, 0);
+      const bool box = maps != nullptr &&
+                       __all_sync(full, item == item0 && itflags != 0 && clen == cunit && clen != 0);
+      std::uint32_t maxlen = clen;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) maxlen = max(maxlen, __shfl_xor_sync(full, maxlen, o));
+      const std::uint32_t nsteps = (maxlen + kP - 1) / kP;
+      const bool src_vec = (reinterpret_cast<std::uintptr_t>(src) & 15) == 0;
+      for (std::uint32_t s = 0; s < nsteps; ++s) {
+        mbar_wait(&sm.empty[stage], phase ^ 1);
+        Meta& m = sm.meta[stage];
+        const std::uint32_t g = s * kP;
+        const std::uint32_t piece = g < clen ? min(static_cast<std::uint32_t>(kP), clen - g) : 0;
+        const bool last = s + 1 == nsteps;
+        m.piece[lane] = piece;
+        m.clen[lane] = clen;
+        if (last) m.expect[lane] = expect;
+        if (box) {
+          if (lane == 0) {
+            m.batch = b;
+            m.step = s;
+            m.last = last;
+            m.box = 1;
+            m.item = item0;
+            m.y0 = y0;
+            m.g = g;
+            m.bpiece = piece;
+          }
+          __syncwarp();
+          if (lane == 0) {
+            mbar_arrive_tx(&sm.full[stage], 32 * piece);
+            const void* map = maps + 256 * std::size_t(item0);
+            for (std::uint32_t j = 0; j < piece / kMapBoxCols; ++j)
+              tensor_load_2d(sm.stage[stage] + j * 4096, map, static_cast<int>(g + j * kMapBoxCols),
+                             static_cast<int>(y0), &sm.full[stage]);
+          }
+        } else {
+          std::uint8_t* slot = sm.stage[stage] + lane * C::kSlot;
+          const std::uint32_t bulk = src_vec ? (piece & ~15u) : 0;
+          for (std::uint32_t k = bulk; k < piece; ++k) slot[k] = __ldcg(src + g + k);
+          m.dst[lane] = dst ? reinterpret_cast<std::uint64_t>(dst + g) : 0;
+          std::uint32_t tx = bulk;
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) tx += __shfl_xor_sync(full, tx, o);
+          if (lane == 0) {
+            m.batch = b;
+            m.step = s;
+            m.last = last;
+            m.box = 0;
+          }
+          __syncwarp();
+          if (lane == 0) mbar_arrive_tx(&sm.full[stage], tx);
+          __syncwarp();
+          if (bulk) bulk_g2s(slot, src + g, bulk, &sm.full[stage]);
+        }
+        advance(stage, phase);
+      }
+      abort_seen = abort_next;
+    }
+    mbar_wait(&sm.empty[stage], phase ^ 1);  // poison pill: nothing more
+    if (lane == 0) {
+      sm.meta[stage].batch = kPill;
+      mbar_arrive(&sm.full[stage]);
+    }
+  } else {
+    // ================================ consumer ==============================
+    int stage = 0;
+    unsigned phase = 0;
+    std::uint64_t v1 = 0, v2 = 0, v3 = 0, v4 = 0, digest = 0;
+    std::uint32_t pend_b = kPill;  // batch whose watermark awaits its stores
+    std::uint64_t pend_bytes = 0;
+    bool failed = false;
+    const std::uint32_t swz = (static_cast<std::uint32_t>(lane) & 7u) << 4;
+    auto release_pending = [&](bool newer_group) {
+      if (pend_b == kPill) return;
+      if (newer_group) bulk_wait<1>();
+      else bulk_wait<0>();
+      fence_proxy_async_global();
+      __syncwarp();
+      if (lane == 0) {
+        if (p.dst_flags) st_release_sys(&p.dst_flags[pend_b], p.dst_epoch);
+        atomicAdd(&p.status->batches_done, 1u);
+        atomicAdd(reinterpret_cast<unsigned long long*>(&p.status->bytes),
+                  static_cast<unsigned long long>(pend_bytes));
+      }
+      pend_b = kPill;
+    };
+    for (;;) {
+      mbar_wait(&sm.full[stage], phase);
+      const Meta& m = sm.meta[stage];
+      const std::uint32_t b = m.batch;
+      if (b == kPill) break;
+      if (failed) {  // drain until the pill
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sm.empty[stage]);
+        advance(stage, phase);
+        continue;
+      }
+      const std::uint32_t s = m.step;
+      const std::uint32_t piece = m.piece[lane];
+      const std::uint32_t clen = m.clen[lane];
+      const bool last = m.last != 0;
+      const bool box = m.box != 0;
+      std::uint8_t* st = sm.stage[stage];
+      bool committed = false;
+      if (s == 0) {
+        v1 = kP1 + kP2;
+        v2 = kP2;
+        v3 = 0;
+        v4 = 0 - kP1;
+      }
+      const int stripes = static_cast<int>(piece >> 5);
+      if (box) {
+        // 1) land: one tensor store per box, issued by lane 0
+        if (lane == 0) {
+          const std::uint8_t* dmap = maps + 256 * std::size_t(m.item) + 128;
+          const bool has_dst = items[m.item].dst != 0;
+          if (has_dst) {
+            fence_proxy_async_smem();
+            for (std::uint32_t j = 0; j < m.bpiece / kMapBoxCols; ++j)
+              tensor_store_2d(dmap, static_cast<int>(m.g + j * kMapBoxCols), static_cast<int>(m.y0),
+                              st + j * 4096);
+            bulk_commit();
+            committed = true;
+          }
+        }
+        // 2) hash row `lane` of the swizzled boxes
+        const std::uint8_t* rowbase = st + lane * 128;
+#pragma unroll 4
+        for (int k = 0; k < stripes; ++k) {
+          const std::uint8_t* boxp = rowbase + (k >> 2) * 4096;
+          const std::uint32_t x = static_cast<std::uint32_t>(k & 3) * 32;
+          const uint4 a = *reinterpret_cast<const uint4*>(boxp + (x ^ swz));
+          const uint4 q = *reinterpret_cast<const uint4*>(boxp + ((x + 16) ^ swz));
+          v1 = xround(v1, (std::uint64_t(a.y) << 32) | a.x);
+          v2 = xround(v2, (std::uint64_t(a.w) << 32) | a.z);
+          v3 = xround(v3, (std::uint64_t(q.y) << 32) | q.x);
+          v4 = xround(v4, (std::uint64_t(q.w) << 32) | q.z);
+        }
+        if (clen && s * kP + piece == clen) {
+          std::uint64_t h = clen >= 32 ? merge4(v1, v2, v3, v4) : kP5;
+          h += clen;
+          // box rows are whole 128-byte multiples: no tail
+          digest = finish_tail(h, nullptr, 0);
+        }
+      } else {
+        std::uint8_t* slot = st + lane * C::kSlot;
+        const std::uint64_t dstp = m.dst[lane];
+        if (dstp && piece) {
+          const std::uint32_t bulk = (dstp & 15) == 0 ? (piece & ~15u) : 0;
+          if (bulk) {
+            fence_proxy_async_smem();
+            bulk_s2g(reinterpret_cast<void*>(dstp), slot, bulk);
+            bulk_commit();
+            committed = true;
+          }
+          for (std::uint32_t k = bulk; k < piece; ++k)
+            reinterpret_cast<std::uint8_t*>(dstp)[k] = slot[k];
+        }
+#pragma unroll 4
+        for (int k = 0; k < stripes; ++k) {
+          const uint4 a = *reinterpret_cast<const uint4*>(slot + 32 * k);
+          const uint4 q = *reinterpret_cast<const uint4*>(slot + 32 * k + 16);
+          v1 = xround(v1, (std::uint64_t(a.y) << 32) | a.x);
+          v2 = xround(v2, (std::uint64_t(a.w) << 32) | a.z);
+          v3 = xround(v3, (std::uint64_t(q.y) << 32) | q.x);
+          v4 = xround(v4, (std::uint64_t(q.w) << 32) | q.z);
+        }
+        if (clen && s * kP + piece == clen) {
+          std::uint64_t h = clen >= 32 ? merge4(v1, v2, v3, v4) : kP5;
+          h += clen;
+          digest = finish_tail(h, slot + (piece & ~31u), static_cast<int>(piece & 31u));
+        }
+      }
+      const std::uint64_t expect = last ? m.expect[lane] : 0;
+      // 3) the previous batch's stores are done by now: publish its watermark
+      release_pending(committed);
+      // 4) free the stage once the stores issued from it have read it
+      if (committed) bulk_wait_read<0>();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sm.empty[stage]);
+      advance(stage, phase);
+      if (!last) continue;
+      // 5) batch complete: verify and record
+      const std::uint32_t c = b * kBatchChunks + lane;
+      bool lane_ok = clen == 0 || p.src_digests == nullptr || digest == expect;
+      if (__ballot_sync(full, !lane_ok)) {
+        if (lane == 0) atomicAdd(&p.status->retried_batches, 1u);
+        bulk_wait<0>();  // earlier stores of these chunks must not land after the re-pull
+        if (!lane_ok) {
+          const ItemDesc d = items[find_item(items, p.n_items, c)];
+          const std::uint64_t off = std::uint64_t(c - d.chunk0) * (d.chunk_len & kChunkLenMask);
+          digest = repull_chunk(reinterpret_cast<const std::uint8_t*>(d.src) + off,
+                                d.dst ? reinterpret_cast<std::uint8_t*>(d.dst) + off : nullptr,
+                                clen);
+          lane_ok = digest == expect;
+        }
+        const unsigned bad = __ballot_sync(full, !lane_ok);
+        if (bad) {
+          if (lane == 0) {
+            atomicCAS(&p.status->code, 0u, static_cast<std::uint32_t>(kPullChecksum));
+            atomicExch(&p.status->bad_chunk, b * kBatchChunks + (__ffs(bad) - 1));
+            atomicExch(&p.work[1], 1u);
+            if (p.dst_flags) st_release_sys(&p.dst_flags[b], p.dst_epoch | kAbort);
+          }
+          failed = true;
+          continue;
+        }
+      }
+      if (p.dst_digests && clen) p.dst_digests[c] = digest;
+      std::uint64_t landed = clen;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) landed += __shfl_xor_sync(full, landed, o);
+      pend_b = b;
+      pend_bytes = landed;
+    }
+    release_pending(false);
+    bulk_wait<0>();
+  }
+}
+
+template <class C>
+cudaError_t launch_variant(const PullParams& p, int sms, cudaStream_t s) {
+  static bool attr_done[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 64 && !attr_done[dev]) {
+    cudaError_t e = cudaFuncSetAttribute(pull_tma_kernel<C>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
+    if (e != cudaSuccess) return e;
+    attr_done[dev] = true;
+  }
+  const std::uint32_t todo = p.n_batches - p.first_batch;
+  int grid = sms * C::kCtas;
+  if (static_cast<std::uint32_t>(grid) > todo) grid = static_cast<int>(todo);
+  pull_tma_kernel<C><<<grid, 64, C::kSmemBytes, s>>>(p);
+  return cudaGetLastError();
+}
+
+using V0 = Cfg<512, 3, 3, 512>;
+using V1 = Cfg<512, 4, 2, 576>;
+using V2 = Cfg<1024, 3, 2, 256>;
+using V3 = Cfg<256, 6, 3, 256>;
+
+int variant() {
+  static const int v = [] {
+    const char* e = std::getenv("RSB_TMA_VARIANT");
+    return e ? std::atoi(e) : 0;
+  }();
+  return v;
+}
+
+}  // namespace
+
+cudaError_t launch_pull_tma(const PullParams& p, int sms, cudaStream_t s) {
+  switch (variant()) {
+    case 1: return launch_variant<V1>(p, sms, s);
+    case 2: return launch_variant<V2>(p, sms, s);
+    case 3: return launch_variant<V3>(p, sms, s);
+    default: return launch_variant<V0>(p, sms, s);
+  }
+}
+
+}  // namespace rsb::dev

@@ -1,0 +1,108 @@
+// Host side of a pull launch: item table + TMA tensor maps + work/status
+// words, uploaded in one H2D copy.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstring>
+#include <vector>
+
+#include "device.hpp"
+
+namespace rsb::dev {
+
+namespace {
+
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                   const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) !=
+            cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return static_cast<EncodeTiledFn>(nullptr);
+    return reinterpret_cast<EncodeTiledFn>(p);
+  }();
+  return fn;
+}
+
+// [rows][chunk_len] byte tensor at `base`, box 128 B x 32 rows, 128B swizzle.
+bool encode(CUtensorMap* m, std::uint64_t base, std::uint64_t chunk_len, std::uint64_t rows) {
+  auto fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[2] = {chunk_len, rows};
+  cuuint64_t strides[1] = {chunk_len};
+  cuuint32_t box[2] = {static_cast<cuuint32_t>(kMapBoxCols), 32};
+  cuuint32_t estr[2] = {1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, reinterpret_cast<void*>(base), dims, strides, box,
+            estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+constexpr std::size_t kHdr = 128;  // work words (64 B) + PullStatus (32 B), padded
+
+}  // namespace
+
+cudaError_t upload_pull_plan(int device, cudaStream_t s, ItemDesc* items, std::uint32_t n,
+                             PlanUpload* up, PullParams* p) {
+  const std::size_t items_off = kHdr;
+  const std::size_t maps_off = (items_off + n * sizeof(ItemDesc) + 255) / 256 * 256;
+  const std::size_t total = maps_off + std::size_t(n) * 256;
+  if (up->scratch_bytes < total) {
+    if (up->scratch) cudaFree(up->scratch);
+    up->scratch = nullptr;
+    up->scratch_bytes = 0;
+    cudaError_t e = cudaMalloc(&up->scratch, total);
+    if (e != cudaSuccess) return e;
+    up->scratch_bytes = total;
+  }
+  std::vector<std::uint8_t> host(total, 0);
+  bool any_map = false;
+  for (std::uint32_t i = 0; i < n; ++i) {
+    ItemDesc& d = items[i];
+    const std::uint64_t cl = d.chunk_len & kChunkLenMask;
+    d.chunk_len = static_cast<std::uint32_t>(cl);
+    const std::uint64_t rows = cl ? d.len / cl : 0;
+    const bool aligned = (d.src % 16 == 0) && (d.dst % 16 == 0) && cl % kMapBoxCols == 0 &&
+                         cl % 16 == 0;
+    if (aligned && rows >= 32 && d.src) {
+      auto* m = reinterpret_cast<CUtensorMap*>(host.data() + maps_off + 256 * std::size_t(i));
+      bool ok = encode(m, d.src, cl, rows);
+      if (ok && d.dst) ok = encode(m + 1, d.dst, cl, rows);
+      if (ok) {
+        d.chunk_len |= kHasMap;
+        any_map = true;
+      }
+    }
+  }
+  std::memcpy(host.data() + items_off, items, n * sizeof(ItemDesc));
+  auto* base = static_cast<std::uint8_t*>(up->scratch);
+  // Only the header, the item table and (if any) the maps travel.
+  const std::size_t bytes = any_map ? total : items_off + n * sizeof(ItemDesc);
+  cudaError_t e = cudaMemcpyAsync(base, host.data(), bytes, cudaMemcpyHostToDevice, s);
+  if (e != cudaSuccess) return e;
+  up->h2d_bytes = bytes;
+  p->work = reinterpret_cast<std::uint32_t*>(base);
+  p->status = reinterpret_cast<PullStatus*>(base + 64);
+  p->items = reinterpret_cast<const ItemDesc*>(base + items_off);
+  p->n_items = n;
+  p->maps = any_map ? base + maps_off : nullptr;
+  return cudaSuccess;
+}
+
+void free_pull_plan(int device, PlanUpload* up) {
+  if (!up->scratch) return;
+  int prev = 0;
+  cudaGetDevice(&prev);
+  cudaSetDevice(device);
+  cudaFree(up->scratch);
+  cudaSetDevice(prev);
+  up->scratch = nullptr;
+  up->scratch_bytes = 0;
+}
+
+}  // namespace rsb::dev

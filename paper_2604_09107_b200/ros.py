@@ -319,14 +319,32 @@ def pull_spans(srcs, dsts, lens, chunk_bytes=4096, expect=None, out_digests=None
     """Standalone fused copy+verify over explicit device spans.  Returns
     (kernel_code, kernel_ms)."""
     import numpy as np
+    import torch
     s = np.asarray(srcs, np.uint64)
     d = np.asarray(dsts, np.uint64) if dsts is not None else None
     n = np.asarray(lens, np.uint64)
+    # dense (caller) <-> batch-aligned (kernel) chunk-table index maps
+    idx, base = [], 0
+    for ln in lens:
+        cnt = (int(ln) + chunk_bytes - 1) // chunk_bytes
+        idx.extend(range(base, base + cnt))
+        base += (cnt + 31) // 32 * 32
+    dev = torch.device("cuda", device)
+    pos = torch.tensor(idx, dtype=torch.int64, device=dev)
+    exp_al = out_al = None
+    if expect is not None:
+        exp_al = torch.zeros(max(base, 1), dtype=torch.int64, device=dev)
+        exp_al[pos] = expect
+    if out_digests is not None:
+        out_al = torch.zeros(max(base, 1), dtype=torch.int64, device=dev)
+    torch.cuda.synchronize(dev)
     code, ms = C.c_int(), C.c_float()
     raw = 0 if stream is None else stream.cuda_stream
     check(lib.rs_pull_spans(s.ctypes.data, None if d is None else d.ctypes.data, n.ctypes.data,
                             len(s), chunk_bytes,
-                            None if expect is None else C.c_void_p(expect.data_ptr()),
-                            None if out_digests is None else C.c_void_p(out_digests.data_ptr()),
+                            None if exp_al is None else C.c_void_p(exp_al.data_ptr()),
+                            None if out_al is None else C.c_void_p(out_al.data_ptr()),
                             device, C.c_void_p(raw), C.byref(code), C.byref(ms)), "rs_pull_spans")
+    if out_al is not None:
+        out_digests.copy_(out_al[pos])
     return code.value, ms.value

@@ -126,3 +126,17 @@ def test_e4m3_all_bf16_patterns(dev, oracle):
     # NaN inputs: any e4m3 NaN encoding (0x7F / 0xFF) is accepted
     assert np.all((got[nan] & 0x7F) == 0x7F)
     assert np.array_equal(got[~nan], want[~nan])
+
+
+def test_ldg_kernel_variant_still_bit_exact(dev):
+    """The LDGSTS (non-TMA) pull kernel, selected with RSB_PULL_KERNEL=ldg,
+    passes the same copy/digest parity tests."""
+    import os
+    import subprocess
+    import sys
+    from tests.conftest import ROOT
+    env = dict(os.environ, RSB_PULL_KERNEL="ldg")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-m", "gpu", "-x",
+                        "tests/test_gpu_kernels.py", "-k", "pull_spans"],
+                       cwd=ROOT, env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
