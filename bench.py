@@ -331,6 +331,7 @@ def main():
     ap.add_argument("--workload", default="llama3_8b")
     ap.add_argument("--chunk", type=int, default=4096)
     ap.add_argument("--no-verify", action="store_true")
+    ap.add_argument("--fanout", default="chain", choices=["chain", "pairs"])
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-bytes", type=int, default=2 << 30)
     ap.add_argument("--cpu-reps", type=int, default=3)

@@ -36,10 +36,14 @@ def run(args):
     dc = DistCluster()
     shapes = B.workload_shapes(args.workload)
     total = sum(2 * B._numel(s) for _, s in shapes)
-    is_trainer = rank == 0
+    # chain (default): rank 0 trains, ranks 1.. read (planner: a chain).
+    # pairs: even ranks train, odd ranks read (diagnostic: no GPU both
+    # sends and receives).
+    pairs = getattr(args, "fanout", "chain") == "pairs"
+    is_trainer = rank % 2 == 0 if pairs else rank == 0
     arena, views = B.alloc_replica(shapes, dev, seed_base=42 if is_trainer else None)
     torch.cuda.synchronize()
-    name = "trainer" if is_trainer else f"rollout{rank}"
+    name = (f"trainer{rank}" if pairs else "trainer") if is_trainer else f"rollout{rank}"
     h = dc.open("m", name, 1, endpoints=[f"rank{rank}:cuda{local}"], chunk_bytes=args.chunk,
                 pull_timeout_s=30.0)
     for n, v in views:
@@ -47,7 +51,11 @@ def run(args):
     stream = torch.cuda.Stream(device=dev)
     h.set_stream(0, stream)
     t0 = time.perf_counter()
-    r = dc.publish(h if is_trainer else None, 1)
+    r = None
+    for tr in ([x for x in range(world) if x % 2 == 0] if pairs else [0]):
+        rr = dc.publish(h if rank == tr else None, 1)
+        if rank == tr:
+            r = rr
     publish_s = time.perf_counter() - t0
     if is_trainer:
         assert r.status == Status.ok, r
@@ -100,12 +108,13 @@ def run(args):
     total_landed = sum(a[0][2] for a in allv)
     dev_s = sum(step_dev_ms) / 1e3
     wall_s = max(a[0][4] for a in allv)
-    receivers = world - 1
+    receivers = world // 2 if pairs else world - 1
     assert total_landed == args.steps * receivers * total, (total_landed, total)
     hashes = dc.gather(None if args.no_verify else table_hash())
     verified = verified and (args.no_verify or all(x == hashes[0] for x in hashes))
     if rank == 0:
-        per_rx = [round(total / (statistics.mean(a[1]) / 1e3) / 1e9, 2) for a in allv[1:]]
+        per_rx = [round(total / (statistics.mean(a[1]) / 1e3) / 1e9, 2) for a in allv
+                  if a[1] and statistics.mean(a[1]) > 0]
         value = total_landed / dev_s / 1e9
         mean_rx = statistics.mean(per_rx)
         line = {

@@ -67,6 +67,23 @@ bool parse_spec(const char* spec, rsb::VersionSpec* out) {
   return true;
 }
 
+// Runs `fn` with the device that owns `ptr` current (kernels must launch on
+// the device whose memory they touch).
+template <class F>
+int on_ptr_device(const void* ptr, F fn) {
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, ptr) != cudaSuccess || a.type != cudaMemoryTypeDevice) {
+    cudaGetLastError();
+    return st(rsb::Status::invalid_argument);
+  }
+  int prev = 0;
+  cudaGetDevice(&prev);
+  if (prev != a.device) cudaSetDevice(a.device);
+  cudaError_t e = fn();
+  if (prev != a.device) cudaSetDevice(prev);
+  return e == cudaSuccess ? 0 : st(rsb::Status::transfer_failed);
+}
+
 }  // namespace
 
 extern "C" {
@@ -448,18 +465,22 @@ int rs_digest_spans(const uint64_t* dev_ptrs, const uint64_t* lens, int n, uint6
 
 int rs_synth_bf16(void* dev_dst, uint64_t n_elems, uint64_t seed, uint64_t first_elem,
                   void* cuda_stream) {
-  if (!dev_dst && n_elems) return st(rsb::Status::invalid_argument);
-  auto e = rsb::dev::launch_synth_bf16(static_cast<std::uint16_t*>(dev_dst), n_elems, seed,
+  if (!n_elems) return 0;
+  if (!dev_dst) return st(rsb::Status::invalid_argument);
+  return on_ptr_device(dev_dst, [&] {
+    return rsb::dev::launch_synth_bf16(static_cast<std::uint16_t*>(dev_dst), n_elems, seed,
                                        first_elem, static_cast<cudaStream_t>(cuda_stream));
-  return e == cudaSuccess ? 0 : st(rsb::Status::transfer_failed);
+  });
 }
 
 int rs_bf16_to_e4m3(const void* dev_src, void* dev_dst, uint64_t n_elems, void* cuda_stream) {
-  if ((!dev_src || !dev_dst) && n_elems) return st(rsb::Status::invalid_argument);
-  auto e = rsb::dev::launch_bf16_to_e4m3(static_cast<const std::uint16_t*>(dev_src),
+  if (!n_elems) return 0;
+  if (!dev_src || !dev_dst) return st(rsb::Status::invalid_argument);
+  return on_ptr_device(dev_dst, [&] {
+    return rsb::dev::launch_bf16_to_e4m3(static_cast<const std::uint16_t*>(dev_src),
                                          static_cast<std::uint8_t*>(dev_dst), n_elems,
                                          static_cast<cudaStream_t>(cuda_stream));
-  return e == cudaSuccess ? 0 : st(rsb::Status::transfer_failed);
+  });
 }
 
 int rs_pull_spans(const uint64_t* src_ptrs, const uint64_t* dst_ptrs, const uint64_t* lens,

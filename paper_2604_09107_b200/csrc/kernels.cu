@@ -264,12 +264,25 @@ __global__ void __launch_bounds__(kDigWarps * 32)
     cp_async_wait<kDigRing - 1>();
     __syncwarp();
     if (lane < 4) {
-      const std::uint8_t* st = ring + (s % kDigRing) * kDigStep;
+      const std::uint8_t* st = ring + (s % kDigRing) * kDigStep + 8 * lane;
       const std::uint64_t first = s * (kDigStep / 32);
       std::uint64_t cnt = full_stripes > first ? full_stripes - first : 0;
       if (cnt > kDigStep / 32) cnt = kDigStep / 32;
-      for (std::uint64_t k = 0; k < cnt; ++k)
-        acc = xround(acc, *reinterpret_cast<const std::uint64_t*>(st + 32 * k + 8 * lane));
+      if (cnt == kDigStep / 32) {
+        // full step: loads hoisted 8 ahead so only the accumulator chain
+        // (round64, the serial part of XXH64) is on the critical path
+#pragma unroll
+        for (int k0 = 0; k0 < kDigStep / 32; k0 += 8) {
+          std::uint64_t w[8];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) w[j] = *reinterpret_cast<const std::uint64_t*>(st + 32 * (k0 + j));
+#pragma unroll
+          for (int j = 0; j < 8; ++j) acc = xround(acc, w[j]);
+        }
+      } else {
+        for (std::uint64_t k = 0; k < cnt; ++k)
+          acc = xround(acc, *reinterpret_cast<const std::uint64_t*>(st + 32 * k));
+      }
     }
     if (s + 1 < nsteps) __syncwarp();
   }

@@ -3,6 +3,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -45,6 +46,11 @@ bool encode(CUtensorMap* m, std::uint64_t base, std::uint64_t chunk_len, std::ui
 
 constexpr std::size_t kHdr = 128;  // work words (64 B) + PullStatus (32 B), padded
 
+bool maps_disabled() {
+  static const bool v = std::getenv("RSB_NO_MAPS") != nullptr;  // diagnostic knob
+  return v;
+}
+
 }  // namespace
 
 cudaError_t upload_pull_plan(int device, cudaStream_t s, ItemDesc* items, std::uint32_t n,
@@ -69,7 +75,7 @@ cudaError_t upload_pull_plan(int device, cudaStream_t s, ItemDesc* items, std::u
     const std::uint64_t rows = cl ? d.len / cl : 0;
     const bool aligned = (d.src % 16 == 0) && (d.dst % 16 == 0) && cl % kMapBoxCols == 0 &&
                          cl % 16 == 0;
-    if (aligned && rows >= 32 && d.src) {
+    if (aligned && rows >= 32 && d.src && !maps_disabled()) {
       auto* m = reinterpret_cast<CUtensorMap*>(host.data() + maps_off + 256 * std::size_t(i));
       bool ok = encode(m, d.src, cl, rows);
       if (ok && d.dst) ok = encode(m + 1, d.dst, cl, rows);
