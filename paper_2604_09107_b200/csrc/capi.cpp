@@ -498,8 +498,14 @@ int rs_pull_spans(const uint64_t* src_ptrs, const uint64_t* dst_ptrs, const uint
   std::vector<rsb::dev::ItemDesc> descs(n_items);
   std::uint32_t chunk = 0;
   for (int i = 0; i < n_items; ++i) {
-    descs[i] = {src_ptrs[i], dst_ptrs ? dst_ptrs[i] : 0, lens[i], chunk,
-                static_cast<std::uint32_t>(chunk_bytes)};
+    descs[i] = {};
+    descs[i].src = src_ptrs[i];
+    descs[i].dst = dst_ptrs ? dst_ptrs[i] : 0;
+    descs[i].len = lens[i];
+    descs[i].chunk0 = chunk;
+    descs[i].chunk_len = static_cast<std::uint32_t>(chunk_bytes);
+    descs[i].src_chunk0 = chunk;
+    descs[i].q = descs[i].m = 1;
     const auto n = static_cast<std::uint32_t>((lens[i] + chunk_bytes - 1) / chunk_bytes);
     chunk += (n + rsb::dev::kBatchChunks - 1) / rsb::dev::kBatchChunks * rsb::dev::kBatchChunks;
   }
@@ -508,13 +514,13 @@ int rs_pull_spans(const uint64_t* src_ptrs, const uint64_t* dst_ptrs, const uint
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   rsb::dev::PullStatus ps{};
   rsb::dev::PullParams p{};
+  const rsb::dev::SrcDesc sdesc{expect_dev, nullptr, 0, 0};
   if (rsb::dev::upload_pull_plan(device, stream, descs.data(), static_cast<std::uint32_t>(n_items),
-                                 &plan, &p) != cudaSuccess)
+                                 &sdesc, 1, &plan, &p) != cudaSuccess)
     rc = st(rsb::Status::transfer_failed);
   if (!rc) {
     p.n_chunks = chunk;
     p.n_batches = (chunk + rsb::dev::kBatchChunks - 1) / rsb::dev::kBatchChunks;
-    p.src_digests = expect_dev;
     p.dst_digests = out_digests_dev;
     p.timeout_ns = 4000000000ull;
     cudaEventCreate(&e0);

@@ -169,6 +169,21 @@ ChunkMap ChunkMap::uniform(const Manifest& m, std::uint64_t chunk_bytes) {
   return c;
 }
 
+dev::ItemDesc identity_segment(std::uint64_t src, std::uint64_t dst, std::uint64_t len,
+                               const ChunkMap& cm, std::size_t item) {
+  dev::ItemDesc d{};
+  d.src = src;
+  d.dst = dst;
+  d.len = len;
+  d.chunk0 = cm.chunk0[item];
+  d.chunk_len = cm.chunk_len[item];
+  d.src_chunk0 = cm.chunk0[item];
+  d.q = 1;
+  d.m = 1;
+  d.src_id = 0;
+  return d;
+}
+
 // ----------------------------------------------------------- ServeRegistry
 
 std::string ServeRegistry::key(const std::string& model, const std::string& replica,
@@ -524,10 +539,12 @@ Status Client::build_payload(Shard& sh, VersionId v, std::shared_ptr<Payload>* o
     // watermark set: a complete source.
     std::vector<dev::ItemDesc> descs(items.size());
     for (std::size_t i = 0; i < items.size(); ++i)
-      descs[i] = {p->item_ptrs[i], 0, items[i].length, p->cmap.chunk0[i], p->cmap.chunk_len[i]};
+      descs[i] = identity_segment(p->item_ptrs[i], 0, items[i].length, p->cmap, i);
+    const dev::SrcDesc self{nullptr, nullptr, 0, 0};
     dev::PullParams pp{};
     RS_CUDA(dev::upload_pull_plan(sh.device, sh.stream, descs.data(),
-                                  static_cast<std::uint32_t>(descs.size()), &sh.plan, &pp));
+                                  static_cast<std::uint32_t>(descs.size()), &self, 1, &sh.plan,
+                                  &pp));
     pp.n_chunks = nc;
     pp.n_batches = nb;
     pp.dst_digests = static_cast<std::uint64_t*>(p->digests.p);
@@ -735,18 +752,18 @@ Status Client::launch_fill(Shard& sh, const SourceView& src, bool src_complete) 
   const auto& items = p.manifest.items();
   std::vector<dev::ItemDesc> descs(items.size());
   for (std::size_t i = 0; i < items.size(); ++i)
-    descs[i] = {src.item_ptrs[i], p.item_ptrs[i], items[i].length, p.cmap.chunk0[i],
-                p.cmap.chunk_len[i]};
+    descs[i] = identity_segment(src.item_ptrs[i], p.item_ptrs[i], items[i].length, p.cmap, i);
+  const dev::SrcDesc sdesc{reinterpret_cast<const std::uint64_t*>(src.digests),
+                           src_complete ? nullptr : reinterpret_cast<const std::uint32_t*>(src.flags),
+                           src.epoch, 0};
   dev::PullParams pp{};
   RS_CUDA(dev::upload_pull_plan(sh.device, sh.stream, descs.data(),
-                                static_cast<std::uint32_t>(descs.size()), &sh.plan, &pp));
+                                static_cast<std::uint32_t>(descs.size()), &sdesc, 1, &sh.plan,
+                                &pp));
   stats_.h2d_bytes += sh.plan.h2d_bytes;
   pp.n_chunks = p.cmap.n_chunks();
   pp.n_batches = p.cmap.n_batches();
-  pp.src_digests = reinterpret_cast<const std::uint64_t*>(src.digests);
   pp.dst_digests = static_cast<std::uint64_t*>(p.digests.p);
-  pp.src_flags = src_complete ? nullptr : reinterpret_cast<const std::uint32_t*>(src.flags);
-  pp.src_epoch = src.epoch;
   pp.dst_flags = static_cast<std::uint32_t*>(p.flags.p);
   pp.dst_epoch = p.epoch;
   pp.timeout_ns = static_cast<std::uint64_t>(cfg_.pull_timeout_s * 1e9);

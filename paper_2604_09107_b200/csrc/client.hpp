@@ -264,6 +264,11 @@ class Client {
   ClientStats stats_;
 };
 
+// A whole item copied as-is (q == m == 1), source and landing chunk indices
+// equal.
+dev::ItemDesc identity_segment(std::uint64_t src, std::uint64_t dst, std::uint64_t len,
+                               const ChunkMap& cm, std::size_t item);
+
 // Peer / IPC address translation for the reader's device.
 Status map_source(const std::shared_ptr<ServeState>& st, int reader_device, SourceView* out);
 Status enable_peer(int reader_device, int owner_device);

@@ -206,6 +206,36 @@ static __device__ __noinline__ std::uint64_t repull_chunk(const std::uint8_t* sr
   return finish_tail(h, tail, t);
 }
 
+// Landing chunk k of a segment: its source/landing addresses, length and
+// source chunk index (see ItemDesc).  clen == 0: a hole between segments.
+struct ChunkRef {
+  const std::uint8_t* src;
+  std::uint8_t* dst;
+  std::uint32_t clen;
+  std::uint32_t src_chunk;
+};
+__device__ __forceinline__ ChunkRef chunk_ref(const ItemDesc& d, std::uint32_t k) {
+  const std::uint32_t c = d.chunk_len & kChunkLenMask;
+  const std::uint64_t doff = std::uint64_t(k) * c;
+  ChunkRef r{nullptr, nullptr, 0u, 0u};
+  if (doff >= d.len) return r;
+  std::uint64_t soff;
+  if (d.q == d.m) {
+    soff = doff;
+    r.src_chunk = d.src_chunk0 + k;
+  } else {
+    const std::uint32_t t = k / d.q, j = k - t * d.q;
+    const std::uint32_t sc = t * d.m + j;
+    soff = std::uint64_t(sc) * c;
+    r.src_chunk = d.src_chunk0 + sc;
+  }
+  r.src = reinterpret_cast<const std::uint8_t*>(d.src) + soff;
+  r.dst = d.dst ? reinterpret_cast<std::uint8_t*>(d.dst) + doff : nullptr;
+  const std::uint64_t rem = d.len - doff;
+  r.clen = static_cast<std::uint32_t>(rem < c ? rem : c);
+  return r;
+}
+
 // Last item whose first chunk is <= c (items sorted by chunk0).
 __device__ __forceinline__ std::uint32_t find_item(const ItemDesc* items, std::uint32_t n,
                                                    std::uint32_t c) {

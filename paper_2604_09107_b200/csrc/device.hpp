@@ -18,23 +18,43 @@ constexpr std::uint32_t kAbort = 0x80000000u;
 constexpr int kBatchChunks = 32;  // chunks per warp batch = per watermark flag
 constexpr int kPiece = 256;       // bytes of each chunk staged per step
 
-// One transfer item as the reader sees it: where its bytes come from (any
-// address the reader's device can load: local HBM, a peer GPU through
-// NVLink/UVA, or an IPC-mapped peer allocation), where they land, and how
-// the item is cut into digest chunks.
+// One segment of the landing stream as the reader sees it: where its chunks
+// come from (any address the reader's device can load: local HBM, a peer
+// GPU through NVLink/UVA, or an IPC-mapped peer allocation), where they land
+// and how they map.  Landing chunk k of the segment (k = 0..) is source
+// chunk (row t = k / q, column j = k % q) of a source item whose rows are m
+// chunks long: source offset (t*m + j) * chunk_len, source chunk index
+// src_chunk0 + t*m + j.  It lands densely at dst + k * chunk_len.  q == m is
+// a contiguous copy (an identity pull, or a dim-0 reshard); q < m takes a
+// column band of every row (a dim-1 / row-parallel reshard).
 struct ItemDesc {
-  std::uint64_t src;        // source address (0: hash-only / dst is source)
-  std::uint64_t dst;        // landing address (0: hash-only)
-  std::uint64_t len;        // bytes
-  std::uint32_t chunk0;     // global index of the item's first chunk
-  std::uint32_t chunk_len;  // uniform chunk length inside the item | kHasMap
+  std::uint64_t src;         // source address of the segment's first chunk
+  std::uint64_t dst;         // landing address of the first chunk (0: hash-only)
+  std::uint64_t len;         // bytes landed by the segment
+  std::uint32_t chunk0;      // landing chunk index of the first chunk (global)
+  std::uint32_t chunk_len;   // chunk length | kHasMap | kMap3D
+  std::uint32_t src_chunk0;  // source chunk index of the first chunk
+  std::uint16_t q, m;        // chunks taken per source row / chunks per source row
+  std::uint32_t src_id;      // index into PullParams.srcs
+  std::uint32_t pad;
 };
-// ItemDesc.chunk_len flag: the item has TMA tensor maps (2-D view
-// [len / chunk_len rows][chunk_len bytes]) at PullParams.maps + 256*i
-// (source) and + 256*i + 128 (destination).
+static_assert(sizeof(ItemDesc) == 48, "ItemDesc layout");
+// chunk_len flags: the segment has TMA tensor maps at PullParams.maps +
+// 256*i (source) and + 256*i + 128 (destination).  Source map: 2-D
+// [rows = chunks][chunk_len] when q == m, 3-D [rows][q][chunk_len] (row
+// stride m*chunk_len, kMap3D) when q < m.  Destination map: 2-D.
 constexpr std::uint32_t kHasMap = 0x80000000u;
-constexpr std::uint32_t kChunkLenMask = 0x7fffffffu;
-constexpr int kMapBoxCols = 128;  // TMA box: 128 bytes x 32 rows, 128B swizzle
+constexpr std::uint32_t kMap3D = 0x40000000u;
+constexpr std::uint32_t kChunkLenMask = 0x3fffffffu;
+constexpr int kMapBoxCols = 128;  // TMA box: 128 bytes x 32 chunks, 128B swizzle
+
+// A source serve state as the reader's device sees it.
+struct SrcDesc {
+  const std::uint64_t* digests;  // source chunk-digest table (null: compute only)
+  const std::uint32_t* flags;    // source watermarks (null: source complete)
+  std::uint32_t epoch;           // source fill epoch to wait for
+  std::uint32_t pad;
+};
 
 enum PullCode : std::uint32_t {
   kPullOk = 0,
@@ -54,36 +74,36 @@ struct PullStatus {
 };
 
 struct PullParams {
-  const ItemDesc* items;
+  const ItemDesc* items;             // segments, sorted by chunk0
   std::uint32_t n_items;
   std::uint32_t n_chunks;
   std::uint32_t n_batches;
-  std::uint32_t first_batch;   // batches below this are skipped (resume)
-  const std::uint64_t* src_digests;  // expected per chunk (null: compute only)
-  std::uint64_t* dst_digests;        // own table to fill (null: don't)
-  const std::uint32_t* src_flags;    // upstream watermarks (null: complete)
-  std::uint32_t src_epoch;
+  std::uint32_t first_batch;         // batches below this are skipped
+  const SrcDesc* srcs;               // source table (segments' src_id)
+  std::uint32_t n_srcs;
   std::uint32_t dst_epoch;
+  std::uint64_t* dst_digests;        // own table to fill (null: don't)
   std::uint32_t* dst_flags;          // own watermarks (null: not serving)
   std::uint32_t* work;               // [0] batch ticket, [1] abort
   PullStatus* status;
   std::uint64_t timeout_ns;
   std::uint32_t resume;              // dst_flags may already hold dst_epoch
   std::uint32_t pad;
-  const void* maps;                  // CUtensorMap pairs per item (or null)
+  const void* maps;                  // CUtensorMap pairs per segment (or null)
 };
 
-// Uploads a pull plan (item table + TMA tensor maps + work/status words)
-// into `scratch` on `device` and points `p` at it.  Items whose source (and
-// destination) are 16-byte aligned get tensor maps (kHasMap).  Declared
-// here, implemented in pullplan.cpp.
+// Uploads a pull plan (segment table + source table + TMA tensor maps +
+// work/status words) into `up->scratch` on `device` and points `p` at it.
+// Segments whose addresses are 16-byte aligned and whose geometry fits a box
+// get tensor maps (kHasMap).  Implemented in pullplan.cpp.
 struct PlanUpload {
   void* scratch = nullptr;       // device buffer (grown by the callee)
   std::size_t scratch_bytes = 0;
   std::size_t h2d_bytes = 0;     // bytes uploaded by the last call
 };
 cudaError_t upload_pull_plan(int device, cudaStream_t s, ItemDesc* items, std::uint32_t n_items,
-                             PlanUpload* up, PullParams* p);
+                             const SrcDesc* srcs, std::uint32_t n_srcs, PlanUpload* up,
+                             PullParams* p);
 void free_pull_plan(int device, PlanUpload* up);
 
 // Fused mover: copy + per-chunk XXH64 verify + watermark publish.  `sms` is

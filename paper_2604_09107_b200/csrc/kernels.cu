@@ -106,38 +106,38 @@ __global__ void __launch_bounds__(kThreads, 2) pull_kernel(const PullParams p) {
     b = __shfl_sync(full, b, 0);
     if (b >= p.n_batches) break;
     if (ld_volatile(&p.work[1])) break;
-    if (p.dst_flags && ld_volatile(&p.dst_flags[b]) == p.dst_epoch) continue;  // resume
-    if (p.src_flags) {
-      std::uint32_t code = 0;
-      if (lane == 0) code = wait_flag(&p.src_flags[b], p.src_epoch, p.timeout_ns, &p.work[1]);
-      code = __shfl_sync(full, code, 0);
-      if (code != kPullOk) {
-        if (lane == 0) {
-          if (code != kPullAborted) {
-            atomicCAS(&p.status->code, 0u, code);
-            atomicExch(&p.status->bad_chunk, b * kBatchChunks);
-          }
-          atomicExch(&p.work[1], 1u);
-          if (p.dst_flags) st_release_sys(&p.dst_flags[b], p.dst_epoch | kAbort);
-        }
-        break;
-      }
-    }
+    if (p.resume && ld_volatile(&p.dst_flags[b]) == p.dst_epoch) continue;  // landed already
     const std::uint32_t c = b * kBatchChunks + lane;
     LaneChunk mine{nullptr, nullptr, 0u, 0u};
     std::uint64_t expect = 0;
+    const SrcDesc* sd = nullptr;
+    ChunkRef r{nullptr, nullptr, 0u, 0u};
     if (c < p.n_chunks) {
       const ItemDesc it = p.items[find_item(p.items, p.n_items, c)];
-      const std::uint32_t cunit = it.chunk_len & kChunkLenMask;
-      const std::uint64_t off = std::uint64_t(c - it.chunk0) * cunit;
-      if (off < it.len) {  // else: a hole between batch-aligned items
-        const std::uint64_t rem = it.len - off;
-        mine.len = static_cast<std::uint32_t>(rem < cunit ? rem : cunit);
-        mine.src = reinterpret_cast<const std::uint8_t*>(it.src) + off;
-        mine.dst = it.dst ? reinterpret_cast<std::uint8_t*>(it.dst) + off : nullptr;
+      r = chunk_ref(it, c - it.chunk0);
+      if (r.clen) {
+        mine = {r.src, r.dst, r.clen, 0u};
+        sd = &p.srcs[it.src_id];
       }
-      if (p.src_digests) expect = __ldcg(&p.src_digests[c]);
     }
+    // chase the source watermark (every lane its own source batch)
+    std::uint32_t code = kPullOk;
+    if (sd && sd->flags)
+      code = wait_flag(&sd->flags[r.src_chunk / kBatchChunks], sd->epoch, p.timeout_ns, &p.work[1]);
+    code = __reduce_max_sync(full, code);
+    if (code != kPullOk) {
+      if (lane == 0) {
+        if (code != kPullAborted) {
+          atomicCAS(&p.status->code, 0u, code);
+          atomicExch(&p.status->bad_chunk, b * kBatchChunks);
+        }
+        atomicExch(&p.work[1], 1u);
+        if (p.dst_flags) st_release_sys(&p.dst_flags[b], p.dst_epoch | kAbort);
+      }
+      break;
+    }
+    const bool verify = sd && sd->digests;
+    if (verify) expect = __ldcg(&sd->digests[r.src_chunk]);
     refs[lane] = mine;
     std::uint32_t maxlen = mine.len;
 #pragma unroll
@@ -184,13 +184,13 @@ __global__ void __launch_bounds__(kThreads, 2) pull_kernel(const PullParams p) {
         __syncwarp();
       }
       cp_async_wait<0>();
-      const bool lane_ok = mine.len == 0 || p.src_digests == nullptr || digest == expect;
+      const bool lane_ok = mine.len == 0 || !verify || digest == expect;
       good = __all_sync(full, lane_ok);
       if (!good && lane == 0 && attempt == 0) atomicAdd(&p.status->retried_batches, 1u);
       __syncwarp();
     }
     if (!good) {
-      const bool lane_ok = mine.len == 0 || digest == expect;
+      const bool lane_ok = mine.len == 0 || !verify || digest == expect;
       const unsigned bad = __ballot_sync(full, !lane_ok);
       if (lane == 0) {
         atomicCAS(&p.status->code, 0u, static_cast<std::uint32_t>(kPullChecksum));

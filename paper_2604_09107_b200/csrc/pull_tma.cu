@@ -1,31 +1,33 @@
-// K1+K2 on the TMA path: the fused pull + per-chunk XXH64 verify + watermark
-// kernel (replaces copy_slice_locked, transport.cpp:51-69, and the per-item
-// digest64 check of TransferTask::verify_ready, client_core.cpp:306-334).
+// K1+K2 (+K4 reshard) on the TMA path: the fused pull + per-chunk XXH64
+// verify + watermark kernel.  Replaces copy_slice_locked (transport.cpp:51-69)
+// and the per-item digest64 check of TransferTask::verify_ready
+// (client_core.cpp:306-334); with segment mappings (ItemDesc q < m, several
+// sources) it also performs the TP/FSDP reshard gather/split.
 //
 // Warp-specialized, persistent: each CTA is one producer warp and one
 // consumer warp sharing a ring of S stages in shared memory.  A stage holds
 // the next P bytes of each of the 32 chunks of one watermark batch; lane l
-// of the consumer hashes chunk 32b+l.
+// of the consumer hashes landing chunk 32b+l.
 //
 // Two stage layouts:
-//  * box (the common case: all 32 chunks of the batch are full-length rows
-//    of one item that has TMA tensor maps).  The item is viewed as a 2-D
-//    tensor [len/chunk_len rows][chunk_len bytes]; a stage is P/128 boxes of
-//    [32 rows x 128 B] with 128-byte swizzle, each moved by ONE
-//    cp.async.bulk.tensor load (and landed by ONE tensor store) issued by a
-//    single lane.  The swizzle keeps the per-row 128-bit reads of the hash
-//    lanes bank-conflict free.
-//  * slot (batches with a short last chunk, item holes, unaligned regions):
-//    one padded slot of P+16 bytes per chunk, every lane issuing its own
-//    cp.async.bulk copy (plain loads/stores for unaligned bytes and tails).
+//  * box (the common case: all 32 chunks of the batch are whole chunks of one
+//    segment that has TMA tensor maps).  A stage is P/128 boxes of
+//    [32 chunks x 128 B] with 128-byte swizzle, each moved by ONE
+//    cp.async.bulk.tensor load (2-D for contiguous segments, 3-D
+//    [rows][q][chunk] for a column band of a row-split reshard) and landed by
+//    ONE 2-D tensor store, both issued by a single lane.  The swizzle keeps
+//    the per-chunk 128-bit reads of the hash lanes bank-conflict free.
+//  * slot (batches with a short last chunk, holes, mixed segments, unaligned
+//    regions): one padded slot of P+16 bytes per chunk, every lane issuing
+//    its own cp.async.bulk copy (plain loads/stores for unaligned bytes).
 //
 //   producer  walks its batches (static schedule b = blockIdx.x + k*grid, so
-//             the landed prefix advances front to back), waits the upstream
-//             watermark when the source is still filling, fills stages.
+//             the landed prefix advances front to back), waits the source
+//             watermark(s) when a source is still filling, fills stages.
 //   consumer  per stage: lands the stage (tensor store / bulk stores), hashes
 //             (XXH64 32-byte stripes), frees the stage once the stores have
 //             read it.  After a batch's last step it verifies the 32 chunk
-//             digests against the source's table (one quiet re-pull of a bad
+//             digests against the sources' tables (one quiet re-pull of a bad
 //             chunk), writes its own digest table, and one stage later --
 //             when the batch's stores have completed -- publishes the batch
 //             watermark (fence.proxy.async + st.release.sys, cumulative over
@@ -54,6 +56,14 @@ __device__ __forceinline__ void tensor_load_2d(void* smem, const void* map, int 
       "l"(map), "r"(x), "r"(y), "r"(smem_u32(bar))
       : "memory");
 }
+__device__ __forceinline__ void tensor_load_3d(void* smem, const void* map, int x, int y, int z,
+                                               unsigned long long* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes "
+      "[%0], [%1, {%2, %3, %4}], [%5];\n" ::"r"(smem_u32(smem)),
+      "l"(map), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
+      : "memory");
+}
 __device__ __forceinline__ void tensor_store_2d(const void* map, int x, int y, const void* smem) {
   asm volatile(
       "cp.async.bulk.tensor.2d.global.shared::cta.tile.bulk_group [%0, {%1, %2}], [%3];\n" ::"l"(map),
@@ -75,11 +85,11 @@ struct Cfg {
     std::uint32_t batch;
     std::uint32_t step;
     std::uint32_t last;
-    std::uint32_t box;   // 1: box layout
-    std::uint32_t item;  // box layout: item index
-    std::uint32_t y0;    // box layout: first row (chunk) of the batch in the item
-    std::uint32_t g;     // box layout: byte offset of the step within the chunk
-    std::uint32_t bpiece;
+    std::uint32_t box;     // 1: box layout
+    std::uint32_t item;    // box layout: segment index
+    std::uint32_t k0;      // box layout: first chunk of the batch within the segment
+    std::uint32_t g;       // box layout: byte offset of the step within the chunk
+    std::uint32_t bpiece;  // box layout: bytes per chunk in this step
     std::uint64_t dst[32];
     std::uint32_t piece[32];
     std::uint32_t clen[32];
@@ -102,8 +112,7 @@ __global__ void __launch_bounds__(64, C::kCtas) pull_tma_kernel(const PullParams
   constexpr int kP = C::kP;
   constexpr int kStages = C::kStages;
   extern __shared__ __align__(1024) std::uint8_t smraw[];
-  // 1 KiB-align the stages (128B-swizzled boxes)
-  const std::uint32_t mis = smem_u32(smraw) & 1023u;
+  const std::uint32_t mis = smem_u32(smraw) & 1023u;  // 1 KiB-align the stages
   Smem& sm = *reinterpret_cast<Smem*>(smraw + (mis ? 1024 - mis : 0));
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -120,7 +129,8 @@ __global__ void __launch_bounds__(64, C::kCtas) pull_tma_kernel(const PullParams
   if (smem_items) {
     const uint4* s = reinterpret_cast<const uint4*>(p.items);
     uint4* d = reinterpret_cast<uint4*>(sm.items);
-    for (std::uint32_t i = threadIdx.x; i < p.n_items * 2; i += blockDim.x) d[i] = s[i];
+    const std::uint32_t n16 = p.n_items * (sizeof(ItemDesc) / 16);
+    for (std::uint32_t i = threadIdx.x; i < n16; i += blockDim.x) d[i] = s[i];
   }
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
@@ -144,60 +154,64 @@ __global__ void __launch_bounds__(64, C::kCtas) pull_tma_kernel(const PullParams
         abort_seen = abort_next;
         continue;
       }
-      if (p.src_flags) {
-        std::uint32_t code = 0;
-        if (lane == 0) code = wait_flag(&p.src_flags[b], p.src_epoch, p.timeout_ns, &p.work[1]);
-        code = __shfl_sync(full, code, 0);
-        if (code != kPullOk) {
-          if (lane == 0) {
-            if (code != kPullAborted) {
-              atomicCAS(&p.status->code, 0u, code);
-              atomicExch(&p.status->bad_chunk, b * kBatchChunks);
-            }
-            atomicExch(&p.work[1], 1u);
-            if (p.dst_flags) st_release_sys(&p.dst_flags[b], p.dst_epoch | kAbort);
-          }
-          break;
-        }
-        fence_proxy_async_global();  // upstream bytes are read by the async proxy
-      }
       const std::uint32_t c = b * kBatchChunks + lane;
-      const std::uint8_t* src = nullptr;
-      std::uint8_t* dst = nullptr;
-      std::uint32_t clen = 0, cunit = 0, item = 0xffffffffu, itflags = 0, row = 0;
-      std::uint64_t expect = 0;
+      ChunkRef r{nullptr, nullptr, 0u, 0u};
+      std::uint32_t seg = 0xffffffffu, cunit = 0, itflags = 0, k = 0, src_id = 0;
       if (c < p.n_chunks) {
-        if (p.src_digests) expect = __ldcg(&p.src_digests[c]);  // consumed at the last step
-        item = find_item(items, p.n_items, c);
-        const ItemDesc d = items[item];
+        seg = find_item(items, p.n_items, c);
+        const ItemDesc d = items[seg];
         cunit = d.chunk_len & kChunkLenMask;
-        itflags = d.chunk_len & kHasMap;
-        row = c - d.chunk0;
-        const std::uint64_t off = std::uint64_t(row) * cunit;
-        if (off < d.len) {
-          const std::uint64_t rem = d.len - off;
-          clen = static_cast<std::uint32_t>(rem < cunit ? rem : cunit);
-          src = reinterpret_cast<const std::uint8_t*>(d.src) + off;
-          dst = d.dst ? reinterpret_cast<std::uint8_t*>(d.dst) + off : nullptr;
-        }  // else: a hole between batch-aligned items
+        itflags = d.chunk_len & (kHasMap | kMap3D);
+        k = c - d.chunk0;
+        r = chunk_ref(d, k);
+        src_id = d.src_id;
       }
-      const std::uint32_t item0 = __shfl_sync(full, item, 0);
-      const std::uint32_t y0 = __shfl_sync(full, row, 0);
+      // Chase the source watermark(s) when the source is still filling.
+      const SrcDesc* sd = r.clen ? &p.srcs[src_id] : nullptr;
+      std::uint32_t code = kPullOk;
+      const std::uint32_t sbatch = r.src_chunk / kBatchChunks;
+      const std::uint32_t sb0 = __shfl_sync(full, sbatch, 0);
+      const std::uint32_t sid0 = __shfl_sync(full, src_id, 0);
+      const bool need0 = __shfl_sync(full, sd != nullptr && sd->flags != nullptr, 0);
+      if (lane == 0 && need0) code = wait_flag(&sd->flags[sbatch], sd->epoch, p.timeout_ns, &p.work[1]);
+      if (sd && sd->flags && (sbatch != sb0 || src_id != sid0) && lane != 0)
+        code = wait_flag(&sd->flags[sbatch], sd->epoch, p.timeout_ns, &p.work[1]);
+      const std::uint32_t worst = __reduce_max_sync(full, code);
+      if (worst != kPullOk) {
+        if (lane == 0) {
+          if (worst != kPullAborted) {
+            atomicCAS(&p.status->code, 0u, worst);
+            atomicExch(&p.status->bad_chunk, b * kBatchChunks);
+          }
+          atomicExch(&p.work[1], 1u);
+          if (p.dst_flags) st_release_sys(&p.dst_flags[b], p.dst_epoch | kAbort);
+        }
+        break;
+      }
+      if (__any_sync(full, sd != nullptr && sd->flags != nullptr)) fence_proxy_async_global();
+      const std::uint64_t expect = (sd && sd->digests) ? __ldcg(&sd->digests[r.src_chunk]) : 0;
+      const std::uint32_t seg0 = __shfl_sync(full, seg, 0);
+      const std::uint32_t k0 = __shfl_sync(full, k, 0);
+      const std::uint32_t q0 = seg0 < p.n_items ? items[seg0].q : 1;
       const bool box = maps != nullptr &&
-                       __all_sync(full, item == item0 && itflags != 0 && clen == cunit && clen != 0);
-      std::uint32_t maxlen = clen;
+                       __all_sync(full, seg == seg0 && (itflags & kHasMap) && r.clen == cunit &&
+                                            r.clen != 0) &&
+                       (k0 % q0) == 0;
+      const bool map3d = box && (items[seg0].chunk_len & kMap3D) != 0;
+      std::uint32_t maxlen = r.clen;
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) maxlen = max(maxlen, __shfl_xor_sync(full, maxlen, o));
       const std::uint32_t nsteps = (maxlen + kP - 1) / kP;
-      const bool src_vec = (reinterpret_cast<std::uintptr_t>(src) & 15) == 0;
+      const bool src_vec = (reinterpret_cast<std::uintptr_t>(r.src) & 15) == 0;
       for (std::uint32_t s = 0; s < nsteps; ++s) {
         mbar_wait(&sm.empty[stage], phase ^ 1);
         Meta& m = sm.meta[stage];
         const std::uint32_t g = s * kP;
-        const std::uint32_t piece = g < clen ? min(static_cast<std::uint32_t>(kP), clen - g) : 0;
+        const std::uint32_t piece =
+            g < r.clen ? min(static_cast<std::uint32_t>(kP), r.clen - g) : 0;
         const bool last = s + 1 == nsteps;
         m.piece[lane] = piece;
-        m.clen[lane] = clen;
+        m.clen[lane] = r.clen;
         if (last) m.expect[lane] = expect;
         if (box) {
           if (lane == 0) {
@@ -205,24 +219,31 @@ __global__ void __launch_bounds__(64, C::kCtas) pull_tma_kernel(const PullParams
             m.step = s;
             m.last = last;
             m.box = 1;
-            m.item = item0;
-            m.y0 = y0;
+            m.item = seg0;
+            m.k0 = k0;
             m.g = g;
             m.bpiece = piece;
           }
           __syncwarp();
           if (lane == 0) {
             mbar_arrive_tx(&sm.full[stage], 32 * piece);
-            const void* map = maps + 256 * std::size_t(item0);
-            for (std::uint32_t j = 0; j < piece / kMapBoxCols; ++j)
-              tensor_load_2d(sm.stage[stage] + j * 4096, map, static_cast<int>(g + j * kMapBoxCols),
-                             static_cast<int>(y0), &sm.full[stage]);
+            const void* map = maps + 256 * std::size_t(seg0);
+            const std::uint32_t qq = q0;
+            for (std::uint32_t j = 0; j < piece / kMapBoxCols; ++j) {
+              const int x = static_cast<int>(g + j * kMapBoxCols);
+              if (map3d)
+                tensor_load_3d(sm.stage[stage] + j * 4096, map, x, 0, static_cast<int>(k0 / qq),
+                               &sm.full[stage]);
+              else
+                tensor_load_2d(sm.stage[stage] + j * 4096, map, x, static_cast<int>(k0),
+                               &sm.full[stage]);
+            }
           }
         } else {
           std::uint8_t* slot = sm.stage[stage] + lane * C::kSlot;
           const std::uint32_t bulk = src_vec ? (piece & ~15u) : 0;
-          for (std::uint32_t k = bulk; k < piece; ++k) slot[k] = __ldcg(src + g + k);
-          m.dst[lane] = dst ? reinterpret_cast<std::uint64_t>(dst + g) : 0;
+          for (std::uint32_t kk = bulk; kk < piece; ++kk) slot[kk] = __ldcg(r.src + g + kk);
+          m.dst[lane] = r.dst ? reinterpret_cast<std::uint64_t>(r.dst + g) : 0;
           std::uint32_t tx = bulk;
 #pragma unroll
           for (int o = 16; o > 0; o >>= 1) tx += __shfl_xor_sync(full, tx, o);
@@ -235,7 +256,7 @@ __global__ void __launch_bounds__(64, C::kCtas) pull_tma_kernel(const PullParams
           __syncwarp();
           if (lane == 0) mbar_arrive_tx(&sm.full[stage], tx);
           __syncwarp();
-          if (bulk) bulk_g2s(slot, src + g, bulk, &sm.full[stage]);
+          if (bulk) bulk_g2s(slot, r.src + g, bulk, &sm.full[stage]);
         }
         advance(stage, phase);
       }
@@ -296,24 +317,21 @@ __global__ void __launch_bounds__(64, C::kCtas) pull_tma_kernel(const PullParams
       const int stripes = static_cast<int>(piece >> 5);
       if (box) {
         // 1) land: one tensor store per box, issued by lane 0
-        if (lane == 0) {
+        if (lane == 0 && items[m.item].dst != 0) {
           const std::uint8_t* dmap = maps + 256 * std::size_t(m.item) + 128;
-          const bool has_dst = items[m.item].dst != 0;
-          if (has_dst) {
-            fence_proxy_async_smem();
-            for (std::uint32_t j = 0; j < m.bpiece / kMapBoxCols; ++j)
-              tensor_store_2d(dmap, static_cast<int>(m.g + j * kMapBoxCols), static_cast<int>(m.y0),
-                              st + j * 4096);
-            bulk_commit();
-            committed = true;
-          }
+          fence_proxy_async_smem();
+          for (std::uint32_t j = 0; j < m.bpiece / kMapBoxCols; ++j)
+            tensor_store_2d(dmap, static_cast<int>(m.g + j * kMapBoxCols), static_cast<int>(m.k0),
+                            st + j * 4096);
+          bulk_commit();
+          committed = true;
         }
-        // 2) hash row `lane` of the swizzled boxes
+        // 2) hash chunk `lane` = row `lane` of the swizzled boxes
         const std::uint8_t* rowbase = st + lane * 128;
 #pragma unroll 4
-        for (int k = 0; k < stripes; ++k) {
-          const std::uint8_t* boxp = rowbase + (k >> 2) * 4096;
-          const std::uint32_t x = static_cast<std::uint32_t>(k & 3) * 32;
+        for (int kk = 0; kk < stripes; ++kk) {
+          const std::uint8_t* boxp = rowbase + (kk >> 2) * 4096;
+          const std::uint32_t x = static_cast<std::uint32_t>(kk & 3) * 32;
           const uint4 a = *reinterpret_cast<const uint4*>(boxp + (x ^ swz));
           const uint4 q = *reinterpret_cast<const uint4*>(boxp + ((x + 16) ^ swz));
           v1 = xround(v1, (std::uint64_t(a.y) << 32) | a.x);
@@ -324,8 +342,7 @@ __global__ void __launch_bounds__(64, C::kCtas) pull_tma_kernel(const PullParams
         if (clen && s * kP + piece == clen) {
           std::uint64_t h = clen >= 32 ? merge4(v1, v2, v3, v4) : kP5;
           h += clen;
-          // box rows are whole 128-byte multiples: no tail
-          digest = finish_tail(h, nullptr, 0);
+          digest = finish_tail(h, nullptr, 0);  // whole 128-byte rows: no tail
         }
       } else {
         std::uint8_t* slot = st + lane * C::kSlot;
@@ -338,13 +355,13 @@ __global__ void __launch_bounds__(64, C::kCtas) pull_tma_kernel(const PullParams
             bulk_commit();
             committed = true;
           }
-          for (std::uint32_t k = bulk; k < piece; ++k)
-            reinterpret_cast<std::uint8_t*>(dstp)[k] = slot[k];
+          for (std::uint32_t kk = bulk; kk < piece; ++kk)
+            reinterpret_cast<std::uint8_t*>(dstp)[kk] = slot[kk];
         }
 #pragma unroll 4
-        for (int k = 0; k < stripes; ++k) {
-          const uint4 a = *reinterpret_cast<const uint4*>(slot + 32 * k);
-          const uint4 q = *reinterpret_cast<const uint4*>(slot + 32 * k + 16);
+        for (int kk = 0; kk < stripes; ++kk) {
+          const uint4 a = *reinterpret_cast<const uint4*>(slot + 32 * kk);
+          const uint4 q = *reinterpret_cast<const uint4*>(slot + 32 * kk + 16);
           v1 = xround(v1, (std::uint64_t(a.y) << 32) | a.x);
           v2 = xround(v2, (std::uint64_t(a.w) << 32) | a.z);
           v3 = xround(v3, (std::uint64_t(q.y) << 32) | q.x);
@@ -367,16 +384,15 @@ __global__ void __launch_bounds__(64, C::kCtas) pull_tma_kernel(const PullParams
       if (!last) continue;
       // 5) batch complete: verify and record
       const std::uint32_t c = b * kBatchChunks + lane;
-      bool lane_ok = clen == 0 || p.src_digests == nullptr || digest == expect;
+      const ItemDesc* dseg = clen ? &items[find_item(items, p.n_items, c)] : nullptr;
+      const bool verify = dseg && p.srcs[dseg->src_id].digests != nullptr;
+      bool lane_ok = !verify || digest == expect;
       if (__ballot_sync(full, !lane_ok)) {
         if (lane == 0) atomicAdd(&p.status->retried_batches, 1u);
         bulk_wait<0>();  // earlier stores of these chunks must not land after the re-pull
         if (!lane_ok) {
-          const ItemDesc d = items[find_item(items, p.n_items, c)];
-          const std::uint64_t off = std::uint64_t(c - d.chunk0) * (d.chunk_len & kChunkLenMask);
-          digest = repull_chunk(reinterpret_cast<const std::uint8_t*>(d.src) + off,
-                                d.dst ? reinterpret_cast<std::uint8_t*>(d.dst) + off : nullptr,
-                                clen);
+          const ChunkRef rr = chunk_ref(*dseg, c - dseg->chunk0);
+          digest = repull_chunk(rr.src, rr.dst, clen);
           lane_ok = digest == expect;
         }
         const unsigned bad = __ballot_sync(full, !lane_ok);
@@ -421,10 +437,10 @@ cudaError_t launch_variant(const PullParams& p, int sms, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-using V0 = Cfg<512, 3, 3, 512>;
+using V0 = Cfg<512, 3, 3, 320>;
 using V1 = Cfg<512, 4, 2, 576>;
-using V2 = Cfg<1024, 3, 2, 256>;
-using V3 = Cfg<256, 6, 3, 256>;
+using V2 = Cfg<1024, 3, 2, 192>;
+using V3 = Cfg<256, 6, 3, 192>;
 
 int variant() {
   static const int v = [] {

@@ -1,5 +1,5 @@
-// Host side of a pull launch: item table + TMA tensor maps + work/status
-// words, uploaded in one H2D copy.
+// Host side of a pull launch: segment table + source table + TMA tensor maps
+// + work/status words, uploaded in one H2D copy.
 #include <cuda.h>
 #include <cuda_runtime.h>
 
@@ -31,16 +31,27 @@ EncodeTiledFn encode_fn() {
   return fn;
 }
 
-// [rows][chunk_len] byte tensor at `base`, box 128 B x 32 rows, 128B swizzle.
-bool encode(CUtensorMap* m, std::uint64_t base, std::uint64_t chunk_len, std::uint64_t rows) {
+// 2-D [rows][c] or 3-D [rows][q][c] (row stride m*c) byte tensor at `base`;
+// box 128 B x 32 chunks, 128B swizzle.
+bool encode(CUtensorMap* map, std::uint64_t base, std::uint64_t c, std::uint64_t q,
+            std::uint64_t m, std::uint64_t rows) {
   auto fn = encode_fn();
   if (!fn) return false;
-  cuuint64_t dims[2] = {chunk_len, rows};
-  cuuint64_t strides[1] = {chunk_len};
-  cuuint32_t box[2] = {static_cast<cuuint32_t>(kMapBoxCols), 32};
-  cuuint32_t estr[2] = {1, 1};
-  return fn(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, reinterpret_cast<void*>(base), dims, strides, box,
-            estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+  cuuint32_t estr[3] = {1, 1, 1};
+  if (q == m) {
+    cuuint64_t dims[2] = {c, rows};
+    cuuint64_t strides[1] = {c};
+    cuuint32_t box[2] = {static_cast<cuuint32_t>(kMapBoxCols), 32};
+    return fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, reinterpret_cast<void*>(base), dims, strides,
+              box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+  }
+  cuuint64_t dims[3] = {c, q, rows};
+  cuuint64_t strides[2] = {c, m * c};
+  cuuint32_t box[3] = {static_cast<cuuint32_t>(kMapBoxCols), static_cast<cuuint32_t>(q),
+                       static_cast<cuuint32_t>(32 / q)};
+  return fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, reinterpret_cast<void*>(base), dims, strides,
+            box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
@@ -54,9 +65,11 @@ bool maps_disabled() {
 }  // namespace
 
 cudaError_t upload_pull_plan(int device, cudaStream_t s, ItemDesc* items, std::uint32_t n,
-                             PlanUpload* up, PullParams* p) {
+                             const SrcDesc* srcs, std::uint32_t n_srcs, PlanUpload* up,
+                             PullParams* p) {
   const std::size_t items_off = kHdr;
-  const std::size_t maps_off = (items_off + n * sizeof(ItemDesc) + 255) / 256 * 256;
+  const std::size_t srcs_off = items_off + n * sizeof(ItemDesc);
+  const std::size_t maps_off = (srcs_off + n_srcs * sizeof(SrcDesc) + 255) / 256 * 256;
   const std::size_t total = maps_off + std::size_t(n) * 256;
   if (up->scratch_bytes < total) {
     if (up->scratch) cudaFree(up->scratch);
@@ -70,25 +83,28 @@ cudaError_t upload_pull_plan(int device, cudaStream_t s, ItemDesc* items, std::u
   bool any_map = false;
   for (std::uint32_t i = 0; i < n; ++i) {
     ItemDesc& d = items[i];
-    const std::uint64_t cl = d.chunk_len & kChunkLenMask;
-    d.chunk_len = static_cast<std::uint32_t>(cl);
-    const std::uint64_t rows = cl ? d.len / cl : 0;
-    const bool aligned = (d.src % 16 == 0) && (d.dst % 16 == 0) && cl % kMapBoxCols == 0 &&
-                         cl % 16 == 0;
-    if (aligned && rows >= 32 && d.src && !maps_disabled()) {
-      auto* m = reinterpret_cast<CUtensorMap*>(host.data() + maps_off + 256 * std::size_t(i));
-      bool ok = encode(m, d.src, cl, rows);
-      if (ok && d.dst) ok = encode(m + 1, d.dst, cl, rows);
-      if (ok) {
-        d.chunk_len |= kHasMap;
-        any_map = true;
-      }
+    const std::uint64_t c = d.chunk_len & kChunkLenMask;
+    d.chunk_len = static_cast<std::uint32_t>(c);
+    if (d.q == 0) d.q = 1;
+    if (d.m == 0) d.m = d.q;
+    const std::uint64_t q = d.q, m = d.m;
+    const std::uint64_t full = c ? d.len / c : 0;  // whole chunks in the segment
+    bool ok = !maps_disabled() && d.src && c % kMapBoxCols == 0 && d.src % 16 == 0 &&
+              d.dst % 16 == 0 && full >= 32 && (32 % q) == 0 && (full % q) == 0;
+    if (ok) {
+      auto* mp = reinterpret_cast<CUtensorMap*>(host.data() + maps_off + 256 * std::size_t(i));
+      ok = encode(mp, d.src, c, q, m, full / q);
+      if (ok && d.dst) ok = encode(mp + 1, d.dst, c, 1, 1, full);
+    }
+    if (ok) {
+      d.chunk_len |= kHasMap | (q < m ? kMap3D : 0u);
+      any_map = true;
     }
   }
   std::memcpy(host.data() + items_off, items, n * sizeof(ItemDesc));
+  if (n_srcs) std::memcpy(host.data() + srcs_off, srcs, n_srcs * sizeof(SrcDesc));
   auto* base = static_cast<std::uint8_t*>(up->scratch);
-  // Only the header, the item table and (if any) the maps travel.
-  const std::size_t bytes = any_map ? total : items_off + n * sizeof(ItemDesc);
+  const std::size_t bytes = any_map ? total : srcs_off + n_srcs * sizeof(SrcDesc);
   cudaError_t e = cudaMemcpyAsync(base, host.data(), bytes, cudaMemcpyHostToDevice, s);
   if (e != cudaSuccess) return e;
   up->h2d_bytes = bytes;
@@ -96,7 +112,10 @@ cudaError_t upload_pull_plan(int device, cudaStream_t s, ItemDesc* items, std::u
   p->status = reinterpret_cast<PullStatus*>(base + 64);
   p->items = reinterpret_cast<const ItemDesc*>(base + items_off);
   p->n_items = n;
+  p->srcs = reinterpret_cast<const SrcDesc*>(base + srcs_off);
+  p->n_srcs = n_srcs;
   p->maps = any_map ? base + maps_off : nullptr;
+  (void)device;
   return cudaSuccess;
 }
 
