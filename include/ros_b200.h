@@ -40,6 +40,7 @@ typedef struct {
   int checksum_retries;    /* failure reports per fill before giving up (default 3) */
   double pull_timeout_s;   /* upstream silence before a failure report (default 4)  */
   char datacenter[32];     /* ClientConfig.datacenter (default "dc0")                */
+  uint32_t reshard_align;  /* chunk rule: TP splits up to this stay chunk aligned (2) */
 } rs_config;
 
 /* Assignment (reference messages.hpp:40-52) minus the manifest bytes, which
@@ -101,6 +102,19 @@ int rs_open(rs_cluster* c, const char* model, const char* replica, uint32_t num_
 /* register_tensor (client_core.hpp:72-73): dev_ptr is caller-owned device
  * memory that must outlive the handle (weights live in place). */
 int rs_register(rs_handle* h, uint32_t shard, const char* name, void* dev_ptr, uint64_t bytes);
+/* NEW (no reference counterpart): register a region that holds the slice
+ * [r0, r0+nr) x [c0, c0+nc) (byte columns) of the logical tensor `name` of
+ * shape [rows x row_bytes], densely (bytes == nr * nc).  Replicas whose
+ * slicing differs reshard on pull (TP/FSDP gather and split). */
+int rs_register_slice(rs_handle* h, uint32_t shard, const char* name, void* dev_ptr,
+                      uint64_t bytes, uint64_t rows, uint64_t row_bytes, uint64_t r0, uint64_t nr,
+                      uint64_t c0, uint64_t nc);
+/* The chunk length a region of geometry (row_bytes, slice width nc) is cut
+ * into: the largest multiple of 128 <= chunk_bytes dividing
+ * gcd(nc, row_bytes / align) (chunk_bytes when none). */
+uint32_t rs_chunk_len_for(uint64_t row_bytes, uint64_t nc, uint64_t chunk_bytes, uint32_t align);
+/* Slicing key of the replica ("" when no region has a geometry). */
+int rs_layout_key(rs_handle* h, char* buf, size_t cap, size_t* len);
 int rs_set_endpoint(rs_handle* h, uint32_t shard, const char* endpoint);
 /* Launch the shard's device work on this cudaStream_t (default: a private
  * non-blocking stream). */
@@ -124,15 +138,30 @@ int rs_stats_get(rs_handle* h, rs_stats* out);
 int rs_manifest(rs_handle* h, uint32_t shard, char* buf, size_t cap, size_t* len);
 /* The shard's per-chunk XXH64 table (device path integrity metadata). */
 int rs_chunk_digests(rs_handle* h, uint32_t shard, uint64_t* out, size_t cap, size_t* n);
+/* The shard's layout blob (entry geometries + per-item chunk lengths). */
+int rs_layout(rs_handle* h, uint32_t shard, char* buf, size_t cap, size_t* len);
+/* 1 if the bound fill reshards (its manifest/layout are derived), else 0. */
+int rs_transfer_derived(rs_handle* h);
+/* The replica's own-slicing derived manifest (what=0) or layout (what=1) of
+ * `shard`, computed from its registrations; len 0 for a plain replica. */
+int rs_derived(rs_handle* h, uint32_t shard, int what, char* buf, size_t cap, size_t* len);
 /* Drop the landed watermark so the next fill re-pulls every byte. */
 int rs_invalidate(rs_handle* h);
 
 /* ---- split phase: the caller drives the registry (replicated across
  *      processes: every rank applies the same rs_server_* sequence) ------- */
+/* derived_*: the replica's own-slicing manifests/layouts (rs_derived; NULL
+ * for a plain replica). */
 int rs_server_open(rs_cluster* c, const char* model, const char* replica, uint32_t num_shards,
-                   const char* datacenter, const char* const* endpoints);
+                   const char* datacenter, const char* const* endpoints, const char* layout_key,
+                   const char* const* derived_manifests, const size_t* dm_lens,
+                   const char* const* derived_layouts, const size_t* dl_lens);
 int rs_server_publish(rs_cluster* c, const char* model, const char* replica, uint64_t version,
-                      uint32_t num_shards, const char* const* manifests, const size_t* lens);
+                      uint32_t num_shards, const char* const* manifests, const size_t* lens,
+                      const char* const* layouts, const size_t* layout_lens);
+int rs_server_add_layout(rs_cluster* c, const char* model, uint64_t version, const char* layout_key,
+                         uint32_t num_shards, const char* const* manifests, const size_t* lens,
+                         const char* const* layouts, const size_t* layout_lens);
 int rs_server_unpublish(rs_cluster* c, const char* model, const char* replica);
 int rs_server_replicate(rs_cluster* c, const char* model, const char* replica, const char* spec);
 int rs_server_update(rs_cluster* c, const char* model, const char* replica, const char* spec,

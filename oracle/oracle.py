@@ -53,6 +53,8 @@ def port():
         lib.ro_manifest_encode.argtypes = [C.c_size_t, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                                            C.c_void_p, C.c_int, C.c_void_p, C.c_void_p]
         lib.ro_bf16_to_e4m3.argtypes = [C.c_void_p, C.c_size_t, C.c_void_p]
+        lib.ro_chunk_len_for.restype = C.c_uint32
+        lib.ro_chunk_len_for.argtypes = [C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint32]
         _port = lib
     return _port
 
@@ -177,6 +179,25 @@ def publish_manifest(names, arrays, tiny=2 << 20, target=64 << 20) -> bytes:
         staging = np.concatenate([arrs[e] for e in range(len(arrs)) if g[e] == k])
         gds.append(xxh64(staging))
     return manifest_encode(names, lens, digests, g, off, ng, gds)
+
+
+def chunk_len_for(row_bytes: int, nc: int, chunk_bytes: int = 4096, align: int = 2) -> int:
+    """The reshard chunk rule (ros_oracle.h ro_chunk_len_for)."""
+    return int(port().ro_chunk_len_for(row_bytes, nc, chunk_bytes, align))
+
+
+def slice_bytes(full: np.ndarray, geometry) -> np.ndarray:
+    """Bytes a region with geometry (rows, row_bytes, r0, nr, c0, nc) holds,
+    cut from the logical tensor's bytes `full` (row-major)."""
+    rows, w, r0, nr, c0, nc = geometry
+    b = np.ascontiguousarray(full).view(np.uint8).reshape(rows, w)
+    return np.ascontiguousarray(b[r0:r0 + nr, c0:c0 + nc]).reshape(-1)
+
+
+def chunk_digests_lens(items: list[np.ndarray], lens: list[int]) -> np.ndarray:
+    """Chunk digests with a chunk length per item (concatenated, item order)."""
+    out = [chunk_digests([a], int(l)) for a, l in zip(items, lens)]
+    return np.concatenate(out) if out else np.zeros(0, np.uint64)
 
 
 def bf16_to_e4m3(x: np.ndarray) -> np.ndarray:

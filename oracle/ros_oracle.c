@@ -210,6 +210,25 @@ size_t ro_manifest_encode(size_t n, const char* const* names,
   return b.n;
 }
 
+/* ------------------------------------------------------ reshard chunks -- */
+static uint64_t gcd64(uint64_t a, uint64_t b) {
+  while (b) {
+    uint64_t t = a % b;
+    a = b;
+    b = t;
+  }
+  return a;
+}
+
+uint32_t ro_chunk_len_for(uint64_t row_bytes, uint64_t nc, uint64_t chunk_bytes, uint32_t align) {
+  if (row_bytes == 0 || align == 0 || row_bytes % align || nc == 0) return (uint32_t)chunk_bytes;
+  uint64_t g = gcd64(nc, row_bytes / align);
+  uint64_t start = (chunk_bytes < g ? chunk_bytes : g) / 128 * 128;
+  for (uint64_t c = start; c >= 128; c -= 128)
+    if (g % c == 0) return (uint32_t)c;
+  return (uint32_t)chunk_bytes;
+}
+
 /* -------------------------------------------------------- bf16 -> e4m3 -- */
 void ro_bf16_to_e4m3(const uint16_t* in, size_t n, uint8_t* out) {
   for (size_t i = 0; i < n; ++i) {

@@ -55,6 +55,13 @@ size_t ro_manifest_encode(size_t n, const char* const* names,
                           int n_groups, const uint64_t* group_digests,
                           uint8_t* out);
 
+/* Reshard chunk rule (NEW, pinned here): for a region holding nc bytes of
+ * every row of a logical tensor with row_bytes bytes per row, the chunk
+ * length is the largest multiple of 128 that is <= chunk_bytes and divides
+ * gcd(nc, row_bytes / align); chunk_bytes when row_bytes % align != 0 or no
+ * such multiple exists, or the region has no geometry (row_bytes == 0). */
+uint32_t ro_chunk_len_for(uint64_t row_bytes, uint64_t nc, uint64_t chunk_bytes, uint32_t align);
+
 /* bf16 -> fp8 e4m3fn, round-to-nearest-even, saturating to +-448, NaN ->
  * 0x7F (NEW: the reference has no cast; this is the pinned definition). */
 void ro_bf16_to_e4m3(const uint16_t* in, size_t n, uint8_t* out);

@@ -25,7 +25,7 @@ cstr = C.c_char_p
 class RsConfig(C.Structure):
     _fields_ = [("chunk_bytes", u64), ("tiny_threshold", u64), ("group_target", u64),
                 ("pipeline", i32), ("checksum_retries", i32), ("pull_timeout_s", dbl),
-                ("datacenter", C.c_char * 32)]
+                ("datacenter", C.c_char * 32), ("reshard_align", u32)]
 
 
 class RsAssignment(C.Structure):
@@ -55,6 +55,11 @@ _SIGS = {
     "rs_cluster_source": (i32, [vp, cstr, cstr, vp, sz, C.POINTER(sz)]),
     "rs_open": (i32, [vp, cstr, cstr, u32, C.POINTER(RsConfig), C.POINTER(vp)]),
     "rs_register": (i32, [vp, u32, cstr, vp, u64]),
+    "rs_register_slice": (i32, [vp, u32, cstr, vp, u64, u64, u64, u64, u64, u64, u64]),
+    "rs_layout_key": (i32, [vp, vp, sz, C.POINTER(sz)]),
+    "rs_chunk_len_for": (u32, [u64, u64, u64, u32]),
+    "rs_layout": (i32, [vp, u32, vp, sz, C.POINTER(sz)]),
+    "rs_transfer_derived": (i32, [vp]),
     "rs_set_endpoint": (i32, [vp, u32, cstr]),
     "rs_set_stream": (i32, [vp, u32, vp]),
     "rs_publish": (i32, [vp, u64]),
@@ -69,8 +74,10 @@ _SIGS = {
     "rs_manifest": (i32, [vp, u32, vp, sz, C.POINTER(sz)]),
     "rs_chunk_digests": (i32, [vp, u32, vp, sz, C.POINTER(sz)]),
     "rs_invalidate": (i32, [vp]),
-    "rs_server_open": (i32, [vp, cstr, cstr, u32, cstr, vp]),
-    "rs_server_publish": (i32, [vp, cstr, cstr, u64, u32, vp, vp]),
+    "rs_server_open": (i32, [vp, cstr, cstr, u32, cstr, vp, cstr, vp, vp, vp, vp]),
+    "rs_derived": (i32, [vp, u32, i32, vp, sz, C.POINTER(sz)]),
+    "rs_server_publish": (i32, [vp, cstr, cstr, u64, u32, vp, vp, vp, vp]),
+    "rs_server_add_layout": (i32, [vp, cstr, u64, cstr, u32, vp, vp, vp, vp]),
     "rs_server_unpublish": (i32, [vp, cstr, cstr]),
     "rs_server_replicate": (i32, [vp, cstr, cstr, cstr]),
     "rs_server_update": (i32, [vp, cstr, cstr, cstr, i32, u64]),

@@ -44,10 +44,10 @@ def run(args):
     arena, views = B.alloc_replica(shapes, dev, seed_base=42 if is_trainer else None)
     torch.cuda.synchronize()
     name = (f"trainer{rank}" if pairs else "trainer") if is_trainer else f"rollout{rank}"
-    h = dc.open("m", name, 1, endpoints=[f"rank{rank}:cuda{local}"], chunk_bytes=args.chunk,
-                pull_timeout_s=30.0)
+    h = dc.create("m", name, 1, chunk_bytes=args.chunk, pull_timeout_s=30.0)
     for n, v in views:
         assert h.register_tensor(0, n, v) == Status.ok
+    dc.open(h, endpoints=[f"rank{rank}:cuda{local}"])
     stream = torch.cuda.Stream(device=dev)
     h.set_stream(0, stream)
     t0 = time.perf_counter()

@@ -56,6 +56,7 @@ rsb::ClientConfig to_cfg(const rs_config* c) {
   cfg.checksum_retries = c->checksum_retries;
   if (c->pull_timeout_s > 0) cfg.pull_timeout_s = c->pull_timeout_s;
   if (c->datacenter[0]) cfg.dc = std::string(c->datacenter, strnlen(c->datacenter, 32));
+  if (c->reshard_align) cfg.reshard_align = c->reshard_align;
   return cfg;
 }
 
@@ -104,6 +105,7 @@ void rs_config_default(rs_config* cfg) {
   cfg->checksum_retries = d.checksum_retries;
   cfg->pull_timeout_s = d.pull_timeout_s;
   std::strncpy(cfg->datacenter, d.dc.c_str(), sizeof(cfg->datacenter) - 1);
+  cfg->reshard_align = d.reshard_align;
 }
 
 int rs_cluster_create(int pipeline, int smart_skipping, rs_cluster** out) {
@@ -181,6 +183,38 @@ int rs_open(rs_cluster* c, const char* model, const char* replica, uint32_t num_
 int rs_register(rs_handle* h, uint32_t shard, const char* name, void* dev_ptr, uint64_t bytes) {
   if (!h || !name) return st(rsb::Status::invalid_argument);
   return st(h->client->register_tensor(shard, name, dev_ptr, bytes));
+}
+
+int rs_register_slice(rs_handle* h, uint32_t shard, const char* name, void* dev_ptr,
+                      uint64_t bytes, uint64_t rows, uint64_t row_bytes, uint64_t r0, uint64_t nr,
+                      uint64_t c0, uint64_t nc) {
+  if (!h || !name || rows == 0) return st(rsb::Status::invalid_argument);
+  rsb::Geometry g{rows, row_bytes, r0, nr, c0, nc};
+  return st(h->client->register_tensor(shard, name, dev_ptr, bytes, g));
+}
+
+uint32_t rs_chunk_len_for(uint64_t row_bytes, uint64_t nc, uint64_t chunk_bytes, uint32_t align) {
+  rsb::Geometry g{1, row_bytes, 0, 1, 0, nc};
+  if (row_bytes == 0) g.rows = 0;
+  return rsb::chunk_len_for(g, chunk_bytes, align);
+}
+
+int rs_layout_key(rs_handle* h, char* buf, size_t cap, size_t* len) {
+  if (!h) return st(rsb::Status::invalid_argument);
+  return put_bytes(h->client->layout_key(), buf, cap, len);
+}
+
+int rs_layout(rs_handle* h, uint32_t shard, char* buf, size_t cap, size_t* len) {
+  if (!h) return st(rsb::Status::invalid_argument);
+  auto m = h->client->layout_bytes(shard);
+  if (!m) return st(m.status());
+  return put_bytes(*m, buf, cap, len);
+}
+
+int rs_transfer_derived(rs_handle* h) {
+  if (!h) return 0;
+  std::vector<std::string> m, l;
+  return h->client->derived_layout(&m, &l) ? 1 : 0;
 }
 
 int rs_set_endpoint(rs_handle* h, uint32_t shard, const char* endpoint) {
@@ -300,22 +334,53 @@ int rs_invalidate(rs_handle* h) {
 
 // ------------------------------------------------------------ split phase
 
+namespace {
+std::vector<std::string> blobs(uint32_t n, const char* const* p, const size_t* lens) {
+  std::vector<std::string> out;
+  if (!p || !lens) return out;
+  for (uint32_t i = 0; i < n; ++i) out.emplace_back(p[i] ? std::string(p[i], lens[i]) : std::string());
+  return out;
+}
+}  // namespace
+
 int rs_server_open(rs_cluster* c, const char* model, const char* replica, uint32_t num_shards,
-                   const char* datacenter, const char* const* endpoints) {
+                   const char* datacenter, const char* const* endpoints, const char* layout_key,
+                   const char* const* derived_manifests, const size_t* dm_lens,
+                   const char* const* derived_layouts, const size_t* dl_lens) {
   if (!c || !model || !replica || !endpoints) return st(rsb::Status::invalid_argument);
   std::vector<std::string> eps;
   for (uint32_t i = 0; i < num_shards; ++i) eps.emplace_back(endpoints[i] ? endpoints[i] : "");
-  return st(c->reg.open(model, replica, num_shards, datacenter ? datacenter : "dc0", eps));
+  return st(c->reg.open(model, replica, num_shards, datacenter ? datacenter : "dc0", eps,
+                        layout_key ? layout_key : "",
+                        blobs(num_shards, derived_manifests, dm_lens),
+                        blobs(num_shards, derived_layouts, dl_lens)));
+}
+
+int rs_derived(rs_handle* h, uint32_t shard, int what, char* buf, size_t cap, size_t* len) {
+  if (!h || shard >= h->client->num_shards()) return st(rsb::Status::invalid_argument);
+  std::vector<std::string> m, l;
+  if (auto s = h->client->derived_blobs(&m, &l); !rsb::ok(s)) return st(s);
+  const std::string empty;
+  const std::string& b = m.empty() ? empty : (what == 0 ? m[shard] : l[shard]);
+  return put_bytes(b, buf, cap, len);
 }
 
 int rs_server_publish(rs_cluster* c, const char* model, const char* replica, uint64_t version,
-                      uint32_t num_shards, const char* const* manifests, const size_t* lens) {
+                      uint32_t num_shards, const char* const* manifests, const size_t* lens,
+                      const char* const* layouts, const size_t* layout_lens) {
   if (!c || !model || !replica || !manifests || !lens) return st(rsb::Status::invalid_argument);
-  std::vector<std::string> ms;
-  for (uint32_t i = 0; i < num_shards; ++i) ms.emplace_back(manifests[i], lens[i]);
   rsb::OpOutcome o;
-  auto s = c->reg.publish(model, replica, version, ms, &o);
+  auto s = c->reg.publish(model, replica, version, blobs(num_shards, manifests, lens), &o,
+                          blobs(num_shards, layouts, layout_lens));
   return st(rsb::ok(s) ? o.status : s);
+}
+
+int rs_server_add_layout(rs_cluster* c, const char* model, uint64_t version, const char* layout_key,
+                         uint32_t num_shards, const char* const* manifests, const size_t* lens,
+                         const char* const* layouts, const size_t* layout_lens) {
+  if (!c || !model || !layout_key || !manifests || !lens) return st(rsb::Status::invalid_argument);
+  return st(c->reg.add_layout(model, version, layout_key, blobs(num_shards, manifests, lens),
+                              blobs(num_shards, layouts, layout_lens)));
 }
 
 int rs_server_unpublish(rs_cluster* c, const char* model, const char* replica) {

@@ -156,12 +156,19 @@ Status DevBuf::alloc(int device, std::size_t bytes) {
 // ---------------------------------------------------------------- ChunkMap
 
 ChunkMap ChunkMap::uniform(const Manifest& m, std::uint64_t chunk_bytes) {
+  return from_lens(m, std::vector<std::uint32_t>(m.items().size(),
+                                                 static_cast<std::uint32_t>(chunk_bytes)));
+}
+
+ChunkMap ChunkMap::from_lens(const Manifest& m, const std::vector<std::uint32_t>& lens) {
   ChunkMap c;
   std::uint32_t next = 0;
-  for (const auto& it : m.items()) {
-    const auto n = static_cast<std::uint32_t>((it.length + chunk_bytes - 1) / chunk_bytes);
+  const auto& items = m.items();
+  for (std::size_t i = 0; i < items.size(); ++i) {
+    const std::uint64_t cl = i < lens.size() && lens[i] ? lens[i] : 4096;
+    const auto n = static_cast<std::uint32_t>((items[i].length + cl - 1) / cl);
     c.chunk0.push_back(next);
-    c.chunk_len.push_back(static_cast<std::uint32_t>(chunk_bytes));
+    c.chunk_len.push_back(static_cast<std::uint32_t>(cl));
     c.count.push_back(n);
     next += (n + dev::kBatchChunks - 1) / dev::kBatchChunks * dev::kBatchChunks;
   }
@@ -394,8 +401,11 @@ Client::~Client() {
 }
 
 Status Client::register_tensor(std::uint32_t shard, const std::string& name, void* ptr,
-                               std::uint64_t len) {
+                               std::uint64_t len, const Geometry& geo) {
   if (shard >= num_shards_ || name.empty() || !ptr || len == 0) return Status::invalid_argument;
+  if (geo.has() && (geo.nr * geo.nc != len || geo.r0 + geo.nr > geo.rows ||
+                    geo.c0 + geo.nc > geo.row_bytes))
+    return Status::invalid_argument;
   Shard& sh = shards_[shard];
   if (sh.by_name.count(name)) return Status::already_exists;
   if (published_ || current_) return Status::invalid_state;
@@ -408,8 +418,33 @@ Status Client::register_tensor(std::uint32_t shard, const std::string& name, voi
   if (sh.device != attr.device) return Status::invalid_argument;  // one device per shard
   if (sh.endpoint.empty()) sh.endpoint = "cuda:" + std::to_string(sh.device);
   sh.by_name[name] = static_cast<std::uint32_t>(sh.regs.size());
-  sh.regs.push_back({name, static_cast<std::uint8_t*>(ptr), len});
+  sh.regs.push_back({name, static_cast<std::uint8_t*>(ptr), len, geo});
   return Status::ok;
+}
+
+std::string Client::layout_key() const {
+  // FNV-1a over (shard, name, length, geometry) of every region; plain
+  // replicas (no geometry anywhere) keep the reference's single slicing "".
+  bool any = false;
+  std::uint64_t h = 1469598103934665603ull;
+  auto mix = [&](const void* p, std::size_t n) {
+    const auto* b = static_cast<const unsigned char*>(p);
+    for (std::size_t i = 0; i < n; ++i) h = (h ^ b[i]) * 1099511628211ull;
+  };
+  for (const auto& sh : shards_) {
+    mix(&sh.idx, sizeof(sh.idx));
+    for (const auto& r : sh.regs) {
+      any |= r.geo.has();
+      mix(r.name.data(), r.name.size());
+      const std::uint64_t v[7] = {r.len, r.geo.rows, r.geo.row_bytes, r.geo.r0,
+                                  r.geo.nr, r.geo.c0, r.geo.nc};
+      mix(v, sizeof(v));
+    }
+  }
+  if (!any) return "";
+  char buf[32];
+  std::snprintf(buf, sizeof(buf), "L%016llx", static_cast<unsigned long long>(h));
+  return buf;
 }
 
 void Client::set_shard_endpoint(std::uint32_t shard, std::string ep) {
@@ -445,7 +480,9 @@ Status Client::open() {
     if (sh.device < 0) return Status::invalid_state;  // nothing registered on a shard
     eps.push_back(sh.endpoint);
   }
-  Status s = reg_->open(model_, replica_, num_shards_, cfg_.dc, eps);
+  std::vector<std::string> dman, dlay;
+  if (Status s = derived_blobs(&dman, &dlay); !ok(s)) return s;
+  Status s = reg_->open(model_, replica_, num_shards_, cfg_.dc, eps, layout_key(), dman, dlay);
   if (ok(s)) opened_ = true;
   return s;
 }
@@ -527,33 +564,19 @@ Status Client::build_payload(Shard& sh, VersionId v, std::shared_ptr<Payload>* o
     p->item_ptrs[i] = items[i].is_group
                           ? reinterpret_cast<std::uint64_t>(p->group_bufs[items[i].index]->p)
                           : ptrs[items[i].index];
-  p->cmap = ChunkMap::uniform(p->manifest, cfg_.chunk_bytes);
-  const std::uint32_t nc = p->cmap.n_chunks(), nb = p->cmap.n_batches();
-  if (Status s = p->digests.alloc(sh.device, std::size_t(nc) * 8); !ok(s)) return s;
-  if (Status s = p->flags.alloc(sh.device, std::size_t(nb) * 4); !ok(s)) return s;
-  RS_CUDA(cudaMemsetAsync(p->flags.p, 0, std::size_t(nb) * 4, sh.stream));
-  RS_CUDA(cudaMemsetAsync(p->digests.p, 0, std::size_t(nc) * 8, sh.stream));
+  // Chunk lengths from the regions' geometry (layout.hpp chunk rule).
+  ShardLayout lay;
+  for (const auto& r : sh.regs) lay.geo.push_back(r.geo);
+  lay.chunk_len = item_chunk_lens(p->manifest, lay.geo, cfg_.chunk_bytes, cfg_.reshard_align);
+  p->cmap = ChunkMap::from_lens(p->manifest, lay.chunk_len);
+  p->layout = lay.encode();
+  if (Status s = alloc_tables(sh, *p, 0); !ok(s)) return s;
   p->epoch = ++sh.epoch_ctr;
-  if (nc) {
-    // Chunk digest table of the published bytes (hash-only pull), and every
-    // watermark set: a complete source.
-    std::vector<dev::ItemDesc> descs(items.size());
-    for (std::size_t i = 0; i < items.size(); ++i)
-      descs[i] = identity_segment(p->item_ptrs[i], 0, items[i].length, p->cmap, i);
-    const dev::SrcDesc self{nullptr, nullptr, 0, 0};
-    dev::PullParams pp{};
-    RS_CUDA(dev::upload_pull_plan(sh.device, sh.stream, descs.data(),
-                                  static_cast<std::uint32_t>(descs.size()), &self, 1, &sh.plan,
-                                  &pp));
-    pp.n_chunks = nc;
-    pp.n_batches = nb;
-    pp.dst_digests = static_cast<std::uint64_t*>(p->digests.p);
-    pp.dst_flags = static_cast<std::uint32_t*>(p->flags.p);
-    pp.dst_epoch = p->epoch;
-    pp.timeout_ns = static_cast<std::uint64_t>(cfg_.pull_timeout_s * 1e9);
-    RS_CUDA(dev::launch_pull(pp, dev::pull_grid(sh.device), sh.stream));
-    stats_.h2d_bytes += sh.plan.h2d_bytes;
-  }
+  // Chunk digest table of the published bytes (hash-only pull), and every
+  // watermark set: a complete source.
+  std::vector<std::uint32_t> all(items.size());
+  for (std::size_t i = 0; i < items.size(); ++i) all[i] = static_cast<std::uint32_t>(i);
+  if (Status s = hash_items(sh, *p, all); !ok(s)) return s;
   RS_CUDA(cudaEventRecord(sh.ev1, sh.stream));
   RS_CUDA(cudaStreamSynchronize(sh.stream));
   float ms = 0;
@@ -564,15 +587,71 @@ Status Client::build_payload(Shard& sh, VersionId v, std::shared_ptr<Payload>* o
   return Status::ok;
 }
 
-Status Client::prepare_publish(VersionId v, std::vector<std::string>* manifests) {
+Status Client::alloc_tables(Shard& sh, Payload& p, std::uint32_t extra_chunks) {
+  DeviceGuard g(sh.device);
+  const std::uint32_t nc = p.cmap.n_chunks() + extra_chunks;
+  const std::uint32_t nb = (nc + dev::kBatchChunks - 1) / dev::kBatchChunks;
+  if (Status s = p.digests.alloc(sh.device, std::size_t(nc) * 8); !ok(s)) return s;
+  if (Status s = p.flags.alloc(sh.device, std::size_t(nb) * 4); !ok(s)) return s;
+  RS_CUDA(cudaMemsetAsync(p.flags.p, 0, std::size_t(nb) * 4, sh.stream));
+  RS_CUDA(cudaMemsetAsync(p.digests.p, 0, std::size_t(nc) * 8, sh.stream));
+  return Status::ok;
+}
+
+Status Client::hash_items(Shard& sh, Payload& p, const std::vector<std::uint32_t>& which) {
+  // Hash-only pull over some of the payload's own items: fills their chunk
+  // digests and releases their watermarks in the current epoch.
+  if (which.empty() || p.cmap.n_chunks() == 0) return Status::ok;
+  DeviceGuard g(sh.device);
+  const auto& items = p.manifest.items();
+  std::vector<dev::ItemDesc> descs;
+  for (std::uint32_t i : which)
+    descs.push_back(identity_segment(p.item_ptrs[i], 0, items[i].length, p.cmap, i));
+  const dev::SrcDesc self{nullptr, nullptr, 0, 0};
+  dev::PullParams pp{};
+  RS_CUDA(dev::upload_pull_plan(sh.device, sh.stream, descs.data(),
+                                static_cast<std::uint32_t>(descs.size()), &self, 1, &sh.plan, &pp));
+  pp.n_chunks = p.cmap.n_chunks();
+  pp.n_batches = p.cmap.n_batches();
+  pp.first_batch = descs.front().chunk0 / dev::kBatchChunks;
+  pp.dst_digests = static_cast<std::uint64_t*>(p.digests.p);
+  pp.dst_flags = static_cast<std::uint32_t*>(p.flags.p);
+  pp.dst_epoch = p.epoch;
+  pp.timeout_ns = static_cast<std::uint64_t>(cfg_.pull_timeout_s * 1e9);
+  RS_CUDA(dev::launch_pull(pp, dev::pull_grid(sh.device), sh.stream));
+  stats_.h2d_bytes += sh.plan.h2d_bytes;
+  return Status::ok;
+}
+
+Status Client::prepare_publish(VersionId v, std::vector<std::string>* manifests,
+                               std::vector<std::string>* layouts) {
   manifests->clear();
+  if (layouts) layouts->clear();
   for (auto& sh : shards_) {
     std::shared_ptr<Payload> p;
     if (Status s = build_payload(sh, v, &p); !ok(s)) return s;
     sh.holding = std::move(p);
     manifests->push_back(sh.holding->encoded);
+    if (layouts) layouts->push_back(sh.holding->layout);
   }
   return Status::ok;
+}
+
+bool Client::derived_layout(std::vector<std::string>* manifests,
+                            std::vector<std::string>* layouts) const {
+  manifests->clear();
+  layouts->clear();
+  for (const auto& sh : shards_) {
+    if (!sh.holding || !sh.holding->reshard) return false;
+    manifests->push_back(sh.holding->encoded);
+    layouts->push_back(sh.holding->layout);
+  }
+  return true;
+}
+
+Result<std::string> Client::layout_bytes(std::uint32_t shard) const {
+  if (shard >= num_shards_ || !shards_[shard].holding) return Status::not_found;
+  return shards_[shard].holding->layout;
 }
 
 void Client::commit_publish(VersionId v, Status st) {
@@ -590,10 +669,10 @@ Status Client::publish(VersionId v) {
     if (Status s = open(); !ok(s)) return s;
   }
   if (published_) return Status::mutability_violation;
-  std::vector<std::string> manifests;
-  if (Status s = prepare_publish(v, &manifests); !ok(s)) return s;
+  std::vector<std::string> manifests, layouts;
+  if (Status s = prepare_publish(v, &manifests, &layouts); !ok(s)) return s;
   OpOutcome o;
-  Status s = reg_->publish(model_, replica_, v, manifests, &o);
+  Status s = reg_->publish(model_, replica_, v, manifests, &o, layouts);
   if (ok(s)) s = o.status;
   commit_publish(v, s);
   return s;
@@ -709,9 +788,17 @@ Status Client::bind(Shard& sh, const Assignment& a, VersionId v) {
     p->group_bufs.push_back(std::move(buf));
   }
   const auto& items = p->manifest.items();
-  // The chunk map is a pure function of (manifest, chunk_bytes), so a reader
-  // can start serving its own fill before its source is even reachable.
-  p->cmap = ChunkMap::uniform(p->manifest, cfg_.chunk_bytes);
+  // The chunk map is a pure function of (manifest, the publisher's chunk
+  // lengths), so a reader can serve its own fill before its source is even
+  // reachable.
+  if (!a.layout.empty()) {
+    auto lay = ShardLayout::decode(a.layout);
+    if (!lay || lay->chunk_len.size() != items.size()) return Status::protocol_error;
+    p->cmap = ChunkMap::from_lens(p->manifest, lay->chunk_len);
+    p->layout = a.layout;
+  } else {
+    p->cmap = ChunkMap::uniform(p->manifest, cfg_.chunk_bytes);
+  }
   p->item_ptrs.resize(items.size());
   for (std::size_t i = 0; i < items.size(); ++i) {
     const auto& it = items[i];
@@ -720,12 +807,125 @@ Status Client::bind(Shard& sh, const Assignment& a, VersionId v) {
                     : reinterpret_cast<std::uint64_t>(
                           sh.regs[sh.by_name.at(p->manifest.entries[it.index].name)].ptr);
   }
-  const std::uint32_t nc = p->cmap.n_chunks(), nb = p->cmap.n_batches();
-  if (Status s = p->digests.alloc(sh.device, std::size_t(nc) * 8); !ok(s)) return s;
-  if (Status s = p->flags.alloc(sh.device, std::size_t(nb) * 4); !ok(s)) return s;
-  RS_CUDA(cudaMemsetAsync(p->flags.p, 0, std::size_t(nb) * 4, sh.stream));
-  RS_CUDA(cudaMemsetAsync(p->digests.p, 0, std::size_t(nc) * 8, sh.stream));
+  if (Status s = alloc_tables(sh, *p, 0); !ok(s)) return s;
   RS_CUDA(cudaStreamSynchronize(sh.stream));
+  p->epoch = ++sh.epoch_ctr;
+  sh.holding = std::move(p);
+  sh.partial_version = v;
+  return Status::ok;
+}
+
+Status Client::derive(const Shard& sh, Manifest* m, std::string* encoded, std::string* layout,
+                      std::vector<std::uint32_t>* lens) const {
+  std::vector<EntryInfo> infos;
+  for (const auto& r : sh.regs) infos.push_back({r.name, r.len, 0});
+  auto mr = assemble(infos, cfg_.limits);
+  if (!mr) return mr.status();
+  *m = std::move(*mr);
+  m->alg = kAlgDerived;
+  *encoded = m->encode();
+  ShardLayout lay;
+  for (const auto& r : sh.regs) lay.geo.push_back(r.geo);
+  lay.chunk_len = item_chunk_lens(*m, lay.geo, cfg_.chunk_bytes, cfg_.reshard_align);
+  *layout = lay.encode();
+  if (lens) *lens = lay.chunk_len;
+  return Status::ok;
+}
+
+Status Client::derived_blobs(std::vector<std::string>* manifests,
+                             std::vector<std::string>* layouts) const {
+  manifests->clear();
+  layouts->clear();
+  if (layout_key().empty()) return Status::ok;  // plain replica: nothing derived
+  for (const auto& sh : shards_) {
+    Manifest m;
+    std::string enc, lay;
+    if (Status s = derive(sh, &m, &enc, &lay, nullptr); !ok(s)) return s;
+    manifests->push_back(std::move(enc));
+    layouts->push_back(std::move(lay));
+  }
+  return Status::ok;
+}
+
+Status Client::bind_reshard(Shard& sh, const Assignment& a, VersionId v) {
+  // K4 reshard: this shard's slicing differs from the source's.  Its own
+  // manifest is derived (alg 2: same entries/groups as the reference would
+  // assemble, digests not computed); its chunks follow the chunk rule on its
+  // own geometry; the plan maps them onto the source shards' chunks.
+  if (Status s = ensure_stream(sh); !ok(s)) return s;
+  if (sh.holding && sh.holding->reshard && sh.partial_version && *sh.partial_version == v) {
+    return Status::ok;  // resume the same reshard fill
+  }
+  DeviceGuard g(sh.device);
+  auto p = std::make_shared<Payload>();
+  std::vector<std::uint32_t> lens;
+  if (Status s = derive(sh, &p->manifest, &p->encoded, &p->layout, &lens); !ok(s)) return s;
+  p->cmap = ChunkMap::from_lens(p->manifest, lens);
+  for (const auto& grp : p->manifest.groups) {
+    auto buf = std::make_unique<DevBuf>();
+    if (Status s = buf->alloc(sh.device, grp.packed_length); !ok(s)) return s;
+    p->group_bufs.push_back(std::move(buf));
+  }
+  const auto& items = p->manifest.items();
+  p->item_ptrs.resize(items.size());
+  for (std::size_t i = 0; i < items.size(); ++i)
+    p->item_ptrs[i] = items[i].is_group
+                          ? reinterpret_cast<std::uint64_t>(p->group_bufs[items[i].index]->p)
+                          : reinterpret_cast<std::uint64_t>(sh.regs[items[i].index].ptr);
+  // Source shards as the planner sees them.
+  auto rs = std::make_unique<Reshard>();
+  rs->endpoints = a.all_endpoints;
+  for (std::size_t s = 0; s < a.all_manifests.size(); ++s) {
+    SourceShard ss;
+    auto sm = Manifest::decode(a.all_manifests[s]);
+    if (!sm) return Status::protocol_error;
+    ss.manifest = std::move(*sm);
+    if (s < a.all_layouts.size() && !a.all_layouts[s].empty()) {
+      auto sl = ShardLayout::decode(a.all_layouts[s]);
+      if (!sl) return Status::protocol_error;
+      ss.layout = std::move(*sl);
+    } else {
+      ss.layout.chunk_len.assign(ss.manifest.items().size(),
+                                 static_cast<std::uint32_t>(cfg_.chunk_bytes));
+    }
+    ss.chunk0 = ChunkMap::from_lens(ss.manifest, ss.layout.chunk_len).chunk0;
+    rs->srcs.push_back(std::move(ss));
+  }
+  std::vector<ReaderEntry> rd;
+  for (std::uint32_t e = 0; e < sh.regs.size(); ++e) {
+    ReaderEntry re;
+    re.name = sh.regs[e].name;
+    re.ptr = reinterpret_cast<std::uint64_t>(sh.regs[e].ptr);
+    re.len = sh.regs[e].len;
+    re.geo = sh.regs[e].geo;
+    re.in_group = p->manifest.group_of(e) >= 0;
+    if (!re.in_group) {
+      for (std::uint32_t i = 0; i < items.size(); ++i)
+        if (!items[i].is_group && items[i].index == e) {
+          re.item = i;
+          re.chunk0 = p->cmap.chunk0[i];
+          re.chunk_len = p->cmap.chunk_len[i];
+        }
+    }
+    rd.push_back(std::move(re));
+  }
+  if (Status s = plan_reshard(rd, rs->srcs, &rs->plan); !ok(s)) return s;
+  // Gathered source items land in library staging, behind the reader's own
+  // chunk range (batch aligned), verified against the source chunk digests.
+  rs->own_chunks = p->cmap.n_chunks();
+  std::uint32_t extra = 0;
+  for (const auto& gth : rs->plan.gathers) {
+    const auto& it = rs->srcs[gth.src_shard].manifest.items()[gth.src_item];
+    auto buf = std::make_unique<DevBuf>();
+    if (Status s = buf->alloc(sh.device, it.length); !ok(s)) return s;
+    rs->gather_bufs.push_back(std::move(buf));
+    const std::uint64_t cl = rs->srcs[gth.src_shard].layout.chunk_len[gth.src_item];
+    const auto n = static_cast<std::uint32_t>((it.length + cl - 1) / cl);
+    extra += (n + dev::kBatchChunks - 1) / dev::kBatchChunks * dev::kBatchChunks;
+  }
+  if (Status s = alloc_tables(sh, *p, extra); !ok(s)) return s;
+  RS_CUDA(cudaStreamSynchronize(sh.stream));
+  p->reshard = std::move(rs);
   p->epoch = ++sh.epoch_ctr;
   sh.holding = std::move(p);
   sh.partial_version = v;
@@ -736,7 +936,8 @@ Status Client::bind_all(const std::vector<Assignment>& as, VersionId v) {
   if (as.size() != num_shards_) return Status::protocol_error;
   for (std::uint32_t i = 0; i < num_shards_; ++i) {
     if (as[i].version != v) return Status::protocol_error;
-    if (Status s = bind(shards_[i], as[i], v); !ok(s)) return s;
+    Status s = as[i].reshard ? bind_reshard(shards_[i], as[i], v) : bind(shards_[i], as[i], v);
+    if (!ok(s)) return s;
   }
   // The incoming version overwrites registered regions in place: until every
   // shard verifies, this replica holds no coherent version.
@@ -783,6 +984,16 @@ std::vector<Client::FillOutcome> Client::fill_shards(const std::vector<Assignmen
   for (std::uint32_t i : which) {
     Shard& sh = shards_[i];
     const Assignment& a = as[i];
+    if (sh.holding && sh.holding->reshard) {
+      Status s = a.reshard ? launch_reshard_fill(sh, a, a.source_complete)
+                           : Status::protocol_error;
+      if (!ok(s)) {
+        out[i] = {s, 0, 0};
+        continue;
+      }
+      launched[i] = true;
+      continue;
+    }
     SourceView view;
     Status s = resolve_source(sh, a, a.version, &view, cfg_.pull_timeout_s);
     // Every replica of a cluster digests with the same chunk size; a source
@@ -834,10 +1045,15 @@ std::vector<Client::FillOutcome> Client::fill_shards(const std::vector<Assignmen
         break;
     }
   }
-  // Unpack verified groups into their members (K3, unpack_group).
+  // Unpack verified groups into their members (K3, unpack_group); a reshard
+  // fill instead slices the gathered items and packs its own groups.
   for (std::uint32_t i : which) {
     if (!ok(out[i].status)) continue;
     Shard& sh = shards_[i];
+    if (sh.holding->reshard) {
+      if (Status s = finish_reshard(sh); !ok(s)) out[i] = {s, 0, 0};
+      continue;
+    }
     const auto& p = *sh.holding;
     std::vector<std::uint64_t> srcs, dsts, ls;
     for (std::size_t gi = 0; gi < p.manifest.groups.size(); ++gi)
@@ -847,23 +1063,148 @@ std::vector<Client::FillOutcome> Client::fill_shards(const std::vector<Assignmen
             sh.regs[sh.by_name.at(p.manifest.entries[mem.entry].name)].ptr));
         ls.push_back(p.manifest.entries[mem.entry].length);
       }
-    if (srcs.empty()) continue;
-    DeviceGuard g(sh.device);
-    DevBuf t;
-    const std::size_t nm = srcs.size();
-    if (!ok(t.alloc(sh.device, 3 * nm * 8))) {
-      out[i] = {Status::transfer_failed, 0, 0};
-      continue;
-    }
-    auto* d = static_cast<std::uint64_t*>(t.p);
-    cudaMemcpyAsync(d, srcs.data(), nm * 8, cudaMemcpyHostToDevice, sh.stream);
-    cudaMemcpyAsync(d + nm, dsts.data(), nm * 8, cudaMemcpyHostToDevice, sh.stream);
-    cudaMemcpyAsync(d + 2 * nm, ls.data(), nm * 8, cudaMemcpyHostToDevice, sh.stream);
-    dev::launch_copy_spans(d, d + nm, d + 2 * nm, static_cast<int>(nm), sh.stream);
-    if (cudaStreamSynchronize(sh.stream) != cudaSuccess) out[i] = {Status::transfer_failed, 0, 0};
-    stats_.h2d_bytes += 24 * nm;
+    if (Status s = copy_spans(sh, srcs, dsts, ls); !ok(s)) out[i] = {s, 0, 0};
   }
   return out;
+}
+
+Status Client::copy_spans(Shard& sh, const std::vector<std::uint64_t>& srcs,
+                          const std::vector<std::uint64_t>& dsts,
+                          const std::vector<std::uint64_t>& lens) {
+  if (srcs.empty()) return Status::ok;
+  DeviceGuard g(sh.device);
+  DevBuf t;
+  const std::size_t n = srcs.size();
+  if (Status s = t.alloc(sh.device, 3 * n * 8); !ok(s)) return s;
+  auto* d = static_cast<std::uint64_t*>(t.p);
+  RS_CUDA(cudaMemcpyAsync(d, srcs.data(), n * 8, cudaMemcpyHostToDevice, sh.stream));
+  RS_CUDA(cudaMemcpyAsync(d + n, dsts.data(), n * 8, cudaMemcpyHostToDevice, sh.stream));
+  RS_CUDA(cudaMemcpyAsync(d + 2 * n, lens.data(), n * 8, cudaMemcpyHostToDevice, sh.stream));
+  RS_CUDA(dev::launch_copy_spans(d, d + n, d + 2 * n, static_cast<int>(n), sh.stream));
+  RS_CUDA(cudaStreamSynchronize(sh.stream));
+  stats_.h2d_bytes += 24 * n;
+  return Status::ok;
+}
+
+Status Client::resolve_shard(Shard& sh, const std::string& replica, std::uint32_t shard,
+                             VersionId v, SourceView* out) {
+  auto deadline =
+      std::chrono::steady_clock::now() + std::chrono::duration<double>(cfg_.pull_timeout_s);
+  const std::string k = ServeRegistry::key(model_, replica, shard);
+  for (;;) {
+    auto st = serves_->is_silent(k) ? nullptr : serves_->find(k);
+    if (st) {
+      bool ready;
+      {
+        std::lock_guard lk(st->m);
+        ready = st->serving && st->version == v && !st->cmap.chunk0.empty();
+      }
+      if (ready) return map_source(st, sh.device, out);
+    }
+    if (std::chrono::steady_clock::now() > deadline) return Status::not_serving;
+    std::this_thread::sleep_for(std::chrono::microseconds(200));
+  }
+}
+
+Status Client::launch_reshard_fill(Shard& sh, const Assignment& a, bool src_complete) {
+  DeviceGuard g(sh.device);
+  Payload& p = *sh.holding;
+  Reshard& rs = *p.reshard;
+  const auto nsrc = static_cast<std::uint32_t>(rs.srcs.size());
+  std::vector<SourceView> views(nsrc);
+  std::vector<dev::SrcDesc> sd(nsrc);
+  std::vector<bool> need(nsrc, false);
+  for (const auto& d : rs.plan.segs) need[d.src_id] = true;
+  for (const auto& gth : rs.plan.gathers) need[gth.src_shard] = true;
+  for (std::uint32_t s = 0; s < nsrc; ++s) {
+    if (!need[s]) continue;
+    if (Status st = resolve_shard(sh, a.source_replica, s, a.version, &views[s]); !ok(st))
+      return st;
+    if (views[s].cmap.chunk0 != rs.srcs[s].chunk0) return Status::protocol_error;
+    sd[s] = {reinterpret_cast<const std::uint64_t*>(views[s].digests),
+             src_complete ? nullptr : reinterpret_cast<const std::uint32_t*>(views[s].flags),
+             views[s].epoch, 0};
+  }
+  std::vector<dev::ItemDesc> descs = rs.plan.segs;
+  for (auto& d : descs) {
+    d.src = views[d.src_id].item_ptrs[d.pad] + d.src;
+    d.pad = 0;
+  }
+  std::uint32_t next = rs.own_chunks;
+  for (std::size_t gi = 0; gi < rs.plan.gathers.size(); ++gi) {
+    const auto& gth = rs.plan.gathers[gi];
+    const SourceShard& ss = rs.srcs[gth.src_shard];
+    const auto& it = ss.manifest.items()[gth.src_item];
+    dev::ItemDesc d{};
+    d.src = views[gth.src_shard].item_ptrs[gth.src_item];
+    d.dst = reinterpret_cast<std::uint64_t>(rs.gather_bufs[gi]->p);
+    d.len = it.length;
+    d.chunk0 = next;
+    d.chunk_len = ss.layout.chunk_len[gth.src_item];
+    d.src_chunk0 = ss.chunk0[gth.src_item];
+    d.q = d.m = 1;
+    d.src_id = gth.src_shard;
+    descs.push_back(d);
+    const auto n = static_cast<std::uint32_t>((it.length + d.chunk_len - 1) / d.chunk_len);
+    next += (n + dev::kBatchChunks - 1) / dev::kBatchChunks * dev::kBatchChunks;
+  }
+  dev::PullParams pp{};
+  RS_CUDA(dev::upload_pull_plan(sh.device, sh.stream, descs.data(),
+                                static_cast<std::uint32_t>(descs.size()), sd.data(), nsrc,
+                                &sh.plan, &pp));
+  stats_.h2d_bytes += sh.plan.h2d_bytes;
+  pp.n_chunks = next;
+  pp.n_batches = (next + dev::kBatchChunks - 1) / dev::kBatchChunks;
+  pp.dst_digests = static_cast<std::uint64_t*>(p.digests.p);
+  pp.dst_flags = static_cast<std::uint32_t*>(p.flags.p);
+  pp.dst_epoch = p.epoch;
+  pp.timeout_ns = static_cast<std::uint64_t>(cfg_.pull_timeout_s * 1e9);
+  pp.resume = p.landed_some ? 1u : 0u;
+  RS_CUDA(cudaEventRecord(sh.ev0, sh.stream));
+  RS_CUDA(dev::launch_pull(pp, dev::pull_grid(sh.device), sh.stream));
+  RS_CUDA(cudaEventRecord(sh.ev1, sh.stream));
+  p.landed_some = true;
+  return Status::ok;
+}
+
+Status Client::finish_reshard(Shard& sh) {
+  Payload& p = *sh.holding;
+  Reshard& rs = *p.reshard;
+  // 1) slices out of gathered source items (rows of nc bytes)
+  std::map<std::pair<std::uint32_t, std::uint32_t>, std::size_t> gidx;
+  for (std::size_t gi = 0; gi < rs.plan.gathers.size(); ++gi)
+    gidx[{rs.plan.gathers[gi].src_shard, rs.plan.gathers[gi].src_item}] = gi;
+  std::vector<std::uint64_t> srcs, dsts, lens;
+  for (const auto& c : rs.plan.copies) {
+    const auto base = reinterpret_cast<std::uint64_t>(rs.gather_bufs[gidx.at({c.src_shard, c.src_item})]->p);
+    for (std::uint64_t r = 0; r < c.rows; ++r) {
+      srcs.push_back(base + c.src_off + r * c.src_stride);
+      dsts.push_back(c.dst + r * c.dst_stride);
+      lens.push_back(c.nc);
+    }
+  }
+  if (Status s = copy_spans(sh, srcs, dsts, lens); !ok(s)) return s;
+  // 2) pack this reader's own groups (its tiny slices) for re-serving
+  srcs.clear();
+  dsts.clear();
+  lens.clear();
+  std::vector<std::uint32_t> group_items;
+  const auto& items = p.manifest.items();
+  for (std::uint32_t i = 0; i < items.size(); ++i) {
+    if (!items[i].is_group) continue;
+    group_items.push_back(i);
+    for (const auto& mem : p.manifest.groups[items[i].index].members) {
+      srcs.push_back(reinterpret_cast<std::uint64_t>(sh.regs[mem.entry].ptr));
+      dsts.push_back(reinterpret_cast<std::uint64_t>(p.group_bufs[items[i].index]->p) + mem.offset);
+      lens.push_back(sh.regs[mem.entry].len);
+    }
+  }
+  if (Status s = copy_spans(sh, srcs, dsts, lens); !ok(s)) return s;
+  // 3) digest + release those group items (its own chunk table / watermarks)
+  if (Status s = hash_items(sh, p, group_items); !ok(s)) return s;
+  DeviceGuard g(sh.device);
+  RS_CUDA(cudaStreamSynchronize(sh.stream));
+  return Status::ok;
 }
 
 void Client::finish_transfers(VersionId v, bool good) {

@@ -31,6 +31,7 @@
 #include "common.hpp"
 #include "device.hpp"
 #include "manifest.hpp"
+#include "layout.hpp"
 #include "registry.hpp"
 
 namespace rsb {
@@ -42,6 +43,7 @@ struct ClientConfig {
   int checksum_retries = 3;          // failure reports per fill (config.hpp:42)
   double pull_timeout_s = 4.0;       // upstream silence before reporting
   std::string dc = "dc0";
+  std::uint32_t reshard_align = 2;   // chunk rule: TP splits up to this stay chunk aligned
 };
 
 // Owned device allocation.
@@ -76,6 +78,7 @@ struct ChunkMap {
     return n;
   }
   static ChunkMap uniform(const Manifest& m, std::uint64_t chunk_bytes);
+  static ChunkMap from_lens(const Manifest& m, const std::vector<std::uint32_t>& lens);
   bool operator==(const ChunkMap& o) const {
     return chunk0 == o.chunk0 && chunk_len == o.chunk_len && count == o.count;
   }
@@ -165,8 +168,10 @@ class Client {
   ~Client();
 
   Status register_tensor(std::uint32_t shard, const std::string& name, void* ptr,
-                         std::uint64_t len);
+                         std::uint64_t len, const Geometry& geo = {});
   void set_shard_endpoint(std::uint32_t shard, std::string ep);
+  // Slicing key of the replica ("" when no region carries a geometry).
+  std::string layout_key() const;
   void set_stream(std::uint32_t shard, cudaStream_t s);
 
   // --- blocking ops (in-process registry) ---------------------------------
@@ -179,7 +184,16 @@ class Client {
 
   // --- split phase (caller drives the registry, e.g. replicated across
   //     processes) -----------------------------------------------------------
-  Status prepare_publish(VersionId v, std::vector<std::string>* manifests);
+  Status prepare_publish(VersionId v, std::vector<std::string>* manifests,
+                         std::vector<std::string>* layouts = nullptr);
+  // After bind_all on a reshard: the derived manifests/layouts of this
+  // replica's slicing (to register with Registry::add_layout).
+  bool derived_layout(std::vector<std::string>* manifests, std::vector<std::string>* layouts) const;
+  // The derived manifests/layouts of this replica's own slicing (empty for a
+  // plain replica), computed from its registrations; sent with open.
+  Status derived_blobs(std::vector<std::string>* manifests,
+                       std::vector<std::string>* layouts) const;
+  Result<std::string> layout_bytes(std::uint32_t shard) const;
   void commit_publish(VersionId v, Status st);
   // Binds every shard to its assignment and starts serving the (empty)
   // fill so downstream readers can chase it.
@@ -215,10 +229,20 @@ class Client {
     std::string name;
     std::uint8_t* ptr = nullptr;
     std::uint64_t len = 0;
+    Geometry geo;
+  };
+  // Reshard state of a bound payload (Assignment.reshard).
+  struct Reshard {
+    std::vector<SourceShard> srcs;           // manifests/layouts/chunk0 of the source shards
+    std::vector<std::string> endpoints;      // per source shard
+    ReshardPlan plan;                        // segments (source offsets) / gathers / copies
+    std::vector<std::unique_ptr<DevBuf>> gather_bufs;  // per plan.gathers entry
+    std::uint32_t own_chunks = 0;            // landing chunks of the reader's own items
   };
   struct Payload {
     Manifest manifest;
     std::string encoded;
+    std::string layout;  // encoded ShardLayout of this payload
     std::vector<std::unique_ptr<DevBuf>> group_bufs;
     ChunkMap cmap;
     DevBuf digests;
@@ -226,6 +250,7 @@ class Client {
     std::uint32_t epoch = 0;
     bool landed_some = false;  // a fill ran in this epoch: flags may be set
     std::vector<std::uint64_t> item_ptrs;  // own landing/serving address per item
+    std::unique_ptr<Reshard> reshard;      // set when pulling from another slicing
   };
   struct Shard {
     std::uint32_t idx = 0;
@@ -246,6 +271,17 @@ class Client {
   Status ensure_stream(Shard& sh);
   Status build_payload(Shard& sh, VersionId v, std::shared_ptr<Payload>* out);
   Status bind(Shard& sh, const Assignment& a, VersionId v);
+  Status bind_reshard(Shard& sh, const Assignment& a, VersionId v);
+  Status derive(const Shard& sh, Manifest* m, std::string* encoded, std::string* layout,
+                std::vector<std::uint32_t>* lens) const;
+  Status alloc_tables(Shard& sh, Payload& p, std::uint32_t extra_chunks);
+  Status launch_reshard_fill(Shard& sh, const Assignment& a, bool src_complete);
+  Status finish_reshard(Shard& sh);
+  Status hash_items(Shard& sh, Payload& p, const std::vector<std::uint32_t>& items);
+  Status copy_spans(Shard& sh, const std::vector<std::uint64_t>& srcs,
+                    const std::vector<std::uint64_t>& dsts, const std::vector<std::uint64_t>& lens);
+  Status resolve_shard(Shard& sh, const std::string& replica, std::uint32_t shard, VersionId v,
+                       SourceView* out);
   void serve(Shard& sh, VersionId v, bool complete);
   Status resolve_source(Shard& sh, const Assignment& a, VersionId v, SourceView* out,
                         double wait_s);

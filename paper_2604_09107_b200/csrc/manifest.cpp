@@ -180,7 +180,7 @@ void Manifest::set_group_digest(std::uint32_t g, std::uint64_t d) {
 std::string Manifest::encode() const {
   std::string out;
   field_u64(out, 1, 1);  // format version
-  field_u64(out, 2, 1);  // digest algorithm tag: XXH64 seed 0
+  field_u64(out, 2, alg);  // digest algorithm tag: 1 = XXH64 seed 0
   std::vector<std::string> blobs;
   blobs.reserve(entries.size());
   for (const auto& e : entries) {
@@ -211,11 +211,12 @@ Result<Manifest> Manifest::decode(std::string_view bytes) {
   Fields top(bytes);
   std::uint64_t fmt = 0, alg = 0;
   if (!top.ok) return Status::protocol_error;
-  if (!top.u64(1, fmt) || fmt != 1 || !top.u64(2, alg) || alg != 1)
+  if (!top.u64(1, fmt) || fmt != 1 || !top.u64(2, alg) || (alg != kAlgXxh64 && alg != kAlgDerived))
     return Status::protocol_error;
   std::vector<std::string_view> eb, gb;
   if (!top.list(3, eb) || !top.list(4, gb)) return Status::protocol_error;
   Manifest m;
+  m.alg = static_cast<std::uint8_t>(alg);
   for (auto blob : eb) {
     Fields f(blob);
     ManifestEntry e;

@@ -46,10 +46,18 @@ struct PackLimits {
   std::uint64_t group_target = 64ull << 20;
 };
 
+// Digest algorithm tag carried by the manifest (field 2).  1 = reference
+// XXH64 of every entry / group (digest.hpp:13).  2 = derived reshard layout:
+// entry and group digests are not computed (0); the bytes were verified
+// chunk by chunk against the source layout's chunk digests.
+constexpr std::uint8_t kAlgXxh64 = 1;
+constexpr std::uint8_t kAlgDerived = 2;
+
 class Manifest {
  public:
   std::vector<ManifestEntry> entries;
   std::vector<PackGroup> groups;
+  std::uint8_t alg = kAlgXxh64;
 
   Status finalize();  // validates + derives items (manifest.cpp:12-72)
   const std::vector<StreamItem>& items() const { return items_; }

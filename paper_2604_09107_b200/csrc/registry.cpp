@@ -61,7 +61,9 @@ void Registry::trace(std::string kind,
 
 Status Registry::open(const std::string& model, const std::string& replica,
                       std::uint32_t num_shards, const std::string& dc,
-                      const std::vector<std::string>& endpoints) {
+                      const std::vector<std::string>& endpoints, const std::string& layout,
+                      const std::vector<std::string>& derived_manifests,
+                      const std::vector<std::string>& derived_layouts) {
   std::lock_guard lk(mu_);
   if (model.empty() || replica.empty() || num_shards == 0 ||
       endpoints.size() != num_shards)
@@ -76,6 +78,9 @@ Status Registry::open(const std::string& model, const std::string& replica,
       if (r.num_shards != num_shards) return Status::invalid_argument;
       r.endpoints = endpoints;
       r.dc = dc;
+      r.layout = layout;
+      r.derived_manifests = derived_manifests;
+      r.derived_layouts = derived_layouts;
       return Status::ok;
     }
     m.reps.erase(it);
@@ -86,6 +91,9 @@ Status Registry::open(const std::string& model, const std::string& replica,
   r->dc = dc;
   r->num_shards = num_shards;
   r->endpoints = endpoints;
+  r->layout = layout;
+  r->derived_manifests = derived_manifests;
+  r->derived_layouts = derived_layouts;
   r->shards.assign(num_shards, {});
   m.reps.emplace(replica, std::move(r));
   trace("open", {{"model", model}, {"replica", replica}, {"shards", n2s(num_shards)}});
@@ -138,38 +146,64 @@ std::set<VersionId> Registry::available(ModelState& m, const std::string& dc) {
 bool Registry::still_good(const Rep& c, const Rep& reader, VersionId v) const {
   if (&c == &reader || c.life == Life::failed || c.version != v) return false;
   bool complete_copy = c.visible && c.life == Life::published && c.complete_all();
+  // A differently sliced copy serves only a reshard-capable reader, and only
+  // once complete (chasing is item-for-item).
+  if (c.layout != reader.layout) return complete_copy && !reader.layout.empty();
   bool pipeline_copy = cfg_.pipeline && c.life == Life::replicating &&
                        !c.seeding && c.dc == reader.dc;
   return complete_copy || pipeline_copy;
 }
 
+bool Registry::servable(ModelState& m, VersionId v, const Rep& reader) {
+  auto vit = m.versions.find(v);
+  if (vit == m.versions.end()) return false;
+  auto lit = vit->second.by_layout.find(reader.layout);
+  if (lit != vit->second.by_layout.end()) return lit->second.num_shards == reader.num_shards;
+  return !reader.layout.empty();  // reshard from another slicing
+}
+
 Registry::Rep* Registry::pick_source(ModelState& m, VersionId v,
                                      const Rep& reader) {
   const std::string& rep0 = reader.endpoints.empty() ? reader.name : reader.endpoints[0];
+  // Reference key (own_seed, same_dc, serving, last_assigned, name) with two
+  // B200 terms that are constant when every replica has the same slicing and
+  // the box is uniform: same slicing first, then topology cost.
   auto key = [&](const Rep* c) {
     const std::string& ep0 = c->endpoints.empty() ? c->name : c->endpoints[0];
     return std::make_tuple(1 /* no own seed buffers */, c->dc == reader.dc ? 0 : 1,
-                           topo_(rep0, ep0), c->serving, c->last_assigned,
-                           std::cref(c->name));
+                           c->layout == reader.layout ? 0 : 1, topo_(rep0, ep0), c->serving,
+                           c->last_assigned, std::cref(c->name));
   };
+  auto vit = m.versions.find(v);
   Rep* best = nullptr;
   for (auto& [name, rp] : m.reps) {
     Rep* c = rp.get();
     if (!still_good(*c, reader, v)) continue;
+    // a copy is a source only once its slicing's metadata is known for v
+    if (vit == m.versions.end() || !vit->second.by_layout.count(c->layout)) continue;
     if (!best || key(c) < key(best)) best = c;
   }
   return best;
 }
 
 Assignment Registry::make_assignment(ModelState& m, Rep& src, VersionId v,
-                                     std::uint32_t shard, const std::string& dc) {
+                                     std::uint32_t shard, const Rep& reader) {
   Assignment a;
   a.version = v;
   a.source_replica = src.name;
   a.source_endpoint = shard < src.endpoints.size() ? src.endpoints[shard] : "";
   a.source_complete = src.life == Life::published && src.complete_all();
-  a.cross_dc = src.dc != dc;
-  a.manifest = m.versions[v].manifests[shard];
+  a.cross_dc = src.dc != reader.dc;
+  const LayoutInfo& li = m.versions[v].by_layout[src.layout];
+  if (src.layout == reader.layout) {
+    a.manifest = shard < li.manifests.size() ? li.manifests[shard] : "";
+    a.layout = shard < li.layouts.size() ? li.layouts[shard] : "";
+  } else {
+    a.reshard = true;
+    a.all_manifests = li.manifests;
+    a.all_layouts = li.layouts;
+    a.all_endpoints = src.endpoints;
+  }
   return a;
 }
 
@@ -177,12 +211,13 @@ Assignment Registry::make_assignment(ModelState& m, Rep& src, VersionId v,
 
 Status Registry::publish(const std::string& model, const std::string& replica,
                          VersionId v, const std::vector<std::string>& manifests,
-                         OpOutcome* out) {
+                         OpOutcome* out, const std::vector<std::string>& layouts) {
   std::lock_guard lk(mu_);
   Rep* r = find(model, replica);
   if (!r) return Status::not_found;
   if (r->txn) return Status::invalid_state;
   if (manifests.size() != r->num_shards) return Status::invalid_argument;
+  if (!layouts.empty() && layouts.size() != r->num_shards) return Status::invalid_argument;
   auto reject = [&](Status s, const char* why) {
     if (why)
       trace("publish_reject", {{"model", model}, {"replica", replica}, {"v", n2s(v)},
@@ -202,14 +237,19 @@ Status Registry::publish(const std::string& model, const std::string& replica,
     items[s] = mf->items().size();
   }
   auto& m = ms(model);
-  auto vit = m.versions.find(v);
-  if (vit != m.versions.end()) {
-    if (vit->second.num_shards != r->num_shards) return reject(Status::manifest_conflict, nullptr);
+  // A version number already defined for this slicing must carry
+  // byte-identical manifests (server_core.cpp:666-683).
+  auto& vi = m.versions[v];
+  auto lit = vi.by_layout.find(r->layout);
+  if (lit != vi.by_layout.end()) {
+    if (lit->second.num_shards != r->num_shards) return reject(Status::manifest_conflict, nullptr);
     for (std::uint32_t s = 0; s < r->num_shards; ++s)
-      if (vit->second.manifests[s] != manifests[s])
+      if (lit->second.manifests[s] != manifests[s])
         return reject(Status::manifest_conflict, "manifest_conflict");
   } else {
-    m.versions[v] = VersionInfo{r->num_shards, manifests};
+    LayoutInfo li{r->num_shards, manifests, layouts};
+    li.layouts.resize(r->num_shards);
+    vi.by_layout.emplace(r->layout, std::move(li));
   }
   r->life = Life::published;
   r->visible = true;
@@ -222,6 +262,23 @@ Status Registry::publish(const std::string& model, const std::string& replica,
   if (out) *out = r->last;
   wake_blocked(model);
   cv_.notify_all();
+  return Status::ok;
+}
+
+Status Registry::add_layout(const std::string& model, VersionId v, const std::string& key,
+                            const std::vector<std::string>& manifests,
+                            const std::vector<std::string>& layouts) {
+  std::lock_guard lk(mu_);
+  auto& m = ms(model);
+  auto vit = m.versions.find(v);
+  if (vit == m.versions.end()) return Status::version_unavailable;
+  auto lit = vit->second.by_layout.find(key);
+  if (lit != vit->second.by_layout.end())
+    return lit->second.manifests == manifests ? Status::ok : Status::manifest_conflict;
+  LayoutInfo li{static_cast<std::uint32_t>(manifests.size()), manifests, layouts};
+  li.layouts.resize(manifests.size());
+  vit->second.by_layout.emplace(key, std::move(li));
+  trace("layout_added", {{"model", model}, {"v", n2s(v)}, {"shards", n2s(manifests.size())}});
   return Status::ok;
 }
 
@@ -288,9 +345,7 @@ void Registry::start_replicate(Rep& r) {
     }
     return;  // parked; wake_blocked retries
   }
-  auto vit = m.versions.find(*target);
-  if (vit == m.versions.end() || vit->second.num_shards != r.num_shards)
-    return finish_op(r, Status::invalid_argument);
+  if (!servable(m, *target, r)) return finish_op(r, Status::invalid_argument);
   Rep* src = pick_source(m, *target, r);
   if (!src) return finish_op(r, Status::version_unavailable);
   t.blocked = false;
@@ -344,9 +399,7 @@ void Registry::start_update(Rep& r) {
     r.txn.reset();
   };
   if (!target || (current && *target == *current)) return no_change();
-  auto vit = m.versions.find(*target);
-  if (vit == m.versions.end() || vit->second.num_shards != r.num_shards)
-    return finish_op(r, Status::invalid_argument);
+  if (!servable(m, *target, r)) return finish_op(r, Status::invalid_argument);
   Rep* src = pick_source(m, *target, r);
   if (!src) return no_change();
   t.resolved = true;
@@ -444,6 +497,16 @@ void Registry::apply_settle(Rep& r) {
                        {"v", n2s(*t.target)}, {"src", t.source},
                        {"cross_dc", src->dc != r.dc ? "1" : "0"},
                        {"src_serving", n2s(src->serving)}});
+      if (src->layout != r.layout && r.derived_manifests.size() == r.num_shards) {
+        // a resharding fill: its slicing becomes a layout of the version
+        auto& vi = m.versions[*t.target];
+        if (!vi.by_layout.count(r.layout)) {
+          LayoutInfo li{r.num_shards, r.derived_manifests, r.derived_layouts};
+          li.layouts.resize(r.num_shards);
+          vi.by_layout.emplace(r.layout, std::move(li));
+          trace("layout_added", {{"model", r.model}, {"v", n2s(*t.target)}, {"replica", r.name}});
+        }
+      }
       if (is_update && old && *old != *t.target) prune_version(m, *old);
       settle_ok(r);
       return;
@@ -466,7 +529,7 @@ void Registry::settle_ok(Rep& r) {
     o.status = Status::version_unavailable;
   } else {
     for (std::uint32_t s = 0; s < r.num_shards; ++s) {
-      Assignment a = make_assignment(m, *sit->second, *t.target, s, r.dc);
+      Assignment a = make_assignment(m, *sit->second, *t.target, s, r);
       a.seeding = r.seeding;
       o.assignments.push_back(std::move(a));
     }
@@ -627,7 +690,7 @@ Result<Assignment> Registry::failure_report(const std::string& model,
   }
   Rep* s = find(model, r->source);
   if (!s) return Status::version_unavailable;
-  Assignment a = make_assignment(m, *s, v, shard, r->dc);
+  Assignment a = make_assignment(m, *s, v, shard, *r);
   a.seeding = r->seeding;
   cv_.notify_all();
   return a;
@@ -644,12 +707,10 @@ Result<Assignment> Registry::locate(const std::string& model, const std::string&
   auto& m = ms(model);
   auto target = resolve_version(spec, available(m, r->dc));
   if (!target) return Status::version_unavailable;
-  auto vit = m.versions.find(*target);
-  if (vit == m.versions.end() || vit->second.num_shards != r->num_shards)
-    return Status::invalid_argument;
+  if (!servable(m, *target, *r)) return Status::invalid_argument;
   Rep* src = pick_source(m, *target, *r);
   if (!src) return Status::version_unavailable;
-  return make_assignment(m, *src, *target, shard, r->dc);
+  return make_assignment(m, *src, *target, shard, *r);
 }
 
 Result<Assignment> Registry::current_assignment(const std::string& model,
@@ -662,7 +723,7 @@ Result<Assignment> Registry::current_assignment(const std::string& model,
     return Status::invalid_state;
   Rep* s = find(model, r->source);
   if (!s) return Status::version_unavailable;
-  Assignment a = make_assignment(ms(model), *s, *r->version, shard, r->dc);
+  Assignment a = make_assignment(ms(model), *s, *r->version, shard, *r);
   a.seeding = r->seeding;
   return a;
 }

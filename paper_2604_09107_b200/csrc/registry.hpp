@@ -40,7 +40,7 @@
 
 namespace rsb {
 
-// messages.hpp:40-52.
+// messages.hpp:40-52, plus the layout fields of the B200 path.
 struct Assignment {
   VersionId version = 0;
   std::string source_replica;
@@ -49,7 +49,12 @@ struct Assignment {
   bool cross_dc = false;
   bool seeding = false;
   bool local_seed_consume = false;
-  std::string manifest;  // encoded Manifest of this shard
+  std::string manifest;  // encoded Manifest of this shard ("" on a reshard)
+  std::string layout;    // encoded ShardLayout of this shard (chunk lengths)
+  // Reshard (the source's slicing differs from the reader's): every source
+  // shard's manifest, layout and endpoint.
+  bool reshard = false;
+  std::vector<std::string> all_manifests, all_layouts, all_endpoints;
 };
 
 enum class OpKind : std::uint8_t { none, publish, unpublish, replicate, update };
@@ -94,16 +99,31 @@ class Registry {
 
   void set_topology(TopoFn fn);
 
+  // `layout` keys the replica's slicing ("" = plain, the reference's only
+  // kind).  Replicas with equal keys pull item-for-item (and may chase each
+  // other); a reader with a different non-empty key reshards from complete
+  // copies.
+  // A reshard-capable replica also hands over its derived per-shard
+  // manifests/layouts (they depend only on its registrations); they become a
+  // layout of version v the moment it is assigned a differently sliced
+  // source, so same-slicing readers can chase it in the same round.
   Status open(const std::string& model, const std::string& replica,
               std::uint32_t num_shards, const std::string& dc,
-              const std::vector<std::string>& endpoints);
+              const std::vector<std::string>& endpoints, const std::string& layout = "",
+              const std::vector<std::string>& derived_manifests = {},
+              const std::vector<std::string>& derived_layouts = {});
   Status close(const std::string& model, const std::string& replica);
 
   // Each returns the immediate status; if ok and the op is parked,
   // *pending = true and the outcome arrives through op_result().
   Status publish(const std::string& model, const std::string& replica,
                  VersionId v, const std::vector<std::string>& manifests,
-                 OpOutcome* out);
+                 OpOutcome* out, const std::vector<std::string>& layouts = {});
+  // A resharding reader registers the derived manifests/layouts of its own
+  // slicing so readers of the same slicing can later pull from it.
+  Status add_layout(const std::string& model, VersionId v, const std::string& layout_key,
+                    const std::vector<std::string>& manifests,
+                    const std::vector<std::string>& layouts);
   Status unpublish(const std::string& model, const std::string& replica,
                    OpOutcome* out);
   Status replicate(const std::string& model, const std::string& replica,
@@ -164,6 +184,8 @@ class Registry {
   };
   struct Rep {
     std::string model, name, dc;
+    std::string layout;  // slicing key ("" plain)
+    std::vector<std::string> derived_manifests, derived_layouts;  // reshard readers
     std::uint32_t num_shards = 1;
     std::vector<std::string> endpoints;
     Life life = Life::registered;
@@ -181,9 +203,13 @@ class Registry {
       return true;
     }
   };
-  struct VersionInfo {
+  struct LayoutInfo {
     std::uint32_t num_shards = 0;
     std::vector<std::string> manifests;
+    std::vector<std::string> layouts;
+  };
+  struct VersionInfo {
+    std::map<std::string, LayoutInfo> by_layout;  // slicing key -> per-shard metadata
   };
   struct ModelState {
     std::map<std::string, std::unique_ptr<Rep>> reps;
@@ -202,7 +228,8 @@ class Registry {
   bool still_good(const Rep& cand, const Rep& reader, VersionId v) const;
   Rep* settle_source(Rep& r, Txn& t);
   Assignment make_assignment(ModelState& m, Rep& src, VersionId v,
-                             std::uint32_t shard, const std::string& dc);
+                             std::uint32_t shard, const Rep& reader);
+  bool servable(ModelState& m, VersionId v, const Rep& reader);
   void start_replicate(Rep& r);
   void start_update(Rep& r);
   void try_settle(Rep& r);

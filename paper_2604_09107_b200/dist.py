@@ -13,9 +13,9 @@ buffers, chunk-digest tables, watermark words) travel as CUDA IPC handles
 and readers pull them with the SM-driven kernel, chasing upstream
 watermarks in device memory.
 
-All methods are collective over the group: every rank calls them in the
-same order, passing its local handle (or None when it has no part in that
-operation).
+All methods except create() are collective over the group: every rank calls
+them in the same order, passing its local handle (or None when it has no
+part in that operation).
 """
 from __future__ import annotations
 
@@ -28,6 +28,12 @@ from .ros import Cluster, Handle, OpResult, Status, _read_bytes, check
 
 def _b(s: str) -> bytes:
     return s.encode()
+
+
+def _blob_arrays(blobs):
+    arr = (C.c_char_p * max(len(blobs), 1))(*blobs)
+    lens = (C.c_size_t * max(len(blobs), 1))(*[len(x) for x in blobs])
+    return C.cast(arr, C.c_void_p), C.cast(lens, C.c_void_p), arr, lens
 
 
 class DistCluster:
@@ -55,11 +61,15 @@ class DistCluster:
             for b in bl:
                 check(lib.rs_serve_import(self.local.h, b, len(b)), "rs_serve_import")
 
+    def _source(self, model, replica) -> str:
+        return _read_bytes(lib.rs_cluster_source, self.local.h, _b(model), _b(replica)).decode()
+
     def server_ops(self, op):
         """Collective: all-gather one registry operation per rank (or None)
         and apply them to the local registry replica in rank order.  Ops:
-        ("open", model, replica, shards, dc, endpoints),
-        ("publish", model, replica, version, [manifest bytes per shard]),
+        ("open", model, replica, shards, dc, endpoints[, layout_key]),
+        ("publish", model, replica, version, [manifests][, [layouts]]),
+        ("add_layout", model, version, layout_key, [manifests], [layouts]),
         ("unpublish", model, replica), ("replicate", model, replica, spec),
         ("update", model, replica, spec, current|None),
         ("complete", model, replica, shard, status),
@@ -74,15 +84,32 @@ class DistCluster:
         c = self.local.h
         kind = o[0]
         if kind == "open":
-            _, m, r, n, dc, eps = o
+            _, m, r, n, dc, eps = o[:6]
+            key = o[6] if len(o) > 6 else ""
+            dman = o[7] if len(o) > 7 else []
+            dlay = o[8] if len(o) > 8 else []
             arr = (C.c_char_p * n)(*[_b(e) for e in eps])
-            return lib.rs_server_open(c, _b(m), _b(r), n, _b(dc), C.cast(arr, C.c_void_p))
+            if dman:
+                pm, pl, _k1, _k2 = _blob_arrays(dman)
+                qm, ql, _k3, _k4 = _blob_arrays(dlay)
+            else:
+                pm = pl = qm = ql = None
+            return lib.rs_server_open(c, _b(m), _b(r), n, _b(dc), C.cast(arr, C.c_void_p), _b(key),
+                                      pm, pl, qm, ql)
         if kind == "publish":
-            _, m, r, v, mans = o
-            arr = (C.c_char_p * len(mans))(*mans)
-            lens = (C.c_size_t * len(mans))(*[len(x) for x in mans])
-            return lib.rs_server_publish(c, _b(m), _b(r), v, len(mans), C.cast(arr, C.c_void_p),
-                                         C.cast(lens, C.c_void_p))
+            _, m, r, v, mans = o[:5]
+            lays = o[5] if len(o) > 5 else []
+            pm, pl, _k1, _k2 = _blob_arrays(mans)
+            if lays:
+                qm, ql, _k3, _k4 = _blob_arrays(lays)
+            else:
+                qm = ql = None
+            return lib.rs_server_publish(c, _b(m), _b(r), v, len(mans), pm, pl, qm, ql)
+        if kind == "add_layout":
+            _, m, v, key, mans, lays = o
+            pm, pl, _k1, _k2 = _blob_arrays(mans)
+            qm, ql, _k3, _k4 = _blob_arrays(lays)
+            return lib.rs_server_add_layout(c, _b(m), v, _b(key), len(mans), pm, pl, qm, ql)
         if kind == "unpublish":
             return lib.rs_server_unpublish(c, _b(o[1]), _b(o[2]))
         if kind == "replicate":
@@ -102,73 +129,54 @@ class DistCluster:
                              C.byref(v), C.byref(ch))
         return bool(d.value), Status(s.value), v.value, bool(ch.value)
 
-    def _source(self, model, replica) -> str:
-        return _read_bytes(lib.rs_cluster_source, self.local.h, _b(model), _b(replica)).decode()
-
     # ---- ops ---------------------------------------------------------------
-    def open(self, model: str, replica: Optional[str], num_shards: int = 1,
-             endpoints: Optional[list[str]] = None, datacenter: str = "dc0",
-             **cfg) -> Optional[Handle]:
-        """Collective open.  Ranks with replica=None only mirror the others'
-        records.  Tensors are registered on the returned handle afterwards."""
+    def create(self, model: str, replica: str, num_shards: int = 1, **cfg) -> Handle:
+        """Local: a handle to register tensors on, before the collective open()."""
+        return self.local.open(model, replica, num_shards, **cfg)
+
+    def open(self, h: Optional[Handle], endpoints: Optional[list[str]] = None,
+             datacenter: str = "dc0") -> None:
+        """Collective: every rank mirrors every opened replica's record
+        (with its slicing key, known once its tensors are registered)."""
         mine = None
-        h = None
-        if replica is not None:
-            h = self.local.open(model, replica, num_shards, datacenter=datacenter, **cfg)
-            eps = endpoints or [f"rank{self.rank}:{i}" for i in range(num_shards)]
+        if h is not None:
+            eps = endpoints or [f"rank{self.rank}:{i}" for i in range(h.num_shards)]
             for i, e in enumerate(eps):
                 h.set_endpoint(i, e)
-            mine = (model, replica, num_shards, datacenter, eps)
-        for op in self.gather(mine):
-            if op is None:
-                continue
-            m, r, n, dc, eps = op
-            arr = (C.c_char_p * n)(*[_b(e) for e in eps])
-            check(lib.rs_server_open(self.local.h, _b(m), _b(r), n, _b(dc), C.cast(arr, C.c_void_p)),
-                  "rs_server_open")
-        return h
+            key = h.layout_key
+            dman = [h.derived(s, 0) for s in range(h.num_shards)] if key else []
+            dlay = [h.derived(s, 1) for s in range(h.num_shards)] if key else []
+            mine = ("open", h.model, h.replica, h.num_shards, datacenter, eps, key, dman, dlay)
+        for rc in self.server_ops(mine):
+            assert rc in (None, 0), rc
 
     def publish(self, h: Optional[Handle], version: int) -> Optional[OpResult]:
         mine = None
         if h is not None:
             check(lib.rs_prepare_publish(h.h, version), "rs_prepare_publish")
-            mine = (h.model, h.replica, version, [h.manifest(s) for s in range(h.num_shards)])
-        statuses = {}
-        for op in self.gather(mine):
-            if op is None:
-                continue
-            m, r, v, mans = op
-            arr = (C.c_char_p * len(mans))(*mans)
-            lens = (C.c_size_t * len(mans))(*[len(x) for x in mans])
-            statuses[r] = lib.rs_server_publish(self.local.h, _b(m), _b(r), v, len(mans),
-                                                C.cast(arr, C.c_void_p), C.cast(lens, C.c_void_p))
+            mine = ("publish", h.model, h.replica, version,
+                    [h.manifest(s) for s in range(h.num_shards)],
+                    [h.layout(s) for s in range(h.num_shards)])
+        rcs = self.server_ops(mine)
         blobs = None
         if h is not None:
-            st = statuses[h.replica]
+            st = rcs[self.rank]
             lib.rs_commit_publish(h.h, version, st)
             if st == 0:
                 blobs = [h.serve_export(s) for s in range(h.num_shards)]
         self._import_all(self.gather(blobs))
         if h is None:
             return None
-        st = Status(statuses[h.replica])
+        st = Status(rcs[self.rank])
         return OpResult(st, version if st == Status.ok else None)
 
     def unpublish(self, h: Optional[Handle]) -> Optional[OpResult]:
-        mine = (h.model, h.replica) if h is not None else None
-        res = {}
-        for op in self.gather(mine):
-            if op is not None:
-                res[op[1]] = lib.rs_server_unpublish(self.local.h, _b(op[0]), _b(op[1]))
+        rcs = self.server_ops(("unpublish", h.model, h.replica) if h is not None else None)
         if h is None:
             return None
-        d, s, v, ch = C.c_int(), C.c_int(), C.c_uint64(), C.c_int()
-        lib.rs_server_result(self.local.h, _b(h.model), _b(h.replica), C.byref(d), C.byref(s),
-                             C.byref(v), C.byref(ch))
-        st = Status(res[h.replica]) if res[h.replica] else Status(s.value)
-        if not d.value:
-            st = Status.timeout  # readers still draining
-        return OpResult(st)
+        done, s, _, _ = self.result(h.model, h.replica)
+        st = Status(rcs[self.rank]) if rcs[self.rank] else s
+        return OpResult(st if done else Status.timeout)
 
     def replicate(self, h: Optional[Handle], spec: str = "latest", update: bool = False,
                   max_rounds: int = 8) -> Optional[OpResult]:
@@ -178,30 +186,20 @@ class DistCluster:
         mine = None
         if h is not None:
             cur = h.current_version
-            mine = (h.model, h.replica, spec, update, cur)
-        for op in self.gather(mine):
-            if op is None:
-                continue
-            m, r, sp, upd, cur = op
-            if upd:
-                lib.rs_server_update(self.local.h, _b(m), _b(r), _b(sp), int(cur is not None),
-                                     cur or 0)
-            else:
-                lib.rs_server_replicate(self.local.h, _b(m), _b(r), _b(sp))
-        # every rank: outcome of the local op
+            mine = ("update", h.model, h.replica, spec, cur) if update else \
+                ("replicate", h.model, h.replica, spec)
+        self.server_ops(mine)
         active, result, version, changed = False, None, None, False
         if h is not None:
-            d, s, v, ch = C.c_int(), C.c_int(), C.c_uint64(), C.c_int()
-            lib.rs_server_result(self.local.h, _b(h.model), _b(h.replica), C.byref(d), C.byref(s),
-                                 C.byref(v), C.byref(ch))
-            if not d.value:
+            d, s, v, ch = self.result(h.model, h.replica)
+            if not d:
                 result = OpResult(Status.timeout)  # parked: no version yet
-            elif s.value != 0:
-                result = OpResult(Status(s.value))
-            elif update and not ch.value:
-                result = OpResult(Status.ok, v.value or cur, False)
+            elif s != Status.ok:
+                result = OpResult(s)
+            elif update and not ch:
+                result = OpResult(Status.ok, v or cur, False)
             else:
-                version, changed = v.value, bool(ch.value) or not update
+                version, changed = v, ch or not update
                 rc = lib.rs_transfer_bind(h.h, version)
                 if rc != 0:
                     result = OpResult(Status(rc))
@@ -209,7 +207,6 @@ class DistCluster:
                     active = True
         blobs = [h.serve_export(s) for s in range(h.num_shards)] if active else None
         self._import_all(self.gather(blobs))
-        # fill rounds: failures are reported to every registry replica
         rounds = 0
         while True:
             outcome = None
@@ -217,38 +214,33 @@ class DistCluster:
                 n = h.num_shards
                 sts, rsn = (C.c_int * n)(), (C.c_int * n)()
                 lib.rs_transfer_fill(h.h, C.cast(sts, C.c_void_p), C.cast(rsn, C.c_void_p))
-                srcs = self._source(h.model, h.replica)
-                outcome = (h.model, h.replica, [int(x) for x in sts], [int(x) for x in rsn], srcs)
-            outs = self.gather(outcome)
+                outcome = (h.model, h.replica, [int(x) for x in sts], [int(x) for x in rsn],
+                           self._source(h.model, h.replica))
             retry = {}
-            for o in outs:
+            for o in self.gather(outcome):
                 if o is None:
                     continue
                 m, r, sts, rsn, src = o
                 failed = [i for i, x in enumerate(sts) if x != 0]
                 if not failed:
                     continue
-                ok = True
+                good = True
                 for i in failed:
-                    rc = lib.rs_server_failure_report(self.local.h, _b(m), _b(r), i, _b(src), rsn[i])
-                    ok &= rc == 0
-                retry[r] = ok and rounds + 1 < max_rounds
+                    good &= self._apply(("report", m, r, i, src, rsn[i])) == 0
+                retry[r] = good and rounds + 1 < max_rounds
             if active:
                 mine_failed = any(x != 0 for x in outcome[2])
                 if not mine_failed or not retry.get(h.replica, False):
                     if mine_failed:
-                        bad = next(x for x in outcome[2] if x != 0)
-                        result = OpResult(Status(bad))
+                        result = OpResult(Status(next(x for x in outcome[2] if x != 0)))
                         lib.rs_transfer_finish(h.h, version, 0)
                     else:
                         lib.rs_transfer_finish(h.h, version, 1)
                         result = OpResult(Status.ok, version, changed)
                     active = False
-            # the loop ends when no rank still has a retry pending
             if not any(self.gather(active)):
                 break
             rounds += 1
-        # completions, applied in rank order everywhere
         done = (h.model, h.replica, h.num_shards, int(result.status)) if (
             h is not None and result is not None and version is not None) else None
         for o in self.gather(done):
@@ -256,7 +248,7 @@ class DistCluster:
                 continue
             m, r, n, st = o
             for i in range(n):
-                lib.rs_server_complete(self.local.h, _b(m), _b(r), i, st)
+                self._apply(("complete", m, r, i, st))
         return result
 
     def update(self, h: Optional[Handle], spec: str = "latest") -> Optional[OpResult]:

@@ -103,7 +103,8 @@ def _read_bytes(fn, *args) -> bytes:
 
 
 def make_config(chunk_bytes=4096, tiny_threshold=2 << 20, group_target=64 << 20, pipeline=True,
-                checksum_retries=3, pull_timeout_s=4.0, datacenter="dc0") -> RsConfig:
+                checksum_retries=3, pull_timeout_s=4.0, datacenter="dc0",
+                reshard_align=2) -> RsConfig:
     cfg = RsConfig()
     lib.rs_config_default(C.byref(cfg))
     cfg.chunk_bytes = chunk_bytes
@@ -113,7 +114,28 @@ def make_config(chunk_bytes=4096, tiny_threshold=2 << 20, group_target=64 << 20,
     cfg.checksum_retries = checksum_retries
     cfg.pull_timeout_s = pull_timeout_s
     cfg.datacenter = datacenter.encode()
+    cfg.reshard_align = reshard_align
     return cfg
+
+
+def tp_slice(shape, elem_bytes: int, split_dim, tp: int, rank: int):
+    """Geometry (rows, row_bytes, r0, nr, c0, nc) of rank `rank`'s slice of a
+    tensor of `shape` split `tp` ways along `split_dim` (None: replicated).
+    1-D tensors are [1 x N]: a dim-0 split of them is a column split."""
+    if len(shape) == 1:
+        rows, w = 1, shape[0] * elem_bytes
+        if split_dim is None or tp == 1:
+            return rows, w, 0, 1, 0, w
+        return rows, w, 0, 1, rank * w // tp, w // tp
+    rows = shape[0]
+    w = elem_bytes
+    for d in shape[1:]:
+        w *= d
+    if split_dim is None or tp == 1:
+        return rows, w, 0, rows, 0, w
+    if split_dim == 0:
+        return rows, w, rank * rows // tp, rows // tp, 0, w
+    return rows, w, 0, rows, rank * w // tp, w // tp
 
 
 _ASSIGN = re.compile(r"^\d+ assign (.*)$")
@@ -219,6 +241,28 @@ class Handle:
             ptr, nbytes = tensor.data_ptr(), tensor.numel() * tensor.element_size()
             self._keep.append(tensor)
         return Status(lib.rs_register(self.h, shard, _b(name), C.c_void_p(ptr), nbytes))
+
+    def register_slice(self, shard: int, name: str, tensor, geometry) -> Status:
+        """Register a region holding a slice of a logical tensor;
+        geometry = (rows, row_bytes, r0, nr, c0, nc) as from tp_slice()."""
+        if not tensor.is_cuda or not tensor.is_contiguous():
+            return Status.invalid_argument
+        self._keep.append(tensor)
+        rows, w, r0, nr, c0, nc = (int(x) for x in geometry)
+        return Status(lib.rs_register_slice(self.h, shard, _b(name), C.c_void_p(tensor.data_ptr()),
+                                            tensor.numel() * tensor.element_size(), rows, w, r0, nr,
+                                            c0, nc))
+
+    def layout(self, shard: int = 0) -> bytes:
+        return _read_bytes(lib.rs_layout, self.h, shard)
+
+    def derived(self, shard: int, what: int) -> bytes:
+        """Own-slicing derived manifest (0) / layout (1) of a shard."""
+        return _read_bytes(lib.rs_derived, self.h, shard, what)
+
+    @property
+    def layout_key(self) -> str:
+        return _read_bytes(lib.rs_layout_key, self.h).decode()
 
     def set_endpoint(self, shard: int, endpoint: str):
         check(lib.rs_set_endpoint(self.h, shard, _b(endpoint)))
