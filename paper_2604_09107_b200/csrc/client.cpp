@@ -1200,8 +1200,13 @@ Status Client::finish_reshard(Shard& sh) {
     }
   }
   if (Status s = copy_spans(sh, srcs, dsts, lens); !ok(s)) return s;
-  // 3) digest + release those group items (its own chunk table / watermarks)
-  if (Status s = hash_items(sh, p, group_items); !ok(s)) return s;
+  // 3) digest + release the items whose bytes arrived by copy: the groups and
+  //    big items sliced out of gathered source items (own chunk table and
+  //    watermarks)
+  std::vector<std::uint32_t> rehash = group_items;
+  rehash.insert(rehash.end(), rs.plan.rehash.begin(), rs.plan.rehash.end());
+  std::sort(rehash.begin(), rehash.end());
+  if (Status s = hash_items(sh, p, rehash); !ok(s)) return s;
   DeviceGuard g(sh.device);
   RS_CUDA(cudaStreamSynchronize(sh.stream));
   return Status::ok;

@@ -101,6 +101,7 @@ Status plan_reshard(const std::vector<ReaderEntry>& reader, const std::vector<So
   out->segs.clear();
   out->gathers.clear();
   out->copies.clear();
+  out->rehash.clear();
   std::map<std::pair<std::uint32_t, std::uint32_t>, bool> gathered;
   for (const auto& r : reader) {
     const Geometry rg = r.geo.has() ? r.geo : full_geometry(r.len);
@@ -154,6 +155,9 @@ Status plan_reshard(const std::vector<ReaderEntry>& reader, const std::vector<So
         cp.rows = b - a;
         cp.nc = c1 - c0;
         out->copies.push_back(cp);
+        if (!r.in_group &&
+            std::find(out->rehash.begin(), out->rehash.end(), r.item) == out->rehash.end())
+          out->rehash.push_back(r.item);
       }
     }
     if (covered != rg.nr * rg.nc || rg.nr * rg.nc != r.len) return Status::version_unavailable;

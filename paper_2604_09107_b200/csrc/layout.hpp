@@ -76,6 +76,7 @@ struct ReshardPlan {
   std::vector<dev::ItemDesc> segs;  // src addresses filled from SourceShard.item_ptrs
   std::vector<GatherNeed> gathers;  // whole source items to land in staging
   std::vector<SliceCopy> copies;    // staging -> reader regions
+  std::vector<std::uint32_t> rehash;  // reader big items (partly) filled by copies
 };
 
 // Reader entry e (name, region address, geometry, own item index + chunk0 +

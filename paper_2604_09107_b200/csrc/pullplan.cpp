@@ -93,7 +93,8 @@ cudaError_t upload_pull_plan(int device, cudaStream_t s, ItemDesc* items, std::u
               d.dst % 16 == 0 && full >= 32 && (32 % q) == 0 && (full % q) == 0;
     if (ok) {
       auto* mp = reinterpret_cast<CUtensorMap*>(host.data() + maps_off + 256 * std::size_t(i));
-      ok = encode(mp, d.src, c, q, m, full / q);
+      // 2-D: one row per chunk; 3-D: one row per source row (q chunks each)
+      ok = encode(mp, d.src, c, q, m, q == m ? full : full / q);
       if (ok && d.dst) ok = encode(mp + 1, d.dst, c, 1, 1, full);
     }
     if (ok) {
