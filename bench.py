@@ -148,6 +148,22 @@ def alloc_replica(shapes, dev, seed_base=None):
     return arena, views
 
 
+def tp_dim(name: str):
+    """Megatron-style TP split of a Llama/Qwen tensor: column-parallel (dim 0)
+    for q/k/v/gate/up/embed/lm_head and biases, row-parallel (dim 1) for
+    o_proj/down_proj, replicated norms."""
+    if "norm" in name:
+        return None
+    if "o_proj" in name or "down_proj" in name:
+        return 1
+    return 0
+
+
+def tp_slice(shape, elem, dim, tp, rank):
+    from paper_2604_09107_b200.ros import tp_slice as ts
+    return ts(shape, elem, dim, tp, rank)
+
+
 def _numel(shape):
     n = 1
     for d in shape:
@@ -214,11 +230,29 @@ def run_single(args):
     stream = torch.cuda.Stream(device=dev)
     cl = Cluster()
     t = cl.open("m", "trainer", 1, chunk_bytes=args.chunk)
-    r = cl.open("m", "rollout1", 1, chunk_bytes=args.chunk)
-    for (n, v), (_, w) in zip(tviews, rviews):
-        assert t.register_tensor(0, n, v) == Status.ok
-        assert r.register_tensor(0, n, w) == Status.ok
-    r.set_stream(0, stream)
+    reshard = args.reshard == "tp2"
+    r = cl.open("m", "rollout1", 2 if reshard else 1, chunk_bytes=args.chunk)
+    rslices = {}
+    for (n, v), (_, w), (_, shape) in zip(tviews, rviews, shapes):
+        if not reshard:
+            assert t.register_tensor(0, n, v) == Status.ok
+            assert r.register_tensor(0, n, w) == Status.ok
+            continue
+        # TP=1 trainer -> TP=2 reader: both shards on this GPU, landing
+        # straight into the reader arena (shard 0 then shard 1 per tensor)
+        assert t.register_slice(0, n, v, tp_slice(shape, 2, None, 1, 0)) == Status.ok
+        dim = tp_dim(n)
+        for s in range(2):
+            geo = tp_slice(shape, 2, dim, 2, s)
+            off = 0 if s == 0 else rslices[(0, n)][1]
+            if dim is None and s == 1:  # replicated: every shard holds it whole
+                buf = torch.empty(geo[3] * geo[5], dtype=torch.uint8, device=dev)
+            else:
+                buf = w[off:off + geo[3] * geo[5]]
+            rslices[(s, n)] = (buf, geo[3] * geo[5], geo)
+            assert r.register_slice(s, n, buf, geo) == Status.ok
+    for s in range(r.num_shards):
+        r.set_stream(s, stream)
     t0 = time.perf_counter()
     assert t.publish(1).status == Status.ok
     publish_s = time.perf_counter() - t0
@@ -234,11 +268,21 @@ def run_single(args):
         assert res.status == Status.ok, res
         return w1 - w0
 
+    def verify():
+        if not reshard:
+            assert torch.equal(tarena, rarena), "reader bytes differ from trainer"
+            assert (r.chunk_digests(0) == t.chunk_digests(0)).all()
+            return
+        for (n, v), (_, shape) in zip(tviews, shapes):
+            for s in range(2):
+                buf, nb, (rows, w, r0, nr, c0, nc) = rslices[(s, n)]
+                want = v.view(rows, w)[r0:r0 + nr, c0:c0 + nc]
+                assert torch.equal(buf.view(nr, nc), want), (s, n)
+
     for _ in range(args.warmup):
         step()
     if not args.no_verify:
-        assert torch.equal(tarena, rarena), "reader bytes differ from trainer"
-        assert (r.chunk_digests(0) == t.chunk_digests(0)).all()
+        verify()
     clk = ClockSampler(0)
     torch.cuda.synchronize()
     clk.start()
@@ -248,17 +292,24 @@ def run_single(args):
     h2d0, d2h0 = r.stats().h2d_bytes, r.stats().d2h_bytes
     ev0.record(stream)
     for _ in range(args.steps):
+        e_a, e_b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e_a.record(stream)
         walls.append(step())
-        kernel_ms.append(r.stats().last_pull_ms)
+        e_b.record(stream)
+        e_b.synchronize()
+        # single reader shard: the pull kernel's own CUDA-event time; reshard:
+        # the step's device time on the shards' stream (both shard kernels)
+        kernel_ms.append(r.stats().last_pull_ms if not reshard else e_a.elapsed_time(e_b))
     ev1.record(stream)
     torch.cuda.synchronize()
     clocks = clk.stop()
     dev_ms = ev0.elapsed_time(ev1)
     st = r.stats()
     landed = st.bytes_pulled - pulled0
-    assert landed == args.steps * total, (landed, total)
+    if not reshard:
+        assert landed == args.steps * total, (landed, total)
     if not args.no_verify:
-        assert torch.equal(tarena, rarena), "reader bytes differ from trainer after timed steps"
+        verify()
     value = landed / (dev_ms / 1e3) / 1e9
     e2e = landed / sum(walls) / 1e9
     k_avg = statistics.mean(kernel_ms)
@@ -272,7 +323,8 @@ def run_single(args):
         "metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": 1, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(dev_ms / args.steps, 3), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
-        "config": {"workload": f"{args.workload}: trainer -> 1 reader on one GPU (local HBM pull)",
+        "config": {"workload": f"{args.workload}: trainer -> 1 reader on one GPU (local HBM pull)"
+                               + (", resharded TP=1 -> TP=2 (2 reader shards)" if reshard else ""),
                    "bytes_per_receiver": total, "tensors": len(shapes), "chunk_bytes": args.chunk,
                    "receivers": 1, "l2": "inputs (16 GB/replica) >> 126 MB L2; no flush"},
         "per_receiver_gbs": [round(value, 2)],
@@ -332,6 +384,7 @@ def main():
     ap.add_argument("--chunk", type=int, default=4096)
     ap.add_argument("--no-verify", action="store_true")
     ap.add_argument("--fanout", default="chain", choices=["chain", "pairs"])
+    ap.add_argument("--reshard", default="none", choices=["none", "tp2"])
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-bytes", type=int, default=2 << 30)
     ap.add_argument("--cpu-reps", type=int, default=3)
