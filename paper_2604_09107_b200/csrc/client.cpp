@@ -853,8 +853,18 @@ Status Client::bind_reshard(Shard& sh, const Assignment& a, VersionId v) {
   // assemble, digests not computed); its chunks follow the chunk rule on its
   // own geometry; the plan maps them onto the source shards' chunks.
   if (Status s = ensure_stream(sh); !ok(s)) return s;
-  if (sh.holding && sh.holding->reshard && sh.partial_version && *sh.partial_version == v) {
-    return Status::ok;  // resume the same reshard fill
+  if (sh.holding && sh.holding->reshard && sh.holding->reshard->src_manifests == a.all_manifests &&
+      sh.holding->reshard->src_layouts == a.all_layouts) {
+    // Same source slicing and bytes' manifests: keep the plan and the tables;
+    // a new fill epoch unless this resumes the same version's fill.
+    bool resume = (current_ && *current_ == v) || (sh.partial_version && *sh.partial_version == v);
+    if (!resume) {
+      sh.holding->epoch = ++sh.epoch_ctr;
+      sh.holding->landed_some = false;
+    }
+    sh.holding->reshard->endpoints = a.all_endpoints;
+    sh.partial_version = v;
+    return Status::ok;
   }
   DeviceGuard g(sh.device);
   auto p = std::make_shared<Payload>();
@@ -875,6 +885,8 @@ Status Client::bind_reshard(Shard& sh, const Assignment& a, VersionId v) {
   // Source shards as the planner sees them.
   auto rs = std::make_unique<Reshard>();
   rs->endpoints = a.all_endpoints;
+  rs->src_manifests = a.all_manifests;
+  rs->src_layouts = a.all_layouts;
   for (std::size_t s = 0; s < a.all_manifests.size(); ++s) {
     SourceShard ss;
     auto sm = Manifest::decode(a.all_manifests[s]);
