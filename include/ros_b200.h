@@ -109,6 +109,16 @@ int rs_register(rs_handle* h, uint32_t shard, const char* name, void* dev_ptr, u
 int rs_register_slice(rs_handle* h, uint32_t shard, const char* name, void* dev_ptr,
                       uint64_t bytes, uint64_t rows, uint64_t row_bytes, uint64_t r0, uint64_t nr,
                       uint64_t c0, uint64_t nc);
+/* NEW (K5, no reference counterpart): register a region that receives the
+ * version's bf16 entry `name` (`bytes` bf16 bytes; the slice geometry as in
+ * rs_register_slice, rows == 0 for none) as fp8 e4m3: dev_ptr holds bytes/2
+ * bytes, each element the saturating round-to-nearest-even cast of its bf16
+ * source (NaN -> 0x7F).  Checksums are verified on the bf16 bytes before the
+ * cast.  A replica with any cast region is terminal: it pulls, never serves
+ * or publishes (rs_publish returns the invalid_state status). */
+int rs_register_cast(rs_handle* h, uint32_t shard, const char* name, void* dev_ptr,
+                     uint64_t bytes, uint64_t rows, uint64_t row_bytes, uint64_t r0, uint64_t nr,
+                     uint64_t c0, uint64_t nc);
 /* The chunk length a region of geometry (row_bytes, slice width nc) is cut
  * into: the largest multiple of 128 <= chunk_bytes dividing
  * gcd(nc, row_bytes / align) (chunk_bytes when none). */

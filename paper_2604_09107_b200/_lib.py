@@ -56,6 +56,7 @@ _SIGS = {
     "rs_open": (i32, [vp, cstr, cstr, u32, C.POINTER(RsConfig), C.POINTER(vp)]),
     "rs_register": (i32, [vp, u32, cstr, vp, u64]),
     "rs_register_slice": (i32, [vp, u32, cstr, vp, u64, u64, u64, u64, u64, u64, u64]),
+    "rs_register_cast": (i32, [vp, u32, cstr, vp, u64, u64, u64, u64, u64, u64, u64]),
     "rs_layout_key": (i32, [vp, vp, sz, C.POINTER(sz)]),
     "rs_chunk_len_for": (u32, [u64, u64, u64, u32]),
     "rs_layout": (i32, [vp, u32, vp, sz, C.POINTER(sz)]),

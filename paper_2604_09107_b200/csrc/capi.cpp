@@ -193,6 +193,15 @@ int rs_register_slice(rs_handle* h, uint32_t shard, const char* name, void* dev_
   return st(h->client->register_tensor(shard, name, dev_ptr, bytes, g));
 }
 
+int rs_register_cast(rs_handle* h, uint32_t shard, const char* name, void* dev_ptr,
+                     uint64_t bytes, uint64_t rows, uint64_t row_bytes, uint64_t r0, uint64_t nr,
+                     uint64_t c0, uint64_t nc) {
+  if (!h || !name) return st(rsb::Status::invalid_argument);
+  rsb::Geometry g{rows, row_bytes, r0, nr, c0, nc};
+  if (rows == 0) g = {};
+  return st(h->client->register_tensor(shard, name, dev_ptr, bytes, g, true));
+}
+
 uint32_t rs_chunk_len_for(uint64_t row_bytes, uint64_t nc, uint64_t chunk_bytes, uint32_t align) {
   rsb::Geometry g{1, row_bytes, 0, 1, 0, nc};
   if (row_bytes == 0) g.rows = 0;

@@ -5,6 +5,8 @@
 
 #include <algorithm>
 #include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <thread>
 
@@ -23,14 +25,18 @@ struct DeviceGuard {
   }
 };
 
-Status cuda_status(cudaError_t e) {
-  return e == cudaSuccess ? Status::ok : Status::transfer_failed;
+Status cuda_status(cudaError_t e, const char* what = nullptr, int line = 0) {
+  if (e == cudaSuccess) return Status::ok;
+  static const bool debug = std::getenv("RSB_DEBUG") != nullptr;
+  if (debug && what)
+    std::fprintf(stderr, "[rsb] client.cpp:%d %s -> %s\n", line, what, cudaGetErrorString(e));
+  return Status::transfer_failed;
 }
 
-#define RS_CUDA(expr)                              \
-  do {                                             \
-    cudaError_t _e = (expr);                       \
-    if (_e != cudaSuccess) return cuda_status(_e); \
+#define RS_CUDA(expr)                                          \
+  do {                                                         \
+    cudaError_t _e = (expr);                                   \
+    if (_e != cudaSuccess) return cuda_status(_e, #expr, __LINE__); \
   } while (0)
 
 // cuMemGetAddressRange through the runtime's driver entry point (no libcuda
@@ -401,8 +407,9 @@ Client::~Client() {
 }
 
 Status Client::register_tensor(std::uint32_t shard, const std::string& name, void* ptr,
-                               std::uint64_t len, const Geometry& geo) {
+                               std::uint64_t len, const Geometry& geo, bool cast) {
   if (shard >= num_shards_ || name.empty() || !ptr || len == 0) return Status::invalid_argument;
+  if (cast && (len % 2 || (geo.has() && geo.nc % 2))) return Status::invalid_argument;  // bf16
   if (geo.has() && (geo.nr * geo.nc != len || geo.r0 + geo.nr > geo.rows ||
                     geo.c0 + geo.nc > geo.row_bytes))
     return Status::invalid_argument;
@@ -418,7 +425,7 @@ Status Client::register_tensor(std::uint32_t shard, const std::string& name, voi
   if (sh.device != attr.device) return Status::invalid_argument;  // one device per shard
   if (sh.endpoint.empty()) sh.endpoint = "cuda:" + std::to_string(sh.device);
   sh.by_name[name] = static_cast<std::uint32_t>(sh.regs.size());
-  sh.regs.push_back({name, static_cast<std::uint8_t*>(ptr), len, geo});
+  sh.regs.push_back({name, static_cast<std::uint8_t*>(ptr), len, geo, cast});
   return Status::ok;
 }
 
@@ -441,10 +448,18 @@ std::string Client::layout_key() const {
       mix(v, sizeof(v));
     }
   }
-  if (!any) return "";
+  const std::string mark = terminal() ? "!" : "";
+  if (!any) return mark;
   char buf[32];
   std::snprintf(buf, sizeof(buf), "L%016llx", static_cast<unsigned long long>(h));
-  return buf;
+  return mark + buf;
+}
+
+bool Client::terminal() const {
+  for (const auto& sh : shards_)
+    for (const auto& r : sh.regs)
+      if (r.cast) return true;
+  return false;
 }
 
 void Client::set_shard_endpoint(std::uint32_t shard, std::string ep) {
@@ -625,6 +640,7 @@ Status Client::hash_items(Shard& sh, Payload& p, const std::vector<std::uint32_t
 
 Status Client::prepare_publish(VersionId v, std::vector<std::string>* manifests,
                                std::vector<std::string>* layouts) {
+  if (terminal()) return Status::invalid_state;  // regions hold a cast, not the version
   manifests->clear();
   if (layouts) layouts->clear();
   for (auto& sh : shards_) {
@@ -836,7 +852,7 @@ Status Client::derived_blobs(std::vector<std::string>* manifests,
                              std::vector<std::string>* layouts) const {
   manifests->clear();
   layouts->clear();
-  if (layout_key().empty()) return Status::ok;  // plain replica: nothing derived
+  if (slicing(layout_key()).empty()) return Status::ok;  // plain replica: nothing derived
   for (const auto& sh : shards_) {
     Manifest m;
     std::string enc, lay;
@@ -910,6 +926,7 @@ Status Client::bind_reshard(Shard& sh, const Assignment& a, VersionId v) {
     re.ptr = reinterpret_cast<std::uint64_t>(sh.regs[e].ptr);
     re.len = sh.regs[e].len;
     re.geo = sh.regs[e].geo;
+    re.cast = sh.regs[e].cast;
     re.in_group = p->manifest.group_of(e) >= 0;
     if (!re.in_group) {
       for (std::uint32_t i = 0; i < items.size(); ++i)
@@ -964,8 +981,12 @@ Status Client::launch_fill(Shard& sh, const SourceView& src, bool src_complete) 
   const auto& p = *sh.holding;
   const auto& items = p.manifest.items();
   std::vector<dev::ItemDesc> descs(items.size());
-  for (std::size_t i = 0; i < items.size(); ++i)
+  for (std::size_t i = 0; i < items.size(); ++i) {
     descs[i] = identity_segment(src.item_ptrs[i], p.item_ptrs[i], items[i].length, p.cmap, i);
+    if (!items[i].is_group &&
+        sh.regs[sh.by_name.at(p.manifest.entries[items[i].index].name)].cast)
+      descs[i].chunk_len |= dev::kCastE4M3;
+  }
   const dev::SrcDesc sdesc{reinterpret_cast<const std::uint64_t*>(src.digests),
                            src_complete ? nullptr : reinterpret_cast<const std::uint32_t*>(src.flags),
                            src.epoch, 0};
@@ -1071,9 +1092,9 @@ std::vector<Client::FillOutcome> Client::fill_shards(const std::vector<Assignmen
     for (std::size_t gi = 0; gi < p.manifest.groups.size(); ++gi)
       for (const auto& mem : p.manifest.groups[gi].members) {
         srcs.push_back(reinterpret_cast<std::uint64_t>(p.group_bufs[gi]->p) + mem.offset);
-        dsts.push_back(reinterpret_cast<std::uint64_t>(
-            sh.regs[sh.by_name.at(p.manifest.entries[mem.entry].name)].ptr));
-        ls.push_back(p.manifest.entries[mem.entry].length);
+        const Reg& r = sh.regs[sh.by_name.at(p.manifest.entries[mem.entry].name)];
+        dsts.push_back(reinterpret_cast<std::uint64_t>(r.ptr));
+        ls.push_back(p.manifest.entries[mem.entry].length | (r.cast ? dev::kSpanCastE4M3 : 0));
       }
     if (Status s = copy_spans(sh, srcs, dsts, ls); !ok(s)) out[i] = {s, 0, 0};
   }
@@ -1192,10 +1213,11 @@ Status Client::finish_reshard(Shard& sh) {
     for (std::uint64_t r = 0; r < c.rows; ++r) {
       srcs.push_back(base + c.src_off + r * c.src_stride);
       dsts.push_back(c.dst + r * c.dst_stride);
-      lens.push_back(c.nc);
+      lens.push_back(c.nc | (c.cast ? dev::kSpanCastE4M3 : 0));
     }
   }
   if (Status s = copy_spans(sh, srcs, dsts, lens); !ok(s)) return s;
+  if (terminal()) return Status::ok;  // a cast copy never re-serves: nothing to pack or digest
   // 2) pack this reader's own groups (its tiny slices) for re-serving
   srcs.clear();
   dsts.clear();

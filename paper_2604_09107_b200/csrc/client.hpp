@@ -167,11 +167,15 @@ class Client {
          std::uint32_t num_shards, ClientConfig cfg);
   ~Client();
 
+  // cast: the region receives the version's bf16 bytes (len of them) as
+  // e4m3 (len/2 bytes at ptr, K5); the replica becomes terminal (never serves
+  // or publishes; layout key "!" + its slicing).
   Status register_tensor(std::uint32_t shard, const std::string& name, void* ptr,
-                         std::uint64_t len, const Geometry& geo = {});
+                         std::uint64_t len, const Geometry& geo = {}, bool cast = false);
   void set_shard_endpoint(std::uint32_t shard, std::string ep);
   // Slicing key of the replica ("" when no region carries a geometry).
   std::string layout_key() const;
+  bool terminal() const;  // some region lands as a cast
   void set_stream(std::uint32_t shard, cudaStream_t s);
 
   // --- blocking ops (in-process registry) ---------------------------------
@@ -228,8 +232,9 @@ class Client {
   struct Reg {
     std::string name;
     std::uint8_t* ptr = nullptr;
-    std::uint64_t len = 0;
+    std::uint64_t len = 0;  // bytes of the version's entry (bf16 bytes for a cast region)
     Geometry geo;
+    bool cast = false;      // lands as e4m3: len/2 bytes at ptr
   };
   // Reshard state of a bound payload (Assignment.reshard).
   struct Reshard {

@@ -174,11 +174,34 @@ __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
 }
 
+// Four bf16 (two words, little-endian order) -> four e4m3 bytes (RNE,
+// satfinite), element 0 in the low byte.
+__device__ __forceinline__ std::uint32_t cvt4_e4m3(std::uint32_t a, std::uint32_t b) {
+  const float f0 = __uint_as_float(a << 16), f1 = __uint_as_float(a & 0xffff0000u);
+  const float f2 = __uint_as_float(b << 16), f3 = __uint_as_float(b & 0xffff0000u);
+  std::uint16_t lo, hi;
+  asm("cvt.rn.satfinite.e4m3x2.f32 %0, %1, %2;\n" : "=h"(lo) : "f"(f1), "f"(f0));
+  asm("cvt.rn.satfinite.e4m3x2.f32 %0, %1, %2;\n" : "=h"(hi) : "f"(f3), "f"(f2));
+  return std::uint32_t(lo) | (std::uint32_t(hi) << 16);
+}
+// 16 bf16 (one 32-byte stripe) -> 16 e4m3 bytes.
+__device__ __forceinline__ uint4 cvt16_e4m3(const uint4& a, const uint4& b) {
+  return make_uint4(cvt4_e4m3(a.x, a.y), cvt4_e4m3(a.z, a.w), cvt4_e4m3(b.x, b.y),
+                    cvt4_e4m3(b.z, b.w));
+}
+// Tail bf16 elements (n bytes, even) -> e4m3 bytes.
+__device__ __forceinline__ void cvt_tail_e4m3(const std::uint8_t* src, std::uint8_t* dst, int n) {
+  for (int i = 0; i + 1 < n; i += 2) {
+    const std::uint32_t w = std::uint32_t(src[i]) | (std::uint32_t(src[i + 1]) << 8);
+    dst[i / 2] = static_cast<std::uint8_t>(cvt4_e4m3(w, 0) & 0xFF);
+  }
+}
+
 // XXH64 of one chunk straight from (possibly peer) global memory, optionally
-// storing it to dst: the quiet same-source retry after a mismatch
-// (client_core.cpp:336-357).  Rare path.
+// storing it to dst (as e4m3 when cast): the quiet same-source retry after a
+// mismatch (client_core.cpp:336-357).  Rare path.
 static __device__ __noinline__ std::uint64_t repull_chunk(const std::uint8_t* src, std::uint8_t* dst,
-                                                   std::uint32_t len) {
+                                                   std::uint32_t len, bool cast = false) {
   std::uint64_t v1 = kP1 + kP2, v2 = kP2, v3 = 0, v4 = 0 - kP1;
   std::uint32_t i = 0;
   std::uint8_t tail[32];
@@ -193,14 +216,24 @@ static __device__ __noinline__ std::uint64_t repull_chunk(const std::uint8_t* sr
     v2 = xround(v2, w[1]);
     v3 = xround(v3, w[2]);
     v4 = xround(v4, w[3]);
-    if (dst)
+    if (dst && cast) {
+      const uint4 a = make_uint4(static_cast<std::uint32_t>(w[0]), static_cast<std::uint32_t>(w[0] >> 32),
+                                 static_cast<std::uint32_t>(w[1]), static_cast<std::uint32_t>(w[1] >> 32));
+      const uint4 q = make_uint4(static_cast<std::uint32_t>(w[2]), static_cast<std::uint32_t>(w[2] >> 32),
+                                 static_cast<std::uint32_t>(w[3]), static_cast<std::uint32_t>(w[3] >> 32));
+      const uint4 o = cvt16_e4m3(a, q);
+      const std::uint32_t ow[4] = {o.x, o.y, o.z, o.w};
+      for (int b = 0; b < 16; ++b) dst[i / 2 + b] = static_cast<std::uint8_t>(ow[b >> 2] >> (8 * (b & 3)));
+    } else if (dst) {
       for (int b = 0; b < 32; ++b) dst[i + b] = static_cast<std::uint8_t>(w[b >> 3] >> (8 * (b & 7)));
+    }
   }
   const int t = static_cast<int>(len - i);
   for (int b = 0; b < t; ++b) {
     tail[b] = __ldcg(src + i + b);
-    if (dst) dst[i + b] = tail[b];
+    if (dst && !cast) dst[i + b] = tail[b];
   }
+  if (dst && cast) cvt_tail_e4m3(tail, dst + i / 2, t);
   std::uint64_t h = len >= 32 ? merge4(v1, v2, v3, v4) : kP5;
   h += len;
   return finish_tail(h, tail, t);
@@ -217,6 +250,7 @@ struct ChunkRef {
 __device__ __forceinline__ ChunkRef chunk_ref(const ItemDesc& d, std::uint32_t k) {
   const std::uint32_t c = d.chunk_len & kChunkLenMask;
   const std::uint64_t doff = std::uint64_t(k) * c;
+  const std::uint64_t land = (d.chunk_len & kCastE4M3) ? doff / 2 : doff;
   ChunkRef r{nullptr, nullptr, 0u, 0u};
   if (doff >= d.len) return r;
   std::uint64_t soff;
@@ -230,7 +264,7 @@ __device__ __forceinline__ ChunkRef chunk_ref(const ItemDesc& d, std::uint32_t k
     r.src_chunk = d.src_chunk0 + sc;
   }
   r.src = reinterpret_cast<const std::uint8_t*>(d.src) + soff;
-  r.dst = d.dst ? reinterpret_cast<std::uint8_t*>(d.dst) + doff : nullptr;
+  r.dst = d.dst ? reinterpret_cast<std::uint8_t*>(d.dst) + land : nullptr;
   const std::uint64_t rem = d.len - doff;
   r.clen = static_cast<std::uint32_t>(rem < c ? rem : c);
   return r;

@@ -30,7 +30,7 @@ constexpr int kPiece = 256;       // bytes of each chunk staged per step
 struct ItemDesc {
   std::uint64_t src;         // source address of the segment's first chunk
   std::uint64_t dst;         // landing address of the first chunk (0: hash-only)
-  std::uint64_t len;         // bytes landed by the segment
+  std::uint64_t len;         // source bytes of the segment (landed as-is, or halved by kCastE4M3)
   std::uint32_t chunk0;      // landing chunk index of the first chunk (global)
   std::uint32_t chunk_len;   // chunk length | kHasMap | kMap3D
   std::uint32_t src_chunk0;  // source chunk index of the first chunk
@@ -45,7 +45,11 @@ static_assert(sizeof(ItemDesc) == 48, "ItemDesc layout");
 // stride m*chunk_len, kMap3D) when q < m.  Destination map: 2-D.
 constexpr std::uint32_t kHasMap = 0x80000000u;
 constexpr std::uint32_t kMap3D = 0x40000000u;
-constexpr std::uint32_t kChunkLenMask = 0x3fffffffu;
+// The segment lands as fp8 e4m3 (K5): source chunks are bf16; landing chunk
+// k holds chunk_len/2 bytes at dst + k*chunk_len/2 (saturating RNE cast,
+// oracle ro_bf16_to_e4m3).  Verification is on the bf16 bytes.
+constexpr std::uint32_t kCastE4M3 = 0x20000000u;
+constexpr std::uint32_t kChunkLenMask = 0x1fffffffu;
 constexpr int kMapBoxCols = 128;  // TMA box: 128 bytes x 32 chunks, 128B swizzle
 
 // A source serve state as the reader's device sees it.
@@ -117,6 +121,8 @@ cudaError_t launch_span_digests(const std::uint64_t* ptrs, const std::uint64_t* 
                                 std::uint64_t* out, int n, cudaStream_t s);
 
 // Gather/scatter copies: span i copies lens[i] bytes srcs[i] -> dsts[i].
+// lens[i] | kSpanCastE4M3: the span's bf16 bytes land as e4m3 (lens/2 bytes).
+constexpr std::uint64_t kSpanCastE4M3 = 1ull << 63;
 cudaError_t launch_copy_spans(const std::uint64_t* srcs, const std::uint64_t* dsts,
                               const std::uint64_t* lens, int n, cudaStream_t s);
 

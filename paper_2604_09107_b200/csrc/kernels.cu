@@ -44,7 +44,7 @@ struct LaneChunk {
   const std::uint8_t* src;
   std::uint8_t* dst;
   std::uint32_t len;
-  std::uint32_t pad;
+  std::uint32_t cast;  // lands as e4m3 (the owning lane converts from its slot)
 };
 
 __device__ __forceinline__ void load_step(const LaneChunk* refs, std::uint8_t* stage, int s,
@@ -78,7 +78,7 @@ __device__ __forceinline__ void store_step(const LaneChunk* refs, const std::uin
     const int k = 2 * u + half;
     const LaneChunk r = refs[k];
     const std::uint32_t g = static_cast<std::uint32_t>(s) * kPiece + off;
-    if (r.dst == nullptr || g >= r.len) continue;
+    if (r.dst == nullptr || r.cast || g >= r.len) continue;
     const std::uint8_t* src = stage + k * kSlot + off;
     std::uint8_t* dst = r.dst + g;
     const std::uint32_t n = r.len - g;
@@ -116,7 +116,7 @@ __global__ void __launch_bounds__(kThreads, 2) pull_kernel(const PullParams p) {
       const ItemDesc it = p.items[find_item(p.items, p.n_items, c)];
       r = chunk_ref(it, c - it.chunk0);
       if (r.clen) {
-        mine = {r.src, r.dst, r.clen, 0u};
+        mine = {r.src, r.dst, r.clen, (it.chunk_len & kCastE4M3) ? 1u : 0u};
         sd = &p.srcs[it.src_id];
       }
     }
@@ -174,7 +174,15 @@ __global__ void __launch_bounds__(kThreads, 2) pull_kernel(const PullParams p) {
             v2 = xround(v2, (std::uint64_t(a.w) << 32) | a.z);
             v3 = xround(v3, (std::uint64_t(bq.y) << 32) | bq.x);
             v4 = xround(v4, (std::uint64_t(bq.w) << 32) | bq.z);
+            if (mine.cast && mine.dst) {
+              const uint4 o = cvt16_e4m3(a, bq);
+              const std::uint32_t ow[4] = {o.x, o.y, o.z, o.w};
+              std::uint8_t* cb = mine.dst + g / 2 + 16 * k;
+              for (int bb = 0; bb < 16; ++bb) cb[bb] = static_cast<std::uint8_t>(ow[bb >> 2] >> (8 * (bb & 3)));
+            }
           }
+          if (mine.cast && mine.dst && (n & 31u))
+            cvt_tail_e4m3(slot + (n & ~31u), mine.dst + (g + (n & ~31u)) / 2, static_cast<int>(n & 31u));
           if (g + n == mine.len) {
             std::uint64_t h = mine.len >= 32 ? merge4(v1, v2, v3, v4) : kP5;
             h += mine.len;
@@ -313,11 +321,25 @@ __global__ void copy_spans_kernel(const std::uint64_t* srcs, const std::uint64_t
   if (span >= n) return;
   const std::uint8_t* src = reinterpret_cast<const std::uint8_t*>(srcs[span]);
   std::uint8_t* dst = reinterpret_cast<std::uint8_t*>(dsts[span]);
-  const std::uint64_t len = lens[span];
-  const bool vec =
-      ((reinterpret_cast<std::uintptr_t>(src) | reinterpret_cast<std::uintptr_t>(dst)) & 15) == 0;
+  const std::uint64_t len = lens[span] & ~kSpanCastE4M3;
   const std::uint64_t stride = std::uint64_t(gridDim.x) * blockDim.x;
   const std::uint64_t tid = std::uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (lens[span] & kSpanCastE4M3) {  // bf16 in, e4m3 out (len/2 bytes)
+    const bool v8 = (reinterpret_cast<std::uintptr_t>(src) & 15) == 0 &&
+                    (reinterpret_cast<std::uintptr_t>(dst) & 7) == 0;
+    const std::uint64_t units = v8 ? len / 16 : 0;
+    for (std::uint64_t i = tid; i < units; i += stride) {
+      const uint4 a = reinterpret_cast<const uint4*>(src)[i];
+      reinterpret_cast<uint2*>(dst)[i] = make_uint2(cvt4_e4m3(a.x, a.y), cvt4_e4m3(a.z, a.w));
+    }
+    for (std::uint64_t i = units * 8 + tid; i < len / 2; i += stride) {
+      const std::uint32_t w = std::uint32_t(src[2 * i]) | (std::uint32_t(src[2 * i + 1]) << 8);
+      dst[i] = static_cast<std::uint8_t>(cvt4_e4m3(w, 0) & 0xFF);
+    }
+    return;
+  }
+  const bool vec =
+      ((reinterpret_cast<std::uintptr_t>(src) | reinterpret_cast<std::uintptr_t>(dst)) & 15) == 0;
   if (vec) {
     const std::uint64_t units = len / 16;
     for (std::uint64_t i = tid; i < units; i += stride)

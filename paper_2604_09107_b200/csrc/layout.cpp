@@ -129,11 +129,11 @@ Status plan_reshard(const std::vector<ReaderEntry>& reader, const std::vector<So
       if (aligned) {
         dev::ItemDesc d{};
         d.src = ((a - sg.r0) * sg.nc + (c0 - sg.c0));  // offset; base added by the caller
-        d.dst = r.ptr + (a - rg.r0) * rg.nc;
+        d.dst = r.ptr + (a - rg.r0) * rg.nc / (r.cast ? 2 : 1);
         d.len = (b - a) * (c1 - c0);
         const std::uint64_t m = sg.nc / c, q = (c1 - c0) / c;
         d.chunk0 = r.chunk0 + static_cast<std::uint32_t>((a - rg.r0) * q);
-        d.chunk_len = c;
+        d.chunk_len = c | (r.cast ? dev::kCastE4M3 : 0u);
         d.src_chunk0 = ss.chunk0[item] + static_cast<std::uint32_t>((a - sg.r0) * m + (c0 - sg.c0) / c);
         d.q = static_cast<std::uint16_t>(q);
         d.m = static_cast<std::uint16_t>(m);
@@ -150,12 +150,14 @@ Status plan_reshard(const std::vector<ReaderEntry>& reader, const std::vector<So
         cp.src_item = item;
         cp.src_off = ioff + (a - sg.r0) * sg.nc + (c0 - sg.c0);
         cp.src_stride = sg.nc;
-        cp.dst = r.ptr + (a - rg.r0) * rg.nc + (c0 - rg.c0);
-        cp.dst_stride = rg.nc;
+        const std::uint64_t shrink = r.cast ? 2 : 1;
+        cp.dst = r.ptr + ((a - rg.r0) * rg.nc + (c0 - rg.c0)) / shrink;
+        cp.dst_stride = rg.nc / shrink;
         cp.rows = b - a;
         cp.nc = c1 - c0;
+        cp.cast = r.cast;
         out->copies.push_back(cp);
-        if (!r.in_group &&
+        if (!r.in_group && !r.cast &&
             std::find(out->rehash.begin(), out->rehash.end(), r.item) == out->rehash.end())
           out->rehash.push_back(r.item);
       }

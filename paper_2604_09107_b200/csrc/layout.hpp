@@ -70,6 +70,7 @@ struct SliceCopy {  // rows x nc bytes from a gathered source item into a region
   std::uint64_t src_off = 0, src_stride = 0;
   std::uint64_t dst = 0, dst_stride = 0;
   std::uint64_t rows = 0, nc = 0;
+  bool cast = false;  // region lands as e4m3: dst/dst_stride in e4m3 bytes, nc in bf16 bytes
 };
 
 struct ReshardPlan {
@@ -86,6 +87,7 @@ struct ReaderEntry {
   std::uint64_t ptr = 0;
   std::uint64_t len = 0;
   Geometry geo;
+  bool cast = false;            // lands as e4m3 (ptr holds len/2 bytes)
   bool in_group = false;        // reader packs it into a group
   std::uint32_t item = 0;       // reader item (big entries)
   std::uint32_t chunk0 = 0;     // reader landing chunk index of the item

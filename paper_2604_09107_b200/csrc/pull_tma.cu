@@ -90,6 +90,8 @@ struct Cfg {
     std::uint32_t k0;      // box layout: first chunk of the batch within the segment
     std::uint32_t g;       // box layout: byte offset of the step within the chunk
     std::uint32_t bpiece;  // box layout: bytes per chunk in this step
+    std::uint32_t cast;    // lanes whose chunk lands as e4m3
+    std::uint32_t pad2;
     std::uint64_t dst[32];
     std::uint32_t piece[32];
     std::uint32_t clen[32];
@@ -98,7 +100,7 @@ struct Cfg {
   struct Smem {
     std::uint8_t stage[S][kStage];
     Meta meta[S];
-    ItemDesc items[ITEMS];
+    alignas(16) ItemDesc items[ITEMS];  // copied in with 16-byte vectors
     unsigned long long full[S];
     unsigned long long empty[S];
   };
@@ -190,6 +192,8 @@ __global__ void __launch_bounds__(64, C::kCtas) pull_tma_kernel(const PullParams
       }
       if (__any_sync(full, sd != nullptr && sd->flags != nullptr)) fence_proxy_async_global();
       const std::uint64_t expect = (sd && sd->digests) ? __ldcg(&sd->digests[r.src_chunk]) : 0;
+      const bool is_cast = r.clen && seg < p.n_items && (items[seg].chunk_len & kCastE4M3);
+      const std::uint32_t cast_mask = __ballot_sync(full, is_cast);
       const std::uint32_t seg0 = __shfl_sync(full, seg, 0);
       const std::uint32_t k0 = __shfl_sync(full, k, 0);
       const std::uint32_t q0 = seg0 < p.n_items ? items[seg0].q : 1;
@@ -212,7 +216,9 @@ __global__ void __launch_bounds__(64, C::kCtas) pull_tma_kernel(const PullParams
         const bool last = s + 1 == nsteps;
         m.piece[lane] = piece;
         m.clen[lane] = r.clen;
+        m.dst[lane] = r.dst ? reinterpret_cast<std::uint64_t>(r.dst + (is_cast ? g / 2 : g)) : 0;
         if (last) m.expect[lane] = expect;
+        if (lane == 0) m.cast = cast_mask;
         if (box) {
           if (lane == 0) {
             m.batch = b;
@@ -243,7 +249,6 @@ __global__ void __launch_bounds__(64, C::kCtas) pull_tma_kernel(const PullParams
           std::uint8_t* slot = sm.stage[stage] + lane * C::kSlot;
           const std::uint32_t bulk = src_vec ? (piece & ~15u) : 0;
           for (std::uint32_t kk = bulk; kk < piece; ++kk) slot[kk] = __ldcg(r.src + g + kk);
-          m.dst[lane] = r.dst ? reinterpret_cast<std::uint64_t>(r.dst + g) : 0;
           std::uint32_t tx = bulk;
 #pragma unroll
           for (int o = 16; o > 0; o >>= 1) tx += __shfl_xor_sync(full, tx, o);
@@ -315,9 +320,12 @@ __global__ void __launch_bounds__(64, C::kCtas) pull_tma_kernel(const PullParams
         v4 = 0 - kP1;
       }
       const int stripes = static_cast<int>(piece >> 5);
+      const bool lane_cast = (m.cast >> lane) & 1u;
+      auto* castp = reinterpret_cast<uint4*>(lane_cast ? m.dst[lane] : 0);  // e4m3 landing
       if (box) {
-        // 1) land: one tensor store per box, issued by lane 0
-        if (lane == 0 && items[m.item].dst != 0) {
+        // 1) land: one tensor store per box, issued by lane 0 (a cast batch
+        //    lands from registers in the hash loop instead)
+        if (lane == 0 && items[m.item].dst != 0 && m.cast == 0) {
           const std::uint8_t* dmap = maps + 256 * std::size_t(m.item) + 128;
           fence_proxy_async_smem();
           for (std::uint32_t j = 0; j < m.bpiece / kMapBoxCols; ++j)
@@ -338,6 +346,7 @@ __global__ void __launch_bounds__(64, C::kCtas) pull_tma_kernel(const PullParams
           v2 = xround(v2, (std::uint64_t(a.w) << 32) | a.z);
           v3 = xround(v3, (std::uint64_t(q.y) << 32) | q.x);
           v4 = xround(v4, (std::uint64_t(q.w) << 32) | q.z);
+          if (castp) castp[kk] = cvt16_e4m3(a, q);
         }
         if (clen && s * kP + piece == clen) {
           std::uint64_t h = clen >= 32 ? merge4(v1, v2, v3, v4) : kP5;
@@ -347,7 +356,7 @@ __global__ void __launch_bounds__(64, C::kCtas) pull_tma_kernel(const PullParams
       } else {
         std::uint8_t* slot = st + lane * C::kSlot;
         const std::uint64_t dstp = m.dst[lane];
-        if (dstp && piece) {
+        if (dstp && piece && !lane_cast) {
           const std::uint32_t bulk = (dstp & 15) == 0 ? (piece & ~15u) : 0;
           if (bulk) {
             fence_proxy_async_smem();
@@ -358,6 +367,7 @@ __global__ void __launch_bounds__(64, C::kCtas) pull_tma_kernel(const PullParams
           for (std::uint32_t kk = bulk; kk < piece; ++kk)
             reinterpret_cast<std::uint8_t*>(dstp)[kk] = slot[kk];
         }
+        const bool cast_vec = castp && (reinterpret_cast<std::uintptr_t>(castp) & 15) == 0;
 #pragma unroll 4
         for (int kk = 0; kk < stripes; ++kk) {
           const uint4 a = *reinterpret_cast<const uint4*>(slot + 32 * kk);
@@ -366,7 +376,18 @@ __global__ void __launch_bounds__(64, C::kCtas) pull_tma_kernel(const PullParams
           v2 = xround(v2, (std::uint64_t(a.w) << 32) | a.z);
           v3 = xround(v3, (std::uint64_t(q.y) << 32) | q.x);
           v4 = xround(v4, (std::uint64_t(q.w) << 32) | q.z);
+          if (cast_vec) {
+            castp[kk] = cvt16_e4m3(a, q);
+          } else if (castp) {
+            const uint4 o = cvt16_e4m3(a, q);
+            const std::uint32_t ow[4] = {o.x, o.y, o.z, o.w};
+            auto* cb = reinterpret_cast<std::uint8_t*>(castp) + 16 * kk;
+            for (int bb = 0; bb < 16; ++bb) cb[bb] = static_cast<std::uint8_t>(ow[bb >> 2] >> (8 * (bb & 3)));
+          }
         }
+        if (castp && (piece & 31u))
+          cvt_tail_e4m3(slot + (piece & ~31u), reinterpret_cast<std::uint8_t*>(castp) + (piece & ~31u) / 2,
+                        static_cast<int>(piece & 31u));
         if (clen && s * kP + piece == clen) {
           std::uint64_t h = clen >= 32 ? merge4(v1, v2, v3, v4) : kP5;
           h += clen;
@@ -392,7 +413,7 @@ __global__ void __launch_bounds__(64, C::kCtas) pull_tma_kernel(const PullParams
         bulk_wait<0>();  // earlier stores of these chunks must not land after the re-pull
         if (!lane_ok) {
           const ChunkRef rr = chunk_ref(*dseg, c - dseg->chunk0);
-          digest = repull_chunk(rr.src, rr.dst, clen);
+          digest = repull_chunk(rr.src, rr.dst, clen, (dseg->chunk_len & kCastE4M3) != 0);
           lane_ok = digest == expect;
         }
         const unsigned bad = __ballot_sync(full, !lane_ok);

@@ -84,7 +84,8 @@ cudaError_t upload_pull_plan(int device, cudaStream_t s, ItemDesc* items, std::u
   for (std::uint32_t i = 0; i < n; ++i) {
     ItemDesc& d = items[i];
     const std::uint64_t c = d.chunk_len & kChunkLenMask;
-    d.chunk_len = static_cast<std::uint32_t>(c);
+    const bool cast = (d.chunk_len & kCastE4M3) != 0;  // lands from registers: no dst map
+    d.chunk_len = static_cast<std::uint32_t>(c) | (cast ? kCastE4M3 : 0u);
     if (d.q == 0) d.q = 1;
     if (d.m == 0) d.m = d.q;
     const std::uint64_t q = d.q, m = d.m;
@@ -95,7 +96,7 @@ cudaError_t upload_pull_plan(int device, cudaStream_t s, ItemDesc* items, std::u
       auto* mp = reinterpret_cast<CUtensorMap*>(host.data() + maps_off + 256 * std::size_t(i));
       // 2-D: one row per chunk; 3-D: one row per source row (q chunks each)
       ok = encode(mp, d.src, c, q, m, q == m ? full : full / q);
-      if (ok && d.dst) ok = encode(mp + 1, d.dst, c, 1, 1, full);
+      if (ok && d.dst && !cast) ok = encode(mp + 1, d.dst, c, 1, 1, full);
     }
     if (ok) {
       d.chunk_len |= kHasMap | (q < m ? kMap3D : 0u);

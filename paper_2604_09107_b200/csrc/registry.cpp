@@ -145,10 +145,13 @@ std::set<VersionId> Registry::available(ModelState& m, const std::string& dc) {
 
 bool Registry::still_good(const Rep& c, const Rep& reader, VersionId v) const {
   if (&c == &reader || c.life == Life::failed || c.version != v) return false;
+  // A terminal copy (its regions hold a cast of the version's bytes) never
+  // serves: its landed bytes are not the bytes the digests describe.
+  if (terminal_layout(c.layout)) return false;
   bool complete_copy = c.visible && c.life == Life::published && c.complete_all();
   // A differently sliced copy serves only a reshard-capable reader, and only
   // once complete (chasing is item-for-item).
-  if (c.layout != reader.layout) return complete_copy && !reader.layout.empty();
+  if (c.layout != slicing(reader.layout)) return complete_copy && !slicing(reader.layout).empty();
   bool pipeline_copy = cfg_.pipeline && c.life == Life::replicating &&
                        !c.seeding && c.dc == reader.dc;
   return complete_copy || pipeline_copy;
@@ -157,9 +160,9 @@ bool Registry::still_good(const Rep& c, const Rep& reader, VersionId v) const {
 bool Registry::servable(ModelState& m, VersionId v, const Rep& reader) {
   auto vit = m.versions.find(v);
   if (vit == m.versions.end()) return false;
-  auto lit = vit->second.by_layout.find(reader.layout);
+  auto lit = vit->second.by_layout.find(slicing(reader.layout));
   if (lit != vit->second.by_layout.end()) return lit->second.num_shards == reader.num_shards;
-  return !reader.layout.empty();  // reshard from another slicing
+  return !slicing(reader.layout).empty();  // reshard from another slicing
 }
 
 Registry::Rep* Registry::pick_source(ModelState& m, VersionId v,
@@ -171,7 +174,7 @@ Registry::Rep* Registry::pick_source(ModelState& m, VersionId v,
   auto key = [&](const Rep* c) {
     const std::string& ep0 = c->endpoints.empty() ? c->name : c->endpoints[0];
     return std::make_tuple(1 /* no own seed buffers */, c->dc == reader.dc ? 0 : 1,
-                           c->layout == reader.layout ? 0 : 1, topo_(rep0, ep0), c->serving,
+                           c->layout == slicing(reader.layout) ? 0 : 1, topo_(rep0, ep0), c->serving,
                            c->last_assigned, std::cref(c->name));
   };
   auto vit = m.versions.find(v);
@@ -195,7 +198,7 @@ Assignment Registry::make_assignment(ModelState& m, Rep& src, VersionId v,
   a.source_complete = src.life == Life::published && src.complete_all();
   a.cross_dc = src.dc != reader.dc;
   const LayoutInfo& li = m.versions[v].by_layout[src.layout];
-  if (src.layout == reader.layout) {
+  if (src.layout == slicing(reader.layout)) {
     a.manifest = shard < li.manifests.size() ? li.manifests[shard] : "";
     a.layout = shard < li.layouts.size() ? li.layouts[shard] : "";
   } else {
@@ -218,6 +221,7 @@ Status Registry::publish(const std::string& model, const std::string& replica,
   if (r->txn) return Status::invalid_state;
   if (manifests.size() != r->num_shards) return Status::invalid_argument;
   if (!layouts.empty() && layouts.size() != r->num_shards) return Status::invalid_argument;
+  if (terminal_layout(r->layout)) return Status::invalid_state;  // holds a cast, not the bytes
   auto reject = [&](Status s, const char* why) {
     if (why)
       trace("publish_reject", {{"model", model}, {"replica", replica}, {"v", n2s(v)},
@@ -497,7 +501,8 @@ void Registry::apply_settle(Rep& r) {
                        {"v", n2s(*t.target)}, {"src", t.source},
                        {"cross_dc", src->dc != r.dc ? "1" : "0"},
                        {"src_serving", n2s(src->serving)}});
-      if (src->layout != r.layout && r.derived_manifests.size() == r.num_shards) {
+      if (src->layout != r.layout && !terminal_layout(r.layout) &&
+          r.derived_manifests.size() == r.num_shards) {
         // a resharding fill: its slicing becomes a layout of the version
         auto& vi = m.versions[*t.target];
         if (!vi.by_layout.count(r.layout)) {

@@ -40,6 +40,13 @@
 
 namespace rsb {
 
+// Layout keys: "" is the reference's single slicing, "L<hash>" another
+// slicing (layout.hpp).  A leading '!' marks a terminal replica -- one whose
+// regions receive a cast of the version (K5, bf16 -> e4m3): it pulls like a
+// replica of the slicing after the '!', but never serves or publishes.
+inline bool terminal_layout(const std::string& k) { return !k.empty() && k[0] == '!'; }
+inline std::string slicing(const std::string& k) { return terminal_layout(k) ? k.substr(1) : k; }
+
 // messages.hpp:40-52, plus the layout fields of the B200 path.
 struct Assignment {
   VersionId version = 0;

@@ -253,6 +253,20 @@ class Handle:
                                             tensor.numel() * tensor.element_size(), rows, w, r0, nr,
                                             c0, nc))
 
+    def register_cast(self, shard: int, name: str, tensor, nbytes: int, geometry=None) -> Status:
+        """Register an fp8 e4m3 region (uint8 / float8_e4m3fn, nbytes/2
+        bytes) that receives the version's bf16 entry `name` (nbytes bf16
+        bytes) cast on landing (K5).  geometry as for register_slice, or None.
+        The replica becomes terminal: it pulls, never serves or publishes."""
+        if not tensor.is_cuda or not tensor.is_contiguous():
+            return Status.invalid_argument
+        if tensor.numel() * tensor.element_size() * 2 != nbytes:
+            return Status.invalid_argument
+        self._keep.append(tensor)
+        rows, w, r0, nr, c0, nc = (int(x) for x in (geometry or (0, 0, 0, 0, 0, 0)))
+        return Status(lib.rs_register_cast(self.h, shard, _b(name), C.c_void_p(tensor.data_ptr()),
+                                           nbytes, rows, w, r0, nr, c0, nc))
+
     def layout(self, shard: int = 0) -> bytes:
         return _read_bytes(lib.rs_layout, self.h, shard)
 
