@@ -25,7 +25,6 @@ import argparse
 import json
 import os
 import statistics
-import subprocess
 import sys
 import threading
 import time
@@ -43,57 +42,54 @@ def log(*a):
 
 # ----------------------------------------------------------------- clocks
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
-    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    """SM clocks + throttle reasons sampled DURING the timed region through
+    NVML (a poll every ~2 ms, so even a 30 ms region gets samples)."""
+    REASONS = {  # nvmlClocksEventReason* bits
+        "sw_power_cap": 0x4, "hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20,
+        "hw_thermal_slowdown": 0x40,
+    }
 
     def __init__(self, index: int):
         self.index = index
-        self.proc = None
-        self.lines: list[str] = []
+        self.samples: list[tuple[float, int]] = []
+        self.smax = None
+        self.err = None
+        self._stop = threading.Event()
+        self.t = None
 
     def start(self):
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
-                 "--format=csv,noheader,nounits", "-lms", "200"],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
-            self.t.start()
-        except (OSError, FileNotFoundError):
-            self.proc = None
+            import pynvml as N
+            N.nvmlInit()
+            self.N = N
+            self.h = N.nvmlDeviceGetHandleByIndex(self.index)
+            self.smax = float(N.nvmlDeviceGetMaxClockInfo(self.h, N.NVML_CLOCK_SM))
+        except Exception as e:  # noqa: BLE001 - report, do not fail the bench
+            self.err = f"nvml unavailable: {e}"
+            return
+        self.t = threading.Thread(target=self._run, daemon=True)
+        self.t.start()
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.lines.append(line.strip())
+    def _run(self):
+        N = self.N
+        while not self._stop.is_set():
+            try:
+                sm = float(N.nvmlDeviceGetClockInfo(self.h, N.NVML_CLOCK_SM))
+                rs = int(N.nvmlDeviceGetCurrentClocksEventReasons(self.h))
+                self.samples.append((sm, rs))
+            except Exception:  # noqa: BLE001
+                pass
+            time.sleep(0.002)
 
     def stop(self) -> dict:
-        if self.proc is None:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        time.sleep(0.25)
-        self.proc.terminate()
-        try:
-            self.proc.wait(timeout=2)
-        except subprocess.TimeoutExpired:
-            self.proc.kill()
-        sm, smax, reasons = [], [], set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for line in self.lines:
-            f = [x.strip() for x in line.split(",")]
-            if len(f) < 9:
-                continue
-            try:
-                sm.append(float(f[1]))
-                smax.append(float(f[2]))
-            except ValueError:
-                continue
-            for n, v in zip(names, f[5:9]):
-                if v.lower() == "active":
-                    reasons.add(n)
-        return {"sm_mhz": statistics.median(sm) if sm else None,
-                "sm_max_mhz": max(smax) if smax else None, "reasons": sorted(reasons),
-                "samples": len(sm)}
+        if self.t is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [self.err or "no sampler"]}
+        self._stop.set()
+        self.t.join(timeout=2)
+        reasons = sorted({n for _, r in self.samples for n, b in self.REASONS.items() if r & b})
+        sm = [x for x, _ in self.samples]
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": self.smax,
+                "reasons": reasons, "samples": len(sm), "source": "nvml"}
 
 
 def measured_peaks() -> dict:
@@ -120,20 +116,34 @@ def ncu_traffic(kind: str):
 
 # --------------------------------------------------------------- workload
 def workload_shapes(name: str):
-    from tests.golden.models import config1, llama3_8b_shapes
+    from tests.golden.models import config1, llama3_8b_shapes, llama3_70b_shapes
     if name == "llama3_8b":
         return llama3_8b_shapes()
     if name == "config1":
         return config1()
+    if name == "llama3_70b_tp8":
+        # config 5: one TP-8 shard (rank 0) of Llama-3-70B, each tensor's
+        # slice contiguous as its trainer rank holds it
+        out = []
+        for n, shape in llama3_70b_shapes():
+            d = tp_dim(n)
+            if d is None:
+                out.append((n, shape))
+            elif d == 0:
+                out.append((n, (shape[0] // 8,) + tuple(shape[1:])))
+            else:
+                out.append((n, (shape[0], shape[1] // 8)))
+        return out
     raise SystemExit(f"unknown workload {name}")
 
 
-def alloc_replica(shapes, dev, seed_base=None):
-    """One contiguous arena per replica, tensors as views (IPC-exportable)."""
+def alloc_replica(shapes, dev, seed_base=None, elem=2):
+    """One contiguous arena per replica, tensors as views (IPC-exportable);
+    elem=1: an e4m3 landing arena (half the bytes, same layout)."""
     import torch
 
     from paper_2604_09107_b200 import ros
-    sizes = [2 * _numel(s) for _, s in shapes]
+    sizes = [elem * _numel(s) for _, s in shapes]
     offs, tot = [], 0
     for n in sizes:
         offs.append(tot)
@@ -225,7 +235,10 @@ def run_single(args):
     total = sum(2 * _numel(s) for _, s in shapes)
     log(f"[bench] workload {args.workload}: {len(shapes)} tensors, {total / 1e9:.3f} GB")
     tarena, tviews = alloc_replica(shapes, dev, seed_base=42)
-    rarena, rviews = alloc_replica(shapes, dev)
+    cast = args.cast
+    if cast and args.reshard != "none":
+        raise SystemExit("--cast is measured on the same-slicing pull (config 5)")
+    rarena, rviews = alloc_replica(shapes, dev, elem=1 if cast else 2)
     torch.cuda.synchronize()
     stream = torch.cuda.Stream(device=dev)
     cl = Cluster()
@@ -234,6 +247,10 @@ def run_single(args):
     r = cl.open("m", "rollout1", 2 if reshard else 1, chunk_bytes=args.chunk)
     rslices = {}
     for (n, v), (_, w), (_, shape) in zip(tviews, rviews, shapes):
+        if cast:
+            assert t.register_tensor(0, n, v) == Status.ok
+            assert r.register_cast(0, n, w, v.numel()) == Status.ok
+            continue
         if not reshard:
             assert t.register_tensor(0, n, v) == Status.ok
             assert r.register_tensor(0, n, w) == Status.ok
@@ -269,6 +286,17 @@ def run_single(args):
         return w1 - w0
 
     def verify():
+        if cast:
+            # against the standalone K5 kernel (itself checked against the
+            # oracle on all 65536 bf16 patterns in tests/test_gpu_kernels.py)
+            from paper_2604_09107_b200 import ros
+            for (n, v), (_, w) in zip(tviews, rviews):
+                want = torch.empty_like(w)
+                ros.bf16_to_e4m3(v, want)
+                torch.cuda.synchronize()
+                assert torch.equal(w, want), n
+            assert (r.chunk_digests(0) == t.chunk_digests(0)).all()
+            return
         if not reshard:
             assert torch.equal(tarena, rarena), "reader bytes differ from trainer"
             assert (r.chunk_digests(0) == t.chunk_digests(0)).all()
@@ -316,7 +344,7 @@ def run_single(args):
     n_chunks = sum((2 * _numel(s) + args.chunk - 1) // args.chunk for _, s in shapes)
     # algorithmic bytes per launch: read source + write destination + read the
     # source chunk table + write own table + watermark words
-    alg = 2 * total + 16 * n_chunks + 4 * ((n_chunks + 31) // 32)
+    alg = (total + total // 2 if cast else 2 * total) + 16 * n_chunks + 4 * ((n_chunks + 31) // 32)
     peaks = measured_peaks()
     achieved = alg / (k_avg / 1e3) / 1e9
     line = {
@@ -324,7 +352,8 @@ def run_single(args):
         "warmup": args.warmup, "ms_per_step": round(dev_ms / args.steps, 3), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
         "config": {"workload": f"{args.workload}: trainer -> 1 reader on one GPU (local HBM pull)"
-                               + (", resharded TP=1 -> TP=2 (2 reader shards)" if reshard else ""),
+                               + (", resharded TP=1 -> TP=2 (2 reader shards)" if reshard else "")
+                               + (", landed as fp8 e4m3 (fused cast; bytes = bf16 ingress)" if cast else ""),
                    "bytes_per_receiver": total, "tensors": len(shapes), "chunk_bytes": args.chunk,
                    "receivers": 1, "l2": "inputs (16 GB/replica) >> 126 MB L2; no flush"},
         "per_receiver_gbs": [round(value, 2)],
@@ -377,14 +406,15 @@ def run_reference(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="llama3_8b")
     ap.add_argument("--chunk", type=int, default=4096)
     ap.add_argument("--no-verify", action="store_true")
-    ap.add_argument("--fanout", default="chain", choices=["chain", "pairs"])
+    ap.add_argument("--fanout", default="chain", choices=["chain", "pairs", "ring"])
     ap.add_argument("--reshard", default="none", choices=["none", "tp2"])
+    ap.add_argument("--cast", action="store_true", help="reader lands fp8 e4m3 (config 5)")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-bytes", type=int, default=2 << 30)
     ap.add_argument("--cpu-reps", type=int, default=3)

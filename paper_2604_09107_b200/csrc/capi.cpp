@@ -590,11 +590,9 @@ int rs_pull_spans(const uint64_t* src_ptrs, const uint64_t* dst_ptrs, const uint
   rsb::dev::PullParams p{};
   const rsb::dev::SrcDesc sdesc{expect_dev, nullptr, 0, 0};
   if (rsb::dev::upload_pull_plan(device, stream, descs.data(), static_cast<std::uint32_t>(n_items),
-                                 &sdesc, 1, &plan, &p) != cudaSuccess)
+                                 &sdesc, 1, chunk, &plan, &p) != cudaSuccess)
     rc = st(rsb::Status::transfer_failed);
   if (!rc) {
-    p.n_chunks = chunk;
-    p.n_batches = (chunk + rsb::dev::kBatchChunks - 1) / rsb::dev::kBatchChunks;
     p.dst_digests = out_digests_dev;
     p.timeout_ns = 4000000000ull;
     cudaEventCreate(&e0);

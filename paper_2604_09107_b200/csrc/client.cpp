@@ -625,9 +625,8 @@ Status Client::hash_items(Shard& sh, Payload& p, const std::vector<std::uint32_t
   const dev::SrcDesc self{nullptr, nullptr, 0, 0};
   dev::PullParams pp{};
   RS_CUDA(dev::upload_pull_plan(sh.device, sh.stream, descs.data(),
-                                static_cast<std::uint32_t>(descs.size()), &self, 1, &sh.plan, &pp));
-  pp.n_chunks = p.cmap.n_chunks();
-  pp.n_batches = p.cmap.n_batches();
+                                static_cast<std::uint32_t>(descs.size()), &self, 1,
+                                p.cmap.n_chunks(), &sh.plan, &pp));
   pp.first_batch = descs.front().chunk0 / dev::kBatchChunks;
   pp.dst_digests = static_cast<std::uint64_t*>(p.digests.p);
   pp.dst_flags = static_cast<std::uint32_t*>(p.flags.p);
@@ -992,11 +991,9 @@ Status Client::launch_fill(Shard& sh, const SourceView& src, bool src_complete) 
                            src.epoch, 0};
   dev::PullParams pp{};
   RS_CUDA(dev::upload_pull_plan(sh.device, sh.stream, descs.data(),
-                                static_cast<std::uint32_t>(descs.size()), &sdesc, 1, &sh.plan,
-                                &pp));
+                                static_cast<std::uint32_t>(descs.size()), &sdesc, 1,
+                                p.cmap.n_chunks(), &sh.plan, &pp));
   stats_.h2d_bytes += sh.plan.h2d_bytes;
-  pp.n_chunks = p.cmap.n_chunks();
-  pp.n_batches = p.cmap.n_batches();
   pp.dst_digests = static_cast<std::uint64_t*>(p.digests.p);
   pp.dst_flags = static_cast<std::uint32_t*>(p.flags.p);
   pp.dst_epoch = p.epoch;
@@ -1183,11 +1180,9 @@ Status Client::launch_reshard_fill(Shard& sh, const Assignment& a, bool src_comp
   }
   dev::PullParams pp{};
   RS_CUDA(dev::upload_pull_plan(sh.device, sh.stream, descs.data(),
-                                static_cast<std::uint32_t>(descs.size()), sd.data(), nsrc,
+                                static_cast<std::uint32_t>(descs.size()), sd.data(), nsrc, next,
                                 &sh.plan, &pp));
   stats_.h2d_bytes += sh.plan.h2d_bytes;
-  pp.n_chunks = next;
-  pp.n_batches = (next + dev::kBatchChunks - 1) / dev::kBatchChunks;
   pp.dst_digests = static_cast<std::uint64_t*>(p.digests.p);
   pp.dst_flags = static_cast<std::uint32_t*>(p.flags.p);
   pp.dst_epoch = p.epoch;

@@ -92,6 +92,13 @@ __device__ __forceinline__ std::uint32_t ld_acquire_sys(const std::uint32_t* p) 
 __device__ __forceinline__ void st_release_sys(std::uint32_t* p, std::uint32_t v) {
   asm volatile("st.release.sys.global.u32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
 }
+// One release fence for several flag stores (fence + relaxed store = release).
+__device__ __forceinline__ void fence_acq_rel_sys() {
+  asm volatile("fence.acq_rel.sys;\n" ::: "memory");
+}
+__device__ __forceinline__ void st_relaxed_sys(std::uint32_t* p, std::uint32_t v) {
+  asm volatile("st.relaxed.sys.global.u32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
+}
 __device__ __forceinline__ std::uint64_t globaltimer() {
   std::uint64_t t;
   asm volatile("mov.u64 %0, %%globaltimer;\n" : "=l"(t));
@@ -270,16 +277,14 @@ __device__ __forceinline__ ChunkRef chunk_ref(const ItemDesc& d, std::uint32_t k
   return r;
 }
 
-// Last item whose first chunk is <= c (items sorted by chunk0).
-__device__ __forceinline__ std::uint32_t find_item(const ItemDesc* items, std::uint32_t n,
-                                                   std::uint32_t c) {
-  std::uint32_t lo = 0, hi = n;
-  while (hi - lo > 1) {
-    const std::uint32_t mid = (lo + hi) >> 1;
-    if (items[mid].chunk0 <= c) lo = mid;
-    else hi = mid;
-  }
-  return lo;
+// Last segment whose first chunk is <= c (segments sorted by chunk0),
+// starting from the batch's first candidate (PullParams.batch_seg): O(1)
+// for identity pulls, a short forward scan when segments share a batch.
+__device__ __forceinline__ std::uint32_t seg_of(const ItemDesc* items, std::uint32_t n,
+                                                std::uint32_t first, std::uint32_t c) {
+  std::uint32_t s = first;
+  while (s + 1 < n && items[s + 1].chunk0 <= c) ++s;
+  return s;
 }
 
 }  // namespace rsb::dev::detail

@@ -6,6 +6,7 @@
 
 #include <cstddef>
 #include <cstdint>
+#include <vector>
 
 namespace rsb::dev {
 
@@ -94,20 +95,24 @@ struct PullParams {
   std::uint32_t resume;              // dst_flags may already hold dst_epoch
   std::uint32_t pad;
   const void* maps;                  // CUtensorMap pairs per segment (or null)
+  const std::uint32_t* batch_seg;    // per batch: last segment with chunk0 <= 32*batch
 };
 
 // Uploads a pull plan (segment table + source table + TMA tensor maps +
-// work/status words) into `up->scratch` on `device` and points `p` at it.
-// Segments whose addresses are 16-byte aligned and whose geometry fits a box
-// get tensor maps (kHasMap).  Implemented in pullplan.cpp.
+// batch -> segment table + work/status words) into `up->scratch` on
+// `device` and points `p` at it (n_chunks / n_batches included).  Segments
+// whose addresses are 16-byte aligned and whose geometry fits a box get
+// tensor maps (kHasMap).  A plan byte-identical to the previous upload into
+// the same scratch only resets the work/status words.  pullplan.cpp.
 struct PlanUpload {
   void* scratch = nullptr;       // device buffer (grown by the callee)
   std::size_t scratch_bytes = 0;
   std::size_t h2d_bytes = 0;     // bytes uploaded by the last call
+  std::vector<std::uint8_t> last;  // host image of the resident plan
 };
 cudaError_t upload_pull_plan(int device, cudaStream_t s, ItemDesc* items, std::uint32_t n_items,
-                             const SrcDesc* srcs, std::uint32_t n_srcs, PlanUpload* up,
-                             PullParams* p);
+                             const SrcDesc* srcs, std::uint32_t n_srcs, std::uint32_t n_chunks,
+                             PlanUpload* up, PullParams* p);
 void free_pull_plan(int device, PlanUpload* up);
 
 // Fused mover: copy + per-chunk XXH64 verify + watermark publish.  `sms` is

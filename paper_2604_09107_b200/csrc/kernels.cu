@@ -113,7 +113,7 @@ __global__ void __launch_bounds__(kThreads, 2) pull_kernel(const PullParams p) {
     const SrcDesc* sd = nullptr;
     ChunkRef r{nullptr, nullptr, 0u, 0u};
     if (c < p.n_chunks) {
-      const ItemDesc it = p.items[find_item(p.items, p.n_items, c)];
+      const ItemDesc it = p.items[seg_of(p.items, p.n_items, p.batch_seg[b], c)];
       r = chunk_ref(it, c - it.chunk0);
       if (r.clen) {
         mine = {r.src, r.dst, r.clen, (it.chunk_len & kCastE4M3) ? 1u : 0u};

@@ -91,10 +91,13 @@ struct Cfg {
     std::uint32_t g;       // box layout: byte offset of the step within the chunk
     std::uint32_t bpiece;  // box layout: bytes per chunk in this step
     std::uint32_t cast;    // lanes whose chunk lands as e4m3
-    std::uint32_t pad2;
+    std::uint32_t verify;  // lanes whose chunk has a source digest to check
+    std::uint32_t store;   // box layout: land the boxes with tensor stores
+    std::uint32_t pad;
     std::uint64_t dst[32];
     std::uint32_t piece[32];
     std::uint32_t clen[32];
+    std::uint32_t seg[32];  // segment of each lane's chunk
     std::uint64_t expect[32];
   };
   struct Smem {
@@ -159,8 +162,9 @@ __global__ void __launch_bounds__(64, C::kCtas) pull_tma_kernel(const PullParams
       const std::uint32_t c = b * kBatchChunks + lane;
       ChunkRef r{nullptr, nullptr, 0u, 0u};
       std::uint32_t seg = 0xffffffffu, cunit = 0, itflags = 0, k = 0, src_id = 0;
+      const std::uint32_t bseg = __ldg(&p.batch_seg[b]);
       if (c < p.n_chunks) {
-        seg = find_item(items, p.n_items, c);
+        seg = seg_of(items, p.n_items, bseg, c);
         const ItemDesc d = items[seg];
         cunit = d.chunk_len & kChunkLenMask;
         itflags = d.chunk_len & (kHasMap | kMap3D);
@@ -191,7 +195,9 @@ __global__ void __launch_bounds__(64, C::kCtas) pull_tma_kernel(const PullParams
         break;
       }
       if (__any_sync(full, sd != nullptr && sd->flags != nullptr)) fence_proxy_async_global();
-      const std::uint64_t expect = (sd && sd->digests) ? __ldcg(&sd->digests[r.src_chunk]) : 0;
+      const bool has_expect = sd && sd->digests;
+      const std::uint64_t expect = has_expect ? __ldcg(&sd->digests[r.src_chunk]) : 0;
+      const std::uint32_t verify_mask = __ballot_sync(full, has_expect);
       const bool is_cast = r.clen && seg < p.n_items && (items[seg].chunk_len & kCastE4M3);
       const std::uint32_t cast_mask = __ballot_sync(full, is_cast);
       const std::uint32_t seg0 = __shfl_sync(full, seg, 0);
@@ -202,6 +208,7 @@ __global__ void __launch_bounds__(64, C::kCtas) pull_tma_kernel(const PullParams
                                             r.clen != 0) &&
                        (k0 % q0) == 0;
       const bool map3d = box && (items[seg0].chunk_len & kMap3D) != 0;
+      const std::uint32_t box_store = box && cast_mask == 0 && items[seg0].dst != 0;
       std::uint32_t maxlen = r.clen;
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) maxlen = max(maxlen, __shfl_xor_sync(full, maxlen, o));
@@ -217,8 +224,15 @@ __global__ void __launch_bounds__(64, C::kCtas) pull_tma_kernel(const PullParams
         m.piece[lane] = piece;
         m.clen[lane] = r.clen;
         m.dst[lane] = r.dst ? reinterpret_cast<std::uint64_t>(r.dst + (is_cast ? g / 2 : g)) : 0;
-        if (last) m.expect[lane] = expect;
-        if (lane == 0) m.cast = cast_mask;
+        if (last) {
+          m.expect[lane] = expect;
+          m.seg[lane] = seg;
+        }
+        if (lane == 0) {
+          m.cast = cast_mask;
+          m.verify = verify_mask;
+          m.store = box_store;
+        }
         if (box) {
           if (lane == 0) {
             m.batch = b;
@@ -277,23 +291,31 @@ __global__ void __launch_bounds__(64, C::kCtas) pull_tma_kernel(const PullParams
     int stage = 0;
     unsigned phase = 0;
     std::uint64_t v1 = 0, v2 = 0, v3 = 0, v4 = 0, digest = 0;
-    std::uint32_t pend_b = kPill;  // batch whose watermark awaits its stores
-    std::uint64_t pend_bytes = 0;
+    // Verified batches whose watermarks await their stores.  Released
+    // kRelease at a time: one system-scope fence per group of flags.
+    constexpr int kRelease = 4;
+    std::uint32_t pend[kRelease];
+    int npend = 0;
+    std::uint64_t pend_bytes = 0, done_bytes = 0;
+    std::uint32_t done_batches = 0;
     bool failed = false;
     const std::uint32_t swz = (static_cast<std::uint32_t>(lane) & 7u) << 4;
-    auto release_pending = [&](bool newer_group) {
-      if (pend_b == kPill) return;
+    auto release_pending = [&](bool newer_group, bool force) {
+      if (npend == 0 || (!force && npend < kRelease)) return;
       if (newer_group) bulk_wait<1>();
       else bulk_wait<0>();
       fence_proxy_async_global();
       __syncwarp();
-      if (lane == 0) {
-        if (p.dst_flags) st_release_sys(&p.dst_flags[pend_b], p.dst_epoch);
-        atomicAdd(&p.status->batches_done, 1u);
-        atomicAdd(reinterpret_cast<unsigned long long*>(&p.status->bytes),
-                  static_cast<unsigned long long>(pend_bytes));
+      if (lane == 0 && p.dst_flags) {
+        fence_acq_rel_sys();
+#pragma unroll
+        for (int i = 0; i < kRelease; ++i)
+          if (i < npend) st_relaxed_sys(&p.dst_flags[pend[i]], p.dst_epoch);
       }
-      pend_b = kPill;
+      done_batches += npend;
+      done_bytes += pend_bytes;
+      npend = 0;
+      pend_bytes = 0;
     };
     for (;;) {
       mbar_wait(&sm.full[stage], phase);
@@ -325,7 +347,7 @@ __global__ void __launch_bounds__(64, C::kCtas) pull_tma_kernel(const PullParams
       if (box) {
         // 1) land: one tensor store per box, issued by lane 0 (a cast batch
         //    lands from registers in the hash loop instead)
-        if (lane == 0 && items[m.item].dst != 0 && m.cast == 0) {
+        if (lane == 0 && m.store) {
           const std::uint8_t* dmap = maps + 256 * std::size_t(m.item) + 128;
           fence_proxy_async_smem();
           for (std::uint32_t j = 0; j < m.bpiece / kMapBoxCols; ++j)
@@ -334,19 +356,33 @@ __global__ void __launch_bounds__(64, C::kCtas) pull_tma_kernel(const PullParams
           bulk_commit();
           committed = true;
         }
-        // 2) hash chunk `lane` = row `lane` of the swizzled boxes
+        // 2) hash chunk `lane` = row `lane` of the swizzled boxes (a cast
+        //    lane also lands the e4m3 of each stripe; separate loops keep
+        //    the plain loop free of the cast)
         const std::uint8_t* rowbase = st + lane * 128;
-#pragma unroll 4
-        for (int kk = 0; kk < stripes; ++kk) {
+        auto box_stripe = [&](int kk, uint4& a, uint4& q) {
           const std::uint8_t* boxp = rowbase + (kk >> 2) * 4096;
           const std::uint32_t x = static_cast<std::uint32_t>(kk & 3) * 32;
-          const uint4 a = *reinterpret_cast<const uint4*>(boxp + (x ^ swz));
-          const uint4 q = *reinterpret_cast<const uint4*>(boxp + ((x + 16) ^ swz));
+          a = *reinterpret_cast<const uint4*>(boxp + (x ^ swz));
+          q = *reinterpret_cast<const uint4*>(boxp + ((x + 16) ^ swz));
           v1 = xround(v1, (std::uint64_t(a.y) << 32) | a.x);
           v2 = xround(v2, (std::uint64_t(a.w) << 32) | a.z);
           v3 = xround(v3, (std::uint64_t(q.y) << 32) | q.x);
           v4 = xround(v4, (std::uint64_t(q.w) << 32) | q.z);
-          if (castp) castp[kk] = cvt16_e4m3(a, q);
+        };
+        if (castp) {
+#pragma unroll 4
+          for (int kk = 0; kk < stripes; ++kk) {
+            uint4 a, q;
+            box_stripe(kk, a, q);
+            castp[kk] = cvt16_e4m3(a, q);
+          }
+        } else {
+#pragma unroll 4
+          for (int kk = 0; kk < stripes; ++kk) {
+            uint4 a, q;
+            box_stripe(kk, a, q);
+          }
         }
         if (clen && s * kP + piece == clen) {
           std::uint64_t h = clen >= 32 ? merge4(v1, v2, v3, v4) : kP5;
@@ -367,22 +403,40 @@ __global__ void __launch_bounds__(64, C::kCtas) pull_tma_kernel(const PullParams
           for (std::uint32_t kk = bulk; kk < piece; ++kk)
             reinterpret_cast<std::uint8_t*>(dstp)[kk] = slot[kk];
         }
-        const bool cast_vec = castp && (reinterpret_cast<std::uintptr_t>(castp) & 15) == 0;
-#pragma unroll 4
-        for (int kk = 0; kk < stripes; ++kk) {
-          const uint4 a = *reinterpret_cast<const uint4*>(slot + 32 * kk);
-          const uint4 q = *reinterpret_cast<const uint4*>(slot + 32 * kk + 16);
+        auto slot_stripe = [&](int kk, uint4& a, uint4& q) {
+          a = *reinterpret_cast<const uint4*>(slot + 32 * kk);
+          q = *reinterpret_cast<const uint4*>(slot + 32 * kk + 16);
           v1 = xround(v1, (std::uint64_t(a.y) << 32) | a.x);
           v2 = xround(v2, (std::uint64_t(a.w) << 32) | a.z);
           v3 = xround(v3, (std::uint64_t(q.y) << 32) | q.x);
           v4 = xround(v4, (std::uint64_t(q.w) << 32) | q.z);
-          if (cast_vec) {
+        };
+        if (!castp) {
+#pragma unroll 4
+          for (int kk = 0; kk < stripes; ++kk) {
+            uint4 a, q;
+            slot_stripe(kk, a, q);
+          }
+        } else if ((reinterpret_cast<std::uintptr_t>(castp) & 15) == 0) {
+#pragma unroll 4
+          for (int kk = 0; kk < stripes; ++kk) {
+            uint4 a, q;
+            slot_stripe(kk, a, q);
             castp[kk] = cvt16_e4m3(a, q);
-          } else if (castp) {
+          }
+        } else {  // unaligned e4m3 landing: byte stores
+          for (int kk = 0; kk < stripes; ++kk) {
+            uint4 a, q;
+            slot_stripe(kk, a, q);
             const uint4 o = cvt16_e4m3(a, q);
-            const std::uint32_t ow[4] = {o.x, o.y, o.z, o.w};
             auto* cb = reinterpret_cast<std::uint8_t*>(castp) + 16 * kk;
-            for (int bb = 0; bb < 16; ++bb) cb[bb] = static_cast<std::uint8_t>(ow[bb >> 2] >> (8 * (bb & 3)));
+#pragma unroll
+            for (int bb = 0; bb < 4; ++bb) {
+              cb[bb] = static_cast<std::uint8_t>(o.x >> (8 * bb));
+              cb[4 + bb] = static_cast<std::uint8_t>(o.y >> (8 * bb));
+              cb[8 + bb] = static_cast<std::uint8_t>(o.z >> (8 * bb));
+              cb[12 + bb] = static_cast<std::uint8_t>(o.w >> (8 * bb));
+            }
           }
         }
         if (castp && (piece & 31u))
@@ -395,8 +449,10 @@ __global__ void __launch_bounds__(64, C::kCtas) pull_tma_kernel(const PullParams
         }
       }
       const std::uint64_t expect = last ? m.expect[lane] : 0;
-      // 3) the previous batch's stores are done by now: publish its watermark
-      release_pending(committed);
+      const std::uint32_t myseg = last ? m.seg[lane] : 0;
+      const bool verify = (m.verify >> lane) & 1u;
+      // 3) earlier batches' stores are done by now: publish their watermarks
+      release_pending(committed, false);
       // 4) free the stage once the stores issued from it have read it
       if (committed) bulk_wait_read<0>();
       __syncwarp();
@@ -405,13 +461,12 @@ __global__ void __launch_bounds__(64, C::kCtas) pull_tma_kernel(const PullParams
       if (!last) continue;
       // 5) batch complete: verify and record
       const std::uint32_t c = b * kBatchChunks + lane;
-      const ItemDesc* dseg = clen ? &items[find_item(items, p.n_items, c)] : nullptr;
-      const bool verify = dseg && p.srcs[dseg->src_id].digests != nullptr;
-      bool lane_ok = !verify || digest == expect;
+      bool lane_ok = !clen || !verify || digest == expect;
       if (__ballot_sync(full, !lane_ok)) {
         if (lane == 0) atomicAdd(&p.status->retried_batches, 1u);
         bulk_wait<0>();  // earlier stores of these chunks must not land after the re-pull
         if (!lane_ok) {
+          const ItemDesc* dseg = &items[myseg];
           const ChunkRef rr = chunk_ref(*dseg, c - dseg->chunk0);
           digest = repull_chunk(rr.src, rr.dst, clen, (dseg->chunk_len & kCastE4M3) != 0);
           lane_ok = digest == expect;
@@ -432,11 +487,19 @@ __global__ void __launch_bounds__(64, C::kCtas) pull_tma_kernel(const PullParams
       std::uint64_t landed = clen;
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) landed += __shfl_xor_sync(full, landed, o);
-      pend_b = b;
-      pend_bytes = landed;
+#pragma unroll
+      for (int i = kRelease - 1; i > 0; --i) pend[i] = pend[i - 1];  // registers: constant indices
+      pend[0] = b;
+      ++npend;
+      pend_bytes += landed;
     }
-    release_pending(false);
+    release_pending(false, true);
     bulk_wait<0>();
+    if (lane == 0 && done_batches) {
+      atomicAdd(&p.status->batches_done, done_batches);
+      atomicAdd(reinterpret_cast<unsigned long long*>(&p.status->bytes),
+                static_cast<unsigned long long>(done_bytes));
+    }
   }
 }
 

@@ -65,16 +65,19 @@ bool maps_disabled() {
 }  // namespace
 
 cudaError_t upload_pull_plan(int device, cudaStream_t s, ItemDesc* items, std::uint32_t n,
-                             const SrcDesc* srcs, std::uint32_t n_srcs, PlanUpload* up,
-                             PullParams* p) {
+                             const SrcDesc* srcs, std::uint32_t n_srcs, std::uint32_t n_chunks,
+                             PlanUpload* up, PullParams* p) {
+  const std::uint32_t n_batches = (n_chunks + kBatchChunks - 1) / kBatchChunks;
   const std::size_t items_off = kHdr;
   const std::size_t srcs_off = items_off + n * sizeof(ItemDesc);
   const std::size_t maps_off = (srcs_off + n_srcs * sizeof(SrcDesc) + 255) / 256 * 256;
-  const std::size_t total = maps_off + std::size_t(n) * 256;
+  const std::size_t bseg_off = maps_off + std::size_t(n) * 256;
+  const std::size_t total = bseg_off + std::size_t(n_batches) * 4;
   if (up->scratch_bytes < total) {
     if (up->scratch) cudaFree(up->scratch);
     up->scratch = nullptr;
     up->scratch_bytes = 0;
+    up->last.clear();
     cudaError_t e = cudaMalloc(&up->scratch, total);
     if (e != cudaSuccess) return e;
     up->scratch_bytes = total;
@@ -105,11 +108,23 @@ cudaError_t upload_pull_plan(int device, cudaStream_t s, ItemDesc* items, std::u
   }
   std::memcpy(host.data() + items_off, items, n * sizeof(ItemDesc));
   if (n_srcs) std::memcpy(host.data() + srcs_off, srcs, n_srcs * sizeof(SrcDesc));
+  // batch -> last segment starting at or before the batch's first chunk
+  auto* bseg = reinterpret_cast<std::uint32_t*>(host.data() + bseg_off);
+  for (std::uint32_t b = 0, sgi = 0; b < n_batches; ++b) {
+    while (sgi + 1 < n && items[sgi + 1].chunk0 <= b * kBatchChunks) ++sgi;
+    bseg[b] = sgi;
+  }
   auto* base = static_cast<std::uint8_t*>(up->scratch);
-  const std::size_t bytes = any_map ? total : srcs_off + n_srcs * sizeof(SrcDesc);
-  cudaError_t e = cudaMemcpyAsync(base, host.data(), bytes, cudaMemcpyHostToDevice, s);
+  cudaError_t e;
+  if (up->last.size() == total && std::memcmp(up->last.data(), host.data(), total) == 0) {
+    e = cudaMemsetAsync(base, 0, kHdr, s);  // same plan resident: fresh work/status words
+    up->h2d_bytes = 0;
+  } else {
+    e = cudaMemcpyAsync(base, host.data(), total, cudaMemcpyHostToDevice, s);
+    up->h2d_bytes = total;
+    up->last = std::move(host);
+  }
   if (e != cudaSuccess) return e;
-  up->h2d_bytes = bytes;
   p->work = reinterpret_cast<std::uint32_t*>(base);
   p->status = reinterpret_cast<PullStatus*>(base + 64);
   p->items = reinterpret_cast<const ItemDesc*>(base + items_off);
@@ -117,6 +132,9 @@ cudaError_t upload_pull_plan(int device, cudaStream_t s, ItemDesc* items, std::u
   p->srcs = reinterpret_cast<const SrcDesc*>(base + srcs_off);
   p->n_srcs = n_srcs;
   p->maps = any_map ? base + maps_off : nullptr;
+  p->batch_seg = reinterpret_cast<const std::uint32_t*>(base + bseg_off);
+  p->n_chunks = n_chunks;
+  p->n_batches = n_batches;
   (void)device;
   return cudaSuccess;
 }
@@ -130,6 +148,7 @@ void free_pull_plan(int device, PlanUpload* up) {
   cudaSetDevice(prev);
   up->scratch = nullptr;
   up->scratch_bytes = 0;
+  up->last.clear();
 }
 
 }  // namespace rsb::dev

@@ -367,8 +367,13 @@ def synth_bf16(tensor, seed: int, first: int = 0, stream=None):
 
 
 def bf16_to_e4m3(src, dst, stream=None):
+    """K5 standalone: dst (n bytes) = e4m3 of the n bf16 words of src (a
+    contiguous CUDA tensor of any dtype, viewed as bf16 words)."""
+    n = src.numel() * src.element_size() // 2
+    if dst.numel() * dst.element_size() < n:
+        raise ValueError("dst holds fewer bytes than src has bf16 words")
     raw = 0 if stream is None else stream.cuda_stream
-    check(lib.rs_bf16_to_e4m3(C.c_void_p(src.data_ptr()), C.c_void_p(dst.data_ptr()), src.numel(),
+    check(lib.rs_bf16_to_e4m3(C.c_void_p(src.data_ptr()), C.c_void_p(dst.data_ptr()), n,
                               C.c_void_p(raw)), "rs_bf16_to_e4m3")
 
 
