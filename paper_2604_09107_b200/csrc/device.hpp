@@ -93,7 +93,7 @@ struct PullParams {
   PullStatus* status;
   std::uint64_t timeout_ns;
   std::uint32_t resume;              // dst_flags may already hold dst_epoch
-  std::uint32_t pad;
+  std::uint32_t has_cast;            // some segment lands as e4m3 (kernel shape choice)
   const void* maps;                  // CUtensorMap pairs per segment (or null)
   const std::uint32_t* batch_seg;    // per batch: last segment with chunk0 <= 32*batch
 };

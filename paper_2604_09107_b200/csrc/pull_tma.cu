@@ -103,7 +103,7 @@ struct Cfg {
   struct Smem {
     std::uint8_t stage[S][kStage];
     Meta meta[S];
-    alignas(16) ItemDesc items[ITEMS];  // copied in with 16-byte vectors
+    alignas(16) ItemDesc items[ITEMS > 0 ? ITEMS : 1];  // ITEMS == 0: segments stay in global  // copied in with 16-byte vectors
     unsigned long long full[S];
     unsigned long long empty[S];
   };
@@ -130,7 +130,7 @@ __global__ void __launch_bounds__(64, C::kCtas) pull_tma_kernel(const PullParams
     }
   };
 
-  const bool smem_items = p.n_items <= static_cast<std::uint32_t>(C::kItems);
+  const bool smem_items = C::kItems > 0 && p.n_items <= static_cast<std::uint32_t>(C::kItems);
   if (smem_items) {
     const uint4* s = reinterpret_cast<const uint4*>(p.items);
     uint4* d = reinterpret_cast<uint4*>(sm.items);
@@ -525,11 +525,14 @@ using V0 = Cfg<512, 3, 3, 320>;
 using V1 = Cfg<512, 4, 2, 576>;
 using V2 = Cfg<1024, 3, 2, 192>;
 using V3 = Cfg<256, 6, 3, 192>;
+using V4 = Cfg<512, 3, 4, 0>;  // segment table in global (L1-cached): 4 CTAs per SM
+using V5 = Cfg<512, 2, 6, 0>;  // 2-stage rings, 6 CTAs per SM
+using V6 = Cfg<256, 3, 7, 0>;  // 7 CTAs per SM
 
-int variant() {
+int variant() {  // -1: by workload
   static const int v = [] {
     const char* e = std::getenv("RSB_TMA_VARIANT");
-    return e ? std::atoi(e) : 0;
+    return e ? std::atoi(e) : -1;
   }();
   return v;
 }
@@ -537,10 +540,18 @@ int variant() {
 }  // namespace
 
 cudaError_t launch_pull_tma(const PullParams& p, int sms, cudaStream_t s) {
-  switch (variant()) {
+  // Measured on B200 (profiles/r1/variants.txt): plain pulls are fastest with
+  // 3 CTAs/SM and the segment table in shared memory (V0); a cast pull's
+  // consumers do ~60% more work per byte and want the 4th CTA (V4).
+  int v = variant();
+  if (v < 0) v = p.has_cast ? 4 : 0;
+  switch (v) {
     case 1: return launch_variant<V1>(p, sms, s);
     case 2: return launch_variant<V2>(p, sms, s);
     case 3: return launch_variant<V3>(p, sms, s);
+    case 4: return launch_variant<V4>(p, sms, s);
+    case 5: return launch_variant<V5>(p, sms, s);
+    case 6: return launch_variant<V6>(p, sms, s);
     default: return launch_variant<V0>(p, sms, s);
   }
 }

@@ -84,10 +84,12 @@ cudaError_t upload_pull_plan(int device, cudaStream_t s, ItemDesc* items, std::u
   }
   std::vector<std::uint8_t> host(total, 0);
   bool any_map = false;
+  std::uint32_t any_cast = 0;
   for (std::uint32_t i = 0; i < n; ++i) {
     ItemDesc& d = items[i];
     const std::uint64_t c = d.chunk_len & kChunkLenMask;
-    const bool cast = (d.chunk_len & kCastE4M3) != 0;  // lands from registers: no dst map
+    const bool cast = (d.chunk_len & kCastE4M3) != 0;
+    any_cast |= cast ? 1u : 0u;  // lands from registers: no dst map
     d.chunk_len = static_cast<std::uint32_t>(c) | (cast ? kCastE4M3 : 0u);
     if (d.q == 0) d.q = 1;
     if (d.m == 0) d.m = d.q;
@@ -134,6 +136,7 @@ cudaError_t upload_pull_plan(int device, cudaStream_t s, ItemDesc* items, std::u
   p->maps = any_map ? base + maps_off : nullptr;
   p->batch_seg = reinterpret_cast<const std::uint32_t*>(base + bseg_off);
   p->n_chunks = n_chunks;
+  p->has_cast = any_cast;
   p->n_batches = n_batches;
   (void)device;
   return cudaSuccess;
