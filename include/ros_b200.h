@@ -119,6 +119,15 @@ int rs_register_slice(rs_handle* h, uint32_t shard, const char* name, void* dev_
 int rs_register_cast(rs_handle* h, uint32_t shard, const char* name, void* dev_ptr,
                      uint64_t bytes, uint64_t rows, uint64_t row_bytes, uint64_t r0, uint64_t nr,
                      uint64_t c0, uint64_t nc);
+/* Replicas whose shards live in several processes (one process per GPU).
+ * A shard is local to a handle once a region of it is registered there; the
+ * split-phase calls (rs_prepare_publish, rs_transfer_*) act on local shards
+ * only.  The replica's slicing key (rs_layout_key) is rs_combine_layout_key
+ * of every shard's rs_shard_hash, gathered from the processes holding them. */
+int rs_shard_local(rs_handle* h, uint32_t shard);
+int rs_shard_hash(rs_handle* h, uint32_t shard, uint64_t* hash, int* geometry, int* cast);
+int rs_combine_layout_key(uint32_t n, const uint64_t* hashes, const int* geometry, const int* cast,
+                          char* buf, size_t cap, size_t* len);
 /* The chunk length a region of geometry (row_bytes, slice width nc) is cut
  * into: the largest multiple of 128 <= chunk_bytes dividing
  * gcd(nc, row_bytes / align) (chunk_bytes when none). */

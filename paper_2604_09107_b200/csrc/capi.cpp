@@ -208,6 +208,27 @@ uint32_t rs_chunk_len_for(uint64_t row_bytes, uint64_t nc, uint64_t chunk_bytes,
   return rsb::chunk_len_for(g, chunk_bytes, align);
 }
 
+int rs_shard_local(rs_handle* h, uint32_t shard) {
+  return h && h->client->is_local(shard) ? 1 : 0;
+}
+
+int rs_shard_hash(rs_handle* h, uint32_t shard, uint64_t* hash, int* geometry, int* cast) {
+  if (!h || shard >= h->client->num_shards()) return st(rsb::Status::invalid_argument);
+  const auto sh = h->client->shard_hash(shard);
+  if (hash) *hash = sh.hash;
+  if (geometry) *geometry = sh.geometry ? 1 : 0;
+  if (cast) *cast = sh.cast ? 1 : 0;
+  return 0;
+}
+
+int rs_combine_layout_key(uint32_t n, const uint64_t* hashes, const int* geometry, const int* cast,
+                          char* buf, size_t cap, size_t* len) {
+  if (n && (!hashes || !geometry || !cast)) return st(rsb::Status::invalid_argument);
+  std::vector<rsb::Client::ShardHash> hs(n);
+  for (uint32_t i = 0; i < n; ++i) hs[i] = {hashes[i], geometry[i] != 0, cast[i] != 0};
+  return put_bytes(rsb::Client::combine_layout_key(hs), buf, cap, len);
+}
+
 int rs_layout_key(rs_handle* h, char* buf, size_t cap, size_t* len) {
   if (!h) return st(rsb::Status::invalid_argument);
   return put_bytes(h->client->layout_key(), buf, cap, len);
@@ -457,16 +478,18 @@ int rs_commit_publish(rs_handle* h, uint64_t version, int status) {
 int rs_transfer_bind(rs_handle* h, uint64_t version) {
   if (!h) return st(rsb::Status::invalid_argument);
   auto& cl = *h->client;
-  std::vector<rsb::Assignment> as;
+  std::vector<rsb::Assignment> as(cl.num_shards());
   for (std::uint32_t i = 0; i < cl.num_shards(); ++i) {
+    if (!cl.is_local(i)) continue;  // bound by the process that holds it
     auto a = h->cluster->reg.current_assignment(cl.model(), cl.replica(), i);
     if (!a) return st(a.status());
-    as.push_back(std::move(*a));
+    as[i] = std::move(*a);
   }
   auto s = cl.bind_all(as, version);
   h->pending.clear();
   if (rsb::ok(s))
-    for (std::uint32_t i = 0; i < cl.num_shards(); ++i) h->pending.push_back(i);
+    for (std::uint32_t i = 0; i < cl.num_shards(); ++i)
+      if (cl.is_local(i)) h->pending.push_back(i);
   return st(s);
 }
 

@@ -429,30 +429,55 @@ Status Client::register_tensor(std::uint32_t shard, const std::string& name, voi
   return Status::ok;
 }
 
-std::string Client::layout_key() const {
-  // FNV-1a over (shard, name, length, geometry) of every region; plain
-  // replicas (no geometry anywhere) keep the reference's single slicing "".
-  bool any = false;
+namespace {
+struct Fnv {
   std::uint64_t h = 1469598103934665603ull;
-  auto mix = [&](const void* p, std::size_t n) {
+  void mix(const void* p, std::size_t n) {
     const auto* b = static_cast<const unsigned char*>(p);
     for (std::size_t i = 0; i < n; ++i) h = (h ^ b[i]) * 1099511628211ull;
-  };
-  for (const auto& sh : shards_) {
-    mix(&sh.idx, sizeof(sh.idx));
-    for (const auto& r : sh.regs) {
-      any |= r.geo.has();
-      mix(r.name.data(), r.name.size());
-      const std::uint64_t v[7] = {r.len, r.geo.rows, r.geo.row_bytes, r.geo.r0,
-                                  r.geo.nr, r.geo.c0, r.geo.nc};
-      mix(v, sizeof(v));
-    }
   }
-  const std::string mark = terminal() ? "!" : "";
+};
+}  // namespace
+
+Client::ShardHash Client::shard_hash(std::uint32_t shard) const {
+  // FNV-1a over (shard, name, length, geometry) of the shard's regions
+  ShardHash out;
+  if (shard >= num_shards_) return out;
+  const Shard& sh = shards_[shard];
+  Fnv f;
+  f.mix(&sh.idx, sizeof(sh.idx));
+  for (const auto& r : sh.regs) {
+    out.geometry |= r.geo.has();
+    out.cast |= r.cast;
+    f.mix(r.name.data(), r.name.size());
+    const std::uint64_t v[7] = {r.len, r.geo.rows, r.geo.row_bytes, r.geo.r0,
+                                r.geo.nr, r.geo.c0, r.geo.nc};
+    f.mix(v, sizeof(v));
+  }
+  out.hash = f.h;
+  return out;
+}
+
+std::string Client::combine_layout_key(const std::vector<ShardHash>& shards) {
+  // plain replicas (no geometry anywhere) keep the reference's single slicing ""
+  bool any = false, cast = false;
+  Fnv f;
+  for (const auto& s : shards) {
+    any |= s.geometry;
+    cast |= s.cast;
+    f.mix(&s.hash, sizeof(s.hash));
+  }
+  const std::string mark = cast ? "!" : "";
   if (!any) return mark;
   char buf[32];
-  std::snprintf(buf, sizeof(buf), "L%016llx", static_cast<unsigned long long>(h));
+  std::snprintf(buf, sizeof(buf), "L%016llx", static_cast<unsigned long long>(f.h));
   return mark + buf;
+}
+
+std::string Client::layout_key() const {
+  std::vector<ShardHash> hs;
+  for (std::uint32_t i = 0; i < num_shards_; ++i) hs.push_back(shard_hash(i));
+  return combine_layout_key(hs);
 }
 
 bool Client::terminal() const {
@@ -643,6 +668,11 @@ Status Client::prepare_publish(VersionId v, std::vector<std::string>* manifests,
   manifests->clear();
   if (layouts) layouts->clear();
   for (auto& sh : shards_) {
+    if (sh.device < 0) {  // another process publishes it
+      manifests->emplace_back();
+      if (layouts) layouts->emplace_back();
+      continue;
+    }
     std::shared_ptr<Payload> p;
     if (Status s = build_payload(sh, v, &p); !ok(s)) return s;
     sh.holding = std::move(p);
@@ -657,6 +687,11 @@ bool Client::derived_layout(std::vector<std::string>* manifests,
   manifests->clear();
   layouts->clear();
   for (const auto& sh : shards_) {
+    if (sh.device < 0) {
+      manifests->emplace_back();
+      layouts->emplace_back();
+      continue;
+    }
     if (!sh.holding || !sh.holding->reshard) return false;
     manifests->push_back(sh.holding->encoded);
     layouts->push_back(sh.holding->layout);
@@ -672,6 +707,7 @@ Result<std::string> Client::layout_bytes(std::uint32_t shard) const {
 void Client::commit_publish(VersionId v, Status st) {
   if (!ok(st)) return;
   for (auto& sh : shards_) {
+    if (sh.device < 0) continue;
     sh.partial_version.reset();
     serve(sh, v, true);
   }
@@ -851,8 +887,15 @@ Status Client::derived_blobs(std::vector<std::string>* manifests,
                              std::vector<std::string>* layouts) const {
   manifests->clear();
   layouts->clear();
-  if (slicing(layout_key()).empty()) return Status::ok;  // plain replica: nothing derived
+  bool any_geo = false;
+  for (std::uint32_t i = 0; i < num_shards_; ++i) any_geo |= shard_hash(i).geometry;
+  if (!any_geo) return Status::ok;  // plain replica: nothing derived
   for (const auto& sh : shards_) {
+    if (sh.device < 0) {  // a shard of this replica held by another process
+      manifests->emplace_back();
+      layouts->emplace_back();
+      continue;
+    }
     Manifest m;
     std::string enc, lay;
     if (Status s = derive(sh, &m, &enc, &lay, nullptr); !ok(s)) return s;
@@ -963,6 +1006,7 @@ Status Client::bind_reshard(Shard& sh, const Assignment& a, VersionId v) {
 Status Client::bind_all(const std::vector<Assignment>& as, VersionId v) {
   if (as.size() != num_shards_) return Status::protocol_error;
   for (std::uint32_t i = 0; i < num_shards_; ++i) {
+    if (!is_local(i)) continue;
     if (as[i].version != v) return Status::protocol_error;
     Status s = as[i].reshard ? bind_reshard(shards_[i], as[i], v) : bind(shards_[i], as[i], v);
     if (!ok(s)) return s;
@@ -971,7 +1015,8 @@ Status Client::bind_all(const std::vector<Assignment>& as, VersionId v) {
   // shard verifies, this replica holds no coherent version.
   current_.reset();
   published_ = false;
-  for (auto& sh : shards_) serve(sh, v, false);
+  for (auto& sh : shards_)
+    if (sh.device >= 0) serve(sh, v, false);
   return Status::ok;
 }
 
@@ -1244,6 +1289,7 @@ Status Client::finish_reshard(Shard& sh) {
 void Client::finish_transfers(VersionId v, bool good) {
   if (good) {
     for (auto& sh : shards_) {
+      if (sh.device < 0 || !sh.holding) continue;
       sh.partial_version.reset();
       {
         std::lock_guard lk(sh.serve->m);

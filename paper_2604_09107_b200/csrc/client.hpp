@@ -173,9 +173,26 @@ class Client {
   Status register_tensor(std::uint32_t shard, const std::string& name, void* ptr,
                          std::uint64_t len, const Geometry& geo = {}, bool cast = false);
   void set_shard_endpoint(std::uint32_t shard, std::string ep);
-  // Slicing key of the replica ("" when no region carries a geometry).
+  // Slicing key of the replica ("" when no region carries a geometry;
+  // "!" prefix when some region lands as a cast).  combine_layout_key of
+  // every shard's shard_hash: a replica whose shards live in several
+  // processes gets the same key from the gathered per-shard hashes.
   std::string layout_key() const;
-  bool terminal() const;  // some region lands as a cast
+  struct ShardHash {
+    std::uint64_t hash = 0;
+    bool geometry = false;  // some region of the shard carries a geometry
+    bool cast = false;      // some region of the shard lands as e4m3
+  };
+  ShardHash shard_hash(std::uint32_t shard) const;
+  static std::string combine_layout_key(const std::vector<ShardHash>& shards);
+  bool terminal() const;  // some local region lands as a cast
+  // A shard is local when this process registered its regions.  A replica
+  // whose shards live in several processes (one process per GPU) has a
+  // Client in each, every one driving only its local shards; the split-phase
+  // calls then skip the others.
+  bool is_local(std::uint32_t shard) const {
+    return shard < num_shards_ && shards_[shard].device >= 0;
+  }
   void set_stream(std::uint32_t shard, cudaStream_t s);
 
   // --- blocking ops (in-process registry) ---------------------------------

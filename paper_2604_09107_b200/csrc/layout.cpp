@@ -106,6 +106,13 @@ Status plan_reshard(const std::vector<ReaderEntry>& reader, const std::vector<So
   for (const auto& r : reader) {
     const Geometry rg = r.geo.has() ? r.geo : full_geometry(r.len);
     std::uint64_t covered = 0;
+    // Source slices already taken for this region.  Replicated tensors (a
+    // norm every TP rank holds whole) overlap identically: the first source
+    // serves, the rest are skipped; TP/FSDP slices are disjoint.
+    struct Rect {
+      std::uint64_t a, b, c0, c1;
+    };
+    std::vector<Rect> taken;
     for (std::uint32_t si = 0; si < srcs.size(); ++si) {
       const SourceShard& ss = srcs[si];
       const int e = entry_of(ss.manifest, r.name);
@@ -119,6 +126,16 @@ Status plan_reshard(const std::vector<ReaderEntry>& reader, const std::vector<So
       const std::uint64_t a = std::max(rg.r0, sg.r0), b = std::min(rg.r0 + rg.nr, sg.r0 + sg.nr);
       const std::uint64_t c0 = std::max(rg.c0, sg.c0), c1 = std::min(rg.c0 + rg.nc, sg.c0 + sg.nc);
       if (a >= b || c0 >= c1) continue;
+      bool dup = false, partial = false;
+      for (const Rect& t : taken) {
+        const bool meet = a < t.b && t.a < b && c0 < t.c1 && t.c0 < c1;
+        if (!meet) continue;
+        if (a >= t.a && b <= t.b && c0 >= t.c0 && c1 <= t.c1) dup = true;
+        else partial = true;
+      }
+      if (dup) continue;
+      if (partial) return Status::invalid_argument;  // overlapping but unequal source slices
+      taken.push_back({a, b, c0, c1});
       covered += (b - a) * (c1 - c0);
       const auto [item, ioff] = item_of(ss.manifest, static_cast<std::uint32_t>(e));
       const bool src_big = !ss.manifest.items()[item].is_group;

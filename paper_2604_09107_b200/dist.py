@@ -23,7 +23,7 @@ import ctypes as C
 from typing import Optional
 
 from ._lib import lib
-from .ros import Cluster, Handle, OpResult, Status, _read_bytes, check
+from .ros import Cluster, Handle, OpResult, Status, _read_bytes, check, combine_layout_key
 
 
 def _b(s: str) -> bytes:
@@ -130,68 +130,119 @@ class DistCluster:
         return bool(d.value), Status(s.value), v.value, bool(ch.value)
 
     # ---- ops ---------------------------------------------------------------
+    # A replica may span several ranks (a TP/FSDP group: one process per
+    # GPU, each holding some of the replica's shards).  Every rank holding
+    # shards of a replica passes its handle; the parts are merged per
+    # replica (rank order) into the one registry operation the reference's
+    # server would receive from that replica's client.
     def create(self, model: str, replica: str, num_shards: int = 1, **cfg) -> Handle:
         """Local: a handle to register tensors on, before the collective open()."""
         return self.local.open(model, replica, num_shards, **cfg)
 
-    def open(self, h: Optional[Handle], endpoints: Optional[list[str]] = None,
-             datacenter: str = "dc0") -> None:
-        """Collective: every rank mirrors every opened replica's record
-        (with its slicing key, known once its tensors are registered)."""
+    @staticmethod
+    def _merge(parts):
+        """{(model, replica): [part, ...]} in rank order (None parts skipped)."""
+        out = {}
+        for p in parts:
+            if p is not None:
+                out.setdefault((p["model"], p["replica"]), []).append(p)
+        return out
+
+    def open(self, h: Optional[Handle], endpoints=None, datacenter: str = "dc0") -> None:
+        """Collective: every rank mirrors every opened replica's record (its
+        endpoints per shard and slicing key, gathered from the ranks holding
+        its shards).  endpoints: one per local shard (list) or {shard: ep}."""
         mine = None
         if h is not None:
-            eps = endpoints or [f"rank{self.rank}:{i}" for i in range(h.num_shards)]
-            for i, e in enumerate(eps):
-                h.set_endpoint(i, e)
-            key = h.layout_key
-            dman = [h.derived(s, 0) for s in range(h.num_shards)] if key else []
-            dlay = [h.derived(s, 1) for s in range(h.num_shards)] if key else []
-            mine = ("open", h.model, h.replica, h.num_shards, datacenter, eps, key, dman, dlay)
-        for rc in self.server_ops(mine):
-            assert rc in (None, 0), rc
+            loc = h.local_shards()
+            if endpoints is None:
+                eps = {s: f"rank{self.rank}:{s}" for s in loc}
+            elif isinstance(endpoints, dict):
+                eps = dict(endpoints)
+            else:
+                eps = dict(zip(loc, endpoints))
+            for sh, e in eps.items():
+                h.set_endpoint(sh, e)
+            hashes = {sh: h.shard_hash(sh) for sh in loc}
+            geo = any(x[1] for x in hashes.values())
+            derived = {sh: (h.derived(sh, 0), h.derived(sh, 1)) for sh in loc} if geo else {}
+            mine = {"model": h.model, "replica": h.replica, "n": h.num_shards, "dc": datacenter,
+                    "eps": eps, "hashes": hashes, "derived": derived}
+        for (m, r), parts in self._merge(self.gather(mine)).items():
+            n = parts[0]["n"]
+            eps, hashes, derived = {}, {}, {}
+            for p in parts:
+                eps.update(p["eps"])
+                hashes.update(p["hashes"])
+                derived.update(p["derived"])
+            if sorted(hashes) != list(range(n)):
+                raise RuntimeError(f"open {m}/{r}: shards {sorted(hashes)} registered, {n} expected")
+            key = combine_layout_key([hashes[i] for i in range(n)])
+            dman = [derived[i][0] for i in range(n)] if derived else []
+            dlay = [derived[i][1] for i in range(n)] if derived else []
+            rc = self._apply(("open", m, r, n, parts[0]["dc"], [eps[i] for i in range(n)], key,
+                              dman, dlay))
+            assert rc == 0, (m, r, rc)
 
     def publish(self, h: Optional[Handle], version: int) -> Optional[OpResult]:
         mine = None
         if h is not None:
             check(lib.rs_prepare_publish(h.h, version), "rs_prepare_publish")
-            mine = ("publish", h.model, h.replica, version,
-                    [h.manifest(s) for s in range(h.num_shards)],
-                    [h.layout(s) for s in range(h.num_shards)])
-        rcs = self.server_ops(mine)
+            mine = {"model": h.model, "replica": h.replica, "n": h.num_shards,
+                    "shards": {s: (h.manifest(s), h.layout(s)) for s in h.local_shards()}}
+        rcs = {}
+        for (m, r), parts in self._merge(self.gather(mine)).items():
+            n = parts[0]["n"]
+            sh = {}
+            for p in parts:
+                sh.update(p["shards"])
+            if sorted(sh) != list(range(n)):
+                rcs[(m, r)] = int(Status.invalid_argument)
+                continue
+            rcs[(m, r)] = self._apply(("publish", m, r, version, [sh[i][0] for i in range(n)],
+                                       [sh[i][1] for i in range(n)]))
         blobs = None
         if h is not None:
-            st = rcs[self.rank]
+            st = rcs[(h.model, h.replica)]
             lib.rs_commit_publish(h.h, version, st)
             if st == 0:
-                blobs = [h.serve_export(s) for s in range(h.num_shards)]
+                blobs = [h.serve_export(s) for s in h.local_shards()]
         self._import_all(self.gather(blobs))
         if h is None:
             return None
-        st = Status(rcs[self.rank])
+        st = Status(rcs[(h.model, h.replica)])
         return OpResult(st, version if st == Status.ok else None)
 
     def unpublish(self, h: Optional[Handle]) -> Optional[OpResult]:
-        rcs = self.server_ops(("unpublish", h.model, h.replica) if h is not None else None)
+        mine = {"model": h.model, "replica": h.replica} if h is not None else None
+        rcs = {k: self._apply(("unpublish",) + k) for k in self._merge(self.gather(mine))}
         if h is None:
             return None
         done, s, _, _ = self.result(h.model, h.replica)
-        st = Status(rcs[self.rank]) if rcs[self.rank] else s
+        rc = rcs[(h.model, h.replica)]
+        st = Status(rc) if rc else s
         return OpResult(st if done else Status.timeout)
 
     def replicate(self, h: Optional[Handle], spec: str = "latest", update: bool = False,
                   max_rounds: int = 8) -> Optional[OpResult]:
         """Collective replicate/update: plan on every rank, bind + serve,
-        exchange serve states, then every reader fills (kernels chase each
-        other's watermarks), with failure reports applied collectively."""
+        exchange serve states, then every reader shard fills (kernels chase
+        each other's watermarks), with failure reports applied collectively.
+        A replica spanning several ranks completes only when all its shards
+        verified."""
         mine = None
         if h is not None:
-            cur = h.current_version
-            mine = ("update", h.model, h.replica, spec, cur) if update else \
-                ("replicate", h.model, h.replica, spec)
-        self.server_ops(mine)
+            mine = {"model": h.model, "replica": h.replica, "update": update, "spec": spec,
+                    "cur": h.current_version}
+        for (m, r), parts in self._merge(self.gather(mine)).items():
+            p = parts[0]
+            self._apply(("update", m, r, p["spec"], p["cur"]) if p["update"] else
+                        ("replicate", m, r, p["spec"]))
         active, result, version, changed = False, None, None, False
+        loc = h.local_shards() if h is not None else []
         if h is not None:
             d, s, v, ch = self.result(h.model, h.replica)
+            cur = h.current_version
             if not d:
                 result = OpResult(Status.timeout)  # parked: no version yet
             elif s != Status.ok:
@@ -205,49 +256,56 @@ class DistCluster:
                     result = OpResult(Status(rc))
                 else:
                     active = True
-        blobs = [h.serve_export(s) for s in range(h.num_shards)] if active else None
+        blobs = [h.serve_export(s) for s in loc] if active else None
         self._import_all(self.gather(blobs))
+        # a replica whose bind failed on one rank fails on all of its ranks
+        bind = self.gather((h.model, h.replica, active, result is not None) if h is not None else None)
+        broken = {(b[0], b[1]) for b in bind if b is not None and b[3] and not b[2]}
+        if active and (h.model, h.replica) in broken:
+            lib.rs_transfer_finish(h.h, version, 0)
+            result = OpResult(Status.transfer_failed)
+            active = False
         rounds = 0
+        final = None  # this replica's outcome once decided
         while True:
             outcome = None
             if active:
                 n = h.num_shards
                 sts, rsn = (C.c_int * n)(), (C.c_int * n)()
                 lib.rs_transfer_fill(h.h, C.cast(sts, C.c_void_p), C.cast(rsn, C.c_void_p))
-                outcome = (h.model, h.replica, [int(x) for x in sts], [int(x) for x in rsn],
-                           self._source(h.model, h.replica))
-            retry = {}
+                outcome = {"model": h.model, "replica": h.replica,
+                           "failed": {i: (int(sts[i]), int(rsn[i])) for i in loc if sts[i] != 0},
+                           "src": self._source(h.model, h.replica)}
+            reps = {}
             for o in self.gather(outcome):
                 if o is None:
                     continue
-                m, r, sts, rsn, src = o
-                failed = [i for i, x in enumerate(sts) if x != 0]
-                if not failed:
-                    continue
-                good = True
-                for i in failed:
-                    good &= self._apply(("report", m, r, i, src, rsn[i])) == 0
-                retry[r] = good and rounds + 1 < max_rounds
+                st = reps.setdefault((o["model"], o["replica"]), {"failed": {}, "retry": True})
+                for i, (code, reason) in o["failed"].items():
+                    st["failed"][i] = code
+                    st["retry"] &= self._apply(("report", o["model"], o["replica"], i, o["src"],
+                                                reason)) == 0
             if active:
-                mine_failed = any(x != 0 for x in outcome[2])
-                if not mine_failed or not retry.get(h.replica, False):
-                    if mine_failed:
-                        result = OpResult(Status(next(x for x in outcome[2] if x != 0)))
-                        lib.rs_transfer_finish(h.h, version, 0)
-                    else:
-                        lib.rs_transfer_finish(h.h, version, 1)
-                        result = OpResult(Status.ok, version, changed)
+                st = reps.get((h.model, h.replica), {"failed": {}, "retry": True})
+                if not st["failed"]:
+                    final = Status.ok
+                elif not (st["retry"] and rounds + 1 < max_rounds):
+                    final = Status(next(iter(st["failed"].values())))
+                if final is not None:
+                    lib.rs_transfer_finish(h.h, version, int(final == Status.ok))
+                    result = OpResult(final, version if final == Status.ok else None, changed)
                     active = False
             if not any(self.gather(active)):
                 break
             rounds += 1
-        done = (h.model, h.replica, h.num_shards, int(result.status)) if (
-            h is not None and result is not None and version is not None) else None
+        done = None
+        if h is not None and result is not None and version is not None:
+            done = (h.model, h.replica, loc, int(result.status))
         for o in self.gather(done):
             if o is None:
                 continue
-            m, r, n, st = o
-            for i in range(n):
+            m, r, shards, st = o
+            for i in shards:
                 self._apply(("complete", m, r, i, st))
         return result
 

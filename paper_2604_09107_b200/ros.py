@@ -267,6 +267,17 @@ class Handle:
         return Status(lib.rs_register_cast(self.h, shard, _b(name), C.c_void_p(tensor.data_ptr()),
                                            nbytes, rows, w, r0, nr, c0, nc))
 
+    def local_shards(self) -> list[int]:
+        """Shards whose regions this process registered (a replica may span
+        several processes, one per GPU)."""
+        return [s for s in range(self.num_shards) if lib.rs_shard_local(self.h, s)]
+
+    def shard_hash(self, shard: int) -> tuple[int, bool, bool]:
+        """(hash, has geometry, has cast) of one shard's registrations."""
+        hv, g, c = C.c_uint64(), C.c_int(), C.c_int()
+        check(lib.rs_shard_hash(self.h, shard, C.byref(hv), C.byref(g), C.byref(c)))
+        return hv.value, bool(g.value), bool(c.value)
+
     def layout(self, shard: int = 0) -> bytes:
         return _read_bytes(lib.rs_layout, self.h, shard)
 
@@ -343,6 +354,18 @@ class Handle:
 
     def serve_export(self, shard: int = 0) -> bytes:
         return _read_bytes(lib.rs_serve_export, self.h, shard)
+
+
+def combine_layout_key(shard_hashes) -> str:
+    """Slicing key of a replica from its shards' (hash, geometry, cast), in
+    shard order (the key Handle.layout_key computes when one process holds
+    every shard)."""
+    n = len(shard_hashes)
+    hs = (C.c_uint64 * max(n, 1))(*[int(h[0]) for h in shard_hashes])
+    gs = (C.c_int * max(n, 1))(*[int(bool(h[1])) for h in shard_hashes])
+    cs = (C.c_int * max(n, 1))(*[int(bool(h[2])) for h in shard_hashes])
+    return _read_bytes(lib.rs_combine_layout_key, n, C.cast(hs, C.c_void_p), C.cast(gs, C.c_void_p),
+                       C.cast(cs, C.c_void_p)).decode()
 
 
 # ----------------------------------------------------------------------------

@@ -1,0 +1,160 @@
+"""GPU, one process per GPU (gloo for the registry, CUDA IPC for the data):
+replicas whose shards live in different processes.
+
+World 2.  A TP-2 trainer holds shard r on GPU r.  Three readers pull it:
+  * "tp2": the same slicing, shard s on GPU (s+1) % 2 -- item-for-item pulls
+    across NVLink, chunk digests equal to the trainer's;
+  * "fp8": the same slicing landed as e4m3 (config 5 in miniature);
+  * "tp1": one process holding whole tensors -- a reshard gathering from both
+    trainer shards (one local, one over NVLink).
+Bytes are checked against the numpy slices of the synthetic tensors and the
+oracle cast; the plan against the planner's rules.  Skipped below 2 GPUs."""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+from tests.conftest import ROOT
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, q):
+    import hashlib
+    import sys
+    sys.path.insert(0, ROOT)
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank),
+                      WORLD_SIZE=str(world))
+    import torch
+    import torch.distributed as dist
+
+    import oracle as O
+    from paper_2604_09107_b200 import ros
+    from paper_2604_09107_b200.dist import DistCluster
+    from paper_2604_09107_b200.ros import Status, tp_slice
+    from tests.test_cast import _tensors
+    from tests.test_reshard import numel
+    try:
+        torch.cuda.set_device(rank)
+        dev = torch.device("cuda", rank)
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        dc = DistCluster()
+        tiny = 64 << 10
+        tensors = _tensors()
+        full = {}
+        for i, (n, shape, _) in enumerate(tensors):  # every rank builds the same bytes
+            t = torch.empty(numel(shape) * 2, dtype=torch.uint8, device=dev)
+            ros.synth_bf16(t, 500 + i)
+            full[n] = t
+
+        def piece(n, geo):
+            rows, w, r0, nr, c0, nc = geo
+            return full[n].view(rows, w)[r0:r0 + nr, c0:c0 + nc].contiguous().view(-1)
+
+        t = dc.create("m", "trainer", 2, tiny_threshold=tiny)
+        keep = []
+        for n, shape, dim in tensors:
+            geo = tp_slice(shape, 2, dim, 2, rank)
+            keep.append(piece(n, geo))
+            assert t.register_slice(rank, n, keep[-1], geo) == Status.ok
+        dc.open(t, endpoints=[f"rank{rank}:cuda{rank}"])
+        s = (rank + 1) % 2  # the reader shard this GPU holds
+        r = dc.create("m", "tp2", 2, tiny_threshold=tiny)
+        f = dc.create("m", "fp8", 2, tiny_threshold=tiny)
+        rb, fb = {}, {}
+        for n, shape, dim in tensors:
+            geo = tp_slice(shape, 2, dim, 2, s)
+            rb[n] = torch.zeros(geo[3] * geo[5], dtype=torch.uint8, device=dev)
+            fb[n] = torch.zeros(geo[3] * geo[5] // 2, dtype=torch.uint8, device=dev)
+            assert r.register_slice(s, n, rb[n], geo) == Status.ok
+            assert f.register_cast(s, n, fb[n], geo[3] * geo[5], geo) == Status.ok
+        dc.open(r, endpoints=[f"rank{rank}:cuda{rank}"])
+        dc.open(f, endpoints=[f"rank{rank}:cuda{rank}"])
+        u, ub = None, {}
+        if rank == 0:
+            u = dc.create("m", "tp1", 1, tiny_threshold=tiny)
+            for n, shape, _ in tensors:
+                ub[n] = torch.zeros_like(full[n])
+                assert u.register_slice(0, n, ub[n], tp_slice(shape, 2, None, 1, 0)) == Status.ok
+        dc.open(u)
+        out = {}
+        out["publish"] = int(dc.publish(t, 1).status)
+        out["tp2"] = int(dc.replicate(r).status)
+        out["fp8"] = int(dc.replicate(f).status)
+        res_u = dc.replicate(u)
+        if rank == 0:
+            out["tp1"] = int(res_u.status)
+        torch.cuda.synchronize()
+        bad = []
+        for n, shape, dim in tensors:
+            geo = tp_slice(shape, 2, dim, 2, s)
+            want = piece(n, geo)
+            if not torch.equal(rb[n], want):
+                bad.append(("tp2", n))
+            cast = torch.empty_like(fb[n])
+            ros.bf16_to_e4m3(want, cast)
+            torch.cuda.synchronize()
+            if not torch.equal(fb[n], cast):
+                bad.append(("fp8", n))
+            if rank == 0 and not torch.equal(ub[n], full[n]):
+                bad.append(("tp1", n))
+        # the oracle's cast on the host for a few tensors
+        for n, shape, dim in tensors[-3:]:
+            geo = tp_slice(shape, 2, dim, 2, s)
+            host = piece(n, geo).cpu().numpy().view(np.uint16)
+            if not np.array_equal(fb[n].cpu().numpy(), O.bf16_to_e4m3(host)):
+                bad.append(("fp8-oracle", n))
+        out["bad"] = bad
+        dig = lambda h, sh: hashlib.sha256(h.chunk_digests(sh).tobytes()).hexdigest()
+        hs = dc.gather({"t": dig(t, rank), "r": dig(r, s), "f": dig(f, s)})
+        out["digests_equal"] = hs[rank]["r"] == hs[s]["t"] and hs[rank]["f"] == hs[s]["t"]
+        out["plan"] = sorted({(a.replica, a.src) for a in dc.assigns()})
+        q.put((rank, out))
+        dc.close()
+        dist.destroy_process_group()
+    except Exception as e:  # pragma: no cover - surfaced by the parent
+        import traceback
+        q.put((rank, {"error": repr(e) + traceback.format_exc()}))
+        raise
+
+
+def test_replicas_split_across_processes():
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs >= 2 GPUs")
+    import multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    res = {}
+    for _ in range(2):
+        r = q.get(timeout=300)
+        res[r[0]] = r[1]
+    for p in ps:
+        p.join(timeout=60)
+    for r in range(2):
+        assert "error" not in res[r], res[r].get("error")
+        o = res[r]
+        assert o["publish"] == 0 and o["tp2"] == 0 and o["fp8"] == 0, o
+        assert o["bad"] == [], o["bad"]
+        assert o["digests_equal"]
+        plan = dict(o["plan"])
+        # tp2 comes from the trainer; the later readers from any complete copy
+        # that is not terminal (the planner prefers the least recently used)
+        assert plan["tp2"] == "trainer" and plan["fp8"] in ("trainer", "tp2"), plan
+        assert plan["tp1"] in ("trainer", "tp2"), plan
+    assert res[0]["tp1"] == 0
