@@ -121,6 +121,11 @@ def workload_shapes(name: str):
         return llama3_8b_shapes()
     if name == "config1":
         return config1()
+    if name == "big16":  # diagnostic: 16 x 512 MiB (the nvlink_dir_probe span set)
+        return [(f"w{i}", (16384, 16384)) for i in range(16)]
+    if name == "qwen25_32b":
+        from tests.golden.models import qwen25_32b_shapes
+        return qwen25_32b_shapes()
     if name == "llama3_70b_tp8":
         # config 5: one TP-8 shard (rank 0) of Llama-3-70B, each tensor's
         # slice contiguous as its trainer rank holds it
@@ -413,7 +418,7 @@ def main():
     ap.add_argument("--chunk", type=int, default=4096)
     ap.add_argument("--no-verify", action="store_true")
     ap.add_argument("--fanout", default="chain", choices=["chain", "pairs", "ring"])
-    ap.add_argument("--reshard", default="none", choices=["none", "tp2"])
+    ap.add_argument("--reshard", default="none", choices=["none", "tp2", "fsdp_tp2"])
     ap.add_argument("--cast", action="store_true", help="reader lands fp8 e4m3 (config 5)")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-bytes", type=int, default=2 << 30)

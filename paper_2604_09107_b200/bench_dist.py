@@ -18,6 +18,8 @@ import time
 
 
 def run(args):
+    if getattr(args, "reshard", "none") == "fsdp_tp2":
+        return run_fsdp_tp2(args)
     if getattr(args, "fanout", "chain") == "ring":
         return run_ring(args)
     import torch
@@ -157,9 +159,8 @@ def run_ring(args):
     """Config 5 shape: a TP-N trainer group (shard i on GPU i) pulled
     shard-for-shard by a reader group placed on GPU (i+1) mod N, optionally
     landing fp8 e4m3 (--cast).  Every GPU sends its trainer shard and
-    receives its reader shard at the same time.  Shard i is published as its
-    own single-shard model m{i} (the registry plans shard i -> shard i
-    either way; one process per GPU holds one shard of each group)."""
+    receives its reader shard at the same time.  Both groups are replicas
+    split across processes (one process per GPU holds one shard of each)."""
     import hashlib
 
     import torch
@@ -184,18 +185,18 @@ def run_ring(args):
     tarena, tviews = B.alloc_replica(shapes, dev, seed_base=42 + 1000 * rank)
     rarena, rviews = B.alloc_replica(shapes, dev, elem=1 if cast else 2)
     torch.cuda.synchronize()
-    t = dc.create(f"m{rank}", "trainer", 1, chunk_bytes=args.chunk, pull_timeout_s=30.0)
-    r = dc.create(f"m{up}", "reader", 1, chunk_bytes=args.chunk, pull_timeout_s=30.0)
+    t = dc.create("m", "trainer", world, chunk_bytes=args.chunk, pull_timeout_s=30.0)
+    r = dc.create("m", "reader", world, chunk_bytes=args.chunk, pull_timeout_s=30.0)
     for (n, v), (_, w) in zip(tviews, rviews):
-        assert t.register_tensor(0, n, v) == Status.ok
+        assert t.register_tensor(rank, n, v) == Status.ok
         if cast:
-            assert r.register_cast(0, n, w, v.numel()) == Status.ok
+            assert r.register_cast(up, n, w, v.numel()) == Status.ok
         else:
-            assert r.register_tensor(0, n, w) == Status.ok
+            assert r.register_tensor(up, n, w) == Status.ok
     dc.open(t, endpoints=[f"rank{rank}:cuda{local}"])
     dc.open(r, endpoints=[f"rank{rank}:cuda{local}"])
     stream = torch.cuda.Stream(device=dev)
-    r.set_stream(0, stream)
+    r.set_stream(up, stream)
     t0 = time.perf_counter()
     assert dc.publish(t, 1).status == Status.ok
     publish_s = time.perf_counter() - t0
@@ -218,8 +219,8 @@ def run_ring(args):
     verified = True
     if not args.no_verify:
         # digest tables: the reader's (bf16 bytes it verified) == its trainer's
-        th = hashlib.sha256(t.chunk_digests(0).tobytes()).hexdigest()
-        rh = hashlib.sha256(r.chunk_digests(0).tobytes()).hexdigest()
+        th = hashlib.sha256(t.chunk_digests(rank).tobytes()).hexdigest()
+        rh = hashlib.sha256(r.chunk_digests(up).tobytes()).hexdigest()
         allh = dc.gather((th, rh))
         verified = allh[rank][1] == allh[up][0]
         # landed bytes: regenerate the upstream shard here (same seeds) and
@@ -274,6 +275,192 @@ def run_ring(args):
                          "peak_src": "nominal NVLink5 per direction", "kernel": "pull_tma_kernel",
                          "kernel_ms_avg": round(statistics.mean(step_dev_ms), 3),
                          "alg_bytes_per_launch": total},
+            "e2e": {"value": round(total_landed / wall_s / 1e9, 2), "unit": B.UNIT,
+                    "h2d_bytes_per_step": None, "d2h_bytes_per_step": None,
+                    "what": "wall clock of the collective replicate (plan+bind+IPC exchange+kernel)"},
+            "gpu_launches": args.steps * world,
+            "clocks": clocks,
+            "verified": verified,
+        }
+        print(json.dumps(line), flush=True)
+    dist.barrier(group=dc.pg)
+    dc.close()
+    dist.destroy_process_group()
+
+
+def _synth_full(shape, seed, dev):
+    import torch
+
+    from paper_2604_09107_b200 import ros
+    n = 1
+    for d in shape:
+        n *= d
+    t = torch.empty(2 * n, dtype=torch.uint8, device=dev)
+    ros.synth_bf16(t, seed)
+    return t
+
+
+def _piece(full, geo):
+    rows, w, r0, nr, c0, nc = geo
+    return full.view(rows, w)[r0:r0 + nr, c0:c0 + nc].contiguous().view(-1)
+
+
+def run_fsdp_tp2(args):
+    """Config 3: a trainer sharded FSDP-N (Shard(0): shard i = rows
+    [i*R/N, (i+1)*R/N) of every tensor, on GPU i) is pulled by N/2 rollout
+    replicas in the TP-2 layout (column-parallel q/k/v/gate/up/embed/lm_head
+    and biases, row-parallel o/down, replicated norms); replica j's shard s
+    lives on GPU 2j+s.  All replicas replicate at once: the planner has
+    replica 0 reshard from the N FSDP sources and chains the others onto the
+    same-slicing copy before them, each chasing its upstream's watermarks.
+    Both groups are replicas split across processes (one process per GPU)."""
+    import hashlib
+
+    import torch
+    import torch.distributed as dist
+
+    import bench as B
+    from paper_2604_09107_b200.dist import DistCluster
+    from paper_2604_09107_b200.ros import Status, tp_slice
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", str(rank)))
+    if world % 2:
+        raise SystemExit("--reshard fsdp_tp2 needs an even number of GPUs")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist.init_process_group("gloo")
+    dc = DistCluster()
+    shapes = B.workload_shapes(args.workload)
+    rep, s = rank // 2, rank % 2  # this GPU's rollout replica and TP shard
+    fsdp = [tp_slice(shape, 2, 0, world, rank) for _, shape in shapes]
+    tp2 = [tp_slice(shape, 2, B.tp_dim(n), 2, s) for n, shape in shapes]
+    tsizes = [g[3] * g[5] for g in fsdp]
+    rsizes = [g[3] * g[5] for g in tp2]
+
+    def arena(sizes):
+        offs, tot = [], 0
+        for n in sizes:
+            offs.append(tot)
+            tot += (n + 255) // 256 * 256
+        a = torch.zeros(tot, dtype=torch.uint8, device=dev)
+        return a, [a[o:o + n] for o, n in zip(offs, sizes)]
+
+    tarena, tviews = arena(tsizes)
+    for i, ((n, shape), g) in enumerate(zip(shapes, fsdp)):
+        full = _synth_full(shape, 42 + i, dev)
+        tviews[i].copy_(_piece(full, g))
+        del full
+    rarena, rviews = arena(rsizes)
+    torch.cuda.synchronize()
+    t = dc.create("m", "trainer", world, chunk_bytes=args.chunk, pull_timeout_s=60.0)
+    for (n, _), v, g in zip(shapes, tviews, fsdp):
+        assert t.register_slice(rank, n, v, g) == Status.ok
+    r = dc.create("m", f"tp2_{rep}", 2, chunk_bytes=args.chunk, pull_timeout_s=60.0)
+    for (n, _), v, g in zip(shapes, rviews, tp2):
+        assert r.register_slice(s, n, v, g) == Status.ok
+    dc.open(t, endpoints=[f"rank{rank}:cuda{local}"])
+    dc.open(r, endpoints=[f"rank{rank}:cuda{local}"])
+    stream = torch.cuda.Stream(device=dev)
+    r.set_stream(s, stream)
+    t0 = time.perf_counter()
+    assert dc.publish(t, 1).status == Status.ok
+    publish_s = time.perf_counter() - t0
+
+    def step():
+        dc.unpublish(r if r.is_published else None)
+        r.invalidate()
+        dist.barrier(group=dc.pg)
+        torch.cuda.synchronize()
+        w0 = time.perf_counter()
+        res = dc.replicate(r, "latest")
+        torch.cuda.synchronize()
+        wall = time.perf_counter() - w0
+        assert res.status == Status.ok, res
+        st = r.stats()
+        return wall, st.last_pull_ms, st.last_pull_bytes
+
+    for _ in range(args.warmup):
+        step()
+    verified = True
+    if not args.no_verify:
+        # the landed TP-2 slices against slices of the regenerated tensors
+        for i, ((n, shape), g) in enumerate(zip(shapes, tp2)):
+            full = _synth_full(shape, 42 + i, dev)
+            verified &= bool(torch.equal(rviews[i], _piece(full, g)))
+            del full
+        # same-slicing replicas hold identical chunk-digest tables
+        hs = dc.gather((s, hashlib.sha256(r.chunk_digests(s).tobytes()).hexdigest()))
+        for sh in (0, 1):
+            verified &= len({h for x, h in hs if x == sh}) == 1
+        verified = all(dc.gather(verified))
+    clk = B.ClockSampler(local)
+    dist.barrier(group=dc.pg)
+    torch.cuda.synchronize()
+    clk.start()
+    walls, kms, landed = [], [], 0
+    for _ in range(args.steps):
+        w, k, b = step()
+        walls.append(w)
+        kms.append(k)
+        landed += b
+    clocks = clk.stop()
+    # Roofline of this shard's fill: bytes that cross NVLink (from sources on
+    # other GPUs) vs bytes read from local HBM, all written to local HBM.
+    src = {a.replica: a.src for a in dc.assigns()}.get(f"tp2_{rep}")
+    remote = local_b = 0
+    for (n, shape), g in zip(shapes, tp2):
+        if src != "trainer":  # a same-slicing upstream replica on other GPUs
+            remote += g[3] * g[5]
+            continue
+        for i in range(world):
+            fg = tp_slice(shape, 2, 0, world, i)
+            a0, a1 = max(g[2], fg[2]), min(g[2] + g[3], fg[2] + fg[3])
+            c0, c1 = max(g[4], fg[4]), min(g[4] + g[5], fg[4] + fg[5])
+            if a0 < a1 and c0 < c1:
+                if i == rank:
+                    local_b += (a1 - a0) * (c1 - c0)
+                else:
+                    remote += (a1 - a0) * (c1 - c0)
+    hbm = B.measured_peaks()["hbm_gbs"] * 1e9
+    t_min = max(remote / 900e9, (local_b + sum(rsizes)) / hbm)
+    allv = dc.gather((kms, landed, sum(walls), clocks, sum(rsizes), rep, s, remote, local_b, t_min))
+    step_dev_ms = [max(a[0][i] for a in allv) for i in range(args.steps)]
+    total_landed = args.steps * sum(a[4] for a in allv)  # reader-layout bytes landed
+    dev_s = sum(step_dev_ms) / 1e3
+    wall_s = max(a[2] for a in allv)
+    if rank == 0:
+        per_rx = [round(a[4] / (statistics.mean(a[0]) / 1e3) / 1e9, 2) for a in allv]
+        mean_rx = statistics.mean(per_rx)
+        plan = sorted({f"{a.replica}<-{a.src}" for a in dc.assigns()})
+        line = {
+            "metric": B.METRIC, "value": round(total_landed / dev_s / 1e9, 2), "unit": B.UNIT,
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(sum(step_dev_ms) / args.steps, 3), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+            "config": {"workload": f"{args.workload}: FSDP-{world} trainer (Shard(0), GPU i) -> "
+                                   f"{world // 2} TP-2 rollout replicas (replica j on GPUs 2j, 2j+1), "
+                                   "resharded on pull",
+                       "bytes_per_receiver_shard": [a[4] for a in allv],
+                       "receivers": world, "chunk_bytes": args.chunk, "plan": plan,
+                       "l2": "inputs >> 126 MB L2; no flush"},
+            "per_receiver_gbs": per_rx,
+            "weight_update_latency_s": round(wall_s / args.steps, 5),
+            "publish_s": round(publish_s, 4),
+            "roofline": {"bound": "nvlink+hbm", "achieved": round(mean_rx, 1),
+                         "peak": round(statistics.mean(a[4] / a[9] / 1e9 for a in allv), 1),
+                         "unit": "GB/s",
+                         "frac": round(max(a[9] for a in allv) / (statistics.mean(step_dev_ms) / 1e3), 4),
+                         "traffic": None,
+                         "peak_src": "per shard: max(NVLink bytes / 900 GB/s nominal, (local-read + "
+                                     "written bytes) / measured HBM peak); frac = slowest shard's bound "
+                                     "/ step time",
+                         "nvlink_bytes_per_shard": [a[7] for a in allv],
+                         "local_read_bytes_per_shard": [a[8] for a in allv],
+                         "kernel": "pull_tma_kernel",
+                         "kernel_ms_avg": round(statistics.mean(step_dev_ms), 3),
+                         "alg_bytes_per_launch": max(a[4] for a in allv)},
             "e2e": {"value": round(total_landed / wall_s / 1e9, 2), "unit": B.UNIT,
                     "h2d_bytes_per_step": None, "d2h_bytes_per_step": None,
                     "what": "wall clock of the collective replicate (plan+bind+IPC exchange+kernel)"},

@@ -6,6 +6,7 @@
 #include <cstring>
 #include <memory>
 #include <string>
+#include <set>
 #include <vector>
 
 #include "client.hpp"
@@ -590,6 +591,23 @@ int rs_pull_spans(const uint64_t* src_ptrs, const uint64_t* dst_ptrs, const uint
   cudaGetDevice(&prev);
   cudaSetDevice(device);
   auto stream = static_cast<cudaStream_t>(cuda_stream);
+  // spans in a peer GPU's memory (a pull from it, or a push into it)
+  std::set<int> peers;
+  for (int i = 0; i < n_items; ++i)
+    for (const uint64_t* p : {src_ptrs, dst_ptrs}) {
+      if (!p || !p[i]) continue;
+      cudaPointerAttributes a{};
+      if (cudaPointerGetAttributes(&a, reinterpret_cast<void*>(p[i])) == cudaSuccess &&
+          a.type == cudaMemoryTypeDevice && a.device != device)
+        peers.insert(a.device);
+      cudaGetLastError();
+    }
+  for (int o : peers)
+    if (!rsb::ok(rsb::enable_peer(device, o))) {
+      cudaSetDevice(prev);
+      return st(rsb::Status::not_serving);
+    }
+  const bool remote = !peers.empty();
   // Item i's chunks start at a multiple of 32 (batch aligned, as in
   // ChunkMap::uniform); indices in between are holes of expect/out tables.
   std::vector<rsb::dev::ItemDesc> descs(n_items);
@@ -616,6 +634,7 @@ int rs_pull_spans(const uint64_t* src_ptrs, const uint64_t* dst_ptrs, const uint
                                  &sdesc, 1, chunk, &plan, &p) != cudaSuccess)
     rc = st(rsb::Status::transfer_failed);
   if (!rc) {
+    p.remote = remote ? 1u : 0u;
     p.dst_digests = out_digests_dev;
     p.timeout_ns = 4000000000ull;
     cudaEventCreate(&e0);

@@ -334,6 +334,15 @@ Status ServeRegistry::import_state(const std::string& blob) {
 
 // --------------------------------------------------------- address mapping
 
+int ptr_device(std::uint64_t p) {
+  cudaPointerAttributes a{};
+  if (!p || cudaPointerGetAttributes(&a, reinterpret_cast<void*>(p)) != cudaSuccess) {
+    cudaGetLastError();
+    return -1;
+  }
+  return a.type == cudaMemoryTypeDevice ? a.device : -1;
+}
+
 Status enable_peer(int reader_device, int owner_device) {
   if (reader_device == owner_device) return Status::ok;
   static std::mutex mu;
@@ -1034,6 +1043,9 @@ Status Client::launch_fill(Shard& sh, const SourceView& src, bool src_complete) 
   const dev::SrcDesc sdesc{reinterpret_cast<const std::uint64_t*>(src.digests),
                            src_complete ? nullptr : reinterpret_cast<const std::uint32_t*>(src.flags),
                            src.epoch, 0};
+  bool remote = false;
+  for (std::size_t i = 0; i < items.size() && !remote; ++i)
+    remote = ptr_device(src.item_ptrs[i]) != sh.device;
   dev::PullParams pp{};
   RS_CUDA(dev::upload_pull_plan(sh.device, sh.stream, descs.data(),
                                 static_cast<std::uint32_t>(descs.size()), &sdesc, 1,
@@ -1044,6 +1056,7 @@ Status Client::launch_fill(Shard& sh, const SourceView& src, bool src_complete) 
   pp.dst_epoch = p.epoch;
   pp.timeout_ns = static_cast<std::uint64_t>(cfg_.pull_timeout_s * 1e9);
   pp.resume = p.landed_some ? 1u : 0u;
+  pp.remote = remote ? 1u : 0u;
   RS_CUDA(cudaEventRecord(sh.ev0, sh.stream));
   RS_CUDA(dev::launch_pull(pp, dev::pull_grid(sh.device), sh.stream));
   RS_CUDA(cudaEventRecord(sh.ev1, sh.stream));
@@ -1200,6 +1213,9 @@ Status Client::launch_reshard_fill(Shard& sh, const Assignment& a, bool src_comp
              src_complete ? nullptr : reinterpret_cast<const std::uint32_t*>(views[s].flags),
              views[s].epoch, 0};
   }
+  bool remote = false;
+  for (std::uint32_t s = 0; s < nsrc; ++s)
+    if (need[s] && !views[s].item_ptrs.empty()) remote |= ptr_device(views[s].item_ptrs[0]) != sh.device;
   std::vector<dev::ItemDesc> descs = rs.plan.segs;
   for (auto& d : descs) {
     d.src = views[d.src_id].item_ptrs[d.pad] + d.src;
@@ -1233,6 +1249,7 @@ Status Client::launch_reshard_fill(Shard& sh, const Assignment& a, bool src_comp
   pp.dst_epoch = p.epoch;
   pp.timeout_ns = static_cast<std::uint64_t>(cfg_.pull_timeout_s * 1e9);
   pp.resume = p.landed_some ? 1u : 0u;
+  pp.remote = remote ? 1u : 0u;
   RS_CUDA(cudaEventRecord(sh.ev0, sh.stream));
   RS_CUDA(dev::launch_pull(pp, dev::pull_grid(sh.device), sh.stream));
   RS_CUDA(cudaEventRecord(sh.ev1, sh.stream));

@@ -331,5 +331,6 @@ dev::ItemDesc identity_segment(std::uint64_t src, std::uint64_t dst, std::uint64
 // Peer / IPC address translation for the reader's device.
 Status map_source(const std::shared_ptr<ServeState>& st, int reader_device, SourceView* out);
 Status enable_peer(int reader_device, int owner_device);
+int ptr_device(std::uint64_t p);  // device holding a (possibly IPC-mapped) address, -1: none
 
 }  // namespace rsb

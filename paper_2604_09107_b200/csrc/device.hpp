@@ -96,6 +96,8 @@ struct PullParams {
   std::uint32_t has_cast;            // some segment lands as e4m3 (kernel shape choice)
   const void* maps;                  // CUtensorMap pairs per segment (or null)
   const std::uint32_t* batch_seg;    // per batch: last segment with chunk0 <= 32*batch
+  std::uint32_t remote;              // some source is another GPU's HBM (kernel shape choice)
+  std::uint32_t pad;
 };
 
 // Uploads a pull plan (segment table + source table + TMA tensor maps +

@@ -196,7 +196,17 @@ __global__ void __launch_bounds__(64, C::kCtas) pull_tma_kernel(const PullParams
       }
       if (__any_sync(full, sd != nullptr && sd->flags != nullptr)) fence_proxy_async_global();
       const bool has_expect = sd && sd->digests;
-      const std::uint64_t expect = has_expect ? __ldcg(&sd->digests[r.src_chunk]) : 0;
+      // Expected digests: when the batch's 32 source chunks are consecutive
+      // in one source table (the common case) they arrive as ONE 256-byte
+      // bulk copy into the last stage's metadata, asynchronously like the
+      // data; otherwise each lane loads its own (that load's latency then
+      // stalls this warp once per batch -- costly when the link is loaded).
+      const std::uint32_t sc0 = __shfl_sync(full, r.src_chunk, 0);
+      const bool dig_bulk = __all_sync(full, has_expect && r.clen != 0 && src_id == sid0 &&
+                                                 r.src_chunk == sc0 + lane) &&
+                            (sc0 & 1u) == 0;
+      const std::uint64_t* dig_src = dig_bulk ? p.srcs[sid0].digests + sc0 : nullptr;
+      const std::uint64_t expect = (has_expect && !dig_bulk) ? __ldcg(&sd->digests[r.src_chunk]) : 0;
       const std::uint32_t verify_mask = __ballot_sync(full, has_expect);
       const bool is_cast = r.clen && seg < p.n_items && (items[seg].chunk_len & kCastE4M3);
       const std::uint32_t cast_mask = __ballot_sync(full, is_cast);
@@ -225,9 +235,11 @@ __global__ void __launch_bounds__(64, C::kCtas) pull_tma_kernel(const PullParams
         m.clen[lane] = r.clen;
         m.dst[lane] = r.dst ? reinterpret_cast<std::uint64_t>(r.dst + (is_cast ? g / 2 : g)) : 0;
         if (last) {
-          m.expect[lane] = expect;
+          if (!dig_bulk) m.expect[lane] = expect;
           m.seg[lane] = seg;
         }
+        const std::uint32_t dig_tx = (last && dig_bulk) ? 256u : 0u;
+        if (dig_tx && lane == 0) fence_proxy_async_smem();  // earlier generic writes of m.expect
         if (lane == 0) {
           m.cast = cast_mask;
           m.verify = verify_mask;
@@ -246,7 +258,8 @@ __global__ void __launch_bounds__(64, C::kCtas) pull_tma_kernel(const PullParams
           }
           __syncwarp();
           if (lane == 0) {
-            mbar_arrive_tx(&sm.full[stage], 32 * piece);
+            mbar_arrive_tx(&sm.full[stage], 32 * piece + dig_tx);
+            if (dig_tx) bulk_g2s(m.expect, dig_src, dig_tx, &sm.full[stage]);
             const void* map = maps + 256 * std::size_t(seg0);
             const std::uint32_t qq = q0;
             for (std::uint32_t j = 0; j < piece / kMapBoxCols; ++j) {
@@ -273,7 +286,10 @@ __global__ void __launch_bounds__(64, C::kCtas) pull_tma_kernel(const PullParams
             m.box = 0;
           }
           __syncwarp();
-          if (lane == 0) mbar_arrive_tx(&sm.full[stage], tx);
+          if (lane == 0) {
+            mbar_arrive_tx(&sm.full[stage], tx + dig_tx);
+            if (dig_tx) bulk_g2s(m.expect, dig_src, dig_tx, &sm.full[stage]);
+          }
           __syncwarp();
           if (bulk) bulk_g2s(slot, r.src + g, bulk, &sm.full[stage]);
         }
@@ -540,11 +556,14 @@ int variant() {  // -1: by workload
 }  // namespace
 
 cudaError_t launch_pull_tma(const PullParams& p, int sms, cudaStream_t s) {
-  // Measured on B200 (profiles/r1/variants.txt): plain pulls are fastest with
-  // 3 CTAs/SM and the segment table in shared memory (V0); a cast pull's
-  // consumers do ~60% more work per byte and want the 4th CTA (V4).
+  // Measured on B200: local plain pulls are fastest with 3 CTAs/SM and the
+  // segment table in shared memory (V0, profiles/r1/variants.txt); a cast
+  // pull's consumers do ~60% more work per byte and want the 4th CTA, and a
+  // pull over NVLink wants its extra in-flight stages -- with both
+  // directions of a link busy V0 drops to ~675 GB/s, V4 holds ~775
+  // (profiles/r1/nvlink_dir.json).
   int v = variant();
-  if (v < 0) v = p.has_cast ? 4 : 0;
+  if (v < 0) v = (p.has_cast || p.remote) ? 4 : 0;
   switch (v) {
     case 1: return launch_variant<V1>(p, sms, s);
     case 2: return launch_variant<V2>(p, sms, s);
