@@ -420,6 +420,8 @@ def main():
     ap.add_argument("--fanout", default="chain", choices=["chain", "pairs", "ring"])
     ap.add_argument("--reshard", default="none", choices=["none", "tp2", "fsdp_tp2"])
     ap.add_argument("--cast", action="store_true", help="reader lands fp8 e4m3 (config 5)")
+    ap.add_argument("--scenario", default="steady", choices=["steady", "elastic"],
+                    help="elastic: config 4 (join at 50%% + version bump), N >= 3")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-bytes", type=int, default=2 << 30)
     ap.add_argument("--cpu-reps", type=int, default=3)

@@ -202,6 +202,13 @@ int rs_transfer_bind(rs_handle* h, uint64_t version);
 /* One fill attempt of every shard still pending; statuses/reasons per shard
  * (reason 0 timeout/not serving, 1 checksum). */
 int rs_transfer_fill(rs_handle* h, int* statuses, int* reasons);
+/* rs_transfer_fill in two halves: launch the pending shards' pull kernels
+ * (returns at once), then wait for them.  In between, rs_transfer_progress
+ * reads a running fill's verified-batch count (32-chunk batches) -- the
+ * watermark a late joiner chases. */
+int rs_transfer_launch(rs_handle* h);
+int rs_transfer_progress(rs_handle* h, uint32_t shard, uint32_t* batches_done, uint32_t* n_batches);
+int rs_transfer_wait(rs_handle* h, int* statuses, int* reasons);
 int rs_transfer_finish(rs_handle* h, uint64_t version, int ok);
 /* Cross-process serve state (CUDA IPC handles + watermarks). */
 int rs_serve_export(rs_handle* h, uint32_t shard, void* buf, size_t cap, size_t* len);

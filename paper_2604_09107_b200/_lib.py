@@ -59,6 +59,9 @@ _SIGS = {
     "rs_register_cast": (i32, [vp, u32, cstr, vp, u64, u64, u64, u64, u64, u64, u64]),
     "rs_layout_key": (i32, [vp, vp, sz, C.POINTER(sz)]),
     "rs_shard_local": (i32, [vp, u32]),
+    "rs_transfer_launch": (i32, [vp]),
+    "rs_transfer_progress": (i32, [vp, u32, C.POINTER(u32), C.POINTER(u32)]),
+    "rs_transfer_wait": (i32, [vp, vp, vp]),
     "rs_shard_hash": (i32, [vp, u32, C.POINTER(u64), C.POINTER(i32), C.POINTER(i32)]),
     "rs_combine_layout_key": (i32, [u32, vp, vp, vp, vp, sz, C.POINTER(sz)]),
     "rs_chunk_len_for": (u32, [u64, u64, u64, u32]),

@@ -18,6 +18,8 @@ import time
 
 
 def run(args):
+    if getattr(args, "scenario", "steady") == "elastic":
+        return run_elastic(args)
     if getattr(args, "reshard", "none") == "fsdp_tp2":
         return run_fsdp_tp2(args)
     if getattr(args, "fanout", "chain") == "ring":
@@ -466,6 +468,141 @@ def run_fsdp_tp2(args):
                     "what": "wall clock of the collective replicate (plan+bind+IPC exchange+kernel)"},
             "gpu_launches": args.steps * world,
             "clocks": clocks,
+            "verified": verified,
+        }
+        print(json.dumps(line), flush=True)
+    dist.barrier(group=dc.pg)
+    dc.close()
+    dist.destroy_process_group()
+
+
+def run_elastic(args):
+    """Config 4: elastic join + version bump.  Rank 0 trains; ranks
+    1..N-2 replicate version v at once (a chain); rank N-1 joins when rank 1
+    has verified half of its batches and is planned onto a partially landed
+    copy, chasing its watermarks.  Then the trainer unpublishes v, mutates its
+    weights in place (new bytes), publishes v+1 and every reader updates to
+    "latest"; v copies are never v+1 sources.  Per step: the joiner's
+    join -> complete latency and the bump latency (trainer unpublish ->
+    every reader on v+1), max over ranks, wall clock."""
+    import hashlib
+
+    import torch
+    import torch.distributed as dist
+
+    import bench as B
+    from paper_2604_09107_b200 import ros
+    from paper_2604_09107_b200.dist import DistCluster
+    from paper_2604_09107_b200.ros import Status
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", str(rank)))
+    if world < 3:
+        raise SystemExit("--scenario elastic needs >= 3 GPUs (trainer, readers, a joiner)")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist.init_process_group("gloo")
+    dc = DistCluster()
+    shapes = B.workload_shapes(args.workload)
+    total = sum(2 * B._numel(s) for _, s in shapes)
+    is_trainer, joiner = rank == 0, world - 1
+    arena, views = B.alloc_replica(shapes, dev, seed_base=42 if is_trainer else None)
+    torch.cuda.synchronize()
+    name = "trainer" if is_trainer else (f"rollout{rank}" if rank != joiner else "joiner")
+    h = dc.create("m", name, 1, chunk_bytes=args.chunk, pull_timeout_s=60.0)
+    for n, v in views:
+        assert h.register_tensor(0, n, v) == Status.ok
+    dc.open(h, endpoints=[f"rank{rank}:cuda{local}"])
+    version = 1
+    dc.publish(h if is_trainer else None, version)
+    reader = None if is_trainer else h
+
+    def table():
+        return hashlib.sha256(h.chunk_digests(0).tobytes()).hexdigest()
+
+    joins, bumps, publishes, updates, verified = [], [], [], [], True
+    for step in range(args.warmup + args.steps):
+        # ---- phase A: readers 1..N-2 pull v; the joiner comes in at 50% ----
+        dc.unpublish(reader if (reader is not None and reader.is_published) else None)
+        if reader is not None:
+            reader.invalidate()
+        dist.barrier(group=dc.pg)
+        dc.replicate_start(reader if 0 < rank < joiner else None, "latest")
+        if rank == 1:
+            while True:
+                done, nb = dc.progress(h, 0)
+                if nb and done * 2 >= nb:
+                    break
+                time.sleep(20e-6)
+        dist.barrier(group=dc.pg)  # rank 1 is half way: the joiner arrives now
+        j0 = time.perf_counter()
+        dc.replicate_start(h if rank == joiner else None, "latest")
+        res = dc.replicate_finish(reader)
+        join_s = time.perf_counter() - j0
+        if reader is not None:
+            assert res.status == Status.ok, res
+        src_of = {a.replica: a.src for a in dc.assigns() if a.version == version}
+        jl = dc.gather(join_s if rank == joiner else None)[joiner]
+        # ---- phase B: version bump ----
+        dist.barrier(group=dc.pg)
+        b0 = time.perf_counter()
+        if is_trainer:
+            assert dc.unpublish(h).status == Status.ok
+            for i, (n, v) in enumerate(views):  # new weights, in place
+                ros.synth_bf16(v, 1000 * (version + 1) + i)
+            torch.cuda.synchronize()
+            p0 = time.perf_counter()
+            assert dc.publish(h, version + 1).status == Status.ok
+            pub_s = time.perf_counter() - p0
+        else:
+            dc.unpublish(None)
+            dc.publish(None, version + 1)
+            pub_s = 0.0
+        u0 = time.perf_counter()
+        res = dc.update(reader, "latest")
+        torch.cuda.synchronize()
+        t_end = time.perf_counter()
+        if reader is not None and not (res.status == Status.ok and res.version == version + 1):
+            raise RuntimeError(f"step {step} update on {name}: {res}\n" + dc.local.trace()[-3000:])
+        version += 1
+        lat = dc.gather((t_end - b0, t_end - u0, pub_s))
+        new_src = {a.replica: a.src for a in dc.assigns() if a.version == version}
+        # v copies never serve v+1: every v+1 source is the trainer or a v+1 copy
+        verified &= all(s == "trainer" or new_src.get(s) is not None for s in new_src.values())
+        if not args.no_verify:
+            tabs = dc.gather(table())
+            verified &= len(set(tabs)) == 1
+        if step >= args.warmup:
+            joins.append(jl)
+            bumps.append(max(x[0] for x in lat))
+            updates.append(max(x[1] for x in lat))
+            publishes.append(max(x[2] for x in lat))
+    verified = all(dc.gather(verified))
+    if rank == 0:
+        upd = statistics.mean(updates)
+        line = {
+            "metric": B.METRIC, "value": round((world - 1) * total / upd / 1e9, 2), "unit": B.UNIT,
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(1e3 * statistics.mean(bumps), 3), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+            "config": {"workload": f"{args.workload}: elastic join + version bump (config 4): "
+                                   f"trainer GPU0, readers GPU1..{world - 2} chained, joiner "
+                                   f"GPU{world - 1} arrives at 50% of rollout1's batches",
+                       "bytes_per_receiver": total, "receivers": world - 1, "chunk_bytes": args.chunk,
+                       "join_plan": src_of, "bump_plan": new_src,
+                       "l2": "inputs >> 126 MB L2; no flush"},
+            "per_receiver_gbs": [round(total / upd / 1e9, 2)],
+            "join_latency_s": round(statistics.mean(joins), 5),
+            "bump_latency_s": round(statistics.mean(bumps), 5),
+            "bump_publish_s": round(statistics.mean(publishes), 5),
+            "bump_update_s": round(upd, 5),
+            "weight_update_latency_s": round(upd, 5),
+            "roofline": None,
+            "e2e": {"value": round((world - 1) * total / statistics.mean(bumps) / 1e9, 2),
+                    "unit": B.UNIT, "h2d_bytes_per_step": None, "d2h_bytes_per_step": None,
+                    "what": "unpublish + re-publish (K6 digests) + every reader on v+1, wall clock"},
+            "gpu_launches": None,
             "verified": verified,
         }
         print(json.dumps(line), flush=True)

@@ -494,7 +494,7 @@ int rs_transfer_bind(rs_handle* h, uint64_t version) {
   return st(s);
 }
 
-int rs_transfer_fill(rs_handle* h, int* statuses, int* reasons) {
+int rs_transfer_launch(rs_handle* h) {
   if (!h) return st(rsb::Status::invalid_argument);
   auto& cl = *h->client;
   std::vector<rsb::Assignment> as(cl.num_shards());
@@ -503,7 +503,19 @@ int rs_transfer_fill(rs_handle* h, int* statuses, int* reasons) {
     if (!a) return st(a.status());
     as[i] = std::move(*a);
   }
-  auto res = cl.fill_shards(as, h->pending);
+  cl.launch_shards(as, h->pending);
+  return 0;
+}
+
+int rs_transfer_progress(rs_handle* h, uint32_t shard, uint32_t* batches_done, uint32_t* n_batches) {
+  if (!h || !batches_done || !n_batches) return st(rsb::Status::invalid_argument);
+  return st(h->client->progress(shard, batches_done, n_batches));
+}
+
+int rs_transfer_wait(rs_handle* h, int* statuses, int* reasons) {
+  if (!h) return st(rsb::Status::invalid_argument);
+  auto& cl = *h->client;
+  auto res = cl.wait_shards(h->pending);
   std::vector<std::uint32_t> still;
   int worst = 0;
   for (std::uint32_t i = 0; i < cl.num_shards(); ++i) {
@@ -519,6 +531,11 @@ int rs_transfer_fill(rs_handle* h, int* statuses, int* reasons) {
   }
   h->pending = std::move(still);
   return worst;
+}
+
+int rs_transfer_fill(rs_handle* h, int* statuses, int* reasons) {
+  if (int rc = rs_transfer_launch(h); rc != 0) return rc;
+  return rs_transfer_wait(h, statuses, reasons);
 }
 
 int rs_transfer_finish(rs_handle* h, uint64_t version, int good) {

@@ -113,21 +113,58 @@ struct R {
 
 constexpr std::uint32_t kBlobMagic = 0x31425352;  // "RSB1"
 
-// IPC mappings opened in this process, keyed by (handle bytes, device).
+// IPC mappings opened in this process.  An exported allocation is mapped
+// once per reader device and kept while some imported serve state refers to
+// it; when the last such state moves to other allocations (its owner re-bound
+// or re-published and freed the old tables) the mappings are closed -- the
+// owner's allocator may hand the same addresses out again, and a stale
+// mapping of them would make the new handle unmappable.
+struct IpcEntry {
+  int refs = 0;                 // imported serve states referring to the allocation
+  std::map<int, void*> mapped;  // reader device -> mapped base
+};
 std::mutex g_ipc_mu;
-std::map<std::pair<std::string, int>, void*> g_ipc_open;
+std::map<std::string, IpcEntry> g_ipc;
+
+std::string ipc_key(const cudaIpcMemHandle_t& h) {
+  return std::string(reinterpret_cast<const char*>(&h), sizeof(h));
+}
 
 Result<std::uint64_t> open_ipc(const cudaIpcMemHandle_t& h, int device) {
-  std::string key(reinterpret_cast<const char*>(&h), sizeof(h));
   std::lock_guard lk(g_ipc_mu);
-  auto it = g_ipc_open.find({key, device});
-  if (it != g_ipc_open.end()) return reinterpret_cast<std::uint64_t>(it->second);
+  IpcEntry& e = g_ipc[ipc_key(h)];
+  auto it = e.mapped.find(device);
+  if (it != e.mapped.end()) return reinterpret_cast<std::uint64_t>(it->second);
   DeviceGuard g(device);
   void* p = nullptr;
-  if (cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess)
+  if (cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+    cudaGetLastError();
     return Status::not_serving;
-  g_ipc_open[{key, device}] = p;
+  }
+  e.mapped[device] = p;
   return reinterpret_cast<std::uint64_t>(p);
+}
+
+// An imported state now refers to `now` instead of `before`.
+void retarget_ipc(const std::vector<ServeState::Alloc>& before,
+                  const std::vector<ServeState::Alloc>& now) {
+  std::set<std::string> b, n;
+  for (const auto& a : before) b.insert(ipc_key(a.handle));
+  for (const auto& a : now) n.insert(ipc_key(a.handle));
+  std::lock_guard lk(g_ipc_mu);
+  for (const auto& k : n)
+    if (!b.count(k)) ++g_ipc[k].refs;
+  for (const auto& k : b) {
+    if (n.count(k)) continue;
+    auto it = g_ipc.find(k);
+    if (it == g_ipc.end() || --it->second.refs > 0) continue;
+    for (auto& [dev, p] : it->second.mapped) {
+      DeviceGuard g(dev);
+      cudaIpcCloseMemHandle(p);
+      cudaGetLastError();
+    }
+    g_ipc.erase(it);
+  }
 }
 
 }  // namespace
@@ -218,8 +255,17 @@ std::shared_ptr<ServeState> ServeRegistry::find(const std::string& k) const {
 }
 
 void ServeRegistry::erase(const std::string& k) {
-  std::lock_guard lk(m_);
-  map_.erase(k);
+  std::shared_ptr<ServeState> st;
+  {
+    std::lock_guard lk(m_);
+    auto it = map_.find(k);
+    if (it == map_.end()) return;
+    st = it->second;
+    map_.erase(it);
+  }
+  std::lock_guard lk(st->m);
+  if (st->imported) retarget_ipc(st->allocs, {});
+  st->allocs.clear();
 }
 
 void ServeRegistry::set_silent(const std::string& model, const std::string& replica, bool on) {
@@ -325,6 +371,7 @@ Status ServeRegistry::import_state(const std::string& blob) {
   st->cmap.chunk0 = std::move(c0);
   st->cmap.chunk_len = std::move(cl);
   st->cmap.count = std::move(cc);
+  retarget_ipc(st->imported ? st->allocs : std::vector<ServeState::Alloc>{}, allocs);
   st->allocs = std::move(allocs);
   st->item_loc = std::move(item_loc);
   st->digests_loc = dl;
@@ -411,6 +458,7 @@ Client::~Client() {
     if (sh.ev0) cudaEventDestroy(sh.ev0);
     if (sh.ev1) cudaEventDestroy(sh.ev1);
     if (sh.own_stream && sh.stream) cudaStreamDestroy(sh.stream);
+    if (sh.poll) cudaStreamDestroy(sh.poll);
     dev::free_pull_plan(sh.device, &sh.plan);
   }
 }
@@ -1066,9 +1114,16 @@ Status Client::launch_fill(Shard& sh, const SourceView& src, bool src_complete) 
 
 std::vector<Client::FillOutcome> Client::fill_shards(const std::vector<Assignment>& as,
                                                      const std::vector<std::uint32_t>& which) {
-  std::vector<FillOutcome> out(num_shards_);
-  std::vector<dev::PullStatus> st(num_shards_);
-  std::vector<bool> launched(num_shards_, false);
+  launch_shards(as, which);
+  return wait_shards(which);
+}
+
+void Client::launch_shards(const std::vector<Assignment>& as,
+                           const std::vector<std::uint32_t>& which) {
+  launch_out_.assign(num_shards_, FillOutcome{});
+  launched_.assign(num_shards_, false);
+  auto& out = launch_out_;
+  auto& launched = launched_;
   for (std::uint32_t i : which) {
     Shard& sh = shards_[i];
     const Assignment& a = as[i];
@@ -1098,6 +1153,31 @@ std::vector<Client::FillOutcome> Client::fill_shards(const std::vector<Assignmen
     }
     launched[i] = true;
   }
+}
+
+Status Client::progress(std::uint32_t shard, std::uint32_t* batches_done, std::uint32_t* n_batches) {
+  if (shard >= num_shards_ || !is_local(shard)) return Status::invalid_argument;
+  Shard& sh = shards_[shard];
+  *batches_done = 0;
+  *n_batches = sh.holding ? sh.holding->cmap.n_batches() : 0;
+  if (!sh.plan.scratch || shard >= launched_.size() || !launched_[shard]) return Status::ok;
+  DeviceGuard g(sh.device);
+  if (!sh.poll) RS_CUDA(cudaStreamCreateWithFlags(&sh.poll, cudaStreamNonBlocking));
+  // the running kernel's status word, read on a side stream (copy engine)
+  auto* status = reinterpret_cast<dev::PullStatus*>(static_cast<std::uint8_t*>(sh.plan.scratch) + 64);
+  std::uint32_t v = 0;
+  RS_CUDA(cudaMemcpyAsync(&v, &status->batches_done, 4, cudaMemcpyDeviceToHost, sh.poll));
+  RS_CUDA(cudaStreamSynchronize(sh.poll));
+  *batches_done = v;
+  return Status::ok;
+}
+
+std::vector<Client::FillOutcome> Client::wait_shards(const std::vector<std::uint32_t>& which) {
+  std::vector<FillOutcome> out = launch_out_;
+  if (out.size() != num_shards_) out.assign(num_shards_, FillOutcome{});
+  std::vector<bool> launched = launched_;
+  if (launched.size() != num_shards_) launched.assign(num_shards_, false);
+  std::vector<dev::PullStatus> st(num_shards_);
   for (std::uint32_t i : which) {
     if (!launched[i]) continue;
     Shard& sh = shards_[i];

@@ -228,6 +228,12 @@ class Client {
   };
   std::vector<FillOutcome> fill_shards(const std::vector<Assignment>& a,
                                        const std::vector<std::uint32_t>& which);
+  // fill_shards in two halves: launch the shards' pull kernels (returns at
+  // once), then wait for them and unpack.  Between the two, progress() reads
+  // a running fill's verified-batch count (elastic joins key off it).
+  void launch_shards(const std::vector<Assignment>& a, const std::vector<std::uint32_t>& which);
+  std::vector<FillOutcome> wait_shards(const std::vector<std::uint32_t>& which);
+  Status progress(std::uint32_t shard, std::uint32_t* batches_done, std::uint32_t* n_batches);
   void finish_transfers(VersionId v, bool ok);
   void stop_serving();
   // Forget held bytes: the next fill of any version re-pulls everything
@@ -288,6 +294,7 @@ class Client {
     bool own_stream = false;
     dev::PlanUpload plan;  // item table + tensor maps + work/status words
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    cudaStream_t poll = nullptr;  // progress reads while a fill runs
     std::uint32_t epoch_ctr = 0;
   };
 
@@ -318,6 +325,8 @@ class Client {
   ClientConfig cfg_;
   std::vector<Shard> shards_;
   std::optional<VersionId> current_;
+  std::vector<FillOutcome> launch_out_;  // launch_shards -> wait_shards
+  std::vector<bool> launched_;
   bool published_ = false;
   bool opened_ = false;
   ClientStats stats_;

@@ -313,7 +313,6 @@ __global__ void __launch_bounds__(64, C::kCtas) pull_tma_kernel(const PullParams
     std::uint32_t pend[kRelease];
     int npend = 0;
     std::uint64_t pend_bytes = 0, done_bytes = 0;
-    std::uint32_t done_batches = 0;
     bool failed = false;
     const std::uint32_t swz = (static_cast<std::uint32_t>(lane) & 7u) << 4;
     auto release_pending = [&](bool newer_group, bool force) {
@@ -328,7 +327,7 @@ __global__ void __launch_bounds__(64, C::kCtas) pull_tma_kernel(const PullParams
         for (int i = 0; i < kRelease; ++i)
           if (i < npend) st_relaxed_sys(&p.dst_flags[pend[i]], p.dst_epoch);
       }
-      done_batches += npend;
+      if (lane == 0) atomicAdd(&p.status->batches_done, static_cast<std::uint32_t>(npend));
       done_bytes += pend_bytes;
       npend = 0;
       pend_bytes = 0;
@@ -511,11 +510,9 @@ __global__ void __launch_bounds__(64, C::kCtas) pull_tma_kernel(const PullParams
     }
     release_pending(false, true);
     bulk_wait<0>();
-    if (lane == 0 && done_batches) {
-      atomicAdd(&p.status->batches_done, done_batches);
+    if (lane == 0 && done_bytes)
       atomicAdd(reinterpret_cast<unsigned long long*>(&p.status->bytes),
                 static_cast<unsigned long long>(done_bytes));
-    }
   }
 }
 

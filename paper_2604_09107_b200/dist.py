@@ -44,6 +44,7 @@ class DistCluster:
         self.world = dist.get_world_size()
         self.pg = group if group is not None else dist.new_group(backend="gloo")
         self.local = Cluster(pipeline=pipeline, smart_skipping=smart_skipping)
+        self._txn = {}  # id(handle) -> replicate_start state awaiting replicate_finish
 
     # ---- plumbing ----------------------------------------------------------
     def gather(self, obj):
@@ -229,7 +230,15 @@ class DistCluster:
         exchange serve states, then every reader shard fills (kernels chase
         each other's watermarks), with failure reports applied collectively.
         A replica spanning several ranks completes only when all its shards
-        verified."""
+        verified.  = replicate_start + replicate_finish."""
+        self.replicate_start(h, spec, update)
+        return self.replicate_finish(h, max_rounds)
+
+    def replicate_start(self, h: Optional[Handle], spec: str = "latest",
+                        update: bool = False) -> None:
+        """Collective first half: plan, bind, exchange serve states and LAUNCH
+        the local shards' pull kernels; returns while they run.  Another
+        replicate_start (a late joiner) may follow before replicate_finish."""
         mine = None
         if h is not None:
             mine = {"model": h.model, "replica": h.replica, "update": update, "spec": spec,
@@ -238,33 +247,55 @@ class DistCluster:
             p = parts[0]
             self._apply(("update", m, r, p["spec"], p["cur"]) if p["update"] else
                         ("replicate", m, r, p["spec"]))
-        active, result, version, changed = False, None, None, False
-        loc = h.local_shards() if h is not None else []
+        txn = {"active": False, "result": None, "version": None, "changed": False,
+               "loc": h.local_shards() if h is not None else [], "launched": False}
         if h is not None:
             d, s, v, ch = self.result(h.model, h.replica)
             cur = h.current_version
             if not d:
-                result = OpResult(Status.timeout)  # parked: no version yet
+                txn["result"] = OpResult(Status.timeout)  # parked: no version yet
             elif s != Status.ok:
-                result = OpResult(s)
+                txn["result"] = OpResult(s)
             elif update and not ch:
-                result = OpResult(Status.ok, v or cur, False)
+                txn["result"] = OpResult(Status.ok, v or cur, False)
             else:
-                version, changed = v, ch or not update
-                rc = lib.rs_transfer_bind(h.h, version)
+                txn["version"], txn["changed"] = v, ch or not update
+                rc = lib.rs_transfer_bind(h.h, v)
                 if rc != 0:
-                    result = OpResult(Status(rc))
+                    txn["result"] = OpResult(Status(rc))
                 else:
-                    active = True
-        blobs = [h.serve_export(s) for s in loc] if active else None
+                    txn["active"] = True
+        blobs = [h.serve_export(s) for s in txn["loc"]] if txn["active"] else None
         self._import_all(self.gather(blobs))
         # a replica whose bind failed on one rank fails on all of its ranks
-        bind = self.gather((h.model, h.replica, active, result is not None) if h is not None else None)
+        bind = self.gather((h.model, h.replica, txn["active"], txn["result"] is not None)
+                           if h is not None else None)
         broken = {(b[0], b[1]) for b in bind if b is not None and b[3] and not b[2]}
-        if active and (h.model, h.replica) in broken:
-            lib.rs_transfer_finish(h.h, version, 0)
-            result = OpResult(Status.transfer_failed)
-            active = False
+        if txn["active"] and (h.model, h.replica) in broken:
+            lib.rs_transfer_finish(h.h, txn["version"], 0)
+            txn["result"] = OpResult(Status.transfer_failed)
+            txn["active"] = False
+        if txn["active"]:
+            check(lib.rs_transfer_launch(h.h), "rs_transfer_launch")
+            txn["launched"] = True
+        if h is not None:
+            self._txn[id(h)] = txn
+
+    def progress(self, h: Handle, shard: int) -> tuple[int, int]:
+        """Local: (verified batches, batches) of a running fill of one shard."""
+        done, n = C.c_uint32(), C.c_uint32()
+        check(lib.rs_transfer_progress(h.h, shard, C.byref(done), C.byref(n)))
+        return done.value, n.value
+
+    def replicate_finish(self, h: Optional[Handle], max_rounds: int = 8) -> Optional[OpResult]:
+        """Collective second half: wait for the launched fills, report
+        failures (re-filling from the re-picked source while allowed) and
+        complete every shard."""
+        txn = self._txn.pop(id(h), None) if h is not None else None
+        active = bool(txn and txn["active"])
+        result = txn["result"] if txn else None
+        version = txn["version"] if txn else None
+        loc = txn["loc"] if txn else []
         rounds = 0
         final = None  # this replica's outcome once decided
         while True:
@@ -272,7 +303,9 @@ class DistCluster:
             if active:
                 n = h.num_shards
                 sts, rsn = (C.c_int * n)(), (C.c_int * n)()
-                lib.rs_transfer_fill(h.h, C.cast(sts, C.c_void_p), C.cast(rsn, C.c_void_p))
+                step = lib.rs_transfer_wait if txn["launched"] else lib.rs_transfer_fill
+                txn["launched"] = False
+                step(h.h, C.cast(sts, C.c_void_p), C.cast(rsn, C.c_void_p))
                 outcome = {"model": h.model, "replica": h.replica,
                            "failed": {i: (int(sts[i]), int(rsn[i])) for i in loc if sts[i] != 0},
                            "src": self._source(h.model, h.replica)}
@@ -293,7 +326,8 @@ class DistCluster:
                     final = Status(next(iter(st["failed"].values())))
                 if final is not None:
                     lib.rs_transfer_finish(h.h, version, int(final == Status.ok))
-                    result = OpResult(final, version if final == Status.ok else None, changed)
+                    result = OpResult(final, version if final == Status.ok else None,
+                                      txn["changed"])
                     active = False
             if not any(self.gather(active)):
                 break
