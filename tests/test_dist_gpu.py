@@ -158,3 +158,86 @@ def test_replicas_split_across_processes():
         assert plan["tp2"] == "trainer" and plan["fp8"] in ("trainer", "tp2"), plan
         assert plan["tp1"] in ("trainer", "tp2"), plan
     assert res[0]["tp1"] == 0
+
+
+def _bump_worker(rank, world, port, q):
+    """Trainer (rank 0) re-publishes new bytes 4 times; the reader (rank 1)
+    updates each time through the split-phase calls (launch, poll, wait)."""
+    import sys
+    sys.path.insert(0, ROOT)
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank),
+                      WORLD_SIZE=str(world))
+    import torch
+    import torch.distributed as dist
+
+    from paper_2604_09107_b200 import ros
+    from paper_2604_09107_b200.dist import DistCluster
+    from paper_2604_09107_b200.ros import Status
+    try:
+        torch.cuda.set_device(rank)
+        dev = torch.device("cuda", rank)
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        dc = DistCluster()
+        sizes = [(64 << 20) + 4096 * 7, 3000, 5 << 20]
+        bufs = [torch.zeros(n, dtype=torch.uint8, device=dev) for n in sizes]
+        name = "trainer" if rank == 0 else "reader"
+        h = dc.create("m", name, 1, tiny_threshold=1 << 20)
+        for i, b in enumerate(bufs):
+            assert h.register_tensor(0, f"w{i}", b) == Status.ok
+        dc.open(h)
+        out, seen = [], []
+        for v in range(1, 5):
+            r = dc.unpublish(h if (rank == 0 and v > 1) else None)
+            if r is not None:
+                assert r.status == Status.ok
+            if rank == 0:
+                for i, b in enumerate(bufs):
+                    ros.synth_bf16(b, 100 * v + i)
+                torch.cuda.synchronize()
+                assert dc.publish(h, v).status == Status.ok
+                dc.replicate_start(None)
+                res = dc.replicate_finish(None)
+            else:
+                dc.publish(None, v)
+                dc.replicate_start(h, "latest", update=v > 1)
+                done, nb = dc.progress(h, 0)
+                seen.append((done, nb))
+                res = dc.replicate_finish(h)
+                out.append((int(res.status), res.version))
+            digest = ros.digest_spans([b.data_ptr() for b in bufs], sizes, rank)
+            got = dc.gather(digest)
+            out.append(got[0] == got[1])
+        q.put((rank, {"out": out, "seen": seen}))
+        dc.close()
+        dist.destroy_process_group()
+    except Exception as e:  # pragma: no cover - surfaced by the parent
+        import traceback
+        q.put((rank, {"error": repr(e) + traceback.format_exc()}))
+        raise
+
+
+def test_version_bumps_across_processes():
+    """Regression: a re-published owner frees and re-allocates its tables; the
+    reader's process must drop its stale IPC mappings (failed on the third
+    version before).  Bytes equal after every bump."""
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs >= 2 GPUs")
+    import multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_bump_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    res = {}
+    for _ in range(2):
+        r = q.get(timeout=300)
+        res[r[0]] = r[1]
+    for p in ps:
+        p.join(timeout=60)
+    for r in range(2):
+        assert "error" not in res[r], res[r].get("error")
+    assert res[0]["out"] == [True] * 4
+    reader = res[1]["out"]
+    assert reader == [(0, 1), True, (0, 2), True, (0, 3), True, (0, 4), True], reader
+    assert all(nb > 0 for _, nb in res[1]["seen"])
