@@ -247,8 +247,9 @@ def run_single(args):
     torch.cuda.synchronize()
     stream = torch.cuda.Stream(device=dev)
     cl = Cluster()
-    t = cl.open("m", "trainer", 1, chunk_bytes=args.chunk)
-    reshard = args.reshard == "tp2"
+    t = cl.open("m", "trainer", 8 if args.reshard == "fsdp_tp2" else 1, chunk_bytes=args.chunk)
+    reshard = args.reshard in ("tp2", "fsdp_tp2")
+    fsdp = t.num_shards  # trainer shards (FSDP-8: Shard(0) row blocks)
     r = cl.open("m", "rollout1", 2 if reshard else 1, chunk_bytes=args.chunk)
     rslices = {}
     for (n, v), (_, w), (_, shape) in zip(tviews, rviews, shapes):
@@ -260,9 +261,14 @@ def run_single(args):
             assert t.register_tensor(0, n, v) == Status.ok
             assert r.register_tensor(0, n, w) == Status.ok
             continue
-        # TP=1 trainer -> TP=2 reader: both shards on this GPU, landing
+        # TP=1 (or FSDP-8: Shard(0) row blocks, contiguous views of the
+        # trainer's tensors) -> TP=2 reader: every shard on this GPU, landing
         # straight into the reader arena (shard 0 then shard 1 per tensor)
-        assert t.register_slice(0, n, v, tp_slice(shape, 2, None, 1, 0)) == Status.ok
+        for i in range(fsdp):
+            g = tp_slice(shape, 2, 0 if fsdp > 1 else None, fsdp, i)
+            rows, wb, r0, nr, c0, nc = g
+            off = r0 * wb + c0
+            assert t.register_slice(i, n, v[off:off + nr * nc], g) == Status.ok
         dim = tp_dim(n)
         for s in range(2):
             geo = tp_slice(shape, 2, dim, 2, s)
@@ -357,7 +363,8 @@ def run_single(args):
         "warmup": args.warmup, "ms_per_step": round(dev_ms / args.steps, 3), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
         "config": {"workload": f"{args.workload}: trainer -> 1 reader on one GPU (local HBM pull)"
-                               + (", resharded TP=1 -> TP=2 (2 reader shards)" if reshard else "")
+                               + (f", resharded {'FSDP-8' if fsdp > 1 else 'TP=1'} -> TP=2 "
+                                  "(all shards on this GPU)" if reshard else "")
                                + (", landed as fp8 e4m3 (fused cast; bytes = bf16 ingress)" if cast else ""),
                    "bytes_per_receiver": total, "tensors": len(shapes), "chunk_bytes": args.chunk,
                    "receivers": 1, "l2": "inputs (16 GB/replica) >> 126 MB L2; no flush"},

@@ -460,6 +460,7 @@ Client::~Client() {
     if (sh.own_stream && sh.stream) cudaStreamDestroy(sh.stream);
     if (sh.poll) cudaStreamDestroy(sh.poll);
     dev::free_pull_plan(sh.device, &sh.plan);
+    dev::free_pull_plan(sh.device, &sh.hash_plan);
   }
 }
 
@@ -634,21 +635,16 @@ Status Client::build_payload(Shard& sh, VersionId v, std::shared_ptr<Payload>* o
       gl[gi] = grp.packed_length;
       p->group_bufs.push_back(std::move(buf));
     }
-    const std::size_t nm = srcs.size();
+    if (Status s = copy_spans(sh, srcs, dsts, ls); !ok(s)) return s;
     DevBuf gt;
-    if (Status s = gt.alloc(sh.device, (3 * nm + 3 * ng) * 8); !ok(s)) return s;
-    auto* t = static_cast<std::uint64_t*>(gt.p);
-    RS_CUDA(cudaMemcpyAsync(t, srcs.data(), nm * 8, cudaMemcpyHostToDevice, sh.stream));
-    RS_CUDA(cudaMemcpyAsync(t + nm, dsts.data(), nm * 8, cudaMemcpyHostToDevice, sh.stream));
-    RS_CUDA(cudaMemcpyAsync(t + 2 * nm, ls.data(), nm * 8, cudaMemcpyHostToDevice, sh.stream));
-    RS_CUDA(dev::launch_copy_spans(t, t + nm, t + 2 * nm, static_cast<int>(nm), sh.stream));
-    auto* g2 = t + 3 * nm;
+    if (Status s = gt.alloc(sh.device, 3 * ng * 8); !ok(s)) return s;
+    auto* g2 = static_cast<std::uint64_t*>(gt.p);
     RS_CUDA(cudaMemcpyAsync(g2, gp.data(), ng * 8, cudaMemcpyHostToDevice, sh.stream));
     RS_CUDA(cudaMemcpyAsync(g2 + ng, gl.data(), ng * 8, cudaMemcpyHostToDevice, sh.stream));
     RS_CUDA(dev::launch_span_digests(g2, g2 + ng, g2 + 2 * ng, static_cast<int>(ng), sh.stream));
     RS_CUDA(cudaMemcpyAsync(gd.data(), g2 + 2 * ng, ng * 8, cudaMemcpyDeviceToHost, sh.stream));
     RS_CUDA(cudaStreamSynchronize(sh.stream));
-    stats_.h2d_bytes += 24 * nm + 16 * ng;
+    stats_.h2d_bytes += 16 * ng;
     stats_.d2h_bytes += 8 * ng;
     for (std::size_t gi = 0; gi < ng; ++gi)
       p->manifest.set_group_digest(static_cast<std::uint32_t>(gi), gd[gi]);
@@ -708,14 +704,14 @@ Status Client::hash_items(Shard& sh, Payload& p, const std::vector<std::uint32_t
   dev::PullParams pp{};
   RS_CUDA(dev::upload_pull_plan(sh.device, sh.stream, descs.data(),
                                 static_cast<std::uint32_t>(descs.size()), &self, 1,
-                                p.cmap.n_chunks(), &sh.plan, &pp));
+                                p.cmap.n_chunks(), &sh.hash_plan, &pp));
   pp.first_batch = descs.front().chunk0 / dev::kBatchChunks;
   pp.dst_digests = static_cast<std::uint64_t*>(p.digests.p);
   pp.dst_flags = static_cast<std::uint32_t*>(p.flags.p);
   pp.dst_epoch = p.epoch;
   pp.timeout_ns = static_cast<std::uint64_t>(cfg_.pull_timeout_s * 1e9);
   RS_CUDA(dev::launch_pull(pp, dev::pull_grid(sh.device), sh.stream));
-  stats_.h2d_bytes += sh.plan.h2d_bytes;
+  stats_.h2d_bytes += sh.hash_plan.h2d_bytes;
   return Status::ok;
 }
 
@@ -1243,14 +1239,22 @@ Status Client::copy_spans(Shard& sh, const std::vector<std::uint64_t>& srcs,
   DeviceGuard g(sh.device);
   DevBuf t;
   const std::size_t n = srcs.size();
-  if (Status s = t.alloc(sh.device, 3 * n * 8); !ok(s)) return s;
+  std::vector<std::uint64_t> host(4 * n);
+  std::uint64_t tiles = 0;
+  for (std::size_t i = 0; i < n; ++i) {
+    host[i] = srcs[i];
+    host[n + i] = dsts[i];
+    host[2 * n + i] = lens[i];
+    host[3 * n + i] = tiles;
+    tiles += dev::copy_span_tiles(lens[i]);
+  }
+  if (Status s = t.alloc(sh.device, 4 * n * 8); !ok(s)) return s;
   auto* d = static_cast<std::uint64_t*>(t.p);
-  RS_CUDA(cudaMemcpyAsync(d, srcs.data(), n * 8, cudaMemcpyHostToDevice, sh.stream));
-  RS_CUDA(cudaMemcpyAsync(d + n, dsts.data(), n * 8, cudaMemcpyHostToDevice, sh.stream));
-  RS_CUDA(cudaMemcpyAsync(d + 2 * n, lens.data(), n * 8, cudaMemcpyHostToDevice, sh.stream));
-  RS_CUDA(dev::launch_copy_spans(d, d + n, d + 2 * n, static_cast<int>(n), sh.stream));
+  RS_CUDA(cudaMemcpyAsync(d, host.data(), 4 * n * 8, cudaMemcpyHostToDevice, sh.stream));
+  RS_CUDA(dev::launch_copy_spans(d, d + n, d + 2 * n, d + 3 * n, static_cast<int>(n), tiles,
+                                 sh.stream));
   RS_CUDA(cudaStreamSynchronize(sh.stream));
-  stats_.h2d_bytes += 24 * n;
+  stats_.h2d_bytes += 32 * n;
   return Status::ok;
 }
 
@@ -1347,10 +1351,18 @@ Status Client::finish_reshard(Shard& sh) {
   std::vector<std::uint64_t> srcs, dsts, lens;
   for (const auto& c : rs.plan.copies) {
     const auto base = reinterpret_cast<std::uint64_t>(rs.gather_bufs[gidx.at({c.src_shard, c.src_item})]->p);
+    const std::uint64_t flag = c.cast ? dev::kSpanCastE4M3 : 0;
+    if (c.src_stride == c.nc && c.dst_stride * (c.cast ? 2 : 1) == c.nc) {
+      // whole rows on both sides: one contiguous span
+      srcs.push_back(base + c.src_off);
+      dsts.push_back(c.dst);
+      lens.push_back((c.rows * c.nc) | flag);
+      continue;
+    }
     for (std::uint64_t r = 0; r < c.rows; ++r) {
       srcs.push_back(base + c.src_off + r * c.src_stride);
       dsts.push_back(c.dst + r * c.dst_stride);
-      lens.push_back(c.nc | (c.cast ? dev::kSpanCastE4M3 : 0));
+      lens.push_back(c.nc | flag);
     }
   }
   if (Status s = copy_spans(sh, srcs, dsts, lens); !ok(s)) return s;

@@ -292,7 +292,9 @@ class Client {
     std::shared_ptr<ServeState> serve;
     cudaStream_t stream = nullptr;
     bool own_stream = false;
-    dev::PlanUpload plan;  // item table + tensor maps + work/status words
+    dev::PlanUpload plan;       // fill: item table + tensor maps + work/status words
+    dev::PlanUpload hash_plan;  // hash-only passes (publish, reshard groups): kept apart so
+                                // the fill plan stays resident between fills
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     cudaStream_t poll = nullptr;  // progress reads while a fill runs
     std::uint32_t epoch_ctr = 0;

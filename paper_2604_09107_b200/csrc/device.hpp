@@ -111,6 +111,12 @@ struct PlanUpload {
   std::size_t scratch_bytes = 0;
   std::size_t h2d_bytes = 0;     // bytes uploaded by the last call
   std::vector<std::uint8_t> last;  // host image of the resident plan
+  // the inputs the resident plan was built from: an identical request skips
+  // the host build (tensor-map encoding) and only resets work/status words
+  std::vector<ItemDesc> key_items;
+  std::vector<SrcDesc> key_srcs;
+  std::uint32_t key_chunks = 0;
+  PullParams built{};
 };
 cudaError_t upload_pull_plan(int device, cudaStream_t s, ItemDesc* items, std::uint32_t n_items,
                              const SrcDesc* srcs, std::uint32_t n_srcs, std::uint32_t n_chunks,
@@ -130,8 +136,11 @@ cudaError_t launch_span_digests(const std::uint64_t* ptrs, const std::uint64_t* 
 // Gather/scatter copies: span i copies lens[i] bytes srcs[i] -> dsts[i].
 // lens[i] | kSpanCastE4M3: the span's bf16 bytes land as e4m3 (lens/2 bytes).
 constexpr std::uint64_t kSpanCastE4M3 = 1ull << 63;
+// tile0[i]: first tile (copy_span_tiles units) of span i; tiles: the total.
 cudaError_t launch_copy_spans(const std::uint64_t* srcs, const std::uint64_t* dsts,
-                              const std::uint64_t* lens, int n, cudaStream_t s);
+                              const std::uint64_t* lens, const std::uint64_t* tile0, int n,
+                              std::uint64_t tiles, cudaStream_t s);
+std::uint64_t copy_span_tiles(std::uint64_t len);  // tiles of one span (len may carry the cast flag)
 
 // Synthetic bf16 weights (SURVEY.md §8d generator; oracle ro_synth_bf16).
 cudaError_t launch_synth_bf16(std::uint16_t* dst, std::uint64_t n, std::uint64_t seed,

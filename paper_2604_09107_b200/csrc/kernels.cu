@@ -315,38 +315,62 @@ __global__ void __launch_bounds__(kDigWarps * 32)
 }
 
 // ---------------------------------------------------------------- K3 -----
-__global__ void copy_spans_kernel(const std::uint64_t* srcs, const std::uint64_t* dsts,
-                                  const std::uint64_t* lens, int n, int span0) {
-  const int span = span0 + static_cast<int>(blockIdx.y);
-  if (span >= n) return;
-  const std::uint8_t* src = reinterpret_cast<const std::uint8_t*>(srcs[span]);
-  std::uint8_t* dst = reinterpret_cast<std::uint8_t*>(dsts[span]);
-  const std::uint64_t len = lens[span] & ~kSpanCastE4M3;
-  const std::uint64_t stride = std::uint64_t(gridDim.x) * blockDim.x;
-  const std::uint64_t tid = std::uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (lens[span] & kSpanCastE4M3) {  // bf16 in, e4m3 out (len/2 bytes)
-    const bool v8 = (reinterpret_cast<std::uintptr_t>(src) & 15) == 0 &&
-                    (reinterpret_cast<std::uintptr_t>(dst) & 7) == 0;
-    const std::uint64_t units = v8 ? len / 16 : 0;
-    for (std::uint64_t i = tid; i < units; i += stride) {
-      const uint4 a = reinterpret_cast<const uint4*>(src)[i];
-      reinterpret_cast<uint2*>(dst)[i] = make_uint2(cvt4_e4m3(a.x, a.y), cvt4_e4m3(a.z, a.w));
+// Tiles of kCopyTile source bytes over all spans (tile0[i] = first tile of
+// span i): a block per tile, so many tiny spans and a few huge ones both
+// spread over the whole grid.
+constexpr std::uint64_t kCopyTile = 16384;
+
+__global__ void __launch_bounds__(256) copy_spans_kernel(const std::uint64_t* srcs,
+                                                         const std::uint64_t* dsts,
+                                                         const std::uint64_t* lens,
+                                                         const std::uint64_t* tile0, int n,
+                                                         std::uint64_t tiles) {
+  __shared__ int span_s;
+  for (std::uint64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+    if (threadIdx.x == 0) {
+      int lo = 0, hi = n;  // last span with tile0 <= t
+      while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (tile0[mid] <= t) lo = mid;
+        else hi = mid;
+      }
+      span_s = lo;
     }
-    for (std::uint64_t i = units * 8 + tid; i < len / 2; i += stride) {
-      const std::uint32_t w = std::uint32_t(src[2 * i]) | (std::uint32_t(src[2 * i + 1]) << 8);
-      dst[i] = static_cast<std::uint8_t>(cvt4_e4m3(w, 0) & 0xFF);
+    __syncthreads();
+    const int span = span_s;
+    __syncthreads();
+    const std::uint8_t* src = reinterpret_cast<const std::uint8_t*>(srcs[span]);
+    std::uint8_t* dst = reinterpret_cast<std::uint8_t*>(dsts[span]);
+    const std::uint64_t raw = lens[span];
+    const std::uint64_t len = raw & ~kSpanCastE4M3;
+    const std::uint64_t off = (t - tile0[span]) * kCopyTile;
+    const std::uint64_t end = off + kCopyTile < len ? off + kCopyTile : len;
+    if (raw & kSpanCastE4M3) {  // bf16 in, e4m3 out (half the bytes)
+      const bool v8 = ((reinterpret_cast<std::uintptr_t>(src) | off) & 15) == 0 &&
+                      (reinterpret_cast<std::uintptr_t>(dst) & 7) == 0;
+      std::uint64_t i = off;
+      if (v8) {
+        for (std::uint64_t k = off + 16 * threadIdx.x; k + 16 <= end; k += 16 * blockDim.x) {
+          const uint4 a = *reinterpret_cast<const uint4*>(src + k);
+          *reinterpret_cast<uint2*>(dst + k / 2) = make_uint2(cvt4_e4m3(a.x, a.y), cvt4_e4m3(a.z, a.w));
+        }
+        i = off + (end - off) / 16 * 16;
+      }
+      for (std::uint64_t k = i + 2 * threadIdx.x; k + 1 < end; k += 2 * blockDim.x) {
+        const std::uint32_t w = std::uint32_t(src[k]) | (std::uint32_t(src[k + 1]) << 8);
+        dst[k / 2] = static_cast<std::uint8_t>(cvt4_e4m3(w, 0) & 0xFF);
+      }
+      continue;
     }
-    return;
-  }
-  const bool vec =
-      ((reinterpret_cast<std::uintptr_t>(src) | reinterpret_cast<std::uintptr_t>(dst)) & 15) == 0;
-  if (vec) {
-    const std::uint64_t units = len / 16;
-    for (std::uint64_t i = tid; i < units; i += stride)
-      reinterpret_cast<uint4*>(dst)[i] = reinterpret_cast<const uint4*>(src)[i];
-    for (std::uint64_t i = units * 16 + tid; i < len; i += stride) dst[i] = src[i];
-  } else {
-    for (std::uint64_t i = tid; i < len; i += stride) dst[i] = src[i];
+    const bool vec =
+        ((reinterpret_cast<std::uintptr_t>(src) | reinterpret_cast<std::uintptr_t>(dst) | off) & 15) == 0;
+    std::uint64_t i = off;
+    if (vec) {
+      for (std::uint64_t k = off + 16 * threadIdx.x; k + 16 <= end; k += 16 * blockDim.x)
+        *reinterpret_cast<uint4*>(dst + k) = *reinterpret_cast<const uint4*>(src + k);
+      i = off + (end - off) / 16 * 16;
+    }
+    for (std::uint64_t k = i + threadIdx.x; k < end; k += blockDim.x) dst[k] = src[k];
   }
 }
 
@@ -457,15 +481,20 @@ cudaError_t launch_span_digests(const std::uint64_t* ptrs, const std::uint64_t* 
 }
 
 cudaError_t launch_copy_spans(const std::uint64_t* srcs, const std::uint64_t* dsts,
-                              const std::uint64_t* lens, int n, cudaStream_t s) {
-  for (int span0 = 0; span0 < n; span0 += 65535) {
-    const int cnt = n - span0 < 65535 ? n - span0 : 65535;
-    dim3 grid(64, static_cast<unsigned>(cnt));
-    copy_spans_kernel<<<grid, 256, 0, s>>>(srcs, dsts, lens, n, span0);
-    cudaError_t e = cudaGetLastError();
-    if (e != cudaSuccess) return e;
-  }
-  return cudaSuccess;
+                              const std::uint64_t* lens, const std::uint64_t* tile0, int n,
+                              std::uint64_t tiles, cudaStream_t s) {
+  if (n <= 0 || tiles == 0) return cudaSuccess;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const std::uint64_t cap = static_cast<std::uint64_t>(pull_grid(dev)) * 8;
+  const auto grid = static_cast<unsigned>(tiles < cap ? tiles : cap);
+  copy_spans_kernel<<<grid, 256, 0, s>>>(srcs, dsts, lens, tile0, n, tiles);
+  return cudaGetLastError();
+}
+
+std::uint64_t copy_span_tiles(std::uint64_t len) {
+  len &= ~kSpanCastE4M3;
+  return (len + kCopyTile - 1) / kCopyTile;
 }
 
 cudaError_t launch_synth_bf16(std::uint16_t* dst, std::uint64_t n, std::uint64_t seed,

@@ -68,6 +68,28 @@ cudaError_t upload_pull_plan(int device, cudaStream_t s, ItemDesc* items, std::u
                              const SrcDesc* srcs, std::uint32_t n_srcs, std::uint32_t n_chunks,
                              PlanUpload* up, PullParams* p) {
   const std::uint32_t n_batches = (n_chunks + kBatchChunks - 1) / kBatchChunks;
+  if (up->scratch && up->key_chunks == n_chunks && up->key_items.size() == n &&
+      up->key_srcs.size() == n_srcs &&
+      (n == 0 || std::memcmp(up->key_items.data(), items, n * sizeof(ItemDesc)) == 0) &&
+      (n_srcs == 0 || std::memcmp(up->key_srcs.data(), srcs, n_srcs * sizeof(SrcDesc)) == 0)) {
+    cudaError_t e = cudaMemsetAsync(up->scratch, 0, kHdr, s);  // fresh work/status words
+    if (e != cudaSuccess) return e;
+    up->h2d_bytes = 0;
+    const PullParams& b = up->built;
+    p->work = b.work;
+    p->status = b.status;
+    p->items = b.items;
+    p->n_items = b.n_items;
+    p->srcs = b.srcs;
+    p->n_srcs = b.n_srcs;
+    p->maps = b.maps;
+    p->batch_seg = b.batch_seg;
+    p->n_chunks = b.n_chunks;
+    p->n_batches = b.n_batches;
+    p->has_cast = b.has_cast;
+    return cudaSuccess;
+  }
+  std::vector<ItemDesc> key(items, items + n);  // the request, before flags are added below
   const std::size_t items_off = kHdr;
   const std::size_t srcs_off = items_off + n * sizeof(ItemDesc);
   const std::size_t maps_off = (srcs_off + n_srcs * sizeof(SrcDesc) + 255) / 256 * 256;
@@ -138,6 +160,10 @@ cudaError_t upload_pull_plan(int device, cudaStream_t s, ItemDesc* items, std::u
   p->n_chunks = n_chunks;
   p->has_cast = any_cast;
   p->n_batches = n_batches;
+  up->built = *p;
+  up->key_items = std::move(key);
+  up->key_srcs.assign(srcs, srcs + n_srcs);
+  up->key_chunks = n_chunks;
   (void)device;
   return cudaSuccess;
 }
@@ -152,6 +178,8 @@ void free_pull_plan(int device, PlanUpload* up) {
   up->scratch = nullptr;
   up->scratch_bytes = 0;
   up->last.clear();
+  up->key_items.clear();
+  up->key_srcs.clear();
 }
 
 }  // namespace rsb::dev
