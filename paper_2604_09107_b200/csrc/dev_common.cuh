@@ -26,8 +26,8 @@ __device__ __forceinline__ std::uint64_t rotl64(std::uint64_t x, int r) {
 // dependent instructions: the 64-bit add (lo, hi+carry), the rotation as two
 // independent funnel shifts, and the product as one wide multiply plus two
 // cross products folded by a 3-input add.  (w * P2 does not depend on acc.)
-__device__ __forceinline__ std::uint64_t xround(std::uint64_t acc, std::uint64_t w) {
-  const std::uint64_t t = acc + w * kP2;
+__device__ __forceinline__ std::uint64_t xround_pre(std::uint64_t acc, std::uint64_t wp2) {
+  const std::uint64_t t = acc + wp2;  // wp2 = w * P2
   const std::uint32_t lo = static_cast<std::uint32_t>(t), hi = static_cast<std::uint32_t>(t >> 32);
   const std::uint32_t rlo = __funnelshift_l(hi, lo, 31);  // (lo << 31) | (hi >> 1)
   const std::uint32_t rhi = __funnelshift_l(lo, hi, 31);  // (hi << 31) | (lo >> 1)
@@ -36,6 +36,9 @@ __device__ __forceinline__ std::uint64_t xround(std::uint64_t acc, std::uint64_t
   const std::uint64_t wl = static_cast<std::uint64_t>(rlo) * p1lo;
   const std::uint32_t h = static_cast<std::uint32_t>(wl >> 32) + rhi * p1lo + rlo * p1hi;
   return (static_cast<std::uint64_t>(h) << 32) | static_cast<std::uint32_t>(wl);
+}
+__device__ __forceinline__ std::uint64_t xround(std::uint64_t acc, std::uint64_t w) {
+  return xround_pre(acc, w * kP2);
 }
 __device__ __forceinline__ std::uint64_t avalanche(std::uint64_t h) {
   h ^= h >> 33;

@@ -225,77 +225,107 @@ __global__ void __launch_bounds__(kThreads, 2) pull_kernel(const PullParams p) {
 }
 
 // ---------------------------------------------------------------- K6 -----
-// One warp per span.  All lanes stage 1 KiB per step into a ring with
-// cp.async; lanes 0..3 run the four XXH64 accumulators of the reference's
-// 32-byte stripe loop (each lane one accumulator: digest.cpp:89-95), lane 0
-// merges and finalizes.
-constexpr int kDigWarps = 8;
-constexpr int kDigStep = 1024;
-constexpr int kDigRing = 8;
+// One warp per span.  XXH64 is serial within a span (each of the reference's
+// four accumulators, digest.cpp:89-95, is a dependent chain of round64), so a
+// span's digest is bound by the round latency (28 cycles on B200, measured by
+// tools/micro/xxh_chain.cu): lanes 0..3 run the four accumulators and must
+// never wait for data.  Lane 0 streams the span into a ring of 4 KiB slots
+// with one cp.async.bulk per slot (mbarrier completion), several slots ahead;
+// the accumulator lanes read their words from shared memory.  Lane 0 merges
+// and finalizes; the < 32-byte tail is read from global memory.  Spans that
+// are not 16-byte aligned take a per-lane cp.async path.
+constexpr int kDigWarps = 4;
+constexpr int kDigSlot = 4096;
+constexpr int kDigSlots = 8;
+
+__device__ __forceinline__ void digest_rounds(const std::uint8_t* st, int lane, int cnt,
+                                              std::uint64_t& acc) {
+  // Software-pipelined: the loads and w * P2 products of the next 16
+  // stripes are issued in the bubbles of this group's dependent chain.
+  const std::uint8_t* p = st + 8 * lane;
+  int k = 0;
+  if (cnt >= 16) {
+    std::uint64_t cur[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) cur[j] = *reinterpret_cast<const std::uint64_t*>(p + 32 * j) * kP2;
+    for (; k + 32 <= cnt; k += 16) {
+      std::uint64_t nxt[16];
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        nxt[j] = *reinterpret_cast<const std::uint64_t*>(p + 32 * (k + 16 + j)) * kP2;
+        acc = xround_pre(acc, cur[j]);
+      }
+#pragma unroll
+      for (int j = 0; j < 16; ++j) cur[j] = nxt[j];
+    }
+#pragma unroll
+    for (int j = 0; j < 16; ++j) acc = xround_pre(acc, cur[j]);
+    k += 16;
+  }
+  for (; k < cnt; ++k) acc = xround(acc, *reinterpret_cast<const std::uint64_t*>(p + 32 * k));
+}
 
 __global__ void __launch_bounds__(kDigWarps * 32)
     span_digest_kernel(const std::uint64_t* ptrs, const std::uint64_t* lens, std::uint64_t* out,
                        int n) {
-  extern __shared__ __align__(128) std::uint8_t dsm[];
+  extern __shared__ __align__(1024) std::uint8_t dsm[];
+  __shared__ __align__(8) unsigned long long bars[kDigWarps][kDigSlots];
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const int span = blockIdx.x * kDigWarps + warp;
   if (span >= n) return;
-  std::uint8_t* ring = dsm + warp * (kDigRing * kDigStep);
+  std::uint8_t* ring = dsm + warp * (kDigSlots * kDigSlot);
   const std::uint8_t* base = reinterpret_cast<const std::uint8_t*>(ptrs[span]);
   const std::uint64_t len = lens[span];
-  const bool aligned = (reinterpret_cast<std::uintptr_t>(base) & 15) == 0;
-  const std::uint64_t nsteps = (len + kDigStep - 1) / kDigStep;
-  auto load = [&](std::uint64_t s) {
-    std::uint8_t* dst = ring + (s % kDigRing) * kDigStep;
-#pragma unroll
-    for (int u = 0; u < kDigStep / 16 / 32; ++u) {
-      const std::uint64_t g = s * kDigStep + u * 512 + lane * 16;
-      if (g >= len) continue;
-      if (aligned && len - g >= 16) {
-        cp_async16(dst + u * 512 + lane * 16, base + g);
-      } else {
-        const std::uint64_t m = len - g < 16 ? len - g : 16;
-        for (std::uint64_t b = 0; b < m; ++b) dst[u * 512 + lane * 16 + b] = base[g + b];
-      }
-    }
-  };
-  std::uint64_t acc = lane == 0 ? kP1 + kP2 : lane == 1 ? kP2 : lane == 2 ? 0 : 0 - kP1;
   const std::uint64_t full_stripes = len >> 5;
-  for (int s = 0; s < kDigRing - 1; ++s) {
-    if (static_cast<std::uint64_t>(s) < nsteps) load(s);
-    cp_async_commit();
-  }
-  for (std::uint64_t s = 0; s < nsteps; ++s) {
-    if (s + kDigRing - 1 < nsteps) load(s + kDigRing - 1);
-    cp_async_commit();
-    cp_async_wait<kDigRing - 1>();
-    __syncwarp();
-    if (lane < 4) {
-      const std::uint8_t* st = ring + (s % kDigRing) * kDigStep + 8 * lane;
-      const std::uint64_t first = s * (kDigStep / 32);
-      std::uint64_t cnt = full_stripes > first ? full_stripes - first : 0;
-      if (cnt > kDigStep / 32) cnt = kDigStep / 32;
-      if (cnt == kDigStep / 32) {
-        // full step: loads hoisted 8 ahead so only the accumulator chain
-        // (round64, the serial part of XXH64) is on the critical path
-#pragma unroll
-        for (int k0 = 0; k0 < kDigStep / 32; k0 += 8) {
-          std::uint64_t w[8];
-#pragma unroll
-          for (int j = 0; j < 8; ++j) w[j] = *reinterpret_cast<const std::uint64_t*>(st + 32 * (k0 + j));
-#pragma unroll
-          for (int j = 0; j < 8; ++j) acc = xround(acc, w[j]);
-        }
-      } else {
-        for (std::uint64_t k = 0; k < cnt; ++k)
-          acc = xround(acc, *reinterpret_cast<const std::uint64_t*>(st + 32 * k));
-      }
+  std::uint64_t acc = lane == 0 ? kP1 + kP2 : lane == 1 ? kP2 : lane == 2 ? 0 : 0 - kP1;
+  const std::uint64_t nslots = (len + kDigSlot - 1) / kDigSlot;
+  constexpr int kSlotStripes = kDigSlot / 32;
+  if ((reinterpret_cast<std::uintptr_t>(base) & 15) == 0) {
+    unsigned long long* bar = bars[warp];
+    if (lane == 0) {
+      for (int k = 0; k < kDigSlots; ++k) mbar_init(&bar[k], 1);
+      asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
-    if (s + 1 < nsteps) __syncwarp();
+    __syncwarp();
+    auto issue = [&](std::uint64_t k) {  // lane 0: slot k of the span
+      unsigned long long* b = &bar[k % kDigSlots];
+      const std::uint64_t rem = len - k * kDigSlot;
+      const auto bytes = static_cast<unsigned>((rem < kDigSlot ? rem : kDigSlot) & ~15ull);
+      if (bytes) {
+        mbar_arrive_tx(b, bytes);
+        bulk_g2s(ring + (k % kDigSlots) * kDigSlot, base + k * kDigSlot, bytes, b);
+      } else {
+        mbar_arrive(b);
+      }
+    };
+    if (lane == 0)
+      for (std::uint64_t k = 0; k + 1 < kDigSlots && k < nslots; ++k) issue(k);
+    for (std::uint64_t k = 0; k < nslots; ++k) {
+      if (lane == 0 && k + kDigSlots - 1 < nslots) {
+        fence_proxy_async_smem();  // the slot's previous words were read by the generic proxy
+        issue(k + kDigSlots - 1);
+      }
+      mbar_wait(&bar[k % kDigSlots], static_cast<unsigned>((k / kDigSlots) & 1));
+      if (lane < 4) {
+        const std::uint64_t first = k * kSlotStripes;
+        const std::uint64_t cnt = full_stripes > first ? full_stripes - first : 0;
+        digest_rounds(ring + (k % kDigSlots) * kDigSlot, lane,
+                      static_cast<int>(cnt < kSlotStripes ? cnt : kSlotStripes), acc);
+      }
+      __syncwarp();
+    }
+  } else {
+    // unaligned span: per-lane stripe words straight from global memory
+    if (lane < 4)
+      for (std::uint64_t k = 0; k < full_stripes; ++k) {
+        std::uint64_t w = 0;
+        const std::uint8_t* q = base + 32 * k + 8 * lane;
+#pragma unroll
+        for (int b = 0; b < 8; ++b) w |= std::uint64_t(q[b]) << (8 * b);
+        acc = xround(acc, w);
+      }
   }
-  cp_async_wait<0>();
-  __syncwarp();
   const std::uint64_t a = __shfl_sync(0xffffffffu, acc, 0);
   const std::uint64_t b = __shfl_sync(0xffffffffu, acc, 1);
   const std::uint64_t c = __shfl_sync(0xffffffffu, acc, 2);
@@ -304,17 +334,10 @@ __global__ void __launch_bounds__(kDigWarps * 32)
     std::uint64_t h = len >= 32 ? merge4(a, b, c, d) : kP5;
     h += len;
     const std::uint64_t tail_at = full_stripes * 32;
-    const int tail = static_cast<int>(len - tail_at);
-    const std::uint8_t* tp = ring;
-    if (tail > 0) {
-      const std::uint64_t s = tail_at / kDigStep;
-      tp = ring + (s % kDigRing) * kDigStep + (tail_at - s * kDigStep);
-    }
-    out[span] = finish_tail(h, tp, tail);
+    out[span] = finish_tail(h, base + tail_at, static_cast<int>(len - tail_at));
   }
 }
 
-// ---------------------------------------------------------------- K3 -----
 // Tiles of kCopyTile source bytes over all spans (tile0[i] = first tile of
 // span i): a block per tile, so many tiny spans and a few huge ones both
 // spread over the whole grid.
@@ -465,7 +488,7 @@ cudaError_t launch_pull(const PullParams& p, int sms, cudaStream_t s) {
 cudaError_t launch_span_digests(const std::uint64_t* ptrs, const std::uint64_t* lens,
                                 std::uint64_t* out, int n, cudaStream_t s) {
   if (n <= 0) return cudaSuccess;
-  constexpr int smem = kDigWarps * kDigRing * kDigStep;
+  constexpr int smem = kDigWarps * kDigSlots * kDigSlot;
   static bool attr_done[64] = {};
   int dev = 0;
   cudaGetDevice(&dev);
