@@ -4,10 +4,12 @@
 // (client_core.cpp:306-334); with segment mappings (ItemDesc q < m, several
 // sources) it also performs the TP/FSDP reshard gather/split.
 //
-// Warp-specialized, persistent: each CTA is one producer warp and one
-// consumer warp sharing a ring of S stages in shared memory.  A stage holds
-// the next P bytes of each of the 32 chunks of one watermark batch; lane l
-// of the consumer hashes landing chunk 32b+l.
+// Warp-specialized, persistent: a pipeline is one producer warp and one
+// consumer warp sharing a ring of S stages in shared memory; a CTA holds
+// PIPES pipelines (default: one CTA per SM with four, so the four hashing
+// consumers sit on the four SM sub-partitions).  A stage holds the next P
+// bytes of each of the 32 chunks of one watermark batch; lane l of the
+// consumer hashes landing chunk 32b+l.
 //
 // Two stage layouts:
 //  * box (the common case: all 32 chunks of the batch are whole chunks of one
@@ -21,7 +23,7 @@
 //    regions): one padded slot of P+16 bytes per chunk, every lane issuing
 //    its own cp.async.bulk copy (plain loads/stores for unaligned bytes).
 //
-//   producer  walks its batches (static schedule b = blockIdx.x + k*grid, so
+//   producer  walks its batches (static schedule b = pipeline + k*pipelines, so
 //             the landed prefix advances front to back), waits the source
 //             watermark(s) when a source is still filling, fills stages.
 //   consumer  per stage: lands the stage (tensor store / bulk stores), hashes
@@ -71,8 +73,10 @@ __device__ __forceinline__ void tensor_store_2d(const void* map, int x, int y, c
       : "memory");
 }
 
-template <int P, int S, int CTAS, int ITEMS>
+template <int P, int S, int CTAS, int ITEMS, int PIPES = 1>
 struct Cfg {
+  static constexpr int kPipes = PIPES;  // producer/consumer pairs per CTA
+  static constexpr int kThreads = 64 * PIPES;
   static constexpr int kP = P;
   static constexpr int kSlot = P + 16;
   static constexpr int kStage = (32 * kSlot + 1023) / 1024 * 1024;  // box layout needs 1 KiB
@@ -100,18 +104,23 @@ struct Cfg {
     std::uint32_t seg[32];  // segment of each lane's chunk
     std::uint64_t expect[32];
   };
-  struct Smem {
+  // One pipeline: a ring of S stages between a producer and a consumer warp.
+  struct alignas(1024) Pipe {
     std::uint8_t stage[S][kStage];
     Meta meta[S];
-    alignas(16) ItemDesc items[ITEMS > 0 ? ITEMS : 1];  // ITEMS == 0: segments stay in global  // copied in with 16-byte vectors
     unsigned long long full[S];
     unsigned long long empty[S];
+  };
+  struct Smem {
+    Pipe pipes[PIPES];
+    // ITEMS == 0: segments stay in global; copied in with 16-byte vectors
+    alignas(16) ItemDesc items[ITEMS > 0 ? ITEMS : 1];
   };
   static constexpr int kSmemBytes = static_cast<int>(sizeof(Smem)) + 1024;
 };
 
 template <class C>
-__global__ void __launch_bounds__(64, C::kCtas) pull_tma_kernel(const PullParams p) {
+__global__ void __launch_bounds__(C::kThreads, C::kCtas) pull_tma_kernel(const PullParams p) {
   using Smem = typename C::Smem;
   using Meta = typename C::Meta;
   constexpr int kP = C::kP;
@@ -138,21 +147,30 @@ __global__ void __launch_bounds__(64, C::kCtas) pull_tma_kernel(const PullParams
     for (std::uint32_t i = threadIdx.x; i < n16; i += blockDim.x) d[i] = s[i];
   }
   if (threadIdx.x == 0) {
-    for (int s = 0; s < kStages; ++s) {
-      mbar_init(&sm.full[s], 1);
-      mbar_init(&sm.empty[s], 1);
-    }
+    for (int qq = 0; qq < C::kPipes; ++qq)
+      for (int s = 0; s < kStages; ++s) {
+        mbar_init(&sm.pipes[qq].full[s], 1);
+        mbar_init(&sm.pipes[qq].empty[s], 1);
+      }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();
   const ItemDesc* items = smem_items ? sm.items : p.items;
+  // Warps 0..PIPES-1 consume, PIPES..2*PIPES-1 produce; pipeline q pairs
+  // consumer q with producer PIPES+q.  With PIPES == 4 the four consumers
+  // (the hashing warps) sit on the four SM sub-partitions, one each.
+  const int q = warp % C::kPipes;
+  typename C::Pipe& pp = sm.pipes[q];
+  // each pipeline is a virtual CTA of the persistent batch schedule
+  const std::uint32_t vcta = blockIdx.x * C::kPipes + q;
+  const std::uint32_t vgrid = gridDim.x * C::kPipes;
 
-  if (warp == 0) {
+  if (warp >= C::kPipes) {
     // ================================ producer ==============================
     int stage = 0;
     unsigned phase = 0;
     std::uint32_t abort_seen = 0;
-    for (std::uint32_t b = p.first_batch + blockIdx.x; b < p.n_batches; b += gridDim.x) {
+    for (std::uint32_t b = p.first_batch + vcta; b < p.n_batches; b += vgrid) {
       if (abort_seen) break;
       const std::uint32_t abort_next = ld_volatile(&p.work[1]);  // acted on next batch
       if (p.resume && ld_volatile(&p.dst_flags[b]) == p.dst_epoch) {  // landed already
@@ -225,8 +243,8 @@ __global__ void __launch_bounds__(64, C::kCtas) pull_tma_kernel(const PullParams
       const std::uint32_t nsteps = (maxlen + kP - 1) / kP;
       const bool src_vec = (reinterpret_cast<std::uintptr_t>(r.src) & 15) == 0;
       for (std::uint32_t s = 0; s < nsteps; ++s) {
-        mbar_wait(&sm.empty[stage], phase ^ 1);
-        Meta& m = sm.meta[stage];
+        mbar_wait(&pp.empty[stage], phase ^ 1);
+        Meta& m = pp.meta[stage];
         const std::uint32_t g = s * kP;
         const std::uint32_t piece =
             g < r.clen ? min(static_cast<std::uint32_t>(kP), r.clen - g) : 0;
@@ -258,22 +276,22 @@ __global__ void __launch_bounds__(64, C::kCtas) pull_tma_kernel(const PullParams
           }
           __syncwarp();
           if (lane == 0) {
-            mbar_arrive_tx(&sm.full[stage], 32 * piece + dig_tx);
-            if (dig_tx) bulk_g2s(m.expect, dig_src, dig_tx, &sm.full[stage]);
+            mbar_arrive_tx(&pp.full[stage], 32 * piece + dig_tx);
+            if (dig_tx) bulk_g2s(m.expect, dig_src, dig_tx, &pp.full[stage]);
             const void* map = maps + 256 * std::size_t(seg0);
             const std::uint32_t qq = q0;
             for (std::uint32_t j = 0; j < piece / kMapBoxCols; ++j) {
               const int x = static_cast<int>(g + j * kMapBoxCols);
               if (map3d)
-                tensor_load_3d(sm.stage[stage] + j * 4096, map, x, 0, static_cast<int>(k0 / qq),
-                               &sm.full[stage]);
+                tensor_load_3d(pp.stage[stage] + j * 4096, map, x, 0, static_cast<int>(k0 / qq),
+                               &pp.full[stage]);
               else
-                tensor_load_2d(sm.stage[stage] + j * 4096, map, x, static_cast<int>(k0),
-                               &sm.full[stage]);
+                tensor_load_2d(pp.stage[stage] + j * 4096, map, x, static_cast<int>(k0),
+                               &pp.full[stage]);
             }
           }
         } else {
-          std::uint8_t* slot = sm.stage[stage] + lane * C::kSlot;
+          std::uint8_t* slot = pp.stage[stage] + lane * C::kSlot;
           const std::uint32_t bulk = src_vec ? (piece & ~15u) : 0;
           for (std::uint32_t kk = bulk; kk < piece; ++kk) slot[kk] = __ldcg(r.src + g + kk);
           std::uint32_t tx = bulk;
@@ -287,20 +305,20 @@ __global__ void __launch_bounds__(64, C::kCtas) pull_tma_kernel(const PullParams
           }
           __syncwarp();
           if (lane == 0) {
-            mbar_arrive_tx(&sm.full[stage], tx + dig_tx);
-            if (dig_tx) bulk_g2s(m.expect, dig_src, dig_tx, &sm.full[stage]);
+            mbar_arrive_tx(&pp.full[stage], tx + dig_tx);
+            if (dig_tx) bulk_g2s(m.expect, dig_src, dig_tx, &pp.full[stage]);
           }
           __syncwarp();
-          if (bulk) bulk_g2s(slot, r.src + g, bulk, &sm.full[stage]);
+          if (bulk) bulk_g2s(slot, r.src + g, bulk, &pp.full[stage]);
         }
         advance(stage, phase);
       }
       abort_seen = abort_next;
     }
-    mbar_wait(&sm.empty[stage], phase ^ 1);  // poison pill: nothing more
+    mbar_wait(&pp.empty[stage], phase ^ 1);  // poison pill: nothing more
     if (lane == 0) {
-      sm.meta[stage].batch = kPill;
-      mbar_arrive(&sm.full[stage]);
+      pp.meta[stage].batch = kPill;
+      mbar_arrive(&pp.full[stage]);
     }
   } else {
     // ================================ consumer ==============================
@@ -333,13 +351,13 @@ __global__ void __launch_bounds__(64, C::kCtas) pull_tma_kernel(const PullParams
       pend_bytes = 0;
     };
     for (;;) {
-      mbar_wait(&sm.full[stage], phase);
-      const Meta& m = sm.meta[stage];
+      mbar_wait(&pp.full[stage], phase);
+      const Meta& m = pp.meta[stage];
       const std::uint32_t b = m.batch;
       if (b == kPill) break;
       if (failed) {  // drain until the pill
         __syncwarp();
-        if (lane == 0) mbar_arrive(&sm.empty[stage]);
+        if (lane == 0) mbar_arrive(&pp.empty[stage]);
         advance(stage, phase);
         continue;
       }
@@ -348,7 +366,7 @@ __global__ void __launch_bounds__(64, C::kCtas) pull_tma_kernel(const PullParams
       const std::uint32_t clen = m.clen[lane];
       const bool last = m.last != 0;
       const bool box = m.box != 0;
-      std::uint8_t* st = sm.stage[stage];
+      std::uint8_t* st = pp.stage[stage];
       bool committed = false;
       if (s == 0) {
         v1 = kP1 + kP2;
@@ -471,7 +489,7 @@ __global__ void __launch_bounds__(64, C::kCtas) pull_tma_kernel(const PullParams
       // 4) free the stage once the stores issued from it have read it
       if (committed) bulk_wait_read<0>();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&sm.empty[stage]);
+      if (lane == 0) mbar_arrive(&pp.empty[stage]);
       advance(stage, phase);
       if (!last) continue;
       // 5) batch complete: verify and record
@@ -529,8 +547,9 @@ cudaError_t launch_variant(const PullParams& p, int sms, cudaStream_t s) {
   }
   const std::uint32_t todo = p.n_batches - p.first_batch;
   int grid = sms * C::kCtas;
-  if (static_cast<std::uint32_t>(grid) > todo) grid = static_cast<int>(todo);
-  pull_tma_kernel<C><<<grid, 64, C::kSmemBytes, s>>>(p);
+  const auto per = static_cast<std::uint32_t>(C::kPipes);
+  if (static_cast<std::uint32_t>(grid) * per > todo) grid = static_cast<int>((todo + per - 1) / per);
+  pull_tma_kernel<C><<<grid, C::kThreads, C::kSmemBytes, s>>>(p);
   return cudaGetLastError();
 }
 
@@ -541,6 +560,8 @@ using V3 = Cfg<256, 6, 3, 192>;
 using V4 = Cfg<512, 3, 4, 0>;  // segment table in global (L1-cached): 4 CTAs per SM
 using V5 = Cfg<512, 2, 6, 0>;  // 2-stage rings, 6 CTAs per SM
 using V6 = Cfg<256, 3, 7, 0>;  // 7 CTAs per SM
+using V7 = Cfg<512, 3, 1, 0, 4>;    // one CTA per SM: 4 pipelines, consumers on 4 sub-partitions
+using V8 = Cfg<512, 2, 1, 320, 4>;  // 4 two-stage pipelines + the segment table in smem
 
 int variant() {  // -1: by workload
   static const int v = [] {
@@ -553,14 +574,14 @@ int variant() {  // -1: by workload
 }  // namespace
 
 cudaError_t launch_pull_tma(const PullParams& p, int sms, cudaStream_t s) {
-  // Measured on B200: local plain pulls are fastest with 3 CTAs/SM and the
-  // segment table in shared memory (V0, profiles/r1/variants.txt); a cast
-  // pull's consumers do ~60% more work per byte and want the 4th CTA, and a
-  // pull over NVLink wants its extra in-flight stages -- with both
-  // directions of a link busy V0 drops to ~675 GB/s, V4 holds ~775
-  // (profiles/r1/nvlink_dir.json).
+  // Default V8: one CTA per SM with four producer/consumer pipelines (two
+  // stages each), so the four hashing warps sit on the four sub-partitions.
+  // Measured on B200 (profiles/r1/variants_pipes.txt): local plain pull 90.7%
+  // of HBM (V0, 3 two-warp CTAs with both consumers' hashing on two
+  // sub-partitions: 88-90%), fp8 cast pull 84.8% (V4: 80.7%); over NVLink
+  // equal to V4 (785 GB/s one way, 672 with both directions busy).
   int v = variant();
-  if (v < 0) v = (p.has_cast || p.remote) ? 4 : 0;
+  if (v < 0) v = 8;
   switch (v) {
     case 1: return launch_variant<V1>(p, sms, s);
     case 2: return launch_variant<V2>(p, sms, s);
@@ -568,6 +589,8 @@ cudaError_t launch_pull_tma(const PullParams& p, int sms, cudaStream_t s) {
     case 4: return launch_variant<V4>(p, sms, s);
     case 5: return launch_variant<V5>(p, sms, s);
     case 6: return launch_variant<V6>(p, sms, s);
+    case 7: return launch_variant<V7>(p, sms, s);
+    case 8: return launch_variant<V8>(p, sms, s);
     default: return launch_variant<V0>(p, sms, s);
   }
 }
