@@ -373,8 +373,9 @@ def run_single(args):
         "publish_s": round(publish_s, 4), "publish_device_ms": round(publish_ms, 3),
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peaks["hbm_gbs"],
                      "unit": "GB/s", "frac": round(achieved / peaks["hbm_gbs"], 4),
-                     "traffic": ncu_traffic("local"), "peak_src": peaks["src"],
-                     "kernel": "pull_kernel", "kernel_ms_avg": round(k_avg, 3),
+                     "traffic": ncu_traffic("cast" if cast else "local") if not reshard else None,
+                     "peak_src": peaks["src"],
+                     "kernel": "pull_tma_kernel", "kernel_ms_avg": round(k_avg, 3),
                      "alg_bytes_per_launch": alg},
         "e2e": {"value": round(e2e, 2), "unit": UNIT,
                 "h2d_bytes_per_step": (st.h2d_bytes - h2d0) // args.steps,

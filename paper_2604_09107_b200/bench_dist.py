@@ -139,7 +139,7 @@ def run(args):
             "roofline": {"bound": "nvlink", "achieved": round(mean_rx, 1), "peak": 900.0,
                          "unit": "GB/s", "frac": round(mean_rx / 900.0, 4),
                          "traffic": B.ncu_traffic("nvlink"), "peak_src": "nominal NVLink5 per direction "
-                         "(measured peer copy 770 GB/s)", "kernel": "pull_kernel",
+                         "(measured peer copy 777 GB/s)", "kernel": "pull_tma_kernel",
                          "kernel_ms_avg": round(statistics.mean(step_dev_ms), 3),
                          "alg_bytes_per_launch": total},
             "e2e": {"value": round(total_landed / wall_s / 1e9, 2), "unit": B.UNIT,
