@@ -214,6 +214,38 @@ int rs_transfer_finish(rs_handle* h, uint64_t version, int ok);
 int rs_serve_export(rs_handle* h, uint32_t shard, void* buf, size_t cap, size_t* len);
 int rs_serve_import(rs_cluster* c, const void* blob, size_t len);
 
+/* ---- retention offload (RetentionRule types.hpp:119-123; client_core.cpp
+ * 1675-1717; server_core.cpp 1387-1485, 1592-1645) ---------------------------
+ * A replica may ask the cluster to keep the versions at some lags behind the
+ * newest published one reachable.  When the last durable copy of such a
+ * version unpublishes (or updates away), its client first parks it in pinned
+ * host memory (POSIX shared memory registered with CUDA) and the registry
+ * adds replica "<owner>+offload@<v>", which serves readers like any copy
+ * (the pull kernel reads host memory over PCIe) until a worker holds the
+ * version again or it leaves the retained window.  rs_unpublish/rs_update do
+ * all of this; the split-phase calls below let a multi-process caller do it. */
+int rs_set_retention(rs_handle* h, const uint64_t* lags, size_t n);  /* before the first op */
+/* ClientCore::open (client_core.hpp:83): join the cluster without an op (a
+ * pure observer whose retention rule keeps versions reachable). */
+int rs_connect(rs_handle* h);
+int rs_offload_lanes(rs_handle* h, uint64_t version);                 /* park v (local shards) */
+int rs_lane_export(rs_handle* h, uint32_t shard, uint64_t version, void* buf, size_t cap,
+                   size_t* len);
+int rs_offload_release(rs_handle* h, uint64_t version);
+int rs_poll(rs_handle* h);  /* free the lanes the registry released */
+int rs_lanes(rs_handle* h, uint64_t* versions, size_t cap, size_t* n);
+int rs_server_set_retention(rs_cluster* c, const char* model, const char* replica,
+                            const uint64_t* lags, size_t n);
+/* 1 (and *version) while the replica's unpublish/update waits for an offload. */
+int rs_server_offload_pending(rs_cluster* c, const char* model, const char* replica,
+                              uint64_t* version);
+int rs_server_offload_confirm(rs_cluster* c, const char* model, const char* replica,
+                              uint32_t shard, uint64_t version, int ok, const char* endpoint);
+int rs_server_take_releases(rs_cluster* c, const char* model, const char* owner,
+                            uint64_t* versions, size_t cap, size_t* n);
+int rs_cluster_kind(rs_cluster* c, const char* model, const char* replica, char* buf, size_t cap,
+                    size_t* len);  /* "worker" | "offload" */
+
 /* ---- device primitives (kernel boundary) --------------------------------- */
 /* digest64 (digest.cpp:79-106) of n device spans; out is host memory. */
 int rs_digest_spans(const uint64_t* dev_ptrs, const uint64_t* lens, int n, uint64_t* out,

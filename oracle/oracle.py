@@ -90,6 +90,8 @@ def ref():
                                                      C.c_uint64]
         lib.ref_cluster_publish.argtypes = [C.c_void_p, C.c_char_p, C.c_uint64, C.c_void_p]
         lib.ref_cluster_unpublish.argtypes = [C.c_void_p, C.c_char_p]
+        lib.ref_cluster_set_retention.argtypes = [C.c_void_p, C.c_char_p, C.c_void_p, C.c_int]
+        lib.ref_cluster_open.argtypes = [C.c_void_p, C.c_char_p]
         lib.ref_cluster_pull_many.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_char_p, C.c_int,
                                               C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
         lib.ref_cluster_settle.argtypes = [C.c_void_p]
@@ -295,6 +297,14 @@ class RefCluster:
 
     def unpublish(self, replica):
         return self.lib.ref_cluster_unpublish(self.h, replica.encode())
+
+    def open(self, replica):
+        return self.lib.ref_cluster_open(self.h, replica.encode())
+
+    def set_retention(self, replica, lags):
+        arr = (C.c_uint64 * max(len(lags), 1))(*lags)
+        return self.lib.ref_cluster_set_retention(self.h, replica.encode(), C.cast(arr, C.c_void_p),
+                                                  len(lags))
 
     def pull_many(self, replicas, spec="latest", update=False):
         n = len(replicas)

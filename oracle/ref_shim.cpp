@@ -259,6 +259,25 @@ int ref_cluster_publish(void* h, const char* replica, std::uint64_t v,
   return static_cast<int>(r[0].status);
 }
 
+// ClientCore::set_retention (client_core.cpp:528): sent with the handle's
+// open (OpenReq.retain), so call before the replica's first operation.
+int ref_cluster_set_retention(void* h, const char* replica, const std::uint64_t* lags, int n) {
+  auto* c = static_cast<Cluster*>(h);
+  auto it = c->nodes.find(replica);
+  if (it == c->nodes.end()) return -1;
+  RetentionRule rule;
+  for (int i = 0; i < n; ++i) rule.lags.insert(lags[i]);
+  it->second->core->set_retention(rule);
+  return 0;
+}
+
+int ref_cluster_open(void* h, const char* replica) {
+  auto* c = static_cast<Cluster*>(h);
+  auto* core = c->nodes.at(replica)->core.get();
+  auto r = c->run_many({[&](ClientCore::OpFn cb) { core->open(cb); }}, nullptr);
+  return static_cast<int>(r[0].status);
+}
+
 int ref_cluster_unpublish(void* h, const char* replica) {
   auto* c = static_cast<Cluster*>(h);
   auto* core = c->nodes.at(replica)->core.get();

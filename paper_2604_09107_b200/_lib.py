@@ -59,6 +59,18 @@ _SIGS = {
     "rs_register_cast": (i32, [vp, u32, cstr, vp, u64, u64, u64, u64, u64, u64, u64]),
     "rs_layout_key": (i32, [vp, vp, sz, C.POINTER(sz)]),
     "rs_shard_local": (i32, [vp, u32]),
+    "rs_set_retention": (i32, [vp, vp, sz]),
+    "rs_connect": (i32, [vp]),
+    "rs_offload_lanes": (i32, [vp, u64]),
+    "rs_lane_export": (i32, [vp, u32, u64, vp, sz, C.POINTER(sz)]),
+    "rs_offload_release": (i32, [vp, u64]),
+    "rs_poll": (i32, [vp]),
+    "rs_lanes": (i32, [vp, vp, sz, C.POINTER(sz)]),
+    "rs_server_set_retention": (i32, [vp, cstr, cstr, vp, sz]),
+    "rs_server_offload_pending": (i32, [vp, cstr, cstr, C.POINTER(u64)]),
+    "rs_server_offload_confirm": (i32, [vp, cstr, cstr, u32, u64, i32, cstr]),
+    "rs_server_take_releases": (i32, [vp, cstr, cstr, vp, sz, C.POINTER(sz)]),
+    "rs_cluster_kind": (i32, [vp, cstr, cstr, vp, sz, C.POINTER(sz)]),
     "rs_transfer_launch": (i32, [vp]),
     "rs_transfer_progress": (i32, [vp, u32, C.POINTER(u32), C.POINTER(u32)]),
     "rs_transfer_wait": (i32, [vp, vp, vp]),

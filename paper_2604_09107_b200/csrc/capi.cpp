@@ -556,6 +556,94 @@ int rs_serve_import(rs_cluster* c, const void* blob, size_t len) {
   return st(c->serves.import_state(std::string(static_cast<const char*>(blob), len)));
 }
 
+// ------------------------------------------------------- retention offload
+
+int rs_connect(rs_handle* h) {
+  if (!h) return st(rsb::Status::invalid_argument);
+  return st(h->client->open());
+}
+
+int rs_set_retention(rs_handle* h, const uint64_t* lags, size_t n) {
+  if (!h || (n && !lags)) return st(rsb::Status::invalid_argument);
+  h->client->set_retention(std::set<std::uint64_t>(lags, lags + n));
+  return 0;
+}
+
+int rs_offload_lanes(rs_handle* h, uint64_t version) {
+  if (!h) return st(rsb::Status::invalid_argument);
+  std::vector<std::string> eps;
+  return st(h->client->make_retention_lanes(version, &eps));
+}
+
+int rs_lane_export(rs_handle* h, uint32_t shard, uint64_t version, void* buf, size_t cap,
+                   size_t* len) {
+  if (!h) return st(rsb::Status::invalid_argument);
+  auto b = h->client->export_lane(shard, version);
+  if (!b) return st(b.status());
+  return put_bytes(*b, static_cast<char*>(buf), cap, len);
+}
+
+int rs_offload_release(rs_handle* h, uint64_t version) {
+  if (!h) return st(rsb::Status::invalid_argument);
+  h->client->release_lane(version);
+  return 0;
+}
+
+int rs_poll(rs_handle* h) {
+  if (!h) return st(rsb::Status::invalid_argument);
+  h->client->apply_releases();
+  return 0;
+}
+
+int rs_lanes(rs_handle* h, uint64_t* versions, size_t cap, size_t* n) {
+  if (!h) return st(rsb::Status::invalid_argument);
+  auto vs = h->client->lanes();
+  if (n) *n = vs.size();
+  if (versions)
+    for (size_t i = 0; i < vs.size() && i < cap; ++i) versions[i] = vs[i];
+  return 0;
+}
+
+int rs_server_set_retention(rs_cluster* c, const char* model, const char* replica,
+                            const uint64_t* lags, size_t n) {
+  if (!c || !model || !replica || (n && !lags)) return st(rsb::Status::invalid_argument);
+  return st(c->reg.set_retention(model, replica, std::set<std::uint64_t>(lags, lags + n)));
+}
+
+int rs_server_offload_pending(rs_cluster* c, const char* model, const char* replica,
+                              uint64_t* version) {
+  if (!c || !model || !replica) return 0;
+  auto o = c->reg.op_result(model, replica);
+  if (o.done || !o.offload_first) return 0;
+  if (version) *version = *o.offload_first;
+  return 1;
+}
+
+int rs_server_offload_confirm(rs_cluster* c, const char* model, const char* replica,
+                              uint32_t shard, uint64_t version, int ok, const char* endpoint) {
+  if (!c || !model || !replica) return st(rsb::Status::invalid_argument);
+  return st(c->reg.offload_confirm(model, replica, shard, version, ok != 0,
+                                   endpoint ? endpoint : ""));
+}
+
+int rs_server_take_releases(rs_cluster* c, const char* model, const char* owner,
+                            uint64_t* versions, size_t cap, size_t* n) {
+  if (!c || !model || !owner) return st(rsb::Status::invalid_argument);
+  auto rs = c->reg.take_releases(model, owner);
+  if (n) *n = rs.size();
+  if (versions)
+    for (size_t i = 0; i < rs.size() && i < cap; ++i) versions[i] = rs[i].version;
+  return 0;
+}
+
+int rs_cluster_kind(rs_cluster* c, const char* model, const char* replica, char* buf, size_t cap,
+                    size_t* len) {
+  if (!c || !model || !replica) return st(rsb::Status::invalid_argument);
+  auto v = c->reg.view(model, replica);
+  if (!v) return st(rsb::Status::not_found);
+  return put_bytes(v->kind, buf, cap, len);
+}
+
 // ------------------------------------------------------- device primitives
 
 int rs_digest_spans(const uint64_t* dev_ptrs, const uint64_t* lens, int n, uint64_t* out,

@@ -1,6 +1,8 @@
 #include "client.hpp"
 
 #include <cuda.h>
+#include <fcntl.h>
+#include <sys/mman.h>
 #include <unistd.h>
 
 #include <algorithm>
@@ -167,9 +169,85 @@ void retarget_ipc(const std::vector<ServeState::Alloc>& before,
   }
 }
 
+// Host (retention offload) segments mapped into this process by name, kept
+// while an imported serve state refers to them.
+struct HostEntry {
+  int refs = 0;
+  void* p = nullptr;
+  std::size_t n = 0;
+};
+std::mutex g_host_mu;
+std::map<std::string, HostEntry> g_host;
+
+Result<std::uint64_t> open_host(const std::string& name, std::size_t n) {
+  std::lock_guard lk(g_host_mu);
+  HostEntry& e = g_host[name];
+  if (e.p) return reinterpret_cast<std::uint64_t>(e.p);
+  const int fd = shm_open(name.c_str(), O_RDWR, 0);
+  if (fd < 0) return Status::not_serving;
+  void* p = mmap(nullptr, n, PROT_READ | PROT_WRITE, MAP_SHARED, fd, 0);
+  close(fd);
+  if (p == MAP_FAILED) return Status::not_serving;
+  if (cudaHostRegister(p, n, cudaHostRegisterPortable | cudaHostRegisterMapped) != cudaSuccess) {
+    cudaGetLastError();
+    munmap(p, n);
+    return Status::not_serving;
+  }
+  e.p = p;
+  e.n = n;
+  return reinterpret_cast<std::uint64_t>(p);
+}
+
+void retarget_host(const std::string& before, const std::string& now) {
+  if (before == now) return;
+  std::lock_guard lk(g_host_mu);
+  if (!now.empty()) ++g_host[now].refs;
+  if (before.empty()) return;
+  auto it = g_host.find(before);
+  if (it == g_host.end() || --it->second.refs > 0) return;
+  if (it->second.p) {
+    cudaHostUnregister(it->second.p);
+    cudaGetLastError();
+    munmap(it->second.p, it->second.n);
+  }
+  g_host.erase(it);
+}
+
 }  // namespace
 
 // ------------------------------------------------------------------ DevBuf
+
+HostBuf::~HostBuf() {
+  if (!p) return;
+  cudaHostUnregister(p);
+  cudaGetLastError();
+  munmap(p, n);
+  shm_unlink(name.c_str());
+}
+
+Status HostBuf::alloc(std::size_t bytes) {
+  static std::atomic<std::uint64_t> ctr{0};
+  name = "/rsb-" + std::to_string(getpid()) + "-" + std::to_string(ctr++);
+  n = bytes ? bytes : 1;
+  const int fd = shm_open(name.c_str(), O_CREAT | O_EXCL | O_RDWR, 0600);
+  if (fd < 0) return Status::offload_failed;
+  const bool sized = ftruncate(fd, static_cast<off_t>(n)) == 0;
+  void* q = sized ? mmap(nullptr, n, PROT_READ | PROT_WRITE, MAP_SHARED | MAP_POPULATE, fd, 0)
+                  : MAP_FAILED;
+  close(fd);
+  if (q == MAP_FAILED) {
+    shm_unlink(name.c_str());
+    return Status::offload_failed;
+  }
+  if (cudaHostRegister(q, n, cudaHostRegisterPortable | cudaHostRegisterMapped) != cudaSuccess) {
+    cudaGetLastError();
+    munmap(q, n);
+    shm_unlink(name.c_str());
+    return Status::offload_failed;
+  }
+  p = q;
+  return Status::ok;
+}
 
 DevBuf::~DevBuf() {
   if (p) {
@@ -264,7 +342,10 @@ void ServeRegistry::erase(const std::string& k) {
     map_.erase(it);
   }
   std::lock_guard lk(st->m);
-  if (st->imported) retarget_ipc(st->allocs, {});
+  if (st->imported) {
+    retarget_ipc(st->allocs, {});
+    retarget_host(st->host_name, {});
+  }
   st->allocs.clear();
 }
 
@@ -287,6 +368,31 @@ Result<std::string> ServeRegistry::export_state(const std::string& k) {
   if (!st) return Status::not_found;
   std::lock_guard lk(st->m);
   if (st->imported) return Status::invalid_state;
+  if (!st->host_name.empty()) {  // a retention offload: named shared memory
+    std::vector<std::pair<std::uint32_t, std::uint64_t>> item_loc(st->item_ptrs.size());
+    for (std::size_t i = 0; i < st->item_ptrs.size(); ++i) item_loc[i] = {0, st->item_ptrs[i] - st->host_base};
+    W w;
+    w.pod(kBlobMagic);
+    w.str(k);
+    w.pod(st->version);
+    w.pod(static_cast<std::uint8_t>(st->serving));
+    w.pod(static_cast<std::uint8_t>(st->complete));
+    w.pod(st->progress);
+    w.pod(st->epoch);
+    w.pod(st->device);
+    w.pod(static_cast<std::int32_t>(getpid()));
+    w.vec(st->item_ends);
+    w.vec(st->cmap.chunk0);
+    w.vec(st->cmap.chunk_len);
+    w.vec(st->cmap.count);
+    w.vec(std::vector<ServeState::Alloc>{});
+    w.vec(item_loc);
+    w.pod(std::pair<std::uint32_t, std::uint64_t>{0, st->digests - st->host_base});
+    w.pod(std::pair<std::uint32_t, std::uint64_t>{0, 0});
+    w.str(st->host_name);
+    w.pod(st->host_size);
+    return w.s;
+  }
   auto range = get_range_fn();
   if (!range) return Status::transfer_failed;
   DeviceGuard g(st->device);
@@ -333,6 +439,8 @@ Result<std::string> ServeRegistry::export_state(const std::string& k) {
   w.vec(item_loc);
   w.pod(dl);
   w.pod(fl);
+  w.str(std::string());
+  w.pod(std::uint64_t{0});
   return w.s;
 }
 
@@ -355,6 +463,8 @@ Status ServeRegistry::import_state(const std::string& blob) {
   auto item_loc = r.vec<std::pair<std::uint32_t, std::uint64_t>>();
   auto dl = r.pod<std::pair<std::uint32_t, std::uint64_t>>();
   auto fl = r.pod<std::pair<std::uint32_t, std::uint64_t>>();
+  std::string host_name = r.str();
+  auto host_size = r.pod<std::uint64_t>();
   if (!r.ok) return Status::protocol_error;
   if (pid == getpid()) return Status::ok;  // our own state: nothing to import
   auto st = ensure(k);
@@ -372,6 +482,9 @@ Status ServeRegistry::import_state(const std::string& blob) {
   st->cmap.chunk_len = std::move(cl);
   st->cmap.count = std::move(cc);
   retarget_ipc(st->imported ? st->allocs : std::vector<ServeState::Alloc>{}, allocs);
+  retarget_host(st->imported ? st->host_name : std::string(), host_name);
+  st->host_name = std::move(host_name);
+  st->host_size = host_size;
   st->allocs = std::move(allocs);
   st->item_loc = std::move(item_loc);
   st->digests_loc = dl;
@@ -416,10 +529,20 @@ Status map_source(const std::shared_ptr<ServeState>& st, int reader_device, Sour
   out->epoch = st->epoch;
   out->total = st->item_ends.empty() ? 0 : st->item_ends.back();
   if (!st->imported) {
-    if (Status s = enable_peer(reader_device, st->device); !ok(s)) return s;
+    if (st->device >= 0)  // a host lane (device < 0) needs no peer mapping
+      if (Status s = enable_peer(reader_device, st->device); !ok(s)) return s;
     out->item_ptrs = st->item_ptrs;
     out->digests = st->digests;
     out->flags = st->flags;
+    return Status::ok;
+  }
+  if (!st->host_name.empty()) {  // another process's retention offload
+    auto b = open_host(st->host_name, st->host_size);
+    if (!b) return b.status();
+    out->item_ptrs.resize(st->item_loc.size());
+    for (std::size_t i = 0; i < st->item_loc.size(); ++i) out->item_ptrs[i] = *b + st->item_loc[i].second;
+    out->digests = *b + st->digests_loc.second;
+    out->flags = 0;
     return Status::ok;
   }
   std::vector<std::uint64_t> bases(st->allocs.size());
@@ -581,6 +704,7 @@ Status Client::open() {
   std::vector<std::string> dman, dlay;
   if (Status s = derived_blobs(&dman, &dlay); !ok(s)) return s;
   Status s = reg_->open(model_, replica_, num_shards_, cfg_.dc, eps, layout_key(), dman, dlay);
+  if (ok(s) && !retain_.empty()) s = reg_->set_retention(model_, replica_, retain_);
   if (ok(s)) opened_ = true;
   return s;
 }
@@ -784,9 +908,11 @@ Status Client::publish(VersionId v) {
 
 Status Client::unpublish() {
   if (!opened_) return Status::invalid_state;
+  apply_releases();
   OpOutcome o;
   Status s = reg_->unpublish(model_, replica_, &o);
   if (!ok(s)) return s;
+  if (Status so = settle_offload(&o, 600.0); !ok(so)) return so;
   if (!o.done) o = reg_->wait_op(model_, replica_, 600.0);
   if (!o.done) return Status::timeout;
   if (ok(o.status)) {
@@ -1461,6 +1587,7 @@ Status Client::replicate(const VersionSpec& spec, VersionId* out, double wait_s)
   if (!opened_) {
     if (Status s = open(); !ok(s)) return s;
   }
+  apply_releases();
   OpOutcome o;
   Status s = reg_->replicate(model_, replica_, spec, &o);
   if (!ok(s)) return s;
@@ -1476,9 +1603,11 @@ Status Client::update(const VersionSpec& spec, bool* changed, VersionId* out, do
   if (!opened_) {
     if (Status s = open(); !ok(s)) return s;
   }
+  apply_releases();
   OpOutcome o;
   Status s = reg_->update(model_, replica_, spec, current_, &o);
   if (!ok(s)) return s;
+  if (Status so = settle_offload(&o, wait_s); !ok(so)) return so;
   if (!o.done) o = reg_->wait_op(model_, replica_, wait_s);
   if (!o.done) return Status::timeout;
   if (!ok(o.status)) return o.status;
@@ -1519,6 +1648,139 @@ Status Client::chunk_digests(std::uint32_t shard, std::vector<std::uint64_t>* ou
   out->reserve(cm.n_real());
   for (std::size_t i = 0; i < cm.count.size(); ++i)
     out->insert(out->end(), raw.begin() + cm.chunk0[i], raw.begin() + cm.chunk0[i] + cm.count[i]);
+  return Status::ok;
+}
+
+// ---- retention offload lanes ---------------------------------------------
+
+Status Client::make_retention_lane(Shard& sh, VersionId v, std::string* endpoint) {
+  auto it = sh.lanes.find(v);
+  if (it != sh.lanes.end()) {  // re-confirm is idempotent
+    *endpoint = it->second.endpoint;
+    return Status::ok;
+  }
+  if (!sh.holding || !current_ || *current_ != v) return Status::invalid_state;
+  const Payload& p = *sh.holding;
+  const auto& items = p.manifest.items();
+  // [items, 256-byte aligned][chunk-digest table]
+  std::vector<std::uint64_t> off(items.size());
+  std::uint64_t tot = 0, bytes = 0;
+  for (std::size_t i = 0; i < items.size(); ++i) {
+    off[i] = tot;
+    tot += (items[i].length + 255) / 256 * 256;
+    bytes += items[i].length;
+  }
+  const std::uint64_t dig_off = tot;
+  tot += std::uint64_t(p.cmap.n_chunks()) * 8;
+  std::unique_ptr<HostBuf> buf;
+  for (auto it = host_pool_.begin(); it != host_pool_.end(); ++it)
+    if ((*it)->n >= tot) {
+      buf = std::move(*it);
+      host_pool_.erase(it);
+      break;
+    }
+  if (!buf) {
+    buf = std::make_unique<HostBuf>();
+    if (Status s = buf->alloc(tot); !ok(s)) return s;
+  }
+  auto* base = static_cast<std::uint8_t*>(buf->p);
+  {
+    DeviceGuard g(sh.device);
+    for (std::size_t i = 0; i < items.size(); ++i)
+      RS_CUDA(cudaMemcpyAsync(base + off[i], reinterpret_cast<const void*>(p.item_ptrs[i]),
+                              items[i].length, cudaMemcpyDeviceToHost, sh.stream));
+    if (p.cmap.n_chunks())
+      RS_CUDA(cudaMemcpyAsync(base + dig_off, p.digests.p, std::size_t(p.cmap.n_chunks()) * 8,
+                              cudaMemcpyDeviceToHost, sh.stream));
+    RS_CUDA(cudaStreamSynchronize(sh.stream));
+  }
+  stats_.bytes_copied_local += bytes;
+  Shard::Lane lane;
+  lane.key = ServeRegistry::key(model_, replica_ + "+offload@" + std::to_string(v), sh.idx);
+  lane.endpoint = "host:" + replica_ + ":" + std::to_string(sh.idx);
+  lane.serve = serves_->ensure(lane.key);
+  {
+    std::vector<std::uint64_t> ends, ptrs;
+    for (std::size_t i = 0; i < items.size(); ++i) {
+      ends.push_back(items[i].stream_offset + items[i].length);
+      ptrs.push_back(reinterpret_cast<std::uint64_t>(base + off[i]));
+    }
+    std::lock_guard lk(lane.serve->m);
+    lane.serve->serving = true;
+    lane.serve->imported = false;
+    lane.serve->version = v;
+    lane.serve->complete = true;
+    lane.serve->progress = items.size();
+    lane.serve->device = -1;
+    lane.serve->pid = static_cast<int>(getpid());
+    lane.serve->item_ends = std::move(ends);
+    lane.serve->item_ptrs = std::move(ptrs);
+    lane.serve->cmap = p.cmap;
+    lane.serve->digests = reinterpret_cast<std::uint64_t>(base + dig_off);
+    lane.serve->flags = 0;
+    lane.serve->epoch = 1;
+    lane.serve->host_name = buf->name;
+    lane.serve->host_size = buf->n;
+    lane.serve->host_base = reinterpret_cast<std::uint64_t>(base);
+  }
+  lane.buf = std::move(buf);
+  *endpoint = lane.endpoint;
+  sh.lanes.emplace(v, std::move(lane));
+  return Status::ok;
+}
+
+Status Client::make_retention_lanes(VersionId v, std::vector<std::string>* endpoints) {
+  endpoints->assign(num_shards_, "");
+  for (auto& sh : shards_) {
+    if (sh.device < 0) continue;
+    if (Status s = make_retention_lane(sh, v, &(*endpoints)[sh.idx]); !ok(s)) return s;
+  }
+  return Status::ok;
+}
+
+Result<std::string> Client::export_lane(std::uint32_t shard, VersionId v) {
+  if (shard >= num_shards_) return Status::invalid_argument;
+  auto it = shards_[shard].lanes.find(v);
+  if (it == shards_[shard].lanes.end()) return Status::not_found;
+  return serves_->export_state(it->second.key);
+}
+
+void Client::release_lane(VersionId v) {
+  for (auto& sh : shards_) {
+    auto it = sh.lanes.find(v);
+    if (it == sh.lanes.end()) continue;
+    {
+      std::lock_guard lk(it->second.serve->m);
+      it->second.serve->serving = false;
+    }
+    serves_->erase(it->second.key);
+    if (host_pool_.size() < 2) host_pool_.push_back(std::move(it->second.buf));
+    sh.lanes.erase(it);  // a buffer not pooled is unregistered and unlinked
+  }
+}
+
+void Client::apply_releases() {
+  for (const auto& r : reg_->take_releases(model_, replica_)) release_lane(r.version);
+}
+
+std::vector<VersionId> Client::lanes() const {
+  std::set<VersionId> vs;
+  for (const auto& sh : shards_)
+    for (const auto& [v, lane] : sh.lanes) vs.insert(v);
+  return {vs.begin(), vs.end()};
+}
+
+Status Client::settle_offload(OpOutcome* o, double wait_s) {
+  // ResponseKind::offload_first (client_core.cpp:1237-1253): park the named
+  // version in host memory, confirm every shard, then the op proceeds.
+  if (o->done || !o->offload_first) return Status::ok;
+  const VersionId v = *o->offload_first;
+  std::vector<std::string> eps;
+  const bool ok_lane = ok(make_retention_lanes(v, &eps));
+  for (std::uint32_t i = 0; i < num_shards_; ++i)
+    if (Status s = reg_->offload_confirm(model_, replica_, i, v, ok_lane, eps[i]); !ok(s)) return s;
+  *o = reg_->op_result(model_, replica_);
+  if (!o->done) *o = reg_->wait_op(model_, replica_, wait_s);
   return Status::ok;
 }
 

@@ -110,6 +110,24 @@ struct ServeState {
   std::vector<Alloc> allocs;
   std::vector<std::pair<std::uint32_t, std::uint64_t>> item_loc;  // (alloc, offset)
   std::pair<std::uint32_t, std::uint64_t> digests_loc{0, 0}, flags_loc{0, 0};
+  // A retention offload in pinned host memory (device < 0): a POSIX shared
+  // memory segment registered with CUDA, so other processes map it by name.
+  std::string host_name;
+  std::uint64_t host_size = 0;
+  std::uint64_t host_base = 0;  // owner's mapping (offsets in the blob are from here)
+};
+
+// Owned pinned host buffer backed by POSIX shared memory (mapped into the
+// device address space with cudaHostRegister).
+struct HostBuf {
+  std::string name;
+  void* p = nullptr;
+  std::size_t n = 0;
+  HostBuf() = default;
+  HostBuf(const HostBuf&) = delete;
+  HostBuf& operator=(const HostBuf&) = delete;
+  ~HostBuf();
+  Status alloc(std::size_t bytes);
 };
 
 // (model, replica, shard) -> serve state, process-wide (transport.hpp:72-85).
@@ -172,6 +190,10 @@ class Client {
   // or publishes; layout key "!" + its slicing).
   Status register_tensor(std::uint32_t shard, const std::string& name, void* ptr,
                          std::uint64_t len, const Geometry& geo = {}, bool cast = false);
+  // RetentionRule: versions at these lags behind the newest stay reachable
+  // (sent with open; the split phase sends it as its own registry op).
+  void set_retention(std::set<std::uint64_t> lags) { retain_ = std::move(lags); }
+  const std::set<std::uint64_t>& retention() const { return retain_; }
   void set_shard_endpoint(std::uint32_t shard, std::string ep);
   // Slicing key of the replica ("" when no region carries a geometry;
   // "!" prefix when some region lands as a cast).  combine_layout_key of
@@ -249,6 +271,16 @@ class Client {
   Result<std::string> manifest_bytes(std::uint32_t shard) const;
   Status chunk_digests(std::uint32_t shard, std::vector<std::uint64_t>* out);
   Result<std::string> export_serve(std::uint32_t shard);
+
+  // --- retention offload lanes (client_core.cpp:1675-1717) ------------------
+  // Park version v of every local shard in pinned host memory and serve it as
+  // replica "<replica>+offload@<v>"; the endpoints go to offload_confirm.
+  Status make_retention_lanes(VersionId v, std::vector<std::string>* endpoints);
+  Result<std::string> export_lane(std::uint32_t shard, VersionId v);
+  void release_lane(VersionId v);
+  // Free the lanes the registry released (DirectiveKind::offload_release).
+  void apply_releases();
+  std::vector<VersionId> lanes() const;
   std::string endpoint(std::uint32_t shard) const { return shards_[shard].endpoint; }
 
  private:
@@ -298,7 +330,16 @@ class Client {
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     cudaStream_t poll = nullptr;  // progress reads while a fill runs
     std::uint32_t epoch_ctr = 0;
+    struct Lane {
+      std::string key;
+      std::shared_ptr<ServeState> serve;
+      std::unique_ptr<HostBuf> buf;
+      std::string endpoint;
+    };
+    std::map<VersionId, Lane> lanes;  // retention offloads held for the registry
   };
+  Status make_retention_lane(Shard& sh, VersionId v, std::string* endpoint);
+  Status settle_offload(OpOutcome* o, double wait_s);
 
   Status ensure_stream(Shard& sh);
   Status build_payload(Shard& sh, VersionId v, std::shared_ptr<Payload>* out);
@@ -327,6 +368,10 @@ class Client {
   ClientConfig cfg_;
   std::vector<Shard> shards_;
   std::optional<VersionId> current_;
+  std::set<std::uint64_t> retain_;
+  // Released lanes' pinned host buffers, reused by the next offload: pinning
+  // fresh host memory runs at ~2 GB/s, a D2H copy into pinned memory at ~50.
+  std::vector<std::unique_ptr<HostBuf>> host_pool_;
   std::vector<FillOutcome> launch_out_;  // launch_shards -> wait_shards
   std::vector<bool> launched_;
   bool published_ = false;

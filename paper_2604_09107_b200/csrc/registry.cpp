@@ -109,7 +109,19 @@ Status Registry::close(const std::string& model, const std::string& replica) {
   if (busy) fail_replica(*r, "closed");
   if (r->txn) finish_op(*r, Status::closed);
   auto& m = ms(model);
-  if (r->serving == 0) {
+  // owned offload buffers die with their owner (server_core.cpp:1715-1733)
+  std::vector<std::string> owned;
+  for (const auto& [name, o] : m.reps)
+    if (o->kind == Kind::offload && o->owner == replica) owned.push_back(name);
+  for (const auto& name : owned) {
+    auto it = m.reps.find(name);
+    const VersionId v = *it->second->version;
+    trace("offload_dropped", {{"model", model}, {"replica", name}, {"reason", "owner_closed"}});
+    m.reps.erase(it);
+    prune_version(m, v);
+  }
+  r = find(model, replica);
+  if (r && r->serving == 0) {
     m.reps.erase(replica);
   }
   cv_.notify_all();
@@ -262,6 +274,7 @@ Status Registry::publish(const std::string& model, const std::string& replica,
   for (std::uint32_t s = 0; s < r->num_shards; ++s) r->shards[s] = {items[s], true};
   if (!m.max_published || v > *m.max_published) m.max_published = v;
   trace("publish_commit", {{"model", model}, {"replica", replica}, {"v", n2s(v)}});
+  eval_offload_releases(model);
   r->last = {true, Status::ok, v, false, {}};
   if (out) *out = r->last;
   wake_blocked(model);
@@ -307,9 +320,12 @@ Status Registry::unpublish(const std::string& model, const std::string& replica,
   r->visible = false;  // no new readers from here on
   r->txn = t;
   r->last = {};
+  auto& m = ms(model);
+  const bool offload = needs_offload(m, *r, *r->version);
   trace("unpublish_start", {{"model", model}, {"replica", replica},
-                            {"v", n2s(*r->version)}, {"offload_first", "0"},
+                            {"v", n2s(*r->version)}, {"offload_first", offload ? "1" : "0"},
                             {"serving", n2s(r->serving)}});
+  if (offload) request_offload(*r, *r->txn, *r->version);
   try_settle(*r);
   if (out) *out = r->last;
   cv_.notify_all();
@@ -414,10 +430,12 @@ void Registry::start_update(Rep& r) {
   src->last_assigned = ++tick_;
   t.was_visible = r.visible;
   if (r.life == Life::published && r.version) r.visible = false;
+  const bool offload = r.life == Life::published && r.version && needs_offload(m, r, *r.version);
   trace("update_change", {{"model", r.model}, {"replica", r.name},
                           {"from", current ? n2s(*current) : "none"},
                           {"to", n2s(*target)}, {"src", src->name},
-                          {"offload_first", "0"}, {"serving", n2s(r.serving)}});
+                          {"offload_first", offload ? "1" : "0"}, {"serving", n2s(r.serving)}});
+  if (offload) request_offload(r, t, *r.version);
   try_settle(r);
 }
 
@@ -427,6 +445,7 @@ void Registry::try_settle(Rep& r) {
   if (!r.txn) return;
   Txn& t = *r.txn;
   if (!t.resolved || t.settled || t.blocked) return;
+  if (t.offload_needed && !t.offload_done) return;  // the client parks the version first
   bool needs_drain =
       t.kind == OpKind::unpublish || (t.kind == OpKind::update && t.changed);
   if (needs_drain && r.serving > 0) return;  // wait for readers to finish
@@ -469,6 +488,7 @@ void Registry::apply_settle(Rep& r) {
       prune_version(m, v);
       r.last = {true, Status::ok, std::nullopt, false, {}};
       r.txn.reset();
+      eval_offload_releases(r.model);
       return;
     }
     case OpKind::replicate:
@@ -602,6 +622,7 @@ void Registry::finish_replication(Rep& r) {
   trace("replica_complete", {{"model", r.model}, {"replica", r.name},
                              {"v", n2s(*r.version)}, {"seeded", was_seeding ? "1" : "0"}});
   wake_blocked(r.model);
+  eval_offload_releases(r.model);
 }
 
 void Registry::release_source(Rep& r) {
@@ -615,6 +636,7 @@ void Registry::release_source(Rep& r) {
 
 void Registry::check_drain(Rep& src) {
   if (src.serving > 0) return;
+  if (src.kind == Kind::offload && src.releasing) return finish_offload_release(src);
   try_settle(src);
   if (src.life == Life::failed && !src.txn) {
     // nothing else to do; failed records linger until re-opened
@@ -651,6 +673,168 @@ void Registry::prune_version(ModelState& m, VersionId v) {
   for (const auto& [name, r] : m.reps)
     if (r->life != Life::failed && r->version == v) return;
   m.versions.erase(v);
+}
+
+// --------------------------------------------------------------- retention
+
+Status Registry::set_retention(const std::string& model, const std::string& replica,
+                               const std::set<std::uint64_t>& lags) {
+  std::lock_guard lk(mu_);
+  Rep* r = find(model, replica);
+  if (!r || r->kind != Kind::worker) return Status::not_found;
+  r->retain = lags;
+  return Status::ok;
+}
+
+std::set<VersionId> Registry::retained_versions(ModelState& m) {
+  std::set<VersionId> out;
+  if (!m.max_published) return out;
+  const VersionId max = *m.max_published;
+  for (const auto& [name, r] : m.reps)
+    for (auto lag : r->retain)
+      if (lag <= max) out.insert(max - lag);
+  return out;
+}
+
+bool Registry::needs_offload(ModelState& m, const Rep& r, VersionId v) {
+  if (r.kind != Kind::worker || !retained_versions(m).count(v)) return false;
+  for (const auto& [name, other] : m.reps) {
+    if (other.get() == &r) continue;
+    if (other->visible && other->life == Life::published && other->version == v &&
+        other->complete_all())
+      return false;  // another durable copy exists
+  }
+  return true;
+}
+
+void Registry::request_offload(Rep& r, Txn& t, VersionId v) {
+  t.offload_needed = true;
+  t.offload_v = v;
+  t.offload_endpoints.assign(r.num_shards, "");
+  trace("offload_first", {{"model", r.model}, {"replica", r.name}, {"v", n2s(v)}});
+  r.last.done = false;
+  r.last.offload_first = v;
+}
+
+Status Registry::offload_confirm(const std::string& model, const std::string& replica,
+                                 std::uint32_t shard, VersionId version, bool ok,
+                                 const std::string& endpoint) {
+  std::lock_guard lk(mu_);
+  Rep* r = find(model, replica);
+  if (!r) return Status::not_found;
+  if (!r->txn || !r->txn->offload_needed || r->txn->offload_v != version ||
+      shard >= r->num_shards)
+    return Status::invalid_state;
+  Txn& t = *r->txn;
+  if (t.offload_done) return Status::ok;
+  if (!ok) {
+    // Host memory unavailable: the op fails, the replica stays published and
+    // visible; nothing was given up (server_core.cpp:1404-1421).
+    trace("offload_failed", {{"model", model}, {"replica", replica}, {"v", n2s(version)}});
+    if (t.was_visible && r->life == Life::published) r->visible = true;
+    if (!t.source.empty()) {
+      Rep* s = find(model, t.source);
+      if (s && s->serving > 0) {
+        s->serving--;
+        check_drain(*s);
+      }
+    }
+    finish_op(*r, Status::offload_failed);
+    cv_.notify_all();
+    return Status::ok;
+  }
+  t.offload_confirmed.insert(shard);
+  t.offload_endpoints[shard] = endpoint;
+  trace("offload_confirmed", {{"model", model}, {"replica", replica}, {"shard", n2s(shard)},
+                              {"v", n2s(version)}});
+  if (t.offload_confirmed.size() == r->num_shards) {
+    t.offload_done = true;
+    r->last.offload_first.reset();
+    create_offload_replica(*r, version, t.offload_endpoints);
+    try_settle(*r);
+  }
+  cv_.notify_all();
+  return Status::ok;
+}
+
+void Registry::create_offload_replica(Rep& owner, VersionId v,
+                                      const std::vector<std::string>& endpoints) {
+  auto& m = ms(owner.model);
+  const std::string name = owner.name + "+offload@" + n2s(v);
+  auto it = m.reps.find(name);
+  if (it != m.reps.end()) {
+    // mid-drain toward release when it became needed again: keep it
+    Rep& old = *it->second;
+    old.releasing = false;
+    old.visible = true;
+    old.endpoints = endpoints;
+    trace("offload_reused", {{"model", owner.model}, {"replica", name}});
+    wake_blocked(owner.model);
+    return;
+  }
+  auto rec = std::make_unique<Rep>();
+  rec->kind = Kind::offload;
+  rec->owner = owner.name;
+  rec->model = owner.model;
+  rec->name = name;
+  rec->dc = owner.dc;
+  rec->layout = owner.layout;
+  rec->num_shards = owner.num_shards;
+  rec->endpoints = endpoints;
+  rec->life = Life::published;
+  rec->visible = true;
+  rec->version = v;
+  rec->shards.assign(owner.num_shards, ShardState{0, true});
+  m.reps.emplace(name, std::move(rec));
+  trace("offload_replica", {{"model", owner.model}, {"replica", name}, {"v", n2s(v)},
+                            {"purpose", "retention"}});
+  wake_blocked(owner.model);
+}
+
+void Registry::eval_offload_releases(const std::string& model) {
+  auto& m = ms(model);
+  const auto retained = retained_versions(m);
+  std::vector<Rep*> drop;
+  for (auto& [name, r] : m.reps) {
+    if (r->kind != Kind::offload || r->releasing || r->life != Life::published) continue;
+    const VersionId v = *r->version;
+    bool replaced = false;
+    for (const auto& [oname, other] : m.reps)
+      if (other->kind == Kind::worker && other->visible && other->life == Life::published &&
+          other->version == v && other->complete_all())
+        replaced = true;
+    if (replaced || !retained.count(v)) drop.push_back(r.get());
+  }
+  for (Rep* r : drop) release_offload(*r);
+}
+
+void Registry::release_offload(Rep& off) {
+  if (off.releasing) return;
+  off.releasing = true;
+  off.visible = false;
+  trace("offload_release_start", {{"model", off.model}, {"replica", off.name},
+                                  {"v", off.version ? n2s(*off.version) : "none"},
+                                  {"serving", n2s(off.serving)}});
+  if (off.serving == 0) finish_offload_release(off);
+}
+
+void Registry::finish_offload_release(Rep& off) {
+  const std::string model = off.model, name = off.name;
+  releases_[model].push_back({off.owner, *off.version});
+  trace("offload_released", {{"model", model}, {"replica", name}});
+  auto& m = ms(model);
+  const VersionId v = *off.version;
+  m.reps.erase(name);
+  prune_version(m, v);
+}
+
+std::vector<OffloadRelease> Registry::take_releases(const std::string& model,
+                                                    const std::string& owner) {
+  std::lock_guard lk(mu_);
+  std::vector<OffloadRelease> out, keep;
+  for (auto& d : releases_[model]) (d.owner == owner ? out : keep).push_back(d);
+  releases_[model] = std::move(keep);
+  return out;
 }
 
 Result<Assignment> Registry::failure_report(const std::string& model,
@@ -774,6 +958,7 @@ std::optional<ReplicaView> Registry::view(const std::string& model,
   Rep* r = find(model, replica);
   if (!r) return std::nullopt;
   ReplicaView v;
+  v.kind = r->kind == Kind::offload ? "offload" : "worker";
   v.lifecycle = life_name(r->life);
   v.version = r->version;
   v.serving = r->serving;

@@ -19,7 +19,10 @@
 //    with op_result(); with several threads it may block in wait_op().  The
 //    same call sequence applied on every rank (replicated state machine,
 //    paper_2604_09107_b200/ros.py Cluster) yields the same plan everywhere.
-//  * Offload / seed / retention lanes are not modelled.
+//  * Retention offloads follow the reference (unpublish_needs_offload
+//    1606-1618, on_offload_confirm 1387-1437, create_offload_replica
+//    1439-1485, eval_offload_releases 1620-1645); cross-DC seed lanes are not
+//    modelled (one box, one datacenter).
 //  * pick_source's key gains a topology cost between dc and serving; on a
 //    uniform NVSwitch box every cost is equal and the order is exactly the
 //    reference's (own_seed, same_dc, serving, last_assigned, name).
@@ -72,9 +75,20 @@ struct OpOutcome {
   std::optional<VersionId> version;
   bool changed = false;                 // update
   std::vector<Assignment> assignments;  // replicate/update(change): per shard
+  // Set while an unpublish/update waits for the client to park this version
+  // in host memory first (ResponseKind::offload_first, server_core.cpp:428-440):
+  // the client answers with offload_confirm for every shard.
+  std::optional<VersionId> offload_first;
+};
+
+// A retention offload the owner may now free (DirectiveKind::offload_release).
+struct OffloadRelease {
+  std::string owner;
+  VersionId version = 0;
 };
 
 struct ReplicaView {
+  std::string kind = "worker";  // worker|offload
   std::string lifecycle;  // registered|replicating|published|failed
   std::optional<VersionId> version;
   std::uint32_t serving = 0;
@@ -120,6 +134,18 @@ class Registry {
               const std::vector<std::string>& derived_manifests = {},
               const std::vector<std::string>& derived_layouts = {});
   Status close(const std::string& model, const std::string& replica);
+  // RetentionRule (types.hpp:119-123): versions at these lags behind the
+  // newest published one stay reachable -- the last durable copy of such a
+  // version is parked in host memory (an offload replica) before it goes.
+  Status set_retention(const std::string& model, const std::string& replica,
+                       const std::set<std::uint64_t>& lags);
+  // OffloadConfirmMsg (server_core.cpp:1387-1437): the shard parked
+  // `version` in host memory (ok) and serves it at `endpoint`.
+  Status offload_confirm(const std::string& model, const std::string& replica,
+                         std::uint32_t shard, VersionId version, bool ok,
+                         const std::string& endpoint);
+  // Offload buffers of `owner` the registry no longer needs (drained).
+  std::vector<OffloadRelease> take_releases(const std::string& model, const std::string& owner);
 
   // Each returns the immediate status; if ok and the op is parked,
   // *pending = true and the outcome arrives through op_result().
@@ -175,6 +201,7 @@ class Registry {
 
  private:
   enum class Life { registered, replicating, published, failed };
+  enum class Kind { worker, offload };
   struct Txn {
     OpKind kind = OpKind::none;
     std::uint64_t order = 0;
@@ -184,12 +211,21 @@ class Registry {
     bool was_visible = false;
     std::optional<VersionId> target;
     std::string source;
+    // retention offload of the held version before the op settles
+    bool offload_needed = false, offload_done = false;
+    VersionId offload_v = 0;
+    std::set<std::uint32_t> offload_confirmed;
+    std::vector<std::string> offload_endpoints;
   };
   struct ShardState {
     std::uint64_t progress = 0;
     bool complete = false;
   };
   struct Rep {
+    Kind kind = Kind::worker;
+    std::string owner;        // offload: the worker whose buffer this is
+    bool releasing = false;   // offload: released, draining its readers
+    std::set<std::uint64_t> retain;  // retention lags requested by this replica
     std::string model, name, dc;
     std::string layout;  // slicing key ("" plain)
     std::vector<std::string> derived_manifests, derived_layouts;  // reshard readers
@@ -250,7 +286,15 @@ class Registry {
   void void_replication(Rep& r, const std::string& reason);
   void fail_replica(Rep& r, const std::string& reason);
   void prune_version(ModelState& m, VersionId v);
+  std::set<VersionId> retained_versions(ModelState& m);
+  bool needs_offload(ModelState& m, const Rep& r, VersionId v);
+  void request_offload(Rep& r, Txn& t, VersionId v);
+  void create_offload_replica(Rep& owner, VersionId v, const std::vector<std::string>& endpoints);
+  void eval_offload_releases(const std::string& model);
+  void release_offload(Rep& off);
+  void finish_offload_release(Rep& off);
 
+  std::map<std::string, std::vector<OffloadRelease>> releases_;  // model -> pending directives
   Config cfg_;
   TopoFn topo_;
   std::mutex mu_;

@@ -113,6 +113,13 @@ class DistCluster:
             return lib.rs_server_add_layout(c, _b(m), v, _b(key), len(mans), pm, pl, qm, ql)
         if kind == "unpublish":
             return lib.rs_server_unpublish(c, _b(o[1]), _b(o[2]))
+        if kind == "retain":
+            _, m, r, lags = o
+            arr = (C.c_uint64 * max(len(lags), 1))(*lags)
+            return lib.rs_server_set_retention(c, _b(m), _b(r), C.cast(arr, C.c_void_p), len(lags))
+        if kind == "offload_confirm":
+            _, m, r, shard, v, ok, ep = o
+            return lib.rs_server_offload_confirm(c, _b(m), _b(r), shard, v, int(ok), _b(ep))
         if kind == "replicate":
             return lib.rs_server_replicate(c, _b(o[1]), _b(o[2]), _b(o[3]))
         if kind == "update":
@@ -168,7 +175,8 @@ class DistCluster:
             geo = any(x[1] for x in hashes.values())
             derived = {sh: (h.derived(sh, 0), h.derived(sh, 1)) for sh in loc} if geo else {}
             mine = {"model": h.model, "replica": h.replica, "n": h.num_shards, "dc": datacenter,
-                    "eps": eps, "hashes": hashes, "derived": derived}
+                    "eps": eps, "hashes": hashes, "derived": derived,
+                    "retain": list(getattr(h, "retain", []))}
         for (m, r), parts in self._merge(self.gather(mine)).items():
             n = parts[0]["n"]
             eps, hashes, derived = {}, {}, {}
@@ -184,6 +192,9 @@ class DistCluster:
             rc = self._apply(("open", m, r, n, parts[0]["dc"], [eps[i] for i in range(n)], key,
                               dman, dlay))
             assert rc == 0, (m, r, rc)
+            retain = sorted({x for p in parts for x in p.get("retain", [])})
+            if retain:
+                assert self._apply(("retain", m, r, retain)) == 0
 
     def publish(self, h: Optional[Handle], version: int) -> Optional[OpResult]:
         mine = None
@@ -214,9 +225,33 @@ class DistCluster:
         st = Status(rcs[(h.model, h.replica)])
         return OpResult(st, version if st == Status.ok else None)
 
+    def _offload_first(self, h: Optional[Handle]) -> None:
+        """Collective: replicas whose unpublish/update waits for a retention
+        offload park the version in host memory (their ranks' local shards),
+        confirm every shard, and every rank imports the offload lanes."""
+        mine = None
+        if h is not None:
+            v = C.c_uint64()
+            if lib.rs_server_offload_pending(self.local.h, _b(h.model), _b(h.replica), C.byref(v)):
+                ok = lib.rs_offload_lanes(h.h, v.value) == 0
+                loc = h.local_shards()
+                blobs = [_read_bytes(lib.rs_lane_export, h.h, s, v.value) for s in loc] if ok else []
+                mine = {"model": h.model, "replica": h.replica, "v": v.value, "ok": ok,
+                        "eps": {s: f"host:{h.replica}:{s}" for s in loc}, "blobs": blobs}
+        parts = self.gather(mine)
+        if not any(parts):
+            return
+        for p in parts:
+            if p is None:
+                continue
+            for s, ep in p["eps"].items():
+                self._apply(("offload_confirm", p["model"], p["replica"], s, p["v"], p["ok"], ep))
+        self._import_all([p["blobs"] if p else None for p in parts])
+
     def unpublish(self, h: Optional[Handle]) -> Optional[OpResult]:
         mine = {"model": h.model, "replica": h.replica} if h is not None else None
         rcs = {k: self._apply(("unpublish",) + k) for k in self._merge(self.gather(mine))}
+        self._offload_first(h)
         if h is None:
             return None
         done, s, _, _ = self.result(h.model, h.replica)
@@ -247,6 +282,7 @@ class DistCluster:
             p = parts[0]
             self._apply(("update", m, r, p["spec"], p["cur"]) if p["update"] else
                         ("replicate", m, r, p["spec"]))
+        self._offload_first(h)
         txn = {"active": False, "result": None, "version": None, "changed": False,
                "loc": h.local_shards() if h is not None else [], "launched": False}
         if h is not None:

@@ -201,8 +201,17 @@ class Cluster:
         if rc == Status.not_found:
             return None
         check(rc)
-        return {"lifecycle": life.value.decode(), "version": v.value, "serving": s.value,
-                "visible": bool(vis.value)}
+        kind = _read_bytes(lib.rs_cluster_kind, self.h, _b(model), _b(replica)).decode()
+        return {"kind": kind, "lifecycle": life.value.decode(), "version": v.value,
+                "serving": s.value, "visible": bool(vis.value)}
+
+    def releases(self, model: str, owner: str) -> list[int]:
+        """Retention offloads of `owner` the registry released (taken)."""
+        n = C.c_size_t(0)
+        buf = (C.c_uint64 * 64)()
+        check(lib.rs_server_take_releases(self.h, _b(model), _b(owner), C.cast(buf, C.c_void_p), 64,
+                                          C.byref(n)))
+        return [int(buf[i]) for i in range(min(n.value, 64))]
 
     def locate(self, model: str, replica: str, spec: str = "latest", shard: int = 0) -> dict:
         a = RsAssignment()
@@ -231,6 +240,7 @@ class Handle:
         self.replica = replica
         self.num_shards = num_shards
         self._keep = []
+        self.retain = []
 
     # ---- setup ------------------------------------------------------------
     def register_tensor(self, shard: int, name: str, tensor=None, *, ptr: int = 0,
@@ -266,6 +276,28 @@ class Handle:
         rows, w, r0, nr, c0, nc = (int(x) for x in (geometry or (0, 0, 0, 0, 0, 0)))
         return Status(lib.rs_register_cast(self.h, shard, _b(name), C.c_void_p(tensor.data_ptr()),
                                            nbytes, rows, w, r0, nr, c0, nc))
+
+    def set_retention(self, lags) -> None:
+        """RetentionRule: keep the versions at these lags behind the newest
+        published one reachable (call before the first op)."""
+        arr = (C.c_uint64 * max(len(lags), 1))(*[int(x) for x in lags])
+        check(lib.rs_set_retention(self.h, C.cast(arr, C.c_void_p), len(lags)))
+        self.retain = sorted(int(x) for x in lags)
+
+    def connect(self) -> Status:
+        """ClientCore::open: join the cluster without an operation."""
+        return Status(lib.rs_connect(self.h))
+
+    def lanes(self) -> list[int]:
+        """Versions this handle holds as retention offloads in host memory."""
+        n = C.c_size_t(0)
+        buf = (C.c_uint64 * 64)()
+        check(lib.rs_lanes(self.h, C.cast(buf, C.c_void_p), 64, C.byref(n)))
+        return [int(buf[i]) for i in range(min(n.value, 64))]
+
+    def poll(self) -> None:
+        """Free the retention offloads the registry released."""
+        check(lib.rs_poll(self.h))
 
     def local_shards(self) -> list[int]:
         """Shards whose regions this process registered (a replica may span
