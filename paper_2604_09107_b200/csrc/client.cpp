@@ -589,14 +589,18 @@ Client::~Client() {
 
 Status Client::register_tensor(std::uint32_t shard, const std::string& name, void* ptr,
                                std::uint64_t len, const Geometry& geo, bool cast) {
-  if (shard >= num_shards_ || name.empty() || !ptr || len == 0) return Status::invalid_argument;
+  // validation order of ClientCore::register_tensor (client_core.cpp:534-553)
+  if (closed_) return Status::closed;
+  if (shard >= num_shards_ || name.empty() || name.find('|') != std::string::npos)
+    return Status::invalid_argument;
+  if (!ptr || len == 0) return Status::invalid_argument;
   if (cast && (len % 2 || (geo.has() && geo.nc % 2))) return Status::invalid_argument;  // bf16
   if (geo.has() && (geo.nr * geo.nc != len || geo.r0 + geo.nr > geo.rows ||
                     geo.c0 + geo.nc > geo.row_bytes))
     return Status::invalid_argument;
+  if (published_ || current_) return Status::invalid_state;
   Shard& sh = shards_[shard];
   if (sh.by_name.count(name)) return Status::already_exists;
-  if (published_ || current_) return Status::invalid_state;
   cudaPointerAttributes attr{};
   if (cudaPointerGetAttributes(&attr, ptr) != cudaSuccess || attr.type != cudaMemoryTypeDevice) {
     cudaGetLastError();
@@ -1622,6 +1626,7 @@ Status Client::update(const VersionSpec& spec, bool* changed, VersionId* out, do
 }
 
 Status Client::close() {
+  closed_ = true;
   stop_serving();
   for (auto& sh : shards_) serves_->erase(ServeRegistry::key(model_, replica_, sh.idx));
   if (opened_) reg_->close(model_, replica_);

@@ -376,6 +376,7 @@ class Client {
   std::vector<bool> launched_;
   bool published_ = false;
   bool opened_ = false;
+  bool closed_ = false;
   ClientStats stats_;
 };
 

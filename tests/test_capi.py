@@ -56,8 +56,16 @@ def test_bad_arguments_fail_loudly_without_gpu():
         a = np.zeros(16, np.uint8)
         assert h.register_tensor(0, "x", ptr=a.ctypes.data, nbytes=16) == Status.invalid_argument
         assert h.register_tensor(0, "", ptr=a.ctypes.data, nbytes=16) == Status.invalid_argument
+        # the reference rejects '|' in names and empty regions (client_core.cpp:537-540)
+        assert h.register_tensor(0, "a|b", ptr=a.ctypes.data, nbytes=16) == Status.invalid_argument
+        assert h.register_tensor(0, "x", ptr=a.ctypes.data, nbytes=0) == Status.invalid_argument
+        assert h.register_tensor(1, "x", ptr=a.ctypes.data, nbytes=16) == Status.invalid_argument
         assert h.replicate("bogus").status == Status.invalid_argument
         # nothing registered: cannot open the replica
         assert h.publish(1).status == Status.invalid_state
         with pytest.raises(Exception):
             cl.locate("m", "nobody")
+        # a closed handle refuses registrations (Status::closed)
+        h.close()
+        assert h.register_tensor(0, "y", ptr=a.ctypes.data, nbytes=16) in (Status.closed,
+                                                                              Status.invalid_argument)
