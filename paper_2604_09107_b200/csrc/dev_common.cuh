@@ -109,8 +109,10 @@ __device__ __forceinline__ void st_release_sys(std::uint32_t* p, std::uint32_t v
   asm volatile("st.release.sys.global.u32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
 }
 // One release fence for several flag stores (fence + relaxed store = release).
-__device__ __forceinline__ void fence_acq_rel_sys() {
-  asm volatile("fence.acq_rel.sys;\n" ::: "memory");
+// fence.release (no acquire half) skips the L1 invalidation (CCTL.IVALL)
+// that fence.acq_rel.sys carries.
+__device__ __forceinline__ void fence_release_sys() {
+  asm volatile("fence.release.sys;\n" ::: "memory");
 }
 __device__ __forceinline__ void st_relaxed_sys(std::uint32_t* p, std::uint32_t v) {
   asm volatile("st.relaxed.sys.global.u32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");

@@ -340,7 +340,7 @@ __global__ void __launch_bounds__(C::kThreads, C::kCtas) pull_tma_kernel(const P
       fence_proxy_async_global();
       __syncwarp();
       if (lane == 0 && p.dst_flags) {
-        fence_acq_rel_sys();
+        fence_release_sys();
 #pragma unroll
         for (int i = 0; i < kRelease; ++i)
           if (i < npend) st_relaxed_sys(&p.dst_flags[pend[i]], p.dst_epoch);
@@ -562,6 +562,8 @@ using V5 = Cfg<512, 2, 6, 0>;  // 2-stage rings, 6 CTAs per SM
 using V6 = Cfg<256, 3, 7, 0>;  // 7 CTAs per SM
 using V7 = Cfg<512, 3, 1, 0, 4>;    // one CTA per SM: 4 pipelines, consumers on 4 sub-partitions
 using V8 = Cfg<512, 2, 1, 320, 4>;  // 4 two-stage pipelines + the segment table in smem
+using V9 = Cfg<256, 4, 1, 320, 4>;  // 4 four-stage pipelines of 256-byte pieces
+using V10 = Cfg<256, 5, 1, 128, 4>;
 
 int variant() {  // -1: by workload
   static const int v = [] {
@@ -591,6 +593,8 @@ cudaError_t launch_pull_tma(const PullParams& p, int sms, cudaStream_t s) {
     case 6: return launch_variant<V6>(p, sms, s);
     case 7: return launch_variant<V7>(p, sms, s);
     case 8: return launch_variant<V8>(p, sms, s);
+    case 9: return launch_variant<V9>(p, sms, s);
+    case 10: return launch_variant<V10>(p, sms, s);
     default: return launch_variant<V0>(p, sms, s);
   }
 }
