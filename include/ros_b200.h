@@ -70,6 +70,9 @@ typedef struct {
   uint32_t last_pull_launches;
   uint64_t h2d_bytes;       /* descriptor uploads, cumulative                     */
   uint64_t d2h_bytes;       /* status / digest read-backs, cumulative             */
+  float fill_max_ms;        /* last fill round: the slowest local shard's kernel   */
+  float fill_sum_ms;        /* last fill round: all local shards' kernels, summed  */
+  uint64_t fill_bytes;      /* last fill round: bytes landed by all local shards   */
 } rs_stats;
 
 /* ---- process-level objects ------------------------------------------------ */

@@ -39,7 +39,8 @@ class RsStats(C.Structure):
                 ("items_verified", u64), ("checksum_failures", u64), ("failure_reports", u64),
                 ("failovers", u64), ("last_pull_ms", C.c_float), ("last_publish_ms", C.c_float),
                 ("last_pull_bytes", u64), ("last_pull_launches", u32), ("h2d_bytes", u64),
-                ("d2h_bytes", u64)]
+                ("d2h_bytes", u64), ("fill_max_ms", C.c_float), ("fill_sum_ms", C.c_float),
+                ("fill_bytes", u64)]
 
 
 _SIGS = {

@@ -22,6 +22,8 @@ def run(args):
         return run_elastic(args)
     if getattr(args, "reshard", "none") == "fsdp_tp2":
         return run_fsdp_tp2(args)
+    if getattr(args, "reshard", "none") == "tp2":
+        return run_tp2_fanout(args)
     if getattr(args, "fanout", "chain") == "ring":
         return run_ring(args)
     import torch
@@ -603,6 +605,150 @@ def run_elastic(args):
                     "unit": B.UNIT, "h2d_bytes_per_step": None, "d2h_bytes_per_step": None,
                     "what": "unpublish + re-publish (K6 digests) + every reader on v+1, wall clock"},
             "gpu_launches": None,
+            "verified": verified,
+        }
+        print(json.dumps(line), flush=True)
+    dist.barrier(group=dc.pg)
+    dc.close()
+    dist.destroy_process_group()
+
+
+def run_tp2_fanout(args):
+    """The north-star scenario: a TP=1 trainer (GPU0) fans Llama-3-8B out to
+    TP=2 rollout replicas, resharding on pull.  Replica j's shards live on
+    GPUs 2j+1 and 2j+2 (an odd last GPU holds both shards of its replica).
+    All replicas replicate at once: the first reshards from the trainer, the
+    next chase the first (same slicing) shard-for-shard, and so on.  Every
+    receiver lands a TP-2 shard (8.03 GB).  The trainer must emit the whole
+    model once, so the bound is the busiest GPU's NVLink traffic."""
+    import torch
+    import torch.distributed as dist
+
+    import bench as B
+    from paper_2604_09107_b200.dist import DistCluster
+    from paper_2604_09107_b200.ros import Status, tp_slice
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", str(rank)))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist.init_process_group("gloo")
+    dc = DistCluster()
+    shapes = B.workload_shapes(args.workload)
+    total = sum(2 * B._numel(s) for _, s in shapes)
+    readers = list(range(1, world))
+    groups = [readers[i:i + 2] for i in range(0, len(readers), 2)]
+    mine = [(j, g) for j, g in enumerate(groups) if rank in g]
+    handle, shard_bufs = None, {}
+    if rank == 0:
+        arena, views = B.alloc_replica(shapes, dev, seed_base=42)
+        handle = dc.create("m", "trainer", 1, chunk_bytes=args.chunk, pull_timeout_s=60.0)
+        for (n, v), (_, shape) in zip(views, shapes):
+            assert handle.register_slice(0, n, v, tp_slice(shape, 2, None, 1, 0)) == Status.ok
+    elif mine:
+        j, g = mine[0]
+        my_shards = [0, 1] if len(g) == 1 else [g.index(rank)]
+        handle = dc.create("m", f"tp2_{j}", 2, chunk_bytes=args.chunk, pull_timeout_s=60.0)
+        for s in my_shards:
+            for n, shape in shapes:
+                geo = tp_slice(shape, 2, B.tp_dim(n), 2, s)
+                buf = torch.zeros(geo[3] * geo[5], dtype=torch.uint8, device=dev)
+                shard_bufs[(s, n)] = (buf, geo)
+                assert handle.register_slice(s, n, buf, geo) == Status.ok
+    torch.cuda.synchronize()
+    dc.open(handle, endpoints=None if handle is None else
+            [f"rank{rank}:cuda{local}"] * len(handle.local_shards()))
+    streams = []
+    if handle is not None and rank != 0:
+        for s in handle.local_shards():  # a GPU holding two shards fills them concurrently
+            streams.append(torch.cuda.Stream(device=dev))
+            handle.set_stream(s, streams[-1])
+    t0 = time.perf_counter()
+    dc.publish(handle if rank == 0 else None, 1)
+    publish_s = time.perf_counter() - t0
+    reader = handle if rank != 0 else None
+
+    def step():
+        dc.unpublish(reader if (reader is not None and reader.is_published) else None)
+        if reader is not None:
+            reader.invalidate()
+        dist.barrier(group=dc.pg)
+        torch.cuda.synchronize()
+        w0 = time.perf_counter()
+        res = dc.replicate(reader, "latest")
+        torch.cuda.synchronize()
+        wall = time.perf_counter() - w0
+        if reader is not None:
+            assert res.status == Status.ok, res
+            return wall, reader.stats().fill_max_ms
+        return wall, 0.0
+
+    for _ in range(args.warmup):
+        step()
+    verified = True
+    if not args.no_verify and shard_bufs:
+        for i, (n, shape) in enumerate(shapes):
+            full = _synth_full(shape, 42 + i, dev)
+            for s in (0, 1):
+                if (s, n) in shard_bufs:
+                    buf, geo = shard_bufs[(s, n)]
+                    verified &= bool(torch.equal(buf, _piece(full, geo)))
+            del full
+    verified = all(dc.gather(verified))
+    clk = B.ClockSampler(local)
+    dist.barrier(group=dc.pg)
+    torch.cuda.synchronize()
+    clk.start()
+    walls, kms = [], []
+    for _ in range(args.steps):
+        w, k = step()
+        walls.append(w)
+        kms.append(k)
+    clocks = clk.stop()
+    shard_bytes = {s: sum(g[3] * g[5] for (ss, n), (b, g) in shard_bufs.items() if ss == s)
+                   for s in (0, 1)}
+    my_bytes = sum(shard_bytes.values())
+    allv = dc.gather((kms, my_bytes, sum(walls), clocks, rank))
+    step_dev_ms = [max(a[0][i] for a in allv) for i in range(args.steps)]
+    rx = [a for a in allv if a[1] > 0]
+    total_landed = args.steps * sum(a[1] for a in rx)
+    if rank == 0:
+        per_rx = [round(a[1] / (statistics.mean(a[0]) / 1e3) / 1e9, 2) for a in rx]
+        mean_rx = statistics.mean(per_rx)
+        # busiest GPU: the trainer emits the whole model once (both halves);
+        # a receiver's bound is its bytes over that time
+        t_min = total / 900e9
+        peaks = [a[1] / t_min / 1e9 for a in rx]
+        frac = statistics.mean(x / p for x, p in zip(per_rx, peaks))
+        plan = sorted({f"{a.replica}<-{a.src}" for a in dc.assigns()})
+        line = {
+            "metric": B.METRIC, "value": round(total_landed / (sum(step_dev_ms) / 1e3) / 1e9, 2),
+            "unit": B.UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(sum(step_dev_ms) / args.steps, 3), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+            "config": {"workload": f"{args.workload}: TP=1 trainer (GPU0) -> {len(groups)} TP=2 "
+                                   "replicas on GPU pairs, resharded on pull, chained",
+                       "receivers": len(rx), "bytes_per_receiver": [a[1] for a in rx],
+                       "chunk_bytes": args.chunk, "plan": plan,
+                       "l2": "inputs >> 126 MB L2; no flush"},
+            "per_receiver_gbs": per_rx,
+            "weight_update_latency_s": round(max(a[2] for a in allv) / args.steps, 5),
+            "publish_s": round(publish_s, 4),
+            "roofline": {"bound": "nvlink", "achieved": round(mean_rx, 1),
+                         "peak": round(statistics.mean(peaks), 1),
+                         "unit": "GB/s", "frac": round(frac, 4), "traffic": None,
+                         "peak_src": "per receiver: its bytes / (model bytes / 900 GB/s nominal): "
+                                     "the trainer's NVLink egress carries the whole model once; "
+                                     "frac = mean of achieved/peak over receivers",
+                         "kernel": "pull_tma_kernel",
+                         "kernel_ms_avg": round(statistics.mean(step_dev_ms), 3),
+                         "alg_bytes_per_launch": max(a[1] for a in rx)},
+            "e2e": {"value": round(total_landed / max(a[2] for a in allv) / 1e9, 2), "unit": B.UNIT,
+                    "h2d_bytes_per_step": None, "d2h_bytes_per_step": None,
+                    "what": "wall clock of the collective replicate (plan+bind+IPC exchange+kernel)"},
+            "gpu_launches": args.steps * len(rx),
+            "clocks": clocks,
             "verified": verified,
         }
         print(json.dumps(line), flush=True)

@@ -334,6 +334,9 @@ int rs_stats_get(rs_handle* h, rs_stats* out) {
   out->last_pull_launches = s.last_pull_launches;
   out->h2d_bytes = s.h2d_bytes;
   out->d2h_bytes = s.d2h_bytes;
+  out->fill_max_ms = s.fill_max_ms;
+  out->fill_sum_ms = s.fill_sum_ms;
+  out->fill_bytes = s.fill_bytes;
   return 0;
 }
 

@@ -1304,6 +1304,8 @@ std::vector<Client::FillOutcome> Client::wait_shards(const std::vector<std::uint
   std::vector<bool> launched = launched_;
   if (launched.size() != num_shards_) launched.assign(num_shards_, false);
   std::vector<dev::PullStatus> st(num_shards_);
+  stats_.fill_max_ms = stats_.fill_sum_ms = 0;
+  stats_.fill_bytes = 0;
   for (std::uint32_t i : which) {
     if (!launched[i]) continue;
     Shard& sh = shards_[i];
@@ -1320,6 +1322,9 @@ std::vector<Client::FillOutcome> Client::wait_shards(const std::vector<std::uint
     cudaEventElapsedTime(&ms, sh.ev0, sh.ev1);
     stats_.last_pull_ms = ms;
     stats_.last_pull_bytes = st[i].bytes;
+    stats_.fill_max_ms = std::max(stats_.fill_max_ms, ms);
+    stats_.fill_sum_ms += ms;
+    stats_.fill_bytes += st[i].bytes;
     stats_.last_pull_launches = 1;
     stats_.bytes_pulled += st[i].bytes;
     stats_.checksum_failures += st[i].retried_batches;

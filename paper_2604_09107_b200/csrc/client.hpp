@@ -177,6 +177,9 @@ struct ClientStats {
   std::uint32_t last_pull_launches = 0;
   std::uint64_t h2d_bytes = 0;  // descriptor uploads (cumulative)
   std::uint64_t d2h_bytes = 0;  // status / digest read-backs (cumulative)
+  // the last fill round over every local shard
+  float fill_max_ms = 0, fill_sum_ms = 0;
+  std::uint64_t fill_bytes = 0;
 };
 
 class Client {

@@ -80,6 +80,9 @@ class Stats:
     last_pull_launches: int = 0
     h2d_bytes: int = 0
     d2h_bytes: int = 0
+    fill_max_ms: float = 0.0
+    fill_sum_ms: float = 0.0
+    fill_bytes: int = 0
 
 
 @dataclass
