@@ -249,6 +249,14 @@ int rs_server_take_releases(rs_cluster* c, const char* model, const char* owner,
 int rs_cluster_kind(rs_cluster* c, const char* model, const char* replica, char* buf, size_t cap,
                     size_t* len);  /* "worker" | "offload" */
 
+/* ---- off-box data plane (transport_stream.hpp:36-76)
+ * Serve this process's serve states over TCP (port 0: any free port).  A
+ * reader whose assigned source endpoint is "tcp:<host>:<port>" (set with
+ * rs_set_endpoint on the source) receives the source's chunk map, digest
+ * table and payload batches into pinned, device-mapped host memory; its pull
+ * kernel lands and verifies them, chasing per-batch host watermarks. */
+int rs_cluster_listen(rs_cluster* c, const char* host, int port, int* bound_port);
+
 /* ---- device primitives (kernel boundary) --------------------------------- */
 /* digest64 (digest.cpp:79-106) of n device spans; out is host memory. */
 int rs_digest_spans(const uint64_t* dev_ptrs, const uint64_t* lens, int n, uint64_t* out,

@@ -72,6 +72,7 @@ _SIGS = {
     "rs_server_offload_confirm": (i32, [vp, cstr, cstr, u32, u64, i32, cstr]),
     "rs_server_take_releases": (i32, [vp, cstr, cstr, vp, sz, C.POINTER(sz)]),
     "rs_cluster_kind": (i32, [vp, cstr, cstr, vp, sz, C.POINTER(sz)]),
+    "rs_cluster_listen": (i32, [vp, cstr, i32, C.POINTER(i32)]),
     "rs_transfer_launch": (i32, [vp]),
     "rs_transfer_progress": (i32, [vp, u32, C.POINTER(u32), C.POINTER(u32)]),
     "rs_transfer_wait": (i32, [vp, vp, vp]),

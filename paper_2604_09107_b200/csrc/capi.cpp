@@ -12,10 +12,12 @@
 #include "client.hpp"
 #include "device.hpp"
 #include "registry.hpp"
+#include "stream.hpp"
 
 struct rs_cluster {
   rsb::Registry reg;
   rsb::ServeRegistry serves;
+  std::unique_ptr<rsb::StreamServer> stream;  // off-box data plane (rs_cluster_listen)
   explicit rs_cluster(rsb::Registry::Config c) : reg(c) {}
 };
 
@@ -636,6 +638,15 @@ int rs_server_take_releases(rs_cluster* c, const char* model, const char* owner,
   if (n) *n = rs.size();
   if (versions)
     for (size_t i = 0; i < rs.size() && i < cap; ++i) versions[i] = rs[i].version;
+  return 0;
+}
+
+int rs_cluster_listen(rs_cluster* c, const char* host, int port, int* bound_port) {
+  if (!c || !host) return st(rsb::Status::invalid_argument);
+  if (!c->stream) c->stream = std::make_unique<rsb::StreamServer>(&c->serves);
+  auto r = c->stream->start(host, port);
+  if (!r) return st(r.status());
+  if (bound_port) *bound_port = *r;
   return 0;
 }
 

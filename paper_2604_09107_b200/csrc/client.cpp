@@ -1,5 +1,7 @@
 #include "client.hpp"
 
+#include "stream.hpp"
+
 #include <cuda.h>
 #include <fcntl.h>
 #include <sys/mman.h>
@@ -979,12 +981,18 @@ Status Client::resolve_source(Shard& sh, const Assignment& a, VersionId v, Sourc
   for (;;) {
     auto st = serves_->is_silent(k) ? nullptr : serves_->find(k);
     if (st) {
-      bool ready;
+      bool ready, same_gpu_filling;
       {
         std::lock_guard lk(st->m);
         ready = st->serving && st->version == v && !st->cmap.chunk0.empty();
+        // A persistent pull kernel holds every SM of its GPU, so a chaser on
+        // the upstream's own GPU could start first, spin, and starve the fill
+        // it waits for: on one GPU the chase waits for the upstream instead.
+        same_gpu_filling = !st->imported && st->device == sh.device && !st->complete;
       }
-      if (ready) return map_source(st, sh.device, out);
+      if (ready && !same_gpu_filling) return map_source(st, sh.device, out);
+      if (ready) deadline = std::max(deadline, std::chrono::steady_clock::now() +
+                                                   std::chrono::duration<double>(4 * wait_s));
     }
     if (std::chrono::steady_clock::now() > deadline) return Status::not_serving;
     std::this_thread::sleep_for(std::chrono::microseconds(200));
@@ -1264,15 +1272,28 @@ void Client::launch_shards(const std::vector<Assignment>& as,
       continue;
     }
     SourceView view;
-    Status s = resolve_source(sh, a, a.version, &view, cfg_.pull_timeout_s);
+    Status s;
+    const bool off_box = a.source_endpoint.rfind("tcp:", 0) == 0;
+    if (off_box) {
+      // off-box source: its stream lands in pinned host memory and the pull
+      // kernel chases the host watermarks the receiver raises (stream.hpp)
+      sh.tcp = std::make_shared<StreamSource>();
+      s = sh.tcp->open(a.source_endpoint, ServeRegistry::key(model_, a.source_replica, sh.idx),
+                       a.version, cfg_.pull_timeout_s, &host_pool_);
+      if (ok(s)) view = sh.tcp->view();
+    } else {
+      s = resolve_source(sh, a, a.version, &view, cfg_.pull_timeout_s);
+    }
     // Every replica of a cluster digests with the same chunk size; a source
     // cut differently cannot be verified chunk-by-chunk.
     if (ok(s) && !(view.cmap == sh.holding->cmap)) s = Status::protocol_error;
     if (!ok(s)) {
+      if (sh.tcp) sh.tcp->release(&host_pool_);
+      sh.tcp.reset();
       out[i] = {s, 0, 0};
       continue;
     }
-    s = launch_fill(sh, view, a.source_complete);
+    s = launch_fill(sh, view, off_box ? false : a.source_complete);
     if (!ok(s)) {
       out[i] = {s, 0, 0};
       continue;
@@ -1314,6 +1335,23 @@ std::vector<Client::FillOutcome> Client::wait_shards(const std::vector<std::uint
     cudaMemcpyAsync(&st[i], status, sizeof(dev::PullStatus), cudaMemcpyDeviceToHost, sh.stream);
     cudaError_t e = cudaStreamSynchronize(sh.stream);
     stats_.d2h_bytes += sizeof(dev::PullStatus);
+    Status net = Status::ok;
+    if (sh.tcp) {
+      net = sh.tcp->finish();
+      if (std::getenv("RSB_DEBUG") && st[i].code != dev::kPullOk) {
+        auto fs = sh.tcp->flag_summary();
+        std::fprintf(stderr, "[rsb] tcp source: %u of %u watermarks set, first missing %u, %llu bytes\n",
+                     fs.first, sh.tcp->view().cmap.n_batches(), fs.second,
+                     static_cast<unsigned long long>(sh.tcp->bytes_received()));
+      }
+      sh.tcp->release(&host_pool_);
+      sh.tcp.reset();
+    }
+    if (e == cudaSuccess && !ok(net) && st[i].code == dev::kPullOk) st[i].code = dev::kPullNotServing;
+    if (std::getenv("RSB_DEBUG") && (st[i].code != dev::kPullOk || e != cudaSuccess))
+      std::fprintf(stderr, "[rsb] %s shard %u fill: code %u bad_chunk %u net %d cuda %d\n",
+                   replica_.c_str(), i, st[i].code, st[i].bad_chunk, static_cast<int>(net),
+                   static_cast<int>(e));
     if (e != cudaSuccess) {
       out[i] = {Status::transfer_failed, 0, 0};
       continue;

@@ -36,6 +36,8 @@
 
 namespace rsb {
 
+class StreamSource;  // stream.hpp: a source reached over TCP
+
 struct ClientConfig {
   std::uint64_t chunk_bytes = 4096;  // digest + watermark unit (multiple of 16)
   PackLimits limits;                 // tiny-tensor packing (config.hpp:46)
@@ -340,6 +342,7 @@ class Client {
       std::string endpoint;
     };
     std::map<VersionId, Lane> lanes;  // retention offloads held for the registry
+    std::shared_ptr<StreamSource> tcp;  // the fill's source when it is off-box (tcp:)
   };
   Status make_retention_lane(Shard& sh, VersionId v, std::string* endpoint);
   Status settle_offload(OpOutcome* o, double wait_s);

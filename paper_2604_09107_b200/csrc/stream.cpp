@@ -1,0 +1,490 @@
+#include "stream.hpp"
+
+#include <arpa/inet.h>
+#include <netdb.h>
+#include <netinet/in.h>
+#include <netinet/tcp.h>
+#include <sys/socket.h>
+#include <unistd.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+
+namespace rsb {
+
+namespace {
+
+bool debug() {
+  static const bool d = std::getenv("RSB_DEBUG") != nullptr;
+  return d;
+}
+
+constexpr std::uint32_t kReqMagic = 0x31505352;  // "RSP1"
+constexpr std::uint32_t kEnd = 0xffffffffu;
+constexpr std::uint32_t kFrameBatches = 32;  // up to 32 watermark batches per frame
+constexpr std::size_t kStageBytes = 8u << 20;  // per staging buffer (frames are cut to fit)
+constexpr int kSlots = 8;                      // concurrent connections with staging
+
+bool send_all(int fd, const void* p, std::size_t n) {
+  const auto* b = static_cast<const std::uint8_t*>(p);
+  while (n) {
+    const ssize_t k = ::send(fd, b, n, MSG_NOSIGNAL);
+    if (k <= 0) return false;
+    b += k;
+    n -= static_cast<std::size_t>(k);
+  }
+  return true;
+}
+
+bool recv_all(int fd, void* p, std::size_t n) {
+  auto* b = static_cast<std::uint8_t*>(p);
+  while (n) {
+    const ssize_t k = ::recv(fd, b, n, 0);
+    if (k <= 0) return false;
+    b += k;
+    n -= static_cast<std::size_t>(k);
+  }
+  return true;
+}
+
+template <class T>
+bool send_pod(int fd, const T& v) {
+  return send_all(fd, &v, sizeof(v));
+}
+template <class T>
+bool recv_pod(int fd, T* v) {
+  return recv_all(fd, v, sizeof(T));
+}
+template <class T>
+bool send_vec(int fd, const std::vector<T>& v) {
+  const auto n = static_cast<std::uint32_t>(v.size());
+  return send_pod(fd, n) && (n == 0 || send_all(fd, v.data(), n * sizeof(T)));
+}
+template <class T>
+bool recv_vec(int fd, std::vector<T>* v) {
+  std::uint32_t n = 0;
+  if (!recv_pod(fd, &n)) return false;
+  v->resize(n);
+  return n == 0 || recv_all(fd, v->data(), n * sizeof(T));
+}
+
+void tune(int fd) {
+  int one = 1;
+  setsockopt(fd, IPPROTO_TCP, TCP_NODELAY, &one, sizeof(one));
+  int buf = 8 << 20;
+  setsockopt(fd, SOL_SOCKET, SO_SNDBUF, &buf, sizeof(buf));
+  setsockopt(fd, SOL_SOCKET, SO_RCVBUF, &buf, sizeof(buf));
+}
+
+// One batch's byte range inside its item.
+struct BatchSpan {
+  std::uint32_t item = 0;
+  std::uint64_t off = 0, len = 0;
+};
+
+std::vector<BatchSpan> batch_spans(const ChunkMap& cm, const std::vector<std::uint64_t>& item_len) {
+  std::vector<BatchSpan> out(cm.n_batches());
+  for (std::uint32_t i = 0; i + 1 < cm.chunk0.size(); ++i) {
+    const std::uint32_t b0 = cm.chunk0[i] / dev::kBatchChunks;
+    const std::uint32_t nb = (cm.count[i] + dev::kBatchChunks - 1) / dev::kBatchChunks;
+    for (std::uint32_t k = 0; k < nb; ++k) {
+      const std::uint64_t off = std::uint64_t(k) * dev::kBatchChunks * cm.chunk_len[i];
+      const std::uint64_t end =
+          std::min<std::uint64_t>(off + std::uint64_t(dev::kBatchChunks) * cm.chunk_len[i], item_len[i]);
+      out[b0 + k] = {i, off, end > off ? end - off : 0};
+    }
+  }
+  return out;
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ server
+
+StreamServer::StreamServer(ServeRegistry* serves) : serves_(serves) {}
+
+StreamServer::~StreamServer() { stop(); }
+
+Result<int> StreamServer::start(const std::string& host, int port) {
+  if (listen_fd_ >= 0) return port_;
+  listen_fd_ = ::socket(AF_INET, SOCK_STREAM, 0);
+  if (listen_fd_ < 0) return Status::transfer_failed;
+  int one = 1;
+  setsockopt(listen_fd_, SOL_SOCKET, SO_REUSEADDR, &one, sizeof(one));
+  sockaddr_in a{};
+  a.sin_family = AF_INET;
+  a.sin_port = htons(static_cast<std::uint16_t>(port));
+  if (inet_pton(AF_INET, host.c_str(), &a.sin_addr) != 1 ||
+      ::bind(listen_fd_, reinterpret_cast<sockaddr*>(&a), sizeof(a)) != 0 ||
+      ::listen(listen_fd_, 64) != 0) {
+    ::close(listen_fd_);
+    listen_fd_ = -1;
+    return Status::transfer_failed;
+  }
+  socklen_t len = sizeof(a);
+  getsockname(listen_fd_, reinterpret_cast<sockaddr*>(&a), &len);
+  port_ = ntohs(a.sin_port);
+  for (int i = 0; i < kSlots; ++i) {
+    auto sl = std::make_unique<Slot>();
+    sl->bytes = kStageBytes;
+    if (cudaHostAlloc(&sl->stage[0], kStageBytes, cudaHostAllocPortable) != cudaSuccess ||
+        cudaHostAlloc(&sl->stage[1], kStageBytes, cudaHostAllocPortable) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&sl->stream, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&sl->ev[0], cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&sl->ev[1], cudaEventDisableTiming) != cudaSuccess) {
+      cudaGetLastError();
+      break;
+    }
+    free_slots_.push_back(sl.get());
+    slots_.push_back(std::move(sl));
+  }
+  acceptor_ = std::thread([this] { accept_loop(); });
+  return port_;
+}
+
+void StreamServer::stop() {
+  if (listen_fd_ < 0) return;
+  stop_ = true;
+  ::shutdown(listen_fd_, SHUT_RDWR);
+  ::close(listen_fd_);
+  listen_fd_ = -1;
+  if (acceptor_.joinable()) acceptor_.join();
+  {
+    std::lock_guard lk(conns_mu_);
+    for (auto& t : conns_)
+      if (t.joinable()) t.join();
+    conns_.clear();
+  }
+  for (auto& sl : slots_) {
+    cudaStreamSynchronize(sl->stream);
+    cudaEventDestroy(sl->ev[0]);
+    cudaEventDestroy(sl->ev[1]);
+    cudaStreamDestroy(sl->stream);
+    cudaFreeHost(sl->stage[0]);
+    cudaFreeHost(sl->stage[1]);
+  }
+  cudaGetLastError();
+  slots_.clear();
+  free_slots_.clear();
+}
+
+StreamServer::Slot* StreamServer::take_slot() {
+  for (;;) {
+    {
+      std::lock_guard lk(slots_mu_);
+      if (!free_slots_.empty()) {
+        Slot* s = free_slots_.back();
+        free_slots_.pop_back();
+        return s;
+      }
+      if (slots_.empty() || stop_) return nullptr;
+    }
+    std::this_thread::sleep_for(std::chrono::microseconds(200));
+  }
+}
+
+void StreamServer::give_slot(Slot* s) {
+  std::lock_guard lk(slots_mu_);
+  free_slots_.push_back(s);
+}
+
+void StreamServer::accept_loop() {
+  while (!stop_) {
+    const int fd = ::accept(listen_fd_, nullptr, nullptr);
+    if (fd < 0) {
+      if (stop_) return;
+      continue;
+    }
+    tune(fd);
+    std::lock_guard lk(conns_mu_);
+    conns_.emplace_back([this, fd] { serve_conn(fd); });
+  }
+}
+
+void StreamServer::serve_conn(int fd) {
+  auto finish = [&](std::uint32_t status) {
+    send_pod(fd, status);
+    ::close(fd);
+  };
+  std::uint32_t magic = 0, klen = 0;
+  VersionId version = 0;
+  if (!recv_pod(fd, &magic) || magic != kReqMagic || !recv_pod(fd, &klen) || klen > 4096)
+    return (void)::close(fd);
+  std::string key(klen, '\0');
+  if (!recv_all(fd, key.data(), klen) || !recv_pod(fd, &version)) return (void)::close(fd);
+  auto st = serves_->find(key);
+  if (!st) return finish(static_cast<std::uint32_t>(Status::not_serving));
+  // snapshot of the serve state (addresses in this process)
+  ChunkMap cm;
+  std::vector<std::uint64_t> ptrs, lens;
+  std::uint64_t digests = 0, flags = 0;
+  std::uint32_t epoch = 0;
+  bool complete = false;
+  int device = -1;
+  {
+    std::lock_guard lk(st->m);
+    if (!st->serving || st->version != version || st->imported)
+      return finish(static_cast<std::uint32_t>(Status::not_serving));
+    cm = st->cmap;
+    ptrs = st->item_ptrs;
+    std::uint64_t prev = 0;
+    for (auto e : st->item_ends) {
+      lens.push_back(e - prev);
+      prev = e;
+    }
+    digests = st->digests;
+    flags = st->flags;
+    epoch = st->epoch;
+    complete = st->complete;
+    device = st->device;
+  }
+  if (device >= 0) cudaSetDevice(device);
+  const auto spans = batch_spans(cm, lens);
+  for (const auto& sp : spans)
+    if (sp.len > kStageBytes) return finish(static_cast<std::uint32_t>(Status::invalid_argument));
+  // header: chunk map, item lengths, chunk-digest table
+  std::vector<std::uint64_t> dig(cm.n_chunks());
+  if (!dig.empty() && cudaMemcpy(dig.data(), reinterpret_cast<const void*>(digests), dig.size() * 8,
+                                 cudaMemcpyDefault) != cudaSuccess)
+    return finish(static_cast<std::uint32_t>(Status::transfer_failed));
+  if (!send_pod(fd, std::uint32_t{0}) || !send_vec(fd, cm.chunk0) || !send_vec(fd, cm.chunk_len) ||
+      !send_vec(fd, cm.count) || !send_vec(fd, lens) || !send_vec(fd, dig))
+    return (void)::close(fd);
+  // payload: frames of up to kFrameBatches consecutive batches of one item,
+  // each sent once the source has verified it (double-buffered D2H staging)
+  Slot* slot = take_slot();
+  if (!slot) return (void)::close(fd);
+  void* const* stage = slot->stage;
+  cudaStream_t cs = slot->stream;
+  cudaEvent_t* ev = slot->ev;
+  std::vector<std::uint32_t> fl(complete ? 0 : cm.n_batches());
+  auto landed = [&](std::uint32_t b) {  // the source verified batch b
+    if (complete) return true;
+    auto deadline = std::chrono::steady_clock::now() + std::chrono::seconds(60);
+    while (fl[b] != epoch) {
+      cudaMemcpy(fl.data() + b, reinterpret_cast<const std::uint32_t*>(flags) + b,
+                 (fl.size() - b) * 4, cudaMemcpyDefault);
+      if (fl[b] == epoch) break;
+      if (std::chrono::steady_clock::now() > deadline || (fl[b] & dev::kAbort)) return false;
+      std::this_thread::sleep_for(std::chrono::microseconds(50));
+    }
+    return true;
+  };
+  struct Frame {
+    std::uint32_t b0 = 0, nb = 0;
+    std::uint64_t len = 0;
+  };
+  std::vector<Frame> frames;
+  for (std::uint32_t b = 0; b < spans.size();) {
+    if (spans[b].len == 0) {
+      ++b;
+      continue;
+    }
+    Frame f{b, 0, 0};
+    while (b < spans.size() && f.nb < kFrameBatches && spans[b].len &&
+           spans[b].item == spans[f.b0].item && f.len + spans[b].len <= kStageBytes) {
+      f.len += spans[b].len;
+      ++f.nb;
+      ++b;
+    }
+    frames.push_back(f);
+  }
+  bool good = true;
+  auto issue = [&](std::size_t k) {
+    const Frame& f = frames[k];
+    for (std::uint32_t b = f.b0; b < f.b0 + f.nb; ++b)
+      if (!landed(b)) return false;
+    const BatchSpan& s0 = spans[f.b0];
+    return cudaMemcpyAsync(stage[k & 1], reinterpret_cast<const std::uint8_t*>(ptrs[s0.item]) + s0.off,
+                           f.len, cudaMemcpyDefault, cs) == cudaSuccess &&
+           cudaEventRecord(ev[k & 1], cs) == cudaSuccess;
+  };
+  if (!frames.empty()) good = issue(0);
+  for (std::size_t k = 0; good && k < frames.size(); ++k) {
+    if (k + 1 < frames.size()) good = issue(k + 1);
+    if (!good || cudaEventSynchronize(ev[k & 1]) != cudaSuccess) {
+      good = false;
+      break;
+    }
+    const Frame& f = frames[k];
+    good = send_pod(fd, f.b0) && send_pod(fd, f.nb) && send_pod(fd, f.len) &&
+           send_all(fd, stage[k & 1], f.len);
+  }
+  if (!good && debug())
+    std::fprintf(stderr, "[rsb] stream server: %s aborted (frames %zu)\n", key.c_str(), frames.size());
+  if (good) {
+    send_pod(fd, kEnd);
+    send_pod(fd, std::uint32_t{0});
+    send_pod(fd, std::uint64_t{0});
+  }
+  cudaStreamSynchronize(cs);
+  cudaGetLastError();
+  give_slot(slot);
+  ::close(fd);
+}
+
+// ------------------------------------------------------------------ reader
+
+StreamSource::~StreamSource() {
+  if (fd_ >= 0) ::shutdown(fd_, SHUT_RDWR);
+  if (rx_.joinable()) rx_.join();
+  if (fd_ >= 0) ::close(fd_);
+}
+
+Status StreamSource::open(const std::string& endpoint, const std::string& key, VersionId version,
+                          double timeout_s, std::vector<std::unique_ptr<HostBuf>>* pool) {
+  // endpoint "tcp:host:port"
+  const auto p1 = endpoint.find(':'), p2 = endpoint.rfind(':');
+  if (endpoint.rfind("tcp:", 0) != 0 || p2 == p1) return Status::invalid_argument;
+  const std::string host = endpoint.substr(p1 + 1, p2 - p1 - 1);
+  const int port = std::atoi(endpoint.c_str() + p2 + 1);
+  sockaddr_in a{};
+  a.sin_family = AF_INET;
+  a.sin_port = htons(static_cast<std::uint16_t>(port));
+  if (inet_pton(AF_INET, host.c_str(), &a.sin_addr) != 1) return Status::invalid_argument;
+  // An assigned upstream that is not serving yet is waited for, not
+  // condemned (as on the in-box path, Client::resolve_source).
+  auto deadline = std::chrono::steady_clock::now() + std::chrono::duration<double>(timeout_s);
+  const auto klen = static_cast<std::uint32_t>(key.size());
+  for (;;) {
+    fd_ = ::socket(AF_INET, SOCK_STREAM, 0);
+    std::uint32_t status = static_cast<std::uint32_t>(Status::not_serving);
+    if (fd_ >= 0 && ::connect(fd_, reinterpret_cast<sockaddr*>(&a), sizeof(a)) == 0) {
+      tune(fd_);
+      if (!send_pod(fd_, kReqMagic) || !send_pod(fd_, klen) || !send_all(fd_, key.data(), klen) ||
+          !send_pod(fd_, version) || !recv_pod(fd_, &status))
+        status = static_cast<std::uint32_t>(Status::transfer_failed);
+      if (status == 0) break;
+    }
+    if (fd_ >= 0) ::close(fd_);
+    fd_ = -1;
+    if (status != static_cast<std::uint32_t>(Status::not_serving)) return static_cast<Status>(status);
+    if (std::chrono::steady_clock::now() > deadline) return Status::not_serving;
+    std::this_thread::sleep_for(std::chrono::milliseconds(1));
+  }
+  ChunkMap cm;
+  std::vector<std::uint64_t> lens, dig;
+  if (!recv_vec(fd_, &cm.chunk0) || !recv_vec(fd_, &cm.chunk_len) || !recv_vec(fd_, &cm.count) ||
+      !recv_vec(fd_, &lens) || !recv_vec(fd_, &dig) || lens.size() + 1 != cm.chunk0.size() ||
+      dig.size() != cm.n_chunks())
+    return Status::protocol_error;
+  // pinned, device-mapped landing for the stream + digests + watermarks
+  item_off_.resize(lens.size());
+  std::uint64_t tot = 0;
+  for (std::size_t i = 0; i < lens.size(); ++i) {
+    item_off_[i] = tot;
+    tot += (lens[i] + 255) / 256 * 256;
+  }
+  auto take = [&](std::size_t n, std::unique_ptr<HostBuf>* out) -> Status {
+    if (pool)
+      for (auto it = pool->begin(); it != pool->end(); ++it)
+        if ((*it)->n >= n) {
+          *out = std::move(*it);
+          pool->erase(it);
+          return Status::ok;
+        }
+    *out = std::make_unique<HostBuf>();
+    return (*out)->alloc(n);
+  };
+  if (Status s = take(tot, &data_); !ok(s)) return s;
+  const std::size_t nb = cm.n_batches();
+  if (Status s = take(dig.size() * 8 + nb * 4 + 16, &tables_); !ok(s)) return s;
+  auto* tb = static_cast<std::uint8_t*>(tables_->p);
+  if (!dig.empty()) std::memcpy(tb, dig.data(), dig.size() * 8);
+  std::memset(tb + dig.size() * 8, 0, nb * 4);
+  view_.cmap = cm;
+  view_.item_ptrs.resize(lens.size());
+  for (std::size_t i = 0; i < lens.size(); ++i)
+    view_.item_ptrs[i] = reinterpret_cast<std::uint64_t>(data_->p) + item_off_[i];
+  view_.digests = reinterpret_cast<std::uint64_t>(tb);
+  view_.flags = reinterpret_cast<std::uint64_t>(tb + dig.size() * 8);
+  view_.epoch = 1;
+  view_.total = tot;
+  rx_ = std::thread([this, lens] {
+    (void)lens;
+    receive_loop();
+  });
+  return Status::ok;
+}
+
+void StreamSource::receive_loop() {
+  const ChunkMap& cm = view_.cmap;
+  std::vector<std::uint64_t> lens(item_off_.size());
+  // item of every batch and the batch's offset inside it
+  std::vector<std::uint32_t> item_of(cm.n_batches(), 0);
+  std::vector<std::uint64_t> off_of(cm.n_batches(), 0);
+  for (std::uint32_t i = 0; i + 1 < cm.chunk0.size(); ++i) {
+    const std::uint32_t b0 = cm.chunk0[i] / dev::kBatchChunks;
+    const std::uint32_t nb = (cm.count[i] + dev::kBatchChunks - 1) / dev::kBatchChunks;
+    for (std::uint32_t k = 0; k < nb; ++k) {
+      item_of[b0 + k] = i;
+      off_of[b0 + k] = std::uint64_t(k) * dev::kBatchChunks * cm.chunk_len[i];
+    }
+  }
+  auto* flags = reinterpret_cast<std::uint32_t*>(view_.flags);
+  auto* base = static_cast<std::uint8_t*>(data_->p);
+  for (;;) {
+    std::uint32_t b0 = 0, nb = 0;
+    std::uint64_t len = 0;
+    if (!recv_pod(fd_, &b0) || !recv_pod(fd_, &nb) || !recv_pod(fd_, &len)) {
+      rx_status_ = static_cast<int>(Status::transfer_failed);
+      abort_all();
+      return;
+    }
+    if (b0 == kEnd) break;
+    if (b0 + nb > item_of.size()) {
+      rx_status_ = static_cast<int>(Status::protocol_error);
+      abort_all();
+      return;
+    }
+    const std::uint32_t i = item_of[b0];
+    if (!recv_all(fd_, base + item_off_[i] + off_of[b0], len)) {
+      rx_status_ = static_cast<int>(Status::transfer_failed);
+      abort_all();
+      return;
+    }
+    received_ += len;
+    // the bytes are in memory before the watermarks the GPU polls (x86
+    // stores are ordered; the kernel reads the flag with ld.acquire.sys)
+    std::atomic_thread_fence(std::memory_order_release);
+    for (std::uint32_t b = b0; b < b0 + nb; ++b)
+      __atomic_store_n(&flags[b], 1u, __ATOMIC_RELEASE);
+  }
+  rx_status_ = 0;
+}
+
+void StreamSource::abort_all() {
+  if (debug()) std::fprintf(stderr, "[rsb] stream source: receive failed (%d)\n", rx_status_.load());
+  // the kernel chasing these watermarks stops at once (not_serving)
+  auto* flags = reinterpret_cast<std::uint32_t*>(view_.flags);
+  for (std::uint32_t b = 0; b < view_.cmap.n_batches(); ++b)
+    if (__atomic_load_n(&flags[b], __ATOMIC_ACQUIRE) != 1u)
+      __atomic_store_n(&flags[b], 1u | dev::kAbort, __ATOMIC_RELEASE);
+}
+
+std::pair<std::uint32_t, std::uint32_t> StreamSource::flag_summary() const {
+  const auto* flags = reinterpret_cast<const std::uint32_t*>(view_.flags);
+  std::uint32_t set = 0, first = ~0u;
+  for (std::uint32_t b = 0; b < view_.cmap.n_batches(); ++b) {
+    if (__atomic_load_n(&flags[b], __ATOMIC_ACQUIRE) == 1u) ++set;
+    else if (first == ~0u) first = b;
+  }
+  return {set, first};
+}
+
+void StreamSource::release(std::vector<std::unique_ptr<HostBuf>>* pool) {
+  if (rx_.joinable()) rx_.join();
+  if (!pool) return;
+  for (auto* b : {&data_, &tables_})
+    if (*b && pool->size() < 4) pool->push_back(std::move(*b));
+}
+
+Status StreamSource::finish() {
+  if (rx_.joinable()) rx_.join();
+  return static_cast<Status>(rx_status_.load());
+}
+
+}  // namespace rsb

@@ -208,6 +208,13 @@ class Cluster:
         return {"kind": kind, "lifecycle": life.value.decode(), "version": v.value,
                 "serving": s.value, "visible": bool(vis.value)}
 
+    def listen(self, host: str = "127.0.0.1", port: int = 0) -> int:
+        """Serve this process's serve states over TCP; returns the port.
+        Sources whose endpoint is "tcp:<host>:<port>" are pulled through it."""
+        p = C.c_int()
+        check(lib.rs_cluster_listen(self.h, _b(host), port, C.byref(p)), "rs_cluster_listen")
+        return p.value
+
     def releases(self, model: str, owner: str) -> list[int]:
         """Retention offloads of `owner` the registry released (taken)."""
         n = C.c_size_t(0)
