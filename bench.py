@@ -380,14 +380,68 @@ def run_single(args):
         "e2e": {"value": round(e2e, 2), "unit": UNIT,
                 "h2d_bytes_per_step": (st.h2d_bytes - h2d0) // args.steps,
                 "d2h_bytes_per_step": (st.d2h_bytes - d2h0) // args.steps,
-                "what": "wall clock of rs_replicate (plan+bind+kernel+unpack+complete) per step"},
+                "what": "wall clock of rs_replicate (plan+bind+kernel+unpack+complete) per step, "
+                        "version resident in the trainer's HBM"},
         "gpu_launches": args.steps * (1 + 1),  # pull_kernel + group unpack per step
         "clocks": clocks,
     }
+    if not (reshard or cast or args.no_host_e2e):
+        # End to end from HOST buffers, through the C ABI: the version is
+        # parked in pinned host memory (a retention offload, the reference's
+        # own host-resident copy) and every step the reader pulls it from
+        # there -- host->device bytes inside the timed region, the fill's
+        # status read back.  Same metric and workload as the device arm.
+        line["e2e"] = host_e2e(cl, t, r, stream, total, tarena, rarena, args)
+        line["e2e_device_resident"] = {"value": round(e2e, 2), "unit": UNIT,
+                                       "what": "rs_replicate wall clock, version in the trainer's HBM"}
     if not args.no_cpu:
         line["cpu_baseline"] = cpu_reference_run(shapes, args.cpu_bytes, args.cpu_reps)
     print(json.dumps(line), flush=True)
     cl.close()
+
+
+def host_e2e(cl, t, r, stream, total, tarena, rarena, args):
+    import torch
+
+    from paper_2604_09107_b200.ros import Status
+    dev = tarena.device
+    w = cl.open("m", "watcher", 1)
+    wt = torch.zeros(4096, dtype=torch.uint8, device=dev)
+    assert w.register_tensor(0, "w0", wt) == Status.ok
+    w.set_retention([0])
+    assert w.connect() == Status.ok
+    if r.is_published:
+        assert r.unpublish().status == Status.ok
+    r.invalidate()
+    assert t.unpublish().status == Status.ok  # parks v1 in pinned host memory
+    assert t.lanes() == [1]
+    walls = []
+    h2d0, d2h0 = r.stats().h2d_bytes, r.stats().d2h_bytes
+    for k in range(args.warmup + args.steps):
+        if r.is_published:
+            assert r.unpublish().status == Status.ok
+        r.invalidate()
+        torch.cuda.synchronize()
+        w0 = time.perf_counter()
+        res = r.replicate("1")
+        torch.cuda.synchronize()
+        if k >= args.warmup:
+            walls.append(time.perf_counter() - w0)
+        assert res.status == Status.ok, res
+        if k == 0:
+            h2d0, d2h0 = r.stats().h2d_bytes, r.stats().d2h_bytes
+            srcs = {a.src for a in cl.assigns() if a.replica == r.replica}
+            assert "trainer+offload@1" in srcs, srcs
+    if not args.no_verify:
+        assert torch.equal(tarena, rarena), "bytes pulled from the host offload differ"
+    st = r.stats()
+    steps = args.warmup + args.steps - 1
+    return {"value": round(total / statistics.mean(walls) / 1e9, 2), "unit": UNIT,
+            "h2d_bytes_per_step": total + (st.h2d_bytes - h2d0) // max(steps, 1),
+            "d2h_bytes_per_step": (st.d2h_bytes - d2h0) // max(steps, 1),
+            "what": "rs_replicate wall clock per step with the version in pinned HOST memory "
+                    "(a retention offload): every byte crosses host->device inside the timed "
+                    "region (PCIe), read by the pull kernel and verified; status read back"}
 
 
 def run_reference(args):
@@ -431,6 +485,8 @@ def main():
     ap.add_argument("--scenario", default="steady", choices=["steady", "elastic"],
                     help="elastic: config 4 (join at 50%% + version bump), N >= 3")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-host-e2e", action="store_true",
+                    help="skip the host-buffer end-to-end leg (N=1)")
     ap.add_argument("--cpu-bytes", type=int, default=2 << 30)
     ap.add_argument("--cpu-reps", type=int, default=3)
     args = ap.parse_args()
