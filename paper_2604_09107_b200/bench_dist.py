@@ -120,6 +120,9 @@ def run(args):
     assert total_landed == args.steps * receivers * total, (total_landed, total)
     hashes = dc.gather(None if args.no_verify else table_hash())
     verified = verified and (args.no_verify or all(x == hashes[0] for x in hashes))
+    host_e2e = None
+    if not pairs and not getattr(args, "no_host_e2e", False):
+        host_e2e = _dist_host_e2e(dc, h, reader, rank, dev, total, receivers, args)
     if rank == 0:
         per_rx = [round(total / (statistics.mean(a[1]) / 1e3) / 1e9, 2) for a in allv
                   if a[1] and statistics.mean(a[1]) > 0]
@@ -146,17 +149,72 @@ def run(args):
                          "alg_bytes_per_launch": total},
             "e2e": {"value": round(total_landed / wall_s / 1e9, 2), "unit": B.UNIT,
                     "h2d_bytes_per_step": None, "d2h_bytes_per_step": None,
-                    "what": "wall clock of the collective replicate (plan+bind+IPC exchange+kernel)"},
+                    "what": "wall clock of the collective replicate (plan+bind+IPC exchange+kernel), "
+                            "version resident in the trainer's HBM"},
             "gpu_launches": args.steps * receivers * 2,
             "clocks": allv[0][2] if allv[0][2].get("sm_mhz") else allv[1][2],
             "verified": verified,
         }
+        if host_e2e is not None:
+            line["e2e_device_resident"] = line["e2e"]
+            line["e2e"] = host_e2e
         if not args.no_cpu:
             line["cpu_baseline"] = B.cpu_reference_run(shapes, args.cpu_bytes, args.cpu_reps)
         print(json.dumps(line), flush=True)
     dist.barrier(group=dc.pg)
     dc.close()
     dist.destroy_process_group()
+
+
+def _dist_host_e2e(dc, h, reader, rank, dev, total, receivers, args):
+    """End to end from HOST buffers at N GPUs: the trainer's version is parked
+    in pinned host memory (a retention offload on GPU0's host) and the
+    readers replicate it: the first pulls it host->device over PCIe, the rest
+    chase along the NVLink chain.  Wall clock per step, max over ranks."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2604_09107_b200.ros import Status
+    w = None
+    if rank == 0:
+        w = dc.create("m", "watcher", 1)
+        assert w.register_tensor(0, "w0", torch.zeros(4096, dtype=torch.uint8, device=dev)) == 0
+        w.set_retention([0])
+    dc.open(w)
+    dc.unpublish(reader if (reader is not None and reader.is_published) else None)
+    r = dc.unpublish(h if rank == 0 else None)  # the last durable copy: parked in host memory
+    if rank == 0:
+        assert r.status == Status.ok and h.lanes() == [1], (r, h.lanes())
+    walls = []
+    h2d0 = d2h0 = 0
+    for k in range(args.warmup + args.steps):
+        dc.unpublish(reader if (reader is not None and reader.is_published) else None)
+        if reader is not None:
+            reader.invalidate()
+        dist.barrier(group=dc.pg)
+        torch.cuda.synchronize()
+        w0 = time.perf_counter()
+        res = dc.replicate(reader, "1")
+        torch.cuda.synchronize()
+        if k >= args.warmup:
+            walls.append(time.perf_counter() - w0)
+        if reader is not None:
+            assert res.status == Status.ok, res
+            if k == args.warmup - 1 or (args.warmup == 0 and k == 0):
+                h2d0, d2h0 = reader.stats().h2d_bytes, reader.stats().d2h_bytes
+    st = reader.stats() if reader is not None else None
+    src = {a.replica: a.src for a in dc.assigns() if a.version == 1}
+    per = dc.gather((sum(walls), None if st is None else (st.h2d_bytes - h2d0, st.d2h_bytes - d2h0)))
+    wall = max(p[0] for p in per) / max(len(walls), 1)
+    h2d = sum(p[1][0] for p in per if p[1]) // max(len(walls), 1)
+    d2h = sum(p[1][1] for p in per if p[1]) // max(len(walls), 1)
+    return {"value": round(receivers * total / wall / 1e9, 2), "unit": "GB/s",
+            "h2d_bytes_per_step": total + h2d, "d2h_bytes_per_step": d2h,
+            "first_source": src.get("rollout1"),
+            "what": "collective replicate wall clock per step with the version in pinned HOST "
+                    "memory (a retention offload): it crosses host->device (PCIe) inside the "
+                    "timed region into the first reader, the others chase it over NVLink; "
+                    "statuses read back; whole-job bytes / max-over-ranks time"}
 
 
 def run_ring(args):
