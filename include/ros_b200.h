@@ -147,6 +147,15 @@ int rs_unpublish(rs_handle* h);                              /* unpublish() */
  * Blocking; a parked replicate waits up to wait_s for a version to appear. */
 int rs_replicate(rs_handle* h, const char* spec, double wait_s, uint64_t* out_version);
 int rs_update(rs_handle* h, const char* spec, double wait_s, int* changed, uint64_t* out_version);
+/* The names SURVEY.md §8b recommends for this boundary: rs_pull = replicate;
+ * rs_release = drop a retention offload this handle holds for `version`;
+ * rs_serve_state exposes a shard's device serve tables (chunk digests,
+ * per-batch watermarks, current fill epoch: a batch is landed and verified
+ * when its watermark == epoch) so a caller can chain on them. */
+int rs_pull(rs_handle* h, const char* spec, double wait_s, uint64_t* out_version);
+int rs_release(rs_handle* h, uint64_t version);
+int rs_serve_state(rs_handle* h, uint32_t shard, uint64_t** digests, uint32_t** watermarks,
+                   uint32_t* epoch, uint32_t* n_batches);
 int rs_close(rs_handle* h);                                  /* close(); frees h */
 /* Plan view without side effects: the source `replica` would pull `shard`
  * of `spec` from right now. */

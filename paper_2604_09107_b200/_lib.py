@@ -62,6 +62,9 @@ _SIGS = {
     "rs_shard_local": (i32, [vp, u32]),
     "rs_set_retention": (i32, [vp, vp, sz]),
     "rs_connect": (i32, [vp]),
+    "rs_pull": (i32, [vp, cstr, dbl, C.POINTER(u64)]),
+    "rs_release": (i32, [vp, u64]),
+    "rs_serve_state": (i32, [vp, u32, C.POINTER(vp), C.POINTER(vp), C.POINTER(u32), C.POINTER(u32)]),
     "rs_offload_lanes": (i32, [vp, u64]),
     "rs_lane_export": (i32, [vp, u32, u64, vp, sz, C.POINTER(sz)]),
     "rs_offload_release": (i32, [vp, u64]),

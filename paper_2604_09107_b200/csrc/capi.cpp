@@ -281,6 +281,29 @@ int rs_replicate(rs_handle* h, const char* spec, double wait_s, uint64_t* out_ve
   return st(s);
 }
 
+int rs_pull(rs_handle* h, const char* spec, double wait_s, uint64_t* out_version) {
+  return rs_replicate(h, spec, wait_s, out_version);
+}
+
+int rs_release(rs_handle* h, uint64_t version) {
+  if (!h) return st(rsb::Status::invalid_argument);
+  h->client->release_lane(version);
+  return 0;
+}
+
+int rs_serve_state(rs_handle* h, uint32_t shard, uint64_t** digests, uint32_t** watermarks,
+                   uint32_t* epoch, uint32_t* n_batches) {
+  if (!h) return st(rsb::Status::invalid_argument);
+  std::uint64_t d = 0, f = 0;
+  std::uint32_t e = 0, nb = 0;
+  if (auto s = h->client->serve_tables(shard, &d, &f, &e, &nb); !rsb::ok(s)) return st(s);
+  if (digests) *digests = reinterpret_cast<uint64_t*>(d);
+  if (watermarks) *watermarks = reinterpret_cast<uint32_t*>(f);
+  if (epoch) *epoch = e;
+  if (n_batches) *n_batches = nb;
+  return 0;
+}
+
 int rs_update(rs_handle* h, const char* spec, double wait_s, int* changed, uint64_t* out_version) {
   rsb::VersionSpec vs;
   if (!h || !parse_spec(spec, &vs)) return st(rsb::Status::invalid_argument);

@@ -1832,6 +1832,17 @@ Status Client::settle_offload(OpOutcome* o, double wait_s) {
   return Status::ok;
 }
 
+Status Client::serve_tables(std::uint32_t shard, std::uint64_t* digests, std::uint64_t* flags,
+                            std::uint32_t* epoch, std::uint32_t* n_batches) const {
+  if (shard >= num_shards_ || !shards_[shard].holding) return Status::not_found;
+  const Payload& p = *shards_[shard].holding;
+  *digests = reinterpret_cast<std::uint64_t>(p.digests.p);
+  *flags = reinterpret_cast<std::uint64_t>(p.flags.p);
+  *epoch = p.epoch;
+  *n_batches = p.cmap.n_batches();
+  return Status::ok;
+}
+
 Result<std::string> Client::export_serve(std::uint32_t shard) {
   if (shard >= num_shards_) return Status::invalid_argument;
   return serves_->export_state(ServeRegistry::key(model_, replica_, shard));

@@ -276,6 +276,9 @@ class Client {
   Result<std::string> manifest_bytes(std::uint32_t shard) const;
   Status chunk_digests(std::uint32_t shard, std::vector<std::uint64_t>* out);
   Result<std::string> export_serve(std::uint32_t shard);
+  // The shard's device serve tables (rs_serve_state).
+  Status serve_tables(std::uint32_t shard, std::uint64_t* digests, std::uint64_t* flags,
+                      std::uint32_t* epoch, std::uint32_t* n_batches) const;
 
   // --- retention offload lanes (client_core.cpp:1675-1717) ------------------
   // Park version v of every local shard in pinned host memory and serve it as

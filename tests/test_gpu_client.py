@@ -280,3 +280,25 @@ def test_multi_gpu_chain_with_chasing():
             assert f.same("trainer", r, 0, "w") and f.same("trainer", r, 0, "norm")
     finally:
         f.close()
+
+
+def test_survey_abi_names_pull_serve_state(fx):
+    """rs_pull (= replicate) and rs_serve_state (the device tables a caller
+    chains on) from SURVEY.md §8b's recommended boundary."""
+    import ctypes as C
+    from paper_2604_09107_b200._lib import lib
+    from paper_2604_09107_b200.ros import Status
+    fx.make("t")
+    fx.reg("t", 0, "w", (3 << 20) + 123, 5)
+    assert fx.h["t"].publish(1).status == Status.ok
+    fx.make("r")
+    fx.reg("r", 0, "w", (3 << 20) + 123, 0)
+    v = C.c_uint64()
+    assert lib.rs_pull(fx.h["r"].h, b"latest", C.c_double(30.0), C.byref(v)) == 0 and v.value == 1
+    assert fx.same("t", "r", 0, "w")
+    d, f = C.c_void_p(), C.c_void_p()
+    ep, nb = C.c_uint32(), C.c_uint32()
+    assert lib.rs_serve_state(fx.h["r"].h, 0, C.byref(d), C.byref(f), C.byref(ep), C.byref(nb)) == 0
+    assert d.value and f.value and ep.value > 0
+    n_chunks = ((3 << 20) + 123 + 4095) // 4096
+    assert nb.value == (n_chunks + 31) // 32
