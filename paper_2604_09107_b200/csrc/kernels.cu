@@ -225,106 +225,117 @@ __global__ void __launch_bounds__(kThreads, 2) pull_kernel(const PullParams p) {
 }
 
 // ---------------------------------------------------------------- K6 -----
-// One warp per span.  XXH64 is serial within a span (each of the reference's
-// four accumulators, digest.cpp:89-95, is a dependent chain of round64), so a
-// span's digest is bound by the round latency (28 cycles on B200, measured by
-// tools/micro/xxh_chain.cu): lanes 0..3 run the four accumulators and must
-// never wait for data.  Lane 0 streams the span into a ring of 4 KiB slots
-// with one cp.async.bulk per slot (mbarrier completion), several slots ahead;
-// the accumulator lanes read their words from shared memory.  Lane 0 merges
-// and finalizes; the < 32-byte tail is read from global memory.  Spans that
-// are not 16-byte aligned take a per-lane cp.async path.
-constexpr int kDigWarps = 4;
+// XXH64 is serial within a span: each of the reference's four accumulators
+// (digest.cpp:89-95) is a dependent chain of round64, 28 cycles per round on
+// B200 (tools/micro/xxh_chain.cu), so a span hashes at most ~2.27 GB/s.  To
+// keep the chain itself the only thing on the critical path, a span gets a
+// warp pair:
+//   feeder warp   lane 0 streams the span through a ring of 4 KiB slots (one
+//                 cp.async.bulk per slot); all 32 lanes then replace every
+//                 word of a landed slot by its product w * P2 (the part of
+//                 round64 that does not depend on the accumulator)
+//   chain warp    lanes 0..3 run the four accumulators on the products,
+//                 acc = rotl(acc + p, 31) * P1, and free the slot
+// The chain lane 0 merges and finalizes; the < 32-byte tail is read from
+// global memory.  A span that is not 16-byte aligned is hashed by the chain
+// warp straight from global memory.
+constexpr int kDigSpans = 4;  // warp pairs per CTA
 constexpr int kDigSlot = 4096;
 constexpr int kDigSlots = 8;
 
-__device__ __forceinline__ void digest_rounds(const std::uint8_t* st, int lane, int cnt,
-                                              std::uint64_t& acc) {
-  // Software-pipelined: the loads and w * P2 products of the next 16
-  // stripes are issued in the bubbles of this group's dependent chain.
-  const std::uint8_t* p = st + 8 * lane;
-  int k = 0;
-  if (cnt >= 16) {
-    std::uint64_t cur[16];
-#pragma unroll
-    for (int j = 0; j < 16; ++j) cur[j] = *reinterpret_cast<const std::uint64_t*>(p + 32 * j) * kP2;
-    for (; k + 32 <= cnt; k += 16) {
-      std::uint64_t nxt[16];
-#pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        nxt[j] = *reinterpret_cast<const std::uint64_t*>(p + 32 * (k + 16 + j)) * kP2;
-        acc = xround_pre(acc, cur[j]);
-      }
-#pragma unroll
-      for (int j = 0; j < 16; ++j) cur[j] = nxt[j];
-    }
-#pragma unroll
-    for (int j = 0; j < 16; ++j) acc = xround_pre(acc, cur[j]);
-    k += 16;
-  }
-  for (; k < cnt; ++k) acc = xround(acc, *reinterpret_cast<const std::uint64_t*>(p + 32 * k));
-}
-
-__global__ void __launch_bounds__(kDigWarps * 32)
+__global__ void __launch_bounds__(kDigSpans * 64)
     span_digest_kernel(const std::uint64_t* ptrs, const std::uint64_t* lens, std::uint64_t* out,
                        int n) {
   extern __shared__ __align__(1024) std::uint8_t dsm[];
-  __shared__ __align__(8) unsigned long long bars[kDigWarps][kDigSlots];
+  __shared__ __align__(8) unsigned long long full[kDigSpans][kDigSlots];
+  __shared__ __align__(8) unsigned long long ready[kDigSpans][kDigSlots];
+  __shared__ __align__(8) unsigned long long empty[kDigSpans][kDigSlots];
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const int span = blockIdx.x * kDigWarps + warp;
+  const int pair = warp >> 1;
+  const bool feeder = (warp & 1) != 0;
+  const int span = blockIdx.x * kDigSpans + pair;
+  if (threadIdx.x == 0) {
+    for (int q = 0; q < kDigSpans; ++q)
+      for (int k = 0; k < kDigSlots; ++k) {
+        mbar_init(&full[q][k], 1);
+        mbar_init(&ready[q][k], 1);
+        mbar_init(&empty[q][k], 1);
+      }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
   if (span >= n) return;
-  std::uint8_t* ring = dsm + warp * (kDigSlots * kDigSlot);
+  std::uint8_t* ring = dsm + pair * (kDigSlots * kDigSlot);
   const std::uint8_t* base = reinterpret_cast<const std::uint8_t*>(ptrs[span]);
   const std::uint64_t len = lens[span];
   const std::uint64_t full_stripes = len >> 5;
-  std::uint64_t acc = lane == 0 ? kP1 + kP2 : lane == 1 ? kP2 : lane == 2 ? 0 : 0 - kP1;
   const std::uint64_t nslots = (len + kDigSlot - 1) / kDigSlot;
   constexpr int kSlotStripes = kDigSlot / 32;
-  if ((reinterpret_cast<std::uintptr_t>(base) & 15) == 0) {
-    unsigned long long* bar = bars[warp];
-    if (lane == 0) {
-      for (int k = 0; k < kDigSlots; ++k) mbar_init(&bar[k], 1);
-      asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-    }
-    __syncwarp();
-    auto issue = [&](std::uint64_t k) {  // lane 0: slot k of the span
-      unsigned long long* b = &bar[k % kDigSlots];
-      const std::uint64_t rem = len - k * kDigSlot;
-      const auto bytes = static_cast<unsigned>((rem < kDigSlot ? rem : kDigSlot) & ~15ull);
-      if (bytes) {
-        mbar_arrive_tx(b, bytes);
-        bulk_g2s(ring + (k % kDigSlots) * kDigSlot, base + k * kDigSlot, bytes, b);
-      } else {
-        mbar_arrive(b);
-      }
-    };
-    if (lane == 0)
-      for (std::uint64_t k = 0; k + 1 < kDigSlots && k < nslots; ++k) issue(k);
+  const bool aligned = (reinterpret_cast<std::uintptr_t>(base) & 15) == 0;
+  if (feeder) {
+    if (!aligned) return;
     for (std::uint64_t k = 0; k < nslots; ++k) {
-      if (lane == 0 && k + kDigSlots - 1 < nslots) {
-        fence_proxy_async_smem();  // the slot's previous words were read by the generic proxy
-        issue(k + kDigSlots - 1);
+      const int slot = static_cast<int>(k % kDigSlots);
+      const auto use = static_cast<unsigned>((k / kDigSlots) & 1);
+      if (k >= kDigSlots) mbar_wait(&empty[pair][slot], use ^ 1);  // chain done with it
+      std::uint8_t* st = ring + slot * kDigSlot;
+      if (lane == 0) {
+        const std::uint64_t rem = len - k * kDigSlot;
+        const auto bytes = static_cast<unsigned>((rem < kDigSlot ? rem : kDigSlot) & ~15ull);
+        fence_proxy_async_smem();  // products written there by the generic proxy
+        if (bytes) {
+          mbar_arrive_tx(&full[pair][slot], bytes);
+          bulk_g2s(st, base + k * kDigSlot, bytes, &full[pair][slot]);
+        } else {
+          mbar_arrive(&full[pair][slot]);
+        }
       }
-      mbar_wait(&bar[k % kDigSlots], static_cast<unsigned>((k / kDigSlots) & 1));
+      mbar_wait(&full[pair][slot], use);
+      // every word of the slot's whole stripes -> w * P2, in place
+      const std::uint64_t first = k * kSlotStripes;
+      const std::uint64_t cnt64 = full_stripes > first ? full_stripes - first : 0;
+      const int words = 4 * static_cast<int>(cnt64 < kSlotStripes ? cnt64 : kSlotStripes);
+      auto* w = reinterpret_cast<std::uint64_t*>(st);
+#pragma unroll 4
+      for (int x = lane; x < words; x += 32) w[x] *= kP2;
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&ready[pair][slot]);
+    }
+    return;
+  }
+  // chain warp
+  std::uint64_t acc = lane == 0 ? kP1 + kP2 : lane == 1 ? kP2 : lane == 2 ? 0 : 0 - kP1;
+  if (aligned) {
+    for (std::uint64_t k = 0; k < nslots; ++k) {
+      const int slot = static_cast<int>(k % kDigSlots);
+      mbar_wait(&ready[pair][slot], static_cast<unsigned>((k / kDigSlots) & 1));
       if (lane < 4) {
         const std::uint64_t first = k * kSlotStripes;
-        const std::uint64_t cnt = full_stripes > first ? full_stripes - first : 0;
-        digest_rounds(ring + (k % kDigSlots) * kDigSlot, lane,
-                      static_cast<int>(cnt < kSlotStripes ? cnt : kSlotStripes), acc);
+        const std::uint64_t c64 = full_stripes > first ? full_stripes - first : 0;
+        const int cnt = static_cast<int>(c64 < kSlotStripes ? c64 : kSlotStripes);
+        const std::uint8_t* pw = ring + slot * kDigSlot + 8 * lane;
+        int r = 0;
+        for (; r + 16 <= cnt; r += 16) {
+          std::uint64_t p[16];
+#pragma unroll
+          for (int j = 0; j < 16; ++j) p[j] = *reinterpret_cast<const std::uint64_t*>(pw + 32 * (r + j));
+#pragma unroll
+          for (int j = 0; j < 16; ++j) acc = xround_pre(acc, p[j]);
+        }
+        for (; r < cnt; ++r) acc = xround_pre(acc, *reinterpret_cast<const std::uint64_t*>(pw + 32 * r));
       }
       __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[pair][slot]);
     }
-  } else {
-    // unaligned span: per-lane stripe words straight from global memory
-    if (lane < 4)
-      for (std::uint64_t k = 0; k < full_stripes; ++k) {
-        std::uint64_t w = 0;
-        const std::uint8_t* q = base + 32 * k + 8 * lane;
+  } else if (lane < 4) {
+    for (std::uint64_t k = 0; k < full_stripes; ++k) {
+      std::uint64_t w = 0;
+      const std::uint8_t* q = base + 32 * k + 8 * lane;
 #pragma unroll
-        for (int b = 0; b < 8; ++b) w |= std::uint64_t(q[b]) << (8 * b);
-        acc = xround(acc, w);
-      }
+      for (int b = 0; b < 8; ++b) w |= std::uint64_t(q[b]) << (8 * b);
+      acc = xround(acc, w);
+    }
   }
   const std::uint64_t a = __shfl_sync(0xffffffffu, acc, 0);
   const std::uint64_t b = __shfl_sync(0xffffffffu, acc, 1);
@@ -488,7 +499,7 @@ cudaError_t launch_pull(const PullParams& p, int sms, cudaStream_t s) {
 cudaError_t launch_span_digests(const std::uint64_t* ptrs, const std::uint64_t* lens,
                                 std::uint64_t* out, int n, cudaStream_t s) {
   if (n <= 0) return cudaSuccess;
-  constexpr int smem = kDigWarps * kDigSlots * kDigSlot;
+  constexpr int smem = kDigSpans * kDigSlots * kDigSlot;
   static bool attr_done[64] = {};
   int dev = 0;
   cudaGetDevice(&dev);
@@ -498,7 +509,7 @@ cudaError_t launch_span_digests(const std::uint64_t* ptrs, const std::uint64_t* 
     if (e != cudaSuccess) return e;
     attr_done[dev] = true;
   }
-  span_digest_kernel<<<(n + kDigWarps - 1) / kDigWarps, kDigWarps * 32, smem, s>>>(ptrs, lens,
+  span_digest_kernel<<<(n + kDigSpans - 1) / kDigSpans, kDigSpans * 64, smem, s>>>(ptrs, lens,
                                                                                    out, n);
   return cudaGetLastError();
 }
