@@ -814,8 +814,17 @@ Status Client::alloc_tables(Shard& sh, Payload& p, std::uint32_t extra_chunks) {
   DeviceGuard g(sh.device);
   const std::uint32_t nc = p.cmap.n_chunks() + extra_chunks;
   const std::uint32_t nb = (nc + dev::kBatchChunks - 1) / dev::kBatchChunks;
-  if (Status s = p.digests.alloc(sh.device, std::size_t(nc) * 8); !ok(s)) return s;
-  if (Status s = p.flags.alloc(sh.device, std::size_t(nb) * 4); !ok(s)) return s;
+  if (sh.holding && sh.holding.get() != &p && sh.holding->digests.n >= std::size_t(nc) * 8 &&
+      sh.holding->flags.n >= std::size_t(nb) * 4) {
+    // The payload being replaced has drained (an unpublish or update settles
+    // only with no readers left): keep its tables -- same allocations, so
+    // the IPC mappings other processes hold stay valid and nothing re-pins.
+    p.digests = std::move(sh.holding->digests);
+    p.flags = std::move(sh.holding->flags);
+  } else {
+    if (Status s = p.digests.alloc(sh.device, std::size_t(nc) * 8); !ok(s)) return s;
+    if (Status s = p.flags.alloc(sh.device, std::size_t(nb) * 4); !ok(s)) return s;
+  }
   RS_CUDA(cudaMemsetAsync(p.flags.p, 0, std::size_t(nb) * 4, sh.stream));
   RS_CUDA(cudaMemsetAsync(p.digests.p, 0, std::size_t(nc) * 8, sh.stream));
   return Status::ok;
