@@ -92,6 +92,15 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(sm), "source": "nvml"}
 
 
+# NVLink 5 user-data bounds for SM-driven pulls, from the ncu nvlrx/nvltx
+# counters of the pull kernel (profiles/r1/ncu_nvlink_counters.json): read
+# responses add 12.5% protocol bytes on the wire, read requests 18.75% of the
+# pulled bytes in the opposite direction.  One direction busy: 900/1.125;
+# both directions busy (a chain's middle GPUs): 900/(1.125+0.1875).
+NVL_ONE_WAY = 900.0 / 1.125
+NVL_BOTH_WAYS = 900.0 / (1.125 + 0.1875)
+
+
 def measured_peaks() -> dict:
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):

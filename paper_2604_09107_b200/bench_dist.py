@@ -146,7 +146,17 @@ def run(args):
                          "traffic": B.ncu_traffic("nvlink"), "peak_src": "nominal NVLink5 per direction "
                          "(measured peer copy 777 GB/s)", "kernel": "pull_tma_kernel",
                          "kernel_ms_avg": round(statistics.mean(step_dev_ms), 3),
-                         "alg_bytes_per_launch": total},
+                         "alg_bytes_per_launch": total,
+                         # link-level accounting from ncu nvlrx/nvltx counters
+                         # (profiles/r1/ncu_nvlink_counters.json): read
+                         # responses carry 12.5% protocol, read requests 18.75%
+                         # of the data in the other direction
+                         "protocol_peak_per_receiver": [
+                             round(B.NVL_ONE_WAY if i == receivers - 1 else B.NVL_BOTH_WAYS, 1)
+                             for i in range(receivers)],
+                         "protocol_frac": round(statistics.mean(
+                             x / (B.NVL_ONE_WAY if i == len(per_rx) - 1 else B.NVL_BOTH_WAYS)
+                             for i, x in enumerate(per_rx)), 4)},
             "e2e": {"value": round(total_landed / wall_s / 1e9, 2), "unit": B.UNIT,
                     "h2d_bytes_per_step": None, "d2h_bytes_per_step": None,
                     "what": "wall clock of the collective replicate (plan+bind+IPC exchange+kernel), "
