@@ -335,7 +335,7 @@ def run_single(args):
     torch.cuda.synchronize()
     clk.start()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    kernel_ms, walls = [], []
+    kernel_ms, walls, fill_ms = [], [], []
     pulled0 = r.stats().bytes_pulled
     h2d0, d2h0 = r.stats().h2d_bytes, r.stats().d2h_bytes
     ev0.record(stream)
@@ -348,6 +348,7 @@ def run_single(args):
         # single reader shard: the pull kernel's own CUDA-event time; reshard:
         # the step's device time on the shards' stream (both shard kernels)
         kernel_ms.append(r.stats().last_pull_ms if not reshard else e_a.elapsed_time(e_b))
+        fill_ms.append(r.stats().fill_sum_ms)  # the pull kernels alone (CUDA events)
     ev1.record(stream)
     torch.cuda.synchronize()
     clocks = clk.stop()
@@ -361,12 +362,17 @@ def run_single(args):
     value = landed / (dev_ms / 1e3) / 1e9
     e2e = landed / sum(walls) / 1e9
     k_avg = statistics.mean(kernel_ms)
+    fills_per_step = r.num_shards if reshard else 1
+    fill_avg = statistics.mean(fill_ms) / fills_per_step  # one pull launch
     n_chunks = sum((2 * _numel(s) + args.chunk - 1) // args.chunk for _, s in shapes)
     # algorithmic bytes per launch: read source + write destination + read the
     # source chunk table + write own table + watermark words
     alg = (total + total // 2 if cast else 2 * total) + 16 * n_chunks + 4 * ((n_chunks + 31) // 32)
     peaks = measured_peaks()
-    achieved = alg / (k_avg / 1e3) / 1e9
+    # reshard: the roofline is the pull kernel's (one launch per reader shard,
+    # alg / shards each); the step adds the slice copies, group packing and
+    # host work between launches (step_frac)
+    achieved = (alg / fills_per_step) / (fill_avg / 1e3) / 1e9 if reshard else alg / (k_avg / 1e3) / 1e9
     line = {
         "metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": 1, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(dev_ms / args.steps, 3), "higher_is_better": True,
@@ -384,8 +390,12 @@ def run_single(args):
                      "unit": "GB/s", "frac": round(achieved / peaks["hbm_gbs"], 4),
                      "traffic": ncu_traffic("cast" if cast else "local") if not reshard else None,
                      "peak_src": peaks["src"],
-                     "kernel": "pull_tma_kernel", "kernel_ms_avg": round(k_avg, 3),
-                     "alg_bytes_per_launch": alg},
+                     "kernel": "pull_tma_kernel",
+                     "kernel_ms_avg": round(fill_avg if reshard else k_avg, 3),
+                     "alg_bytes_per_launch": alg // fills_per_step,
+                     **({"step_ms": round(k_avg, 3), "launches_per_step": fills_per_step,
+                         "step_frac": round(alg / (k_avg / 1e3) / 1e9 / peaks["hbm_gbs"], 4)}
+                        if reshard else {})},
         "e2e": {"value": round(e2e, 2), "unit": UNIT,
                 "h2d_bytes_per_step": (st.h2d_bytes - h2d0) // args.steps,
                 "d2h_bytes_per_step": (st.d2h_bytes - d2h0) // args.steps,

@@ -258,6 +258,21 @@ DevBuf::~DevBuf() {
   }
 }
 
+namespace {
+// RSB_TIMING=1: host wall time of the replicate phases on stderr (diagnostic)
+struct PhaseClock {
+  bool on = std::getenv("RSB_TIMING") != nullptr;
+  std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+  void mark(const char* what) {
+    if (!on) return;
+    auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[rsb] %s %.3f ms\n", what,
+                 std::chrono::duration<double, std::milli>(now - t).count());
+    t = now;
+  }
+};
+}  // namespace
+
 Status DevBuf::alloc(int device, std::size_t bytes) {
   if (p && n >= bytes && dev == device) return Status::ok;
   if (p) {
@@ -1336,6 +1351,7 @@ std::vector<Client::FillOutcome> Client::wait_shards(const std::vector<std::uint
   std::vector<dev::PullStatus> st(num_shards_);
   stats_.fill_max_ms = stats_.fill_sum_ms = 0;
   stats_.fill_bytes = 0;
+  PhaseClock wc;
   for (std::uint32_t i : which) {
     if (!launched[i]) continue;
     Shard& sh = shards_[i];
@@ -1391,13 +1407,16 @@ std::vector<Client::FillOutcome> Client::wait_shards(const std::vector<std::uint
         break;
     }
   }
+  wc.mark("wait kernels");
   // Unpack verified groups into their members (K3, unpack_group); a reshard
   // fill instead slices the gathered items and packs its own groups.
   for (std::uint32_t i : which) {
     if (!ok(out[i].status)) continue;
     Shard& sh = shards_[i];
     if (sh.holding->reshard) {
+      PhaseClock fc;
       if (Status s = finish_reshard(sh); !ok(s)) out[i] = {s, 0, 0};
+      fc.mark("finish_reshard");
       continue;
     }
     const auto& p = *sh.holding;
@@ -1410,6 +1429,8 @@ std::vector<Client::FillOutcome> Client::wait_shards(const std::vector<std::uint
         ls.push_back(p.manifest.entries[mem.entry].length | (r.cast ? dev::kSpanCastE4M3 : 0));
       }
     if (Status s = copy_spans(sh, srcs, dsts, ls); !ok(s)) out[i] = {s, 0, 0};
+    if (!srcs.empty() && cudaStreamSynchronize(sh.stream) != cudaSuccess)
+      out[i] = {Status::transfer_failed, 0, 0};
   }
   return out;
 }
@@ -1417,9 +1438,12 @@ std::vector<Client::FillOutcome> Client::wait_shards(const std::vector<std::uint
 Status Client::copy_spans(Shard& sh, const std::vector<std::uint64_t>& srcs,
                           const std::vector<std::uint64_t>& dsts,
                           const std::vector<std::uint64_t>& lens) {
+  // Stream-ordered: returns once the copy is queued on sh.stream (callers
+  // synchronize).  The span tables live in sh.span_tables; a later call's
+  // upload is ordered behind this call's kernel on the same stream.
   if (srcs.empty()) return Status::ok;
   DeviceGuard g(sh.device);
-  DevBuf t;
+  DevBuf& t = sh.span_tables;
   const std::size_t n = srcs.size();
   std::vector<std::uint64_t> host(4 * n);
   std::uint64_t tiles = 0;
@@ -1435,7 +1459,6 @@ Status Client::copy_spans(Shard& sh, const std::vector<std::uint64_t>& srcs,
   RS_CUDA(cudaMemcpyAsync(d, host.data(), 4 * n * 8, cudaMemcpyHostToDevice, sh.stream));
   RS_CUDA(dev::launch_copy_spans(d, d + n, d + 2 * n, d + 3 * n, static_cast<int>(n), tiles,
                                  sh.stream));
-  RS_CUDA(cudaStreamSynchronize(sh.stream));
   stats_.h2d_bytes += 32 * n;
   return Status::ok;
 }
@@ -1600,7 +1623,10 @@ void Client::finish_transfers(VersionId v, bool good) {
 
 Status Client::run_replicate_loop(const OpOutcome& o, VersionId v) {
   std::vector<Assignment> as = o.assignments;
-  if (Status s = bind_all(as, v); !ok(s)) {
+  PhaseClock pc;
+  Status bs = bind_all(as, v);
+  pc.mark("bind");
+  if (Status s = bs; !ok(s)) {
     for (std::uint32_t i = 0; i < num_shards_; ++i) reg_->complete(model_, replica_, i, s);
     finish_transfers(v, false);
     return s;
@@ -1609,7 +1635,10 @@ Status Client::run_replicate_loop(const OpOutcome& o, VersionId v) {
   std::vector<std::uint32_t> pending;
   for (std::uint32_t i = 0; i < num_shards_; ++i) pending.push_back(i);
   while (!pending.empty()) {
-    auto res = fill_shards(as, pending);
+    launch_shards(as, pending);
+    pc.mark("launch");
+    auto res = wait_shards(pending);
+    pc.mark("wait+finish");
     std::vector<std::uint32_t> next;
     for (std::uint32_t i : pending) {
       if (ok(res[i].status)) {
@@ -1636,6 +1665,7 @@ Status Client::run_replicate_loop(const OpOutcome& o, VersionId v) {
   }
   finish_transfers(v, true);
   for (std::uint32_t i = 0; i < num_shards_; ++i) reg_->complete(model_, replica_, i, Status::ok);
+  pc.mark("complete");
   return Status::ok;
 }
 

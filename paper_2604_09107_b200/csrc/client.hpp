@@ -348,6 +348,7 @@ class Client {
                                 // the fill plan stays resident between fills
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     cudaStream_t poll = nullptr;  // progress reads while a fill runs
+    DevBuf span_tables;           // copy_spans' span tables (grow-only: no per-call malloc/free)
     std::uint32_t epoch_ctr = 0;
     struct Lane {
       std::string key;

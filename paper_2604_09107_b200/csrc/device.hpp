@@ -97,7 +97,15 @@ struct PullParams {
   const void* maps;                  // CUtensorMap pairs per segment (or null)
   const std::uint32_t* batch_seg;    // per batch: last segment with chunk0 <= 32*batch
   std::uint32_t remote;              // some source is another GPU's HBM (kernel shape choice)
-  std::uint32_t pad;
+  // Schedule: positions 0..n_sched-1 map to batches order[pos] (first_batch
+  // then unused); null order: batches first_batch..n_batches-1 in order.
+  // The order lists only batches some segment touches (a hash pass over a
+  // few items of a large payload walks just those), and with several sources
+  // interleaves their batches in proportion to their counts, so every
+  // source's link (and the local HBM) stays busy for the whole pull instead
+  // of one source at a time.
+  std::uint32_t n_sched;
+  const std::uint32_t* order;
 };
 
 // Uploads a pull plan (segment table + source table + TMA tensor maps +
@@ -122,6 +130,10 @@ cudaError_t upload_pull_plan(int device, cudaStream_t s, ItemDesc* items, std::u
                              const SrcDesc* srcs, std::uint32_t n_srcs, std::uint32_t n_chunks,
                              PlanUpload* up, PullParams* p);
 void free_pull_plan(int device, PlanUpload* up);
+// The schedule order of a plan (see PullParams.order; empty: every batch,
+// in order).  `bseg`: per batch, the segment holding its first chunk.
+std::vector<std::uint32_t> schedule_order(const ItemDesc* items, std::uint32_t n,
+                                          const std::vector<std::uint32_t>& bseg);
 
 // Fused mover: copy + per-chunk XXH64 verify + watermark publish.  `sms` is
 // the device's SM count (pull_grid); the persistent grid is sized from it.

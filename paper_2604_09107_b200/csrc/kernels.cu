@@ -102,9 +102,10 @@ __global__ void __launch_bounds__(kThreads, 2) pull_kernel(const PullParams p) {
 
   for (;;) {
     std::uint32_t b = 0;
-    if (lane == 0) b = atomicAdd(&p.work[0], 1u) + p.first_batch;
+    if (lane == 0) b = atomicAdd(&p.work[0], 1u) + (p.order ? 0u : p.first_batch);
     b = __shfl_sync(full, b, 0);
-    if (b >= p.n_batches) break;
+    if (b >= (p.order ? p.n_sched : p.n_batches)) break;
+    if (p.order) b = __ldg(&p.order[b]);
     if (ld_volatile(&p.work[1])) break;
     if (p.resume && ld_volatile(&p.dst_flags[b]) == p.dst_epoch) continue;  // landed already
     const std::uint32_t c = b * kBatchChunks + lane;
@@ -477,7 +478,7 @@ int pull_grid(int device) {
 const char* pull_kernel_name() { return use_ldg_kernel() ? "pull_kernel" : "pull_tma_kernel"; }
 
 cudaError_t launch_pull(const PullParams& p, int sms, cudaStream_t s) {
-  if (p.n_batches <= p.first_batch) return cudaSuccess;
+  if (p.order ? p.n_sched == 0 : p.n_batches <= p.first_batch) return cudaSuccess;
   if (!use_ldg_kernel()) return launch_pull_tma(p, sms, s);
   static bool attr_done[64] = {};
   int dev = 0;
@@ -488,7 +489,7 @@ cudaError_t launch_pull(const PullParams& p, int sms, cudaStream_t s) {
     if (e != cudaSuccess) return e;
     attr_done[dev] = true;
   }
-  const std::uint32_t todo = p.n_batches - p.first_batch;
+  const std::uint32_t todo = p.order ? p.n_sched : p.n_batches - p.first_batch;
   const std::uint32_t need = (todo + kWarps - 1) / kWarps;
   int grid = 2 * sms;
   if (static_cast<std::uint32_t>(grid) > need) grid = static_cast<int>(need);

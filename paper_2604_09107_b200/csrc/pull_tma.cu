@@ -23,8 +23,10 @@
 //    regions): one padded slot of P+16 bytes per chunk, every lane issuing
 //    its own cp.async.bulk copy (plain loads/stores for unaligned bytes).
 //
-//   producer  walks its batches (static schedule b = pipeline + k*pipelines, so
-//             the landed prefix advances front to back), waits the source
+//   producer  walks its batches (static schedule: position pipeline +
+//             k*pipelines of the plan's order -- batch order, or with several
+//             sources their batches interleaved -- so each source's landed
+//             prefix advances front to back), waits the source
 //             watermark(s) when a source is still filling, fills stages.
 //   consumer  per stage: lands the stage (tensor store / bulk stores), hashes
 //             (XXH64 32-byte stripes), frees the stage once the stores have
@@ -170,8 +172,11 @@ __global__ void __launch_bounds__(C::kThreads, C::kCtas) pull_tma_kernel(const P
     int stage = 0;
     unsigned phase = 0;
     std::uint32_t abort_seen = 0;
-    for (std::uint32_t b = p.first_batch + vcta; b < p.n_batches; b += vgrid) {
+    const std::uint32_t* order = p.order;
+    const std::uint32_t pos_end = order ? p.n_sched : p.n_batches;
+    for (std::uint32_t pos = (order ? 0 : p.first_batch) + vcta; pos < pos_end; pos += vgrid) {
       if (abort_seen) break;
+      const std::uint32_t b = order ? __ldg(&order[pos]) : pos;
       const std::uint32_t abort_next = ld_volatile(&p.work[1]);  // acted on next batch
       if (p.resume && ld_volatile(&p.dst_flags[b]) == p.dst_epoch) {  // landed already
         abort_seen = abort_next;
@@ -545,7 +550,7 @@ cudaError_t launch_variant(const PullParams& p, int sms, cudaStream_t s) {
     if (e != cudaSuccess) return e;
     attr_done[dev] = true;
   }
-  const std::uint32_t todo = p.n_batches - p.first_batch;
+  const std::uint32_t todo = p.order ? p.n_sched : p.n_batches - p.first_batch;
   int grid = sms * C::kCtas;
   const auto per = static_cast<std::uint32_t>(C::kPipes);
   if (static_cast<std::uint32_t>(grid) * per > todo) grid = static_cast<int>((todo + per - 1) / per);

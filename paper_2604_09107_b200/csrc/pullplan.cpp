@@ -1,8 +1,12 @@
 // Host side of a pull launch: segment table + source table + TMA tensor maps
-// + work/status words, uploaded in one H2D copy.
+// + batch -> segment table + schedule order + work/status words, uploaded in
+// one H2D copy.
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
+#include <cstdio>
+#include <map>
 #include <cstdlib>
 #include <cstring>
 #include <vector>
@@ -62,7 +66,98 @@ bool maps_disabled() {
   return v;
 }
 
+bool plan_debug() {
+  static const bool v = std::getenv("RSB_PLAN_STATS") != nullptr;  // diagnostic knob
+  return v;
+}
+
+// How the kernel will take each batch (box: one tensor load per 128-byte
+// column of a whole-chunk batch; slot: per-lane bulk copies), by bytes.
+void print_plan_stats(const ItemDesc* items, std::uint32_t n, const std::vector<std::uint32_t>& bseg,
+                      std::uint32_t n_chunks) {
+  std::uint64_t box_b = 0, slot_b = 0, box_n = 0, slot_n = 0, band_b = 0;
+  std::map<std::uint32_t, std::uint64_t> by_len;
+  for (std::uint32_t b = 0; b < bseg.size(); ++b) {
+    const std::uint32_t s0 = bseg[b];
+    const ItemDesc& d = items[s0];
+    const std::uint32_t c = d.chunk_len & kChunkLenMask;
+    const std::uint32_t k0 = b * kBatchChunks - d.chunk0;
+    const std::uint64_t full = c ? d.len / c : 0;
+    const bool whole = k0 + kBatchChunks <= full && b * kBatchChunks + kBatchChunks <= n_chunks &&
+                       (s0 + 1 >= n || items[s0 + 1].chunk0 >= (b + 1) * kBatchChunks);
+    const bool box = (d.chunk_len & kHasMap) && whole && (k0 % (d.q ? d.q : 1)) == 0;
+    std::uint64_t bytes = 0;
+    for (std::uint32_t l = 0; l < kBatchChunks; ++l) {
+      const std::uint32_t ch = b * kBatchChunks + l;
+      if (ch >= n_chunks) break;
+      std::uint32_t sg = s0;
+      while (sg + 1 < n && items[sg + 1].chunk0 <= ch) ++sg;
+      const ItemDesc& e = items[sg];
+      const std::uint32_t cl = e.chunk_len & kChunkLenMask;
+      const std::uint64_t k = ch - e.chunk0;
+      if (cl == 0 || k * cl >= e.len) continue;
+      bytes += std::min<std::uint64_t>(cl, e.len - k * cl);
+    }
+    (box ? box_b : slot_b) += bytes;
+    (box ? box_n : slot_n) += 1;
+    if (box && (d.chunk_len & kMap3D)) band_b += bytes;
+    by_len[c] += bytes;
+  }
+  std::fprintf(stderr, "[rsb] plan: %u segments, %zu batches: box %llu (%.3f GB, %.3f GB column bands), "
+               "slot %llu (%.3f GB)\n[rsb] plan: bytes by chunk length:",
+               n, bseg.size(), (unsigned long long)box_n, box_b / 1e9, band_b / 1e9,
+               (unsigned long long)slot_n, slot_b / 1e9);
+  for (const auto& [len, bytes] : by_len) std::fprintf(stderr, " %u:%.3fGB", len, bytes / 1e9);
+  std::fprintf(stderr, "\n");
+}
+
 }  // namespace
+
+std::vector<std::uint32_t> schedule_order(const ItemDesc* items, std::uint32_t n,
+                                          const std::vector<std::uint32_t>& bseg) {
+  // Batches no segment touches are left out.  Class of a batch = the source
+  // of its first chunk.  Batch b, the r-th of its class's n_c batches, is
+  // scheduled at key (r + 1/2) / n_c: every class advances through its
+  // batches at the same fractional rate and each class keeps its own
+  // front-to-back order (what a chaser downstream waits on).  Ties go to the
+  // lower batch.
+  static const bool no_mix = std::getenv("RSB_BATCH_ORDER") &&
+                             std::getenv("RSB_BATCH_ORDER")[0] == '0';  // A/B knob
+  const std::uint32_t nb = static_cast<std::uint32_t>(bseg.size());
+  std::vector<std::uint8_t> touched(nb, 0);
+  for (std::uint32_t i = 0; i < n; ++i) {
+    const std::uint64_t c = items[i].chunk_len & kChunkLenMask;
+    if (c == 0 || items[i].len == 0) continue;
+    const std::uint64_t last = items[i].chunk0 + (items[i].len + c - 1) / c - 1;
+    for (std::uint64_t b = items[i].chunk0 / kBatchChunks; b <= last / kBatchChunks && b < nb; ++b)
+      touched[b] = 1;
+  }
+  std::vector<std::uint32_t> cls(nb), count;
+  std::uint32_t n_touched = 0;
+  for (std::uint32_t b = 0; b < nb; ++b) {
+    if (!touched[b]) continue;
+    ++n_touched;
+    const std::uint32_t c = no_mix ? 0 : items[bseg[b]].src_id;
+    cls[b] = c;
+    if (c >= count.size()) count.resize(c + 1, 0);
+    ++count[c];
+  }
+  int classes = 0;
+  for (std::uint32_t c : count) classes += c != 0;
+  if (classes < 2 && n_touched == nb) return {};
+  std::vector<std::uint32_t> rank(count.size(), 0);
+  std::vector<std::pair<double, std::uint32_t>> key;
+  key.reserve(n_touched);
+  for (std::uint32_t b = 0; b < nb; ++b) {
+    if (!touched[b]) continue;
+    const std::uint32_t c = cls[b];
+    key.push_back({(rank[c]++ + 0.5) / count[c], b});
+  }
+  if (classes > 1) std::sort(key.begin(), key.end());
+  std::vector<std::uint32_t> order(key.size());
+  for (std::size_t i = 0; i < key.size(); ++i) order[i] = key[i].second;
+  return order;
+}
 
 cudaError_t upload_pull_plan(int device, cudaStream_t s, ItemDesc* items, std::uint32_t n,
                              const SrcDesc* srcs, std::uint32_t n_srcs, std::uint32_t n_chunks,
@@ -87,6 +182,8 @@ cudaError_t upload_pull_plan(int device, cudaStream_t s, ItemDesc* items, std::u
     p->n_chunks = b.n_chunks;
     p->n_batches = b.n_batches;
     p->has_cast = b.has_cast;
+    p->order = b.order;
+    p->n_sched = b.n_sched;
     return cudaSuccess;
   }
   std::vector<ItemDesc> key(items, items + n);  // the request, before flags are added below
@@ -94,7 +191,15 @@ cudaError_t upload_pull_plan(int device, cudaStream_t s, ItemDesc* items, std::u
   const std::size_t srcs_off = items_off + n * sizeof(ItemDesc);
   const std::size_t maps_off = (srcs_off + n_srcs * sizeof(SrcDesc) + 255) / 256 * 256;
   const std::size_t bseg_off = maps_off + std::size_t(n) * 256;
-  const std::size_t total = bseg_off + std::size_t(n_batches) * 4;
+  // batch -> last segment starting at or before the batch's first chunk
+  std::vector<std::uint32_t> bseg(n_batches);
+  for (std::uint32_t b = 0, sgi = 0; b < n_batches; ++b) {
+    while (sgi + 1 < n && items[sgi + 1].chunk0 <= b * kBatchChunks) ++sgi;
+    bseg[b] = sgi;
+  }
+  const std::vector<std::uint32_t> order = schedule_order(items, n, bseg);
+  const std::size_t order_off = bseg_off + std::size_t(n_batches) * 4;
+  const std::size_t total = order_off + order.size() * 4;
   if (up->scratch_bytes < total) {
     if (up->scratch) cudaFree(up->scratch);
     up->scratch = nullptr;
@@ -132,12 +237,9 @@ cudaError_t upload_pull_plan(int device, cudaStream_t s, ItemDesc* items, std::u
   }
   std::memcpy(host.data() + items_off, items, n * sizeof(ItemDesc));
   if (n_srcs) std::memcpy(host.data() + srcs_off, srcs, n_srcs * sizeof(SrcDesc));
-  // batch -> last segment starting at or before the batch's first chunk
-  auto* bseg = reinterpret_cast<std::uint32_t*>(host.data() + bseg_off);
-  for (std::uint32_t b = 0, sgi = 0; b < n_batches; ++b) {
-    while (sgi + 1 < n && items[sgi + 1].chunk0 <= b * kBatchChunks) ++sgi;
-    bseg[b] = sgi;
-  }
+  if (n_batches) std::memcpy(host.data() + bseg_off, bseg.data(), std::size_t(n_batches) * 4);
+  if (!order.empty()) std::memcpy(host.data() + order_off, order.data(), order.size() * 4);
+  if (plan_debug()) print_plan_stats(items, n, bseg, n_chunks);
   auto* base = static_cast<std::uint8_t*>(up->scratch);
   cudaError_t e;
   if (up->last.size() == total && std::memcmp(up->last.data(), host.data(), total) == 0) {
@@ -160,6 +262,8 @@ cudaError_t upload_pull_plan(int device, cudaStream_t s, ItemDesc* items, std::u
   p->n_chunks = n_chunks;
   p->has_cast = any_cast;
   p->n_batches = n_batches;
+  p->order = order.empty() ? nullptr : reinterpret_cast<const std::uint32_t*>(base + order_off);
+  p->n_sched = static_cast<std::uint32_t>(order.size());
   up->built = *p;
   up->key_items = std::move(key);
   up->key_srcs.assign(srcs, srcs + n_srcs);
