@@ -99,11 +99,8 @@ struct PullParams {
   std::uint32_t remote;              // some source is another GPU's HBM (kernel shape choice)
   // Schedule: positions 0..n_sched-1 map to batches order[pos] (first_batch
   // then unused); null order: batches first_batch..n_batches-1 in order.
-  // The order lists only batches some segment touches (a hash pass over a
-  // few items of a large payload walks just those), and with several sources
-  // interleaves their batches in proportion to their counts, so every
-  // source's link (and the local HBM) stays busy for the whole pull instead
-  // of one source at a time.
+  // The order lists only the batches some segment touches: a hash pass over
+  // a few items of a large payload walks just those.
   std::uint32_t n_sched;
   const std::uint32_t* order;
 };

@@ -24,8 +24,7 @@
 //    its own cp.async.bulk copy (plain loads/stores for unaligned bytes).
 //
 //   producer  walks its batches (static schedule: position pipeline +
-//             k*pipelines of the plan's order -- batch order, or with several
-//             sources their batches interleaved -- so each source's landed
+//             k*pipelines of the plan's batches in order, so the landed
 //             prefix advances front to back), waits the source
 //             watermark(s) when a source is still filling, fills stages.
 //   consumer  per stage: lands the stage (tensor store / bulk stores), hashes
@@ -75,8 +74,9 @@ __device__ __forceinline__ void tensor_store_2d(const void* map, int x, int y, c
       : "memory");
 }
 
-template <int P, int S, int CTAS, int ITEMS, int PIPES = 1>
+template <int P, int S, int CTAS, int ITEMS, int PIPES = 1, int REL = 4>
 struct Cfg {
+  static constexpr int kRelease = REL;  // verified batches per watermark release (one sys fence)
   static constexpr int kPipes = PIPES;  // producer/consumer pairs per CTA
   static constexpr int kThreads = 64 * PIPES;
   static constexpr int kP = P;
@@ -332,7 +332,7 @@ __global__ void __launch_bounds__(C::kThreads, C::kCtas) pull_tma_kernel(const P
     std::uint64_t v1 = 0, v2 = 0, v3 = 0, v4 = 0, digest = 0;
     // Verified batches whose watermarks await their stores.  Released
     // kRelease at a time: one system-scope fence per group of flags.
-    constexpr int kRelease = 4;
+    constexpr int kRelease = C::kRelease;
     std::uint32_t pend[kRelease];
     int npend = 0;
     std::uint64_t pend_bytes = 0, done_bytes = 0;
@@ -569,6 +569,8 @@ using V7 = Cfg<512, 3, 1, 0, 4>;    // one CTA per SM: 4 pipelines, consumers on
 using V8 = Cfg<512, 2, 1, 320, 4>;  // 4 two-stage pipelines + the segment table in smem
 using V9 = Cfg<256, 4, 1, 320, 4>;  // 4 four-stage pipelines of 256-byte pieces
 using V10 = Cfg<256, 5, 1, 128, 4>;
+using V11 = Cfg<512, 2, 1, 320, 4, 8>;   // V8, releasing 8 batches per fence
+using V12 = Cfg<512, 2, 1, 320, 4, 16>;  // V8, releasing 16 batches per fence
 
 int variant() {  // -1: by workload
   static const int v = [] {
@@ -600,6 +602,8 @@ cudaError_t launch_pull_tma(const PullParams& p, int sms, cudaStream_t s) {
     case 8: return launch_variant<V8>(p, sms, s);
     case 9: return launch_variant<V9>(p, sms, s);
     case 10: return launch_variant<V10>(p, sms, s);
+    case 11: return launch_variant<V11>(p, sms, s);
+    case 12: return launch_variant<V12>(p, sms, s);
     default: return launch_variant<V0>(p, sms, s);
   }
 }
