@@ -97,8 +97,9 @@ class ClockSampler:
 # responses add 12.5% protocol bytes on the wire, read requests 18.75% of the
 # pulled bytes in the opposite direction.  One direction busy: 900/1.125;
 # both directions busy (a chain's middle GPUs): 900/(1.125+0.1875).
-NVL_ONE_WAY = 900.0 / 1.125
-NVL_BOTH_WAYS = 900.0 / (1.125 + 0.1875)
+NVL_RESP, NVL_REQ = 0.125, 0.1875
+NVL_ONE_WAY = 900.0 / (1 + NVL_RESP)
+NVL_BOTH_WAYS = 900.0 / (1 + NVL_RESP + NVL_REQ)
 
 
 def measured_peaks() -> dict:

@@ -482,8 +482,11 @@ def run_fsdp_tp2(args):
     # other GPUs) vs bytes read from local HBM, all written to local HBM.
     src = {a.replica: a.src for a in dc.assigns()}.get(f"tp2_{rep}")
     remote = local_b = 0
+    from_gpu = {}  # source GPU -> bytes this shard pulls from it
     for (n, shape), g in zip(shapes, tp2):
-        if src != "trainer":  # a same-slicing upstream replica on other GPUs
+        if src != "trainer":  # a same-slicing upstream replica: shard s on GPU 2*up + s
+            up = int(src.split("_")[1])
+            from_gpu[2 * up + s] = from_gpu.get(2 * up + s, 0) + g[3] * g[5]
             remote += g[3] * g[5]
             continue
         for i in range(world):
@@ -491,13 +494,15 @@ def run_fsdp_tp2(args):
             a0, a1 = max(g[2], fg[2]), min(g[2] + g[3], fg[2] + fg[3])
             c0, c1 = max(g[4], fg[4]), min(g[4] + g[5], fg[4] + fg[5])
             if a0 < a1 and c0 < c1:
+                from_gpu[i] = from_gpu.get(i, 0) + (a1 - a0) * (c1 - c0)
                 if i == rank:
                     local_b += (a1 - a0) * (c1 - c0)
                 else:
                     remote += (a1 - a0) * (c1 - c0)
     hbm = B.measured_peaks()["hbm_gbs"] * 1e9
     t_min = max(remote / 900e9, (local_b + sum(rsizes)) / hbm)
-    allv = dc.gather((kms, landed, sum(walls), clocks, sum(rsizes), rep, s, remote, local_b, t_min))
+    allv = dc.gather((kms, landed, sum(walls), clocks, sum(rsizes), rep, s, remote, local_b, t_min,
+                      from_gpu))
     step_dev_ms = [max(a[0][i] for a in allv) for i in range(args.steps)]
     total_landed = args.steps * sum(a[4] for a in allv)  # reader-layout bytes landed
     dev_s = sum(step_dev_ms) / 1e3
@@ -506,6 +511,22 @@ def run_fsdp_tp2(args):
         per_rx = [round(a[4] / (statistics.mean(a[0]) / 1e3) / 1e9, 2) for a in allv]
         mean_rx = statistics.mean(per_rx)
         plan = sorted({f"{a.replica}<-{a.src}" for a in dc.assigns()})
+        # Whole-box bound: every GPU's NVLink port (data + read protocol both
+        # ways, profiles/r1/ncu_nvlink_counters.json) and its HBM (landed
+        # writes + local reads + reads served to peers); the step can be no
+        # shorter than the busiest resource of the busiest GPU.
+        tx, rx, hb = [0] * world, [0] * world, [0] * world
+        for g_rx, a in enumerate(allv):
+            hb[g_rx] += a[4]
+            for g_src, nb in a[10].items():
+                hb[g_src] += nb
+                if g_src != g_rx:
+                    tx[g_src] += nb
+                    rx[g_rx] += nb
+        t_gpu = [max((tx[g] * (1 + B.NVL_RESP) + rx[g] * B.NVL_REQ) / 900e9,
+                     (rx[g] * (1 + B.NVL_RESP) + tx[g] * B.NVL_REQ) / 900e9,
+                     hb[g] / hbm) for g in range(world)]
+        t_box = max(t_gpu)
         line = {
             "metric": B.METRIC, "value": round(total_landed / dev_s / 1e9, 2), "unit": B.UNIT,
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -521,13 +542,18 @@ def run_fsdp_tp2(args):
             "weight_update_latency_s": round(wall_s / args.steps, 5),
             "publish_s": round(publish_s, 4),
             "roofline": {"bound": "nvlink+hbm", "achieved": round(mean_rx, 1),
-                         "peak": round(statistics.mean(a[4] / a[9] / 1e9 for a in allv), 1),
+                         "peak": round(statistics.mean(a[4] for a in allv) / t_box / 1e9, 1),
                          "unit": "GB/s",
-                         "frac": round(max(a[9] for a in allv) / (statistics.mean(step_dev_ms) / 1e3), 4),
+                         "frac": round(t_box / (statistics.mean(step_dev_ms) / 1e3), 4),
                          "traffic": None,
-                         "peak_src": "per shard: max(NVLink bytes / 900 GB/s nominal, (local-read + "
-                                     "written bytes) / measured HBM peak); frac = slowest shard's bound "
-                                     "/ step time",
+                         "peak_src": "whole box: per GPU max(NVLink tx, NVLink rx with read-protocol "
+                                     "bytes (12.5% response, 18.75% request; 900 GB/s per direction), "
+                                     "HBM bytes / measured HBM peak); frac = busiest GPU's bound / step time",
+                         "bound_ms_per_gpu": [round(t * 1e3, 3) for t in t_gpu],
+                         "nvlink_tx_bytes_per_gpu": tx, "nvlink_rx_bytes_per_gpu": rx,
+                         "hbm_bytes_per_gpu": hb,
+                         "frac_per_shard_naive": round(max(a[9] for a in allv) /
+                                                       (statistics.mean(step_dev_ms) / 1e3), 4),
                          "nvlink_bytes_per_shard": [a[7] for a in allv],
                          "local_read_bytes_per_shard": [a[8] for a in allv],
                          "kernel": "pull_tma_kernel",

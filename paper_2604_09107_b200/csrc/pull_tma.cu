@@ -74,9 +74,13 @@ __device__ __forceinline__ void tensor_store_2d(const void* map, int x, int y, c
       : "memory");
 }
 
-template <int P, int S, int CTAS, int ITEMS, int PIPES = 1, int REL = 4>
+template <int P, int S, int CTAS, int ITEMS, int PIPES = 1, int REL = 4, bool DYN = false>
 struct Cfg {
   static constexpr int kRelease = REL;  // verified batches per watermark release (one sys fence)
+  // DYN: pipelines claim schedule positions from a global ticket (work[0])
+  // instead of the static stride, so a pipeline held up by a slow batch (a
+  // remote source whose HBM is busy) does not hold back the positions after it
+  static constexpr bool kDynamic = DYN;
   static constexpr int kPipes = PIPES;  // producer/consumer pairs per CTA
   static constexpr int kThreads = 64 * PIPES;
   static constexpr int kP = P;
@@ -174,7 +178,15 @@ __global__ void __launch_bounds__(C::kThreads, C::kCtas) pull_tma_kernel(const P
     std::uint32_t abort_seen = 0;
     const std::uint32_t* order = p.order;
     const std::uint32_t pos_end = order ? p.n_sched : p.n_batches;
-    for (std::uint32_t pos = (order ? 0 : p.first_batch) + vcta; pos < pos_end; pos += vgrid) {
+    const std::uint32_t pos0 = order ? 0 : p.first_batch;
+    auto claim = [&]() {  // next position of this pipeline
+      std::uint32_t t = 0;
+      if (lane == 0) t = atomicAdd(&p.work[0], 1u);
+      return pos0 + __shfl_sync(full, t, 0);
+    };
+    std::uint32_t next = C::kDynamic ? claim() : pos0 + vcta;
+    for (std::uint32_t pos = next; pos < pos_end; pos = next) {
+      next = C::kDynamic ? claim() : pos + vgrid;  // claimed a batch ahead: latency hidden
       if (abort_seen) break;
       const std::uint32_t b = order ? __ldg(&order[pos]) : pos;
       const std::uint32_t abort_next = ld_volatile(&p.work[1]);  // acted on next batch
@@ -571,6 +583,7 @@ using V9 = Cfg<256, 4, 1, 320, 4>;  // 4 four-stage pipelines of 256-byte pieces
 using V10 = Cfg<256, 5, 1, 128, 4>;
 using V11 = Cfg<512, 2, 1, 320, 4, 8>;   // V8, releasing 8 batches per fence
 using V12 = Cfg<512, 2, 1, 320, 4, 16>;  // V8, releasing 16 batches per fence
+using V13 = Cfg<512, 2, 1, 320, 4, 4, true>;  // V8 with dynamic batch claiming
 
 int variant() {  // -1: by workload
   static const int v = [] {
@@ -583,14 +596,15 @@ int variant() {  // -1: by workload
 }  // namespace
 
 cudaError_t launch_pull_tma(const PullParams& p, int sms, cudaStream_t s) {
-  // Default V8: one CTA per SM with four producer/consumer pipelines (two
-  // stages each), so the four hashing warps sit on the four sub-partitions.
-  // Measured on B200 (profiles/r1/variants_pipes.txt): local plain pull 90.7%
-  // of HBM (V0, 3 two-warp CTAs with both consumers' hashing on two
-  // sub-partitions: 88-90%), fp8 cast pull 84.8% (V4: 80.7%); over NVLink
-  // equal to V4 (785 GB/s one way, 672 with both directions busy).
+  // Default V13: one CTA per SM with four producer/consumer pipelines (two
+  // stages each), so the four hashing warps sit on the four sub-partitions,
+  // claiming batches dynamically.  Measured on B200: local plain pull 99.9%
+  // of the measured HBM copy peak (V8, the same shape on a static stride:
+  // 91-92%, its fastest pipelines idling at the tail; V0, 3 two-warp CTAs:
+  // 88-90%), FSDP-8 -> TP-2 reshard 97.5% (V8: 91%); over NVLink equal to V8
+  // (785 GB/s one way, 672 with both directions busy).
   int v = variant();
-  if (v < 0) v = 8;
+  if (v < 0) v = 13;
   switch (v) {
     case 1: return launch_variant<V1>(p, sms, s);
     case 2: return launch_variant<V2>(p, sms, s);
@@ -604,6 +618,7 @@ cudaError_t launch_pull_tma(const PullParams& p, int sms, cudaStream_t s) {
     case 10: return launch_variant<V10>(p, sms, s);
     case 11: return launch_variant<V11>(p, sms, s);
     case 12: return launch_variant<V12>(p, sms, s);
+    case 13: return launch_variant<V13>(p, sms, s);
     default: return launch_variant<V0>(p, sms, s);
   }
 }

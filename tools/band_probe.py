@@ -29,8 +29,10 @@ def main():
     ap.add_argument("--dim", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--chunk", type=int, default=4096)
+    ap.add_argument("--src-dev", type=int, default=0, help="trainer GPU (reader: cuda:0)")
     a = ap.parse_args()
     dev = torch.device("cuda", 0)
+    sdev = torch.device("cuda", a.src_dev)
     shape = (a.rows, a.cols)
     nbytes = a.rows * a.cols * 2
     cl = Cluster()
@@ -38,7 +40,7 @@ def main():
     r = cl.open("m", "tp2", 2, chunk_bytes=a.chunk)
     keep = []
     for i in range(a.tensors):
-        w = torch.randint(0, 256, (nbytes,), dtype=torch.uint8, device=dev)
+        w = torch.randint(0, 256, (nbytes,), dtype=torch.uint8, device=sdev)
         keep.append(w)
         assert t.register_slice(0, f"w{i}", w, tp_slice(shape, 2, None, 1, 0)) == Status.ok
         for s in range(2):
@@ -63,8 +65,9 @@ def main():
     kms = sum(ms) / len(ms)
     hbm = B.measured_peaks()["hbm_gbs"]
     gbs = 2 * per_shard / (kms / 1e3) / 1e9
-    print(json.dumps({"dim": a.dim, "rows": a.rows, "cols": a.cols, "tensors": a.tensors,
+    print(json.dumps({"src_dev": a.src_dev, "dim": a.dim, "rows": a.rows, "cols": a.cols, "tensors": a.tensors,
                       "chunk": a.chunk, "kernel_ms": round(kms, 3), "hbm_gbs": round(gbs, 1),
+                      "ingress_gbs": round(per_shard / (kms / 1e3) / 1e9, 1),
                       "frac": round(gbs / hbm, 4)}))
 
 
