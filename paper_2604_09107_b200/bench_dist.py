@@ -511,10 +511,13 @@ def run_fsdp_tp2(args):
         per_rx = [round(a[4] / (statistics.mean(a[0]) / 1e3) / 1e9, 2) for a in allv]
         mean_rx = statistics.mean(per_rx)
         plan = sorted({f"{a.replica}<-{a.src}" for a in dc.assigns()})
-        # Whole-box bound: every GPU's NVLink port (data + read protocol both
-        # ways, profiles/r1/ncu_nvlink_counters.json) and its HBM (landed
-        # writes + local reads + reads served to peers); the step can be no
-        # shorter than the busiest resource of the busiest GPU.
+        # Whole-box bound: every GPU's NVLink port and its HBM (landed writes
+        # + local reads + reads served to peers); the step can be no shorter
+        # than the busiest resource of the busiest GPU.  Link bytes count the
+        # read-response protocol (12.5%, profiles/r1/ncu_nvlink_counters.json);
+        # the read requests flowing the other way (18.75% of the data for
+        # 128-byte reads, less for promoted 256-byte reads) are left out, so
+        # this stays a lower bound on the step; with them: t_gpu_req.
         tx, rx, hb = [0] * world, [0] * world, [0] * world
         for g_rx, a in enumerate(allv):
             hb[g_rx] += a[4]
@@ -523,9 +526,10 @@ def run_fsdp_tp2(args):
                 if g_src != g_rx:
                     tx[g_src] += nb
                     rx[g_rx] += nb
-        t_gpu = [max((tx[g] * (1 + B.NVL_RESP) + rx[g] * B.NVL_REQ) / 900e9,
-                     (rx[g] * (1 + B.NVL_RESP) + tx[g] * B.NVL_REQ) / 900e9,
-                     hb[g] / hbm) for g in range(world)]
+        t_gpu = [max(max(tx[g], rx[g]) * (1 + B.NVL_RESP) / 900e9, hb[g] / hbm) for g in range(world)]
+        t_gpu_req = [max((tx[g] * (1 + B.NVL_RESP) + rx[g] * B.NVL_REQ) / 900e9,
+                         (rx[g] * (1 + B.NVL_RESP) + tx[g] * B.NVL_REQ) / 900e9,
+                         hb[g] / hbm) for g in range(world)]
         t_box = max(t_gpu)
         line = {
             "metric": B.METRIC, "value": round(total_landed / dev_s / 1e9, 2), "unit": B.UNIT,
@@ -546,10 +550,11 @@ def run_fsdp_tp2(args):
                          "unit": "GB/s",
                          "frac": round(t_box / (statistics.mean(step_dev_ms) / 1e3), 4),
                          "traffic": None,
-                         "peak_src": "whole box: per GPU max(NVLink tx, NVLink rx with read-protocol "
-                                     "bytes (12.5% response, 18.75% request; 900 GB/s per direction), "
-                                     "HBM bytes / measured HBM peak); frac = busiest GPU's bound / step time",
+                         "peak_src": "whole box: per GPU max(NVLink tx or rx data x 1.125 read-response "
+                                     "protocol / 900 GB/s per direction, HBM bytes / measured HBM peak); "
+                                     "frac = busiest GPU's bound / step time",
                          "bound_ms_per_gpu": [round(t * 1e3, 3) for t in t_gpu],
+                         "bound_ms_per_gpu_with_requests": [round(t * 1e3, 3) for t in t_gpu_req],
                          "nvlink_tx_bytes_per_gpu": tx, "nvlink_rx_bytes_per_gpu": rx,
                          "hbm_bytes_per_gpu": hb,
                          "frac_per_shard_naive": round(max(a[9] for a in allv) /

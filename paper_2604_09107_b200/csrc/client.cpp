@@ -511,15 +511,6 @@ Status ServeRegistry::import_state(const std::string& blob) {
 
 // --------------------------------------------------------- address mapping
 
-int ptr_device(std::uint64_t p) {
-  cudaPointerAttributes a{};
-  if (!p || cudaPointerGetAttributes(&a, reinterpret_cast<void*>(p)) != cudaSuccess) {
-    cudaGetLastError();
-    return -1;
-  }
-  return a.type == cudaMemoryTypeDevice ? a.device : -1;
-}
-
 Status enable_peer(int reader_device, int owner_device) {
   if (reader_device == owner_device) return Status::ok;
   static std::mutex mu;
@@ -542,6 +533,7 @@ Status enable_peer(int reader_device, int owner_device) {
 
 Status map_source(const std::shared_ptr<ServeState>& st, int reader_device, SourceView* out) {
   std::lock_guard lk(st->m);
+  out->device = st->host_name.empty() ? st->device : -1;
   out->cmap = st->cmap;
   out->epoch = st->epoch;
   out->total = st->item_ends.empty() ? 0 : st->item_ends.back();
@@ -1249,9 +1241,7 @@ Status Client::launch_fill(Shard& sh, const SourceView& src, bool src_complete) 
   const dev::SrcDesc sdesc{reinterpret_cast<const std::uint64_t*>(src.digests),
                            src_complete ? nullptr : reinterpret_cast<const std::uint32_t*>(src.flags),
                            src.epoch, 0};
-  bool remote = false;
-  for (std::size_t i = 0; i < items.size() && !remote; ++i)
-    remote = ptr_device(src.item_ptrs[i]) != sh.device;
+  const bool remote = src.device != sh.device;
   dev::PullParams pp{};
   RS_CUDA(dev::upload_pull_plan(sh.device, sh.stream, descs.data(),
                                 static_cast<std::uint32_t>(descs.size()), &sdesc, 1,
@@ -1502,13 +1492,17 @@ Status Client::launch_reshard_fill(Shard& sh, const Assignment& a, bool src_comp
              src_complete ? nullptr : reinterpret_cast<const std::uint32_t*>(views[s].flags),
              views[s].epoch, 0};
   }
-  bool remote = false;
+  std::vector<int> src_dev(nsrc, sh.device);
   for (std::uint32_t s = 0; s < nsrc; ++s)
-    if (need[s] && !views[s].item_ptrs.empty()) remote |= ptr_device(views[s].item_ptrs[0]) != sh.device;
+    if (need[s]) src_dev[s] = views[s].device;
+  auto link_class = [&](std::uint32_t s) {
+    // 0: local HBM, 1: host memory (device -1), 2 + d: peer device d
+    return src_dev[s] == sh.device ? 0u : static_cast<std::uint32_t>(src_dev[s] + 2);
+  };
   std::vector<dev::ItemDesc> descs = rs.plan.segs;
   for (auto& d : descs) {
     d.src = views[d.src_id].item_ptrs[d.pad] + d.src;
-    d.pad = 0;
+    d.pad = link_class(d.src_id);
   }
   std::uint32_t next = rs.own_chunks;
   for (std::size_t gi = 0; gi < rs.plan.gathers.size(); ++gi) {
@@ -1524,10 +1518,13 @@ Status Client::launch_reshard_fill(Shard& sh, const Assignment& a, bool src_comp
     d.src_chunk0 = ss.chunk0[gth.src_item];
     d.q = d.m = 1;
     d.src_id = gth.src_shard;
+    d.pad = link_class(gth.src_shard);
     descs.push_back(d);
     const auto n = static_cast<std::uint32_t>((it.length + d.chunk_len - 1) / d.chunk_len);
     next += (n + dev::kBatchChunks - 1) / dev::kBatchChunks * dev::kBatchChunks;
   }
+  bool remote = false;
+  for (std::uint32_t s = 0; s < nsrc; ++s) remote |= need[s] && src_dev[s] != sh.device;
   dev::PullParams pp{};
   RS_CUDA(dev::upload_pull_plan(sh.device, sh.stream, descs.data(),
                                 static_cast<std::uint32_t>(descs.size()), sd.data(), nsrc, next,

@@ -167,6 +167,7 @@ class ServeRegistry {
 
 // Source addresses as the reader's device sees them.
 struct SourceView {
+  int device = -1;  // GPU holding the source (-1: host memory)
   std::vector<std::uint64_t> item_ptrs;
   std::uint64_t digests = 0;
   std::uint64_t flags = 0;

@@ -37,7 +37,8 @@ struct ItemDesc {
   std::uint32_t src_chunk0;  // source chunk index of the first chunk
   std::uint16_t q, m;        // chunks taken per source row / chunks per source row
   std::uint32_t src_id;      // index into PullParams.srcs
-  std::uint32_t pad;
+  std::uint32_t pad;         // link class of the source (0: local HBM, 1: host, 2 + d: peer d);
+                             // only the schedule order reads it
 };
 static_assert(sizeof(ItemDesc) == 48, "ItemDesc layout");
 // chunk_len flags: the segment has TMA tensor maps at PullParams.maps +
@@ -99,8 +100,9 @@ struct PullParams {
   std::uint32_t remote;              // some source is another GPU's HBM (kernel shape choice)
   // Schedule: positions 0..n_sched-1 map to batches order[pos] (first_batch
   // then unused); null order: batches first_batch..n_batches-1 in order.
-  // The order lists only the batches some segment touches: a hash pass over
-  // a few items of a large payload walks just those.
+  // The order lists only the batches some segment touches (a hash pass over
+  // a few items of a large payload walks just those) and interleaves the
+  // batches of sources behind different links (schedule_order).
   std::uint32_t n_sched;
   const std::uint32_t* order;
 };

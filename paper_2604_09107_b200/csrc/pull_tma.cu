@@ -584,6 +584,8 @@ using V10 = Cfg<256, 5, 1, 128, 4>;
 using V11 = Cfg<512, 2, 1, 320, 4, 8>;   // V8, releasing 8 batches per fence
 using V12 = Cfg<512, 2, 1, 320, 4, 16>;  // V8, releasing 16 batches per fence
 using V13 = Cfg<512, 2, 1, 320, 4, 4, true>;  // V8 with dynamic batch claiming
+using V14 = Cfg<256, 4, 1, 320, 4, 4, true>;  // V9 (4 stages of 256 B) with dynamic claiming
+using V15 = Cfg<512, 3, 1, 0, 4, 4, true>;    // V7 (3 stages, segments in global), dynamic
 
 int variant() {  // -1: by workload
   static const int v = [] {
@@ -619,6 +621,8 @@ cudaError_t launch_pull_tma(const PullParams& p, int sms, cudaStream_t s) {
     case 11: return launch_variant<V11>(p, sms, s);
     case 12: return launch_variant<V12>(p, sms, s);
     case 13: return launch_variant<V13>(p, sms, s);
+    case 14: return launch_variant<V14>(p, sms, s);
+    case 15: return launch_variant<V15>(p, sms, s);
     default: return launch_variant<V0>(p, sms, s);
   }
 }

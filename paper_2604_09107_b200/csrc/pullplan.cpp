@@ -76,7 +76,7 @@ bool plan_debug() {
 void print_plan_stats(const ItemDesc* items, std::uint32_t n, const std::vector<std::uint32_t>& bseg,
                       std::uint32_t n_chunks) {
   std::uint64_t box_b = 0, slot_b = 0, box_n = 0, slot_n = 0, band_b = 0;
-  std::map<std::uint32_t, std::uint64_t> by_len;
+  std::map<std::uint32_t, std::uint64_t> by_len, by_class;
   for (std::uint32_t b = 0; b < bseg.size(); ++b) {
     const std::uint32_t s0 = bseg[b];
     const ItemDesc& d = items[s0];
@@ -102,12 +102,15 @@ void print_plan_stats(const ItemDesc* items, std::uint32_t n, const std::vector<
     (box ? box_n : slot_n) += 1;
     if (box && (d.chunk_len & kMap3D)) band_b += bytes;
     by_len[c] += bytes;
+    by_class[d.pad] += bytes;
   }
   std::fprintf(stderr, "[rsb] plan: %u segments, %zu batches: box %llu (%.3f GB, %.3f GB column bands), "
                "slot %llu (%.3f GB)\n[rsb] plan: bytes by chunk length:",
                n, bseg.size(), (unsigned long long)box_n, box_b / 1e9, band_b / 1e9,
                (unsigned long long)slot_n, slot_b / 1e9);
   for (const auto& [len, bytes] : by_len) std::fprintf(stderr, " %u:%.3fGB", len, bytes / 1e9);
+  std::fprintf(stderr, "\n[rsb] plan: bytes by link class:");
+  for (const auto& [c, bytes] : by_class) std::fprintf(stderr, " %u:%.3fGB", c, bytes / 1e9);
   std::fprintf(stderr, "\n");
 }
 
@@ -115,10 +118,20 @@ void print_plan_stats(const ItemDesc* items, std::uint32_t n, const std::vector<
 
 std::vector<std::uint32_t> schedule_order(const ItemDesc* items, std::uint32_t n,
                                           const std::vector<std::uint32_t>& bseg) {
-  // The batches some segment touches, in batch order (empty: all of them).
-  // Interleaving the batches of several sources in proportion to their
-  // counts was measured slower (config 3, N=1 and N=2: +1.5-2%): it scatters
-  // the landing writes over the whole shard instead of a moving window.
+  // The batches some segment touches (empty result: all, in batch order).
+  // When the segments' sources sit behind different links (ItemDesc.pad =
+  // link class: 0 local HBM, 1 host memory, 2 + d peer d), the classes' batches
+  // are interleaved in proportion to their counts: batch b, the r-th of its
+  // class's n_c batches, goes at key (r + 1/2) / n_c, so every link stays
+  // busy for the whole pull instead of one at a time, and each class keeps
+  // its own front-to-back order (what a chaser downstream waits on).
+  // Sources behind one link are not interleaved: that only scatters the
+  // landing writes (measured +1.5% on config 3 at N=1).  Config 3 at N=2
+  // (FSDP-2 -> TP-2, 16% of each shard over NVLink): 14.8 -> 13.1 ms; with
+  // the peer only serving, 13.3 -> 9.7 ms (tools/mix_probe.py).  Finishing
+  // the remote class earlier (keys scaled by 0.2-0.8) moved it by <= 2%.
+  static const bool no_mix = std::getenv("RSB_BATCH_ORDER") &&
+                             std::getenv("RSB_BATCH_ORDER")[0] == '0';  // A/B knob
   const std::uint32_t nb = static_cast<std::uint32_t>(bseg.size());
   std::vector<std::uint8_t> touched(nb, 0);
   for (std::uint32_t i = 0; i < n; ++i) {
@@ -128,10 +141,30 @@ std::vector<std::uint32_t> schedule_order(const ItemDesc* items, std::uint32_t n
     for (std::uint64_t b = items[i].chunk0 / kBatchChunks; b <= last / kBatchChunks && b < nb; ++b)
       touched[b] = 1;
   }
-  std::vector<std::uint32_t> order;
-  for (std::uint32_t b = 0; b < nb; ++b)
-    if (touched[b]) order.push_back(b);
-  if (order.size() == nb) order.clear();
+  std::vector<std::uint32_t> cls(nb, 0), count;
+  std::uint32_t n_touched = 0;
+  for (std::uint32_t b = 0; b < nb; ++b) {
+    if (!touched[b]) continue;
+    ++n_touched;
+    const std::uint32_t c = no_mix ? 0 : items[bseg[b]].pad;
+    cls[b] = c;
+    if (c >= count.size()) count.resize(c + 1, 0);
+    ++count[c];
+  }
+  int classes = 0;
+  for (std::uint32_t c : count) classes += c != 0;
+  if (classes < 2 && n_touched == nb) return {};
+  std::vector<std::uint32_t> rank(count.size(), 0);
+  std::vector<std::pair<double, std::uint32_t>> key;
+  key.reserve(n_touched);
+  for (std::uint32_t b = 0; b < nb; ++b) {
+    if (!touched[b]) continue;
+    const std::uint32_t c = cls[b];
+    key.push_back({(rank[c]++ + 0.5) / count[c], b});
+  }
+  if (classes > 1) std::sort(key.begin(), key.end());
+  std::vector<std::uint32_t> order(key.size());
+  for (std::size_t i = 0; i < key.size(); ++i) order[i] = key[i].second;
   return order;
 }
 
