@@ -51,7 +51,11 @@ constexpr std::uint32_t kMap3D = 0x40000000u;
 // k holds chunk_len/2 bytes at dst + k*chunk_len/2 (saturating RNE cast,
 // oracle ro_bf16_to_e4m3).  Verification is on the bf16 bytes.
 constexpr std::uint32_t kCastE4M3 = 0x20000000u;
-constexpr std::uint32_t kChunkLenMask = 0x1fffffffu;
+// A cast segment whose e4m3 landing has a destination tensor map (2-D
+// [chunks][chunk_len/2], 128B swizzle) at maps + 256*i + 128: the consumer
+// converts into the stage and lands it with tensor stores.
+constexpr std::uint32_t kCastMap = 0x10000000u;
+constexpr std::uint32_t kChunkLenMask = 0x0fffffffu;
 constexpr int kMapBoxCols = 128;  // TMA box: 128 bytes x 32 chunks, 128B swizzle
 
 // A source serve state as the reader's device sees it.

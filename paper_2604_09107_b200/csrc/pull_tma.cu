@@ -253,7 +253,12 @@ __global__ void __launch_bounds__(C::kThreads, C::kCtas) pull_tma_kernel(const P
                                             r.clen != 0) &&
                        (k0 % q0) == 0;
       const bool map3d = box && (items[seg0].chunk_len & kMap3D) != 0;
-      const std::uint32_t box_store = box && cast_mask == 0 && items[seg0].dst != 0;
+      // 1: land the boxes with tensor stores; 2: cast into the stage, then
+      // land the e4m3 boxes with tensor stores; 0: the consumer stores
+      const std::uint32_t box_store =
+          !box ? 0u
+               : cast_mask == 0 ? (items[seg0].dst != 0 ? 1u : 0u)
+                                : (cast_mask == full && (items[seg0].chunk_len & kCastMap) ? 2u : 0u);
       std::uint32_t maxlen = r.clen;
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) maxlen = max(maxlen, __shfl_xor_sync(full, maxlen, o));
@@ -397,7 +402,7 @@ __global__ void __launch_bounds__(C::kThreads, C::kCtas) pull_tma_kernel(const P
       if (box) {
         // 1) land: one tensor store per box, issued by lane 0 (a cast batch
         //    lands from registers in the hash loop instead)
-        if (lane == 0 && m.store) {
+        if (lane == 0 && m.store == 1) {
           const std::uint8_t* dmap = maps + 256 * std::size_t(m.item) + 128;
           fence_proxy_async_smem();
           for (std::uint32_t j = 0; j < m.bpiece / kMapBoxCols; ++j)
@@ -420,7 +425,30 @@ __global__ void __launch_bounds__(C::kThreads, C::kCtas) pull_tma_kernel(const P
           v3 = xround(v3, (std::uint64_t(q.y) << 32) | q.x);
           v4 = xround(v4, (std::uint64_t(q.w) << 32) | q.z);
         };
-        if (castp) {
+        if (m.store == 2) {
+          // e4m3 of stripe kk = 16-byte granule kk of the lane's output row,
+          // written in place over stage bytes already read (output box kk>>3
+          // lies in input box <= kk>>2, output granule kk&7 at or before the
+          // input granules just read), in the same 128B-swizzled box layout
+#pragma unroll 4
+          for (int kk = 0; kk < stripes; ++kk) {
+            uint4 a, q;
+            box_stripe(kk, a, q);
+            *reinterpret_cast<uint4*>(st + (kk >> 3) * 4096 + lane * 128 +
+                                      ((static_cast<std::uint32_t>(kk & 7) << 4) ^ swz)) =
+                cvt16_e4m3(a, q);
+          }
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            const std::uint8_t* dmap = maps + 256 * std::size_t(m.item) + 128;
+            for (std::uint32_t j = 0; j < (m.bpiece / 2 + kMapBoxCols - 1) / kMapBoxCols; ++j)
+              tensor_store_2d(dmap, static_cast<int>(m.g / 2 + j * kMapBoxCols), static_cast<int>(m.k0),
+                              st + j * 4096);
+            bulk_commit();
+            committed = true;
+          }
+        } else if (castp) {
 #pragma unroll 4
           for (int kk = 0; kk < stripes; ++kk) {
             uint4 a, q;

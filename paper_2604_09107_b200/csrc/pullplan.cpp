@@ -238,6 +238,9 @@ cudaError_t upload_pull_plan(int device, cudaStream_t s, ItemDesc* items, std::u
       // 2-D: one row per chunk; 3-D: one row per source row (q chunks each)
       ok = encode(mp, d.src, c, q, m, q == m ? full : full / q);
       if (ok && d.dst && !cast) ok = encode(mp + 1, d.dst, c, 1, 1, full);
+      // e4m3 landing rows of c/2 bytes: whole 128-byte boxes needed
+      if (ok && d.dst && cast && c / 2 >= kMapBoxCols && encode(mp + 1, d.dst, c / 2, 1, 1, full))
+        d.chunk_len |= kCastMap;
     }
     if (ok) {
       d.chunk_len |= kHasMap | (q < m ? kMap3D : 0u);
