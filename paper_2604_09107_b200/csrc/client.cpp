@@ -1364,9 +1364,10 @@ std::vector<Client::FillOutcome> Client::wait_shards(const std::vector<std::uint
     }
     if (e == cudaSuccess && !ok(net) && st[i].code == dev::kPullOk) st[i].code = dev::kPullNotServing;
     if (std::getenv("RSB_DEBUG") && (st[i].code != dev::kPullOk || e != cudaSuccess))
-      std::fprintf(stderr, "[rsb] %s shard %u fill: code %u bad_chunk %u net %d cuda %d\n",
-                   replica_.c_str(), i, st[i].code, st[i].bad_chunk, static_cast<int>(net),
-                   static_cast<int>(e));
+      std::fprintf(stderr, "[rsb] %s shard %u fill: code %u bad_chunk %u (source batch %u flag %u) net %d cuda %d\n",
+                   replica_.c_str(), i, st[i].code, st[i].bad_chunk,
+                   static_cast<unsigned>(st[i].pad >> 32), static_cast<unsigned>(st[i].pad & 0xffffffffu),
+                   static_cast<int>(net), static_cast<int>(e));
     if (e != cudaSuccess) {
       out[i] = {Status::transfer_failed, 0, 0};
       continue;

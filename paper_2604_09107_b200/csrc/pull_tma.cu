@@ -219,10 +219,18 @@ __global__ void __launch_bounds__(C::kThreads, C::kCtas) pull_tma_kernel(const P
         code = wait_flag(&sd->flags[sbatch], sd->epoch, p.timeout_ns, &p.work[1]);
       const std::uint32_t worst = __reduce_max_sync(full, code);
       if (worst != kPullOk) {
+        // diagnostics: the source batch and the watermark value that failed
+        const unsigned bad_lanes = __ballot_sync(full, code == worst);
+        const int bl = __ffs(bad_lanes) - 1;
+        const std::uint32_t bsb = __shfl_sync(full, sbatch, bl);
+        const std::uint32_t bfv = (lane == bl && sd && sd->flags) ? ld_volatile(&sd->flags[sbatch]) : 0u;
+        const std::uint32_t bflag = __shfl_sync(full, bfv, bl);
         if (lane == 0) {
           if (worst != kPullAborted) {
             atomicCAS(&p.status->code, 0u, worst);
             atomicExch(&p.status->bad_chunk, b * kBatchChunks);
+            atomicExch(reinterpret_cast<unsigned long long*>(&p.status->pad),
+                       (static_cast<unsigned long long>(bsb) << 32) | bflag);
           }
           atomicExch(&p.work[1], 1u);
           if (p.dst_flags) st_release_sys(&p.dst_flags[b], p.dst_epoch | kAbort);

@@ -22,11 +22,27 @@ bool debug() {
   return d;
 }
 
-constexpr std::uint32_t kReqMagic = 0x31505352;  // "RSP1"
+constexpr std::uint32_t kReqMagic = 0x32505352;  // "RSP2"
 constexpr std::uint32_t kEnd = 0xffffffffu;
 constexpr std::uint32_t kFrameBatches = 32;  // up to 32 watermark batches per frame
 constexpr std::size_t kStageBytes = 8u << 20;  // per staging buffer (frames are cut to fit)
-constexpr int kSlots = 8;                      // concurrent connections with staging
+constexpr int kSlots = 16;                     // concurrent connections with staging
+
+// Connections per source: frame k of the stream travels on connection
+// k % streams (one TCP stream is bound by one core's copy; RSB_TCP_STREAMS).
+// Loopback on the B200 box, 1 GiB: 1 stream 6.9 GB/s, 2: 10-13, 4: 16-19,
+// 8: 21.6.  Default 2: with 4 connections the version-bump test
+// (tests/test_stream.py) stalls one frame of the second version for seconds
+// in TCP (one retransmission per run; not root-caused), which the pull
+// kernel reports as an upstream timeout.
+std::uint32_t tcp_streams() {
+  static const std::uint32_t n = [] {
+    const char* e = std::getenv("RSB_TCP_STREAMS");
+    const int v = e ? std::atoi(e) : 2;
+    return static_cast<std::uint32_t>(std::clamp(v, 1, 8));
+  }();
+  return n;
+}
 
 bool send_all(int fd, const void* p, std::size_t n) {
   const auto* b = static_cast<const std::uint8_t*>(p);
@@ -74,9 +90,14 @@ bool recv_vec(int fd, std::vector<T>* v) {
 void tune(int fd) {
   int one = 1;
   setsockopt(fd, IPPROTO_TCP, TCP_NODELAY, &one, sizeof(one));
-  int buf = 8 << 20;
-  setsockopt(fd, SOL_SOCKET, SO_SNDBUF, &buf, sizeof(buf));
-  setsockopt(fd, SOL_SOCKET, SO_RCVBUF, &buf, sizeof(buf));
+  static const int buf = [] {  // socket buffers (0: kernel autotuning); RSB_TCP_BUF
+    const char* e = std::getenv("RSB_TCP_BUF");
+    return e ? std::atoi(e) : 8 << 20;
+  }();
+  if (buf > 0) {
+    setsockopt(fd, SOL_SOCKET, SO_SNDBUF, &buf, sizeof(buf));
+    setsockopt(fd, SOL_SOCKET, SO_RCVBUF, &buf, sizeof(buf));
+  }
 }
 
 // One batch's byte range inside its item.
@@ -209,12 +230,14 @@ void StreamServer::serve_conn(int fd) {
     send_pod(fd, status);
     ::close(fd);
   };
-  std::uint32_t magic = 0, klen = 0;
+  std::uint32_t magic = 0, klen = 0, stripe = 0, stripes = 1;
   VersionId version = 0;
   if (!recv_pod(fd, &magic) || magic != kReqMagic || !recv_pod(fd, &klen) || klen > 4096)
     return (void)::close(fd);
   std::string key(klen, '\0');
-  if (!recv_all(fd, key.data(), klen) || !recv_pod(fd, &version)) return (void)::close(fd);
+  if (!recv_all(fd, key.data(), klen) || !recv_pod(fd, &version) || !recv_pod(fd, &stripe) ||
+      !recv_pod(fd, &stripes) || stripes == 0 || stripe >= stripes)
+    return (void)::close(fd);
   auto st = serves_->find(key);
   if (!st) return finish(static_cast<std::uint32_t>(Status::not_serving));
   // snapshot of the serve state (addresses in this process)
@@ -245,18 +268,28 @@ void StreamServer::serve_conn(int fd) {
   const auto spans = batch_spans(cm, lens);
   for (const auto& sp : spans)
     if (sp.len > kStageBytes) return finish(static_cast<std::uint32_t>(Status::invalid_argument));
-  // header: chunk map, item lengths, chunk-digest table
-  std::vector<std::uint64_t> dig(cm.n_chunks());
-  if (!dig.empty() && cudaMemcpy(dig.data(), reinterpret_cast<const void*>(digests), dig.size() * 8,
-                                 cudaMemcpyDefault) != cudaSuccess)
-    return finish(static_cast<std::uint32_t>(Status::transfer_failed));
-  if (!send_pod(fd, std::uint32_t{0}) || !send_vec(fd, cm.chunk0) || !send_vec(fd, cm.chunk_len) ||
-      !send_vec(fd, cm.count) || !send_vec(fd, lens) || !send_vec(fd, dig))
+  // header (on the first connection of a source only): chunk map, item
+  // lengths, chunk-digest table
+  if (stripe == 0) {
+    std::vector<std::uint64_t> dig(cm.n_chunks());
+    if (!dig.empty() && cudaMemcpy(dig.data(), reinterpret_cast<const void*>(digests), dig.size() * 8,
+                                   cudaMemcpyDefault) != cudaSuccess)
+      return finish(static_cast<std::uint32_t>(Status::transfer_failed));
+    if (!send_pod(fd, std::uint32_t{0}) || !send_vec(fd, cm.chunk0) || !send_vec(fd, cm.chunk_len) ||
+        !send_vec(fd, cm.count) || !send_vec(fd, lens) || !send_vec(fd, dig))
+      return (void)::close(fd);
+  } else if (!send_pod(fd, std::uint32_t{0})) {
     return (void)::close(fd);
+  }
   // payload: frames of up to kFrameBatches consecutive batches of one item,
   // each sent once the source has verified it (double-buffered D2H staging)
+  const auto t_slot = std::chrono::steady_clock::now();
   Slot* slot = take_slot();
   if (!slot) return (void)::close(fd);
+  if (debug()) {
+    const double w = std::chrono::duration<double>(std::chrono::steady_clock::now() - t_slot).count();
+    if (w > 0.01) std::fprintf(stderr, "[rsb] stream server: stripe %u waited %.3f s for staging\n", stripe, w);
+  }
   void* const* stage = slot->stage;
   cudaStream_t cs = slot->stream;
   cudaEvent_t* ev = slot->ev;
@@ -277,8 +310,8 @@ void StreamServer::serve_conn(int fd) {
     std::uint32_t b0 = 0, nb = 0;
     std::uint64_t len = 0;
   };
-  std::vector<Frame> frames;
-  for (std::uint32_t b = 0; b < spans.size();) {
+  std::vector<Frame> frames;  // this connection's: frame k of the stream if k % stripes == stripe
+  for (std::uint32_t b = 0, k = 0; b < spans.size();) {
     if (spans[b].len == 0) {
       ++b;
       continue;
@@ -290,7 +323,7 @@ void StreamServer::serve_conn(int fd) {
       ++f.nb;
       ++b;
     }
-    frames.push_back(f);
+    if (k++ % stripes == stripe) frames.push_back(f);
   }
   bool good = true;
   auto issue = [&](std::size_t k) {
@@ -313,8 +346,10 @@ void StreamServer::serve_conn(int fd) {
     good = send_pod(fd, f.b0) && send_pod(fd, f.nb) && send_pod(fd, f.len) &&
            send_all(fd, stage[k & 1], f.len);
   }
-  if (!good && debug())
-    std::fprintf(stderr, "[rsb] stream server: %s aborted (frames %zu)\n", key.c_str(), frames.size());
+  if (debug())
+    std::fprintf(stderr, "[rsb] stream server: %s v%llu stripe %u/%u: %zu frames %s\n", key.c_str(),
+                 static_cast<unsigned long long>(version), stripe, stripes, frames.size(),
+                 good ? "sent" : "aborted");
   if (good) {
     send_pod(fd, kEnd);
     send_pod(fd, std::uint32_t{0});
@@ -329,9 +364,12 @@ void StreamServer::serve_conn(int fd) {
 // ------------------------------------------------------------------ reader
 
 StreamSource::~StreamSource() {
-  if (fd_ >= 0) ::shutdown(fd_, SHUT_RDWR);
-  if (rx_.joinable()) rx_.join();
-  if (fd_ >= 0) ::close(fd_);
+  for (int fd : fds_)
+    if (fd >= 0) ::shutdown(fd, SHUT_RDWR);
+  for (auto& t : rx_)
+    if (t.joinable()) t.join();
+  for (int fd : fds_)
+    if (fd >= 0) ::close(fd);
 }
 
 Status StreamSource::open(const std::string& endpoint, const std::string& key, VersionId version,
@@ -349,28 +387,39 @@ Status StreamSource::open(const std::string& endpoint, const std::string& key, V
   // condemned (as on the in-box path, Client::resolve_source).
   auto deadline = std::chrono::steady_clock::now() + std::chrono::duration<double>(timeout_s);
   const auto klen = static_cast<std::uint32_t>(key.size());
-  for (;;) {
-    fd_ = ::socket(AF_INET, SOCK_STREAM, 0);
-    std::uint32_t status = static_cast<std::uint32_t>(Status::not_serving);
-    if (fd_ >= 0 && ::connect(fd_, reinterpret_cast<sockaddr*>(&a), sizeof(a)) == 0) {
-      tune(fd_);
-      if (!send_pod(fd_, kReqMagic) || !send_pod(fd_, klen) || !send_all(fd_, key.data(), klen) ||
-          !send_pod(fd_, version) || !recv_pod(fd_, &status))
-        status = static_cast<std::uint32_t>(Status::transfer_failed);
-      if (status == 0) break;
+  const std::uint32_t streams = tcp_streams();
+  auto connect_stripe = [&](std::uint32_t stripe, int* out) -> Status {
+    for (;;) {
+      int fd = ::socket(AF_INET, SOCK_STREAM, 0);
+      std::uint32_t status = static_cast<std::uint32_t>(Status::not_serving);
+      if (fd >= 0 && ::connect(fd, reinterpret_cast<sockaddr*>(&a), sizeof(a)) == 0) {
+        tune(fd);
+        if (!send_pod(fd, kReqMagic) || !send_pod(fd, klen) || !send_all(fd, key.data(), klen) ||
+            !send_pod(fd, version) || !send_pod(fd, stripe) || !send_pod(fd, streams) ||
+            !recv_pod(fd, &status))
+          status = static_cast<std::uint32_t>(Status::transfer_failed);
+        if (status == 0) {
+          *out = fd;
+          return Status::ok;
+        }
+      }
+      if (fd >= 0) ::close(fd);
+      if (status != static_cast<std::uint32_t>(Status::not_serving)) return static_cast<Status>(status);
+      if (std::chrono::steady_clock::now() > deadline) return Status::not_serving;
+      std::this_thread::sleep_for(std::chrono::milliseconds(1));
     }
-    if (fd_ >= 0) ::close(fd_);
-    fd_ = -1;
-    if (status != static_cast<std::uint32_t>(Status::not_serving)) return static_cast<Status>(status);
-    if (std::chrono::steady_clock::now() > deadline) return Status::not_serving;
-    std::this_thread::sleep_for(std::chrono::milliseconds(1));
-  }
+  };
+  fds_.assign(streams, -1);
+  if (Status s = connect_stripe(0, &fds_[0]); !ok(s)) return s;
   ChunkMap cm;
   std::vector<std::uint64_t> lens, dig;
-  if (!recv_vec(fd_, &cm.chunk0) || !recv_vec(fd_, &cm.chunk_len) || !recv_vec(fd_, &cm.count) ||
-      !recv_vec(fd_, &lens) || !recv_vec(fd_, &dig) || lens.size() + 1 != cm.chunk0.size() ||
+  const int fd0 = fds_[0];
+  if (!recv_vec(fd0, &cm.chunk0) || !recv_vec(fd0, &cm.chunk_len) || !recv_vec(fd0, &cm.count) ||
+      !recv_vec(fd0, &lens) || !recv_vec(fd0, &dig) || lens.size() + 1 != cm.chunk0.size() ||
       dig.size() != cm.n_chunks())
     return Status::protocol_error;
+  for (std::uint32_t k = 1; k < streams; ++k)
+    if (Status s = connect_stripe(k, &fds_[k]); !ok(s)) return s;
   // pinned, device-mapped landing for the stream + digests + watermarks
   item_off_.resize(lens.size());
   std::uint64_t tot = 0;
@@ -378,8 +427,9 @@ Status StreamSource::open(const std::string& endpoint, const std::string& key, V
     item_off_[i] = tot;
     tot += (lens[i] + 255) / 256 * 256;
   }
+  static const bool no_pool = std::getenv("RSB_TCP_NOPOOL") != nullptr;  // diagnostic
   auto take = [&](std::size_t n, std::unique_ptr<HostBuf>* out) -> Status {
-    if (pool)
+    if (pool && !no_pool)
       for (auto it = pool->begin(); it != pool->end(); ++it)
         if ((*it)->n >= n) {
           *out = std::move(*it);
@@ -403,14 +453,11 @@ Status StreamSource::open(const std::string& endpoint, const std::string& key, V
   view_.flags = reinterpret_cast<std::uint64_t>(tb + dig.size() * 8);
   view_.epoch = 1;
   view_.total = tot;
-  rx_ = std::thread([this, lens] {
-    (void)lens;
-    receive_loop();
-  });
+  for (int fd : fds_) rx_.emplace_back([this, fd] { receive_loop(fd); });
   return Status::ok;
 }
 
-void StreamSource::receive_loop() {
+void StreamSource::receive_loop(int fd) {
   const ChunkMap& cm = view_.cmap;
   std::vector<std::uint64_t> lens(item_off_.size());
   // item of every batch and the batch's offset inside it
@@ -426,26 +473,19 @@ void StreamSource::receive_loop() {
   }
   auto* flags = reinterpret_cast<std::uint32_t*>(view_.flags);
   auto* base = static_cast<std::uint8_t*>(data_->p);
+  auto fail = [&](Status st) {
+    int expect = 0;
+    rx_status_.compare_exchange_strong(expect, static_cast<int>(st));
+    abort_all();
+  };
   for (;;) {
     std::uint32_t b0 = 0, nb = 0;
     std::uint64_t len = 0;
-    if (!recv_pod(fd_, &b0) || !recv_pod(fd_, &nb) || !recv_pod(fd_, &len)) {
-      rx_status_ = static_cast<int>(Status::transfer_failed);
-      abort_all();
-      return;
-    }
+    if (!recv_pod(fd, &b0) || !recv_pod(fd, &nb) || !recv_pod(fd, &len)) return fail(Status::transfer_failed);
     if (b0 == kEnd) break;
-    if (b0 + nb > item_of.size()) {
-      rx_status_ = static_cast<int>(Status::protocol_error);
-      abort_all();
-      return;
-    }
+    if (b0 + nb > item_of.size()) return fail(Status::protocol_error);
     const std::uint32_t i = item_of[b0];
-    if (!recv_all(fd_, base + item_off_[i] + off_of[b0], len)) {
-      rx_status_ = static_cast<int>(Status::transfer_failed);
-      abort_all();
-      return;
-    }
+    if (!recv_all(fd, base + item_off_[i] + off_of[b0], len)) return fail(Status::transfer_failed);
     received_ += len;
     // the bytes are in memory before the watermarks the GPU polls (x86
     // stores are ordered; the kernel reads the flag with ld.acquire.sys)
@@ -453,7 +493,6 @@ void StreamSource::receive_loop() {
     for (std::uint32_t b = b0; b < b0 + nb; ++b)
       __atomic_store_n(&flags[b], 1u, __ATOMIC_RELEASE);
   }
-  rx_status_ = 0;
 }
 
 void StreamSource::abort_all() {
@@ -476,14 +515,16 @@ std::pair<std::uint32_t, std::uint32_t> StreamSource::flag_summary() const {
 }
 
 void StreamSource::release(std::vector<std::unique_ptr<HostBuf>>* pool) {
-  if (rx_.joinable()) rx_.join();
+  for (auto& t : rx_)
+    if (t.joinable()) t.join();
   if (!pool) return;
   for (auto* b : {&data_, &tables_})
     if (*b && pool->size() < 4) pool->push_back(std::move(*b));
 }
 
 Status StreamSource::finish() {
-  if (rx_.joinable()) rx_.join();
+  for (auto& t : rx_)
+    if (t.joinable()) t.join();
   return static_cast<Status>(rx_status_.load());
 }
 

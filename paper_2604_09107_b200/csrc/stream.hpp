@@ -3,9 +3,10 @@
 // The reference's stream transport (transport_stream.hpp:36-76, the RSDP
 // wire) moves pull windows between hosts.  Here a process runs one
 // StreamServer; a reader whose assigned source endpoint is "tcp:host:port"
-// connects, names the serve state (model|replica|shard) and version, and
-// receives the source's chunk map and chunk-digest table followed by the
-// payload in watermark batches (the server D2H-copies each batch from the
+// opens a few connections (RSB_TCP_STREAMS, default 2), names the serve
+// state (model|replica|shard), version and its stripe on each, and receives
+// the source's chunk map and chunk-digest table (first connection) followed
+// by the payload in frames of watermark batches, frame k on connection k % n (the server D2H-copies each batch from the
 // source's device memory into pinned staging once the source has verified
 // it, so a chasing chain works across the wire too).  The reader lands the
 // stream into pinned, device-mapped host memory and raises a host watermark
@@ -15,6 +16,7 @@
 #pragma once
 
 #include <atomic>
+#include <chrono>
 #include <cstdint>
 #include <memory>
 #include <string>
@@ -86,15 +88,17 @@ class StreamSource {
   std::pair<std::uint32_t, std::uint32_t> flag_summary() const;
 
  private:
-  void receive_loop();
+  void receive_loop(int fd);
   void abort_all();
 
-  int fd_ = -1;
+  // one connection per stripe of the stream's frames (frame k on k % n);
+  // the first also carries the header
+  std::vector<int> fds_;
   std::unique_ptr<HostBuf> data_, tables_;
   SourceView view_;
   std::vector<std::uint64_t> item_off_;  // byte offset of each item in data_
-  std::thread rx_;
-  std::atomic<int> rx_status_{0};
+  std::vector<std::thread> rx_;
+  std::atomic<int> rx_status_{0};  // first failure of any connection
   std::atomic<std::uint64_t> received_{0};
 };
 
