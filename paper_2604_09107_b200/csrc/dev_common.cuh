@@ -40,6 +40,21 @@ __device__ __forceinline__ std::uint64_t xround_pre(std::uint64_t acc, std::uint
 __device__ __forceinline__ std::uint64_t xround(std::uint64_t acc, std::uint64_t w) {
   return xround_pre(acc, w * kP2);
 }
+// The chain carried one add ahead: y = acc + p holds the next round's
+// rotation input, and the following product is added inside the multiply
+// (wide multiply-add with a 64-bit addend), so the serial chain per round is
+// the rotation, one wide IMAD and one 3-input add:
+//   returns rotl64(y, 31) * P1 + p_next   (= the next y; p_next = 0 at the end: acc)
+__device__ __forceinline__ std::uint64_t xround_fused(std::uint64_t y, std::uint64_t p_next) {
+  const std::uint32_t lo = static_cast<std::uint32_t>(y), hi = static_cast<std::uint32_t>(y >> 32);
+  const std::uint32_t rlo = __funnelshift_l(hi, lo, 31);
+  const std::uint32_t rhi = __funnelshift_l(lo, hi, 31);
+  constexpr std::uint32_t p1lo = static_cast<std::uint32_t>(kP1);
+  constexpr std::uint32_t p1hi = static_cast<std::uint32_t>(kP1 >> 32);
+  const std::uint64_t wl = static_cast<std::uint64_t>(rlo) * p1lo + p_next;
+  const std::uint32_t h = static_cast<std::uint32_t>(wl >> 32) + rhi * p1lo + rlo * p1hi;
+  return (static_cast<std::uint64_t>(h) << 32) | static_cast<std::uint32_t>(wl);
+}
 __device__ __forceinline__ std::uint64_t avalanche(std::uint64_t h) {
   h ^= h >> 33;
   h *= kP2;

@@ -15,8 +15,10 @@ __global__ void chain(std::uint64_t* out, int rounds, int mode) {
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g0));
   if (mode == 0) {
     for (int i = 0; i < rounds; ++i) { acc = xround(acc, w); w += 0x9E37; }
-  } else {
+  } else if (mode == 1) {
     for (int i = 0; i < rounds; ++i) { acc = xround_pre(acc, w); w += 0x9E37; }
+  } else {  // fused: the next product added inside the multiply
+    for (int i = 0; i < rounds; ++i) { acc = xround_fused(acc, w); w += 0x9E37; }
   }
   long long t1 = clock64();
   std::uint64_t g1;
@@ -31,7 +33,7 @@ __global__ void chain(std::uint64_t* out, int rounds, int mode) {
 int main() {
   std::uint64_t* d;
   cudaMalloc(&d, 64 * 8);
-  for (int mode = 0; mode < 2; ++mode) {
+  for (int mode = 0; mode < 3; ++mode) {
     for (int lanes : {4, 32}) {
       int rounds = 1 << 24;
       chain<<<1, lanes>>>(d, rounds, mode);
