@@ -1242,6 +1242,10 @@ Status Client::launch_fill(Shard& sh, const SourceView& src, bool src_complete) 
                            src_complete ? nullptr : reinterpret_cast<const std::uint32_t*>(src.flags),
                            src.epoch, 0};
   const bool remote = src.device != sh.device;
+  // link class of the source (schedule order, kernel path): 0 local HBM,
+  // 1 host memory, 2 + d peer device d
+  const std::uint32_t link = !remote ? 0u : src.device < 0 ? 1u : static_cast<std::uint32_t>(src.device + 2);
+  for (auto& d : descs) d.pad = link;
   dev::PullParams pp{};
   RS_CUDA(dev::upload_pull_plan(sh.device, sh.stream, descs.data(),
                                 static_cast<std::uint32_t>(descs.size()), &sdesc, 1,
