@@ -350,6 +350,11 @@ class Client {
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     cudaStream_t poll = nullptr;  // progress reads while a fill runs
     DevBuf span_tables;           // copy_spans' span tables (grow-only: no per-call malloc/free)
+    // Copy-engine landing from host memory (launch_fill): frames copied on
+    // `dma`, each raising dma_flags[frame] = dma_epoch for the hash pass
+    cudaStream_t dma = nullptr;
+    DevBuf dma_flags;
+    std::uint32_t dma_epoch = 0;
     std::uint32_t epoch_ctr = 0;
     struct Lane {
       std::string key;
@@ -381,6 +386,7 @@ class Client {
   Status resolve_source(Shard& sh, const Assignment& a, VersionId v, SourceView* out,
                         double wait_s);
   Status launch_fill(Shard& sh, const SourceView& src, bool src_complete);
+  Status launch_host_dma(Shard& sh, const SourceView& src, std::uint32_t* epoch);
   Status run_replicate_loop(const OpOutcome& o, VersionId v);
 
   Registry* reg_;

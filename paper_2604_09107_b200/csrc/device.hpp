@@ -63,7 +63,7 @@ struct SrcDesc {
   const std::uint64_t* digests;  // source chunk-digest table (null: compute only)
   const std::uint32_t* flags;    // source watermarks (null: source complete)
   std::uint32_t epoch;           // source fill epoch to wait for
-  std::uint32_t pad;
+  std::uint32_t flag_shift;      // source batch b is covered by flags[b >> flag_shift]
 };
 
 enum PullCode : std::uint32_t {

@@ -124,7 +124,8 @@ __global__ void __launch_bounds__(kThreads, 2) pull_kernel(const PullParams p) {
     // chase the source watermark (every lane its own source batch)
     std::uint32_t code = kPullOk;
     if (sd && sd->flags)
-      code = wait_flag(&sd->flags[r.src_chunk / kBatchChunks], sd->epoch, p.timeout_ns, &p.work[1]);
+      code = wait_flag(&sd->flags[(r.src_chunk / kBatchChunks) >> sd->flag_shift], sd->epoch, p.timeout_ns,
+                       &p.work[1]);
     code = __reduce_max_sync(full, code);
     if (code != kPullOk) {
       if (lane == 0) {

@@ -214,16 +214,17 @@ __global__ void __launch_bounds__(C::kThreads, C::kCtas) pull_tma_kernel(const P
       const std::uint32_t sb0 = __shfl_sync(full, sbatch, 0);
       const std::uint32_t sid0 = __shfl_sync(full, src_id, 0);
       const bool need0 = __shfl_sync(full, sd != nullptr && sd->flags != nullptr, 0);
-      if (lane == 0 && need0) code = wait_flag(&sd->flags[sbatch], sd->epoch, p.timeout_ns, &p.work[1]);
+      if (lane == 0 && need0)
+        code = wait_flag(&sd->flags[sbatch >> sd->flag_shift], sd->epoch, p.timeout_ns, &p.work[1]);
       if (sd && sd->flags && (sbatch != sb0 || src_id != sid0) && lane != 0)
-        code = wait_flag(&sd->flags[sbatch], sd->epoch, p.timeout_ns, &p.work[1]);
+        code = wait_flag(&sd->flags[sbatch >> sd->flag_shift], sd->epoch, p.timeout_ns, &p.work[1]);
       const std::uint32_t worst = __reduce_max_sync(full, code);
       if (worst != kPullOk) {
         // diagnostics: the source batch and the watermark value that failed
         const unsigned bad_lanes = __ballot_sync(full, code == worst);
         const int bl = __ffs(bad_lanes) - 1;
         const std::uint32_t bsb = __shfl_sync(full, sbatch, bl);
-        const std::uint32_t bfv = (lane == bl && sd && sd->flags) ? ld_volatile(&sd->flags[sbatch]) : 0u;
+        const std::uint32_t bfv = (lane == bl && sd && sd->flags) ? ld_volatile(&sd->flags[sbatch >> sd->flag_shift]) : 0u;
         const std::uint32_t bflag = __shfl_sync(full, bfv, bl);
         if (lane == 0) {
           if (worst != kPullAborted) {

@@ -236,7 +236,7 @@ cudaError_t upload_pull_plan(int device, cudaStream_t s, ItemDesc* items, std::u
     // which the peer's HBM serves better than 32-row boxes of 128 bytes when
     // it is busy with its own pull (config 3 at N=2: 13.1 -> 12.3 ms with
     // every segment on slots); one-way and ring pulls are equal either way.
-    bool ok = !maps_disabled() && d.src && d.pad < 2 && c % kMapBoxCols == 0 && d.src % 16 == 0 &&
+    bool ok = !maps_disabled() && d.src && d.pad == 0 && c % kMapBoxCols == 0 && d.src % 16 == 0 &&
               d.dst % 16 == 0 && full >= 32 && (32 % q) == 0 && (full % q) == 0;
     if (ok) {
       auto* mp = reinterpret_cast<CUtensorMap*>(host.data() + maps_off + 256 * std::size_t(i));

@@ -1,0 +1,15 @@
+import torch, time
+n = 4 << 30
+h = torch.empty(n, dtype=torch.uint8).pin_memory()
+d = torch.empty(n, dtype=torch.uint8, device="cuda")
+for _ in range(2): d.copy_(h, non_blocking=True)
+torch.cuda.synchronize()
+e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+e0.record(); 
+for _ in range(5): d.copy_(h, non_blocking=True)
+e1.record(); torch.cuda.synchronize()
+print("h2d GB/s", 5 * n / (e0.elapsed_time(e1) / 1e3) / 1e9)
+e0.record();
+for _ in range(5): h.copy_(d, non_blocking=True)
+e1.record(); torch.cuda.synchronize()
+print("d2h GB/s", 5 * n / (e0.elapsed_time(e1) / 1e3) / 1e9)
