@@ -61,6 +61,11 @@ bool encode(CUtensorMap* map, std::uint64_t base, std::uint64_t c, std::uint64_t
 
 constexpr std::size_t kHdr = 128;  // work words (64 B) + PullStatus (32 B), padded
 
+bool peer_boxes() {  // A/B knob: tensor-map boxes for peer / host segments too
+  static const bool v = std::getenv("RSB_PEER_BOXES") != nullptr;
+  return v;
+}
+
 bool maps_disabled() {
   static const bool v = std::getenv("RSB_NO_MAPS") != nullptr;  // diagnostic knob
   return v;
@@ -236,7 +241,8 @@ cudaError_t upload_pull_plan(int device, cudaStream_t s, ItemDesc* items, std::u
     // which the peer's HBM serves better than 32-row boxes of 128 bytes when
     // it is busy with its own pull (config 3 at N=2: 13.1 -> 12.3 ms with
     // every segment on slots); one-way and ring pulls are equal either way.
-    bool ok = !maps_disabled() && d.src && d.pad == 0 && c % kMapBoxCols == 0 && d.src % 16 == 0 &&
+    bool ok = !maps_disabled() && d.src && (d.pad == 0 || peer_boxes()) && c % kMapBoxCols == 0 &&
+              d.src % 16 == 0 &&
               d.dst % 16 == 0 && full >= 32 && (32 % q) == 0 && (full % q) == 0;
     if (ok) {
       auto* mp = reinterpret_cast<CUtensorMap*>(host.data() + maps_off + 256 * std::size_t(i));
