@@ -111,14 +111,20 @@ def measured_peaks() -> dict:
     return {"hbm_gbs": 6650.0, "src": "fallback"}
 
 
-def ncu_traffic(kind: str):
-    """Per-launch DRAM bytes of the pull kernel from the committed ncu capture."""
+def ncu_traffic(kind: str, user_bytes: int = 0):
+    """Per-launch bytes of the pull kernel from the committed ncu captures:
+    DRAM bytes for a local pull ("local", "cast"); for a peer pull ("nvlink")
+    the bytes the reader's NVLink port receives (user data + read-response
+    protocol), scaled from the captured ratio to `user_bytes`."""
     p = os.path.join(ROOT, "profiles", "ncu_pull_summary.json")
     if not os.path.exists(p):
         return None
     try:
         with open(p) as f:
             d = json.load(f)
+        if kind == "nvlink":
+            r = d.get("nvlink", {}).get("link_rx_bytes_per_user_byte")
+            return round(r * user_bytes) if r and user_bytes else None
         return d.get(kind, {}).get("dram_bytes_per_launch")
     except (OSError, ValueError):
         return None

@@ -143,7 +143,10 @@ def run(args):
             "publish_s": round(publish_s, 4),
             "roofline": {"bound": "nvlink", "achieved": round(mean_rx, 1), "peak": 900.0,
                          "unit": "GB/s", "frac": round(mean_rx / 900.0, 4),
-                         "traffic": B.ncu_traffic("nvlink"), "peak_src": "nominal NVLink5 per direction "
+                         "traffic": B.ncu_traffic("nvlink", total),
+                         "traffic_src": "NVLink bytes received per launch (user + read-response protocol), "
+                                        "ncu nvlrx ratio from profiles/r1/ncu_nvlink_counters.json",
+                         "peak_src": "nominal NVLink5 per direction "
                          "(measured peer copy 777 GB/s)", "kernel": "pull_tma_kernel",
                          "kernel_ms_avg": round(statistics.mean(step_dev_ms), 3),
                          "alg_bytes_per_launch": total,
@@ -343,10 +346,17 @@ def run_ring(args):
             "weight_update_latency_s": round(wall_s / args.steps, 5),
             "publish_s": round(publish_s, 4),
             "roofline": {"bound": "nvlink", "achieved": round(mean_rx, 1), "peak": 900.0,
-                         "unit": "GB/s", "frac": round(mean_rx / 900.0, 4), "traffic": None,
+                         "unit": "GB/s", "frac": round(mean_rx / 900.0, 4),
+                         "traffic": B.ncu_traffic("nvlink", total),
+                         "traffic_src": "NVLink bytes received per launch (user + read-response protocol), "
+                                        "ncu nvlrx ratio from profiles/r1/ncu_nvlink_counters.json",
                          "peak_src": "nominal NVLink5 per direction", "kernel": "pull_tma_kernel",
                          "kernel_ms_avg": round(statistics.mean(step_dev_ms), 3),
-                         "alg_bytes_per_launch": total},
+                         "alg_bytes_per_launch": total,
+                         # every GPU of the ring sends and receives: read
+                         # responses + the requests of the pull out of it
+                         "protocol_peak": round(B.NVL_BOTH_WAYS, 1),
+                         "protocol_frac": round(mean_rx / B.NVL_BOTH_WAYS, 4)},
             "e2e": {"value": round(total_landed / wall_s / 1e9, 2), "unit": B.UNIT,
                     "h2d_bytes_per_step": None, "d2h_bytes_per_step": None,
                     "what": "wall clock of the collective replicate (plan+bind+IPC exchange+kernel)"},
@@ -820,6 +830,9 @@ def run_tp2_fanout(args):
         t_min = total / 900e9
         peaks = [a[1] / t_min / 1e9 for a in rx]
         frac = statistics.mean(x / p for x, p in zip(per_rx, peaks))
+        # the same bound with the read-response protocol on the trainer's egress
+        t_proto = total * (1 + B.NVL_RESP) / 900e9
+        proto_frac = statistics.mean(x / (a[1] / t_proto / 1e9) for x, a in zip(per_rx, rx))
         plan = sorted({f"{a.replica}<-{a.src}" for a in dc.assigns()})
         line = {
             "metric": B.METRIC, "value": round(total_landed / (sum(step_dev_ms) / 1e3) / 1e9, 2),
@@ -836,7 +849,11 @@ def run_tp2_fanout(args):
             "publish_s": round(publish_s, 4),
             "roofline": {"bound": "nvlink", "achieved": round(mean_rx, 1),
                          "peak": round(statistics.mean(peaks), 1),
-                         "unit": "GB/s", "frac": round(frac, 4), "traffic": None,
+                         "unit": "GB/s", "frac": round(frac, 4),
+                         "traffic": B.ncu_traffic("nvlink", max(a[1] for a in rx)),
+                         "protocol_frac": round(proto_frac, 4),
+                         "traffic_src": "NVLink bytes received per launch by the largest receiver "
+                                        "(user + read-response protocol), ncu nvlrx ratio",
                          "peak_src": "per receiver: its bytes / (model bytes / 900 GB/s nominal): "
                                      "the trainer's NVLink egress carries the whole model once; "
                                      "frac = mean of achieved/peak over receivers",
