@@ -623,6 +623,8 @@ using V12 = Cfg<512, 2, 1, 320, 4, 16>;  // V8, releasing 16 batches per fence
 using V13 = Cfg<512, 2, 1, 320, 4, 4, true>;  // V8 with dynamic batch claiming
 using V14 = Cfg<256, 4, 1, 320, 4, 4, true>;  // V9 (4 stages of 256 B) with dynamic claiming
 using V15 = Cfg<512, 3, 1, 0, 4, 4, true>;    // V7 (3 stages, segments in global), dynamic
+using V16 = Cfg<512, 2, 1, 320, 4, 1, true>;  // V13 releasing every batch at once
+using V17 = Cfg<512, 2, 1, 320, 4, 8, true>;  // V13 releasing 8 batches per fence
 
 int variant() {  // -1: by workload
   static const int v = [] {
@@ -660,6 +662,8 @@ cudaError_t launch_pull_tma(const PullParams& p, int sms, cudaStream_t s) {
     case 13: return launch_variant<V13>(p, sms, s);
     case 14: return launch_variant<V14>(p, sms, s);
     case 15: return launch_variant<V15>(p, sms, s);
+    case 16: return launch_variant<V16>(p, sms, s);
+    case 17: return launch_variant<V17>(p, sms, s);
     default: return launch_variant<V0>(p, sms, s);
   }
 }
