@@ -246,6 +246,48 @@ def test_gpu_reader_pulls_parked_version_from_host():
         assert t.lanes() == []
 
 
+@pytest.mark.gpu
+def test_corrupted_parked_version_fails_loudly():
+    """A byte flipped in the pinned host lane after parking: the copy engine
+    lands it, the pull kernel's chunk check catches it (the re-read sees the
+    same bad byte), and the replicate fails instead of handing out wrong
+    weights."""
+    import glob
+    import mmap
+    _need_gpu()
+    dev = torch.device("cuda:0")
+    with Cluster() as cl:
+        w = cl.open("m", "watcher", 1)
+        assert w.register_tensor(0, "w0", torch.zeros(4096, dtype=torch.uint8, device=dev)) == Status.ok
+        w.set_retention([0, 1])
+        assert w.connect() == Status.ok
+        t = cl.open("m", "trainer", 1, tiny_threshold=1 << 20)
+        tb = _tensors(dev, 30)
+        for i, x in enumerate(tb):
+            assert t.register_tensor(0, f"w{i}", x) == Status.ok
+        before = set(glob.glob(f"/dev/shm/rsb-{os.getpid()}-*"))
+        assert t.publish(1).status == Status.ok
+        assert t.unpublish().status == Status.ok
+        assert t.lanes() == [1]
+        lane = sorted(set(glob.glob(f"/dev/shm/rsb-{os.getpid()}-*")) - before,
+                      key=os.path.getsize)[-1]
+        with open(lane, "r+b") as f, mmap.mmap(f.fileno(), 0) as mm:
+            mm[1 << 20] ^= 0x40  # inside the first item
+        from paper_2604_09107_b200 import ros
+        for i, x in enumerate(tb):
+            ros.synth_bf16(x, 300 + i)
+        assert t.publish(2).status == Status.ok
+        r = cl.open("m", "reader", 1, tiny_threshold=1 << 20, pull_timeout_s=2.0)
+        for i, x in enumerate(tb):
+            assert r.register_tensor(0, f"w{i}", torch.zeros_like(x)) == Status.ok
+        res = r.replicate("1")
+        # the chunk check fails; the failure report condemns the only source
+        # of v1 (the reference: item_failed -> failure_report, client_core.cpp:336-357)
+        assert res.status in (Status.checksum_mismatch, Status.version_unavailable), res
+        assert r.stats().checksum_failures >= 1
+        assert not r.is_published
+
+
 def _free_port():
     s = socket.socket()
     s.bind(("127.0.0.1", 0))
