@@ -1300,8 +1300,7 @@ Status Client::launch_host_dma(Shard& sh, const SourceView& src, std::uint32_t* 
       RS_CUDA(cudaMemcpyAsync(reinterpret_cast<void*>(p.item_ptrs[i] + off),
                               reinterpret_cast<const void*>(src.item_ptrs[i] + off), end - off,
                               cudaMemcpyHostToDevice, sh.dma));
-      stats_.h2d_bytes += end - off;
-      off = end;
+      off = end;  // payload bytes: not in stats_.h2d_bytes (plans and tables), as on the SM path
     }
   }
   return flag_until(frames);
