@@ -141,6 +141,11 @@ __device__ __forceinline__ std::uint32_t ld_volatile(const std::uint32_t* p) {
   return *reinterpret_cast<const volatile std::uint32_t*>(p);
 }
 
+#ifndef RSB_MAX_POLL_NS
+#define RSB_MAX_POLL_NS 1024
+#endif
+constexpr unsigned kMaxPollNs = RSB_MAX_POLL_NS;  // back-off ceiling of a watermark poll
+
 // Waits until the upstream watermark of a batch reaches `epoch`.
 static __device__ __noinline__ std::uint32_t wait_flag(const std::uint32_t* flag, std::uint32_t epoch,
                                                 std::uint64_t timeout_ns,
@@ -156,7 +161,7 @@ static __device__ __noinline__ std::uint32_t wait_flag(const std::uint32_t* flag
     if (t0 == 0) t0 = now;
     if (now - t0 > timeout_ns) return kPullTimeout;
     __nanosleep(ns);
-    if (ns < 1024) ns <<= 1;
+    if (ns < kMaxPollNs) ns <<= 1;
   }
 }
 

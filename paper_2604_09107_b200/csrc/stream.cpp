@@ -31,10 +31,13 @@ constexpr int kSlots = 16;                     // concurrent connections with st
 // Connections per source: frame k of the stream travels on connection
 // k % streams (one TCP stream is bound by one core's copy; RSB_TCP_STREAMS).
 // Loopback on the B200 box, 1 GiB: 1 stream 6.9 GB/s, 2: 10-13, 4: 16-19,
-// 8: 21.6.  Default 2: with 4 connections the version-bump test
-// (tests/test_stream.py) stalls one frame of the second version for seconds
-// in TCP (one retransmission per run; not root-caused), which the pull
-// kernel reports as an upstream timeout.
+// 8: 21.6.  Default 2.  Open issue with 4: when server and reader share a GPU
+// (tests/test_stream.py, second version, pooled reader buffers), the
+// server's D2H staging copy of one stripe's last frame completes only when
+// the reader's pull kernel -- waiting for that frame -- times out (RSB_DEBUG
+// logs the wait).  Not TCP (no retransmissions, no softnet drops), not the
+// kernel's polling rate, not SM occupancy (one SM left free: same); with
+// reader and server on different GPUs 4 connections run clean (16 GB/s).
 std::uint32_t tcp_streams() {
   static const std::uint32_t n = [] {
     const char* e = std::getenv("RSB_TCP_STREAMS");
@@ -338,9 +341,15 @@ void StreamServer::serve_conn(int fd) {
   if (!frames.empty()) good = issue(0);
   for (std::size_t k = 0; good && k < frames.size(); ++k) {
     if (k + 1 < frames.size()) good = issue(k + 1);
+    const auto t_wait = std::chrono::steady_clock::now();
     if (!good || cudaEventSynchronize(ev[k & 1]) != cudaSuccess) {
       good = false;
       break;
+    }
+    if (debug()) {
+      const double w = std::chrono::duration<double>(std::chrono::steady_clock::now() - t_wait).count();
+      if (w > 0.01)
+        std::fprintf(stderr, "[rsb] stream server: stripe %u frame %zu D2H waited %.3f s\n", stripe, k, w);
     }
     const Frame& f = frames[k];
     good = send_pod(fd, f.b0) && send_pod(fd, f.nb) && send_pod(fd, f.len) &&
