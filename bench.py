@@ -467,7 +467,8 @@ def host_e2e(cl, t, r, stream, total, tarena, rarena, args):
             "d2h_bytes_per_step": (st.d2h_bytes - d2h0) // max(steps, 1),
             "what": "rs_replicate wall clock per step with the version in pinned HOST memory "
                     "(a retention offload): every byte crosses host->device inside the timed "
-                    "region (PCIe), read by the pull kernel and verified; status read back"}
+                    "region (PCIe: copy-engine frames into the landing regions, verified in place "
+                    "by the pull kernel); status read back"}
 
 
 def run_reference(args):
