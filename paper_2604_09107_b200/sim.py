@@ -24,8 +24,9 @@ class LinkModel:
     nvlink_one_way: float = 785e9   # bytes/s, one direction busy (profiles/r1/nvlink_dir_v*.json)
     nvlink_both_ways: float = 672e9  # bytes/s per direction, both busy
     hbm: float = 6544e9             # bytes/s, measured copy (MEASURED_PEAKS.json)
-    hbm_efficiency: float = 0.92    # fused copy+verify+watermarks vs a plain copy (bench N=1)
-    pcie: float = 50.8e9            # bytes/s, pull from pinned host memory (tools/offload_probe.py)
+    hbm_efficiency: float = 0.999   # fused copy+verify+watermarks vs a plain copy (bench N=1)
+    pcie: float = 54.9e9            # bytes/s, pull from pinned host memory: copy-engine frames
+                                    # verified in place (tools/offload_probe.py)
 
 
 @dataclass
