@@ -1357,8 +1357,16 @@ Status Client::launch_fill(Shard& sh, const SourceView& src, bool src_complete) 
   pp.timeout_ns = static_cast<std::uint64_t>(cfg_.pull_timeout_s * 1e9);
   pp.resume = p.landed_some ? 1u : 0u;
   pp.remote = remote ? 1u : 0u;
+  sh.t_launch = std::chrono::steady_clock::now();
   RS_CUDA(dev::launch_pull(pp, dev::pull_grid(sh.device), sh.stream));
-  RS_CUDA(cudaEventRecord(sh.ev1, sh.stream));
+  // A fill fed over TCP waits on progress that may need this GPU's copy
+  // engines (a StreamServer in this process staging a frame D2H).  Nothing
+  // is queued behind its kernel: an event record or copy waiting on the
+  // kernel can hold a hardware work queue that the server's copy shares,
+  // and that copy would then wait for the kernel that waits for it (seen
+  // with 4 connections and reader + server on one GPU: the frame moved only
+  // when the kernel timed out).  wait_shards times it on the host.
+  if (!sh.tcp) RS_CUDA(cudaEventRecord(sh.ev1, sh.stream));
   sh.holding->landed_some = true;
   return Status::ok;
 }
@@ -1450,6 +1458,12 @@ std::vector<Client::FillOutcome> Client::wait_shards(const std::vector<std::uint
     Shard& sh = shards_[i];
     DeviceGuard g(sh.device);
     auto* status = reinterpret_cast<dev::PullStatus*>(static_cast<std::uint8_t*>(sh.plan.scratch) + 64);
+    const bool tcp = sh.tcp != nullptr;
+    float host_ms = 0;
+    if (tcp) {  // nothing queued behind the kernel (launch_fill): wait, then read
+      cudaStreamSynchronize(sh.stream);
+      host_ms = std::chrono::duration<float, std::milli>(std::chrono::steady_clock::now() - sh.t_launch).count();
+    }
     cudaMemcpyAsync(&st[i], status, sizeof(dev::PullStatus), cudaMemcpyDeviceToHost, sh.stream);
     cudaError_t e = cudaStreamSynchronize(sh.stream);
     stats_.d2h_bytes += sizeof(dev::PullStatus);
@@ -1475,8 +1489,8 @@ std::vector<Client::FillOutcome> Client::wait_shards(const std::vector<std::uint
       out[i] = {Status::transfer_failed, 0, 0};
       continue;
     }
-    float ms = 0;
-    cudaEventElapsedTime(&ms, sh.ev0, sh.ev1);
+    float ms = host_ms;
+    if (!tcp) cudaEventElapsedTime(&ms, sh.ev0, sh.ev1);
     stats_.last_pull_ms = ms;
     stats_.last_pull_bytes = st[i].bytes;
     stats_.fill_max_ms = std::max(stats_.fill_max_ms, ms);

@@ -19,6 +19,7 @@
 #include <cuda_runtime.h>
 
 #include <atomic>
+#include <chrono>
 #include <cstdint>
 #include <map>
 #include <memory>
@@ -348,6 +349,7 @@ class Client {
     dev::PlanUpload hash_plan;  // hash-only passes (publish, reshard groups): kept apart so
                                 // the fill plan stays resident between fills
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    std::chrono::steady_clock::time_point t_launch;  // host clock of the fill's launch
     cudaStream_t poll = nullptr;  // progress reads while a fill runs
     DevBuf span_tables;           // copy_spans' span tables (grow-only: no per-call malloc/free)
     // Copy-engine landing from host memory (launch_fill): frames copied on

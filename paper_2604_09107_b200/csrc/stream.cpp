@@ -31,17 +31,14 @@ constexpr int kSlots = 16;                     // concurrent connections with st
 // Connections per source: frame k of the stream travels on connection
 // k % streams (one TCP stream is bound by one core's copy; RSB_TCP_STREAMS).
 // Loopback on the B200 box, 1 GiB: 1 stream 6.9 GB/s, 2: 10-13, 4: 16-19,
-// 8: 21.6.  Default 2.  Open issue with 4: when server and reader share a GPU
-// (tests/test_stream.py, second version, pooled reader buffers), the
-// server's D2H staging copy of one stripe's last frame completes only when
-// the reader's pull kernel -- waiting for that frame -- times out (RSB_DEBUG
-// logs the wait).  Not TCP (no retransmissions, no softnet drops), not the
-// kernel's polling rate, not SM occupancy (one SM left free: same); with
-// reader and server on different GPUs 4 connections run clean (16 GB/s).
+// 8: 21.6.  (A same-GPU stall with 4 connections was a hardware work queue
+// shared by the server's staging copy and an event queued behind the
+// reader's waiting kernel; Client::launch_fill queues nothing behind a
+// TCP-fed kernel.)
 std::uint32_t tcp_streams() {
   static const std::uint32_t n = [] {
     const char* e = std::getenv("RSB_TCP_STREAMS");
-    const int v = e ? std::atoi(e) : 2;
+    const int v = e ? std::atoi(e) : 4;
     return static_cast<std::uint32_t>(std::clamp(v, 1, 8));
   }();
   return n;

@@ -3,7 +3,7 @@
 // The reference's stream transport (transport_stream.hpp:36-76, the RSDP
 // wire) moves pull windows between hosts.  Here a process runs one
 // StreamServer; a reader whose assigned source endpoint is "tcp:host:port"
-// opens a few connections (RSB_TCP_STREAMS, default 2), names the serve
+// opens a few connections (RSB_TCP_STREAMS, default 4), names the serve
 // state (model|replica|shard), version and its stripe on each, and receives
 // the source's chunk map and chunk-digest table (first connection) followed
 // by the payload in frames of watermark batches, frame k on connection k % n (the server D2H-copies each batch from the
