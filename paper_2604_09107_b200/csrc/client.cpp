@@ -1356,7 +1356,9 @@ Status Client::launch_fill(Shard& sh, const SourceView& src, bool src_complete) 
   pp.dst_epoch = p.epoch;
   pp.timeout_ns = static_cast<std::uint64_t>(cfg_.pull_timeout_s * 1e9);
   pp.resume = p.landed_some ? 1u : 0u;
-  pp.remote = remote ? 1u : 0u;
+  // 2: a plain peer pull (no cast, the chain's hops): the kernel shape that
+  // releases every verified batch at once, so a chaser downstream sees it sooner
+  pp.remote = dma || !remote ? 0u : (src.device >= 0 && !any_cast) ? 2u : 1u;
   sh.t_launch = std::chrono::steady_clock::now();
   RS_CUDA(dev::launch_pull(pp, dev::pull_grid(sh.device), sh.stream));
   // A fill fed over TCP waits on progress that may need this GPU's copy

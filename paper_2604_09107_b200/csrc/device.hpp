@@ -101,7 +101,8 @@ struct PullParams {
   std::uint32_t has_cast;            // some segment lands as e4m3 (kernel shape choice)
   const void* maps;                  // CUtensorMap pairs per segment (or null)
   const std::uint32_t* batch_seg;    // per batch: last segment with chunk0 <= 32*batch
-  std::uint32_t remote;              // some source is another GPU's HBM (kernel shape choice)
+  std::uint32_t remote;              // 0 local / host, 1 some source is a peer GPU, 2 a plain
+                                     // peer pull (identity, no cast): kernel shape choice
   // Schedule: positions 0..n_sched-1 map to batches order[pos] (first_batch
   // then unused); null order: batches first_batch..n_batches-1 in order.
   // The order lists only the batches some segment touches (a hash pass over

@@ -639,13 +639,17 @@ int variant() {  // -1: by workload
 cudaError_t launch_pull_tma(const PullParams& p, int sms, cudaStream_t s) {
   // Default V13: one CTA per SM with four producer/consumer pipelines (two
   // stages each), so the four hashing warps sit on the four sub-partitions,
-  // claiming batches dynamically.  Measured on B200: local plain pull 99.9%
+  // claiming batches dynamically.  A plain peer pull (remote == 2: a chain
+  // hop) takes V16, the same shape releasing every verified batch at once:
+  // the chaser behind it sees batches sooner (config 2 N=4 last hop
+  // 646-649 -> 653-657 GB/s), while local cast and reshard pulls lose 8-15%
+  // with per-batch fences and stay on V13.  Measured on B200: local plain pull 99.9%
   // of the measured HBM copy peak (V8, the same shape on a static stride:
   // 91-92%, its fastest pipelines idling at the tail; V0, 3 two-warp CTAs:
   // 88-90%), FSDP-8 -> TP-2 reshard 97.5% (V8: 91%); over NVLink equal to V8
   // (785 GB/s one way, 672 with both directions busy).
   int v = variant();
-  if (v < 0) v = 13;
+  if (v < 0) v = p.remote == 2 ? 16 : 13;
   switch (v) {
     case 1: return launch_variant<V1>(p, sms, s);
     case 2: return launch_variant<V2>(p, sms, s);
