@@ -352,6 +352,7 @@ class Client {
     std::chrono::steady_clock::time_point t_launch;  // host clock of the fill's launch
     cudaStream_t poll = nullptr;  // progress reads while a fill runs
     DevBuf span_tables;           // copy_spans' span tables (grow-only: no per-call malloc/free)
+    DevBuf dig_tables, group_tables;  // publish: K6 span tables (grow-only)
     // Copy-engine landing from host memory (launch_fill): frames copied on
     // `dma`, each raising dma_flags[frame] = dma_epoch for the hash pass
     cudaStream_t dma = nullptr;
