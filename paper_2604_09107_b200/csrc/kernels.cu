@@ -232,7 +232,7 @@ __global__ void __launch_bounds__(kThreads, 2) pull_kernel(const PullParams p) {
 // B200 (tools/micro/xxh_chain.cu), so a span hashes at most ~2.27 GB/s.  To
 // keep the chain itself the only thing on the critical path, a span gets a
 // warp pair:
-//   feeder warp   lane 0 streams the span through a ring of 4 KiB slots (one
+//   feeder warp   lane 0 streams the span through a ring of 16 KiB slots (one
 //                 cp.async.bulk per slot); all 32 lanes then replace every
 //                 word of a landed slot by its product w * P2 (the part of
 //                 round64 that does not depend on the accumulator)
@@ -243,8 +243,8 @@ __global__ void __launch_bounds__(kThreads, 2) pull_kernel(const PullParams p) {
 // global memory.  A span that is not 16-byte aligned is hashed by the chain
 // warp straight from global memory.
 constexpr int kDigSpans = 4;  // warp pairs per CTA
-constexpr int kDigSlot = 4096;
-constexpr int kDigSlots = 8;
+constexpr int kDigSlot = 16384;
+constexpr int kDigSlots = 3;
 
 __global__ void __launch_bounds__(kDigSpans * 64)
     span_digest_kernel(const std::uint64_t* ptrs, const std::uint64_t* lens, std::uint64_t* out,
