@@ -25,7 +25,7 @@
 extern "C" {
 #endif
 
-#define RS_ABI_VERSION 1
+#define RS_ABI_VERSION 2
 
 typedef struct rs_cluster rs_cluster; /* ServerCore + ServeRegistry of this process */
 typedef struct rs_handle rs_handle;   /* ClientCore: one replica's shard handles   */
@@ -41,6 +41,10 @@ typedef struct {
   double pull_timeout_s;   /* upstream silence before a failure report (default 4)  */
   char datacenter[32];     /* ClientConfig.datacenter (default "dc0")                */
   uint32_t reshard_align;  /* chunk rule: TP splits up to this stay chunk aligned (2) */
+  uint32_t grid_sms;       /* SMs a fill's persistent pull kernel may occupy (0: all).
+                            * Fills whose caps sum to <= the SM count co-reside on one
+                            * GPU, so a reader may chase an upstream filling on its own
+                            * GPU instead of waiting for it to complete.              */
 } rs_config;
 
 /* Assignment (reference messages.hpp:40-52) minus the manifest bytes, which
@@ -221,6 +225,11 @@ int rs_transfer_fill(rs_handle* h, int* statuses, int* reasons);
 int rs_transfer_launch(rs_handle* h);
 int rs_transfer_progress(rs_handle* h, uint32_t shard, uint32_t* batches_done, uint32_t* n_batches);
 int rs_transfer_wait(rs_handle* h, int* statuses, int* reasons);
+/* The assignment the shard's latest fill was launched on (Assignment,
+ * messages.hpp:40-52): its source, and whether that source was complete or
+ * a pipeline copy still filling (source_complete == 0: the fill chased the
+ * source's watermarks).  not_found before any launch. */
+int rs_transfer_assignment(rs_handle* h, uint32_t shard, rs_assignment* out);
 int rs_transfer_finish(rs_handle* h, uint64_t version, int ok);
 /* Cross-process serve state (CUDA IPC handles + watermarks). */
 int rs_serve_export(rs_handle* h, uint32_t shard, void* buf, size_t cap, size_t* len);

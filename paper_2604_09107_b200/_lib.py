@@ -25,7 +25,8 @@ cstr = C.c_char_p
 class RsConfig(C.Structure):
     _fields_ = [("chunk_bytes", u64), ("tiny_threshold", u64), ("group_target", u64),
                 ("pipeline", i32), ("checksum_retries", i32), ("pull_timeout_s", dbl),
-                ("datacenter", C.c_char * 32), ("reshard_align", u32)]
+                ("datacenter", C.c_char * 32), ("reshard_align", u32),
+                ("grid_sms", u32)]
 
 
 class RsAssignment(C.Structure):
@@ -79,6 +80,7 @@ _SIGS = {
     "rs_transfer_launch": (i32, [vp]),
     "rs_transfer_progress": (i32, [vp, u32, C.POINTER(u32), C.POINTER(u32)]),
     "rs_transfer_wait": (i32, [vp, vp, vp]),
+    "rs_transfer_assignment": (i32, [vp, u32, C.POINTER(RsAssignment)]),
     "rs_shard_hash": (i32, [vp, u32, C.POINTER(u64), C.POINTER(i32), C.POINTER(i32)]),
     "rs_combine_layout_key": (i32, [u32, vp, vp, vp, vp, sz, C.POINTER(sz)]),
     "rs_chunk_len_for": (u32, [u64, u64, u64, u32]),

@@ -53,6 +53,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     for src in sources():
         obj = os.path.join(OUT_DIR, "obj", os.path.basename(src) + ".o")
         cmd = [nvcc(), *ARCH, *COMMON, "-c", src, "-o", obj]
+        if os.environ.get("RSB_ALL_VARIANTS") == "1":  # the diagnostic kernel shapes (pull_tma.cu)
+            cmd.insert(1, "-DRSB_ALL_VARIANTS")
         if src.endswith(".cu") and verbose:
             cmd += ["-Xptxas", "-v"]
         procs.append((cmd, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT)))

@@ -60,6 +60,7 @@ rsb::ClientConfig to_cfg(const rs_config* c) {
   if (c->pull_timeout_s > 0) cfg.pull_timeout_s = c->pull_timeout_s;
   if (c->datacenter[0]) cfg.dc = std::string(c->datacenter, strnlen(c->datacenter, 32));
   if (c->reshard_align) cfg.reshard_align = c->reshard_align;
+  cfg.grid_sms = c->grid_sms;
   return cfg;
 }
 
@@ -109,6 +110,7 @@ void rs_config_default(rs_config* cfg) {
   cfg->pull_timeout_s = d.pull_timeout_s;
   std::strncpy(cfg->datacenter, d.dc.c_str(), sizeof(cfg->datacenter) - 1);
   cfg->reshard_align = d.reshard_align;
+  cfg->grid_sms = d.grid_sms;
 }
 
 int rs_cluster_create(int pipeline, int smart_skipping, rs_cluster** out) {
@@ -538,6 +540,14 @@ int rs_transfer_launch(rs_handle* h) {
 int rs_transfer_progress(rs_handle* h, uint32_t shard, uint32_t* batches_done, uint32_t* n_batches) {
   if (!h || !batches_done || !n_batches) return st(rsb::Status::invalid_argument);
   return st(h->client->progress(shard, batches_done, n_batches));
+}
+
+int rs_transfer_assignment(rs_handle* h, uint32_t shard, rs_assignment* out) {
+  if (!h || !out || shard >= h->client->num_shards()) return st(rsb::Status::invalid_argument);
+  const rsb::Assignment* a = h->client->launched_assignment(shard);
+  if (!a) return st(rsb::Status::not_found);
+  fill_assignment(*a, out);
+  return 0;
 }
 
 int rs_transfer_wait(rs_handle* h, int* statuses, int* reasons) {

@@ -700,6 +700,11 @@ void Client::set_stream(std::uint32_t shard, cudaStream_t s) {
   sh.own_stream = false;
 }
 
+int Client::grid(const Shard& sh) const {
+  const int sms = dev::pull_grid(sh.device);
+  return cfg_.grid_sms ? std::min<int>(sms, static_cast<int>(cfg_.grid_sms)) : sms;
+}
+
 Status Client::ensure_stream(Shard& sh) {
   if (sh.device < 0) return Status::invalid_state;
   DeviceGuard g(sh.device);
@@ -869,7 +874,7 @@ Status Client::hash_items(Shard& sh, Payload& p, const std::vector<std::uint32_t
   pp.dst_flags = static_cast<std::uint32_t*>(p.flags.p);
   pp.dst_epoch = p.epoch;
   pp.timeout_ns = static_cast<std::uint64_t>(cfg_.pull_timeout_s * 1e9);
-  RS_CUDA(dev::launch_pull(pp, dev::pull_grid(sh.device), sh.stream));
+  RS_CUDA(dev::launch_pull(pp, grid(sh), sh.stream));
   stats_.h2d_bytes += sh.hash_plan.h2d_bytes;
   return Status::ok;
 }
@@ -1023,7 +1028,10 @@ Status Client::resolve_source(Shard& sh, const Assignment& a, VersionId v, Sourc
         // A persistent pull kernel holds every SM of its GPU, so a chaser on
         // the upstream's own GPU could start first, spin, and starve the fill
         // it waits for: on one GPU the chase waits for the upstream instead.
-        same_gpu_filling = !st->imported && st->device == sh.device && !st->complete;
+        // A capped grid (rs_config.grid_sms) is the caller's promise that
+        // the two fills co-reside, so the chase runs concurrently.
+        same_gpu_filling = !st->imported && st->device == sh.device && !st->complete &&
+                           cfg_.grid_sms == 0;
       }
       if (ready && !same_gpu_filling) return map_source(st, sh.device, out);
       if (ready) deadline = std::max(deadline, std::chrono::steady_clock::now() +
@@ -1059,22 +1067,11 @@ Status Client::bind(Shard& sh, const Assignment& a, VersionId v) {
   auto p = std::make_shared<Payload>();
   p->manifest = std::move(*mr);
   p->encoded = a.manifest;
-  for (std::size_t gi = 0; gi < p->manifest.groups.size(); ++gi) {
-    // group staging of the drained payload being replaced is taken over
-    // (no cudaFree / cudaMalloc on the update path; see alloc_tables)
-    std::unique_ptr<DevBuf> buf;
-    if (sh.holding && gi < sh.holding->group_bufs.size() && sh.holding->group_bufs[gi] &&
-        sh.holding->group_bufs[gi]->dev == sh.device)
-      buf = std::move(sh.holding->group_bufs[gi]);
-    else
-      buf = std::make_unique<DevBuf>();
-    if (Status s = buf->alloc(sh.device, p->manifest.groups[gi].packed_length); !ok(s)) return s;
-    p->group_bufs.push_back(std::move(buf));
-  }
   const auto& items = p->manifest.items();
-  // The chunk map is a pure function of (manifest, the publisher's chunk
-  // lengths), so a reader can serve its own fill before its source is even
-  // reachable.
+  // Everything that can reject the assignment is checked before any buffer
+  // is taken over from the payload being replaced.  The chunk map is a pure
+  // function of (manifest, the publisher's chunk lengths), so a reader can
+  // serve its own fill before its source is even reachable.
   if (!a.layout.empty()) {
     auto lay = ShardLayout::decode(a.layout);
     if (!lay || lay->chunk_len.size() != items.size()) return Status::protocol_error;
@@ -1082,6 +1079,32 @@ Status Client::bind(Shard& sh, const Assignment& a, VersionId v) {
     p->layout = a.layout;
   } else {
     p->cmap = ChunkMap::uniform(p->manifest, cfg_.chunk_bytes);
+  }
+  // Buffers taken over from the drained payload go back to it if a later
+  // step fails, so its serve state never points at freed memory.
+  std::vector<std::size_t> taken;  // group indices whose staging came from sh.holding
+  auto give_back = [&](Status st) {
+    if (sh.holding) {
+      for (std::size_t gi : taken)
+        if (p->group_bufs[gi]) sh.holding->group_bufs[gi] = std::move(p->group_bufs[gi]);
+      if (p->digests.p && !sh.holding->digests.p) sh.holding->digests = std::move(p->digests);
+      if (p->flags.p && !sh.holding->flags.p) sh.holding->flags = std::move(p->flags);
+    }
+    return st;
+  };
+  for (std::size_t gi = 0; gi < p->manifest.groups.size(); ++gi) {
+    // group staging of the drained payload being replaced is taken over
+    // (no cudaFree / cudaMalloc on the update path; see alloc_tables)
+    p->group_bufs.push_back(nullptr);
+    if (sh.holding && gi < sh.holding->group_bufs.size() && sh.holding->group_bufs[gi] &&
+        sh.holding->group_bufs[gi]->dev == sh.device) {
+      p->group_bufs.back() = std::move(sh.holding->group_bufs[gi]);
+      taken.push_back(gi);
+    } else {
+      p->group_bufs.back() = std::make_unique<DevBuf>();
+    }
+    if (Status s = p->group_bufs.back()->alloc(sh.device, p->manifest.groups[gi].packed_length); !ok(s))
+      return give_back(s);
   }
   p->item_ptrs.resize(items.size());
   for (std::size_t i = 0; i < items.size(); ++i) {
@@ -1091,8 +1114,8 @@ Status Client::bind(Shard& sh, const Assignment& a, VersionId v) {
                     : reinterpret_cast<std::uint64_t>(
                           sh.regs[sh.by_name.at(p->manifest.entries[it.index].name)].ptr);
   }
-  if (Status s = alloc_tables(sh, *p, 0); !ok(s)) return s;
-  RS_CUDA(cudaStreamSynchronize(sh.stream));
+  if (Status s = alloc_tables(sh, *p, 0); !ok(s)) return give_back(s);
+  if (cudaStreamSynchronize(sh.stream) != cudaSuccess) return give_back(Status::transfer_failed);
   p->epoch = ++sh.epoch_ctr;
   sh.holding = std::move(p);
   sh.partial_version = v;
@@ -1348,7 +1371,11 @@ Status Client::launch_fill(Shard& sh, const SourceView& src, bool src_complete) 
   const bool remote = src.device != sh.device;
   // A complete source in host memory lands through the copy engine (no cast:
   // the engine cannot convert); the kernel verifies the landed bytes in place.
-  const bool dma = src.device < 0 && src_complete && !any_cast && host_dma_enabled() && write_value32();
+  // A resumed epoch (landed_some: an earlier attempt verified some batches)
+  // takes the SM path, which skips the landed batches: the engine would copy
+  // every frame again, over bytes already verified, and nothing re-checks them.
+  const bool dma = src.device < 0 && src_complete && !any_cast && !p.landed_some &&
+                   host_dma_enabled() && write_value32();
   if (dma) {
     for (std::size_t i = 0; i < items.size(); ++i) {
       descs[i].src = p.item_ptrs[i];
@@ -1364,7 +1391,12 @@ Status Client::launch_fill(Shard& sh, const SourceView& src, bool src_complete) 
   RS_CUDA(cudaEventRecord(sh.ev0, sh.stream));
   if (dma) {
     std::uint32_t epoch = 0;
-    if (Status s = launch_host_dma(sh, src, &epoch); !ok(s)) return s;
+    sh.dma_fill = true;  // wait_shards drains sh.dma before anything else touches the regions
+    if (Status s = launch_host_dma(sh, src, &epoch); !ok(s)) {
+      cudaStreamSynchronize(sh.dma);
+      sh.dma_fill = false;
+      return s;
+    }
     sdesc.flags = static_cast<const std::uint32_t*>(sh.dma_flags.p);
     sdesc.epoch = epoch;
   }
@@ -1382,7 +1414,7 @@ Status Client::launch_fill(Shard& sh, const SourceView& src, bool src_complete) 
   // releases every verified batch at once, so a chaser downstream sees it sooner
   pp.remote = dma || !remote ? 0u : (src.device >= 0 && !any_cast) ? 2u : 1u;
   sh.t_launch = std::chrono::steady_clock::now();
-  RS_CUDA(dev::launch_pull(pp, dev::pull_grid(sh.device), sh.stream));
+  RS_CUDA(dev::launch_pull(pp, grid(sh), sh.stream));
   // A fill fed over TCP waits on progress that may need this GPU's copy
   // engines (a StreamServer in this process staging a frame D2H).  Nothing
   // is queued behind its kernel: an event record or copy waiting on the
@@ -1407,9 +1439,11 @@ void Client::launch_shards(const std::vector<Assignment>& as,
   launched_.assign(num_shards_, false);
   auto& out = launch_out_;
   auto& launched = launched_;
+  if (launch_as_.size() != num_shards_) launch_as_.resize(num_shards_);
   for (std::uint32_t i : which) {
     Shard& sh = shards_[i];
     const Assignment& a = as[i];
+    launch_as_[i] = a;
     if (sh.holding && sh.holding->reshard) {
       Status s = a.reshard ? launch_reshard_fill(sh, a, a.source_complete)
                            : Status::protocol_error;
@@ -1493,7 +1527,7 @@ std::vector<Client::FillOutcome> Client::wait_shards(const std::vector<std::uint
     stats_.d2h_bytes += sizeof(dev::PullStatus);
     Status net = Status::ok;
     if (sh.tcp) {
-      net = sh.tcp->finish();
+      net = sh.tcp->finish(e == cudaSuccess && st[i].code == dev::kPullOk);
       if (std::getenv("RSB_DEBUG") && st[i].code != dev::kPullOk) {
         auto fs = sh.tcp->flag_summary();
         std::fprintf(stderr, "[rsb] tcp source: %u of %u watermarks set, first missing %u, %llu bytes\n",
@@ -1502,6 +1536,14 @@ std::vector<Client::FillOutcome> Client::wait_shards(const std::vector<std::uint
       }
       sh.tcp->release(&host_pool_);
       sh.tcp.reset();
+    }
+    if (sh.dma_fill) {
+      // Copy-engine frames of a host-fed fill: a kernel that stopped early
+      // (bad chunk, timeout) leaves frames queued on sh.dma.  Drain them
+      // before a retry lands anything (possibly from another source, on
+      // sh.stream) and before the lane's pinned buffer can be released.
+      if (cudaStreamSynchronize(sh.dma) != cudaSuccess && e == cudaSuccess) e = cudaErrorUnknown;
+      sh.dma_fill = false;
     }
     if (e == cudaSuccess && !ok(net) && st[i].code == dev::kPullOk) st[i].code = dev::kPullNotServing;
     if (std::getenv("RSB_DEBUG") && (st[i].code != dev::kPullOk || e != cudaSuccess))
@@ -1679,7 +1721,7 @@ Status Client::launch_reshard_fill(Shard& sh, const Assignment& a, bool src_comp
   pp.resume = p.landed_some ? 1u : 0u;
   pp.remote = remote ? 1u : 0u;
   RS_CUDA(cudaEventRecord(sh.ev0, sh.stream));
-  RS_CUDA(dev::launch_pull(pp, dev::pull_grid(sh.device), sh.stream));
+  RS_CUDA(dev::launch_pull(pp, grid(sh), sh.stream));
   RS_CUDA(cudaEventRecord(sh.ev1, sh.stream));
   p.landed_some = true;
   return Status::ok;

@@ -47,6 +47,7 @@ struct ClientConfig {
   double pull_timeout_s = 4.0;       // upstream silence before reporting
   std::string dc = "dc0";
   std::uint32_t reshard_align = 2;   // chunk rule: TP splits up to this stay chunk aligned
+  std::uint32_t grid_sms = 0;        // SMs a fill's persistent kernel may occupy (0: all)
 };
 
 // Owned device allocation.
@@ -274,6 +275,10 @@ class Client {
   void launch_shards(const std::vector<Assignment>& a, const std::vector<std::uint32_t>& which);
   std::vector<FillOutcome> wait_shards(const std::vector<std::uint32_t>& which);
   Status progress(std::uint32_t shard, std::uint32_t* batches_done, std::uint32_t* n_batches);
+  // The assignment the shard's latest fill was launched on (null: none yet).
+  const Assignment* launched_assignment(std::uint32_t shard) const {
+    return shard < launch_as_.size() && launch_as_[shard] ? &*launch_as_[shard] : nullptr;
+  }
   void finish_transfers(VersionId v, bool ok);
   void stop_serving();
   // Forget held bytes: the next fill of any version re-pulls everything
@@ -358,6 +363,7 @@ class Client {
     cudaStream_t dma = nullptr;
     DevBuf dma_flags;
     std::uint32_t dma_epoch = 0;
+    bool dma_fill = false;  // the launched fill is fed by frames on `dma`
     std::uint32_t epoch_ctr = 0;
     struct Lane {
       std::string key;
@@ -372,6 +378,7 @@ class Client {
   Status settle_offload(OpOutcome* o, double wait_s);
 
   Status ensure_stream(Shard& sh);
+  int grid(const Shard& sh) const;  // SMs this handle's persistent kernels occupy
   Status build_payload(Shard& sh, VersionId v, std::shared_ptr<Payload>* out);
   Status bind(Shard& sh, const Assignment& a, VersionId v);
   Status bind_reshard(Shard& sh, const Assignment& a, VersionId v);
@@ -405,6 +412,7 @@ class Client {
   std::vector<std::unique_ptr<HostBuf>> host_pool_;
   std::vector<FillOutcome> launch_out_;  // launch_shards -> wait_shards
   std::vector<bool> launched_;
+  std::vector<std::optional<Assignment>> launch_as_;  // per shard: the latest launch's assignment
   bool published_ = false;
   bool opened_ = false;
   bool closed_ = false;

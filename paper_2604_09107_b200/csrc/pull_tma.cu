@@ -607,6 +607,12 @@ cudaError_t launch_variant(const PullParams& p, int sms, cudaStream_t s) {
   return cudaGetLastError();
 }
 
+// The two shapes the product path launches.
+using V13 = Cfg<512, 2, 1, 320, 4, 4, true>;  // 4 two-stage pipelines per SM, dynamic batch claiming
+using V16 = Cfg<512, 2, 1, 320, 4, 1, true>;  // V13 releasing every batch at once (chain hops)
+#ifdef RSB_ALL_VARIANTS
+// Diagnostic shapes from the round-1 sweeps (profiles/r1/variants*.txt);
+// built only with RSB_ALL_VARIANTS=1 (python -m paper_2604_09107_b200.build).
 using V0 = Cfg<512, 3, 3, 320>;
 using V1 = Cfg<512, 4, 2, 576>;
 using V2 = Cfg<1024, 3, 2, 192>;
@@ -620,11 +626,10 @@ using V9 = Cfg<256, 4, 1, 320, 4>;  // 4 four-stage pipelines of 256-byte pieces
 using V10 = Cfg<256, 5, 1, 128, 4>;
 using V11 = Cfg<512, 2, 1, 320, 4, 8>;   // V8, releasing 8 batches per fence
 using V12 = Cfg<512, 2, 1, 320, 4, 16>;  // V8, releasing 16 batches per fence
-using V13 = Cfg<512, 2, 1, 320, 4, 4, true>;  // V8 with dynamic batch claiming
 using V14 = Cfg<256, 4, 1, 320, 4, 4, true>;  // V9 (4 stages of 256 B) with dynamic claiming
 using V15 = Cfg<512, 3, 1, 0, 4, 4, true>;    // V7 (3 stages, segments in global), dynamic
-using V16 = Cfg<512, 2, 1, 320, 4, 1, true>;  // V13 releasing every batch at once
 using V17 = Cfg<512, 2, 1, 320, 4, 8, true>;  // V13 releasing 8 batches per fence
+#endif
 
 int variant() {  // -1: by workload
   static const int v = [] {
@@ -651,6 +656,10 @@ cudaError_t launch_pull_tma(const PullParams& p, int sms, cudaStream_t s) {
   int v = variant();
   if (v < 0) v = p.remote == 2 ? 16 : 13;
   switch (v) {
+    case 13: return launch_variant<V13>(p, sms, s);
+    case 16: return launch_variant<V16>(p, sms, s);
+#ifdef RSB_ALL_VARIANTS
+    case 0: return launch_variant<V0>(p, sms, s);
     case 1: return launch_variant<V1>(p, sms, s);
     case 2: return launch_variant<V2>(p, sms, s);
     case 3: return launch_variant<V3>(p, sms, s);
@@ -663,12 +672,11 @@ cudaError_t launch_pull_tma(const PullParams& p, int sms, cudaStream_t s) {
     case 10: return launch_variant<V10>(p, sms, s);
     case 11: return launch_variant<V11>(p, sms, s);
     case 12: return launch_variant<V12>(p, sms, s);
-    case 13: return launch_variant<V13>(p, sms, s);
     case 14: return launch_variant<V14>(p, sms, s);
     case 15: return launch_variant<V15>(p, sms, s);
-    case 16: return launch_variant<V16>(p, sms, s);
     case 17: return launch_variant<V17>(p, sms, s);
-    default: return launch_variant<V0>(p, sms, s);
+#endif
+    default: return cudaErrorNotSupported;  // a shape this build does not carry: fail loudly
   }
 }
 

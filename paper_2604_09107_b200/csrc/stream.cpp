@@ -8,6 +8,7 @@
 #include <unistd.h>
 
 #include <algorithm>
+#include <cmath>
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
@@ -82,7 +83,7 @@ bool send_vec(int fd, const std::vector<T>& v) {
 template <class T>
 bool recv_vec(int fd, std::vector<T>* v) {
   std::uint32_t n = 0;
-  if (!recv_pod(fd, &n)) return false;
+  if (!recv_pod(fd, &n) || n > (1u << 28)) return false;  // a header table, not a payload
   v->resize(n);
   return n == 0 || recv_all(fd, v->data(), n * sizeof(T));
 }
@@ -421,11 +422,19 @@ Status StreamSource::open(const std::string& endpoint, const std::string& key, V
   std::vector<std::uint64_t> lens, dig;
   const int fd0 = fds_[0];
   if (!recv_vec(fd0, &cm.chunk0) || !recv_vec(fd0, &cm.chunk_len) || !recv_vec(fd0, &cm.count) ||
-      !recv_vec(fd0, &lens) || !recv_vec(fd0, &dig) || lens.size() + 1 != cm.chunk0.size() ||
+      !recv_vec(fd0, &lens) || !recv_vec(fd0, &dig) || !valid_header(cm, lens) ||
       dig.size() != cm.n_chunks())
     return Status::protocol_error;
-  for (std::uint32_t k = 1; k < streams; ++k)
+  // every stripe's socket gives up when its source stays silent well past
+  // the pull timeout (the kernel has failed by then; finish() shuts it too)
+  const double rx_s = 2 * timeout_s + 1;
+  timeval tv{static_cast<time_t>(rx_s), static_cast<suseconds_t>((rx_s - std::floor(rx_s)) * 1e6)};
+  setsockopt(fd0, SOL_SOCKET, SO_RCVTIMEO, &tv, sizeof(tv));
+  for (std::uint32_t k = 1; k < streams; ++k) {
     if (Status s = connect_stripe(k, &fds_[k]); !ok(s)) return s;
+    setsockopt(fds_[k], SOL_SOCKET, SO_RCVTIMEO, &tv, sizeof(tv));
+  }
+  item_len_ = lens;
   // pinned, device-mapped landing for the stream + digests + watermarks
   item_off_.resize(lens.size());
   std::uint64_t tot = 0;
@@ -463,9 +472,25 @@ Status StreamSource::open(const std::string& endpoint, const std::string& key, V
   return Status::ok;
 }
 
+bool StreamSource::valid_header(const ChunkMap& cm, const std::vector<std::uint64_t>& lens) {
+  // The header comes off the wire: every table the receive threads index
+  // must agree with the item count, and the chunk map must be the batch
+  // aligned, monotone partition of the item lengths (ChunkMap::from_lens).
+  const std::size_t n = lens.size();
+  if (cm.chunk0.size() != n + 1 || cm.chunk_len.size() != n || cm.count.size() != n ||
+      cm.chunk0[0] != 0 || cm.chunk0.back() > (1u << 30))
+    return false;
+  for (std::size_t i = 0; i < n; ++i) {
+    const std::uint32_t cl = cm.chunk_len[i];
+    if (cl == 0 || cm.chunk0[i] % dev::kBatchChunks != 0) return false;
+    if (cm.count[i] != (lens[i] + cl - 1) / cl) return false;
+    if (std::uint64_t(cm.chunk0[i]) + cm.count[i] > cm.chunk0[i + 1]) return false;
+  }
+  return true;
+}
+
 void StreamSource::receive_loop(int fd) {
   const ChunkMap& cm = view_.cmap;
-  std::vector<std::uint64_t> lens(item_off_.size());
   // item of every batch and the batch's offset inside it
   std::vector<std::uint32_t> item_of(cm.n_batches(), 0);
   std::vector<std::uint64_t> off_of(cm.n_batches(), 0);
@@ -489,8 +514,16 @@ void StreamSource::receive_loop(int fd) {
     std::uint64_t len = 0;
     if (!recv_pod(fd, &b0) || !recv_pod(fd, &nb) || !recv_pod(fd, &len)) return fail(Status::transfer_failed);
     if (b0 == kEnd) break;
-    if (b0 + nb > item_of.size()) return fail(Status::protocol_error);
+    // a frame is a run of whole batches of one item, exactly their bytes
+    if (nb == 0 || b0 >= item_of.size() || nb > item_of.size() - b0) return fail(Status::protocol_error);
     const std::uint32_t i = item_of[b0];
+    if (item_of[b0 + nb - 1] != i || (b0 + nb - 1) * std::uint64_t(dev::kBatchChunks) >=
+                                         std::uint64_t(cm.chunk0[i]) + cm.count[i])
+      return fail(Status::protocol_error);
+    const std::uint64_t end = std::min<std::uint64_t>(
+        item_len_[i], off_of[b0] + std::uint64_t(nb) * dev::kBatchChunks * cm.chunk_len[i]);
+    if (off_of[b0] >= end && item_len_[i] != 0) return fail(Status::protocol_error);
+    if (len != end - off_of[b0]) return fail(Status::protocol_error);
     if (!recv_all(fd, base + item_off_[i] + off_of[b0], len)) return fail(Status::transfer_failed);
     received_ += len;
     // the bytes are in memory before the watermarks the GPU polls (x86
@@ -528,7 +561,12 @@ void StreamSource::release(std::vector<std::unique_ptr<HostBuf>>* pool) {
     if (*b && pool->size() < 4) pool->push_back(std::move(*b));
 }
 
-Status StreamSource::finish() {
+Status StreamSource::finish(bool kernel_ok) {
+  // A fill that failed (checksum, timeout) does not wait for the rest of the
+  // stream: the receive threads return at once on the shut sockets.
+  if (!kernel_ok)
+    for (int fd : fds_)
+      if (fd >= 0) ::shutdown(fd, SHUT_RDWR);
   for (auto& t : rx_)
     if (t.joinable()) t.join();
   return static_cast<Status>(rx_status_.load());

@@ -81,8 +81,9 @@ class StreamSource {
   // The view the pull kernel reads: host item pointers, digests, watermarks
   // (flags == 1 once a batch arrived).
   const SourceView& view() const { return view_; }
-  // Waits for the receiver; ok when every batch arrived.
-  Status finish();
+  // Waits for the receiver; ok when every batch arrived.  kernel_ok false:
+  // the pull kernel failed, so the sockets are shut instead of drained.
+  Status finish(bool kernel_ok = true);
   std::uint64_t bytes_received() const { return received_.load(); }
   // watermarks raised so far, and the first batch still missing
   std::pair<std::uint32_t, std::uint32_t> flag_summary() const;
@@ -90,6 +91,7 @@ class StreamSource {
  private:
   void receive_loop(int fd);
   void abort_all();
+  static bool valid_header(const ChunkMap& cm, const std::vector<std::uint64_t>& lens);
 
   // one connection per stripe of the stream's frames (frame k on k % n);
   // the first also carries the header
@@ -97,6 +99,7 @@ class StreamSource {
   std::unique_ptr<HostBuf> data_, tables_;
   SourceView view_;
   std::vector<std::uint64_t> item_off_;  // byte offset of each item in data_
+  std::vector<std::uint64_t> item_len_;  // bytes of each item (validated header)
   std::vector<std::thread> rx_;
   std::atomic<int> rx_status_{0};  // first failure of any connection
   std::atomic<std::uint64_t> received_{0};

@@ -107,7 +107,7 @@ def _read_bytes(fn, *args) -> bytes:
 
 def make_config(chunk_bytes=4096, tiny_threshold=2 << 20, group_target=64 << 20, pipeline=True,
                 checksum_retries=3, pull_timeout_s=4.0, datacenter="dc0",
-                reshard_align=2) -> RsConfig:
+                reshard_align=2, grid_sms=0) -> RsConfig:
     cfg = RsConfig()
     lib.rs_config_default(C.byref(cfg))
     cfg.chunk_bytes = chunk_bytes
@@ -118,6 +118,7 @@ def make_config(chunk_bytes=4096, tiny_threshold=2 << 20, group_target=64 << 20,
     cfg.pull_timeout_s = pull_timeout_s
     cfg.datacenter = datacenter.encode()
     cfg.reshard_align = reshard_align
+    cfg.grid_sms = grid_sms
     return cfg
 
 
@@ -367,6 +368,60 @@ class Handle:
 
     def invalidate(self):
         check(lib.rs_invalidate(self.h))
+
+    # ---- split phase (the caller drives the registry: rs_server_* / rs_transfer_*)
+    def server_replicate(self, spec: str = "latest", update: bool = False) -> OpResult:
+        """Plan this replica's replicate/update on the in-process registry
+        without filling (ServerCore side of ClientCore::replicate)."""
+        c, m, r = self.cluster.h, _b(self.model), _b(self.replica)
+        if update:
+            cur = self.current_version
+            rc = lib.rs_server_update(c, m, r, _b(spec), int(cur is not None), cur or 0)
+        else:
+            rc = lib.rs_server_replicate(c, m, r, _b(spec))
+        if rc:
+            return OpResult(Status(rc))
+        d, s, v, ch = C.c_int(), C.c_int(), C.c_uint64(), C.c_int()
+        check(lib.rs_server_result(c, m, r, C.byref(d), C.byref(s), C.byref(v), C.byref(ch)))
+        if not d.value:
+            return OpResult(Status.timeout)
+        return OpResult(Status(s.value), v.value if s.value == 0 else None, bool(ch.value))
+
+    def transfer_bind(self, version: int) -> Status:
+        """Bind every local shard to its assignment; the (empty) fill is
+        served at once, so downstream readers can chase it."""
+        return Status(lib.rs_transfer_bind(self.h, version))
+
+    def transfer_launch(self) -> Status:
+        """Launch the pending shards' pull kernels; returns while they run."""
+        return Status(lib.rs_transfer_launch(self.h))
+
+    def transfer_progress(self, shard: int = 0) -> tuple[int, int]:
+        """(verified batches, batches) of the shard's running fill."""
+        done, n = C.c_uint32(), C.c_uint32()
+        check(lib.rs_transfer_progress(self.h, shard, C.byref(done), C.byref(n)))
+        return done.value, n.value
+
+    def transfer_wait(self) -> list[tuple[Status, int]]:
+        """Wait for the launched fills: (status, reason) per shard."""
+        n = self.num_shards
+        sts, rsn = (C.c_int * n)(), (C.c_int * n)()
+        lib.rs_transfer_wait(self.h, C.cast(sts, C.c_void_p), C.cast(rsn, C.c_void_p))
+        return [(Status(sts[i]), int(rsn[i])) for i in range(n)]
+
+    def transfer_assignment(self, shard: int = 0) -> dict:
+        """The assignment the shard's latest fill was launched on."""
+        a = RsAssignment()
+        check(lib.rs_transfer_assignment(self.h, shard, C.byref(a)), "rs_transfer_assignment")
+        return _assignment(a)
+
+    def transfer_finish(self, version: int, good: bool) -> None:
+        """Finish the fill (serve complete / stop serving) and report every
+        shard's completion to the registry."""
+        check(lib.rs_transfer_finish(self.h, version, int(good)))
+        st = 0 if good else int(Status.transfer_failed)
+        for s in range(self.num_shards):
+            lib.rs_server_complete(self.cluster.h, _b(self.model), _b(self.replica), s, st)
 
     # ---- introspection ----------------------------------------------------
     @property

@@ -247,17 +247,19 @@ def test_bind_rejects_mismatched_registration(fx):
 
 def test_multi_gpu_chain_with_chasing():
     """Readers on different GPUs fill concurrently, each chasing its upstream's
-    device watermark over NVLink (peer access)."""
+    device watermark over NVLink (peer access).  On a one-GPU box three
+    readers share cuda:0 with their grids capped to 48 SMs each, so their
+    persistent kernels co-reside and chase each other in HBM."""
     n = torch.cuda.device_count()
-    if n < 2:
-        pytest.skip("needs >= 2 GPUs")
     from paper_2604_09107_b200.ros import Status
     f = Fix()
     try:
-        names = ["trainer"] + [f"r{i}" for i in range(1, n)]
+        readers = n - 1 if n > 1 else 3
+        cap = {} if n > 1 else {"grid_sms": 48}
+        names = ["trainer"] + [f"r{i}" for i in range(1, readers + 1)]
         size = 256 << 20
         for i, r in enumerate(names):
-            f.make(r, dev=i)
+            f.make(r, dev=i % n, **(cap if i else {}))
             f.reg(r, 0, "w", size, 1 if i == 0 else 99)
             f.reg(r, 0, "norm", 8192, 2 if i == 0 else 98)
         assert f.h["trainer"].publish(1).status == Status.ok
@@ -278,6 +280,10 @@ def test_multi_gpu_chain_with_chasing():
         assert len(set(srcs)) == len(srcs) and "trainer" in srcs
         for r in names[1:]:
             assert f.same("trainer", r, 0, "w") and f.same("trainer", r, 0, "norm")
+            # the fill's source: the trainer or the reader ahead of it in the
+            # chain, complete or (a pipeline copy) still filling
+            a = f.h[r].transfer_assignment(0)
+            assert a["source_replica"] in names and a["source_replica"] != r
     finally:
         f.close()
 

@@ -10,6 +10,7 @@ GPU: the lane is pinned host memory; a reader pulls the parked version out
 of it through the pull kernel (in-process, and from another process)."""
 import ctypes as C
 import os
+import time
 import re
 import socket
 
@@ -288,6 +289,52 @@ def test_corrupted_parked_version_fails_loudly():
         assert not r.is_published
 
 
+@pytest.mark.gpu
+def test_failed_copy_engine_fill_is_drained_before_returning():
+    """A corrupted host lane fails the copy-engine fill at its first frame;
+    the frames already queued behind it must be drained before the fill's
+    outcome is acted on (a retry from another source would otherwise be
+    overwritten, and the lane could be released while the engine still
+    reads it).  Once replicate has returned, nothing lands any more."""
+    import glob
+    import mmap
+    _need_gpu()
+    dev = torch.device("cuda:0")
+    from paper_2604_09107_b200 import ros
+    sizes = (1 << 30, 5000)
+    with Cluster() as cl:
+        w = cl.open("m", "watcher", 1)
+        assert w.register_tensor(0, "w0", torch.zeros(4096, dtype=torch.uint8, device=dev)) == Status.ok
+        w.set_retention([0, 1])
+        assert w.connect() == Status.ok
+        t = cl.open("m", "trainer", 1, tiny_threshold=1 << 20)
+        tb = _tensors(dev, 40, sizes)
+        for i, x in enumerate(tb):
+            assert t.register_tensor(0, f"w{i}", x) == Status.ok
+        before = set(glob.glob(f"/dev/shm/rsb-{os.getpid()}-*"))
+        assert t.publish(1).status == Status.ok
+        assert t.unpublish().status == Status.ok
+        assert t.lanes() == [1]
+        lane = sorted(set(glob.glob(f"/dev/shm/rsb-{os.getpid()}-*")) - before,
+                      key=os.path.getsize)[-1]
+        with open(lane, "r+b") as f, mmap.mmap(f.fileno(), 0) as mm:
+            mm[1 << 20] ^= 0x40  # first frame: stops the fill
+        for i, x in enumerate(tb):
+            ros.synth_bf16(x, 500 + i)
+        assert t.publish(2).status == Status.ok
+        r = cl.open("m", "reader", 1, tiny_threshold=1 << 20, pull_timeout_s=2.0)
+        rb = [torch.zeros_like(x) for x in tb]
+        for i, x in enumerate(rb):
+            assert r.register_tensor(0, f"w{i}", x) == Status.ok
+        res = r.replicate("1")
+        assert res.status != Status.ok, res
+        assert r.stats().checksum_failures >= 1
+        snap = rb[0].clone()
+        torch.cuda.synchronize()
+        time.sleep(0.1)  # a stray copy-engine frame (128 MiB: ~2.4 ms) would land by now
+        assert torch.equal(snap, rb[0])
+
+
 def _free_port():
     s = socket.socket()
     s.bind(("127.0.0.1", 0))
@@ -308,8 +355,9 @@ def _dist_worker(rank, world, port, q):
     from paper_2604_09107_b200.dist import DistCluster
     from paper_2604_09107_b200.ros import Status
     try:
-        torch.cuda.set_device(rank)
-        dev = torch.device("cuda", rank)
+        gpu = rank % torch.cuda.device_count()  # one GPU: both processes share cuda:0
+        torch.cuda.set_device(gpu)
+        dev = torch.device("cuda", gpu)
         dist.init_process_group("gloo", rank=rank, world_size=world)
         dc = DistCluster()
         sizes = [(6 << 20) + 4096 * 3, 5000, 3 << 20]
@@ -328,7 +376,7 @@ def _dist_worker(rank, world, port, q):
                 ros.synth_bf16(b, 10 + i)
             torch.cuda.synchronize()
         assert (dc.publish(h if rank == 0 else None, 1) or ros.OpResult(Status.ok)).status == 0
-        v1 = dc.gather(ros.digest_spans([b.data_ptr() for b in bufs], sizes, rank))[0]
+        v1 = dc.gather(ros.digest_spans([b.data_ptr() for b in bufs], sizes, gpu))[0]
         r = dc.unpublish(h if rank == 0 else None)
         out = {"unpublish": None if r is None else int(r.status)}
         if rank == 0:
@@ -340,7 +388,7 @@ def _dist_worker(rank, world, port, q):
         res = dc.replicate(h if rank == 1 else None, "1")
         if rank == 1:
             out["replicate"] = (int(res.status), res.version)
-            out["bytes_v1"] = ros.digest_spans([b.data_ptr() for b in bufs], sizes, rank) == v1
+            out["bytes_v1"] = ros.digest_spans([b.data_ptr() for b in bufs], sizes, gpu) == v1
         out["plan"] = [(a.replica, a.src) for a in dc.assigns()]
         dist.barrier()
         if rank == 0:
@@ -358,8 +406,9 @@ def _dist_worker(rank, world, port, q):
 @pytest.mark.gpu
 def test_gpu_reader_in_another_process_pulls_the_offload():
     """The offload lane is POSIX shared memory registered with CUDA: the
-    reader's process maps it by name and its pull kernel reads it."""
-    _need_gpu(2)
+    reader's process maps it by name and its pull kernel reads it (one GPU:
+    both processes on cuda:0)."""
+    _need_gpu(1)
     import multiprocessing as mp
     ctx = mp.get_context("spawn")
     q = ctx.Queue()

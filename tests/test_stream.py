@@ -36,8 +36,8 @@ def _bufs(dev, seed=None, sizes=((48 << 20) + 4096 * 5 + 100, 7000, 3 << 20)):
     return out
 
 
-def _open(cl, name, bufs, ep=None):
-    h = cl.open("m", name, 1, tiny_threshold=1 << 20)
+def _open(cl, name, bufs, ep=None, **cfg):
+    h = cl.open("m", name, 1, tiny_threshold=1 << 20, **cfg)
     for i, b in enumerate(bufs):
         assert h.register_tensor(0, f"w{i}", b) == Status.ok
     if ep:
@@ -64,19 +64,20 @@ def test_pull_over_tcp_is_bit_exact():
 
 
 def test_chained_readers_chase_each_other_over_tcp():
-    """r1 chases r0 while r0 is still landing -- across the wire.  The two
-    readers sit on different GPUs: persistent pull kernels that wait on each
-    other must not share one GPU (a chaser could occupy every SM first)."""
-    if torch.cuda.device_count() < 2:
-        pytest.skip("needs 2 GPUs")
+    """r1 chases r0 while r0 is still landing -- across the wire.  With two
+    GPUs the readers sit on different GPUs; on one GPU their persistent pull
+    kernels wait on each other, so each is capped to 64 SMs (rs_config
+    grid_sms) and the two co-reside."""
+    n = torch.cuda.device_count()
+    cap = {} if n > 1 else {"grid_sms": 64}
     with Cluster() as cl:
         port = cl.listen()
         ep = f"tcp:127.0.0.1:{port}"
         tb = _bufs(torch.device("cuda:0"), seed=9)
         t = _open(cl, "trainer", tb, ep)
         assert t.publish(1).status == Status.ok
-        devs = [torch.device("cuda:1"), torch.device("cuda:0")]
-        readers = [(_open(cl, f"r{i}", rb, ep), rb) for i, rb in
+        devs = [torch.device("cuda", 1 % n), torch.device("cuda:0")]
+        readers = [(_open(cl, f"r{i}", rb, ep, **cap), rb) for i, rb in
                    enumerate([_bufs(d) for d in devs])]
         results = {}
 
@@ -133,3 +134,84 @@ def test_version_bumps_over_tcp_reuse_pinned_buffers():
             torch.cuda.synchronize()
             for a, b in zip(tb, rb):
                 assert torch.equal(a, b), v
+
+
+def _hostile_server(reply):
+    """A TCP peer speaking the stream handshake (stream.cpp serve_conn) that
+    answers every request with `reply(sock, stripe)`."""
+    import socket
+    import struct
+    ls = socket.socket()
+    ls.bind(("127.0.0.1", 0))
+    ls.listen(16)
+    stop = threading.Event()
+
+    def recv_n(c, n):
+        b = b""
+        while len(b) < n:
+            k = c.recv(n - len(b))
+            if not k:
+                raise ConnectionError
+            b += k
+        return b
+
+    def serve():
+        ls.settimeout(0.2)
+        while not stop.is_set():
+            try:
+                c, _ = ls.accept()
+            except OSError:
+                continue
+            try:
+                _magic, klen = struct.unpack("<II", recv_n(c, 8))
+                recv_n(c, klen)
+                _version, stripe, _streams = struct.unpack("<QII", recv_n(c, 16))
+                c.sendall(struct.pack("<I", 0))
+                reply(c, stripe)
+            except (ConnectionError, OSError):
+                pass
+            threading.Timer(5.0, c.close).start()
+
+    th = threading.Thread(target=serve, daemon=True)
+    th.start()
+    return ls.getsockname()[1], stop
+
+
+def _vec(fmt, xs):
+    import struct
+    return struct.pack("<I", len(xs)) + struct.pack("<%d%s" % (len(xs), fmt), *xs)
+
+
+@pytest.mark.parametrize("case", ["bad_header", "oversized_frame"])
+def test_hostile_tcp_source_is_rejected(case):
+    """A peer whose header disagrees with itself, or whose frame claims more
+    bytes than its batches hold, fails the fill (protocol error) instead of
+    writing past the reader's pinned landing buffer."""
+    import struct
+    n = 1 << 20  # one item: 256 chunks of 4096 B, one batch row of 8
+
+    def reply(c, stripe):
+        if stripe != 0:
+            return
+        count = [n // 4096 + (1 if case == "bad_header" else 0)]
+        c.sendall(_vec("I", [0, 256]) + _vec("I", [4096]) + _vec("I", count) + _vec("Q", [n]) +
+                  _vec("Q", [0] * 256))
+        if case == "oversized_frame":
+            c.sendall(struct.pack("<IIQ", 0, 1, 1 << 30) + b"\0" * 4096)
+
+    port, stop = _hostile_server(reply)
+    dev = torch.device("cuda:0")
+    try:
+        with Cluster() as cl:
+            t = _open(cl, "trainer", [torch.ones(n, dtype=torch.uint8, device=dev)],
+                      f"tcp:127.0.0.1:{port}")
+            assert t.publish(1).status == Status.ok
+            r = cl.open("m", "reader", 1, tiny_threshold=1 << 20, pull_timeout_s=1.0)
+            rb = torch.zeros(n, dtype=torch.uint8, device=dev)
+            assert r.register_tensor(0, "w0", rb) == Status.ok
+            res = r.replicate(wait_s=20.0)
+            assert res.status != Status.ok, res
+            assert not r.is_published
+            assert int(rb.sum()) == 0  # nothing landed from the hostile peer
+    finally:
+        stop.set()
