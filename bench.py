@@ -203,47 +203,169 @@ def _numel(shape):
 
 
 # ------------------------------------------------------------- CPU legs
-def cpu_reference_run(shapes, budget_bytes: int, reps: int, threaded: bool = True):
-    """The reference refstore (oracle/_ref) pulling a bounded sample of the
-    workload through its own MemNetwork path on this host's cores."""
+def workload_label(workload: str, receivers: int) -> str:
+    """config.workload, identical in both arms for the same (workload, N)."""
+    return f"{workload}: trainer -> {receivers} reader{'s' if receivers != 1 else ''}, full model"
+
+
+_HOST = {}
+
+
+def host_workload(shapes):
+    """The workload's synthetic bytes in host memory (SURVEY.md §8d
+    generator, seed 42 + i, the oracle's C restatement -- bit-identical to
+    the device generator), made once per process on every host core (the C
+    generator runs outside the GIL)."""
+    key = tuple((n, tuple(s)) for n, s in shapes)
+    if key in _HOST:
+        return _HOST[key]
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    from concurrent.futures import ThreadPoolExecutor
+
+    import numpy as np
+
+    import oracle as O
+    arrs = [np.empty(_numel(s), np.uint16) for _, s in shapes]
+    lib = O.port()
+    step = 1 << 26  # elements per task
+
+    def fill(job):
+        i, first, n = job
+        lib.ro_synth_bf16(42 + i, first, n, arrs[i][first:first + n].ctypes.data)
+
+    jobs = [(i, f, min(step, a.size - f)) for i, a in enumerate(arrs) for f in range(0, a.size, step)]
+    with ThreadPoolExecutor(os.cpu_count() or 1) as ex:
+        list(ex.map(fill, jobs))
+    _HOST.clear()
+    _HOST[key] = [a.view(np.uint8) for a in arrs]
+    return _HOST[key]
+
+
+def cpu_reference_run(shapes, readers: int = 1, steps: int = 1, warmup: int = 0,
+                      verify: bool = True):
+    """The reference refstore (oracle/_ref, compiled from its own sources)
+    pulling the WHOLE workload through its own public API and stock path:
+    ClientCore publish / replicate over MemNetwork (transport_mem.cpp:170-201:
+    memcpy under the source's lock + digest64 per item on the reader).
+    Throughput mode (SURVEY.md §8d ii): one ThreadExecutor per replica,
+    server and client pipelines off, so `readers` readers pull from the
+    trainer in parallel, each on its own executor thread.  The trainer
+    publishes once; every step adds `readers` fresh replicas that land the
+    full model into the same host buffers, then closes them.  Returns the
+    per-step results (value = bytes landed by all readers / wall time of
+    the step's replicate fan-out)."""
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import numpy as np
 
     import oracle as O
     if not O.ref_available():
         return None
-    sample, tot = [], 0
-    for name, s in shapes:
-        n = 2 * _numel(s)
-        if tot + n > budget_bytes and sample:
-            break
-        sample.append((name, n))
-        tot += n
-    times = []
-    for rep in range(reps):
-        c = O.RefCluster(threaded=threaded, server_pipeline=False, client_pipeline=False)
-        c.add("trainer")
-        c.add("reader")
-        keep = []
-        for i, (name, n) in enumerate(sample):
-            a = O.synth_bf16(42 + i, n // 2).view(np.uint8)
-            b = np.zeros(n, np.uint8)
-            keep += [a, b]
-            c.register("trainer", 0, name, a)
-            c.register("reader", 0, name, b)
-        st, _ = c.publish("trainer", 1)
-        assert st == 0, st
-        sts, _, _, secs = c.pull_many(["reader"])
-        assert sts == [0], sts
-        assert np.array_equal(keep[0], keep[1])
-        times.append(secs)
-        c.close()
-    best = min(times)
-    return {"value": tot / best / 1e9, "unit": UNIT, "cores": 1, "kind": "reference",
-            "threads": 3 if threaded else 1,
-            "sample": f"first {len(sample)} tensors of {len(shapes)} ({tot / 1e9:.2f} GB), "
-                      f"1 trainer -> 1 reader, refstore ThreadExecutor+MemNetwork, pipeline off, "
-                      f"best of {reps}; the copy+digest runs on the reader's one executor thread"}
+    t0 = time.perf_counter()
+    src = host_workload(shapes)
+    gen_s = time.perf_counter() - t0
+    total = sum(a.nbytes for a in src)
+    dst = [[np.empty_like(a) for a in src] for _ in range(readers)]
+    c = O.RefCluster(threaded=True, server_pipeline=False, client_pipeline=False)
+    c.add("trainer")
+    for (name, _), a in zip(shapes, src):
+        assert c.register("trainer", 0, name, a) == 0
+    st, publish_s = c.publish("trainer", 1)
+    assert st == 0, st
+    out = []
+    for k in range(warmup + steps):
+        names = [f"reader{k}_{j}" for j in range(readers)]
+        for nm, bufs in zip(names, dst):
+            c.add(nm)
+            for (name, _), b in zip(shapes, bufs):
+                assert c.register(nm, 0, name, b) == 0
+        sts, _, _, secs = c.pull_many(names)
+        assert sts == [0] * readers, sts
+        if verify and k == 0:
+            for bufs in dst:
+                assert all(np.array_equal(a, b) for a, b in zip(src, bufs)), "reference bytes differ"
+        for nm in names:
+            c.close_replica(nm)
+        if k >= warmup:
+            out.append(secs)
+    c.close()
+    sec = statistics.median(out)
+    nproc = os.cpu_count() or 1
+    return {"value": readers * total / sec / 1e9, "unit": UNIT, "cores": min(readers, nproc),
+            "nproc": nproc, "kind": "reference", "steps_s": [round(x, 4) for x in out],
+            "publish_s": round(publish_s, 3), "host_gen_s": round(gen_s, 2),
+            "sample": f"whole workload ({len(shapes)} tensors, {total / 1e9:.3f} GB) per step: "
+                      f"refstore publish once, then per step {readers} fresh reader replica(s) "
+                      f"replicate('latest') through ClientCore + MemNetwork, ThreadExecutor per "
+                      f"replica, pipeline off; copy + digest64 run on each reader's executor "
+                      f"thread ({min(readers, nproc)} core(s) busy of {nproc}); median of {len(out)}"}
+
+
+def reference_parity(workload, t, r, rviews, cast: bool):
+    """Pre-timing parity against the reference at full scale
+    (tests/golden/scale.json, made by tests/golden/make_scale_golden.py from
+    oracle/_ref): the trainer's manifest bytes (build_publish_payload), the
+    reader's chunk-digest table, and the reference digest64 of every landed
+    tensor (its e4m3 cast for config 5).  None when no fixture covers it."""
+    import hashlib
+
+    import numpy as np
+
+    from paper_2604_09107_b200 import ros
+    key = {"llama3_8b": "config2_llama3_8b", "llama3_70b_tp8": "config5_llama3_70b_tp8"}.get(workload)
+    path = os.path.join(ROOT, "tests", "golden", "scale.json")
+    if key is None or not os.path.exists(path):
+        return None
+    with open(path) as f:
+        g = json.load(f)[key]
+    sha = lambda a: hashlib.sha256(np.ascontiguousarray(a).astype("<u8").tobytes()).hexdigest()
+    landed = ros.digest_spans([w.data_ptr() for _, w in rviews], [w.numel() for _, w in rviews])
+    want = g["cast_digests"] if cast else g["tensor_digests"]
+    out = {"manifest": hashlib.sha256(t.manifest(0)).hexdigest() == g["manifest_sha256"],
+           "chunk_table": sha(r.chunk_digests(0)) == g["chunk_table_sha256"],
+           "landed_tensors": ["%016X" % x for x in landed] == want,
+           "against": "tests/golden/scale.json (reference digest64 / build_publish_payload)"}
+    assert out["manifest"] and out["chunk_table"] and out["landed_tensors"], out
+    return out
+
+
+def register_pair(t, r, shapes, tviews, rviews, dev, reshard: bool, cast: bool):
+    """Registers the trainer's and the reader's regions the way every bench
+    mode (and tests/test_scale_parity.py) lays them out.  Plain: whole tensors
+    on both sides.  cast: the reader lands each tensor as e4m3 (config 5).
+    reshard: the trainer holds TP=1 tensors (one shard) or FSDP row blocks
+    (t.num_shards > 1: Shard(0)), the reader the two TP=2 shards of every
+    tensor, landing in its arena (shard 0 then shard 1 per tensor); returns
+    {(shard, name): (buffer, bytes, geometry)} of the reader's slices."""
+    import torch
+
+    from paper_2604_09107_b200.ros import Status
+    fsdp = t.num_shards
+    rslices = {}
+    for (n, v), (_, w), (_, shape) in zip(tviews, rviews, shapes):
+        if cast:
+            assert t.register_tensor(0, n, v) == Status.ok
+            assert r.register_cast(0, n, w, v.numel()) == Status.ok
+            continue
+        if not reshard:
+            assert t.register_tensor(0, n, v) == Status.ok
+            assert r.register_tensor(0, n, w) == Status.ok
+            continue
+        for i in range(fsdp):
+            g = tp_slice(shape, 2, 0 if fsdp > 1 else None, fsdp, i)
+            rows, wb, r0, nr, c0, nc = g
+            off = r0 * wb + c0
+            assert t.register_slice(i, n, v[off:off + nr * nc], g) == Status.ok
+        dim = tp_dim(n)
+        for sh in range(2):
+            geo = tp_slice(shape, 2, dim, 2, sh)
+            off = 0 if sh == 0 else rslices[(0, n)][1]
+            if dim is None and sh == 1:  # replicated: every shard holds it whole
+                buf = torch.empty(geo[3] * geo[5], dtype=torch.uint8, device=dev)
+            else:
+                buf = w[off:off + geo[3] * geo[5]]
+            rslices[(sh, n)] = (buf, geo[3] * geo[5], geo)
+            assert r.register_slice(sh, n, buf, geo) == Status.ok
+    return rslices
 
 
 # ------------------------------------------------------------- our arm
@@ -267,34 +389,7 @@ def run_single(args):
     reshard = args.reshard in ("tp2", "fsdp_tp2")
     fsdp = t.num_shards  # trainer shards (FSDP-8: Shard(0) row blocks)
     r = cl.open("m", "rollout1", 2 if reshard else 1, chunk_bytes=args.chunk)
-    rslices = {}
-    for (n, v), (_, w), (_, shape) in zip(tviews, rviews, shapes):
-        if cast:
-            assert t.register_tensor(0, n, v) == Status.ok
-            assert r.register_cast(0, n, w, v.numel()) == Status.ok
-            continue
-        if not reshard:
-            assert t.register_tensor(0, n, v) == Status.ok
-            assert r.register_tensor(0, n, w) == Status.ok
-            continue
-        # TP=1 (or FSDP-8: Shard(0) row blocks, contiguous views of the
-        # trainer's tensors) -> TP=2 reader: every shard on this GPU, landing
-        # straight into the reader arena (shard 0 then shard 1 per tensor)
-        for i in range(fsdp):
-            g = tp_slice(shape, 2, 0 if fsdp > 1 else None, fsdp, i)
-            rows, wb, r0, nr, c0, nc = g
-            off = r0 * wb + c0
-            assert t.register_slice(i, n, v[off:off + nr * nc], g) == Status.ok
-        dim = tp_dim(n)
-        for s in range(2):
-            geo = tp_slice(shape, 2, dim, 2, s)
-            off = 0 if s == 0 else rslices[(0, n)][1]
-            if dim is None and s == 1:  # replicated: every shard holds it whole
-                buf = torch.empty(geo[3] * geo[5], dtype=torch.uint8, device=dev)
-            else:
-                buf = w[off:off + geo[3] * geo[5]]
-            rslices[(s, n)] = (buf, geo[3] * geo[5], geo)
-            assert r.register_slice(s, n, buf, geo) == Status.ok
+    rslices = register_pair(t, r, shapes, tviews, rviews, dev, reshard, cast)
     for s in range(r.num_shards):
         r.set_stream(s, stream)
     t0 = time.perf_counter()
@@ -336,8 +431,11 @@ def run_single(args):
 
     for _ in range(args.warmup):
         step()
+    parity = None
     if not args.no_verify:
         verify()
+        if not reshard:
+            parity = reference_parity(args.workload, t, r, rviews, cast)
     clk = ClockSampler(0)
     torch.cuda.synchronize()
     clk.start()
@@ -384,10 +482,11 @@ def run_single(args):
         "metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": 1, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(dev_ms / args.steps, 3), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
-        "config": {"workload": f"{args.workload}: trainer -> 1 reader on one GPU (local HBM pull)"
+        "config": {"workload": workload_label(args.workload, 1)
                                + (f", resharded {'FSDP-8' if fsdp > 1 else 'TP=1'} -> TP=2 "
                                   "(all shards on this GPU)" if reshard else "")
                                + (", landed as fp8 e4m3 (fused cast; bytes = bf16 ingress)" if cast else ""),
+                   "placement": "trainer and reader regions in the HBM of one GPU (local pull)",
                    "bytes_per_receiver": total, "tensors": len(shapes), "chunk_bytes": args.chunk,
                    "receivers": 1, "l2": "inputs (16 GB/replica) >> 126 MB L2; no flush"},
         "per_receiver_gbs": [round(value, 2)],
@@ -408,6 +507,7 @@ def run_single(args):
                 "d2h_bytes_per_step": (st.d2h_bytes - d2h0) // args.steps,
                 "what": "wall clock of rs_replicate (plan+bind+kernel+unpack+complete) per step, "
                         "version resident in the trainer's HBM"},
+        "parity": parity,
         "gpu_launches": args.steps * (1 + 1),  # pull_kernel + group unpack per step
         "clocks": clocks,
     }
@@ -421,7 +521,9 @@ def run_single(args):
         line["e2e_device_resident"] = {"value": round(e2e, 2), "unit": UNIT,
                                        "what": "rs_replicate wall clock, version in the trainer's HBM"}
     if not args.no_cpu:
-        line["cpu_baseline"] = cpu_reference_run(shapes, args.cpu_bytes, args.cpu_reps)
+        cb = cpu_reference_run(shapes, readers=1, steps=args.cpu_reps, warmup=0, verify=False)
+        line["cpu_baseline"] = cb and {k: cb[k] for k in ("value", "unit", "cores", "nproc", "kind",
+                                                          "sample")}
     print(json.dumps(line), flush=True)
     cl.close()
 
@@ -472,27 +574,33 @@ def host_e2e(cl, t, r, stream, total, tarena, rarena, args):
 
 
 def run_reference(args):
+    """--impl reference: the reference's own CPU implementation of the path
+    (oracle/_ref), same workload, metric and config.workload as our arm at
+    this N: rank 0 alone runs it with N-1 readers (1 at N=1)."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
+    world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
+    readers = max(1, max(world, args.gpus) - 1)
     shapes = workload_shapes(args.workload)
-    vals = []
-    for _ in range(args.warmup):
-        cpu_reference_run(shapes, args.cpu_bytes, 1)
-    for _ in range(args.steps):
-        r = cpu_reference_run(shapes, args.cpu_bytes, 1)
-        if r is None:
-            print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built"}))
-            return
-        vals.append(r)
-    v = statistics.median(x["value"] for x in vals)
+    r = cpu_reference_run(shapes, readers=readers, steps=args.steps, warmup=args.warmup,
+                          verify=not args.no_verify)
+    if r is None:
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built"}))
+        return
+    v = r["value"]
+    total = sum(2 * _numel(s) for _, s in shapes)
     line = {"impl": "reference", "metric": METRIC, "value": round(v, 3), "unit": UNIT,
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(1e3 * statistics.median(r["steps_s"]), 3),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
             "data": "synthetic",
-            "config": {"workload": f"{args.workload}: bounded sample, trainer -> 1 reader on host"},
-            "cpu_baseline": {"value": round(v, 3), "unit": UNIT, "cores": vals[0]["cores"],
-                             "kind": "reference", "sample": vals[0]["sample"]},
+            "config": {"workload": workload_label(args.workload, readers),
+                       "placement": "host DRAM (the reference is a CPU library)",
+                       "bytes_per_receiver": total, "tensors": len(shapes), "receivers": readers},
+            "cpu_baseline": {"value": round(v, 3), "unit": UNIT, "cores": r["cores"],
+                             "nproc": r["nproc"], "kind": "reference", "sample": r["sample"]},
+            "publish_s": r["publish_s"],
             "e2e": {"value": round(v, 3), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -514,8 +622,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-host-e2e", action="store_true",
                     help="skip the host-buffer end-to-end leg (N=1)")
-    ap.add_argument("--cpu-bytes", type=int, default=2 << 30)
-    ap.add_argument("--cpu-reps", type=int, default=3)
+    ap.add_argument("--cpu-reps", type=int, default=2,
+                    help="cpu_baseline: whole-workload reference pulls timed in our arm's line")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)

@@ -72,6 +72,9 @@ def ref():
         lib.ref_build_manifest.restype = C.c_long
         lib.ref_build_manifest.argtypes = [C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint64,
                                            C.c_uint64, C.c_char_p, C.c_size_t]
+        lib.ref_build_manifest_pre.restype = C.c_long
+        lib.ref_build_manifest_pre.argtypes = [C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                               C.c_uint64, C.c_uint64, C.c_char_p, C.c_size_t]
         lib.ref_assemble_manifest.restype = C.c_long
         lib.ref_assemble_manifest.argtypes = [C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint64,
                                               C.c_uint64, C.c_int, C.c_char_p, C.c_size_t]
@@ -90,6 +93,7 @@ def ref():
                                                      C.c_uint64]
         lib.ref_cluster_publish.argtypes = [C.c_void_p, C.c_char_p, C.c_uint64, C.c_void_p]
         lib.ref_cluster_unpublish.argtypes = [C.c_void_p, C.c_char_p]
+        lib.ref_cluster_close.argtypes = [C.c_void_p, C.c_char_p]
         lib.ref_cluster_set_retention.argtypes = [C.c_void_p, C.c_char_p, C.c_void_p, C.c_int]
         lib.ref_cluster_open.argtypes = [C.c_void_p, C.c_char_p]
         lib.ref_cluster_pull_many.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_char_p, C.c_int,
@@ -229,6 +233,24 @@ def ref_build_manifest(names, arrays, tiny=2 << 20, target=64 << 20) -> bytes:
     return buf.raw[:n]
 
 
+def ref_build_manifest_pre(names, lens, digests, tiny_arrays: dict, tiny=2 << 20,
+                           target=64 << 20) -> bytes:
+    """build_publish_payload with precomputed (reference digest64) entry
+    digests; tiny_arrays maps entry index -> bytes for the group members."""
+    keep = {i: np.ascontiguousarray(a).view(np.uint8).reshape(-1) for i, a in tiny_arrays.items()}
+    cnames = (C.c_char_p * len(names))(*[n.encode() for n in names])
+    ptrs = np.array([keep[i].ctypes.data if i in keep else 0 for i in range(len(names))], np.uint64)
+    lens = np.asarray(lens, np.uint64)
+    digests = np.asarray(digests, np.uint64)
+    args = (len(names), C.cast(cnames, C.c_void_p), ptrs.ctypes.data, lens.ctypes.data,
+            digests.ctypes.data, tiny, target)
+    n = ref().ref_build_manifest_pre(*args, None, 0)
+    assert n >= 0, n
+    buf = C.create_string_buffer(n)
+    ref().ref_build_manifest_pre(*args, buf, n)
+    return buf.raw[:n]
+
+
 def ref_assemble_manifest(names, lens, digests, tiny=2 << 20, target=64 << 20, seal=False) -> bytes:
     cnames = (C.c_char_p * len(names))(*[n.encode() for n in names])
     lens = np.asarray(lens, np.uint64)
@@ -300,6 +322,10 @@ class RefCluster:
 
     def open(self, replica):
         return self.lib.ref_cluster_open(self.h, replica.encode())
+
+    def close_replica(self, replica):
+        """ClientCore::close: the replica leaves and stops serving."""
+        return self.lib.ref_cluster_close(self.h, replica.encode())
 
     def set_retention(self, replica, lags):
         arr = (C.c_uint64 * max(len(lags), 1))(*lags)

@@ -135,6 +135,33 @@ long ref_build_manifest(int n, const char** names, const void** ptrs,
   return copy_out(m->encode(), out, cap);
 }
 
+// build_publish_payload (client_core.cpp:1547-1579) with the entry digests
+// supplied by the caller -- each one the reference digest64 of that entry,
+// computed elsewhere (in parallel, tensor by tensor) -- so a 16-65 GB
+// synthetic model need not sit in memory at once.  Only group members need
+// a pointer: pack_group stages them and digests the staging, exactly as the
+// reference does.
+long ref_build_manifest_pre(int n, const char** names, const void** ptrs,
+                            const std::uint64_t* lens, const std::uint64_t* digests,
+                            std::uint64_t tiny, std::uint64_t target, char* out,
+                            std::size_t cap) {
+  std::vector<EntryDesc> descs;
+  std::vector<std::span<const std::byte>> regions;
+  for (int i = 0; i < n; ++i) {
+    regions.emplace_back(static_cast<const std::byte*>(ptrs[i]), ptrs[i] ? lens[i] : 0);
+    descs.push_back({names[i], lens[i], digests[i]});
+  }
+  auto m = assemble_manifest(descs, ManifestLimits{tiny, target});
+  if (!m) return -static_cast<long>(m.status());
+  for (std::uint32_t g = 0; g < m->groups.size(); ++g) {
+    for (const auto& mem : m->groups[g].members)
+      if (!ptrs[mem.entry_idx]) return -1;  // a group member without its bytes
+    std::vector<std::byte> staging(m->groups[g].packed_length);
+    pack_group(*m, g, regions, staging);
+  }
+  return copy_out(m->encode(), out, cap);
+}
+
 // assemble_manifest over explicit (name, length, digest) descriptors, groups
 // sealed with seal_groups_modeled when `seal` (modeled payloads).
 long ref_assemble_manifest(int n, const char** names, const std::uint64_t* lens,
@@ -275,6 +302,15 @@ int ref_cluster_open(void* h, const char* replica) {
   auto* c = static_cast<Cluster*>(h);
   auto* core = c->nodes.at(replica)->core.get();
   auto r = c->run_many({[&](ClientCore::OpFn cb) { core->open(cb); }}, nullptr);
+  return static_cast<int>(r[0].status);
+}
+
+// ClientCore::close (client_core.hpp:93): the replica leaves the cluster
+// and stops serving its regions, which the caller may then reuse.
+int ref_cluster_close(void* h, const char* replica) {
+  auto* c = static_cast<Cluster*>(h);
+  auto* core = c->nodes.at(replica)->core.get();
+  auto r = c->run_many({[&](ClientCore::OpFn cb) { core->close(cb); }}, nullptr);
   return static_cast<int>(r[0].status);
 }
 

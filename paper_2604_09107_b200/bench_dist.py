@@ -133,8 +133,9 @@ def run(args):
             "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": round(sum(step_dev_ms) / args.steps, 3), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
-            "config": {"workload": f"{args.workload}: trainer on GPU0 -> {receivers} readers, "
-                                   "chained fan-out over NVLink", "bytes_per_receiver": total,
+            "config": {"workload": B.workload_label(args.workload, receivers),
+                       "placement": "trainer on GPU0, reader i on GPU i: chained fan-out over NVLink",
+                       "bytes_per_receiver": total,
                        "receivers": receivers, "chunk_bytes": args.chunk,
                        "plan": [f"{a.replica}<-{a.src}" for a in dc.assigns()][-receivers:],
                        "l2": "inputs (16 GB/replica) >> 126 MB L2; no flush"},
@@ -171,8 +172,8 @@ def run(args):
         if host_e2e is not None:
             line["e2e_device_resident"] = line["e2e"]
             line["e2e"] = host_e2e
-        if not args.no_cpu:
-            line["cpu_baseline"] = B.cpu_reference_run(shapes, args.cpu_bytes, args.cpu_reps)
+        # cpu_baseline: rank 0 at N=1 only (bench.py); at this N the reference
+        # arm (--impl reference) times the same workload with N-1 readers
         print(json.dumps(line), flush=True)
     dist.barrier(group=dc.pg)
     dc.close()

@@ -245,3 +245,109 @@ def test_version_bumps_across_processes():
     reader = res[1]["out"]
     assert reader == [(0, 1), True, (0, 2), True, (0, 3), True, (0, 4), True], reader
     assert all(nb > 0 for _, nb in res[1]["seen"])
+
+
+def _join_worker(rank, world, port, q):
+    """Rank 0: the trainer T and a reader A whose fill is slowed to one SM;
+    rank 1: a late joiner B, planned while A is part-way through its fill.
+    B's assignment is A as a pipeline copy (source_complete == 0) and B's
+    kernel -- in another process, on the IPC-imported serve state -- chases
+    A's watermarks (config 4's elastic join; server_core.cpp:1534-1540)."""
+    import sys
+    import time
+    sys.path.insert(0, ROOT)
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank),
+                      WORLD_SIZE=str(world))
+    import torch
+    import torch.distributed as dist
+
+    from paper_2604_09107_b200 import ros
+    from paper_2604_09107_b200.dist import DistCluster
+    from paper_2604_09107_b200.ros import Status
+    try:
+        gpu = rank % torch.cuda.device_count()
+        torch.cuda.set_device(gpu)
+        dev = torch.device("cuda", gpu)
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        dc = DistCluster()
+        sizes = [1 << 30, 6000, 3 << 20]
+
+        def make(name, seed=None, **cfg):
+            h = dc.create("m", name, 1, tiny_threshold=1 << 20, pull_timeout_s=30.0, **cfg)
+            bufs = [torch.zeros(n, dtype=torch.uint8, device=dev) for n in sizes]
+            for i, b in enumerate(bufs):
+                if seed is not None:
+                    ros.synth_bf16(b, seed + i)
+                assert h.register_tensor(0, f"w{i}", b) == Status.ok
+            return h, bufs
+
+        if rank == 0:
+            t, tb = make("T", seed=700)
+            a, ab = make("A", grid_sms=1)
+            torch.cuda.synchronize()
+        else:
+            b, bb = make("B")
+        dc.open(t if rank == 0 else b, endpoints=[f"rank{rank}:cuda{gpu}"])
+        dc.open(a if rank == 0 else None, endpoints=[f"rank{rank}:cuda{gpu}"])
+        assert (dc.publish(t if rank == 0 else None, 1) or ros.OpResult(Status.ok)).status == 0
+        out = {}
+        dc.replicate_start(a if rank == 0 else None, "latest")
+        if rank == 0:
+            t0 = time.time()
+            while True:
+                done, nb = dc.progress(a, 0)
+                if done > 0 or time.time() - t0 > 20:
+                    break
+                time.sleep(1e-4)
+            out["a_progress_at_join"] = (done, nb)
+        dist.barrier(group=dc.pg)
+        dc.replicate_start(b if rank == 1 else None, "latest")
+        if rank == 1:
+            out["b_assignment"] = b.transfer_assignment(0)
+        res = dc.replicate_finish(a if rank == 0 else b)
+        out["status"] = int(res.status)
+        mine = tb if rank == 0 else bb
+        dig = ros.digest_spans([x.data_ptr() for x in mine], sizes, gpu)
+        if rank == 0:
+            out["a_equal"] = ros.digest_spans([x.data_ptr() for x in ab], sizes, gpu) == dig
+        got = dc.gather(dig)
+        out["b_equal"] = got[0] == got[1]
+        out["tables"] = dc.gather(__import__("hashlib").sha256(
+            (a if rank == 0 else b).chunk_digests(0).tobytes()).hexdigest())
+        out["plan"] = sorted({(x.replica, x.src) for x in dc.assigns()})
+        q.put((rank, out))
+        dc.close()
+        dist.destroy_process_group()
+    except Exception as e:  # pragma: no cover - surfaced by the parent
+        import traceback
+        q.put((rank, {"error": repr(e) + traceback.format_exc()}))
+        raise
+
+
+def test_late_joiner_in_another_process_chases_a_filling_copy():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_join_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    res = {}
+    for _ in range(2):
+        r = q.get(timeout=300)
+        res[r[0]] = r[1]
+    for p in ps:
+        p.join(timeout=60)
+    for r in range(2):
+        assert "error" not in res[r], res[r].get("error")
+        assert res[r]["status"] == 0, res[r]
+        assert res[r]["b_equal"]
+    done, nb = res[0]["a_progress_at_join"]
+    assert 0 < done < nb, (done, nb)  # A was part-way through when B was planned
+    a = res[1]["b_assignment"]
+    assert a["source_replica"] == "A" and a["source_complete"] is False, a
+    assert res[0]["a_equal"]
+    assert res[0]["tables"][0] == res[0]["tables"][1]  # A's and B's chunk tables
+    assert ("A", "T") in res[0]["plan"] and ("B", "A") in res[0]["plan"]

@@ -112,3 +112,28 @@ def test_e4m3_cast_definition(oracle, x, want):
 
 def test_e4m3_nan(oracle):
     assert int(oracle.bf16_to_e4m3(np.array([0x7FC0], np.uint16))[0]) == 0x7F
+
+
+def test_scale_fixture_is_pinned_to_the_port(oracle):
+    """tests/golden/scale.json (reference digests at BASELINE scale) agrees
+    with the oracle's generator + XXH64 on the tensors small enough to redo
+    here: the norms of Llama-3-8B and of the Llama-3-70B TP-8 shard (bytes
+    and e4m3 cast)."""
+    import json
+    from tests.conftest import golden
+    import bench as B
+    g = json.load(open(golden("scale.json")))
+    c2 = g["config2_llama3_8b"]
+    assert c2["tensors"] == 291 and c2["items"] == 227 and c2["bytes"] == 16_060_522_496
+    assert len(c2["item_digests"]) == 227 and c2["chunks"] == 3_921_026
+    for key, cast in (("config2_llama3_8b", False), ("config5_llama3_70b_tp8", True)):
+        shapes = B.workload_shapes(g[key]["workload"])
+        for i, (n, s) in enumerate(shapes):
+            if "norm" not in n or i % 7:
+                continue
+            a = oracle.synth_bf16(42 + i, s[0])
+            assert "%016X" % oracle.xxh64(a) == g[key]["tensor_digests"][i], n
+            if cast:
+                assert "%016X" % oracle.xxh64(oracle.bf16_to_e4m3(a)) == g[key]["cast_digests"][i], n
+    c3 = g["config3_qwen25_32b"]
+    assert len(c3["trainer_shards"]) == 8 and len(c3["reader_slice_digests"]) == 2
