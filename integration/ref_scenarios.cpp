@@ -1,0 +1,260 @@
+// The reference's own client scenarios, run through the two integration
+// levels of INTEGRATION.md on a GPU.  Compiled against the UNMODIFIED
+// reference headers (/root/reference/proj/include) and linked with the
+// reference library built from its sources (oracle/_ref) plus libros_b200.so.
+//
+//   level A  B200Client (refstore_b200/b200_client.hpp) over the C ABI,
+//            device-resident regions;
+//   level B  the reference ClientCore + ServerCore + SimExecutor, with
+//            B200Transport (refstore_b200/b200_transport.hpp) as the
+//            DataTransport -- the reference's own pull loop and item
+//            verification, the B200 kernel moving the bytes.
+//
+// Scenarios (tests/unit/test_client_core.cpp):
+//   replicate pulls bytes that verify against the manifest  :163-202
+//   corrupt source: quiet retry, report, re-pick             :346-377
+//
+// Prints one "PASS <level> <scenario> k=v ..." or "FAIL ..." line per
+// scenario; exit status 0 iff every scenario passed.  --list prints the
+// scenario names without touching a GPU.
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <cstring>
+#include <functional>
+#include <map>
+#include <memory>
+#include <optional>
+#include <string>
+#include <vector>
+
+#include "refstore/client_core.hpp"
+#include "refstore/server_core.hpp"
+#include "refstore/trace.hpp"
+#include "refstore/transport_mem.hpp"
+#include "refstore_b200/b200_client.hpp"
+#include "refstore_b200/b200_transport.hpp"
+
+using namespace refstore;
+
+namespace {
+
+int failures = 0;
+
+void report(bool ok, const char* level, const char* scenario, const std::string& kv) {
+  std::printf("%s %s %s %s\n", ok ? "PASS" : "FAIL", level, scenario, kv.c_str());
+  std::fflush(stdout);
+  if (!ok) ++failures;
+}
+
+// fill pattern of the reference ClusterFix (test_client_core.cpp:76-81)
+std::vector<std::byte> pattern(std::size_t len, std::uint64_t salt) {
+  std::vector<std::byte> v(len);
+  for (std::size_t i = 0; i < len; ++i) v[i] = std::byte((salt * 1315423911u + i * 131u) & 0xff);
+  return v;
+}
+
+struct Tensor {
+  std::uint32_t shard;
+  std::string name;
+  std::size_t len;
+  std::uint64_t salt;
+};
+const std::vector<Tensor> kT = {{0, "big", 3u << 20, 7}, {0, "t1", 1000, 8}, {0, "t2", 2000, 9},
+                                {1, "u1", 4096, 10}};
+const std::uint64_t kBytes = (3u << 20) + 1000 + 2000 + 4096;
+
+std::string counters(const ClientCore::Stats& s) {
+  return "items_verified=" + std::to_string(s.items_verified) +
+         " bytes_pulled=" + std::to_string(s.bytes_pulled) +
+         " checksum_failures=" + std::to_string(s.checksum_failures) +
+         " failure_reports=" + std::to_string(s.failure_reports);
+}
+
+// ------------------------------------------------------------------ level A
+struct DevBufs {
+  std::map<std::pair<std::uint32_t, std::string>, std::byte*> p;
+  ~DevBufs() {
+    for (auto& [k, v] : p) cudaFree(v);
+  }
+  std::span<std::byte> make(const Tensor& t, std::uint64_t salt) {
+    std::byte* d = nullptr;
+    cudaMalloc(&d, t.len);
+    auto h = pattern(t.len, salt);
+    cudaMemcpy(d, h.data(), t.len, cudaMemcpyHostToDevice);
+    p[{t.shard, t.name}] = d;
+    return {d, t.len};
+  }
+  std::vector<std::byte> host(const Tensor& t) const {
+    std::vector<std::byte> h(t.len);
+    cudaMemcpy(h.data(), p.at({t.shard, t.name}), t.len, cudaMemcpyDeviceToHost);
+    return h;
+  }
+};
+
+void level_a_replicate() {
+  B200Cluster cl;
+  DevBufs tb, rb;
+  B200Client t(cl, "m", "T", 2);
+  for (const auto& x : kT) t.register_tensor(x.shard, x.name, tb.make(x, x.salt));
+  std::optional<ClientCore::OpResult> pr;
+  t.publish(1, [&](ClientCore::OpResult r) { pr = r; });
+  B200Client w(cl, "m", "R", 2);
+  for (const auto& x : kT) w.register_tensor(x.shard, x.name, rb.make(x, 100));
+  std::optional<ClientCore::OpResult> rr;
+  w.replicate(VersionSpec::latest(), [&](ClientCore::OpResult r) { rr = r; });
+  bool ok = pr && pr->status == Status::ok && rr && rr->status == Status::ok && rr->version == VersionId{1};
+  ok &= w.is_published() && w.current_version() == VersionId{1};
+  for (const auto& x : kT) ok &= rb.host(x) == pattern(x.len, x.salt);
+  const auto s = w.stats();
+  ok &= s.items_verified == 3 && s.bytes_pulled == kBytes && s.checksum_failures == 0;
+  auto view = cl.replica_view("m", "R");
+  ok &= view && view->lifecycle == "published" && view->version == VersionId{1};
+  auto lm = cl.listing("m");
+  ok &= lm.count(1) && lm[1].count("T") && lm[1].count("R");
+  report(ok, "A", "replicate_pulls_bytes_that_verify", counters(s));
+}
+
+// ------------------------------------------------------------------ level B
+// ClusterFix (test_client_core.cpp:23-117) with B200Transport as the data
+// plane and managed memory regions.
+struct RefFix {
+  SimExecutor exec;
+  TraceLog log;
+  MemNetwork net;
+  B200Transport b200{&net, 0};
+  ServerCore srv;
+  struct Node {
+    ServeRegistry serves;
+    std::map<std::pair<std::uint32_t, std::string>, std::byte*> bufs;
+    std::unique_ptr<ClientCore> core;
+    ~Node() {
+      core.reset();
+      for (auto& [k, v] : bufs) cudaFree(v);
+    }
+  };
+  std::map<std::string, std::unique_ptr<Node>> nodes;
+
+  RefFix() : srv("A", ServerConfig{}, &exec, &log, net.sender()) {
+    net.register_server("A", &srv, &exec);
+    srv.start();
+  }
+  ~RefFix() {
+    nodes.clear();
+    srv.stop();
+  }
+  ClientCore& make(const std::string& replica, std::uint32_t shards) {
+    auto n = std::make_unique<Node>();
+    ClientConfig cfg;
+    cfg.servers = {"A"};
+    cfg.data_endpoint = "ep:" + replica;
+    b200.register_data(cfg.data_endpoint, &n->serves);
+    n->core = std::make_unique<ClientCore>("m", replica, shards, cfg, &exec, &log, &net, &b200,
+                                           &n->serves);
+    ClientCore& r = *n->core;
+    nodes[replica] = std::move(n);
+    return r;
+  }
+  void reg(const std::string& replica, const Tensor& t, std::uint64_t salt) {
+    Node& n = *nodes.at(replica);
+    std::byte* p = nullptr;
+    cudaMallocManaged(&p, t.len);
+    auto h = pattern(t.len, salt);
+    std::memcpy(p, h.data(), t.len);
+    n.bufs[{t.shard, t.name}] = p;
+    n.core->register_tensor(t.shard, t.name, {p, t.len});
+  }
+  bool same(const std::string& a, const std::string& b, const Tensor& t) {
+    cudaDeviceSynchronize();
+    return std::memcmp(nodes.at(a)->bufs.at({t.shard, t.name}), nodes.at(b)->bufs.at({t.shard, t.name}),
+                       t.len) == 0;
+  }
+  ClientCore::OpResult run(std::function<void(ClientCore::OpFn)> op) {
+    std::optional<ClientCore::OpResult> out;
+    op([&](ClientCore::OpResult r) { out = std::move(r); });
+    Time h = exec.now() + std::chrono::seconds(60);
+    while (!out && exec.step(h)) {
+    }
+    if (!out) {
+      ClientCore::OpResult r;
+      r.status = Status::timeout;
+      return r;
+    }
+    return std::move(*out);
+  }
+  void settle() {
+    Time h = exec.now() + std::chrono::seconds(5);
+    while (exec.step(h)) {
+    }
+  }
+};
+
+void level_b_replicate() {
+  RefFix fx;
+  ClientCore& t = fx.make("T", 2);
+  for (const auto& x : kT) fx.reg("T", x, x.salt);
+  bool ok = fx.run([&](auto cb) { t.publish(1, cb); }).status == Status::ok;
+  ClientCore& w = fx.make("R", 2);
+  for (const auto& x : kT) fx.reg("R", x, 100);
+  auto r = fx.run([&](auto cb) { w.replicate(VersionSpec::latest(), cb); });
+  ok &= r.status == Status::ok && r.version == VersionId{1};
+  ok &= w.is_published() && w.current_version() == VersionId{1};
+  for (const auto& x : kT) ok &= fx.same("T", "R", x);
+  const auto s = w.stats();
+  ok &= s.items_verified == 3 && s.bytes_pulled == kBytes && s.checksum_failures == 0;
+  fx.settle();
+  auto view = fx.srv.replica_view("m", "R");
+  ok &= view && view->lifecycle == "published" && view->version == VersionId{1};
+  // the bytes moved on the GPU, through the B200 kernel
+  ok &= fx.b200.device_pulls() > 0 && fx.b200.device_bytes() == kBytes;
+  report(ok, "B", "replicate_pulls_bytes_that_verify",
+         counters(s) + " device_pulls=" + std::to_string(fx.b200.device_pulls()) +
+             " device_bytes=" + std::to_string(fx.b200.device_bytes()));
+}
+
+void level_b_corrupt_source() {
+  // test_client_core.cpp:346-377: T2's copy is corrupted in place; the
+  // reader's item check fails, retries quietly, reports, and re-picks T1.
+  RefFix fx;
+  const std::vector<Tensor> ts = {{0, "big", 3u << 20, 11}, {0, "tiny", 5000, 12}};
+  ClientCore& t1 = fx.make("T1", 1);
+  for (const auto& x : ts) fx.reg("T1", x, x.salt);
+  bool ok = fx.run([&](auto cb) { t1.publish(1, cb); }).status == Status::ok;
+  ClientCore& t2 = fx.make("T2", 1);
+  fx.reg("T2", ts[0], 20);
+  fx.reg("T2", ts[1], 21);
+  ok &= fx.run([&](auto cb) { t2.replicate(VersionSpec::latest(), cb); }).status == Status::ok;
+  cudaDeviceSynchronize();
+  fx.nodes.at("T2")->bufs.at({0, "big"})[17] ^= std::byte{0xFF};
+  ClientCore& w = fx.make("R", 1);
+  fx.reg("R", ts[0], 30);
+  fx.reg("R", ts[1], 31);
+  auto r = fx.run([&](auto cb) { w.replicate(VersionSpec::latest(), cb); });
+  ok &= r.status == Status::ok;
+  const auto s = w.stats();
+  ok &= s.checksum_failures == 2 && s.failure_reports == 1;
+  for (const auto& x : ts) ok &= fx.same("T1", "R", x);
+  ok &= fx.srv.listing("m")[1].count("T2") == 1;  // corruption does not condemn
+  report(ok, "B", "corrupt_source_quiet_retry_report_repick", counters(s));
+}
+
+}  // namespace
+
+int main(int argc, char** argv) {
+  const std::vector<std::pair<const char*, void (*)()>> scenarios = {
+      {"A replicate_pulls_bytes_that_verify", level_a_replicate},
+      {"B replicate_pulls_bytes_that_verify", level_b_replicate},
+      {"B corrupt_source_quiet_retry_report_repick", level_b_corrupt_source},
+  };
+  if (argc > 1 && std::strcmp(argv[1], "--list") == 0) {
+    for (const auto& [name, fn] : scenarios) std::printf("%s\n", name);
+    return 0;
+  }
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) {
+    std::printf("FAIL no CUDA device\n");
+    return 2;
+  }
+  for (const auto& [name, fn] : scenarios) fn();
+  return failures ? 1 : 0;
+}

@@ -1,0 +1,57 @@
+"""The drop-in boundary proven from the reference side.
+
+integration/ref_scenarios.cpp compiles the reference-side adapters
+(integration/refstore_b200/: level A B200Client over the C ABI, level B
+B200Transport as the reference's DataTransport) against the UNMODIFIED
+reference headers and links them with the reference library built from its
+own sources (oracle/_ref) and libros_b200.so.  It then runs the reference's
+client scenarios (tests/unit/test_client_core.cpp:163-202 and :346-377) on
+the GPU and checks the reference's own counters: items_verified == 3,
+bytes_pulled exact, checksum_failures == 0 (2 + one report for the corrupt
+source), bytes identical.
+
+CPU: the binary builds (here, where /root/reference exists) and lists its
+scenarios without a GPU.  GPU: every scenario passes."""
+import os
+import subprocess
+
+import pytest
+
+from tests.conftest import ROOT
+
+BIN = os.path.join(ROOT, "integration", "_build", "ref_scenarios")
+SCENARIOS = ["A replicate_pulls_bytes_that_verify", "B replicate_pulls_bytes_that_verify",
+             "B corrupt_source_quiet_retry_report_repick"]
+
+
+def _binary():
+    if os.path.isdir("/root/reference/proj/include"):
+        subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "oracle"), "ref"], check=True)
+        subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "integration")], check=True)
+    if not os.path.exists(BIN):
+        pytest.skip("integration/_build/ref_scenarios not built (needs /root/reference headers)")
+    return BIN
+
+
+def test_reference_side_adapters_build_and_list():
+    r = subprocess.run([_binary(), "--list"], capture_output=True, text=True, timeout=60)
+    assert r.returncode == 0, r.stderr
+    assert r.stdout.split("\n")[:3] == SCENARIOS
+
+
+@pytest.mark.gpu
+def test_reference_scenarios_through_the_b200_path():
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    r = subprocess.run([_binary()], capture_output=True, text=True, timeout=600)
+    lines = [x for x in r.stdout.splitlines() if x.startswith(("PASS", "FAIL"))]
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert [" ".join(x.split()[1:3]) for x in lines] == SCENARIOS
+    kv = {" ".join(x.split()[1:3]): dict(f.split("=") for f in x.split()[3:]) for x in lines}
+    for name in SCENARIOS[:2]:
+        assert kv[name]["items_verified"] == "3"
+        assert kv[name]["bytes_pulled"] == str((3 << 20) + 1000 + 2000 + 4096)
+        assert kv[name]["checksum_failures"] == "0"
+    assert int(kv[SCENARIOS[1]]["device_pulls"]) > 0
+    assert kv[SCENARIOS[2]]["checksum_failures"] == "2" and kv[SCENARIOS[2]]["failure_reports"] == "1"
