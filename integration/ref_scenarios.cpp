@@ -206,10 +206,16 @@ void level_b_replicate() {
   auto view = fx.srv.replica_view("m", "R");
   ok &= view && view->lifecycle == "published" && view->version == VersionId{1};
   // the bytes moved on the GPU, through the B200 kernel
-  ok &= fx.b200.device_pulls() > 0 && fx.b200.device_bytes() == kBytes;
+  // the registered regions' bytes moved on the GPU, through the B200 kernel;
+  // the packed groups (host-heap staging in the reference client) on the host
+  ok &= fx.b200.device_pulls() > 0 && fx.b200.device_bytes() == (3u << 20) &&
+        fx.b200.device_bytes() + fx.b200.host_bytes() == kBytes;
   report(ok, "B", "replicate_pulls_bytes_that_verify",
          counters(s) + " device_pulls=" + std::to_string(fx.b200.device_pulls()) +
-             " device_bytes=" + std::to_string(fx.b200.device_bytes()));
+             " device_bytes=" + std::to_string(fx.b200.device_bytes()) +
+             " host_bytes=" + std::to_string(fx.b200.host_bytes()) +
+             " last_error=" + std::to_string(fx.b200.last_error()) +
+             " status=" + std::to_string(static_cast<int>(r.status)));
 }
 
 void level_b_corrupt_source() {
@@ -250,11 +256,33 @@ int main(int argc, char** argv) {
     for (const auto& [name, fn] : scenarios) std::printf("%s\n", name);
     return 0;
   }
+  if (argc > 1 && std::strcmp(argv[1], "--probe") == 0) {
+    // one managed-memory copy through rs_pull_spans (diagnostic)
+    const std::size_t len = 8u << 20;
+    std::byte *a = nullptr, *b = nullptr;
+    cudaMallocManaged(&a, len);
+    cudaMallocManaged(&b, len);
+    auto h = pattern(len, 5);
+    std::memcpy(a, h.data(), len);
+    std::uint64_t src = reinterpret_cast<std::uint64_t>(a), dst = reinterpret_cast<std::uint64_t>(b), n = len;
+    int code = -1;
+    float ms = 0;
+    int rc = rs_pull_spans(&src, &dst, &n, 1, 4096, nullptr, nullptr, 0, nullptr, &code, &ms);
+    cudaDeviceSynchronize();
+    std::printf("probe rc=%d code=%d equal=%d err=%s\n", rc, code, std::memcmp(a, b, len) == 0,
+                cudaGetErrorString(cudaGetLastError()));
+    return rc;
+  }
   int n = 0;
   if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) {
     std::printf("FAIL no CUDA device\n");
     return 2;
   }
-  for (const auto& [name, fn] : scenarios) fn();
+  for (const auto& [name, fn] : scenarios) {
+    if (argc > 1 && std::strstr(name, argv[1]) == nullptr) continue;  // a filter
+    std::fprintf(stderr, "[scenario] %s\n", name);
+    fn();
+    std::fprintf(stderr, "[scenario] %s done\n", name);
+  }
   return failures ? 1 : 0;
 }

@@ -17,11 +17,14 @@
 
 #include <algorithm>
 #include <atomic>
+#include <cstring>
 #include <cstdint>
 #include <map>
 #include <mutex>
 #include <string>
 #include <vector>
+
+#include <cuda_runtime.h>
 
 #include "refstore/transport.hpp"
 #include "refstore/transport_mem.hpp"
@@ -89,13 +92,53 @@ class B200Transport : public DataTransport {
           in_dest = 0;
         }
       }
-      int code = 0;
-      float ms = 0;
-      const int rc = rs_pull_spans(srcs.data(), dsts.data(), lens.data(), static_cast<int>(srcs.size()),
-                                   4096, nullptr, nullptr, device_, nullptr, &code, &ms);
-      if (rc != 0 || code != 0) r.status = Status::transfer_failed;
+      // Registered regions (device or managed memory) move on the GPU.  The
+      // reference's packed-group staging lives on the host heap (pageable,
+      // Payload::group_bufs), which the GPU cannot address: those few small
+      // spans are copied on the host, exactly as MemNetwork would.
+      auto gpu_addressable = [](std::uint64_t p) {
+        cudaPointerAttributes a{};
+        const bool ok = cudaPointerGetAttributes(&a, reinterpret_cast<void*>(p)) == cudaSuccess &&
+                        (a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged);
+        cudaGetLastError();
+        return ok;
+      };
+      std::vector<std::uint64_t> ks, kd, kl;
+      for (std::size_t k = 0; k < srcs.size(); ++k) {
+        if (gpu_addressable(srcs[k]) && gpu_addressable(dsts[k])) {
+          ks.push_back(srcs[k]);
+          kd.push_back(dsts[k]);
+          kl.push_back(lens[k]);
+        } else {
+          cudaDeviceSynchronize();  // managed pages the GPU may still hold
+          std::memcpy(reinterpret_cast<void*>(dsts[k]), reinterpret_cast<const void*>(srcs[k]), lens[k]);
+          host_bytes_.fetch_add(lens[k]);
+        }
+      }
+      if (!ks.empty()) {
+        // managed regions migrate to the pulling GPU first, so the kernel's
+        // bulk-tensor copies touch resident pages (the reference's host-side
+        // digest faults them back afterwards)
+        for (std::size_t k = 0; k < ks.size(); ++k)
+          for (std::uint64_t p : {ks[k], kd[k]}) {
+            cudaPointerAttributes a{};
+            if (cudaPointerGetAttributes(&a, reinterpret_cast<void*>(p)) == cudaSuccess &&
+                a.type == cudaMemoryTypeManaged)
+              cudaMemPrefetchAsync(reinterpret_cast<void*>(p), kl[k], device_, nullptr);
+            cudaGetLastError();
+          }
+        cudaStreamSynchronize(nullptr);
+        int code = 0;
+        float ms = 0;
+        const int rc = rs_pull_spans(ks.data(), kd.data(), kl.data(), static_cast<int>(ks.size()), 4096,
+                                     nullptr, nullptr, device_, nullptr, &code, &ms);
+        if (rc != 0 || code != 0) {
+          r.status = Status::transfer_failed;
+          last_error_.store((static_cast<std::uint64_t>(rc) << 32) | static_cast<std::uint32_t>(code));
+        }
+        for (auto l : kl) device_bytes_.fetch_add(l);
+      }
       pulls_.fetch_add(1);
-      device_bytes_.fetch_add(s.bytes - left);
     }
     if (ok(r.status) && spec.activity) spec.activity->fetch_add(1);
     exec->post([done = std::move(done), r] { done(r); });
@@ -108,13 +151,16 @@ class B200Transport : public DataTransport {
 
   std::uint64_t device_pulls() const { return pulls_.load(); }
   std::uint64_t device_bytes() const { return device_bytes_.load(); }
+  std::uint64_t host_bytes() const { return host_bytes_.load(); }  // group staging on the host
+  // (rs_pull_spans status << 32 | kernel code) of the last failed pull, 0: none
+  std::uint64_t last_error() const { return last_error_.load(); }
 
  private:
   MemNetwork* net_;
   int device_;
   std::mutex m_;
   std::map<std::string, ServeRegistry*> data_;
-  std::atomic<std::uint64_t> pulls_{0}, device_bytes_{0};
+  std::atomic<std::uint64_t> pulls_{0}, device_bytes_{0}, host_bytes_{0}, last_error_{0};
 };
 
 }  // namespace refstore

@@ -3,6 +3,7 @@
 
 #include <cuda_runtime.h>
 
+#include <cstdio>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -782,8 +783,14 @@ int rs_pull_spans(const uint64_t* src_ptrs, const uint64_t* dst_ptrs, const uint
   rsb::dev::PullStatus ps{};
   rsb::dev::PullParams p{};
   const rsb::dev::SrcDesc sdesc{expect_dev, nullptr, 0, 0};
-  if (rsb::dev::upload_pull_plan(device, stream, descs.data(), static_cast<std::uint32_t>(n_items),
-                                 &sdesc, 1, chunk, &plan, &p) != cudaSuccess)
+  const bool debug = std::getenv("RSB_DEBUG") != nullptr;
+  auto failed = [&](cudaError_t e, const char* what) {
+    if (e == cudaSuccess) return false;
+    if (debug) std::fprintf(stderr, "[rsb] rs_pull_spans: %s: %s\n", what, cudaGetErrorString(e));
+    return true;
+  };
+  if (failed(rsb::dev::upload_pull_plan(device, stream, descs.data(), static_cast<std::uint32_t>(n_items),
+                                        &sdesc, 1, chunk, &plan, &p), "plan upload"))
     rc = st(rsb::Status::transfer_failed);
   if (!rc) {
     p.remote = remote ? 1u : 0u;
@@ -791,11 +798,11 @@ int rs_pull_spans(const uint64_t* src_ptrs, const uint64_t* dst_ptrs, const uint
     p.timeout_ns = 4000000000ull;
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
-    if (cudaEventRecord(e0, stream) != cudaSuccess ||
-        rsb::dev::launch_pull(p, rsb::dev::pull_grid(device), stream) != cudaSuccess ||
-        cudaEventRecord(e1, stream) != cudaSuccess ||
-        cudaMemcpyAsync(&ps, p.status, sizeof(ps), cudaMemcpyDeviceToHost, stream) != cudaSuccess ||
-        cudaStreamSynchronize(stream) != cudaSuccess)
+    if (failed(cudaEventRecord(e0, stream), "event") ||
+        failed(rsb::dev::launch_pull(p, rsb::dev::pull_grid(device), stream), "launch") ||
+        failed(cudaEventRecord(e1, stream), "event") ||
+        failed(cudaMemcpyAsync(&ps, p.status, sizeof(ps), cudaMemcpyDeviceToHost, stream), "status copy") ||
+        failed(cudaStreamSynchronize(stream), "kernel"))
       rc = st(rsb::Status::transfer_failed);
     float ms = 0;
     if (!rc) cudaEventElapsedTime(&ms, e0, e1);

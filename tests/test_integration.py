@@ -54,4 +54,5 @@ def test_reference_scenarios_through_the_b200_path():
         assert kv[name]["bytes_pulled"] == str((3 << 20) + 1000 + 2000 + 4096)
         assert kv[name]["checksum_failures"] == "0"
     assert int(kv[SCENARIOS[1]]["device_pulls"]) > 0
+    assert int(kv[SCENARIOS[1]]["device_bytes"]) == 3 << 20  # the big item, moved by the kernel
     assert kv[SCENARIOS[2]]["checksum_failures"] == "2" and kv[SCENARIOS[2]]["failure_reports"] == "1"
