@@ -96,9 +96,22 @@ int rs_cluster_listing(rs_cluster* c, const char* model, char* buf, size_t cap, 
 /* ServerCore::replica_view (server_core.hpp:42-50). lifecycle buffer >= 16. */
 int rs_cluster_view(rs_cluster* c, const char* model, const char* replica, char* lifecycle,
                     uint64_t* version, uint32_t* serving, int* visible);
+/* ReplicaView.min_progress (server_core.hpp:48): the fewest verified items
+ * over the replica's shards, as its fills report them (ProgressMsg,
+ * client_core.cpp:1414-1439) -- it advances while a fill runs. */
+int rs_cluster_progress(rs_cluster* c, const char* model, const char* replica,
+                        uint64_t* min_progress);
 /* The source replica a replicating replica currently pulls from ("" if none). */
 int rs_cluster_source(rs_cluster* c, const char* model, const char* replica, char* buf,
                       size_t cap, size_t* len);
+/* The box's measured topology, as the planner's source cost (pick_source,
+ * server_core.cpp:1517-1543, gains the term between same_dc and serving):
+ * cost[i * n + j] is the cost for a reader whose first data endpoint is
+ * endpoints[i] to pull from a source whose first endpoint is endpoints[j]
+ * (lower is nearer; pairs not listed cost 0).  A uniform matrix (every GPU
+ * pair one NVSwitch hop) leaves every plan exactly the reference's. */
+int rs_cluster_set_topology(rs_cluster* c, uint32_t n, const char* const* endpoints,
+                            const int32_t* cost);
 /* Fault hook (MemNetwork::set_data_silent, transport_mem.hpp:33-46): a
  * silent replica's data plane never answers, so its readers time out. */
 int rs_cluster_set_silent(rs_cluster* c, const char* model, const char* replica, int silent);

@@ -54,6 +54,8 @@ _SIGS = {
     "rs_cluster_listing": (i32, [vp, cstr, vp, sz, C.POINTER(sz)]),
     "rs_cluster_view": (i32, [vp, cstr, cstr, vp, C.POINTER(u64), C.POINTER(u32), C.POINTER(i32)]),
     "rs_cluster_set_silent": (i32, [vp, cstr, cstr, i32]),
+    "rs_cluster_set_topology": (i32, [vp, u32, vp, vp]),
+    "rs_cluster_progress": (i32, [vp, cstr, cstr, C.POINTER(u64)]),
     "rs_cluster_source": (i32, [vp, cstr, cstr, vp, sz, C.POINTER(sz)]),
     "rs_open": (i32, [vp, cstr, cstr, u32, C.POINTER(RsConfig), C.POINTER(vp)]),
     "rs_register": (i32, [vp, u32, cstr, vp, u64]),

@@ -30,6 +30,7 @@ def run(args):
     import torch.distributed as dist
 
     import bench as B
+    from paper_2604_09107_b200 import ros
     from paper_2604_09107_b200.dist import DistCluster
     from paper_2604_09107_b200.ros import Status
 
@@ -42,6 +43,10 @@ def run(args):
     dev = torch.device("cuda", local)
     dist.init_process_group("gloo")
     dc = DistCluster()
+    # the planner's topology term from the box's NVLink state (NVML); every
+    # pair of an NVSwitch box is one hop, so the plan stays the reference's
+    topo = ros.nvlink_cost_matrix(world) if rank == 0 else None
+    dc.set_topology([f"rank{i}:cuda{i}" for i in range(world)], topo or [])
     shapes = B.workload_shapes(args.workload)
     total = sum(2 * B._numel(s) for _, s in shapes)
     # chain (default): rank 0 trains, ranks 1.. read (planner: a chain).

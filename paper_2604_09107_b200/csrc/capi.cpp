@@ -158,6 +158,15 @@ int rs_cluster_view(rs_cluster* c, const char* model, const char* replica, char*
   return 0;
 }
 
+int rs_cluster_progress(rs_cluster* c, const char* model, const char* replica,
+                        uint64_t* min_progress) {
+  if (!c || !model || !replica || !min_progress) return st(rsb::Status::invalid_argument);
+  auto v = c->reg.view(model, replica);
+  if (!v) return st(rsb::Status::not_found);
+  *min_progress = v->min_progress;
+  return 0;
+}
+
 int rs_cluster_source(rs_cluster* c, const char* model, const char* replica, char* buf,
                       size_t cap, size_t* len) {
   if (!c || !model || !replica) return st(rsb::Status::invalid_argument);
@@ -323,6 +332,25 @@ int rs_close(rs_handle* h) {
   auto s = h->client->close();
   delete h;
   return st(s);
+}
+
+int rs_cluster_set_topology(rs_cluster* c, uint32_t n, const char* const* endpoints,
+                            const int32_t* cost) {
+  if (!c || (n && (!endpoints || !cost))) return st(rsb::Status::invalid_argument);
+  auto m = std::make_shared<std::map<std::pair<std::string, std::string>, int>>();
+  for (uint32_t i = 0; i < n; ++i) {
+    if (!endpoints[i]) return st(rsb::Status::invalid_argument);
+    for (uint32_t j = 0; j < n; ++j) (*m)[{endpoints[i], endpoints[j]}] = cost[std::size_t(i) * n + j];
+  }
+  if (n == 0) {
+    c->reg.set_topology(nullptr);
+    return 0;
+  }
+  c->reg.set_topology([m](const std::string& reader, const std::string& source) {
+    auto it = m->find({reader, source});
+    return it == m->end() ? 0 : it->second;
+  });
+  return 0;
 }
 
 int rs_locate(rs_cluster* c, const char* model, const char* replica, const char* spec,

@@ -1053,6 +1053,7 @@ Status Client::bind(Shard& sh, const Assignment& a, VersionId v) {
       sh.holding->landed_some = false;
     }
     sh.partial_version = v;
+    sh.reported = 0;
     return Status::ok;
   }
   auto mr = Manifest::decode(a.manifest);
@@ -1119,6 +1120,7 @@ Status Client::bind(Shard& sh, const Assignment& a, VersionId v) {
   p->epoch = ++sh.epoch_ctr;
   sh.holding = std::move(p);
   sh.partial_version = v;
+  sh.reported = 0;
   return Status::ok;
 }
 
@@ -1485,6 +1487,36 @@ void Client::launch_shards(const std::vector<Assignment>& as,
   }
 }
 
+void Client::report_progress(Shard& sh) {
+  if (!sh.holding || sh.holding->reshard || !sh.holding->flags.p) return;
+  const Payload& p = *sh.holding;
+  const ChunkMap& cm = p.cmap;
+  const std::uint32_t nb = cm.n_batches();
+  DeviceGuard g(sh.device);
+  if (!sh.poll && cudaStreamCreateWithFlags(&sh.poll, cudaStreamNonBlocking) != cudaSuccess) return;
+  sh.flag_host.resize(nb);
+  if (cudaMemcpyAsync(sh.flag_host.data(), p.flags.p, std::size_t(nb) * 4, cudaMemcpyDeviceToHost,
+                      sh.poll) != cudaSuccess ||
+      cudaStreamSynchronize(sh.poll) != cudaSuccess)
+    return;
+  stats_.d2h_bytes += std::size_t(nb) * 4;
+  // items are verified front to back only as a prefix: the first item with a
+  // batch below the epoch ends it
+  std::uint64_t items = sh.reported;
+  for (std::size_t i = items; i + 1 < cm.chunk0.size(); ++i) {
+    const std::uint32_t b0 = cm.chunk0[i] / dev::kBatchChunks;
+    const std::uint32_t n = (cm.count[i] + dev::kBatchChunks - 1) / dev::kBatchChunks;
+    bool done = true;
+    for (std::uint32_t b = b0; b < b0 + n && done; ++b) done = sh.flag_host[b] == p.epoch;
+    if (!done) break;
+    items = i + 1;
+  }
+  if (items > sh.reported) {
+    sh.reported = items;
+    reg_->progress(model_, replica_, sh.idx, items);
+  }
+}
+
 Status Client::progress(std::uint32_t shard, std::uint32_t* batches_done, std::uint32_t* n_batches) {
   if (shard >= num_shards_ || !is_local(shard)) return Status::invalid_argument;
   Shard& sh = shards_[shard];
@@ -1499,6 +1531,7 @@ Status Client::progress(std::uint32_t shard, std::uint32_t* batches_done, std::u
   RS_CUDA(cudaMemcpyAsync(&v, &status->batches_done, 4, cudaMemcpyDeviceToHost, sh.poll));
   RS_CUDA(cudaStreamSynchronize(sh.poll));
   *batches_done = v;
+  report_progress(sh);
   return Status::ok;
 }
 
@@ -1521,6 +1554,19 @@ std::vector<Client::FillOutcome> Client::wait_shards(const std::vector<std::uint
     if (tcp) {  // nothing queued behind the kernel (launch_fill): wait, then read
       cudaStreamSynchronize(sh.stream);
       host_ms = std::chrono::duration<float, std::milli>(std::chrono::steady_clock::now() - sh.t_launch).count();
+    } else if (!sh.holding->reshard) {
+      // Spin on the fill's end event; a fill still running after 10 ms
+      // reports its verified item prefix to the registry every 10 ms
+      // (task_progress), so the replica's view advances while it lands.
+      auto next = sh.t_launch + std::chrono::milliseconds(10);
+      while (cudaEventQuery(sh.ev1) == cudaErrorNotReady) {
+        const auto now = std::chrono::steady_clock::now();
+        if (now >= next) {
+          report_progress(sh);
+          next = now + std::chrono::milliseconds(10);
+        }
+        std::this_thread::yield();
+      }
     }
     cudaMemcpyAsync(&st[i], status, sizeof(dev::PullStatus), cudaMemcpyDeviceToHost, sh.stream);
     cudaError_t e = cudaStreamSynchronize(sh.stream);

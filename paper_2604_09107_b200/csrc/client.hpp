@@ -356,6 +356,8 @@ class Client {
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     std::chrono::steady_clock::time_point t_launch;  // host clock of the fill's launch
     cudaStream_t poll = nullptr;  // progress reads while a fill runs
+    std::vector<std::uint32_t> flag_host;  // report_progress: the fill's watermarks
+    std::uint64_t reported = 0;            // items last reported to the registry
     DevBuf span_tables;           // copy_spans' span tables (grow-only: no per-call malloc/free)
     DevBuf dig_tables, group_tables;  // publish: K6 span tables (grow-only)
     // Copy-engine landing from host memory (launch_fill): frames copied on
@@ -396,6 +398,9 @@ class Client {
   Status resolve_source(Shard& sh, const Assignment& a, VersionId v, SourceView* out,
                         double wait_s);
   Status launch_fill(Shard& sh, const SourceView& src, bool src_complete);
+  // task_progress (client_core.cpp:1414-1439): the verified item prefix of a
+  // running plain fill, read from its watermarks, to the registry.
+  void report_progress(Shard& sh);
   Status launch_host_dma(Shard& sh, const SourceView& src, std::uint32_t* epoch);
   Status run_replicate_loop(const OpOutcome& o, VersionId v);
 

@@ -131,6 +131,12 @@ class DistCluster:
             return lib.rs_server_failure_report(c, _b(o[1]), _b(o[2]), o[3], _b(o[4]), o[5])
         raise ValueError(kind)
 
+    def set_topology(self, endpoints, cost) -> None:
+        """Local, but every rank must call it with the same arguments (the
+        registry replicas must plan alike): rank 0's matrix is broadcast."""
+        endpoints, cost = self.gather((list(endpoints), [list(r) for r in cost]))[0]
+        self.local.set_topology(endpoints, cost)
+
     def result(self, model, replica):
         d, s, v, ch = C.c_int(), C.c_int(), C.c_uint64(), C.c_int()
         lib.rs_server_result(self.local.h, _b(model), _b(replica), C.byref(d), C.byref(s),

@@ -209,6 +209,12 @@ class Cluster:
         return {"kind": kind, "lifecycle": life.value.decode(), "version": v.value,
                 "serving": s.value, "visible": bool(vis.value)}
 
+    def progress(self, model: str, replica: str) -> int:
+        """The replica's verified items (min over shards), as its fills report."""
+        v = C.c_uint64()
+        check(lib.rs_cluster_progress(self.h, _b(model), _b(replica), C.byref(v)))
+        return v.value
+
     def listen(self, host: str = "127.0.0.1", port: int = 0) -> int:
         """Serve this process's serve states over TCP; returns the port.
         Sources whose endpoint is "tcp:<host>:<port>" are pulled through it."""
@@ -228,6 +234,16 @@ class Cluster:
         a = RsAssignment()
         check(lib.rs_locate(self.h, _b(model), _b(replica), _b(spec), shard, C.byref(a)), "rs_locate")
         return _assignment(a)
+
+    def set_topology(self, endpoints, cost) -> None:
+        """The planner's source cost between data endpoints:
+        cost[i][j] for a reader at endpoints[i] pulling from endpoints[j]
+        (see nvlink_cost_matrix).  [] clears it."""
+        n = len(endpoints)
+        eps = (C.c_char_p * max(n, 1))(*[_b(e) for e in endpoints])
+        flat = (C.c_int32 * max(n * n, 1))(*[int(cost[i][j]) for i in range(n) for j in range(n)])
+        check(lib.rs_cluster_set_topology(self.h, n, C.cast(eps, C.c_void_p), C.cast(flat, C.c_void_p)),
+              "rs_cluster_set_topology")
 
     def set_silent(self, model: str, replica: str, silent: bool = True):
         check(lib.rs_cluster_set_silent(self.h, _b(model), _b(replica), int(silent)))
@@ -451,6 +467,31 @@ class Handle:
 
     def serve_export(self, shard: int = 0) -> bytes:
         return _read_bytes(lib.rs_serve_export, self.h, shard)
+
+
+def nvlink_cost_matrix(n: int = None) -> list[list[int]]:
+    """The box's GPU-to-GPU topology measured through NVML: 0 for the same
+    GPU (local HBM), 1 for a pair joined by NVLink (directly or through
+    NVSwitch: every pair of a B200 HGX box), 2 for a pair that only reaches
+    over PCIe.  The planner prefers lower costs (Cluster.set_topology)."""
+    import pynvml as N
+    N.nvmlInit()
+    try:
+        count = N.nvmlDeviceGetCount() if n is None else n
+        hs = [N.nvmlDeviceGetHandleByIndex(i) for i in range(count)]
+        out = [[0] * count for _ in range(count)]
+        for i in range(count):
+            for j in range(count):
+                if i == j:
+                    continue
+                try:
+                    st = N.nvmlDeviceGetP2PStatus(hs[i], hs[j], N.NVML_P2P_CAPS_INDEX_NVLINK)
+                except N.NVMLError:
+                    st = None
+                out[i][j] = 1 if st == N.NVML_P2P_STATUS_OK else 2
+        return out
+    finally:
+        N.nvmlShutdown()
 
 
 def combine_layout_key(shard_hashes) -> str:

@@ -132,3 +132,48 @@ def test_aborted_upstream_is_not_serving(oracle):
         assert hs["A"].stats().checksum_failures >= 2  # first attempt + the quiet re-pull
     finally:
         cl.close()
+
+
+def test_registry_sees_item_progress_while_a_fill_lands(oracle):
+    """task_progress (client_core.cpp:1414-1439): a fill reports its
+    verified item prefix while it runs, so the registry's view of a
+    replicating replica advances before completion.  A fill capped to one SM
+    lands 16 x 64 MiB slowly enough to watch."""
+    from paper_2604_09107_b200.ros import Cluster, Status
+    cl = Cluster()
+    try:
+        dev = torch.device("cuda", 0)
+        n, size = 16, 64 << 20
+        t = cl.open("m", "T", 1)
+        a = cl.open("m", "A", 1, grid_sms=1)
+        keep = []
+        for i in range(n):
+            src = torch.empty(size, dtype=torch.uint8, device=dev)
+            from paper_2604_09107_b200 import ros
+            ros.synth_bf16(src, 50 + i)
+            dst = torch.zeros_like(src)
+            keep += [src, dst]
+            assert t.register_tensor(0, f"w{i}", src) == Status.ok
+            assert a.register_tensor(0, f"w{i}", dst) == Status.ok
+        assert t.publish(1).status == Status.ok
+        assert a.connect() == Status.ok
+        assert a.server_replicate("latest").status == Status.ok
+        assert a.transfer_bind(1) == Status.ok
+        assert cl.progress("m", "A") == 0
+        assert a.transfer_launch() == Status.ok
+        seen = set()
+        t0 = time.time()
+        while time.time() - t0 < 30:
+            done, nb = a.transfer_progress(0)  # reads the watermarks, reports the item prefix
+            seen.add(cl.progress("m", "A"))
+            if done == nb:
+                break
+        assert a.transfer_wait() == [(Status.ok, 0)]
+        mid = sorted(x for x in seen if 0 < x < n)
+        assert mid, sorted(seen)  # the view advanced while the fill ran
+        a.transfer_finish(1, True)
+        assert cl.view("m", "A")["lifecycle"] == "published"
+        for i in range(n):
+            assert torch.equal(keep[2 * i], keep[2 * i + 1])
+    finally:
+        cl.close()

@@ -308,3 +308,26 @@ def test_survey_abi_names_pull_serve_state(fx):
     assert d.value and f.value and ep.value > 0
     n_chunks = ((3 << 20) + 123 + 4095) // 4096
     assert nb.value == (n_chunks + 31) // 32
+
+
+def test_measured_topology_reaches_the_planner(fx):
+    """The box's NVLink state (NVML) as the planner's topology term: a
+    square matrix, 0 on the diagonal, 1 for NVLink/NVSwitch pairs; on such a
+    uniform box the chain plan is unchanged."""
+    from paper_2604_09107_b200 import ros
+    from paper_2604_09107_b200.ros import Status
+    m = ros.nvlink_cost_matrix()
+    n = len(m)
+    assert n == torch.cuda.device_count() and all(len(r) == n for r in m)
+    assert all(m[i][i] == 0 for i in range(n)) and all(x in (0, 1, 2) for r in m for x in r)
+    names = ["T", "r1", "r2"]
+    for i, r in enumerate(names):
+        fx.make(r, dev=i % n)
+        fx.h[r].set_endpoint(0, f"gpu{i % n}:{r}")
+        fx.reg(r, 0, "w", 1 << 20, 5 if i == 0 else 0)
+    fx.cl.set_topology([f"gpu{i % n}:{r}" for i, r in enumerate(names)],
+                       [[m[i % n][j % n] for j in range(3)] for i in range(3)])
+    assert fx.h["T"].publish(1).status == Status.ok
+    for r in names[1:]:
+        assert fx.h[r].replicate().status == Status.ok
+        assert fx.same("T", r, 0, "w")
