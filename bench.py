@@ -92,6 +92,61 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(sm), "source": "nvml"}
 
 
+class NvlinkCounters:
+    """NVLink bytes this GPU sent / received, from NVML's per-link counters
+    (NVML_FI_DEV_NVLINK_COUNT_XMIT_BYTES / _RCV_BYTES summed over the links;
+    the aggregate THROUGHPUT_RAW_TX/RX fields in KiB as a fallback).  Raw
+    link bytes: user data plus protocol, both directions of the port."""
+
+    def __init__(self, index: int):
+        self.err = None
+        try:
+            import pynvml as N
+            N.nvmlInit()
+            self.N = N
+            self.h = N.nvmlDeviceGetHandleByIndex(index)
+            self.links = [l for l in range(18) if self._up(l)]
+        except Exception as e:  # noqa: BLE001 - report, do not fail the bench
+            self.err = f"nvml unavailable: {e}"
+
+    def _up(self, link):
+        try:
+            return self.N.nvmlDeviceGetNvLinkState(self.h, link) == self.N.NVML_FEATURE_ENABLED
+        except Exception:  # noqa: BLE001
+            return False
+
+    def _fields(self, reqs):
+        vals = self.N.nvmlDeviceGetFieldValues(self.h, reqs)
+        out = []
+        for v in vals:
+            if v.nvmlReturn != 0:
+                return None
+            out.append(int(v.value.ullVal))
+        return out
+
+    def read(self):
+        """(tx_bytes, rx_bytes, source) or None."""
+        if self.err:
+            return None
+        N = self.N
+        try:
+            per = self._fields([(N.NVML_FI_DEV_NVLINK_COUNT_XMIT_BYTES, l) for l in self.links] +
+                               [(N.NVML_FI_DEV_NVLINK_COUNT_RCV_BYTES, l) for l in self.links])
+            if per is not None and self.links:
+                k = len(self.links)
+                return sum(per[:k]), sum(per[k:]), "nvml per-link XMIT/RCV bytes"
+        except Exception:  # noqa: BLE001
+            pass
+        try:
+            agg = self._fields([(N.NVML_FI_DEV_NVLINK_THROUGHPUT_RAW_TX, 0xFFFFFFFF),
+                                (N.NVML_FI_DEV_NVLINK_THROUGHPUT_RAW_RX, 0xFFFFFFFF)])
+            if agg is not None:
+                return agg[0] * 1024, agg[1] * 1024, "nvml THROUGHPUT_RAW (KiB)"
+        except Exception as e:  # noqa: BLE001
+            self.err = str(e)
+        return None
+
+
 # NVLink 5 user-data bounds for SM-driven pulls, from the ncu nvlrx/nvltx
 # counters of the pull kernel (profiles/r1/ncu_nvlink_counters.json): read
 # responses add 12.5% protocol bytes on the wire, read requests 18.75% of the

@@ -101,9 +101,11 @@ def run(args):
     hashes = dc.gather(None if args.no_verify else table_hash())
     verified = args.no_verify or all(x == hashes[0] for x in hashes)
     clk = B.ClockSampler(local)
+    nvc = B.NvlinkCounters(local)
     dist.barrier(group=dc.pg)
     torch.cuda.synchronize()
     clk.start()
+    link0 = nvc.read()
     walls, kms, landed = [], [], 0
     for _ in range(args.steps):
         w, k, b = step()
@@ -111,12 +113,13 @@ def run(args):
         kms.append(k)
         landed += b
     torch.cuda.synchronize()
+    link1 = nvc.read()
     clocks = clk.stop()
     # max over ranks of per-step device time; sum of landed bytes
     t = torch.tensor([max(kms) if kms else 0.0, sum(kms), float(landed), max(walls), sum(walls)],
                      dtype=torch.float64)
     allv = [None] * world
-    dist.all_gather_object(allv, (t.tolist(), kms, clocks), group=dc.pg)
+    dist.all_gather_object(allv, (t.tolist(), kms, clocks, link0, link1), group=dc.pg)
     step_dev_ms = [max(a[1][i] for a in allv) for i in range(args.steps)]
     total_landed = sum(a[0][2] for a in allv)
     dev_s = sum(step_dev_ms) / 1e3
@@ -126,6 +129,7 @@ def run(args):
     hashes = dc.gather(None if args.no_verify else table_hash())
     verified = verified and (args.no_verify or all(x == hashes[0] for x in hashes))
     host_e2e = None
+    plan = [f"{a.replica}<-{a.src}" for a in dc.assigns()][-receivers:]
     if not pairs and not getattr(args, "no_host_e2e", False):
         host_e2e = _dist_host_e2e(dc, h, reader, rank, dev, total, receivers, args)
     if rank == 0:
@@ -142,7 +146,7 @@ def run(args):
                        "placement": "trainer on GPU0, reader i on GPU i: chained fan-out over NVLink",
                        "bytes_per_receiver": total,
                        "receivers": receivers, "chunk_bytes": args.chunk,
-                       "plan": [f"{a.replica}<-{a.src}" for a in dc.assigns()][-receivers:],
+                       "plan": plan,
                        "l2": "inputs (16 GB/replica) >> 126 MB L2; no flush"},
             "per_receiver_gbs": per_rx,
             "weight_update_latency_s": round(wall_s / args.steps, 5),
@@ -174,6 +178,22 @@ def run(args):
             "clocks": allv[0][2] if allv[0][2].get("sm_mhz") else allv[1][2],
             "verified": verified,
         }
+        # NVML link counters over the timed steps: raw bytes (data + protocol)
+        # each GPU's port sent and received, per step, and as a rate over the
+        # steps' pull-kernel time against the 900 GB/s per direction
+        kern_s = sum(step_dev_ms) / 1e3
+        links = []
+        for r, a in enumerate(allv):
+            l0, l1 = a[3], a[4]
+            if not (l0 and l1):
+                links.append({"rank": r, "counters": None})
+                continue
+            tx, rx = (l1[0] - l0[0]) / args.steps, (l1[1] - l0[1]) / args.steps
+            links.append({"rank": r, "tx_gb_per_step": round(tx / 1e9, 3), "rx_gb_per_step": round(rx / 1e9, 3),
+                          "tx_frac_900": round(tx * args.steps / kern_s / 900e9, 4),
+                          "rx_frac_900": round(rx * args.steps / kern_s / 900e9, 4)})
+        line["nvlink_counters"] = {"per_rank": links, "source": next((a[4][2] for a in allv if a[4]), None),
+                                   "denominator": "sum of the steps' pull-kernel time (max over readers)"}
         if host_e2e is not None:
             line["e2e_device_resident"] = line["e2e"]
             line["e2e"] = host_e2e
