@@ -28,7 +28,12 @@
 #include <string>
 #include <vector>
 
+#include <future>
+
 #include "refstore/client_core.hpp"
+#include "refstore/digest.hpp"
+#include "refstore/manifest.hpp"
+#include "refstore/transport_stream.hpp"
 #include "refstore/server_core.hpp"
 #include "refstore/trace.hpp"
 #include "refstore/transport_mem.hpp"
@@ -244,6 +249,85 @@ void level_b_corrupt_source() {
   report(ok, "B", "corrupt_source_quiet_retry_report_repick", counters(s));
 }
 
+// ------------------------------------------------------------------ level C
+// The reference's own data-plane dialer (StreamData, transport_stream.cpp)
+// against the B200 process's TCP server, which answers the reference wire
+// (RSDP, transport_stream.hpp:36-76) from device-resident serve states.  The
+// reference decodes the B200 manifest and verifies every item it pulled with
+// its own digest64.
+void level_c_rsdp_reader() {
+  B200Cluster cl;
+  DevBufs tb;
+  B200Client t(cl, "m", "T", 2);
+  for (const auto& x : kT) t.register_tensor(x.shard, x.name, tb.make(x, x.salt));
+  std::optional<ClientCore::OpResult> pr;
+  t.publish(1, [&](ClientCore::OpResult r) { pr = r; });
+  int port = 0;
+  bool ok = pr && pr->status == Status::ok && rs_cluster_listen(cl.get(), "127.0.0.1", 0, &port) == 0;
+  const std::string ep = "127.0.0.1:" + std::to_string(port);
+  StreamData sd;
+  ThreadExecutor exec;
+  std::uint64_t items_verified = 0, bytes = 0;
+  for (std::uint32_t shard = 0; ok && shard < 2; ++shard) {
+    std::size_t n = 0;
+    rs_manifest(t.handle(), shard, nullptr, 0, &n);
+    std::string enc(n, '\0');
+    rs_manifest(t.handle(), shard, enc.data(), enc.size(), &n);
+    auto man = TensorManifest::decode(enc);  // the reference decoder
+    if (!man) {
+      ok = false;
+      break;
+    }
+    const auto& items = man->items();
+    std::uint64_t total = 0;
+    for (const auto& it : items) total += it.length;
+    // long-poll query: the version is complete, every item readable
+    QuerySpec q{"m", "T", 1, shard, items.size()};
+    std::promise<QueryResult> qp;
+    sd.async_query(ep, q, &exec, [&](QueryResult r) { qp.set_value(r); });
+    const QueryResult qr = qp.get_future().get();
+    ok &= qr.status == Status::ok && qr.progress == items.size() && qr.complete;
+    // pull the whole item stream (responses may be short: loop)
+    std::vector<std::byte> stream(total);
+    for (std::uint64_t off = 0; ok && off < total;) {
+      PullSpec ps;
+      ps.model = "m";
+      ps.replica = "T";
+      ps.version = 1;
+      ps.shard = shard;
+      ps.offset = off;
+      ps.max_bytes = total - off;
+      std::promise<PullResult> pp;
+      sd.async_pull(ep, ps, PullDest{{stream.data() + off, total - off}}, &exec,
+                    [&](PullResult r) { pp.set_value(r); });
+      const PullResult r = pp.get_future().get();
+      ok &= r.status == Status::ok && r.bytes > 0 && r.source_complete;
+      off += r.bytes;
+      bytes += r.bytes;
+    }
+    // digest64 of every item against the manifest (TransferTask::verify_ready)
+    std::uint64_t at = 0;
+    for (const auto& it : items) {
+      ok &= digest64(stream.data() + at, it.length) == it.digest;
+      at += it.length;
+      ++items_verified;
+    }
+    // a wrong version is refused (compute_slice: not_serving)
+    PullSpec bad;
+    bad.model = "m";
+    bad.replica = "T";
+    bad.version = 2;
+    bad.shard = shard;
+    bad.max_bytes = 16;
+    std::byte tmp[16];
+    std::promise<PullResult> bp;
+    sd.async_pull(ep, bad, PullDest{{tmp, 16}}, &exec, [&](PullResult r) { bp.set_value(r); });
+    ok &= bp.get_future().get().status == Status::not_serving;
+  }
+  report(ok, "C", "rsdp_reference_reader_pulls_and_verifies",
+         "items_verified=" + std::to_string(items_verified) + " bytes_pulled=" + std::to_string(bytes));
+}
+
 }  // namespace
 
 int main(int argc, char** argv) {
@@ -251,6 +335,7 @@ int main(int argc, char** argv) {
       {"A replicate_pulls_bytes_that_verify", level_a_replicate},
       {"B replicate_pulls_bytes_that_verify", level_b_replicate},
       {"B corrupt_source_quiet_retry_report_repick", level_b_corrupt_source},
+      {"C rsdp_reference_reader_pulls_and_verifies", level_c_rsdp_reader},
   };
   if (argc > 1 && std::strcmp(argv[1], "--list") == 0) {
     for (const auto& [name, fn] : scenarios) std::printf("%s\n", name);

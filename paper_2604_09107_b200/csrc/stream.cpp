@@ -233,8 +233,13 @@ void StreamServer::serve_conn(int fd) {
   };
   std::uint32_t magic = 0, klen = 0, stripe = 0, stripes = 1;
   VersionId version = 0;
-  if (!recv_pod(fd, &magic) || magic != kReqMagic || !recv_pod(fd, &klen) || klen > 4096)
-    return (void)::close(fd);
+  if (!recv_pod(fd, &magic)) return (void)::close(fd);
+  if (magic == 0x50445352u) {  // "RSDP": a reference StreamData peer (rsdp.cpp)
+    std::uint8_t first4[4];
+    std::memcpy(first4, &magic, 4);
+    return serve_rsdp(fd, serves_, first4);
+  }
+  if (magic != kReqMagic || !recv_pod(fd, &klen) || klen > 4096) return (void)::close(fd);
   std::string key(klen, '\0');
   if (!recv_all(fd, key.data(), klen) || !recv_pod(fd, &version) || !recv_pod(fd, &stripe) ||
       !recv_pod(fd, &stripes) || stripes == 0 || stripe >= stripes)

@@ -27,6 +27,11 @@
 
 namespace rsb {
 
+// rsdp.cpp: serves one connection speaking the reference's data wire (RSDP,
+// transport_stream.hpp:36-76) from this process's serve states; `first4`
+// are the header bytes the caller already read.  Closes fd.
+void serve_rsdp(int fd, ServeRegistry* serves, const std::uint8_t first4[4]);
+
 class StreamServer {
  public:
   explicit StreamServer(ServeRegistry* serves);

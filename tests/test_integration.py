@@ -6,7 +6,9 @@ B200Transport as the reference's DataTransport) against the UNMODIFIED
 reference headers and links them with the reference library built from its
 own sources (oracle/_ref) and libros_b200.so.  It then runs the reference's
 client scenarios (tests/unit/test_client_core.cpp:163-202 and :346-377) on
-the GPU and checks the reference's own counters: items_verified == 3,
+the GPU and checks the reference's own counters; level C points the
+reference's own data-plane dialer (StreamData) at the B200 process's TCP
+server, which answers the reference wire (RSDP): items_verified == 3,
 bytes_pulled exact, checksum_failures == 0 (2 + one report for the corrupt
 source), bytes identical.
 
@@ -21,7 +23,7 @@ from tests.conftest import ROOT
 
 BIN = os.path.join(ROOT, "integration", "_build", "ref_scenarios")
 SCENARIOS = ["A replicate_pulls_bytes_that_verify", "B replicate_pulls_bytes_that_verify",
-             "B corrupt_source_quiet_retry_report_repick"]
+             "B corrupt_source_quiet_retry_report_repick", "C rsdp_reference_reader_pulls_and_verifies"]
 
 
 def _binary():
@@ -36,7 +38,7 @@ def _binary():
 def test_reference_side_adapters_build_and_list():
     r = subprocess.run([_binary(), "--list"], capture_output=True, text=True, timeout=60)
     assert r.returncode == 0, r.stderr
-    assert r.stdout.split("\n")[:3] == SCENARIOS
+    assert r.stdout.split("\n")[:4] == SCENARIOS
 
 
 @pytest.mark.gpu
@@ -56,3 +58,6 @@ def test_reference_scenarios_through_the_b200_path():
     assert int(kv[SCENARIOS[1]]["device_pulls"]) > 0
     assert int(kv[SCENARIOS[1]]["device_bytes"]) == 3 << 20  # the big item, moved by the kernel
     assert kv[SCENARIOS[2]]["checksum_failures"] == "2" and kv[SCENARIOS[2]]["failure_reports"] == "1"
+    # the reference's StreamData over the B200 server's RSDP: 3 items verified
+    assert kv[SCENARIOS[3]]["items_verified"] == "3"
+    assert kv[SCENARIOS[3]]["bytes_pulled"] == str((3 << 20) + 1000 + 2000 + 4096)

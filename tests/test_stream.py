@@ -215,3 +215,56 @@ def test_hostile_tcp_source_is_rejected(case):
             assert int(rb.sum()) == 0  # nothing landed from the hostile peer
     finally:
         stop.set()
+
+
+def test_reference_wire_frozen_request_is_served():
+    """The B200 TCP server answers the reference data wire (RSDP,
+    transport_stream.hpp:36-76).  The request is the reference's frozen
+    byte vector (test_transport.cpp:91-131: header "RSDP" v1 pull_req, body
+    model "m", replica "R", version 7, shard 2, offset 4096, max_bytes
+    8 MiB); the response is parsed by the same layout and must carry the
+    stream bytes [4096, 4096 + 8 MiB) of replica R's shard 2."""
+    import socket
+    import struct
+    dev = torch.device("cuda:0")
+    with Cluster() as cl:
+        port = cl.listen()
+        h = cl.open("m", "R", 3, tiny_threshold=1 << 20)
+        bufs = []
+        for s in range(3):
+            b = torch.zeros(16 << 20, dtype=torch.uint8, device=dev)
+            from paper_2604_09107_b200 import ros
+            ros.synth_bf16(b, 70 + s)
+            bufs.append(b)
+            assert h.register_tensor(s, f"w{s}", b) == Status.ok
+        assert h.publish(7).status == Status.ok
+        req = bytes.fromhex("525344500001" "0001" "0000000000000036"
+                            "0102" "00000001" "6d" "0202" "00000001" "52"
+                            "0301" "0000000000000007" "0401" "0000000000000002"
+                            "0501" "0000000000001000" "0601" "0000000000800000")
+        c = socket.create_connection(("127.0.0.1", port))
+        c.sendall(req)
+
+        def recv_n(n):
+            out = b""
+            while len(out) < n:
+                k = c.recv(n - len(out))
+                assert k, "connection closed"
+                out += k
+            return out
+
+        magic, ver, kind, blen = struct.unpack(">IHHQ", recv_n(16))
+        assert (magic, ver, kind) == (0x52534450, 1, 2) and blen == 18 + (8 << 20)
+        st, prog, comp, plen = struct.unpack(">BQBQ", recv_n(18))
+        assert (st, prog, comp, plen) == (0, 1, 1, 8 << 20)
+        payload = recv_n(plen)
+        assert payload == bufs[2][4096:4096 + (8 << 20)].cpu().numpy().tobytes()
+        # query_req (test_transport.cpp:146-168 layout): min_items 1 -> complete
+        body = (b"\x01\x02" + struct.pack(">I", 1) + b"m" + b"\x02\x02" + struct.pack(">I", 1) + b"R" +
+                b"\x03\x01" + struct.pack(">Q", 7) + b"\x04\x01" + struct.pack(">Q", 2) +
+                b"\x05\x01" + struct.pack(">Q", 1))
+        c.sendall(struct.pack(">IHHQ", 0x52534450, 1, 3, len(body)) + body)
+        magic, ver, kind, blen = struct.unpack(">IHHQ", recv_n(16))
+        assert (kind, blen) == (4, 10)
+        assert struct.unpack(">BQB", recv_n(10)) == (0, 1, 1)
+        c.close()
