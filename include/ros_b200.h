@@ -288,6 +288,28 @@ int rs_cluster_kind(rs_cluster* c, const char* model, const char* replica, char*
  * kernel lands and verifies them, chasing per-batch host watermarks. */
 int rs_cluster_listen(rs_cluster* c, const char* host, int port, int* bound_port);
 
+/* ---- dynamic membership: the registry's sequenced operation log -----------
+ * (the reference's one metadata server that clients dial at
+ * any time, StreamServerHost / StreamControl, transport_stream.cpp:582-797.)
+ * Every process keeps a registry replica (rs_cluster) and applies one totally
+ * ordered log of registry operations; the log server orders them.  A process
+ * that starts late replays the log from entry 0 and joins with the same
+ * registry state as the others (paper_2604_09107_b200/shared.py drives it). */
+typedef struct rs_oplog_server rs_oplog_server;
+typedef struct rs_oplog rs_oplog;
+int rs_oplog_serve(const char* host, int port, int* bound_port, rs_oplog_server** out);
+void rs_oplog_server_stop(rs_oplog_server* s);
+uint64_t rs_oplog_server_size(rs_oplog_server* s);
+int rs_oplog_connect(const char* host, int port, double timeout_s, rs_oplog** out);
+/* Appends one entry (opaque bytes); *seq is its position in the log. */
+int rs_oplog_append(rs_oplog* l, const void* entry, size_t len, uint64_t* seq);
+/* Fetches up to max_entries entries from position `from` (long-polls up to
+ * wait_ms when none exist yet); read them with rs_oplog_entry, valid until the
+ * next fetch on this connection. */
+int rs_oplog_fetch(rs_oplog* l, uint64_t from, int wait_ms, uint32_t max_entries, uint64_t* count);
+int rs_oplog_entry(rs_oplog* l, uint64_t i, const void** data, size_t* len);
+void rs_oplog_close(rs_oplog* l);
+
 /* ---- device primitives (kernel boundary) --------------------------------- */
 /* digest64 (digest.cpp:79-106) of n device spans; out is host memory. */
 int rs_digest_spans(const uint64_t* dev_ptrs, const uint64_t* lens, int n, uint64_t* out,

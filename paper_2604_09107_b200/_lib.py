@@ -121,6 +121,14 @@ _SIGS = {
     "rs_transfer_finish": (i32, [vp, u64, i32]),
     "rs_serve_export": (i32, [vp, u32, vp, sz, C.POINTER(sz)]),
     "rs_serve_import": (i32, [vp, vp, sz]),
+    "rs_oplog_serve": (i32, [cstr, i32, C.POINTER(i32), C.POINTER(vp)]),
+    "rs_oplog_server_stop": (None, [vp]),
+    "rs_oplog_server_size": (u64, [vp]),
+    "rs_oplog_connect": (i32, [cstr, i32, dbl, C.POINTER(vp)]),
+    "rs_oplog_append": (i32, [vp, vp, sz, C.POINTER(u64)]),
+    "rs_oplog_fetch": (i32, [vp, u64, i32, u32, C.POINTER(u64)]),
+    "rs_oplog_entry": (i32, [vp, u64, C.POINTER(vp), C.POINTER(sz)]),
+    "rs_oplog_close": (None, [vp]),
     "rs_digest_spans": (i32, [vp, vp, i32, vp, i32]),
     "rs_synth_bf16": (i32, [vp, u64, u64, u64, vp]),
     "rs_bf16_to_e4m3": (i32, [vp, vp, u64, vp]),

@@ -36,6 +36,59 @@ def _blob_arrays(blobs):
     return C.cast(arr, C.c_void_p), C.cast(lens, C.c_void_p), arr, lens
 
 
+def apply_op(c, o) -> int:
+    """Applies one registry operation (see DistCluster.server_ops) to the
+    registry replica `c` (an rs_cluster handle); returns its status code."""
+    kind = o[0]
+    if kind == "open":
+        _, m, r, n, dc, eps = o[:6]
+        key = o[6] if len(o) > 6 else ""
+        dman = o[7] if len(o) > 7 else []
+        dlay = o[8] if len(o) > 8 else []
+        arr = (C.c_char_p * n)(*[_b(e) for e in eps])
+        if dman:
+            pm, pl, _k1, _k2 = _blob_arrays(dman)
+            qm, ql, _k3, _k4 = _blob_arrays(dlay)
+        else:
+            pm = pl = qm = ql = None
+        return lib.rs_server_open(c, _b(m), _b(r), n, _b(dc), C.cast(arr, C.c_void_p), _b(key),
+                                  pm, pl, qm, ql)
+    if kind == "publish":
+        _, m, r, v, mans = o[:5]
+        lays = o[5] if len(o) > 5 else []
+        pm, pl, _k1, _k2 = _blob_arrays(mans)
+        if lays:
+            qm, ql, _k3, _k4 = _blob_arrays(lays)
+        else:
+            qm = ql = None
+        return lib.rs_server_publish(c, _b(m), _b(r), v, len(mans), pm, pl, qm, ql)
+    if kind == "add_layout":
+        _, m, v, key, mans, lays = o
+        pm, pl, _k1, _k2 = _blob_arrays(mans)
+        qm, ql, _k3, _k4 = _blob_arrays(lays)
+        return lib.rs_server_add_layout(c, _b(m), v, _b(key), len(mans), pm, pl, qm, ql)
+    if kind == "unpublish":
+        return lib.rs_server_unpublish(c, _b(o[1]), _b(o[2]))
+    if kind == "retain":
+        _, m, r, lags = o
+        arr = (C.c_uint64 * max(len(lags), 1))(*lags)
+        return lib.rs_server_set_retention(c, _b(m), _b(r), C.cast(arr, C.c_void_p), len(lags))
+    if kind == "offload_confirm":
+        _, m, r, shard, v, ok, ep = o
+        return lib.rs_server_offload_confirm(c, _b(m), _b(r), shard, v, int(ok), _b(ep))
+    if kind == "replicate":
+        return lib.rs_server_replicate(c, _b(o[1]), _b(o[2]), _b(o[3]))
+    if kind == "update":
+        _, m, r, sp, cur = o
+        return lib.rs_server_update(c, _b(m), _b(r), _b(sp), int(cur is not None), cur or 0)
+    if kind == "complete":
+        return lib.rs_server_complete(c, _b(o[1]), _b(o[2]), o[3], o[4])
+    if kind == "report":
+        return lib.rs_server_failure_report(c, _b(o[1]), _b(o[2]), o[3], _b(o[4]), o[5])
+    if kind == "close":
+        return lib.rs_server_close(c, _b(o[1]), _b(o[2]))
+    raise ValueError(kind)
+
 class DistCluster:
     def __init__(self, group=None, pipeline: bool = True, smart_skipping: bool = True):
         import torch.distributed as dist
@@ -82,54 +135,7 @@ class DistCluster:
         return out
 
     def _apply(self, o) -> int:
-        c = self.local.h
-        kind = o[0]
-        if kind == "open":
-            _, m, r, n, dc, eps = o[:6]
-            key = o[6] if len(o) > 6 else ""
-            dman = o[7] if len(o) > 7 else []
-            dlay = o[8] if len(o) > 8 else []
-            arr = (C.c_char_p * n)(*[_b(e) for e in eps])
-            if dman:
-                pm, pl, _k1, _k2 = _blob_arrays(dman)
-                qm, ql, _k3, _k4 = _blob_arrays(dlay)
-            else:
-                pm = pl = qm = ql = None
-            return lib.rs_server_open(c, _b(m), _b(r), n, _b(dc), C.cast(arr, C.c_void_p), _b(key),
-                                      pm, pl, qm, ql)
-        if kind == "publish":
-            _, m, r, v, mans = o[:5]
-            lays = o[5] if len(o) > 5 else []
-            pm, pl, _k1, _k2 = _blob_arrays(mans)
-            if lays:
-                qm, ql, _k3, _k4 = _blob_arrays(lays)
-            else:
-                qm = ql = None
-            return lib.rs_server_publish(c, _b(m), _b(r), v, len(mans), pm, pl, qm, ql)
-        if kind == "add_layout":
-            _, m, v, key, mans, lays = o
-            pm, pl, _k1, _k2 = _blob_arrays(mans)
-            qm, ql, _k3, _k4 = _blob_arrays(lays)
-            return lib.rs_server_add_layout(c, _b(m), v, _b(key), len(mans), pm, pl, qm, ql)
-        if kind == "unpublish":
-            return lib.rs_server_unpublish(c, _b(o[1]), _b(o[2]))
-        if kind == "retain":
-            _, m, r, lags = o
-            arr = (C.c_uint64 * max(len(lags), 1))(*lags)
-            return lib.rs_server_set_retention(c, _b(m), _b(r), C.cast(arr, C.c_void_p), len(lags))
-        if kind == "offload_confirm":
-            _, m, r, shard, v, ok, ep = o
-            return lib.rs_server_offload_confirm(c, _b(m), _b(r), shard, v, int(ok), _b(ep))
-        if kind == "replicate":
-            return lib.rs_server_replicate(c, _b(o[1]), _b(o[2]), _b(o[3]))
-        if kind == "update":
-            _, m, r, sp, cur = o
-            return lib.rs_server_update(c, _b(m), _b(r), _b(sp), int(cur is not None), cur or 0)
-        if kind == "complete":
-            return lib.rs_server_complete(c, _b(o[1]), _b(o[2]), o[3], o[4])
-        if kind == "report":
-            return lib.rs_server_failure_report(c, _b(o[1]), _b(o[2]), o[3], _b(o[4]), o[5])
-        raise ValueError(kind)
+        return apply_op(self.local.h, o)
 
     def set_topology(self, endpoints, cost) -> None:
         """Local, but every rank must call it with the same arguments (the

@@ -1,0 +1,150 @@
+"""GPU: a reader PROCESS that did not exist when the others started joins
+through the registry's operation log and chases a copy that is still filling
+(config 4's elastic join with dynamic membership; shared.py, oplog.cpp).
+
+  process 0   hosts the log; trainer T publishes 1 GiB + tiny tensors; reader
+              A is planned and bound (serving its empty fill) but not filling
+  process 1   joins only now: replays the log, opens reader B, replicates ->
+              planned onto A (a pipeline copy, source_complete == 0), imports
+              A's serve state (CUDA IPC) from the log, launches and waits on
+              A's watermarks; process 0 then fills A and B chases it.
+
+No gloo group, no collective: process 1 is not known to anyone until it
+appends its first entry.  With one GPU both processes share cuda:0."""
+import os
+
+import pytest
+
+from tests.conftest import ROOT
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+SIZES = [1 << 30, 6000, 3 << 20]
+
+
+def _bufs(dev, seed=None):
+    from paper_2604_09107_b200 import ros
+    out = []
+    for i, n in enumerate(SIZES):
+        b = torch.zeros(n, dtype=torch.uint8, device=dev)
+        if seed is not None:
+            ros.synth_bf16(b, seed + i)
+        out.append(b)
+    return out
+
+
+def _host(q, joined, done):
+    import sys
+    sys.path.insert(0, ROOT)
+    import torch
+
+    from paper_2604_09107_b200 import ros
+    from paper_2604_09107_b200.ros import Status
+    from paper_2604_09107_b200.shared import LogServer, SharedCluster
+    try:
+        dev = torch.device("cuda", 0)
+        log = LogServer()
+        sc = SharedCluster("127.0.0.1", log.port)
+        t = sc.create("m", "T", 1, tiny_threshold=1 << 20)
+        tb = _bufs(dev, seed=800)
+        for i, b in enumerate(tb):
+            assert t.register_tensor(0, f"w{i}", b) == Status.ok
+        a = sc.create("m", "A", 1, tiny_threshold=1 << 20, pull_timeout_s=30.0)
+        ab = _bufs(dev)
+        for i, b in enumerate(ab):
+            assert a.register_tensor(0, f"w{i}", b) == Status.ok
+        torch.cuda.synchronize()
+        sc.open(t)
+        sc.open(a)
+        assert sc.publish(t, 1).status == Status.ok
+        assert sc.replicate_start(a) is None  # bound and serving, nothing landed
+        q.put(("host", "port", {"port": log.port}))
+        # the joiner is planned onto A while A has not started filling
+        import time
+        t0 = time.time()
+        while time.time() - t0 < 120:
+            v = sc.local.view("m", "B")
+            if v and v["lifecycle"] == "replicating":
+                break
+            time.sleep(0.01)
+        time.sleep(0.5)  # B binds, imports A's serve state and launches its chase
+        res = {"a": sc.replicate_finish(a)}
+        joined.wait(120)
+        want = ros.digest_spans([b.data_ptr() for b in tb], SIZES, 0)
+        got_a = ros.digest_spans([b.data_ptr() for b in ab], SIZES, 0)
+        sc.sync()
+        q.put(("host", "final", {"a": int(res["a"].status), "a_equal": got_a == want, "want": want,
+                                 "assigns": [(x.replica, x.src) for x in sc.assigns()],
+                                 "listing": {v: sorted(r) for v, r in sc.listing("m").items()}}))
+        done.wait(120)
+        sc.close()
+        log.close()
+    except Exception as e:  # pragma: no cover - surfaced by the parent
+        import traceback
+        q.put(("host", "error", repr(e) + traceback.format_exc()))
+
+
+def _joiner(port, q, joined):
+    import sys
+    sys.path.insert(0, ROOT)
+    import torch
+
+    from paper_2604_09107_b200 import ros
+    from paper_2604_09107_b200.ros import Status
+    from paper_2604_09107_b200.shared import SharedCluster
+    try:
+        dev = torch.device("cuda", torch.cuda.device_count() - 1)
+        sc = SharedCluster("127.0.0.1", port)
+        b = sc.create("m", "B", 1, tiny_threshold=1 << 20, pull_timeout_s=30.0)
+        bb = _bufs(dev)
+        for i, x in enumerate(bb):
+            assert b.register_tensor(0, f"w{i}", x) == Status.ok
+        sc.open(b)
+        r = sc.replicate(b)
+        a = b.transfer_assignment(0)
+        got = ros.digest_spans([x.data_ptr() for x in bb], SIZES, dev.index)
+        q.put(("joiner", "final", {"b": int(r.status), "v": r.version, "assignment": a, "digests": got}))
+        joined.set()
+        sc.close()
+    except Exception as e:  # pragma: no cover - surfaced by the parent
+        import traceback
+        q.put(("joiner", "error", repr(e) + traceback.format_exc()))
+        joined.set()
+
+
+def test_reader_process_joins_mid_fill_through_the_op_log():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    joined, done = ctx.Event(), ctx.Event()
+    host = ctx.Process(target=_host, args=(q, joined, done))
+    host.start()
+    procs = [host]
+    try:
+        who, what, info = q.get(timeout=300)
+        assert what == "port", info
+        j = ctx.Process(target=_joiner, args=(info["port"], q, joined))
+        j.start()
+        procs.append(j)
+        res = {}
+        for _ in range(2):
+            who, what, r = q.get(timeout=300)
+            assert what == "final", r
+            res[who] = r
+        assert res["host"]["a"] == 0 and res["host"]["a_equal"]
+        jb = res["joiner"]
+        assert jb["b"] == 0 and jb["v"] == 1, jb
+        assert jb["assignment"]["source_replica"] == "A", jb
+        assert jb["assignment"]["source_complete"] is False, jb  # chased a filling copy
+        assert jb["digests"] == res["host"]["want"]
+        assert ("A", "T") in res["host"]["assigns"] and ("B", "A") in res["host"]["assigns"]
+        assert res["host"]["listing"] == {1: ["A", "B", "T"]}
+    finally:
+        done.set()
+        joined.set()
+        for p in procs:
+            p.join(timeout=60)
