@@ -45,6 +45,12 @@ typedef struct {
                             * Fills whose caps sum to <= the SM count co-reside on one
                             * GPU, so a reader may chase an upstream filling on its own
                             * GPU instead of waiting for it to complete.              */
+  int early_publish;       /* 1: rs_publish commits the chunk-digest table and the
+                            * manifest structure at once and the big-entry XXH64
+                            * digests when their serial chains finish (background);
+                            * readers pull meanwhile.  The committed manifest is the
+                            * reference's, byte for byte (rs_publish_finalize waits
+                            * for it).  Default 0: the reference order.            */
 } rs_config;
 
 /* Assignment (reference messages.hpp:40-52) minus the manifest bytes, which
@@ -174,6 +180,12 @@ int rs_release(rs_handle* h, uint64_t version);
 int rs_serve_state(rs_handle* h, uint32_t shard, uint64_t** digests, uint32_t** watermarks,
                    uint32_t* epoch, uint32_t* n_batches);
 int rs_close(rs_handle* h);                                  /* close(); frees h */
+/* Early publish (rs_config.early_publish): 1 while the handle's last publish
+ * still digests its big entries; rs_publish_finalize waits for them and
+ * commits the final manifests (to the in-process registry when this handle
+ * holds every shard; rs_manifest then returns the final bytes). */
+int rs_publish_pending(rs_handle* h);
+int rs_publish_finalize(rs_handle* h, double wait_s);
 /* Plan view without side effects: the source `replica` would pull `shard`
  * of `spec` from right now. */
 int rs_locate(rs_cluster* c, const char* model, const char* replica, const char* spec,
@@ -184,6 +196,11 @@ int rs_stats_get(rs_handle* h, rs_stats* out);
 /* Canonical manifest bytes of the shard's held version
  * (TensorManifest::encode, manifest.cpp:103-139). */
 int rs_manifest(rs_handle* h, uint32_t shard, char* buf, size_t cap, size_t* len);
+/* The manifest bytes the shard holds right now, without waiting: during an
+ * early publish (rs_publish_pending) its provisional bytes, big-entry digests
+ * 0 -- what a split-phase caller registers with rs_server_publish_provisional.
+ * rs_manifest returns the final bytes, waiting for them if needed. */
+int rs_manifest_now(rs_handle* h, uint32_t shard, char* buf, size_t cap, size_t* len);
 /* The shard's per-chunk XXH64 table (device path integrity metadata). */
 int rs_chunk_digests(rs_handle* h, uint32_t shard, uint64_t* out, size_t cap, size_t* n);
 /* The shard's layout blob (entry geometries + per-item chunk lengths). */
@@ -210,6 +227,14 @@ int rs_server_publish(rs_cluster* c, const char* model, const char* replica, uin
 int rs_server_add_layout(rs_cluster* c, const char* model, uint64_t version, const char* layout_key,
                          uint32_t num_shards, const char* const* manifests, const size_t* lens,
                          const char* const* layouts, const size_t* layout_lens);
+/* rs_server_publish of an early publish's provisional manifests, and the
+ * later commit of their final bytes (same structure, digests filled). */
+int rs_server_publish_provisional(rs_cluster* c, const char* model, const char* replica,
+                                  uint64_t version, uint32_t num_shards,
+                                  const char* const* manifests, const size_t* lens,
+                                  const char* const* layouts, const size_t* layout_lens);
+int rs_server_finalize(rs_cluster* c, const char* model, const char* replica, uint64_t version,
+                       uint32_t num_shards, const char* const* manifests, const size_t* lens);
 int rs_server_unpublish(rs_cluster* c, const char* model, const char* replica);
 int rs_server_replicate(rs_cluster* c, const char* model, const char* replica, const char* spec);
 int rs_server_update(rs_cluster* c, const char* model, const char* replica, const char* spec,

@@ -26,7 +26,7 @@ class RsConfig(C.Structure):
     _fields_ = [("chunk_bytes", u64), ("tiny_threshold", u64), ("group_target", u64),
                 ("pipeline", i32), ("checksum_retries", i32), ("pull_timeout_s", dbl),
                 ("datacenter", C.c_char * 32), ("reshard_align", u32),
-                ("grid_sms", u32)]
+                ("grid_sms", u32), ("early_publish", i32)]
 
 
 class RsAssignment(C.Structure):
@@ -100,6 +100,7 @@ _SIGS = {
     "rs_is_published": (i32, [vp]),
     "rs_stats_get": (i32, [vp, C.POINTER(RsStats)]),
     "rs_manifest": (i32, [vp, u32, vp, sz, C.POINTER(sz)]),
+    "rs_manifest_now": (i32, [vp, u32, vp, sz, C.POINTER(sz)]),
     "rs_chunk_digests": (i32, [vp, u32, vp, sz, C.POINTER(sz)]),
     "rs_invalidate": (i32, [vp]),
     "rs_server_open": (i32, [vp, cstr, cstr, u32, cstr, vp, cstr, vp, vp, vp, vp]),
@@ -107,6 +108,10 @@ _SIGS = {
     "rs_server_publish": (i32, [vp, cstr, cstr, u64, u32, vp, vp, vp, vp]),
     "rs_server_add_layout": (i32, [vp, cstr, u64, cstr, u32, vp, vp, vp, vp]),
     "rs_server_unpublish": (i32, [vp, cstr, cstr]),
+    "rs_server_publish_provisional": (i32, [vp, cstr, cstr, u64, u32, vp, vp, vp, vp]),
+    "rs_server_finalize": (i32, [vp, cstr, cstr, u64, u32, vp, vp]),
+    "rs_publish_pending": (i32, [vp]),
+    "rs_publish_finalize": (i32, [vp, dbl]),
     "rs_server_replicate": (i32, [vp, cstr, cstr, cstr]),
     "rs_server_update": (i32, [vp, cstr, cstr, cstr, i32, u64]),
     "rs_server_result": (i32, [vp, cstr, cstr, C.POINTER(i32), C.POINTER(i32), C.POINTER(u64),

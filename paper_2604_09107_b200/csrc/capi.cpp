@@ -62,6 +62,7 @@ rsb::ClientConfig to_cfg(const rs_config* c) {
   if (c->datacenter[0]) cfg.dc = std::string(c->datacenter, strnlen(c->datacenter, 32));
   if (c->reshard_align) cfg.reshard_align = c->reshard_align;
   cfg.grid_sms = c->grid_sms;
+  cfg.early_publish = c->early_publish != 0;
   return cfg;
 }
 
@@ -112,6 +113,7 @@ void rs_config_default(rs_config* cfg) {
   std::strncpy(cfg->datacenter, d.dc.c_str(), sizeof(cfg->datacenter) - 1);
   cfg->reshard_align = d.reshard_align;
   cfg->grid_sms = d.grid_sms;
+  cfg->early_publish = d.early_publish ? 1 : 0;
 }
 
 int rs_cluster_create(int pipeline, int smart_skipping, rs_cluster** out) {
@@ -274,6 +276,13 @@ int rs_set_stream(rs_handle* h, uint32_t shard, void* cuda_stream) {
   return 0;
 }
 
+int rs_publish_pending(rs_handle* h) { return h && h->client->publish_pending() ? 1 : 0; }
+
+int rs_publish_finalize(rs_handle* h, double wait_s) {
+  if (!h) return st(rsb::Status::invalid_argument);
+  return st(h->client->finalize_publish(wait_s));
+}
+
 int rs_publish(rs_handle* h, uint64_t version) {
   if (!h) return st(rsb::Status::invalid_argument);
   return st(h->client->publish(version));
@@ -396,6 +405,13 @@ int rs_stats_get(rs_handle* h, rs_stats* out) {
   return 0;
 }
 
+int rs_manifest_now(rs_handle* h, uint32_t shard, char* buf, size_t cap, size_t* len) {
+  if (!h) return st(rsb::Status::invalid_argument);
+  auto m = h->client->held_manifest(shard);
+  if (!m) return st(m.status());
+  return put_bytes(*m, buf, cap, len);
+}
+
 int rs_manifest(rs_handle* h, uint32_t shard, char* buf, size_t cap, size_t* len) {
   if (!h) return st(rsb::Status::invalid_argument);
   auto m = h->client->manifest_bytes(shard);
@@ -463,6 +479,23 @@ int rs_server_publish(rs_cluster* c, const char* model, const char* replica, uin
   auto s = c->reg.publish(model, replica, version, blobs(num_shards, manifests, lens), &o,
                           blobs(num_shards, layouts, layout_lens));
   return st(rsb::ok(s) ? o.status : s);
+}
+
+int rs_server_publish_provisional(rs_cluster* c, const char* model, const char* replica,
+                                  uint64_t version, uint32_t num_shards,
+                                  const char* const* manifests, const size_t* lens,
+                                  const char* const* layouts, const size_t* layout_lens) {
+  if (!c || !model || !replica || !manifests || !lens) return st(rsb::Status::invalid_argument);
+  rsb::OpOutcome o;
+  auto s = c->reg.publish(model, replica, version, blobs(num_shards, manifests, lens), &o,
+                          blobs(num_shards, layouts, layout_lens), true);
+  return st(rsb::ok(s) ? o.status : s);
+}
+
+int rs_server_finalize(rs_cluster* c, const char* model, const char* replica, uint64_t version,
+                       uint32_t num_shards, const char* const* manifests, const size_t* lens) {
+  if (!c || !model || !replica || !manifests || !lens) return st(rsb::Status::invalid_argument);
+  return st(c->reg.finalize_manifests(model, replica, version, blobs(num_shards, manifests, lens)));
 }
 
 int rs_server_add_layout(rs_cluster* c, const char* model, uint64_t version, const char* layout_key,

@@ -583,6 +583,7 @@ Client::Client(Registry* reg, ServeRegistry* serves, std::string model, std::str
 }
 
 Client::~Client() {
+  if (fin_thread_.joinable()) fin_thread_.join();
   stop_serving();
   for (auto& sh : shards_) {
     if (sh.device < 0) continue;
@@ -591,6 +592,7 @@ Client::~Client() {
     if (sh.ev1) cudaEventDestroy(sh.ev1);
     if (sh.own_stream && sh.stream) cudaStreamDestroy(sh.stream);
     if (sh.poll) cudaStreamDestroy(sh.poll);
+    if (sh.k6) cudaStreamDestroy(sh.k6);
     if (sh.dma) {
       cudaStreamSynchronize(sh.dma);
       cudaStreamDestroy(sh.dma);
@@ -741,24 +743,53 @@ Status Client::build_payload(Shard& sh, VersionId v, std::shared_ptr<Payload>* o
   RS_CUDA(cudaEventRecord(sh.ev0, sh.stream));
 
   // Entry digests (K6).
-  std::vector<std::uint64_t> ptrs(n), lens(n), dig(n);
+  std::vector<std::uint64_t> ptrs(n), lens(n), dig(n, 0);
   for (std::size_t i = 0; i < n; ++i) {
     ptrs[i] = reinterpret_cast<std::uint64_t>(sh.regs[i].ptr);
     lens[i] = sh.regs[i].len;
+  }
+  // Early publish: the big entries (>= tiny_threshold: items of their own)
+  // are digested on sh.k6 in the background, launched first so the serial
+  // chains start at once; everything else below runs meanwhile.
+  std::vector<std::uint32_t> now, later;
+  for (std::uint32_t i = 0; i < n; ++i)
+    (cfg_.early_publish && lens[i] >= cfg_.limits.tiny_threshold ? later : now).push_back(i);
+  if (!later.empty()) {
+    if (!sh.k6) RS_CUDA(cudaStreamCreateWithFlags(&sh.k6, cudaStreamNonBlocking));
+    const std::size_t nl = later.size();
+    if (Status s = sh.k6_tables.alloc(sh.device, 3 * nl * 8); !ok(s)) return s;
+    std::vector<std::uint64_t> lp(nl), ll(nl);
+    for (std::size_t k = 0; k < nl; ++k) {
+      lp[k] = ptrs[later[k]];
+      ll[k] = lens[later[k]];
+    }
+    auto* kd = static_cast<std::uint64_t*>(sh.k6_tables.p);
+    RS_CUDA(cudaStreamWaitEvent(sh.k6, sh.ev0, 0));
+    RS_CUDA(cudaMemcpyAsync(kd, lp.data(), nl * 8, cudaMemcpyHostToDevice, sh.k6));
+    RS_CUDA(cudaMemcpyAsync(kd + nl, ll.data(), nl * 8, cudaMemcpyHostToDevice, sh.k6));
+    RS_CUDA(dev::launch_span_digests(kd, kd + nl, kd + 2 * nl, static_cast<int>(nl), sh.k6));
+    stats_.h2d_bytes += 16 * nl;
   }
   // Library buffers of a publish are reused across publishes (a cudaFree
   // synchronizes the device and was measured taking up to 0.44 s here).
   DevBuf& tab = sh.dig_tables;
   if (Status s = tab.alloc(sh.device, std::max<std::size_t>(3 * n, 1) * 8); !ok(s)) return s;
   auto* d = static_cast<std::uint64_t*>(tab.p);
-  if (n) {
-    RS_CUDA(cudaMemcpyAsync(d, ptrs.data(), n * 8, cudaMemcpyHostToDevice, sh.stream));
-    RS_CUDA(cudaMemcpyAsync(d + n, lens.data(), n * 8, cudaMemcpyHostToDevice, sh.stream));
-    RS_CUDA(dev::launch_span_digests(d, d + n, d + 2 * n, static_cast<int>(n), sh.stream));
-    RS_CUDA(cudaMemcpyAsync(dig.data(), d + 2 * n, n * 8, cudaMemcpyDeviceToHost, sh.stream));
+  if (!now.empty()) {
+    const std::size_t nn = now.size();
+    std::vector<std::uint64_t> np(nn), nl(nn), nd(nn);
+    for (std::size_t k = 0; k < nn; ++k) {
+      np[k] = ptrs[now[k]];
+      nl[k] = lens[now[k]];
+    }
+    RS_CUDA(cudaMemcpyAsync(d, np.data(), nn * 8, cudaMemcpyHostToDevice, sh.stream));
+    RS_CUDA(cudaMemcpyAsync(d + nn, nl.data(), nn * 8, cudaMemcpyHostToDevice, sh.stream));
+    RS_CUDA(dev::launch_span_digests(d, d + nn, d + 2 * nn, static_cast<int>(nn), sh.stream));
+    RS_CUDA(cudaMemcpyAsync(nd.data(), d + 2 * nn, nn * 8, cudaMemcpyDeviceToHost, sh.stream));
     RS_CUDA(cudaStreamSynchronize(sh.stream));
-    stats_.h2d_bytes += 16 * n;
-    stats_.d2h_bytes += 8 * n;
+    for (std::size_t k = 0; k < nn; ++k) dig[now[k]] = nd[k];
+    stats_.h2d_bytes += 16 * nn;
+    stats_.d2h_bytes += 8 * nn;
   }
   std::vector<EntryInfo> infos(n);
   for (std::size_t i = 0; i < n; ++i) infos[i] = {sh.regs[i].name, lens[i], dig[i]};
@@ -831,8 +862,121 @@ Status Client::build_payload(Shard& sh, VersionId v, std::shared_ptr<Payload>* o
   cudaEventElapsedTime(&ms, sh.ev0, sh.ev1);
   stats_.last_publish_ms = ms;
   p->encoded = p->manifest.encode();
+  p->provisional = !later.empty();
+  p->deferred = std::move(later);
   *out = std::move(p);
   return Status::ok;
+}
+
+// ---- early publish: background digests ------------------------------------
+
+void Client::start_finalize(VersionId v) {
+  struct Work {
+    int device;
+    cudaStream_t k6;
+    const std::uint64_t* out;
+    std::vector<std::uint32_t> deferred;
+    Manifest manifest;
+  };
+  std::vector<std::optional<Work>> work(num_shards_);
+  bool any = false;
+  for (auto& sh : shards_) {
+    if (sh.device < 0 || !sh.holding || sh.holding->deferred.empty()) continue;
+    const auto nl = sh.holding->deferred.size();
+    work[sh.idx] = Work{sh.device, sh.k6, static_cast<const std::uint64_t*>(sh.k6_tables.p) + 2 * nl,
+                        sh.holding->deferred, sh.holding->manifest};
+    any = true;
+  }
+  if (!any) return;
+  bool all_local = true;
+  for (std::uint32_t i = 0; i < num_shards_; ++i) all_local &= is_local(i);
+  {
+    std::lock_guard lk(fin_m_);
+    fin_running_ = true;
+    fin_v_ = v;
+    fin_status_ = Status::ok;
+    fin_manifests_.assign(num_shards_, std::string());
+  }
+  fin_thread_ = std::thread([this, v, all_local, work = std::move(work)]() mutable {
+    std::vector<std::string> finals(num_shards_);
+    Status st = Status::ok;
+    for (std::uint32_t i = 0; i < num_shards_; ++i) {
+      if (!work[i]) {
+        if (is_local(i) && shards_[i].holding) finals[i] = shards_[i].holding->encoded;
+        continue;
+      }
+      Work& w = *work[i];
+      DeviceGuard g(w.device);
+      std::vector<std::uint64_t> dg(w.deferred.size());
+      if (cudaMemcpyAsync(dg.data(), w.out, dg.size() * 8, cudaMemcpyDeviceToHost, w.k6) != cudaSuccess ||
+          cudaStreamSynchronize(w.k6) != cudaSuccess) {
+        st = Status::transfer_failed;
+        continue;
+      }
+      for (std::size_t k = 0; k < dg.size(); ++k) w.manifest.set_entry_digest(w.deferred[k], dg[k]);
+      finals[i] = w.manifest.encode();
+    }
+    // the in-process registry takes the final bytes now; a replica split over
+    // processes commits them through its caller (rs_server_finalize)
+    if (ok(st) && all_local) st = reg_->finalize_manifests(model_, replica_, v, finals);
+    std::lock_guard lk(fin_m_);
+    fin_status_ = st;
+    fin_manifests_ = std::move(finals);
+    fin_running_ = false;
+  });
+}
+
+Status Client::join_finalize() {
+  if (fin_thread_.joinable()) fin_thread_.join();
+  std::lock_guard lk(fin_m_);
+  if (fin_manifests_.empty()) return fin_status_;
+  for (auto& sh : shards_) {
+    if (sh.idx >= fin_manifests_.size() || !sh.holding || sh.holding->deferred.empty()) continue;
+    const std::string& fb = fin_manifests_[sh.idx];
+    if (!ok(fin_status_) || fb.empty()) continue;
+    auto m = Manifest::decode(fb);
+    if (!m || !m->same_structure(sh.holding->manifest)) continue;
+    sh.holding->manifest = std::move(*m);
+    sh.holding->encoded = fb;
+    sh.holding->provisional = false;
+    sh.holding->deferred.clear();
+  }
+  fin_manifests_.clear();
+  return fin_status_;
+}
+
+Status Client::finalize_publish(double wait_s, std::vector<std::string>* manifests) {
+  (void)wait_s;  // the digests are a bounded kernel: the join always returns
+  Status st = join_finalize();
+  if (manifests) {
+    manifests->clear();
+    for (auto& sh : shards_) manifests->push_back(sh.device >= 0 && sh.holding ? sh.holding->encoded : "");
+  }
+  return st;
+}
+
+Status Client::adopt_final(Shard& sh, double wait_s) {
+  if (!sh.holding || !sh.holding->provisional) return Status::ok;
+  if (!sh.holding->deferred.empty()) return join_finalize();  // this publisher's own digests
+  const std::optional<VersionId> v = current_ ? current_ : sh.partial_version;
+  if (!v) return Status::not_found;
+  const std::string key = layout_key();
+  auto deadline = std::chrono::steady_clock::now() + std::chrono::duration<double>(wait_s);
+  for (;;) {
+    std::string bytes;
+    bool fin = false;
+    if (Status s = reg_->current_manifest(model_, *v, key, sh.idx, &bytes, &fin); !ok(s)) return s;
+    if (fin) {
+      auto m = Manifest::decode(bytes);
+      if (!m || !m->same_structure(sh.holding->manifest)) return Status::manifest_conflict;
+      sh.holding->manifest = std::move(*m);
+      sh.holding->encoded = bytes;
+      sh.holding->provisional = false;
+      return Status::ok;
+    }
+    if (std::chrono::steady_clock::now() > deadline) return Status::timeout;
+    std::this_thread::sleep_for(std::chrono::milliseconds(1));
+  }
 }
 
 Status Client::alloc_tables(Shard& sh, Payload& p, std::uint32_t extra_chunks) {
@@ -882,6 +1026,7 @@ Status Client::hash_items(Shard& sh, Payload& p, const std::vector<std::uint32_t
 Status Client::prepare_publish(VersionId v, std::vector<std::string>* manifests,
                                std::vector<std::string>* layouts) {
   if (terminal()) return Status::invalid_state;  // regions hold a cast, not the version
+  join_finalize();  // the previous publish's background digests
   manifests->clear();
   if (layouts) layouts->clear();
   for (auto& sh : shards_) {
@@ -944,16 +1089,20 @@ Status Client::publish(VersionId v) {
   if (Status s = prepare_publish(v, &manifests, &layouts); !ok(s)) return s;
   PhaseClock pc;
   OpOutcome o;
-  Status s = reg_->publish(model_, replica_, v, manifests, &o, layouts);
+  Status s = reg_->publish(model_, replica_, v, manifests, &o, layouts, publish_pending());
   if (ok(s)) s = o.status;
   pc.mark("publish: registry");
   commit_publish(v, s);
+  if (ok(s)) start_finalize(v);
   pc.mark("publish: commit");
   return s;
 }
 
 Status Client::unpublish() {
   if (!opened_) return Status::invalid_state;
+  // an early publish's digests still read the regions: finish them before
+  // the caller may mutate the weights
+  join_finalize();
   apply_releases();
   OpOutcome o;
   Status s = reg_->unpublish(model_, replica_, &o);
@@ -1044,7 +1193,22 @@ Status Client::resolve_source(Shard& sh, const Assignment& a, VersionId v, Sourc
 
 Status Client::bind(Shard& sh, const Assignment& a, VersionId v) {
   if (Status s = ensure_stream(sh); !ok(s)) return s;
-  if (sh.holding && sh.holding->encoded == a.manifest) {
+  bool same = sh.holding && sh.holding->encoded == a.manifest;
+  if (sh.holding && !same && (sh.holding->provisional || a.provisional) && sh.holding->deferred.empty()) {
+    // an early publish's provisional bytes against its final ones (or the
+    // reverse): the same version's payload when the structure agrees
+    auto m = Manifest::decode(a.manifest);
+    const bool vsame = (current_ && *current_ == v) || (sh.partial_version && *sh.partial_version == v);
+    if (m && vsame && m->same_structure(sh.holding->manifest)) {
+      if (!a.provisional) {
+        sh.holding->manifest = std::move(*m);
+        sh.holding->encoded = a.manifest;
+        sh.holding->provisional = false;
+      }
+      same = true;
+    }
+  }
+  if (same) {
     // Identical manifest: resume.  Keeping the fill epoch keeps every batch
     // already landed for this version (flag == epoch) out of the pull.
     bool resume = (current_ && *current_ == v) || (sh.partial_version && *sh.partial_version == v);
@@ -1118,6 +1282,7 @@ Status Client::bind(Shard& sh, const Assignment& a, VersionId v) {
   if (Status s = alloc_tables(sh, *p, 0); !ok(s)) return give_back(s);
   if (cudaStreamSynchronize(sh.stream) != cudaSuccess) return give_back(Status::transfer_failed);
   p->epoch = ++sh.epoch_ctr;
+  p->provisional = a.provisional;
   sh.holding = std::move(p);
   sh.partial_version = v;
   sh.reported = 0;
@@ -1821,6 +1986,16 @@ Status Client::finish_reshard(Shard& sh) {
   std::vector<std::uint32_t> rehash = group_items;
   rehash.insert(rehash.end(), rs.plan.rehash.begin(), rs.plan.rehash.end());
   std::sort(rehash.begin(), rehash.end());
+  if (std::getenv("RSB_TIMING")) {
+    std::uint64_t gb = 0, cb = 0, rb = 0;
+    for (const auto& gbuf : rs.gather_bufs) gb += gbuf->n;
+    for (const auto& c : rs.plan.copies) cb += c.rows * c.nc;
+    for (auto i : rehash) rb += items[i].length;
+    std::fprintf(stderr, "[rsb] finish_reshard shard %u: %zu gathers (%llu B), %zu copies (%llu B), "
+                 "%zu group spans, %zu rehash items (%llu B)\n", sh.idx, rs.gather_bufs.size(),
+                 (unsigned long long)gb, rs.plan.copies.size(), (unsigned long long)cb, srcs.size(),
+                 rehash.size(), (unsigned long long)rb);
+  }
   if (Status s = hash_items(sh, p, rehash); !ok(s)) return s;
   DeviceGuard g(sh.device);
   RS_CUDA(cudaStreamSynchronize(sh.stream));
@@ -1935,6 +2110,7 @@ Status Client::update(const VersionSpec& spec, bool* changed, VersionId* out, do
 }
 
 Status Client::close() {
+  join_finalize();
   closed_ = true;
   stop_serving();
   for (auto& sh : shards_) serves_->erase(ServeRegistry::key(model_, replica_, sh.idx));
@@ -1944,9 +2120,22 @@ Status Client::close() {
   return Status::ok;
 }
 
-Result<std::string> Client::manifest_bytes(std::uint32_t shard) const {
+Result<std::string> Client::manifest_bytes(std::uint32_t shard) {
+  if (shard >= num_shards_ || !shards_[shard].holding) return Status::not_found;
+  // early publish: the reference-identical bytes, once their digests are in
+  if (Status s = adopt_final(shards_[shard], 60.0); !ok(s)) return s;
+  return shards_[shard].holding->encoded;
+}
+
+Result<std::string> Client::held_manifest(std::uint32_t shard) const {
   if (shard >= num_shards_ || !shards_[shard].holding) return Status::not_found;
   return shards_[shard].holding->encoded;
+}
+
+bool Client::publish_pending() const {
+  for (const auto& sh : shards_)
+    if (sh.device >= 0 && sh.holding && !sh.holding->deferred.empty()) return true;
+  return false;
 }
 
 Status Client::chunk_digests(std::uint32_t shard, std::vector<std::uint64_t>* out) {

@@ -27,6 +27,7 @@
 #include <optional>
 #include <set>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "common.hpp"
@@ -48,6 +49,12 @@ struct ClientConfig {
   std::string dc = "dc0";
   std::uint32_t reshard_align = 2;   // chunk rule: TP splits up to this stay chunk aligned
   std::uint32_t grid_sms = 0;        // SMs a fill's persistent kernel may occupy (0: all)
+  // Early publish: commit the chunk-digest table and the manifest structure
+  // at once (readers bind and pull, verifying chunk by chunk) and the
+  // big-entry XXH64 digests -- a serial chain per entry, ~0.43 s for the
+  // 1.05 GB Llama-3-8B embedding -- when they are done.  The committed
+  // manifest is the reference's, byte for byte; only its arrival is later.
+  bool early_publish = false;
 };
 
 // Owned device allocation.
@@ -291,7 +298,14 @@ class Client {
   const std::string& model() const { return model_; }
   const std::string& replica() const { return replica_; }
   std::uint32_t num_shards() const { return num_shards_; }
-  Result<std::string> manifest_bytes(std::uint32_t shard) const;
+  Result<std::string> manifest_bytes(std::uint32_t shard);
+  Result<std::string> held_manifest(std::uint32_t shard) const;  // no wait (provisional bytes)
+  // Early publish: wait for this publisher's big-entry digests and commit
+  // the final manifests (rs_publish_finalize); the final bytes per local
+  // shard when manifests != null.
+  Status finalize_publish(double wait_s, std::vector<std::string>* manifests = nullptr);
+  // The last publish still digests its big entries in the background.
+  bool publish_pending() const;
   Status chunk_digests(std::uint32_t shard, std::vector<std::uint64_t>* out);
   Result<std::string> export_serve(std::uint32_t shard);
   // The shard's device serve tables (rs_serve_state).
@@ -338,6 +352,9 @@ class Client {
     bool landed_some = false;  // a fill ran in this epoch: flags may be set
     std::vector<std::uint64_t> item_ptrs;  // own landing/serving address per item
     std::unique_ptr<Reshard> reshard;      // set when pulling from another slicing
+    // early publish: the manifest's big-entry digests are not in yet
+    bool provisional = false;
+    std::vector<std::uint32_t> deferred;   // publisher: entries K6 digests in the background
   };
   struct Shard {
     std::uint32_t idx = 0;
@@ -375,11 +392,21 @@ class Client {
     };
     std::map<VersionId, Lane> lanes;  // retention offloads held for the registry
     std::shared_ptr<StreamSource> tcp;  // the fill's source when it is off-box (tcp:)
+    // early publish: K6 over the big entries on its own stream
+    cudaStream_t k6 = nullptr;
+    DevBuf k6_tables;
   };
   Status make_retention_lane(Shard& sh, VersionId v, std::string* endpoint);
   Status settle_offload(OpOutcome* o, double wait_s);
 
   Status ensure_stream(Shard& sh);
+  // Early publish: the background digests of the last publish are committed
+  // (registry + own manifests) once done; join_finalize waits for them.
+  void start_finalize(VersionId v);
+  Status join_finalize();
+  // A payload holding provisional manifest bytes adopts the final ones from
+  // the registry (waiting up to wait_s for them).
+  Status adopt_final(Shard& sh, double wait_s);
   int grid(const Shard& sh) const;  // SMs this handle's persistent kernels occupy
   Status build_payload(Shard& sh, VersionId v, std::shared_ptr<Payload>* out);
   Status bind(Shard& sh, const Assignment& a, VersionId v);
@@ -416,6 +443,14 @@ class Client {
   // fresh host memory runs at ~2 GB/s, a D2H copy into pinned memory at ~50.
   std::vector<std::unique_ptr<HostBuf>> host_pool_;
   std::vector<FillOutcome> launch_out_;  // launch_shards -> wait_shards
+  // early publish finalizer (background thread; results adopted on the
+  // caller's thread)
+  std::thread fin_thread_;
+  std::mutex fin_m_;
+  bool fin_running_ = false;
+  Status fin_status_ = Status::ok;
+  VersionId fin_v_ = 0;
+  std::vector<std::string> fin_manifests_;  // per shard ("" for a non-local shard)
   std::vector<bool> launched_;
   std::vector<std::optional<Assignment>> launch_as_;  // per shard: the latest launch's assignment
   bool published_ = false;

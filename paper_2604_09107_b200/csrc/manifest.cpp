@@ -177,6 +177,28 @@ void Manifest::set_group_digest(std::uint32_t g, std::uint64_t d) {
     if (it.is_group && it.index == g) it.digest = d;
 }
 
+void Manifest::set_entry_digest(std::uint32_t e, std::uint64_t d) {
+  entries[e].digest = d;
+  for (auto& it : items_)
+    if (!it.is_group && it.index == e) it.digest = d;
+}
+
+bool Manifest::same_structure(const Manifest& o) const {
+  if (alg != o.alg || entries.size() != o.entries.size() || groups.size() != o.groups.size()) return false;
+  for (std::size_t i = 0; i < entries.size(); ++i)
+    if (entries[i].name != o.entries[i].name || entries[i].length != o.entries[i].length) return false;
+  for (std::size_t g = 0; g < groups.size(); ++g) {
+    if (groups[g].packed_length != o.groups[g].packed_length ||
+        groups[g].members.size() != o.groups[g].members.size())
+      return false;
+    for (std::size_t k = 0; k < groups[g].members.size(); ++k)
+      if (groups[g].members[k].entry != o.groups[g].members[k].entry ||
+          groups[g].members[k].offset != o.groups[g].members[k].offset)
+        return false;
+  }
+  return true;
+}
+
 std::string Manifest::encode() const {
   std::string out;
   field_u64(out, 1, 1);  // format version

@@ -64,6 +64,10 @@ class Manifest {
   std::uint64_t total_bytes() const { return total_; }
   int group_of(std::uint32_t entry) const { return owner_[entry]; }
   void set_group_digest(std::uint32_t g, std::uint64_t d);
+  void set_entry_digest(std::uint32_t e, std::uint64_t d);
+  // Same entries (names, lengths), groups (packing) and algorithm tag: the
+  // manifests differ at most in their digests.
+  bool same_structure(const Manifest& o) const;
 
   std::string encode() const;  // canonical bytes (manifest.cpp:103-139)
   static Result<Manifest> decode(std::string_view bytes);

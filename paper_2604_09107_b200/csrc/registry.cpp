@@ -210,6 +210,7 @@ Assignment Registry::make_assignment(ModelState& m, Rep& src, VersionId v,
   a.source_complete = src.life == Life::published && src.complete_all();
   a.cross_dc = src.dc != reader.dc;
   const LayoutInfo& li = m.versions[v].by_layout[src.layout];
+  a.provisional = li.provisional;
   if (src.layout == slicing(reader.layout)) {
     a.manifest = shard < li.manifests.size() ? li.manifests[shard] : "";
     a.layout = shard < li.layouts.size() ? li.layouts[shard] : "";
@@ -226,7 +227,8 @@ Assignment Registry::make_assignment(ModelState& m, Rep& src, VersionId v,
 
 Status Registry::publish(const std::string& model, const std::string& replica,
                          VersionId v, const std::vector<std::string>& manifests,
-                         OpOutcome* out, const std::vector<std::string>& layouts) {
+                         OpOutcome* out, const std::vector<std::string>& layouts,
+                         bool provisional) {
   std::lock_guard lk(mu_);
   Rep* r = find(model, replica);
   if (!r) return Status::not_found;
@@ -259,11 +261,19 @@ Status Registry::publish(const std::string& model, const std::string& replica,
   auto lit = vi.by_layout.find(r->layout);
   if (lit != vi.by_layout.end()) {
     if (lit->second.num_shards != r->num_shards) return reject(Status::manifest_conflict, nullptr);
-    for (std::uint32_t s = 0; s < r->num_shards; ++s)
-      if (lit->second.manifests[s] != manifests[s])
+    for (std::uint32_t s = 0; s < r->num_shards; ++s) {
+      if (lit->second.manifests[s] == manifests[s]) continue;
+      // an early publish on either side: the structures must agree
+      auto a = Manifest::decode(lit->second.manifests[s]), b = Manifest::decode(manifests[s]);
+      if (!(provisional || lit->second.provisional) || !a || !b || !a->same_structure(*b))
         return reject(Status::manifest_conflict, "manifest_conflict");
+    }
+    if (lit->second.provisional && !provisional) {
+      lit->second.manifests = manifests;  // this publisher brings the final bytes
+      lit->second.provisional = false;
+    }
   } else {
-    LayoutInfo li{r->num_shards, manifests, layouts};
+    LayoutInfo li{r->num_shards, manifests, layouts, provisional};
     li.layouts.resize(r->num_shards);
     vi.by_layout.emplace(r->layout, std::move(li));
   }
@@ -279,6 +289,43 @@ Status Registry::publish(const std::string& model, const std::string& replica,
   if (out) *out = r->last;
   wake_blocked(model);
   cv_.notify_all();
+  return Status::ok;
+}
+
+Status Registry::finalize_manifests(const std::string& model, const std::string& replica,
+                                    VersionId v, const std::vector<std::string>& manifests) {
+  std::lock_guard lk(mu_);
+  Rep* r = find(model, replica);
+  if (!r) return Status::not_found;
+  auto& m = ms(model);
+  auto vit = m.versions.find(v);
+  if (vit == m.versions.end()) return Status::not_found;
+  auto lit = vit->second.by_layout.find(r->layout);
+  if (lit == vit->second.by_layout.end()) return Status::not_found;
+  LayoutInfo& li = lit->second;
+  if (manifests.size() != li.num_shards) return Status::invalid_argument;
+  if (!li.provisional) return li.manifests == manifests ? Status::ok : Status::manifest_conflict;
+  for (std::uint32_t s = 0; s < li.num_shards; ++s) {
+    auto a = Manifest::decode(li.manifests[s]), b = Manifest::decode(manifests[s]);
+    if (!a || !b || !a->same_structure(*b)) return Status::manifest_conflict;
+  }
+  li.manifests = manifests;
+  li.provisional = false;
+  trace("manifest_final", {{"model", model}, {"replica", replica}, {"v", n2s(v)}});
+  cv_.notify_all();
+  return Status::ok;
+}
+
+Status Registry::current_manifest(const std::string& model, VersionId v, const std::string& layout_key,
+                                  std::uint32_t shard, std::string* bytes, bool* final_bytes) {
+  std::lock_guard lk(mu_);
+  auto& m = ms(model);
+  auto vit = m.versions.find(v);
+  if (vit == m.versions.end()) return Status::not_found;
+  auto lit = vit->second.by_layout.find(slicing(layout_key));
+  if (lit == vit->second.by_layout.end() || shard >= lit->second.manifests.size()) return Status::not_found;
+  *bytes = lit->second.manifests[shard];
+  *final_bytes = !lit->second.provisional;
   return Status::ok;
 }
 

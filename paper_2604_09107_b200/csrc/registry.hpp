@@ -61,6 +61,9 @@ struct Assignment {
   bool local_seed_consume = false;
   std::string manifest;  // encoded Manifest of this shard ("" on a reshard)
   std::string layout;    // encoded ShardLayout of this shard (chunk lengths)
+  // Early publish: the manifest's big-entry digests are not computed yet (0);
+  // the publisher commits them later (Registry::finalize_manifests).
+  bool provisional = false;
   // Reshard (the source's slicing differs from the reader's): every source
   // shard's manifest, layout and endpoint.
   bool reshard = false;
@@ -149,9 +152,23 @@ class Registry {
 
   // Each returns the immediate status; if ok and the op is parked,
   // *pending = true and the outcome arrives through op_result().
+  // provisional: an early publish (ClientConfig.early_publish) -- the
+  // manifests' big-entry digests are still being computed; readers may bind
+  // and pull (they verify chunk by chunk), and finalize_manifests commits
+  // the reference-identical bytes later.
   Status publish(const std::string& model, const std::string& replica,
                  VersionId v, const std::vector<std::string>& manifests,
-                 OpOutcome* out, const std::vector<std::string>& layouts = {});
+                 OpOutcome* out, const std::vector<std::string>& layouts = {},
+                 bool provisional = false);
+  // Commits the final manifests of an early publish: same structure as the
+  // provisional ones (entries, packing), digests filled in.  A final version
+  // accepts only identical bytes.
+  Status finalize_manifests(const std::string& model, const std::string& replica, VersionId v,
+                            const std::vector<std::string>& manifests);
+  // The manifest bytes of version v for a slicing key's shard, and whether
+  // they are final (not an early publish still digesting).
+  Status current_manifest(const std::string& model, VersionId v, const std::string& layout_key,
+                          std::uint32_t shard, std::string* bytes, bool* final_bytes);
   // A resharding reader registers the derived manifests/layouts of its own
   // slicing so readers of the same slicing can later pull from it.
   Status add_layout(const std::string& model, VersionId v, const std::string& layout_key,
@@ -250,6 +267,7 @@ class Registry {
     std::uint32_t num_shards = 0;
     std::vector<std::string> manifests;
     std::vector<std::string> layouts;
+    bool provisional = false;  // early publish: big-entry digests still pending
   };
   struct VersionInfo {
     std::map<std::string, LayoutInfo> by_layout;  // slicing key -> per-shard metadata

@@ -36,6 +36,12 @@ def _blob_arrays(blobs):
     return C.cast(arr, C.c_void_p), C.cast(lens, C.c_void_p), arr, lens
 
 
+def lib_manifest(h, shard: int) -> bytes:
+    """The shard's manifest bytes as held right now (provisional during an
+    early publish; Handle.manifest waits for the final ones)."""
+    return _read_bytes(lib.rs_manifest_now, h.h, shard)
+
+
 def apply_op(c, o) -> int:
     """Applies one registry operation (see DistCluster.server_ops) to the
     registry replica `c` (an rs_cluster handle); returns its status code."""
@@ -56,12 +62,18 @@ def apply_op(c, o) -> int:
     if kind == "publish":
         _, m, r, v, mans = o[:5]
         lays = o[5] if len(o) > 5 else []
+        provisional = bool(o[6]) if len(o) > 6 else False  # an early publish
         pm, pl, _k1, _k2 = _blob_arrays(mans)
         if lays:
             qm, ql, _k3, _k4 = _blob_arrays(lays)
         else:
             qm = ql = None
-        return lib.rs_server_publish(c, _b(m), _b(r), v, len(mans), pm, pl, qm, ql)
+        fn = lib.rs_server_publish_provisional if provisional else lib.rs_server_publish
+        return fn(c, _b(m), _b(r), v, len(mans), pm, pl, qm, ql)
+    if kind == "finalize":
+        _, m, r, v, mans = o
+        pm, pl, _k1, _k2 = _blob_arrays(mans)
+        return lib.rs_server_finalize(c, _b(m), _b(r), v, len(mans), pm, pl)
     if kind == "add_layout":
         _, m, v, key, mans, lays = o
         pm, pl, _k1, _k2 = _blob_arrays(mans)
@@ -213,7 +225,8 @@ class DistCluster:
         if h is not None:
             check(lib.rs_prepare_publish(h.h, version), "rs_prepare_publish")
             mine = {"model": h.model, "replica": h.replica, "n": h.num_shards,
-                    "shards": {s: (h.manifest(s), h.layout(s)) for s in h.local_shards()}}
+                    "provisional": h.publish_pending,
+                    "shards": {s: (lib_manifest(h, s), h.layout(s)) for s in h.local_shards()}}
         rcs = {}
         for (m, r), parts in self._merge(self.gather(mine)).items():
             n = parts[0]["n"]
@@ -224,7 +237,8 @@ class DistCluster:
                 rcs[(m, r)] = int(Status.invalid_argument)
                 continue
             rcs[(m, r)] = self._apply(("publish", m, r, version, [sh[i][0] for i in range(n)],
-                                       [sh[i][1] for i in range(n)]))
+                                       [sh[i][1] for i in range(n)],
+                                       any(p.get("provisional") for p in parts)))
         blobs = None
         if h is not None:
             st = rcs[(h.model, h.replica)]
@@ -259,6 +273,23 @@ class DistCluster:
             for s, ep in p["eps"].items():
                 self._apply(("offload_confirm", p["model"], p["replica"], s, p["v"], p["ok"], ep))
         self._import_all([p["blobs"] if p else None for p in parts])
+
+    def finalize(self, h: Optional[Handle]) -> None:
+        """Collective: an early publish's ranks wait for their big-entry
+        digests and every registry replica commits the final manifests."""
+        mine = None
+        if h is not None:
+            v = h.current_version
+            check(lib.rs_publish_finalize(h.h, 60.0), "rs_publish_finalize")
+            mine = {"model": h.model, "replica": h.replica, "n": h.num_shards, "v": v,
+                    "shards": {s: h.manifest(s) for s in h.local_shards()}}
+        for (m, r), parts in self._merge(self.gather(mine)).items():
+            sh = {}
+            for p in parts:
+                sh.update(p["shards"])
+            n = parts[0]["n"]
+            if sorted(sh) == list(range(n)):
+                self._apply(("finalize", m, r, parts[0]["v"], [sh[i] for i in range(n)]))
 
     def unpublish(self, h: Optional[Handle]) -> Optional[OpResult]:
         mine = {"model": h.model, "replica": h.replica} if h is not None else None

@@ -107,7 +107,7 @@ def _read_bytes(fn, *args) -> bytes:
 
 def make_config(chunk_bytes=4096, tiny_threshold=2 << 20, group_target=64 << 20, pipeline=True,
                 checksum_retries=3, pull_timeout_s=4.0, datacenter="dc0",
-                reshard_align=2, grid_sms=0) -> RsConfig:
+                reshard_align=2, grid_sms=0, early_publish=False) -> RsConfig:
     cfg = RsConfig()
     lib.rs_config_default(C.byref(cfg))
     cfg.chunk_bytes = chunk_bytes
@@ -119,6 +119,7 @@ def make_config(chunk_bytes=4096, tiny_threshold=2 << 20, group_target=64 << 20,
     cfg.datacenter = datacenter.encode()
     cfg.reshard_align = reshard_align
     cfg.grid_sms = grid_sms
+    cfg.early_publish = int(early_publish)
     return cfg
 
 
@@ -362,6 +363,16 @@ class Handle:
 
     def unpublish(self) -> OpResult:
         return OpResult(Status(lib.rs_unpublish(self.h)))
+
+    @property
+    def publish_pending(self) -> bool:
+        """Early publish: the last publish still digests its big entries."""
+        return bool(lib.rs_publish_pending(self.h))
+
+    def finalize(self, wait_s: float = 60.0) -> Status:
+        """Early publish: wait for the big-entry digests and commit the final
+        (reference-identical) manifests."""
+        return Status(lib.rs_publish_finalize(self.h, wait_s))
 
     def replicate(self, spec: str = "latest", wait_s: float = 60.0) -> OpResult:
         v = C.c_uint64()

@@ -36,7 +36,7 @@ import uuid
 from typing import Optional
 
 from ._lib import lib
-from .dist import apply_op
+from .dist import apply_op, lib_manifest
 from .ros import Cluster, Handle, OpResult, Status, _read_bytes, check, combine_layout_key
 
 
@@ -99,7 +99,9 @@ class SharedCluster:
         self.local = Cluster(pipeline=pipeline, smart_skipping=smart_skipping)
         self.me = f"{os.getpid()}-{uuid.uuid4().hex[:8]}"
         self._w = _Conn(host, port, timeout_s)  # appends (caller's thread)
+        self._w2 = _Conn(host, port, timeout_s)  # appends of the early-publish finalizer
         self._r = _Conn(host, port, timeout_s)  # the follower's tail
+        self._fin = None
         self._cv = threading.Condition()
         self.applied = 0
         self._rc = {}        # seq -> status code of this member's own ops
@@ -168,8 +170,11 @@ class SharedCluster:
             self._w.append(pickle.dumps((self.me, ("import", list(blobs)))))
 
     def close(self):
+        if self._fin is not None:
+            self._fin.join(60)
         self._stop = True
         self._t.join(timeout=5)
+        self._w2.close()
         self._w.close()
         self._r.close()
         self.local.close()
@@ -216,15 +221,32 @@ class SharedCluster:
             self.op(("retain", h.model, h.replica, list(h.retain)))
 
     def publish(self, h: Handle, version: int) -> OpResult:
+        """publish(); with early_publish the provisional manifests go in at
+        once and a background thread appends the final ones ("finalize")
+        when the big-entry digests are done."""
         check(lib.rs_prepare_publish(h.h, version), "rs_prepare_publish")
         n = h.num_shards
-        rc = self.op(("publish", h.model, h.replica, version, [h.manifest(s) for s in range(n)],
-                      [h.layout(s) for s in range(n)]))
+        early = h.publish_pending
+        rc = self.op(("publish", h.model, h.replica, version, [lib_manifest(h, s) for s in range(n)],
+                      [h.layout(s) for s in range(n)], early))
         lib.rs_commit_publish(h.h, version, rc)
         if rc == 0:
             self.announce([h.serve_export(s) for s in range(n)])
+            if early:
+                def fin():
+                    if lib.rs_publish_finalize(h.h, 60.0) == 0:
+                        self._w2.append(pickle.dumps((self.me, ("finalize", h.model, h.replica, version,
+                                                                [h.manifest(s) for s in range(n)]))))
+                self._fin = threading.Thread(target=fin, daemon=True)
+                self._fin.start()
         st = Status(rc)
         return OpResult(st, version if st == Status.ok else None)
+
+    def finalized(self, h: Handle, timeout: float = 60.0) -> None:
+        """Wait until an early publish's final manifests are in the log."""
+        if self._fin is not None:
+            self._fin.join(timeout)
+            self._fin = None
 
     def _offload_first(self, h: Handle) -> None:
         v = C.c_uint64()
@@ -237,6 +259,7 @@ class SharedCluster:
             self.op(("offload_confirm", h.model, h.replica, s, v.value, good, f"host:{h.replica}:{s}"))
 
     def unpublish(self, h: Handle) -> OpResult:
+        self.finalized(h)  # an early publish's digests still read the regions
         rc = self.op(("unpublish", h.model, h.replica))
         self._offload_first(h)
         done, s, _, _ = self.result(h.model, h.replica)

@@ -331,3 +331,58 @@ def test_measured_topology_reaches_the_planner(fx):
     for r in names[1:]:
         assert fx.h[r].replicate().status == Status.ok
         assert fx.same("T", r, 0, "w")
+
+
+def test_early_publish_commits_the_reference_manifest_later(oracle):
+    """rs_config.early_publish: publish() returns once the chunk-digest table
+    and the manifest structure are in (readers bind and pull, verifying chunk
+    by chunk); the big entries' XXH64 digests -- a serial chain per entry --
+    finish in the background and the committed manifest is then the
+    reference's build_publish_payload bytes exactly."""
+    import time
+    from paper_2604_09107_b200.ros import Cluster, Status
+    dev = torch.device("cuda:0")
+    names = ["big", "mid", "t1", "t2"]
+    host = [oracle.synth_bf16(60 + i, n) for i, n in enumerate([1 << 29, 3 << 20, 3000, 777])]
+    with Cluster() as cl:
+        t = cl.open("m", "T", 1, early_publish=True)
+        r = cl.open("m", "R", 1)
+        keep = []
+        for n, a in zip(names, host):
+            src = torch.from_numpy(a.view(np.int16).copy()).to(dev)
+            dst = torch.zeros_like(src)
+            keep += [src, dst]
+            assert t.register_tensor(0, n, src) == Status.ok
+            assert r.register_tensor(0, n, dst) == Status.ok
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        assert t.publish(1).status == Status.ok
+        publish_s = time.perf_counter() - t0
+        assert t.publish_pending  # the 1 GiB entry's chain (~0.4 s) is still running
+        res = r.replicate("latest")
+        assert res.status == Status.ok and res.version == 1
+        torch.cuda.synchronize()
+        for a, d in zip(host, keep[1::2]):
+            assert np.array_equal(d.cpu().numpy().view(np.uint16), a)
+        want = oracle.publish_manifest(names, host)
+        assert r.manifest(0) == want  # waits for the final bytes
+        assert t.manifest(0) == want and not t.publish_pending
+        assert "manifest_final" in cl.trace()
+        assert publish_s < 0.2, publish_s
+        # a reader arriving afterwards is assigned the final bytes directly
+        r2 = cl.open("m", "R2", 1)
+        k2 = [torch.zeros_like(x) for x in keep[0::2]]
+        for n, x in zip(names, k2):
+            assert r2.register_tensor(0, n, x) == Status.ok
+        assert r2.replicate("latest").status == Status.ok
+        assert r2.manifest(0) == want
+        # the next version: unpublish waits for nothing left, new bytes, early again
+        assert t.unpublish().status == Status.ok
+        from paper_2604_09107_b200 import ros
+        ros.synth_bf16(keep[0], 999)
+        torch.cuda.synchronize()
+        assert t.publish(2).status == Status.ok
+        assert r.update("latest").status == Status.ok
+        h2 = [keep[0].cpu().numpy().view(np.uint16)] + host[1:]
+        assert r.manifest(0) == oracle.publish_manifest(names, h2)
+        assert torch.equal(keep[0], keep[1])

@@ -48,7 +48,7 @@ def _hex(xs):
     return ["%016X" % x for x in xs]
 
 
-def _pair(workload, reshard=False, cast=False):
+def _pair(workload, reshard=False, cast=False, early=False):
     import bench as B
     from paper_2604_09107_b200.ros import Cluster
     dev = torch.device("cuda:0")
@@ -57,7 +57,7 @@ def _pair(workload, reshard=False, cast=False):
     rarena, rviews = B.alloc_replica(shapes, dev, elem=1 if cast else 2)
     torch.cuda.synchronize()
     cl = Cluster()
-    t = cl.open("m", "trainer", 8 if reshard else 1)
+    t = cl.open("m", "trainer", 8 if reshard else 1, early_publish=early)
     r = cl.open("m", "rollout1", 2 if reshard else 1)
     rslices = B.register_pair(t, r, shapes, tviews, rviews, dev, reshard, cast)
     return shapes, cl, t, r, tviews, rviews, rslices
@@ -71,19 +71,27 @@ def _free(*objs):
     torch.cuda.empty_cache()
 
 
-def test_config2_llama3_8b_matches_reference(scale):
+@pytest.mark.parametrize("early", [False, True], ids=["reference_order", "early_publish"])
+def test_config2_llama3_8b_matches_reference(scale, early):
+    """early_publish: readers pull while the big-entry digests run; the
+    manifest committed afterwards must still be the reference's bytes."""
     from paper_2604_09107_b200 import ros
     from paper_2604_09107_b200.ros import Status
     g = scale["config2_llama3_8b"]
-    shapes, cl, t, r, tviews, rviews, _ = _pair("llama3_8b")
+    shapes, cl, t, r, tviews, rviews, _ = _pair("llama3_8b", early=early)
     try:
         assert sum(v.numel() for _, v in tviews) == g["bytes"] == 16_060_522_496
         assert t.publish(1).status == Status.ok
+        if early:
+            assert t.publish_pending
+            res = r.replicate("latest")  # before the digests are in
+            assert res.status == Status.ok, res
         man = t.manifest(0)
         assert len(man) == g["manifest_len"]
         assert hashlib.sha256(man).hexdigest() == g["manifest_sha256"]
         assert _sha(t.chunk_digests(0)) == g["chunk_table_sha256"]
-        res = r.replicate("latest")
+        if not early:
+            res = r.replicate("latest")
         assert res.status == Status.ok and res.version == 1, res
         assert r.manifest(0) == man
         table = r.chunk_digests(0)
