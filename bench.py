@@ -440,7 +440,8 @@ def run_single(args):
     torch.cuda.synchronize()
     stream = torch.cuda.Stream(device=dev)
     cl = Cluster()
-    t = cl.open("m", "trainer", 8 if args.reshard == "fsdp_tp2" else 1, chunk_bytes=args.chunk)
+    t = cl.open("m", "trainer", 8 if args.reshard == "fsdp_tp2" else 1, chunk_bytes=args.chunk,
+                early_publish=args.early_publish)
     reshard = args.reshard in ("tp2", "fsdp_tp2")
     fsdp = t.num_shards  # trainer shards (FSDP-8: Shard(0) row blocks)
     r = cl.open("m", "rollout1", 2 if reshard else 1, chunk_bytes=args.chunk)
@@ -484,7 +485,14 @@ def run_single(args):
                 want = v.view(rows, w)[r0:r0 + nr, c0:c0 + nc]
                 assert torch.equal(buf.view(nr, nc), want), (s, n)
 
-    for _ in range(args.warmup):
+    # the first pull right after the publish: the weight-update latency a
+    # reader sees from the trainer's publish call (with --early-publish the
+    # big-entry digests are still running; the final manifest lands later)
+    step()
+    publish_to_reader_s = time.perf_counter() - t0
+    assert t.finalize() == Status.ok
+    publish_final_s = time.perf_counter() - t0
+    for _ in range(args.warmup - 1):
         step()
     parity = None
     if not args.no_verify:
@@ -547,6 +555,8 @@ def run_single(args):
         "per_receiver_gbs": [round(value, 2)],
         "weight_update_latency_s": round(statistics.mean(walls), 5),
         "publish_s": round(publish_s, 4), "publish_device_ms": round(publish_ms, 3),
+        "publish_to_first_reader_s": round(publish_to_reader_s, 4),
+        "publish_final_s": round(publish_final_s, 4), "early_publish": args.early_publish,
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peaks["hbm_gbs"],
                      "unit": "GB/s", "frac": round(achieved / peaks["hbm_gbs"], 4),
                      "traffic": ncu_traffic("cast" if cast else "local") if not reshard else None,
@@ -674,6 +684,9 @@ def main():
     ap.add_argument("--cast", action="store_true", help="reader lands fp8 e4m3 (config 5)")
     ap.add_argument("--scenario", default="steady", choices=["steady", "elastic"],
                     help="elastic: config 4 (join at 50%% + version bump), N >= 3")
+    ap.add_argument("--early-publish", action="store_true",
+                    help="trainer publishes early: chunk table + manifest structure first, "
+                         "big-entry digests in the background (rs_config.early_publish)")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-host-e2e", action="store_true",
                     help="skip the host-buffer end-to-end leg (N=1)")
