@@ -661,7 +661,7 @@ def run_elastic(args):
         return hashlib.sha256(h.chunk_digests(0).tobytes()).hexdigest()
 
     joins, bumps, publishes, updates, verified = [], [], [], [], True
-    finals = []
+    finals, phase_log = [], []
     for step in range(args.warmup + args.steps):
         # ---- phase A: readers 1..N-2 pull v; the joiner comes in at 50% ----
         dc.unpublish(reader if (reader is not None and reader.is_published) else None)
@@ -689,6 +689,7 @@ def run_elastic(args):
         b0 = time.perf_counter()
         if is_trainer:
             assert dc.unpublish(h).status == Status.ok
+            m0 = time.perf_counter()
             for i, (n, v) in enumerate(views):  # new weights, in place
                 ros.synth_bf16(v, 1000 * (version + 1) + i)
             torch.cuda.synchronize()
@@ -697,12 +698,18 @@ def run_elastic(args):
             pub_s = time.perf_counter() - p0
         else:
             dc.unpublish(None)
+            m0 = p0 = time.perf_counter()
             dc.publish(None, version + 1)
             pub_s = 0.0
+        phases = [m0 - b0, p0 - m0, time.perf_counter() - p0]
         u0 = time.perf_counter()
+        pub_end = u0
         res = dc.update(reader, "latest")
-        torch.cuda.synchronize()
-        t_end = time.perf_counter()
+        if reader is not None:
+            torch.cuda.synchronize()
+        # the bump ends when the last READER holds v+1 (the trainer's device
+        # may still be digesting an early publish's big entries)
+        t_end = time.perf_counter() if reader is not None else pub_end
         if reader is not None and not (res.status == Status.ok and res.version == version + 1):
             raise RuntimeError(f"step {step} update on {name}: {res}\n" + dc.local.trace()[-3000:])
         version += 1
@@ -712,8 +719,8 @@ def run_elastic(args):
         fin_s = 0.0
         if early:
             dc.finalize(h if is_trainer else None)
-            fin_s = time.perf_counter() - t_end
-        lat = dc.gather((t_end - b0, t_end - u0, pub_s, fin_s))
+            fin_s = time.perf_counter() - u0
+        lat = dc.gather((t_end - b0, t_end - u0, pub_s, fin_s, phases))
         new_src = {a.replica: a.src for a in dc.assigns() if a.version == version}
         # v copies never serve v+1: every v+1 source is the trainer or a v+1 copy
         verified &= all(s == "trainer" or new_src.get(s) is not None for s in new_src.values())
@@ -726,6 +733,7 @@ def run_elastic(args):
             updates.append(max(x[1] for x in lat))
             publishes.append(max(x[2] for x in lat))
             finals.append(max(x[3] for x in lat))
+            phase_log.append([[round(y, 4) for y in x[4]] for x in lat])
     verified = all(dc.gather(verified))
     if rank == 0:
         upd = statistics.mean(updates)
@@ -745,7 +753,10 @@ def run_elastic(args):
             "bump_latency_s": round(statistics.mean(bumps), 5),
             "bump_publish_s": round(statistics.mean(publishes), 5),
             "early_publish": early,
+            "bump_phases_s": {"per_rank_unpublish_mutate_publish": phase_log[-1] if phase_log else None},
             "finalize_after_update_s": round(statistics.mean(finals), 5) if early else None,
+            "finalize_what": "early publish: from the readers' update call to the final manifests "
+                             "committed on every registry replica (max over ranks)",
             "bump_update_s": round(upd, 5),
             "weight_update_latency_s": round(upd, 5),
             "roofline": None,

@@ -948,6 +948,7 @@ Status Client::join_finalize() {
 Status Client::finalize_publish(double wait_s, std::vector<std::string>* manifests) {
   (void)wait_s;  // the digests are a bounded kernel: the join always returns
   Status st = join_finalize();
+  if (ok(st) && publish_pending()) st = Status::invalid_state;  // no committed publish to finish
   if (manifests) {
     manifests->clear();
     for (auto& sh : shards_) manifests->push_back(sh.device >= 0 && sh.holding ? sh.holding->encoded : "");
@@ -1078,6 +1079,7 @@ void Client::commit_publish(VersionId v, Status st) {
   }
   current_ = v;
   published_ = true;
+  start_finalize(v);  // early publish: the background digests (no-op otherwise)
 }
 
 Status Client::publish(VersionId v) {
@@ -1093,7 +1095,6 @@ Status Client::publish(VersionId v) {
   if (ok(s)) s = o.status;
   pc.mark("publish: registry");
   commit_publish(v, s);
-  if (ok(s)) start_finalize(v);
   pc.mark("publish: commit");
   return s;
 }

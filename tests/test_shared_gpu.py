@@ -1,6 +1,9 @@
 """GPU: a reader PROCESS that did not exist when the others started joins
 through the registry's operation log and chases a copy that is still filling
 (config 4's elastic join with dynamic membership; shared.py, oplog.cpp).
+The trainer publishes early (rs_config.early_publish): readers pull while its
+big-entry digests run, and the final manifest reaches every member through
+the log afterwards.
 
   process 0   hosts the log; trainer T publishes 1 GiB + tiny tensors; reader
               A is planned and bound (serving its empty fill) but not filling
@@ -47,7 +50,7 @@ def _host(q, joined, done):
         dev = torch.device("cuda", 0)
         log = LogServer()
         sc = SharedCluster("127.0.0.1", log.port)
-        t = sc.create("m", "T", 1, tiny_threshold=1 << 20)
+        t = sc.create("m", "T", 1, tiny_threshold=1 << 20, early_publish=True)
         tb = _bufs(dev, seed=800)
         for i, b in enumerate(tb):
             assert t.register_tensor(0, f"w{i}", b) == Status.ok
@@ -76,6 +79,7 @@ def _host(q, joined, done):
         got_a = ros.digest_spans([b.data_ptr() for b in ab], SIZES, 0)
         sc.sync()
         q.put(("host", "final", {"a": int(res["a"].status), "a_equal": got_a == want, "want": want,
+                                 "t_manifest": t.manifest(0), "a_manifest": a.manifest(0),
                                  "assigns": [(x.replica, x.src) for x in sc.assigns()],
                                  "listing": {v: sorted(r) for v, r in sc.listing("m").items()}}))
         done.wait(120)
@@ -105,7 +109,9 @@ def _joiner(port, q, joined):
         r = sc.replicate(b)
         a = b.transfer_assignment(0)
         got = ros.digest_spans([x.data_ptr() for x in bb], SIZES, dev.index)
-        q.put(("joiner", "final", {"b": int(r.status), "v": r.version, "assignment": a, "digests": got}))
+        # early publish: the final manifest reaches this member through the log
+        q.put(("joiner", "final", {"b": int(r.status), "v": r.version, "assignment": a, "digests": got,
+                                   "manifest": b.manifest(0)}))
         joined.set()
         sc.close()
     except Exception as e:  # pragma: no cover - surfaced by the parent
@@ -143,6 +149,17 @@ def test_reader_process_joins_mid_fill_through_the_op_log():
         assert jb["digests"] == res["host"]["want"]
         assert ("A", "T") in res["host"]["assigns"] and ("B", "A") in res["host"]["assigns"]
         assert res["host"]["listing"] == {1: ["A", "B", "T"]}
+        # T published early (big-entry digests in the background): every
+        # member ends with the reference's build_publish_payload bytes
+        import sys
+        sys.path.insert(0, os.path.join(ROOT, "oracle"))
+        import numpy as np
+        import oracle as O
+        arrs = [O.synth_bf16(800 + i, n // 2) for i, n in enumerate(SIZES)]
+        want = O.publish_manifest([f"w{i}" for i in range(len(SIZES))], arrs, tiny=1 << 20)
+        assert res["host"]["t_manifest"] == want
+        assert res["host"]["a_manifest"] == want
+        assert jb["manifest"] == want
     finally:
         done.set()
         joined.set()
