@@ -1000,7 +1000,8 @@ Status Client::alloc_tables(Shard& sh, Payload& p, std::uint32_t extra_chunks) {
   return Status::ok;
 }
 
-Status Client::hash_items(Shard& sh, Payload& p, const std::vector<std::uint32_t>& which) {
+Status Client::hash_items(Shard& sh, Payload& p, const std::vector<std::uint32_t>& which,
+                          const std::uint32_t* guard) {
   // Hash-only pull over some of the payload's own items: fills their chunk
   // digests and releases their watermarks in the current epoch.
   if (which.empty() || p.cmap.n_chunks() == 0) return Status::ok;
@@ -1019,6 +1020,7 @@ Status Client::hash_items(Shard& sh, Payload& p, const std::vector<std::uint32_t
   pp.dst_flags = static_cast<std::uint32_t*>(p.flags.p);
   pp.dst_epoch = p.epoch;
   pp.timeout_ns = static_cast<std::uint64_t>(cfg_.pull_timeout_s * 1e9);
+  pp.guard = guard;
   RS_CUDA(dev::launch_pull(pp, grid(sh), sh.stream));
   stats_.h2d_bytes += sh.hash_plan.h2d_bytes;
   return Status::ok;
@@ -1799,12 +1801,7 @@ std::vector<Client::FillOutcome> Client::wait_shards(const std::vector<std::uint
   for (std::uint32_t i : which) {
     if (!ok(out[i].status)) continue;
     Shard& sh = shards_[i];
-    if (sh.holding->reshard) {
-      PhaseClock fc;
-      if (Status s = finish_reshard(sh); !ok(s)) out[i] = {s, 0, 0};
-      fc.mark("finish_reshard");
-      continue;
-    }
+    if (sh.holding->reshard) continue;  // its follow-up ran behind the fill (launch_reshard_fill)
     const auto& p = *sh.holding;
     std::vector<std::uint64_t> srcs, dsts, ls;
     for (std::size_t gi = 0; gi < p.manifest.groups.size(); ++gi)
@@ -1823,7 +1820,8 @@ std::vector<Client::FillOutcome> Client::wait_shards(const std::vector<std::uint
 
 Status Client::copy_spans(Shard& sh, const std::vector<std::uint64_t>& srcs,
                           const std::vector<std::uint64_t>& dsts,
-                          const std::vector<std::uint64_t>& lens) {
+                          const std::vector<std::uint64_t>& lens,
+                          const std::uint32_t* guard) {
   // Stream-ordered: returns once the copy is queued on sh.stream (callers
   // synchronize).  The span tables live in sh.span_tables; a later call's
   // upload is ordered behind this call's kernel on the same stream.
@@ -1844,7 +1842,7 @@ Status Client::copy_spans(Shard& sh, const std::vector<std::uint64_t>& srcs,
   auto* d = static_cast<std::uint64_t*>(t.p);
   RS_CUDA(cudaMemcpyAsync(d, host.data(), 4 * n * 8, cudaMemcpyHostToDevice, sh.stream));
   RS_CUDA(dev::launch_copy_spans(d, d + n, d + 2 * n, d + 3 * n, static_cast<int>(n), tiles,
-                                 sh.stream));
+                                 sh.stream, guard));
   stats_.h2d_bytes += 32 * n;
   return Status::ok;
 }
@@ -1900,24 +1898,55 @@ Status Client::launch_reshard_fill(Shard& sh, const Assignment& a, bool src_comp
     d.src = views[d.src_id].item_ptrs[d.pad] + d.src;
     d.pad = link_class(d.src_id);
   }
+  // Gathered source items (groups, unaligned slices) land in staging, but
+  // only the watermark batches that hold bytes some slice copy reads: a
+  // reader shard that needs a few members of a packed group does not pull
+  // (and verify) the rest of it.  Each range is whole batches of the item,
+  // so the kernel's batch -> segment mapping is unchanged.
+  std::map<std::pair<std::uint32_t, std::uint32_t>, std::vector<std::pair<std::uint64_t, std::uint64_t>>> need_bytes;
+  for (const auto& c : rs.plan.copies)
+    need_bytes[{c.src_shard, c.src_item}].emplace_back(c.src_off,
+                                                      c.src_off + (c.rows - 1) * c.src_stride + c.nc);
   std::uint32_t next = rs.own_chunks;
   for (std::size_t gi = 0; gi < rs.plan.gathers.size(); ++gi) {
     const auto& gth = rs.plan.gathers[gi];
     const SourceShard& ss = rs.srcs[gth.src_shard];
     const auto& it = ss.manifest.items()[gth.src_item];
-    dev::ItemDesc d{};
-    d.src = views[gth.src_shard].item_ptrs[gth.src_item];
-    d.dst = reinterpret_cast<std::uint64_t>(rs.gather_bufs[gi]->p);
-    d.len = it.length;
-    d.chunk0 = next;
-    d.chunk_len = ss.layout.chunk_len[gth.src_item];
-    d.src_chunk0 = ss.chunk0[gth.src_item];
-    d.q = d.m = 1;
-    d.src_id = gth.src_shard;
-    d.pad = link_class(gth.src_shard);
-    descs.push_back(d);
-    const auto n = static_cast<std::uint32_t>((it.length + d.chunk_len - 1) / d.chunk_len);
-    next += (n + dev::kBatchChunks - 1) / dev::kBatchChunks * dev::kBatchChunks;
+    const std::uint64_t cl = ss.layout.chunk_len[gth.src_item];
+    const auto n = static_cast<std::uint32_t>((it.length + cl - 1) / cl);
+    const std::uint32_t nb = (n + dev::kBatchChunks - 1) / dev::kBatchChunks;
+    std::vector<char> want(nb, 0);
+    auto nit = need_bytes.find({gth.src_shard, gth.src_item});
+    if (nit == need_bytes.end()) {
+      std::fill(want.begin(), want.end(), 1);
+    } else {
+      const std::uint64_t per = cl * dev::kBatchChunks;
+      for (const auto& [lo, hi] : nit->second)
+        for (std::uint64_t b = lo / per; b <= (hi - 1) / per && b < nb; ++b) want[b] = 1;
+    }
+    for (std::uint32_t b0 = 0; b0 < nb;) {
+      if (!want[b0]) {
+        ++b0;
+        continue;
+      }
+      std::uint32_t b1 = b0;
+      while (b1 < nb && want[b1]) ++b1;
+      const std::uint64_t off = std::uint64_t(b0) * dev::kBatchChunks * cl;
+      const std::uint64_t end = std::min<std::uint64_t>(it.length, std::uint64_t(b1) * dev::kBatchChunks * cl);
+      dev::ItemDesc d{};
+      d.src = views[gth.src_shard].item_ptrs[gth.src_item] + off;
+      d.dst = reinterpret_cast<std::uint64_t>(rs.gather_bufs[gi]->p) + off;
+      d.len = end - off;
+      d.chunk0 = next + b0 * dev::kBatchChunks;
+      d.chunk_len = static_cast<std::uint32_t>(cl);
+      d.src_chunk0 = ss.chunk0[gth.src_item] + b0 * dev::kBatchChunks;
+      d.q = d.m = 1;
+      d.src_id = gth.src_shard;
+      d.pad = link_class(gth.src_shard);
+      descs.push_back(d);
+      b0 = b1;
+    }
+    next += nb * dev::kBatchChunks;
   }
   bool remote = false;
   for (std::uint32_t s = 0; s < nsrc; ++s) remote |= need[s] && src_dev[s] != sh.device;
@@ -1936,10 +1965,13 @@ Status Client::launch_reshard_fill(Shard& sh, const Assignment& a, bool src_comp
   RS_CUDA(dev::launch_pull(pp, grid(sh), sh.stream));
   RS_CUDA(cudaEventRecord(sh.ev1, sh.stream));
   p.landed_some = true;
-  return Status::ok;
+  // the follow-up (slice copies, packing, re-digests) queued right behind the
+  // fill, skipped on the device if it fails: no host round trip in between
+  auto* code = &reinterpret_cast<dev::PullStatus*>(static_cast<std::uint8_t*>(sh.plan.scratch) + 64)->code;
+  return finish_reshard(sh, code);
 }
 
-Status Client::finish_reshard(Shard& sh) {
+Status Client::finish_reshard(Shard& sh, const std::uint32_t* guard) {
   Payload& p = *sh.holding;
   Reshard& rs = *p.reshard;
   // 1) slices out of gathered source items (rows of nc bytes)
@@ -1963,7 +1995,7 @@ Status Client::finish_reshard(Shard& sh) {
       lens.push_back(c.nc | flag);
     }
   }
-  if (Status s = copy_spans(sh, srcs, dsts, lens); !ok(s)) return s;
+  if (Status s = copy_spans(sh, srcs, dsts, lens, guard); !ok(s)) return s;
   if (terminal()) return Status::ok;  // a cast copy never re-serves: nothing to pack or digest
   // 2) pack this reader's own groups (its tiny slices) for re-serving
   srcs.clear();
@@ -1980,7 +2012,7 @@ Status Client::finish_reshard(Shard& sh) {
       lens.push_back(sh.regs[mem.entry].len);
     }
   }
-  if (Status s = copy_spans(sh, srcs, dsts, lens); !ok(s)) return s;
+  if (Status s = copy_spans(sh, srcs, dsts, lens, guard); !ok(s)) return s;
   // 3) digest + release the items whose bytes arrived by copy: the groups and
   //    big items sliced out of gathered source items (own chunk table and
   //    watermarks)
@@ -1997,10 +2029,7 @@ Status Client::finish_reshard(Shard& sh) {
                  (unsigned long long)gb, rs.plan.copies.size(), (unsigned long long)cb, srcs.size(),
                  rehash.size(), (unsigned long long)rb);
   }
-  if (Status s = hash_items(sh, p, rehash); !ok(s)) return s;
-  DeviceGuard g(sh.device);
-  RS_CUDA(cudaStreamSynchronize(sh.stream));
-  return Status::ok;
+  return hash_items(sh, p, rehash, guard);
 }
 
 void Client::finish_transfers(VersionId v, bool good) {

@@ -415,10 +415,15 @@ class Client {
                 std::vector<std::uint32_t>* lens) const;
   Status alloc_tables(Shard& sh, Payload& p, std::uint32_t extra_chunks);
   Status launch_reshard_fill(Shard& sh, const Assignment& a, bool src_complete);
-  Status finish_reshard(Shard& sh);
-  Status hash_items(Shard& sh, Payload& p, const std::vector<std::uint32_t>& items);
+  // Queues the reshard's follow-up work behind its pull kernel on sh.stream
+  // (slice copies, group packing, re-digests), skipped on the device when the
+  // fill failed (guard = the fill's status code word).
+  Status finish_reshard(Shard& sh, const std::uint32_t* guard);
+  Status hash_items(Shard& sh, Payload& p, const std::vector<std::uint32_t>& items,
+                    const std::uint32_t* guard = nullptr);
   Status copy_spans(Shard& sh, const std::vector<std::uint64_t>& srcs,
-                    const std::vector<std::uint64_t>& dsts, const std::vector<std::uint64_t>& lens);
+                    const std::vector<std::uint64_t>& dsts, const std::vector<std::uint64_t>& lens,
+                    const std::uint32_t* guard = nullptr);
   Status resolve_shard(Shard& sh, const std::string& replica, std::uint32_t shard, VersionId v,
                        SourceView* out);
   void serve(Shard& sh, VersionId v, bool complete);

@@ -110,6 +110,9 @@ struct PullParams {
   // batches of sources behind different links (schedule_order).
   std::uint32_t n_sched;
   const std::uint32_t* order;
+  // Stream-ordered follow-up work: when set and *guard != 0 (the failure
+  // code of the fill this pass follows), the kernel does nothing.
+  const std::uint32_t* guard;
 };
 
 // Uploads a pull plan (segment table + source table + TMA tensor maps +
@@ -153,9 +156,11 @@ cudaError_t launch_span_digests(const std::uint64_t* ptrs, const std::uint64_t* 
 // lens[i] | kSpanCastE4M3: the span's bf16 bytes land as e4m3 (lens/2 bytes).
 constexpr std::uint64_t kSpanCastE4M3 = 1ull << 63;
 // tile0[i]: first tile (copy_span_tiles units) of span i; tiles: the total.
+// guard (may be null): skip the copy when *guard != 0 (a failed fill's code).
 cudaError_t launch_copy_spans(const std::uint64_t* srcs, const std::uint64_t* dsts,
                               const std::uint64_t* lens, const std::uint64_t* tile0, int n,
-                              std::uint64_t tiles, cudaStream_t s);
+                              std::uint64_t tiles, cudaStream_t s,
+                              const std::uint32_t* guard = nullptr);
 std::uint64_t copy_span_tiles(std::uint64_t len);  // tiles of one span (len may carry the cast flag)
 
 // Synthetic bf16 weights (SURVEY.md §8d generator; oracle ro_synth_bf16).

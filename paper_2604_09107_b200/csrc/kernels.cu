@@ -92,6 +92,7 @@ __device__ __forceinline__ void store_step(const LaneChunk* refs, const std::uin
 }
 
 __global__ void __launch_bounds__(kThreads, 2) pull_kernel(const PullParams p) {
+  if (p.guard && *reinterpret_cast<const volatile std::uint32_t*>(p.guard) != 0) return;
   extern __shared__ __align__(128) std::uint8_t smem[];
   __shared__ LaneChunk refs_all[kWarps][32];
   const int warp = threadIdx.x >> 5;
@@ -371,8 +372,10 @@ __global__ void __launch_bounds__(256) copy_spans_kernel(const std::uint64_t* sr
                                                          const std::uint64_t* dsts,
                                                          const std::uint64_t* lens,
                                                          const std::uint64_t* tile0, int n,
-                                                         std::uint64_t tiles) {
+                                                         std::uint64_t tiles,
+                                                         const std::uint32_t* guard) {
   __shared__ int span_s;
+  if (guard && *reinterpret_cast<const volatile std::uint32_t*>(guard) != 0) return;
   for (std::uint64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
     if (threadIdx.x == 0) {
       int lo = 0, hi = n;  // last span with tile0 <= t
@@ -529,13 +532,13 @@ cudaError_t launch_span_digests(const std::uint64_t* ptrs, const std::uint64_t* 
 
 cudaError_t launch_copy_spans(const std::uint64_t* srcs, const std::uint64_t* dsts,
                               const std::uint64_t* lens, const std::uint64_t* tile0, int n,
-                              std::uint64_t tiles, cudaStream_t s) {
+                              std::uint64_t tiles, cudaStream_t s, const std::uint32_t* guard) {
   if (n <= 0 || tiles == 0) return cudaSuccess;
   int dev = 0;
   cudaGetDevice(&dev);
   const std::uint64_t cap = static_cast<std::uint64_t>(pull_grid(dev)) * 8;
   const auto grid = static_cast<unsigned>(tiles < cap ? tiles : cap);
-  copy_spans_kernel<<<grid, 256, 0, s>>>(srcs, dsts, lens, tile0, n, tiles);
+  copy_spans_kernel<<<grid, 256, 0, s>>>(srcs, dsts, lens, tile0, n, tiles, guard);
   return cudaGetLastError();
 }
 

@@ -127,6 +127,7 @@ struct Cfg {
 
 template <class C>
 __global__ void __launch_bounds__(C::kThreads, C::kCtas) pull_tma_kernel(const PullParams p) {
+  if (p.guard && *reinterpret_cast<const volatile std::uint32_t*>(p.guard) != 0) return;  // follow-up of a failed fill
   using Smem = typename C::Smem;
   using Meta = typename C::Meta;
   constexpr int kP = C::kP;
