@@ -749,26 +749,14 @@ Status Client::build_payload(Shard& sh, VersionId v, std::shared_ptr<Payload>* o
     lens[i] = sh.regs[i].len;
   }
   // Early publish: the big entries (>= tiny_threshold: items of their own)
-  // are digested on sh.k6 in the background, launched first so the serial
-  // chains start at once; everything else below runs meanwhile.
+  // are digested on sh.k6 in the background (launched below, beside the
+  // chunk-table hash pass); the manifest carries 0 for them until then.
   std::vector<std::uint32_t> now, later;
   for (std::uint32_t i = 0; i < n; ++i)
     (cfg_.early_publish && lens[i] >= cfg_.limits.tiny_threshold ? later : now).push_back(i);
   if (!later.empty()) {
     if (!sh.k6) RS_CUDA(cudaStreamCreateWithFlags(&sh.k6, cudaStreamNonBlocking));
-    const std::size_t nl = later.size();
-    if (Status s = sh.k6_tables.alloc(sh.device, 3 * nl * 8); !ok(s)) return s;
-    std::vector<std::uint64_t> lp(nl), ll(nl);
-    for (std::size_t k = 0; k < nl; ++k) {
-      lp[k] = ptrs[later[k]];
-      ll[k] = lens[later[k]];
-    }
-    auto* kd = static_cast<std::uint64_t*>(sh.k6_tables.p);
-    RS_CUDA(cudaStreamWaitEvent(sh.k6, sh.ev0, 0));
-    RS_CUDA(cudaMemcpyAsync(kd, lp.data(), nl * 8, cudaMemcpyHostToDevice, sh.k6));
-    RS_CUDA(cudaMemcpyAsync(kd + nl, ll.data(), nl * 8, cudaMemcpyHostToDevice, sh.k6));
-    RS_CUDA(dev::launch_span_digests(kd, kd + nl, kd + 2 * nl, static_cast<int>(nl), sh.k6));
-    stats_.h2d_bytes += 16 * nl;
+    if (Status s = sh.k6_tables.alloc(sh.device, 3 * later.size() * 8); !ok(s)) return s;
   }
   // Library buffers of a publish are reused across publishes (a cudaFree
   // synchronizes the device and was measured taking up to 0.44 s here).
@@ -857,6 +845,24 @@ Status Client::build_payload(Shard& sh, VersionId v, std::shared_ptr<Payload>* o
   for (std::size_t i = 0; i < items.size(); ++i) all[i] = static_cast<std::uint32_t>(i);
   if (Status s = hash_items(sh, *p, all); !ok(s)) return s;
   RS_CUDA(cudaEventRecord(sh.ev1, sh.stream));
+  if (!later.empty()) {
+    // launched only now, after every allocation of this publish (the hash
+    // pass's plan included): a device allocation issued while it runs would
+    // serialise the rest behind it; it runs beside the hash pass
+    const std::size_t nl = later.size();
+    std::vector<std::uint64_t> lp(nl), ll(nl);
+    for (std::size_t k = 0; k < nl; ++k) {
+      lp[k] = ptrs[later[k]];
+      ll[k] = lens[later[k]];
+    }
+    auto* kd = static_cast<std::uint64_t*>(sh.k6_tables.p);
+    RS_CUDA(cudaStreamWaitEvent(sh.k6, sh.ev0, 0));  // behind the caller's prior work on sh.stream
+    RS_CUDA(cudaMemcpyAsync(kd, lp.data(), nl * 8, cudaMemcpyHostToDevice, sh.k6));
+    RS_CUDA(cudaMemcpyAsync(kd + nl, ll.data(), nl * 8, cudaMemcpyHostToDevice, sh.k6));
+    RS_CUDA(dev::launch_span_digests(kd, kd + nl, kd + 2 * nl, static_cast<int>(nl), sh.k6));
+    stats_.h2d_bytes += 16 * nl;
+  }
+
   RS_CUDA(cudaStreamSynchronize(sh.stream));
   float ms = 0;
   cudaEventElapsedTime(&ms, sh.ev0, sh.ev1);
