@@ -386,3 +386,45 @@ def test_early_publish_commits_the_reference_manifest_later(oracle):
         h2 = [keep[0].cpu().numpy().view(np.uint16)] + host[1:]
         assert r.manifest(0) == oracle.publish_manifest(names, h2)
         assert torch.equal(keep[0], keep[1])
+
+
+def test_ragged_sizes_and_registration_errors(fx, oracle):
+    """Sizes around every boundary the path has -- the 16-byte vector, the
+    128-byte TMA box column, the 4096-byte chunk, the 32-chunk watermark
+    batch and the 2 MiB tiny threshold -- publish and pull bit-exact, with
+    the reference's manifest and chunk table.  Registration errors follow
+    ClientCore::register_tensor (client_core.cpp:534-553)."""
+    from paper_2604_09107_b200.ros import Status
+    sizes = [1, 15, 16, 17, 127, 128, 129, 4095, 4096, 4097, 32 * 4096 - 1, 32 * 4096 + 1,
+             (2 << 20) - 1, 2 << 20, (2 << 20) + 1, (5 << 20) + 333]
+    t = fx.make("T")
+    r = fx.make("R")
+    names = [f"e{i}" for i in range(len(sizes))]
+    for i, (n, size) in enumerate(zip(names, sizes)):
+        fx.reg("T", 0, n, size, 40 + i)
+        fx.reg("R", 0, n, size, 0)
+    # the reference's registration rules
+    z = torch.zeros(4, dtype=torch.uint8, device="cuda:0")
+    assert t.register_tensor(0, "zero", ptr=z.data_ptr(), nbytes=0) == Status.invalid_argument
+    assert t.register_tensor(0, "e0", z) == Status.already_exists
+    assert t.register_tensor(0, "bad|name", z) == Status.invalid_argument
+    assert t.register_tensor(5, "x", z) == Status.invalid_argument
+    assert t.publish(1).status == Status.ok
+    assert r.replicate().status == Status.ok
+    arrays = [pattern(size, 40 + i) for i, size in enumerate(sizes)]
+    want = oracle.publish_manifest(names, arrays)
+    assert t.manifest(0) == want and r.manifest(0) == want
+    for n in names:
+        assert fx.same("T", "R", 0, n), n
+    # chunk table over the items in manifest order: big entries, then the
+    # packed group (members at their offsets) where its first member sits
+    ng, g, off = oracle.assemble(sizes)
+    items, seen = [], set()
+    for i, a in enumerate(arrays):
+        if g[i] < 0:
+            items.append(a)
+        elif g[i] not in seen:
+            seen.add(g[i])
+            items.append(np.concatenate([arrays[j] for j in range(len(arrays)) if g[j] == g[i]]))
+    assert np.array_equal(r.chunk_digests(0), oracle.chunk_digests(items, 4096))
+    assert r.stats().items_verified == len(items)
