@@ -895,7 +895,11 @@ void Client::start_finalize(VersionId v) {
   }
   if (!any) return;
   bool all_local = true;
-  for (std::uint32_t i = 0; i < num_shards_; ++i) all_local &= is_local(i);
+  std::vector<std::string> held(num_shards_);  // shards with nothing deferred: final already
+  for (std::uint32_t i = 0; i < num_shards_; ++i) {
+    all_local &= is_local(i);
+    if (!work[i] && is_local(i) && shards_[i].holding) held[i] = shards_[i].holding->encoded;
+  }
   {
     std::lock_guard lk(fin_m_);
     fin_running_ = true;
@@ -903,14 +907,12 @@ void Client::start_finalize(VersionId v) {
     fin_status_ = Status::ok;
     fin_manifests_.assign(num_shards_, std::string());
   }
-  fin_thread_ = std::thread([this, v, all_local, work = std::move(work)]() mutable {
-    std::vector<std::string> finals(num_shards_);
+  // the thread touches no Client state but the fin_ fields and the registry
+  fin_thread_ = std::thread([this, v, all_local, work = std::move(work), held = std::move(held)]() mutable {
+    std::vector<std::string> finals = std::move(held);
     Status st = Status::ok;
     for (std::uint32_t i = 0; i < num_shards_; ++i) {
-      if (!work[i]) {
-        if (is_local(i) && shards_[i].holding) finals[i] = shards_[i].holding->encoded;
-        continue;
-      }
+      if (!work[i]) continue;
       Work& w = *work[i];
       DeviceGuard g(w.device);
       std::vector<std::uint64_t> dg(w.deferred.size());
