@@ -22,8 +22,10 @@ so it can be planned onto a partially landed copy (config 4's elastic join).
 No collective and no fixed process group: unlike ``dist.DistCluster`` (the
 lock-step gloo variant), nobody waits for a member that is not there.
 
-Every replica a SharedCluster opens must have all its shards in this process
-(a TP/FSDP group spread over processes uses ``dist.DistCluster``).
+A replica's shards may live in several member processes (a TP/FSDP group):
+each process appends its shards' part of every replica operation and the
+registry replicas apply the operation once all parts are in the log -- the
+reference server's group transactions, with an abort entry for stragglers.
 """
 from __future__ import annotations
 
@@ -106,6 +108,8 @@ class SharedCluster:
         self.applied = 0
         self._rc = {}        # seq -> status code of this member's own ops
         self._txn = {}       # id(handle) -> (version, changed) between replicate_start/finish
+        self._txns = {}      # group transactions (applied by the follower)
+        self._ctr = {}       # (model, replica, kind) -> operations issued
         self._stop = False
         self._err = None
         self._t = threading.Thread(target=self._follow, daemon=True)
@@ -132,6 +136,13 @@ class SharedCluster:
     def _apply(self, origin, op) -> int:
         kind = op[0]
         if kind == "noop":
+            return 0
+        if kind == "part":
+            return self._part(op)
+        if kind == "txn_abort":
+            t = self._txns.setdefault(op[1], {"n": 0, "parts": {}, "meta": {}, "state": "pending", "rc": None})
+            if t["state"] == "pending":
+                t["state"], t["rc"] = "aborted", int(Status.group_aborted)
             return 0
         if kind == "import":  # serve states another member announces
             if origin != self.me:
@@ -195,48 +206,140 @@ class SharedCluster:
     def _source(self, model, replica) -> str:
         return _read_bytes(lib.rs_cluster_source, self.local.h, _b(model), _b(replica)).decode()
 
+    # ---- group transactions ------------------------------------------------------
+    # A replica's shards may live in several member processes (a TP/FSDP
+    # group, one process per GPU).  Like the reference server joining
+    # per-shard requests into one group transaction (txn_arrive /
+    # maybe_start_txn, server_core.cpp:298-591), each member appends its
+    # shards' part of a replica operation; every registry replica applies the
+    # operation once the parts of all shards are in the log (the same entry
+    # everywhere, so the same plan).  A member that waits too long appends
+    # an abort; whichever of the last part or the abort comes first in the
+    # log decides, and an aborted transaction answers group_aborted.  Members
+    # of a replica issue its operations in the same order
+    # (ClientConfig.first_shard/group_shards, config.hpp:28-33).
+    def _txn_key(self, h: Handle, kind: str):
+        k = (h.model, h.replica, kind)
+        c = self._ctr.get(k, 0)
+        self._ctr[k] = c + 1
+        return (h.model, h.replica, kind, c)
+
+    def _part(self, op) -> int:
+        _, key, n, parts, meta = op
+        t = self._txns.setdefault(key, {"n": n, "parts": {}, "meta": {}, "state": "pending", "rc": None})
+        if t["state"] != "pending":
+            return t["rc"] if t["state"] == "done" else int(Status.group_aborted)
+        t["parts"].update(parts)
+        for k, v in meta.items():  # per-member extras (retention lags, provisional)
+            if isinstance(v, list):
+                t["meta"][k] = sorted(set(t["meta"].get(k, [])) | set(v))
+            elif isinstance(v, bool):
+                t["meta"][k] = t["meta"].get(k, False) or v
+            else:
+                t["meta"][k] = v
+        if sorted(t["parts"]) == list(range(n)):
+            t["rc"] = self._start_txn(key, t)
+            t["state"] = "done"
+        return 0
+
+    def _start_txn(self, key, t) -> int:
+        m, r, kind = key[0], key[1], key[2]
+        n, parts, meta = t["n"], t["parts"], t["meta"]
+        c = self.local.h
+        if kind == "open":
+            eps = [parts[i]["ep"] for i in range(n)]
+            lk = combine_layout_key([parts[i]["hash"] for i in range(n)])
+            geo = any(parts[i]["hash"][1] for i in range(n))
+            dman = [parts[i]["dm"] for i in range(n)] if geo else []
+            dlay = [parts[i]["dl"] for i in range(n)] if geo else []
+            rc = apply_op(c, ("open", m, r, n, meta["dc"], eps, lk, dman, dlay))
+            if rc == 0 and meta.get("retain"):
+                rc = apply_op(c, ("retain", m, r, list(meta["retain"])))
+            return rc
+        if kind == "publish":
+            return apply_op(c, ("publish", m, r, meta["v"], [parts[i][0] for i in range(n)],
+                                [parts[i][1] for i in range(n)], meta.get("prov", False)))
+        if kind == "finalize":
+            return apply_op(c, ("finalize", m, r, meta["v"], [parts[i] for i in range(n)]))
+        if kind == "replicate":
+            if meta["update"]:
+                return apply_op(c, ("update", m, r, meta["spec"], meta["cur"]))
+            return apply_op(c, ("replicate", m, r, meta["spec"]))
+        if kind == "unpublish":
+            return apply_op(c, ("unpublish", m, r))
+        if kind == "close":
+            return apply_op(c, ("close", m, r))
+        raise ValueError(kind)
+
+    def _group(self, h: Handle, kind: str, parts: dict, meta: dict, timeout: float = 120.0,
+               key=None) -> int:
+        """Appends this member's part of a replica operation; returns its
+        status once the group transaction started (or group_aborted)."""
+        return self.group_op(key or self._txn_key(h, kind), h.num_shards, parts, meta, timeout)
+
+    def group_op(self, key, n: int, parts: dict, meta: dict, timeout: float = 120.0) -> int:
+        """One member's part (shard -> payload) of the group transaction
+        `key` = (model, replica, kind, k) over n shards."""
+        self._w.append(pickle.dumps((self.me, ("part", key, n, parts, meta))))
+        state = lambda: self._txns.get(key, {}).get("state")  # noqa: E731
+        if not self._wait(lambda: state() in ("done", "aborted"), timeout):
+            self._w.append(pickle.dumps((self.me, ("txn_abort", key))))
+            self._wait(lambda: state() in ("done", "aborted"), timeout)
+        with self._cv:
+            t = self._txns[key]
+            return int(t["rc"]) if t["state"] == "done" else int(Status.group_aborted)
+
     # ---- ops -------------------------------------------------------------------
     def create(self, model: str, replica: str, num_shards: int = 1, **cfg) -> Handle:
         """Local: a handle to register tensors on, before open()."""
         return self.local.open(model, replica, num_shards, **cfg)
 
-    def open(self, h: Handle, endpoints=None, datacenter: str = "dc0") -> None:
+    def open(self, h: Handle, endpoints=None, datacenter: str = "dc0", timeout: float = 120.0) -> None:
         """Announces the replica (ClientCore::open): endpoints, slicing key,
-        derived manifests of a resharding replica, retention rule."""
-        n = h.num_shards
-        if h.local_shards() != list(range(n)):
-            raise ValueError(f"{h.replica}: every shard must be registered in this process")
-        eps = list(endpoints) if endpoints is not None else [f"{self.me}:{s}" for s in range(n)]
-        for s, e in enumerate(eps):
-            h.set_endpoint(s, e)
-        hashes = [h.shard_hash(s) for s in range(n)]
-        key = combine_layout_key(hashes)
-        geo = any(x[1] for x in hashes)
-        dman = [h.derived(s, 0) for s in range(n)] if geo else []
-        dlay = [h.derived(s, 1) for s in range(n)] if geo else []
-        rc = self.op(("open", h.model, h.replica, n, datacenter, eps, key, dman, dlay))
+        derived manifests of a resharding replica, retention rule -- the
+        shards this process holds; the replica opens once every shard's
+        part is in."""
+        loc = h.local_shards()
+        if not loc:
+            raise ValueError(f"{h.replica}: no shard registered in this process")
+        if endpoints is None:
+            eps = {s: f"{self.me}:{s}" for s in loc}
+        elif isinstance(endpoints, dict):
+            eps = dict(endpoints)
+        else:
+            eps = dict(zip(loc, endpoints))
+        parts = {}
+        for sh in loc:
+            h.set_endpoint(sh, eps[sh])
+            hs = h.shard_hash(sh)
+            parts[sh] = {"ep": eps[sh], "hash": hs,
+                         "dm": h.derived(sh, 0) if hs[1] else b"", "dl": h.derived(sh, 1) if hs[1] else b""}
+        meta = {"dc": datacenter, "retain": list(getattr(h, "retain", []) or [])}
+        rc = self._group(h, "open", parts, meta, timeout)
         if rc:
             raise RuntimeError(f"open {h.replica}: {Status(rc).name}")
-        if getattr(h, "retain", None):
-            self.op(("retain", h.model, h.replica, list(h.retain)))
 
-    def publish(self, h: Handle, version: int) -> OpResult:
-        """publish(); with early_publish the provisional manifests go in at
-        once and a background thread appends the final ones ("finalize")
-        when the big-entry digests are done."""
+    def publish(self, h: Handle, version: int, timeout: float = 120.0) -> OpResult:
+        """publish() of this process's shards (a group transaction over the
+        replica's shards).  With early_publish the provisional manifests go
+        in at once and a background thread appends the final ones (a
+        "finalize" transaction) when the big-entry digests are done."""
         check(lib.rs_prepare_publish(h.h, version), "rs_prepare_publish")
-        n = h.num_shards
+        loc = h.local_shards()
         early = h.publish_pending
-        rc = self.op(("publish", h.model, h.replica, version, [lib_manifest(h, s) for s in range(n)],
-                      [h.layout(s) for s in range(n)], early))
+        parts = {s: (lib_manifest(h, s), h.layout(s)) for s in loc}
+        rc = self._group(h, "publish", parts, {"v": version, "prov": early}, timeout)
         lib.rs_commit_publish(h.h, version, rc)
         if rc == 0:
-            self.announce([h.serve_export(s) for s in range(n)])
+            self.announce([h.serve_export(s) for s in loc])
             if early:
+                key = (h.model, h.replica, "finalize", version)
+
                 def fin():
                     if lib.rs_publish_finalize(h.h, 60.0) == 0:
-                        self._w2.append(pickle.dumps((self.me, ("finalize", h.model, h.replica, version,
-                                                                [h.manifest(s) for s in range(n)]))))
+                        part = {s: h.manifest(s) for s in loc}
+                        self._w2.append(pickle.dumps((self.me, ("part", key, h.num_shards, part,
+                                                                {"v": version}))))
                 self._fin = threading.Thread(target=fin, daemon=True)
                 self._fin.start()
         st = Status(rc)
@@ -252,26 +355,27 @@ class SharedCluster:
         v = C.c_uint64()
         if not lib.rs_server_offload_pending(self.local.h, _b(h.model), _b(h.replica), C.byref(v)):
             return
+        loc = h.local_shards()
         good = lib.rs_offload_lanes(h.h, v.value) == 0
-        blobs = [_read_bytes(lib.rs_lane_export, h.h, s, v.value) for s in range(h.num_shards)] if good else []
+        blobs = [_read_bytes(lib.rs_lane_export, h.h, s, v.value) for s in loc] if good else []
         self.announce(blobs)
-        for s in range(h.num_shards):
+        for s in loc:
             self.op(("offload_confirm", h.model, h.replica, s, v.value, good, f"host:{h.replica}:{s}"))
 
-    def unpublish(self, h: Handle) -> OpResult:
+    def unpublish(self, h: Handle, timeout: float = 120.0) -> OpResult:
         self.finalized(h)  # an early publish's digests still read the regions
-        rc = self.op(("unpublish", h.model, h.replica))
+        rc = self._group(h, "unpublish", {s: None for s in h.local_shards()}, {}, timeout)
         self._offload_first(h)
         done, s, _, _ = self.result(h.model, h.replica)
         return OpResult(Status(rc) if rc else (s if done else Status.timeout))
 
     def replicate(self, h: Handle, spec: str = "latest", update: bool = False, wait_s: float = 60.0,
                   max_rounds: int = 8) -> OpResult:
-        """ClientCore::replicate / update for this member's replica: plan
-        (through the log), bind and announce the serve state (downstream
-        members may chase it at once), fill -- reporting failures through the
-        log and refilling from the re-picked source -- and complete.
-        = replicate_start + replicate_finish."""
+        """ClientCore::replicate / update for this member's shards of the
+        replica: plan (a group transaction through the log), bind and
+        announce the serve state (downstream members may chase it at once),
+        fill -- reporting failures through the log and refilling from the
+        re-picked source -- and complete.  = replicate_start + replicate_finish."""
         early = self.replicate_start(h, spec, update, wait_s)
         if early is not None:
             return early
@@ -283,8 +387,9 @@ class SharedCluster:
         Returns the outcome when there is nothing to fill (failure, parked
         timeout, update without change), else None: call replicate_finish."""
         cur = h.current_version
-        rc = self.op(("update", h.model, h.replica, spec, cur) if update else
-                     ("replicate", h.model, h.replica, spec))
+        loc = h.local_shards()
+        rc = self._group(h, "replicate", {s: None for s in loc},
+                         {"spec": spec, "update": update, "cur": cur}, wait_s)
         if rc:
             return OpResult(Status(rc))
         self._offload_first(h)
@@ -296,26 +401,27 @@ class SharedCluster:
             return OpResult(s)
         if update and not ch:
             return OpResult(Status.ok, v or cur, False)
-        n = h.num_shards
         rc = lib.rs_transfer_bind(h.h, v)
         if rc:
-            for i in range(n):
+            for i in loc:
                 self.op(("complete", h.model, h.replica, i, rc))
             lib.rs_transfer_finish(h.h, v, 0)
             return OpResult(Status(rc))
-        self.announce([h.serve_export(i) for i in range(n)])
+        self.announce([h.serve_export(i) for i in loc])
         self._txn[id(h)] = (v, ch or not update)
         return None
 
-    def replicate_finish(self, h: Handle, max_rounds: int = 8) -> OpResult:
-        """Second half: fill (launch + wait), failure reports, completion."""
+    def replicate_finish(self, h: Handle, max_rounds: int = 8, wait_s: float = 120.0) -> OpResult:
+        """Second half: fill this process's shards (launch + wait), failure
+        reports, completion; the outcome is the replica's (all shards)."""
         v, changed = self._txn.pop(id(h))
         n = h.num_shards
+        loc = h.local_shards()
         final = None
         for _ in range(max_rounds):
             sts, rsn = (C.c_int * n)(), (C.c_int * n)()
             lib.rs_transfer_fill(h.h, C.cast(sts, C.c_void_p), C.cast(rsn, C.c_void_p))
-            failed = {i: (int(sts[i]), int(rsn[i])) for i in range(n) if sts[i] != 0}
+            failed = {i: (int(sts[i]), int(rsn[i])) for i in loc if sts[i] != 0}
             if not failed:
                 final = Status.ok
                 break
@@ -328,15 +434,23 @@ class SharedCluster:
                 break
         if final is None:
             final = Status.transfer_failed
-        lib.rs_transfer_finish(h.h, v, int(final == Status.ok))
-        for i in range(n):
+        for i in loc:
             self.op(("complete", h.model, h.replica, i, int(final)))
+        if final == Status.ok and len(loc) < n:
+            # the replica is published only when every process's shards are
+            self._wait(lambda: (self.local.view(h.model, h.replica) or {}).get("lifecycle") != "replicating",
+                       wait_s)
+            life = (self.local.view(h.model, h.replica) or {}).get("lifecycle")
+            if life != "published":
+                final = Status.transfer_failed
+        lib.rs_transfer_finish(h.h, v, int(final == Status.ok))
         return OpResult(final, v if final == Status.ok else None, changed)
 
     def update(self, h: Handle, spec: str = "latest", wait_s: float = 60.0) -> OpResult:
         return self.replicate(h, spec, update=True, wait_s=wait_s)
 
     def leave(self, h: Handle) -> None:
-        """ClientCore::close: the replica leaves the deployment."""
-        self.op(("close", h.model, h.replica))
+        """ClientCore::close: the replica leaves the deployment (once every
+        process holding its shards left)."""
+        self._group(h, "close", {s: None for s in h.local_shards()}, {})
         h.close()

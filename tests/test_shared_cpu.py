@@ -135,3 +135,90 @@ def test_log_replays_in_order_for_a_member_that_starts_last():
     finally:
         a.close()
         log.close()
+
+
+def _tp2_part(shard, port, q, go):
+    """One process of a TP-2 trainer group: its shard's parts of open and publish."""
+    import sys
+    sys.path.insert(0, ROOT)
+    try:
+        from paper_2604_09107_b200.shared import SharedCluster
+        sc = SharedCluster("127.0.0.1", port)
+        go.wait(60)
+        part = {shard: {"ep": f"ep:T:{shard}", "hash": (0, False, False), "dm": b"", "dl": b""}}
+        rc_open = sc.group_op(("m", "T", "open", 0), 2, part, {"dc": "dc0", "retain": []}, 30)
+        rc_pub = sc.group_op(("m", "T", "publish", 0), 2, {shard: (_manifest(), b"")},
+                             {"v": 1, "prov": False}, 30)
+        sc.sync()
+        q.put((shard, {"open": rc_open, "publish": rc_pub,
+                       "listing": {v: sorted(r) for v, r in sc.listing("m").items()}}))
+        go.wait(60)
+        sc.close()
+    except Exception as e:  # pragma: no cover
+        import traceback
+        q.put((shard, {"error": repr(e) + traceback.format_exc()}))
+
+
+def test_group_transaction_joins_shards_from_two_processes():
+    """server_core.cpp:298-591: the per-shard requests of a replica whose
+    shards live in two processes join into one transaction; the replica
+    opens and publishes once both parts are in, and a reader is then planned
+    with a per-shard endpoint from each process (test_server_core.cpp:342-364)."""
+    from paper_2604_09107_b200.shared import LogServer, SharedCluster
+    log = LogServer()
+    sc = SharedCluster("127.0.0.1", log.port)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    go = ctx.Event()
+    ps = [ctx.Process(target=_tp2_part, args=(s, log.port, q, go)) for s in range(2)]
+    try:
+        for p in ps:
+            p.start()
+        go.set()
+        res = dict(q.get(timeout=120) for _ in range(2))
+        for s in range(2):
+            assert "error" not in res[s], res[s]
+            assert res[s]["open"] == 0 and res[s]["publish"] == 0, res[s]
+            assert res[s]["listing"] == {1: ["T"]}
+        sc.sync()
+        assert sc.op(("open", "m", "R", 2, "dc0", ["ep:R:0", "ep:R:1"], "", [], [])) == 0
+        assert sc.op(("replicate", "m", "R", "latest")) == 0
+        eps = [sc.local.locate("m", "R", "latest", s)["source_endpoint"] for s in range(2)]
+        assert eps == ["ep:T:0", "ep:T:1"]
+    finally:
+        for p in ps:
+            p.join(timeout=30)
+        sc.close()
+        log.close()
+
+
+def test_straggler_aborts_the_group_transaction():
+    """A part that never arrives: the waiting member's abort entry wins the
+    log order and every replica answers group_aborted; a part arriving after
+    the abort changes nothing, and the next transaction starts clean."""
+    from paper_2604_09107_b200.shared import LogServer, SharedCluster
+    log = LogServer()
+    a = SharedCluster("127.0.0.1", log.port)
+    b = SharedCluster("127.0.0.1", log.port)
+    try:
+        part = lambda s: {s: {"ep": f"ep:T:{s}", "hash": (0, False, False), "dm": b"", "dl": b""}}  # noqa: E731
+        key = ("m", "T", "open", 0)
+        assert a.group_op(key, 2, part(0), {"dc": "dc0", "retain": []}, timeout=0.5) == 9  # group_aborted
+        assert b.group_op(key, 2, part(1), {"dc": "dc0", "retain": []}, timeout=5) == 9
+        b.sync()
+        assert b.local.view("m", "T") is None and a.local.view("m", "T") is None
+        key2 = ("m", "T", "open", 1)
+        import threading
+        out = {}
+        th = threading.Thread(target=lambda: out.setdefault(
+            "a", a.group_op(key2, 2, part(0), {"dc": "dc0", "retain": []}, timeout=30)))
+        th.start()
+        out["b"] = b.group_op(key2, 2, part(1), {"dc": "dc0", "retain": []}, timeout=30)
+        th.join()
+        assert out == {"a": 0, "b": 0}
+        a.sync()
+        assert a.local.view("m", "T")["lifecycle"] == "registered"
+    finally:
+        a.close()
+        b.close()
+        log.close()

@@ -165,3 +165,117 @@ def test_reader_process_joins_mid_fill_through_the_op_log():
         joined.set()
         for p in procs:
             p.join(timeout=60)
+
+
+def _group_member(rank, port, q):
+    """Process `rank` of a TP-2 trainer group (trainer shard = rank) that also
+    holds shard (rank + 1) % 2 of a TP-2 reader replica; process 0 also holds
+    a TP-1 reader that reshards from both trainer shards.  Every replica
+    operation is a group transaction through the op log."""
+    import hashlib
+    import sys
+    sys.path.insert(0, ROOT)
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import torch
+
+    from paper_2604_09107_b200 import ros
+    from paper_2604_09107_b200.ros import Status, tp_slice
+    from paper_2604_09107_b200.shared import SharedCluster
+    from tests.test_cast import _tensors
+    from tests.test_reshard import numel
+    try:
+        gpu = rank % torch.cuda.device_count()
+        torch.cuda.set_device(gpu)
+        dev = torch.device("cuda", gpu)
+        sc = SharedCluster("127.0.0.1", port)
+        tiny = 64 << 10
+        tensors = _tensors()
+        full = {}
+        for i, (n, shape, _) in enumerate(tensors):  # every process builds the same bytes
+            t = torch.empty(numel(shape) * 2, dtype=torch.uint8, device=dev)
+            ros.synth_bf16(t, 700 + i)
+            full[n] = t
+
+        def piece(n, geo):
+            rows, w, r0, nr, c0, nc = geo
+            return full[n].view(rows, w)[r0:r0 + nr, c0:c0 + nc].contiguous().view(-1)
+
+        t = sc.create("m", "trainer", 2, tiny_threshold=tiny, early_publish=True)
+        keep = []
+        for n, shape, dim in tensors:
+            geo = tp_slice(shape, 2, dim, 2, rank)
+            keep.append(piece(n, geo))
+            assert t.register_slice(rank, n, keep[-1], geo) == Status.ok
+        sc.open(t, endpoints={rank: f"p{rank}:cuda{gpu}"})
+        s = (rank + 1) % 2
+        r = sc.create("m", "tp2", 2, tiny_threshold=tiny)
+        rb = {}
+        for n, shape, dim in tensors:
+            geo = tp_slice(shape, 2, dim, 2, s)
+            rb[n] = torch.zeros(geo[3] * geo[5], dtype=torch.uint8, device=dev)
+            assert r.register_slice(s, n, rb[n], geo) == Status.ok
+        sc.open(r, endpoints={s: f"p{rank}:cuda{gpu}"})
+        out = {"publish": int(sc.publish(t, 1).status)}
+        out["tp2"] = int(sc.replicate(r).status)
+        if rank == 0:
+            u = sc.create("m", "tp1", 1, tiny_threshold=tiny)
+            ub = {}
+            for n, shape, _ in tensors:
+                ub[n] = torch.zeros_like(full[n])
+                assert u.register_slice(0, n, ub[n], tp_slice(shape, 2, None, 1, 0)) == Status.ok
+            sc.open(u)
+            out["tp1"] = int(sc.replicate(u).status)
+        torch.cuda.synchronize()
+        bad = []
+        for n, shape, dim in tensors:
+            if not torch.equal(rb[n], piece(n, tp_slice(shape, 2, dim, 2, s))):
+                bad.append(("tp2", n))
+            if rank == 0 and not torch.equal(ub[n], full[n]):
+                bad.append(("tp1", n))
+        out["bad"] = bad
+        out["t_manifest"] = hashlib.sha256(t.manifest(rank)).hexdigest()  # final bytes (early publish)
+        out["r_manifest"] = hashlib.sha256(r.manifest(s)).hexdigest()
+        out["plan"] = sorted({(a.replica, a.src) for a in sc.assigns()})
+        q.put((rank, out))
+        sc.finalized(t)
+        import time
+        time.sleep(1.0)  # let the other member read what it needs before this one leaves
+        sc.close()
+    except Exception as e:  # pragma: no cover - surfaced by the parent
+        import traceback
+        q.put((rank, {"error": repr(e) + traceback.format_exc()}))
+
+
+def test_tp_group_split_over_processes_via_group_transactions():
+    """A TP-2 trainer and a TP-2 reader whose shards live in two processes,
+    plus a TP-1 reader resharding from both: open, publish (early) and
+    replicate are group transactions in the op log (no gloo, no collective).
+    Bytes equal the numpy slices; each reader shard's manifest is the
+    trainer shard's final one."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import multiprocessing as mp
+    from paper_2604_09107_b200.shared import LogServer
+    log = LogServer()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    ps = [ctx.Process(target=_group_member, args=(r, log.port, q)) for r in range(2)]
+    try:
+        for p in ps:
+            p.start()
+        res = dict(q.get(timeout=300) for _ in range(2))
+        for r in range(2):
+            assert "error" not in res[r], res[r].get("error")
+            o = res[r]
+            assert o["publish"] == 0 and o["tp2"] == 0, o
+            assert o["bad"] == [], o["bad"]
+        assert res[0]["tp1"] == 0
+        # the reader shard s holds trainer shard s's bytes: the same manifest
+        assert res[0]["r_manifest"] == res[1]["t_manifest"]
+        assert res[1]["r_manifest"] == res[0]["t_manifest"]
+        plan = dict(res[0]["plan"])
+        assert plan["tp2"] == "trainer" and plan["tp1"] in ("trainer", "tp2"), plan
+    finally:
+        for p in ps:
+            p.join(timeout=60)
+        log.close()
