@@ -969,12 +969,11 @@ Status Client::adopt_final(Shard& sh, double wait_s) {
   if (!sh.holding->deferred.empty()) return join_finalize();  // this publisher's own digests
   const std::optional<VersionId> v = current_ ? current_ : sh.partial_version;
   if (!v) return Status::not_found;
-  const std::string key = layout_key();
   auto deadline = std::chrono::steady_clock::now() + std::chrono::duration<double>(wait_s);
   for (;;) {
     std::string bytes;
     bool fin = false;
-    if (Status s = reg_->current_manifest(model_, *v, key, sh.idx, &bytes, &fin); !ok(s)) return s;
+    if (Status s = reg_->replica_manifest(model_, replica_, *v, sh.idx, &bytes, &fin); !ok(s)) return s;
     if (fin) {
       auto m = Manifest::decode(bytes);
       if (!m || !m->same_structure(sh.holding->manifest)) return Status::manifest_conflict;

@@ -329,6 +329,18 @@ Status Registry::current_manifest(const std::string& model, VersionId v, const s
   return Status::ok;
 }
 
+Status Registry::replica_manifest(const std::string& model, const std::string& replica, VersionId v,
+                                  std::uint32_t shard, std::string* bytes, bool* final_bytes) {
+  std::string key;
+  {
+    std::lock_guard lk(mu_);
+    Rep* r = find(model, replica);
+    if (!r) return Status::not_found;
+    key = r->layout;
+  }
+  return current_manifest(model, v, key, shard, bytes, final_bytes);
+}
+
 Status Registry::add_layout(const std::string& model, VersionId v, const std::string& key,
                             const std::vector<std::string>& manifests,
                             const std::vector<std::string>& layouts) {

@@ -169,6 +169,10 @@ class Registry {
   // they are final (not an early publish still digesting).
   Status current_manifest(const std::string& model, VersionId v, const std::string& layout_key,
                           std::uint32_t shard, std::string* bytes, bool* final_bytes);
+  // The same, for the slicing `replica` was opened with (a replica whose
+  // shards live in several processes has its key only in the registry).
+  Status replica_manifest(const std::string& model, const std::string& replica, VersionId v,
+                          std::uint32_t shard, std::string* bytes, bool* final_bytes);
   // A resharding reader registers the derived manifests/layouts of its own
   // slicing so readers of the same slicing can later pull from it.
   Status add_layout(const std::string& model, VersionId v, const std::string& layout_key,
