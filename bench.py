@@ -166,7 +166,7 @@ def measured_peaks() -> dict:
     return {"hbm_gbs": 6650.0, "src": "fallback"}
 
 
-def ncu_traffic(kind: str, user_bytes: int = 0):
+def ncu_traffic(kind: str, user_bytes: int = 0, workload: str = None):
     """Per-launch bytes of the pull kernel from the committed ncu captures:
     DRAM bytes for a local pull ("local", "cast"); for a peer pull ("nvlink")
     the bytes the reader's NVLink port receives (user data + read-response
@@ -180,7 +180,10 @@ def ncu_traffic(kind: str, user_bytes: int = 0):
         if kind == "nvlink":
             r = d.get("nvlink", {}).get("link_rx_bytes_per_user_byte")
             return round(r * user_bytes) if r and user_bytes else None
-        return d.get(kind, {}).get("dram_bytes_per_launch")
+        e = d.get(kind, {})
+        if workload is not None and e.get("workload") not in (None, workload):
+            return None  # captured on another workload
+        return e.get("dram_bytes_per_launch")
     except (OSError, ValueError):
         return None
 
@@ -559,7 +562,9 @@ def run_single(args):
         "publish_final_s": round(publish_final_s, 4), "early_publish": args.early_publish,
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peaks["hbm_gbs"],
                      "unit": "GB/s", "frac": round(achieved / peaks["hbm_gbs"], 4),
-                     "traffic": ncu_traffic("cast" if cast else "local") if not reshard else None,
+                     "traffic": ncu_traffic("reshard" if reshard else "cast" if cast else "local",
+                                            workload=args.workload)
+                     if args.reshard in ("none", "fsdp_tp2") else None,
                      "peak_src": peaks["src"],
                      "kernel": "pull_tma_kernel",
                      "kernel_ms_avg": round(fill_avg if reshard else k_avg, 3),
