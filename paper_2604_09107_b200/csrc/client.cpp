@@ -599,6 +599,7 @@ Client::~Client() {
     }
     dev::free_pull_plan(sh.device, &sh.plan);
     dev::free_pull_plan(sh.device, &sh.hash_plan);
+    dev::free_pull_plan(sh.device, &sh.fuse_plan);
   }
 }
 
@@ -1985,9 +1986,58 @@ Status Client::finish_reshard(Shard& sh, const std::uint32_t* guard) {
   std::map<std::pair<std::uint32_t, std::uint32_t>, std::size_t> gidx;
   for (std::size_t gi = 0; gi < rs.plan.gathers.size(); ++gi)
     gidx[{rs.plan.gathers[gi].src_shard, rs.plan.gathers[gi].src_item}] = gi;
+  const auto& items = p.manifest.items();
+  // A re-digested big item filled entirely by contiguous, chunk-aligned
+  // copies is landed by one more pull pass instead (staging -> region,
+  // digests computed on the way, watermarks released): one read and one
+  // write of its bytes instead of a copy plus a hash pass re-reading them.
+  std::vector<dev::ItemDesc> fused;
+  std::set<std::uint32_t> fused_items;
+  if (!terminal()) {
+    std::map<std::uint64_t, std::uint32_t> by_ptr;  // region address -> reader big item
+    for (std::uint32_t i : rs.plan.rehash) by_ptr[p.item_ptrs[i]] = i;
+    std::map<std::uint32_t, std::vector<std::pair<std::uint64_t, std::uint64_t>>> cover;  // item -> [off, end)
+    std::set<std::uint32_t> bad;
+    for (const auto& c : rs.plan.copies) {
+      auto it = by_ptr.upper_bound(c.dst);
+      if (it == by_ptr.begin()) continue;
+      --it;
+      const std::uint32_t i = it->second;
+      const std::uint64_t off = c.dst - it->first, len = c.rows * c.nc, cl = p.cmap.chunk_len[i];
+      if (off >= items[i].length) continue;
+      const bool contiguous = c.src_stride == c.nc && c.dst_stride == c.nc && !c.cast;
+      if (!contiguous || off % cl || (len % cl && off + len != items[i].length)) bad.insert(i);
+      cover[i].emplace_back(off, off + len);
+    }
+    for (auto& [i, v] : cover) {
+      if (bad.count(i)) continue;
+      std::sort(v.begin(), v.end());
+      std::uint64_t at = 0;
+      for (const auto& [a, b] : v) at = a == at ? b : ~0ull;
+      if (at == items[i].length) fused_items.insert(i);  // copies cover the item exactly
+    }
+  }
   std::vector<std::uint64_t> srcs, dsts, lens;
   for (const auto& c : rs.plan.copies) {
     const auto base = reinterpret_cast<std::uint64_t>(rs.gather_bufs[gidx.at({c.src_shard, c.src_item})]->p);
+    if (!fused_items.empty()) {
+      auto it = std::find_if(fused_items.begin(), fused_items.end(), [&](std::uint32_t i) {
+        return c.dst >= p.item_ptrs[i] && c.dst < p.item_ptrs[i] + items[i].length;
+      });
+      if (it != fused_items.end()) {
+        const std::uint32_t i = *it;
+        const std::uint64_t off = c.dst - p.item_ptrs[i], cl = p.cmap.chunk_len[i];
+        dev::ItemDesc d{};
+        d.src = base + c.src_off;
+        d.dst = c.dst;
+        d.len = c.rows * c.nc;
+        d.chunk0 = p.cmap.chunk0[i] + static_cast<std::uint32_t>(off / cl);
+        d.chunk_len = static_cast<std::uint32_t>(cl);
+        d.q = d.m = 1;
+        fused.push_back(d);
+        continue;
+      }
+    }
     const std::uint64_t flag = c.cast ? dev::kSpanCastE4M3 : 0;
     if (c.src_stride == c.nc && c.dst_stride * (c.cast ? 2 : 1) == c.nc) {
       // whole rows on both sides: one contiguous span
@@ -2009,7 +2059,6 @@ Status Client::finish_reshard(Shard& sh, const std::uint32_t* guard) {
   dsts.clear();
   lens.clear();
   std::vector<std::uint32_t> group_items;
-  const auto& items = p.manifest.items();
   for (std::uint32_t i = 0; i < items.size(); ++i) {
     if (!items[i].is_group) continue;
     group_items.push_back(i);
@@ -2024,17 +2073,35 @@ Status Client::finish_reshard(Shard& sh, const std::uint32_t* guard) {
   //    big items sliced out of gathered source items (own chunk table and
   //    watermarks)
   std::vector<std::uint32_t> rehash = group_items;
-  rehash.insert(rehash.end(), rs.plan.rehash.begin(), rs.plan.rehash.end());
+  for (std::uint32_t i : rs.plan.rehash)
+    if (!fused_items.count(i)) rehash.push_back(i);
   std::sort(rehash.begin(), rehash.end());
+  if (!fused.empty()) {
+    std::sort(fused.begin(), fused.end(),
+              [](const dev::ItemDesc& a, const dev::ItemDesc& b) { return a.chunk0 < b.chunk0; });
+    DeviceGuard g(sh.device);
+    const dev::SrcDesc staging{nullptr, nullptr, 0, 0};  // verified when gathered: compute only
+    dev::PullParams pp{};
+    RS_CUDA(dev::upload_pull_plan(sh.device, sh.stream, fused.data(), static_cast<std::uint32_t>(fused.size()),
+                                  &staging, 1, p.cmap.n_chunks(), &sh.fuse_plan, &pp));
+    stats_.h2d_bytes += sh.fuse_plan.h2d_bytes;
+    pp.first_batch = fused.front().chunk0 / dev::kBatchChunks;
+    pp.dst_digests = static_cast<std::uint64_t*>(p.digests.p);
+    pp.dst_flags = static_cast<std::uint32_t*>(p.flags.p);
+    pp.dst_epoch = p.epoch;
+    pp.timeout_ns = static_cast<std::uint64_t>(cfg_.pull_timeout_s * 1e9);
+    pp.guard = guard;
+    RS_CUDA(dev::launch_pull(pp, grid(sh), sh.stream));
+  }
   if (std::getenv("RSB_TIMING")) {
     std::uint64_t gb = 0, cb = 0, rb = 0;
     for (const auto& gbuf : rs.gather_bufs) gb += gbuf->n;
     for (const auto& c : rs.plan.copies) cb += c.rows * c.nc;
     for (auto i : rehash) rb += items[i].length;
     std::fprintf(stderr, "[rsb] finish_reshard shard %u: %zu gathers (%llu B), %zu copies (%llu B), "
-                 "%zu group spans, %zu rehash items (%llu B)\n", sh.idx, rs.gather_bufs.size(),
-                 (unsigned long long)gb, rs.plan.copies.size(), (unsigned long long)cb, srcs.size(),
-                 rehash.size(), (unsigned long long)rb);
+                 "%zu group spans, %zu rehash items (%llu B), %zu items landed by copy-hash segments\n",
+                 sh.idx, rs.gather_bufs.size(), (unsigned long long)gb, rs.plan.copies.size(),
+                 (unsigned long long)cb, srcs.size(), rehash.size(), (unsigned long long)rb, fused_items.size());
   }
   return hash_items(sh, p, rehash, guard);
 }

@@ -370,6 +370,7 @@ class Client {
     dev::PlanUpload plan;       // fill: item table + tensor maps + work/status words
     dev::PlanUpload hash_plan;  // hash-only passes (publish, reshard groups): kept apart so
                                 // the fill plan stays resident between fills
+    dev::PlanUpload fuse_plan;  // reshard: staging -> region copy-hash pass
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     std::chrono::steady_clock::time_point t_launch;  // host clock of the fill's launch
     cudaStream_t poll = nullptr;  // progress reads while a fill runs
