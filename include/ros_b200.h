@@ -83,6 +83,7 @@ typedef struct {
   float fill_max_ms;        /* last fill round: the slowest local shard's kernel   */
   float fill_sum_ms;        /* last fill round: all local shards' kernels, summed  */
   uint64_t fill_bytes;      /* last fill round: bytes landed by all local shards   */
+  uint64_t kernel_launches; /* this handle's kernels launched, cumulative          */
 } rs_stats;
 
 /* ---- process-level objects ------------------------------------------------ */

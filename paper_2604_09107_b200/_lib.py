@@ -41,7 +41,7 @@ class RsStats(C.Structure):
                 ("failovers", u64), ("last_pull_ms", C.c_float), ("last_publish_ms", C.c_float),
                 ("last_pull_bytes", u64), ("last_pull_launches", u32), ("h2d_bytes", u64),
                 ("d2h_bytes", u64), ("fill_max_ms", C.c_float), ("fill_sum_ms", C.c_float),
-                ("fill_bytes", u64)]
+                ("fill_bytes", u64), ("kernel_launches", u64)]
 
 
 _SIGS = {

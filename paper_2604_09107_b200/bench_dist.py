@@ -106,6 +106,7 @@ def run(args):
     torch.cuda.synchronize()
     clk.start()
     link0 = nvc.read()
+    kl0 = h.stats().kernel_launches
     walls, kms, landed = [], [], 0
     for _ in range(args.steps):
         w, k, b = step()
@@ -114,12 +115,13 @@ def run(args):
         landed += b
     torch.cuda.synchronize()
     link1 = nvc.read()
+    kl1 = h.stats().kernel_launches
     clocks = clk.stop()
     # max over ranks of per-step device time; sum of landed bytes
     t = torch.tensor([max(kms) if kms else 0.0, sum(kms), float(landed), max(walls), sum(walls)],
                      dtype=torch.float64)
     allv = [None] * world
-    dist.all_gather_object(allv, (t.tolist(), kms, clocks, link0, link1), group=dc.pg)
+    dist.all_gather_object(allv, (t.tolist(), kms, clocks, link0, link1, kl1 - kl0), group=dc.pg)
     step_dev_ms = [max(a[1][i] for a in allv) for i in range(args.steps)]
     total_landed = sum(a[0][2] for a in allv)
     dev_s = sum(step_dev_ms) / 1e3
@@ -174,7 +176,7 @@ def run(args):
                     "h2d_bytes_per_step": None, "d2h_bytes_per_step": None,
                     "what": "wall clock of the collective replicate (plan+bind+IPC exchange+kernel), "
                             "version resident in the trainer's HBM"},
-            "gpu_launches": args.steps * receivers * 2,
+            "gpu_launches": sum(a[5] for a in allv),  # every rank's kernels in the timed steps
             "clocks": allv[0][2] if allv[0][2].get("sm_mhz") else allv[1][2],
             "verified": verified,
         }

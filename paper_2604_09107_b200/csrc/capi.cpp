@@ -402,6 +402,7 @@ int rs_stats_get(rs_handle* h, rs_stats* out) {
   out->fill_max_ms = s.fill_max_ms;
   out->fill_sum_ms = s.fill_sum_ms;
   out->fill_bytes = s.fill_bytes;
+  out->kernel_launches = s.kernel_launches;
   return 0;
 }
 

@@ -774,6 +774,7 @@ Status Client::build_payload(Shard& sh, VersionId v, std::shared_ptr<Payload>* o
     RS_CUDA(cudaMemcpyAsync(d, np.data(), nn * 8, cudaMemcpyHostToDevice, sh.stream));
     RS_CUDA(cudaMemcpyAsync(d + nn, nl.data(), nn * 8, cudaMemcpyHostToDevice, sh.stream));
     RS_CUDA(dev::launch_span_digests(d, d + nn, d + 2 * nn, static_cast<int>(nn), sh.stream));
+    ++stats_.kernel_launches;
     RS_CUDA(cudaMemcpyAsync(nd.data(), d + 2 * nn, nn * 8, cudaMemcpyDeviceToHost, sh.stream));
     RS_CUDA(cudaStreamSynchronize(sh.stream));
     for (std::size_t k = 0; k < nn; ++k) dig[now[k]] = nd[k];
@@ -817,6 +818,7 @@ Status Client::build_payload(Shard& sh, VersionId v, std::shared_ptr<Payload>* o
     RS_CUDA(cudaMemcpyAsync(g2, gp.data(), ng * 8, cudaMemcpyHostToDevice, sh.stream));
     RS_CUDA(cudaMemcpyAsync(g2 + ng, gl.data(), ng * 8, cudaMemcpyHostToDevice, sh.stream));
     RS_CUDA(dev::launch_span_digests(g2, g2 + ng, g2 + 2 * ng, static_cast<int>(ng), sh.stream));
+    ++stats_.kernel_launches;
     RS_CUDA(cudaMemcpyAsync(gd.data(), g2 + 2 * ng, ng * 8, cudaMemcpyDeviceToHost, sh.stream));
     RS_CUDA(cudaStreamSynchronize(sh.stream));
     stats_.h2d_bytes += 16 * ng;
@@ -861,6 +863,7 @@ Status Client::build_payload(Shard& sh, VersionId v, std::shared_ptr<Payload>* o
     RS_CUDA(cudaMemcpyAsync(kd, lp.data(), nl * 8, cudaMemcpyHostToDevice, sh.k6));
     RS_CUDA(cudaMemcpyAsync(kd + nl, ll.data(), nl * 8, cudaMemcpyHostToDevice, sh.k6));
     RS_CUDA(dev::launch_span_digests(kd, kd + nl, kd + 2 * nl, static_cast<int>(nl), sh.k6));
+    ++stats_.kernel_launches;
     stats_.h2d_bytes += 16 * nl;
   }
 
@@ -1030,6 +1033,7 @@ Status Client::hash_items(Shard& sh, Payload& p, const std::vector<std::uint32_t
   pp.timeout_ns = static_cast<std::uint64_t>(cfg_.pull_timeout_s * 1e9);
   pp.guard = guard;
   RS_CUDA(dev::launch_pull(pp, grid(sh), sh.stream));
+  stats_.kernel_launches += dev::pull_has_work(pp) ? 1 : 0;
   stats_.h2d_bytes += sh.hash_plan.h2d_bytes;
   return Status::ok;
 }
@@ -1593,6 +1597,7 @@ Status Client::launch_fill(Shard& sh, const SourceView& src, bool src_complete) 
   pp.remote = dma || !remote ? 0u : (src.device >= 0 && !any_cast) ? 2u : 1u;
   sh.t_launch = std::chrono::steady_clock::now();
   RS_CUDA(dev::launch_pull(pp, grid(sh), sh.stream));
+  stats_.kernel_launches += dev::pull_has_work(pp) ? 1 : 0;
   // A fill fed over TCP waits on progress that may need this GPU's copy
   // engines (a StreamServer in this process staging a frame D2H).  Nothing
   // is queued behind its kernel: an event record or copy waiting on the
@@ -1851,6 +1856,7 @@ Status Client::copy_spans(Shard& sh, const std::vector<std::uint64_t>& srcs,
   RS_CUDA(cudaMemcpyAsync(d, host.data(), 4 * n * 8, cudaMemcpyHostToDevice, sh.stream));
   RS_CUDA(dev::launch_copy_spans(d, d + n, d + 2 * n, d + 3 * n, static_cast<int>(n), tiles,
                                  sh.stream, guard));
+  ++stats_.kernel_launches;
   stats_.h2d_bytes += 32 * n;
   return Status::ok;
 }
@@ -1971,6 +1977,7 @@ Status Client::launch_reshard_fill(Shard& sh, const Assignment& a, bool src_comp
   pp.remote = remote ? 1u : 0u;
   RS_CUDA(cudaEventRecord(sh.ev0, sh.stream));
   RS_CUDA(dev::launch_pull(pp, grid(sh), sh.stream));
+  stats_.kernel_launches += dev::pull_has_work(pp) ? 1 : 0;
   RS_CUDA(cudaEventRecord(sh.ev1, sh.stream));
   p.landed_some = true;
   // the follow-up (slice copies, packing, re-digests) queued right behind the
@@ -2092,6 +2099,7 @@ Status Client::finish_reshard(Shard& sh, const std::uint32_t* guard) {
     pp.timeout_ns = static_cast<std::uint64_t>(cfg_.pull_timeout_s * 1e9);
     pp.guard = guard;
     RS_CUDA(dev::launch_pull(pp, grid(sh), sh.stream));
+    stats_.kernel_launches += dev::pull_has_work(pp) ? 1 : 0;
   }
   if (std::getenv("RSB_TIMING")) {
     std::uint64_t gb = 0, cb = 0, rb = 0;

@@ -203,6 +203,7 @@ struct ClientStats {
   // the last fill round over every local shard
   float fill_max_ms = 0, fill_sum_ms = 0;
   std::uint64_t fill_bytes = 0;
+  std::uint64_t kernel_launches = 0;  // every kernel this client launched
 };
 
 class Client {

@@ -145,6 +145,8 @@ std::vector<std::uint32_t> schedule_order(const ItemDesc* items, std::uint32_t n
 // Fused mover: copy + per-chunk XXH64 verify + watermark publish.  `sms` is
 // the device's SM count (pull_grid); the persistent grid is sized from it.
 cudaError_t launch_pull(const PullParams& p, int sms, cudaStream_t s);
+// launch_pull starts a kernel only when the plan has batches to do.
+inline bool pull_has_work(const PullParams& p) { return p.order ? p.n_sched != 0 : p.n_batches > p.first_batch; }
 int pull_grid(int device);  // SM count of the device
 const char* pull_kernel_name();
 

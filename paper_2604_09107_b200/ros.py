@@ -83,6 +83,7 @@ class Stats:
     fill_max_ms: float = 0.0
     fill_sum_ms: float = 0.0
     fill_bytes: int = 0
+    kernel_launches: int = 0
 
 
 @dataclass
