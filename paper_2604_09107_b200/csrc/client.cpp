@@ -1607,6 +1607,14 @@ Status Client::launch_fill(Shard& sh, const SourceView& src, bool src_complete) 
   // when the kernel timed out).  wait_shards times it on the host.
   if (!sh.tcp) RS_CUDA(cudaEventRecord(sh.ev1, sh.stream));
   sh.holding->landed_some = true;
+  // the group unpack queued right behind the fill (skipped on the device
+  // if the fill fails); a TCP-fed fill has nothing queued behind it
+  sh.unpack_queued = false;
+  if (!sh.tcp && !sh.holding->manifest.groups.empty()) {
+    auto* code = &reinterpret_cast<dev::PullStatus*>(static_cast<std::uint8_t*>(sh.plan.scratch) + 64)->code;
+    if (Status s = queue_unpack(sh, code); !ok(s)) return s;
+    sh.unpack_queued = true;
+  }
   return Status::ok;
 }
 
@@ -1815,18 +1823,10 @@ std::vector<Client::FillOutcome> Client::wait_shards(const std::vector<std::uint
     if (!ok(out[i].status)) continue;
     Shard& sh = shards_[i];
     if (sh.holding->reshard) continue;  // its follow-up ran behind the fill (launch_reshard_fill)
-    const auto& p = *sh.holding;
-    std::vector<std::uint64_t> srcs, dsts, ls;
-    for (std::size_t gi = 0; gi < p.manifest.groups.size(); ++gi)
-      for (const auto& mem : p.manifest.groups[gi].members) {
-        srcs.push_back(reinterpret_cast<std::uint64_t>(p.group_bufs[gi]->p) + mem.offset);
-        const Reg& r = sh.regs[sh.by_name.at(p.manifest.entries[mem.entry].name)];
-        dsts.push_back(reinterpret_cast<std::uint64_t>(r.ptr));
-        ls.push_back(p.manifest.entries[mem.entry].length | (r.cast ? dev::kSpanCastE4M3 : 0));
-      }
-    if (Status s = copy_spans(sh, srcs, dsts, ls); !ok(s)) out[i] = {s, 0, 0};
-    if (!srcs.empty() && cudaStreamSynchronize(sh.stream) != cudaSuccess)
-      out[i] = {Status::transfer_failed, 0, 0};
+    if (sh.unpack_queued) continue;     // queued behind the fill; the status read synchronized it
+    if (sh.holding->manifest.groups.empty()) continue;
+    if (Status s = queue_unpack(sh, nullptr); !ok(s)) out[i] = {s, 0, 0};
+    if (cudaStreamSynchronize(sh.stream) != cudaSuccess) out[i] = {Status::transfer_failed, 0, 0};
   }
   return out;
 }
@@ -1834,13 +1834,14 @@ std::vector<Client::FillOutcome> Client::wait_shards(const std::vector<std::uint
 Status Client::copy_spans(Shard& sh, const std::vector<std::uint64_t>& srcs,
                           const std::vector<std::uint64_t>& dsts,
                           const std::vector<std::uint64_t>& lens,
-                          const std::uint32_t* guard) {
+                          const std::uint32_t* guard, DevBuf* table,
+                          std::vector<std::uint64_t>* last) {
   // Stream-ordered: returns once the copy is queued on sh.stream (callers
   // synchronize).  The span tables live in sh.span_tables; a later call's
   // upload is ordered behind this call's kernel on the same stream.
   if (srcs.empty()) return Status::ok;
   DeviceGuard g(sh.device);
-  DevBuf& t = sh.span_tables;
+  DevBuf& t = table ? *table : sh.span_tables;
   const std::size_t n = srcs.size();
   std::vector<std::uint64_t> host(4 * n);
   std::uint64_t tiles = 0;
@@ -1851,14 +1852,31 @@ Status Client::copy_spans(Shard& sh, const std::vector<std::uint64_t>& srcs,
     host[3 * n + i] = tiles;
     tiles += dev::copy_span_tiles(lens[i]);
   }
-  if (Status s = t.alloc(sh.device, 4 * n * 8); !ok(s)) return s;
+  const bool same = last && *last == host && t.p && t.n >= 4 * n * 8;
+  if (!same) {
+    if (Status s = t.alloc(sh.device, 4 * n * 8); !ok(s)) return s;
+    RS_CUDA(cudaMemcpyAsync(t.p, host.data(), 4 * n * 8, cudaMemcpyHostToDevice, sh.stream));
+    stats_.h2d_bytes += 32 * n;
+    if (last) *last = std::move(host);
+  }
   auto* d = static_cast<std::uint64_t*>(t.p);
-  RS_CUDA(cudaMemcpyAsync(d, host.data(), 4 * n * 8, cudaMemcpyHostToDevice, sh.stream));
   RS_CUDA(dev::launch_copy_spans(d, d + n, d + 2 * n, d + 3 * n, static_cast<int>(n), tiles,
                                  sh.stream, guard));
   ++stats_.kernel_launches;
-  stats_.h2d_bytes += 32 * n;
   return Status::ok;
+}
+
+Status Client::queue_unpack(Shard& sh, const std::uint32_t* guard) {
+  const auto& p = *sh.holding;
+  std::vector<std::uint64_t> srcs, dsts, ls;
+  for (std::size_t gi = 0; gi < p.manifest.groups.size(); ++gi)
+    for (const auto& mem : p.manifest.groups[gi].members) {
+      srcs.push_back(reinterpret_cast<std::uint64_t>(p.group_bufs[gi]->p) + mem.offset);
+      const Reg& r = sh.regs[sh.by_name.at(p.manifest.entries[mem.entry].name)];
+      dsts.push_back(reinterpret_cast<std::uint64_t>(r.ptr));
+      ls.push_back(p.manifest.entries[mem.entry].length | (r.cast ? dev::kSpanCastE4M3 : 0));
+    }
+  return copy_spans(sh, srcs, dsts, ls, guard, &sh.unpack_tables, &sh.unpack_last);
 }
 
 Status Client::resolve_shard(Shard& sh, const std::string& replica, std::uint32_t shard,

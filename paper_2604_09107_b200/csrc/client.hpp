@@ -378,6 +378,9 @@ class Client {
     std::vector<std::uint32_t> flag_host;  // report_progress: the fill's watermarks
     std::uint64_t reported = 0;            // items last reported to the registry
     DevBuf span_tables;           // copy_spans' span tables (grow-only: no per-call malloc/free)
+    DevBuf unpack_tables;         // the group unpack's span table (re-uploaded only on change)
+    std::vector<std::uint64_t> unpack_last;
+    bool unpack_queued = false;   // the launched fill's group unpack is queued behind it
     DevBuf dig_tables, group_tables;  // publish: K6 span tables (grow-only)
     // Copy-engine landing from host memory (launch_fill): frames copied on
     // `dma`, each raising dma_flags[frame] = dma_epoch for the hash pass
@@ -423,9 +426,15 @@ class Client {
   Status finish_reshard(Shard& sh, const std::uint32_t* guard);
   Status hash_items(Shard& sh, Payload& p, const std::vector<std::uint32_t>& items,
                     const std::uint32_t* guard = nullptr);
+  // table/last (optional): a dedicated span table whose upload is skipped
+  // when the spans equal the previous call's (the steady-state group unpack).
   Status copy_spans(Shard& sh, const std::vector<std::uint64_t>& srcs,
                     const std::vector<std::uint64_t>& dsts, const std::vector<std::uint64_t>& lens,
-                    const std::uint32_t* guard = nullptr);
+                    const std::uint32_t* guard = nullptr, DevBuf* table = nullptr,
+                    std::vector<std::uint64_t>* last = nullptr);
+  // unpack_group (manifest.cpp:217-225) of every packed group, queued on
+  // sh.stream (behind the fill, skipped on the device if it failed).
+  Status queue_unpack(Shard& sh, const std::uint32_t* guard);
   Status resolve_shard(Shard& sh, const std::string& replica, std::uint32_t shard, VersionId v,
                        SourceView* out);
   void serve(Shard& sh, VersionId v, bool complete);
