@@ -322,7 +322,20 @@ def cpu_reference_run(shapes, readers: int = 1, steps: int = 1, warmup: int = 0,
     src = host_workload(shapes)
     gen_s = time.perf_counter() - t0
     total = sum(a.nbytes for a in src)
-    dst = [[np.empty_like(a) for a in src] for _ in range(readers)]
+    # one landing copy per reader when the host has the memory (N=8: 8 x 16 GB);
+    # otherwise the readers land into shared buffers (identical bytes), said so
+    # in `sample`
+    try:
+        import psutil
+        avail = psutil.virtual_memory().available
+    except Exception:  # noqa: BLE001
+        avail = None
+    shared = avail is not None and (readers + 1) * total > 0.85 * avail
+    if shared:
+        one = [np.empty_like(a) for a in src]
+        dst = [one] * readers
+    else:
+        dst = [[np.empty_like(a) for a in src] for _ in range(readers)]
     c = O.RefCluster(threaded=True, server_pipeline=False, client_pipeline=False)
     c.add("trainer")
     for (name, _), a in zip(shapes, src):
@@ -355,7 +368,9 @@ def cpu_reference_run(shapes, readers: int = 1, steps: int = 1, warmup: int = 0,
                       f"refstore publish once, then per step {readers} fresh reader replica(s) "
                       f"replicate('latest') through ClientCore + MemNetwork, ThreadExecutor per "
                       f"replica, pipeline off; copy + digest64 run on each reader's executor "
-                      f"thread ({min(readers, nproc)} core(s) busy of {nproc}); median of {len(out)}"}
+                      f"thread ({min(readers, nproc)} core(s) busy of {nproc}); median of {len(out)}"
+                      + ("; host RAM short of one copy per reader: the readers share one set of "
+                         "landing buffers" if shared else "")}
 
 
 def reference_parity(workload, t, r, rviews, cast: bool):
