@@ -330,7 +330,7 @@ def cpu_reference_run(shapes, readers: int = 1, steps: int = 1, warmup: int = 0,
         avail = psutil.virtual_memory().available
     except Exception:  # noqa: BLE001
         avail = None
-    shared = avail is not None and (readers + 1) * total > 0.85 * avail
+    shared = avail is not None and readers * total > 0.85 * avail  # the source copy is already resident
     if shared:
         one = [np.empty_like(a) for a in src]
         dst = [one] * readers
