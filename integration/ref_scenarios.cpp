@@ -140,6 +140,7 @@ struct RefFix {
   };
   std::map<std::string, std::unique_ptr<Node>> nodes;
 
+  bool use_b200 = true;  // false: the reference MemNetwork moves the bytes (equivalence runs)
   RefFix() : srv("A", ServerConfig{}, &exec, &log, net.sender()) {
     net.register_server("A", &srv, &exec);
     srv.start();
@@ -154,8 +155,8 @@ struct RefFix {
     cfg.servers = {"A"};
     cfg.data_endpoint = "ep:" + replica;
     b200.register_data(cfg.data_endpoint, &n->serves);
-    n->core = std::make_unique<ClientCore>("m", replica, shards, cfg, &exec, &log, &net, &b200,
-                                           &n->serves);
+    DataTransport* data = use_b200 ? static_cast<DataTransport*>(&b200) : static_cast<DataTransport*>(&net);
+    n->core = std::make_unique<ClientCore>("m", replica, shards, cfg, &exec, &log, &net, data, &n->serves);
     ClientCore& r = *n->core;
     nodes[replica] = std::move(n);
     return r;
@@ -164,10 +165,19 @@ struct RefFix {
     Node& n = *nodes.at(replica);
     std::byte* p = nullptr;
     cudaMallocManaged(&p, t.len);
-    auto h = pattern(t.len, salt);
-    std::memcpy(p, h.data(), t.len);
     n.bufs[{t.shard, t.name}] = p;
+    fill(replica, t, salt);
     n.core->register_tensor(t.shard, t.name, {p, t.len});
+  }
+  void fill(const std::string& replica, const Tensor& t, std::uint64_t salt) {
+    cudaDeviceSynchronize();
+    auto h = pattern(t.len, salt);
+    std::memcpy(nodes.at(replica)->bufs.at({t.shard, t.name}), h.data(), t.len);
+  }
+  std::vector<std::byte> bytes(const std::string& replica, const Tensor& t) {
+    cudaDeviceSynchronize();
+    const std::byte* p = nodes.at(replica)->bufs.at({t.shard, t.name});
+    return {p, p + t.len};
   }
   bool same(const std::string& a, const std::string& b, const Tensor& t) {
     cudaDeviceSynchronize();
@@ -247,6 +257,99 @@ void level_b_corrupt_source() {
   for (const auto& x : ts) ok &= fx.same("T1", "R", x);
   ok &= fx.srv.listing("m")[1].count("T2") == 1;  // corruption does not condemn
   report(ok, "B", "corrupt_source_quiet_retry_report_repick", counters(s));
+}
+
+void level_a_update() {
+  // test_client_core.cpp:204-231: update reports no change, then pulls v2
+  B200Cluster cl;
+  DevBufs tb, rb;
+  const Tensor w{0, "w", 200000, 1};
+  B200Client t(cl, "m", "T", 1);
+  t.register_tensor(0, w.name, tb.make(w, 1));
+  std::optional<ClientCore::OpResult> r;
+  t.publish(1, [&](ClientCore::OpResult x) { r = x; });
+  bool ok = r && r->status == Status::ok;
+  B200Client rd(cl, "m", "R", 1);
+  rd.register_tensor(0, w.name, rb.make(w, 50));
+  rd.replicate(VersionSpec::latest(), [&](ClientCore::OpResult x) { r = x; });
+  ok &= r->status == Status::ok;
+  rd.update(VersionSpec::latest(), [&](ClientCore::OpResult x) { r = x; });
+  ok &= r->status == Status::ok && !r->changed && r->version == VersionId{1};
+  t.unpublish([&](ClientCore::OpResult x) { r = x; });
+  ok &= r->status == Status::ok;
+  auto h2 = pattern(w.len, 2);
+  cudaMemcpy(tb.p.at({0, "w"}), h2.data(), w.len, cudaMemcpyHostToDevice);
+  t.publish(2, [&](ClientCore::OpResult x) { r = x; });
+  ok &= r->status == Status::ok;
+  rd.update(VersionSpec::latest(), [&](ClientCore::OpResult x) { r = x; });
+  ok &= r->status == Status::ok && r->changed && r->version == VersionId{2};
+  ok &= rd.current_version() == VersionId{2} && rb.host(w) == h2;
+  report(ok, "A", "update_no_change_then_newer", counters(rd.stats()));
+}
+
+void level_b_update() {
+  RefFix fx;
+  const Tensor w{0, "w", 200000, 1};
+  ClientCore& t = fx.make("T", 1);
+  fx.reg("T", w, 1);
+  bool ok = fx.run([&](auto cb) { t.publish(1, cb); }).status == Status::ok;
+  ClientCore& rd = fx.make("R", 1);
+  fx.reg("R", w, 50);
+  ok &= fx.run([&](auto cb) { rd.replicate(VersionSpec::latest(), cb); }).status == Status::ok;
+  auto r = fx.run([&](auto cb) { rd.update(VersionSpec::latest(), cb); });
+  ok &= r.status == Status::ok && !r.changed && r.version == VersionId{1};
+  ok &= fx.run([&](auto cb) { t.unpublish(cb); }).status == Status::ok;
+  fx.fill("T", w, 2);
+  ok &= fx.run([&](auto cb) { t.publish(2, cb); }).status == Status::ok;
+  r = fx.run([&](auto cb) { rd.update(VersionSpec::latest(), cb); });
+  ok &= r.status == Status::ok && r.changed && r.version == VersionId{2};
+  ok &= rd.current_version() == VersionId{2} && fx.same("T", "R", w);
+  report(ok, "B", "update_no_change_then_newer", counters(rd.stats()));
+}
+
+void level_b_silent_source() {
+  // test_client_core.cpp:317-344: a silent source is reported (timeout) and
+  // the pull moves to a sibling; the report condemns the silent copy
+  RefFix fx;
+  const Tensor w{0, "w", 150000, 6};
+  ClientCore& t1 = fx.make("T1", 1);
+  fx.reg("T1", w, 6);
+  bool ok = fx.run([&](auto cb) { t1.publish(1, cb); }).status == Status::ok;
+  ClientCore& t2 = fx.make("T2", 1);
+  fx.reg("T2", w, 60);
+  ok &= fx.run([&](auto cb) { t2.replicate(VersionSpec::latest(), cb); }).status == Status::ok;
+  fx.b200.set_data_silent("ep:T2", true);
+  ClientCore& rd = fx.make("R", 1);
+  fx.reg("R", w, 70);
+  auto r = fx.run([&](auto cb) { rd.replicate(VersionSpec::latest(), cb); });
+  ok &= r.status == Status::ok && rd.stats().failure_reports >= 1 && fx.same("T1", "R", w);
+  auto lm = fx.srv.listing("m");
+  ok &= lm.count(1) && !lm[1].count("T2") && lm[1].count("T1");
+  report(ok, "B", "silent_source_reported_and_pull_moves", counters(rd.stats()));
+}
+
+void level_b_equivalence() {
+  // test_transport.cpp:573-587: the same replicate through the reference
+  // MemNetwork and through B200Transport lands identical bytes, equal to the
+  // publisher's pattern
+  std::map<std::pair<std::uint32_t, std::string>, std::vector<std::byte>> got[2];
+  std::uint64_t device_bytes = 0;
+  for (int k = 0; k < 2; ++k) {
+    RefFix fx;
+    fx.use_b200 = k == 1;
+    ClientCore& t = fx.make("T", 2);
+    for (const auto& x : kT) fx.reg("T", x, x.salt);
+    fx.run([&](auto cb) { t.publish(1, cb); });
+    ClientCore& rd = fx.make("R", 2);
+    for (const auto& x : kT) fx.reg("R", x, 100);
+    fx.run([&](auto cb) { rd.replicate(VersionSpec::latest(), cb); });
+    for (const auto& x : kT) got[k][{x.shard, x.name}] = fx.bytes("R", x);
+    if (k == 1) device_bytes = fx.b200.device_bytes();
+  }
+  bool ok = device_bytes > 0;
+  for (const auto& x : kT) ok &= got[0][{x.shard, x.name}] == got[1][{x.shard, x.name}] &&
+                                 got[1][{x.shard, x.name}] == pattern(x.len, x.salt);
+  report(ok, "B", "transport_equivalence_mem_vs_b200", "device_bytes=" + std::to_string(device_bytes));
 }
 
 // ------------------------------------------------------------------ level C
@@ -335,6 +438,10 @@ int main(int argc, char** argv) {
       {"A replicate_pulls_bytes_that_verify", level_a_replicate},
       {"B replicate_pulls_bytes_that_verify", level_b_replicate},
       {"B corrupt_source_quiet_retry_report_repick", level_b_corrupt_source},
+      {"A update_no_change_then_newer", level_a_update},
+      {"B update_no_change_then_newer", level_b_update},
+      {"B silent_source_reported_and_pull_moves", level_b_silent_source},
+      {"B transport_equivalence_mem_vs_b200", level_b_equivalence},
       {"C rsdp_reference_reader_pulls_and_verifies", level_c_rsdp_reader},
   };
   if (argc > 1 && std::strcmp(argv[1], "--list") == 0) {

@@ -21,6 +21,7 @@
 #include <cstdint>
 #include <map>
 #include <mutex>
+#include <set>
 #include <string>
 #include <vector>
 
@@ -46,11 +47,23 @@ class B200Transport : public DataTransport {
     net_->register_data(endpoint, serves);
   }
 
+  // MemNetwork::set_data_silent (transport_mem.hpp:43-46): a silent
+  // endpoint swallows pulls and queries without a reply (a crashed peer).
+  void set_data_silent(const std::string& endpoint, bool silent) {
+    {
+      std::lock_guard lk(m_);
+      if (silent) silent_.insert(endpoint);
+      else silent_.erase(endpoint);
+    }
+    net_->set_data_silent(endpoint, silent);
+  }
+
   void async_pull(const std::string& endpoint, const PullSpec& spec, PullDest dest,
                   Executor* exec, std::function<void(PullResult)> done) override {
     std::shared_ptr<PeerServeState> st;
     {
       std::lock_guard lk(m_);
+      if (silent_.count(endpoint)) return;  // nothing ever comes back
       auto it = data_.find(endpoint);
       if (it != data_.end()) st = it->second->find(ServeRegistry::key(spec.model, spec.replica, spec.shard));
     }
@@ -160,6 +173,7 @@ class B200Transport : public DataTransport {
   int device_;
   std::mutex m_;
   std::map<std::string, ServeRegistry*> data_;
+  std::set<std::string> silent_;
   std::atomic<std::uint64_t> pulls_{0}, device_bytes_{0}, host_bytes_{0}, last_error_{0};
 };
 

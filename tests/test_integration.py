@@ -23,7 +23,9 @@ from tests.conftest import ROOT
 
 BIN = os.path.join(ROOT, "integration", "_build", "ref_scenarios")
 SCENARIOS = ["A replicate_pulls_bytes_that_verify", "B replicate_pulls_bytes_that_verify",
-             "B corrupt_source_quiet_retry_report_repick", "C rsdp_reference_reader_pulls_and_verifies"]
+             "B corrupt_source_quiet_retry_report_repick", "A update_no_change_then_newer",
+             "B update_no_change_then_newer", "B silent_source_reported_and_pull_moves",
+             "B transport_equivalence_mem_vs_b200", "C rsdp_reference_reader_pulls_and_verifies"]
 
 
 def _binary():
@@ -38,7 +40,7 @@ def _binary():
 def test_reference_side_adapters_build_and_list():
     r = subprocess.run([_binary(), "--list"], capture_output=True, text=True, timeout=60)
     assert r.returncode == 0, r.stderr
-    assert r.stdout.split("\n")[:4] == SCENARIOS
+    assert r.stdout.split("\n")[:len(SCENARIOS)] == SCENARIOS
 
 
 @pytest.mark.gpu
@@ -59,5 +61,7 @@ def test_reference_scenarios_through_the_b200_path():
     assert int(kv[SCENARIOS[1]]["device_bytes"]) == 3 << 20  # the big item, moved by the kernel
     assert kv[SCENARIOS[2]]["checksum_failures"] == "2" and kv[SCENARIOS[2]]["failure_reports"] == "1"
     # the reference's StreamData over the B200 server's RSDP: 3 items verified
-    assert kv[SCENARIOS[3]]["items_verified"] == "3"
-    assert kv[SCENARIOS[3]]["bytes_pulled"] == str((3 << 20) + 1000 + 2000 + 4096)
+    assert kv[SCENARIOS[7]]["items_verified"] == "3"
+    assert kv[SCENARIOS[7]]["bytes_pulled"] == str((3 << 20) + 1000 + 2000 + 4096)
+    assert int(kv[SCENARIOS[5]]["failure_reports"]) >= 1
+    assert int(kv[SCENARIOS[6]]["device_bytes"]) > 0
