@@ -1681,22 +1681,29 @@ void Client::report_progress(Shard& sh) {
   const Payload& p = *sh.holding;
   const ChunkMap& cm = p.cmap;
   const std::uint32_t nb = cm.n_batches();
+  if (sh.reported + 1 >= cm.chunk0.size()) return;
   DeviceGuard g(sh.device);
   if (!sh.poll && cudaStreamCreateWithFlags(&sh.poll, cudaStreamNonBlocking) != cudaSuccess) return;
-  sh.flag_host.resize(nb);
-  if (cudaMemcpyAsync(sh.flag_host.data(), p.flags.p, std::size_t(nb) * 4, cudaMemcpyDeviceToHost,
-                      sh.poll) != cudaSuccess ||
+  // a window of watermarks from the first item not reported yet (items are
+  // verified front to back only as a prefix: the first item with a batch
+  // below the epoch ends it), so a poll reads KBs, not the whole table
+  const std::uint32_t w0 = cm.chunk0[sh.reported] / dev::kBatchChunks;
+  const std::uint32_t first_nb = (cm.count[sh.reported] + dev::kBatchChunks - 1) / dev::kBatchChunks;
+  const std::uint32_t wn = std::min<std::uint32_t>(nb - w0, std::max<std::uint32_t>(8192, first_nb));
+  sh.flag_host.resize(wn);
+  if (wn == 0 ||
+      cudaMemcpyAsync(sh.flag_host.data(), static_cast<const std::uint32_t*>(p.flags.p) + w0,
+                      std::size_t(wn) * 4, cudaMemcpyDeviceToHost, sh.poll) != cudaSuccess ||
       cudaStreamSynchronize(sh.poll) != cudaSuccess)
     return;
-  stats_.d2h_bytes += std::size_t(nb) * 4;
-  // items are verified front to back only as a prefix: the first item with a
-  // batch below the epoch ends it
+  stats_.d2h_bytes += std::size_t(wn) * 4;
   std::uint64_t items = sh.reported;
   for (std::size_t i = items; i + 1 < cm.chunk0.size(); ++i) {
     const std::uint32_t b0 = cm.chunk0[i] / dev::kBatchChunks;
     const std::uint32_t n = (cm.count[i] + dev::kBatchChunks - 1) / dev::kBatchChunks;
+    if (b0 + n > w0 + wn) break;  // beyond the window: the next poll
     bool done = true;
-    for (std::uint32_t b = b0; b < b0 + n && done; ++b) done = sh.flag_host[b] == p.epoch;
+    for (std::uint32_t b = b0; b < b0 + n && done; ++b) done = sh.flag_host[b - w0] == p.epoch;
     if (!done) break;
     items = i + 1;
   }
