@@ -373,7 +373,7 @@ def cpu_reference_run(shapes, readers: int = 1, steps: int = 1, warmup: int = 0,
                          "landing buffers" if shared else "")}
 
 
-def reference_parity(workload, t, r, rviews, cast: bool):
+def reference_parity(workload, t, r, rviews, cast: bool, soft: bool = False):
     """Pre-timing parity against the reference at full scale
     (tests/golden/scale.json, made by tests/golden/make_scale_golden.py from
     oracle/_ref): the trainer's manifest bytes (build_publish_payload), the
@@ -391,13 +391,15 @@ def reference_parity(workload, t, r, rviews, cast: bool):
     with open(path) as f:
         g = json.load(f)[key]
     sha = lambda a: hashlib.sha256(np.ascontiguousarray(a).astype("<u8").tobytes()).hexdigest()
-    landed = ros.digest_spans([w.data_ptr() for _, w in rviews], [w.numel() for _, w in rviews])
+    landed = ros.digest_spans([w.data_ptr() for _, w in rviews], [w.numel() for _, w in rviews],
+                              rviews[0][1].device.index or 0)
     want = g["cast_digests"] if cast else g["tensor_digests"]
     out = {"manifest": hashlib.sha256(t.manifest(0)).hexdigest() == g["manifest_sha256"],
            "chunk_table": sha(r.chunk_digests(0)) == g["chunk_table_sha256"],
            "landed_tensors": ["%016X" % x for x in landed] == want,
            "against": "tests/golden/scale.json (reference digest64 / build_publish_payload)"}
-    assert out["manifest"] and out["chunk_table"] and out["landed_tensors"], out
+    if not soft:
+        assert out["manifest"] and out["chunk_table"] and out["landed_tensors"], out
     return out
 
 

@@ -100,6 +100,10 @@ def run(args):
     # must equal the trainer's (computed at publish from the source bytes)
     hashes = dc.gather(None if args.no_verify else table_hash())
     verified = args.no_verify or all(x == hashes[0] for x in hashes)
+    # every rank (trainer and readers) against the reference at full scale
+    # (tests/golden/scale.json): manifest bytes, chunk table, landed tensors
+    parity = dc.gather(None if args.no_verify else
+                       B.reference_parity(args.workload, h, h, views, False, soft=True))
     clk = B.ClockSampler(local)
     nvc = B.NvlinkCounters(local)
     dist.barrier(group=dc.pg)
@@ -177,6 +181,9 @@ def run(args):
                     "what": "wall clock of the collective replicate (plan+bind+IPC exchange+kernel), "
                             "version resident in the trainer's HBM"},
             "gpu_launches": sum(a[5] for a in allv),  # every rank's kernels in the timed steps
+            "parity": {"per_rank": parity,
+                       "all": all(p and p["manifest"] and p["chunk_table"] and p["landed_tensors"]
+                                  for p in parity) if not args.no_verify and parity[0] else None},
             "clocks": allv[0][2] if allv[0][2].get("sm_mhz") else allv[1][2],
             "verified": verified,
         }
