@@ -268,3 +268,75 @@ def test_reference_wire_frozen_request_is_served():
         assert (kind, blen) == (4, 10)
         assert struct.unpack(">BQB", recv_n(10)) == (0, 1, 1)
         c.close()
+
+
+def test_reference_wire_serves_only_the_verified_prefix_of_a_filling_replica():
+    """compute_slice over a B200 replica that is still filling: the RSDP
+    server reads its verified item prefix from the device watermarks -- a
+    query answers progress 0 while nothing landed, a pull returns no bytes,
+    and once the fill ran both see every item (transport.cpp:32-49,
+    transport_stream.cpp:355-411)."""
+    import socket
+    import struct
+    dev = torch.device("cuda:0")
+    with Cluster() as cl:
+        port = cl.listen()
+        tb = _bufs(dev, seed=31)
+        t = _open(cl, "T", tb)
+        assert t.publish(1).status == Status.ok
+        a = cl.open("m", "A", 1, tiny_threshold=1 << 20, grid_sms=32)
+        ab = _bufs(dev)
+        for i, b in enumerate(ab):
+            assert a.register_tensor(0, f"w{i}", b) == Status.ok
+        assert a.connect() == Status.ok
+        assert a.server_replicate("latest").status == Status.ok
+        assert a.transfer_bind(1) == Status.ok  # serving its empty fill
+
+        c = socket.create_connection(("127.0.0.1", port))
+
+        def recv_n(n):
+            out = b""
+            while len(out) < n:
+                k = c.recv(n - len(out))
+                assert k
+                out += k
+            return out
+
+        def body(min_or_off, maxb=None):
+            b = (b"\x01\x02" + struct.pack(">I", 1) + b"m" + b"\x02\x02" + struct.pack(">I", 1) + b"A" +
+                 b"\x03\x01" + struct.pack(">Q", 1) + b"\x04\x01" + struct.pack(">Q", 0) +
+                 b"\x05\x01" + struct.pack(">Q", min_or_off))
+            return b + (b"\x06\x01" + struct.pack(">Q", maxb) if maxb is not None else b"")
+
+        def query(min_items):
+            q = body(min_items)
+            c.sendall(struct.pack(">IHHQ", 0x52534450, 1, 3, len(q)) + q)
+            assert struct.unpack(">IHHQ", recv_n(16))[2] == 4
+            return struct.unpack(">BQB", recv_n(10))
+
+        def pull(off, maxb):
+            q = body(off, maxb)
+            c.sendall(struct.pack(">IHHQ", 0x52534450, 1, 1, len(q)) + q)
+            _, _, kind, blen = struct.unpack(">IHHQ", recv_n(16))
+            st, prog, comp, plen = struct.unpack(">BQBQ", recv_n(18))
+            return st, prog, comp, recv_n(plen)
+
+        assert query(1) == (0, 0, 0)  # long-polled ~1 s: nothing verified yet
+        st, prog, comp, payload = pull(0, 1 << 20)
+        assert (st, prog, comp, len(payload)) == (0, 0, 0, 0)
+        assert a.transfer_launch() == Status.ok
+        assert a.transfer_wait() == [(Status.ok, 0)]
+        st, prog, comp = query(10 ** 6)
+        assert st == 0 and prog == 3  # w0, the group holding w1, w2 -- all verified
+        total = sum(x.numel() for x in ab)
+        got = b""
+        while len(got) < total:
+            st, prog, comp, payload = pull(len(got), total - len(got))
+            assert st == 0 and payload
+            got += payload
+        # the item stream: big items in registration order, the group (w1) at
+        # its first member's position -- here w0, group(w1), w2
+        want = b"".join(x.cpu().numpy().tobytes() for x in tb)
+        assert got == want
+        a.transfer_finish(1, True)
+        c.close()
