@@ -428,3 +428,43 @@ def test_gpu_reader_in_another_process_pulls_the_offload():
     assert res[1]["replicate"] == (0, 1) and res[1]["bytes_v1"]
     assert ("reader", "trainer+offload@1") in res[1]["plan"]
     assert res[0]["lanes_after_release"] == []
+
+
+@pytest.mark.gpu
+def test_early_published_version_parked_and_served_with_its_final_manifest(oracle):
+    """An early publish (big-entry digests in the background) that is later
+    parked in host memory: the unpublish waits for the digests, the offload
+    serves the version, and a reader ends with the reference's manifest."""
+    _need_gpu()
+    dev = torch.device("cuda:0")
+    from paper_2604_09107_b200 import ros
+    sizes = ((6 << 20) + 4096 * 3, 5000, 3 << 20)
+    with Cluster() as cl:
+        w = cl.open("m", "watcher", 1)
+        assert w.register_tensor(0, "w0", torch.zeros(4096, dtype=torch.uint8, device=dev)) == Status.ok
+        w.set_retention([0, 1])
+        assert w.connect() == Status.ok
+        t = cl.open("m", "trainer", 1, tiny_threshold=1 << 20, early_publish=True)
+        tb = _tensors(dev, 70, sizes)
+        for i, x in enumerate(tb):
+            assert t.register_tensor(0, f"w{i}", x) == Status.ok
+        assert t.publish(1).status == Status.ok
+        v1 = [x.clone() for x in tb]
+        want = oracle.publish_manifest([f"w{i}" for i in range(3)],
+                                       [x.cpu().numpy() for x in v1], tiny=1 << 20)
+        assert t.unpublish().status == Status.ok  # waits for the digests, then parks
+        assert t.lanes() == [1] and not t.publish_pending
+        for i, x in enumerate(tb):
+            ros.synth_bf16(x, 170 + i)
+        assert t.publish(2).status == Status.ok
+        r = cl.open("m", "reader", 1, tiny_threshold=1 << 20)
+        rb = [torch.zeros_like(x) for x in tb]
+        for i, x in enumerate(rb):
+            assert r.register_tensor(0, f"w{i}", x) == Status.ok
+        res = r.replicate("1")
+        assert res.status == Status.ok and res.version == 1, res
+        assert [(a.replica, a.src) for a in cl.assigns()][-1] == ("reader", "trainer+offload@1")
+        torch.cuda.synchronize()
+        for a, b in zip(v1, rb):
+            assert torch.equal(a, b)
+        assert r.manifest(0) == want
