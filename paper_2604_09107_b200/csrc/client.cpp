@@ -898,6 +898,7 @@ void Client::start_finalize(VersionId v) {
     any = true;
   }
   if (!any) return;
+  if (fin_thread_.joinable()) fin_thread_.join();  // a previous publish's (normally joined already)
   bool all_local = true;
   std::vector<std::string> held(num_shards_);  // shards with nothing deferred: final already
   for (std::uint32_t i = 0; i < num_shards_; ++i) {
