@@ -351,6 +351,7 @@ def run_ring(args):
     dist.barrier(group=dc.pg)
     torch.cuda.synchronize()
     clk.start()
+    kl0 = r.stats().kernel_launches
     walls, kms, landed = [], [], 0
     for _ in range(args.steps):
         w, k, b = step()
@@ -358,7 +359,8 @@ def run_ring(args):
         kms.append(k)
         landed += b
     clocks = clk.stop()
-    allv = dc.gather((kms, landed, sum(walls), clocks))
+    kl = r.stats().kernel_launches - kl0
+    allv = dc.gather((kms, landed, sum(walls), clocks, kl))
     step_dev_ms = [max(a[0][i] for a in allv) for i in range(args.steps)]
     total_landed = sum(a[1] for a in allv)
     assert total_landed == args.steps * world * total, (total_landed, total)
@@ -395,7 +397,7 @@ def run_ring(args):
             "e2e": {"value": round(total_landed / wall_s / 1e9, 2), "unit": B.UNIT,
                     "h2d_bytes_per_step": None, "d2h_bytes_per_step": None,
                     "what": "wall clock of the collective replicate (plan+bind+IPC exchange+kernel)"},
-            "gpu_launches": args.steps * world,
+            "gpu_launches": sum(a[4] for a in allv),  # counted by the library
             "clocks": clocks,
             "verified": verified,
         }
@@ -516,6 +518,7 @@ def run_fsdp_tp2(args):
     dist.barrier(group=dc.pg)
     torch.cuda.synchronize()
     clk.start()
+    kl0 = (r.stats().kernel_launches if r is not None else 0)
     walls, kms, landed = [], [], 0
     for _ in range(args.steps):
         w, k, b = step()
@@ -523,6 +526,8 @@ def run_fsdp_tp2(args):
         kms.append(k)
         landed += b
     clocks = clk.stop()
+    kl = (r.stats().kernel_launches if r is not None else 0) - kl0
+    kls = dc.gather(kl)  # collective: every rank
     # Roofline of this shard's fill: bytes that cross NVLink (from sources on
     # other GPUs) vs bytes read from local HBM, all written to local HBM.
     src = {a.replica: a.src for a in dc.assigns()}.get(f"tp2_{rep}")
@@ -612,7 +617,7 @@ def run_fsdp_tp2(args):
             "e2e": {"value": round(total_landed / wall_s / 1e9, 2), "unit": B.UNIT,
                     "h2d_bytes_per_step": None, "d2h_bytes_per_step": None,
                     "what": "wall clock of the collective replicate (plan+bind+IPC exchange+kernel)"},
-            "gpu_launches": args.steps * world,
+            "gpu_launches": sum(kls),  # counted by the library
             "clocks": clocks,
             "verified": verified,
         }
