@@ -599,13 +599,39 @@ def run_single(args):
         "gpu_launches": st.kernel_launches - launches0,  # the reader's kernels in the timed steps (counted by the library)
         "clocks": clocks,
     }
+    version = 1
+    if not (reshard or cast):
+        # Version bumps with a warm reader (config 4's bump at N=1): the
+        # trainer unpublishes and publishes v+1 (same bytes), in the
+        # reference order and then with early publish (the big-entry digests
+        # in the background), and the reader updates.  bump = publish call +
+        # update call, wall clock; final_manifest = until the reference
+        # manifest is committed.
+        bumps = {}
+        for mode, early in (("reference_order", False), ("early_publish", True)):
+            t.set_early_publish(early)
+            assert t.unpublish().status == Status.ok
+            b0 = time.perf_counter()
+            assert t.publish(version + 1).status == Status.ok
+            b1 = time.perf_counter()
+            res = r.update("latest")
+            b2 = time.perf_counter()
+            assert res.status == Status.ok and res.version == version + 1 and res.changed, res
+            assert t.finalize() == Status.ok
+            b3 = time.perf_counter()
+            version += 1
+            bumps[mode] = {"publish_s": round(b1 - b0, 5), "update_s": round(b2 - b1, 5),
+                           "bump_latency_s": round(b2 - b0, 5), "final_manifest_s": round(b3 - b0, 5)}
+        t.set_early_publish(args.early_publish)
+        assert r.manifest(0) == t.manifest(0)
+        line["bump"] = dict(bumps, what="warm reader: trainer publish(v+1) + reader update, wall clock")
     if not (reshard or cast or args.no_host_e2e):
         # End to end from HOST buffers, through the C ABI: the version is
         # parked in pinned host memory (a retention offload, the reference's
         # own host-resident copy) and every step the reader pulls it from
         # there -- host->device bytes inside the timed region, the fill's
         # status read back.  Same metric and workload as the device arm.
-        line["e2e"] = host_e2e(cl, t, r, stream, total, tarena, rarena, args)
+        line["e2e"] = host_e2e(cl, t, r, stream, total, tarena, rarena, args, version)
         line["e2e_device_resident"] = {"value": round(e2e, 2), "unit": UNIT,
                                        "what": "rs_replicate wall clock, version in the trainer's HBM"}
     if not args.no_cpu:
@@ -616,7 +642,7 @@ def run_single(args):
     cl.close()
 
 
-def host_e2e(cl, t, r, stream, total, tarena, rarena, args):
+def host_e2e(cl, t, r, stream, total, tarena, rarena, args, version: int = 1):
     import torch
 
     from paper_2604_09107_b200.ros import Status
@@ -630,7 +656,7 @@ def host_e2e(cl, t, r, stream, total, tarena, rarena, args):
         assert r.unpublish().status == Status.ok
     r.invalidate()
     assert t.unpublish().status == Status.ok  # parks v1 in pinned host memory
-    assert t.lanes() == [1]
+    assert t.lanes() == [version]
     walls = []
     h2d0, d2h0 = r.stats().h2d_bytes, r.stats().d2h_bytes
     for k in range(args.warmup + args.steps):
@@ -639,7 +665,7 @@ def host_e2e(cl, t, r, stream, total, tarena, rarena, args):
         r.invalidate()
         torch.cuda.synchronize()
         w0 = time.perf_counter()
-        res = r.replicate("1")
+        res = r.replicate(str(version))
         torch.cuda.synchronize()
         if k >= args.warmup:
             walls.append(time.perf_counter() - w0)
@@ -647,7 +673,7 @@ def host_e2e(cl, t, r, stream, total, tarena, rarena, args):
         if k == 0:
             h2d0, d2h0 = r.stats().h2d_bytes, r.stats().d2h_bytes
             srcs = {a.src for a in cl.assigns() if a.replica == r.replica}
-            assert "trainer+offload@1" in srcs, srcs
+            assert f"trainer+offload@{version}" in srcs, srcs
     if not args.no_verify:
         assert torch.equal(tarena, rarena), "bytes pulled from the host offload differ"
     st = r.stats()

@@ -186,6 +186,8 @@ int rs_close(rs_handle* h);                                  /* close(); frees h
  * commits the final manifests (to the in-process registry when this handle
  * holds every shard; rs_manifest then returns the final bytes). */
 int rs_publish_pending(rs_handle* h);
+/* Switch rs_config.early_publish for the handle's next publish. */
+int rs_set_early_publish(rs_handle* h, int on);
 int rs_publish_finalize(rs_handle* h, double wait_s);
 /* Plan view without side effects: the source `replica` would pull `shard`
  * of `spec` from right now. */

@@ -111,6 +111,7 @@ _SIGS = {
     "rs_server_publish_provisional": (i32, [vp, cstr, cstr, u64, u32, vp, vp, vp, vp]),
     "rs_server_finalize": (i32, [vp, cstr, cstr, u64, u32, vp, vp]),
     "rs_publish_pending": (i32, [vp]),
+    "rs_set_early_publish": (i32, [vp, i32]),
     "rs_publish_finalize": (i32, [vp, dbl]),
     "rs_server_replicate": (i32, [vp, cstr, cstr, cstr]),
     "rs_server_update": (i32, [vp, cstr, cstr, cstr, i32, u64]),

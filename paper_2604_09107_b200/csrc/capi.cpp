@@ -278,6 +278,12 @@ int rs_set_stream(rs_handle* h, uint32_t shard, void* cuda_stream) {
 
 int rs_publish_pending(rs_handle* h) { return h && h->client->publish_pending() ? 1 : 0; }
 
+int rs_set_early_publish(rs_handle* h, int on) {
+  if (!h) return st(rsb::Status::invalid_argument);
+  h->client->set_early_publish(on != 0);
+  return 0;
+}
+
 int rs_publish_finalize(rs_handle* h, double wait_s) {
   if (!h) return st(rsb::Status::invalid_argument);
   return st(h->client->finalize_publish(wait_s));

@@ -307,6 +307,7 @@ class Client {
   Status finalize_publish(double wait_s, std::vector<std::string>* manifests = nullptr);
   // The last publish still digests its big entries in the background.
   bool publish_pending() const;
+  void set_early_publish(bool on) { cfg_.early_publish = on; }
   Status chunk_digests(std::uint32_t shard, std::vector<std::uint64_t>* out);
   Result<std::string> export_serve(std::uint32_t shard);
   // The shard's device serve tables (rs_serve_state).

@@ -370,6 +370,10 @@ class Handle:
         """Early publish: the last publish still digests its big entries."""
         return bool(lib.rs_publish_pending(self.h))
 
+    def set_early_publish(self, on: bool) -> None:
+        """rs_config.early_publish for the next publish."""
+        check(lib.rs_set_early_publish(self.h, int(on)))
+
     def finalize(self, wait_s: float = 60.0) -> Status:
         """Early publish: wait for the big-entry digests and commit the final
         (reference-identical) manifests."""
