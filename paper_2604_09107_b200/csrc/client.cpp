@@ -1942,52 +1942,63 @@ Status Client::launch_reshard_fill(Shard& sh, const Assignment& a, bool src_comp
   // only the watermark batches that hold bytes some slice copy reads: a
   // reader shard that needs a few members of a packed group does not pull
   // (and verify) the rest of it.  Each range is whole batches of the item,
-  // so the kernel's batch -> segment mapping is unchanged.
-  std::map<std::pair<std::uint32_t, std::uint32_t>, std::vector<std::pair<std::uint64_t, std::uint64_t>>> need_bytes;
-  for (const auto& c : rs.plan.copies)
-    need_bytes[{c.src_shard, c.src_item}].emplace_back(c.src_off,
-                                                      c.src_off + (c.rows - 1) * c.src_stride + c.nc);
-  std::uint32_t next = rs.own_chunks;
-  for (std::size_t gi = 0; gi < rs.plan.gathers.size(); ++gi) {
-    const auto& gth = rs.plan.gathers[gi];
-    const SourceShard& ss = rs.srcs[gth.src_shard];
-    const auto& it = ss.manifest.items()[gth.src_item];
-    const std::uint64_t cl = ss.layout.chunk_len[gth.src_item];
-    const auto n = static_cast<std::uint32_t>((it.length + cl - 1) / cl);
-    const std::uint32_t nb = (n + dev::kBatchChunks - 1) / dev::kBatchChunks;
-    std::vector<char> want(nb, 0);
-    auto nit = need_bytes.find({gth.src_shard, gth.src_item});
-    if (nit == need_bytes.end()) {
-      std::fill(want.begin(), want.end(), 1);
-    } else {
-      const std::uint64_t per = cl * dev::kBatchChunks;
-      for (const auto& [lo, hi] : nit->second)
-        for (std::uint64_t b = lo / per; b <= (hi - 1) / per && b < nb; ++b) want[b] = 1;
-    }
-    for (std::uint32_t b0 = 0; b0 < nb;) {
-      if (!want[b0]) {
-        ++b0;
-        continue;
+  // so the kernel's batch -> segment mapping is unchanged.  The ranges are a
+  // function of the plan: built once per bind, re-addressed per launch.
+  if (rs.gather_segs.empty() && !rs.plan.gathers.empty()) {
+    std::map<std::pair<std::uint32_t, std::uint32_t>, std::vector<std::pair<std::uint64_t, std::uint64_t>>> need_bytes;
+    for (const auto& c : rs.plan.copies)
+      need_bytes[{c.src_shard, c.src_item}].emplace_back(c.src_off,
+                                                        c.src_off + (c.rows - 1) * c.src_stride + c.nc);
+    std::uint32_t next = rs.own_chunks;
+    for (std::size_t gi = 0; gi < rs.plan.gathers.size(); ++gi) {
+      const auto& gth = rs.plan.gathers[gi];
+      const SourceShard& ss = rs.srcs[gth.src_shard];
+      const auto& it = ss.manifest.items()[gth.src_item];
+      const std::uint64_t cl = ss.layout.chunk_len[gth.src_item];
+      const auto n = static_cast<std::uint32_t>((it.length + cl - 1) / cl);
+      const std::uint32_t nb = (n + dev::kBatchChunks - 1) / dev::kBatchChunks;
+      std::vector<char> want(nb, 0);
+      auto nit = need_bytes.find({gth.src_shard, gth.src_item});
+      if (nit == need_bytes.end()) {
+        std::fill(want.begin(), want.end(), 1);
+      } else {
+        const std::uint64_t per = cl * dev::kBatchChunks;
+        for (const auto& [lo, hi] : nit->second)
+          for (std::uint64_t b = lo / per; b <= (hi - 1) / per && b < nb; ++b) want[b] = 1;
       }
-      std::uint32_t b1 = b0;
-      while (b1 < nb && want[b1]) ++b1;
-      const std::uint64_t off = std::uint64_t(b0) * dev::kBatchChunks * cl;
-      const std::uint64_t end = std::min<std::uint64_t>(it.length, std::uint64_t(b1) * dev::kBatchChunks * cl);
-      dev::ItemDesc d{};
-      d.src = views[gth.src_shard].item_ptrs[gth.src_item] + off;
-      d.dst = reinterpret_cast<std::uint64_t>(rs.gather_bufs[gi]->p) + off;
-      d.len = end - off;
-      d.chunk0 = next + b0 * dev::kBatchChunks;
-      d.chunk_len = static_cast<std::uint32_t>(cl);
-      d.src_chunk0 = ss.chunk0[gth.src_item] + b0 * dev::kBatchChunks;
-      d.q = d.m = 1;
-      d.src_id = gth.src_shard;
-      d.pad = link_class(gth.src_shard);
-      descs.push_back(d);
-      b0 = b1;
+      for (std::uint32_t b0 = 0; b0 < nb;) {
+        if (!want[b0]) {
+          ++b0;
+          continue;
+        }
+        std::uint32_t b1 = b0;
+        while (b1 < nb && want[b1]) ++b1;
+        const std::uint64_t off = std::uint64_t(b0) * dev::kBatchChunks * cl;
+        const std::uint64_t end = std::min<std::uint64_t>(it.length, std::uint64_t(b1) * dev::kBatchChunks * cl);
+        dev::ItemDesc d{};
+        d.src = off;  // + the source item's address at launch
+        d.dst = reinterpret_cast<std::uint64_t>(rs.gather_bufs[gi]->p) + off;
+        d.len = end - off;
+        d.chunk0 = next + b0 * dev::kBatchChunks;
+        d.chunk_len = static_cast<std::uint32_t>(cl);
+        d.src_chunk0 = ss.chunk0[gth.src_item] + b0 * dev::kBatchChunks;
+        d.q = d.m = 1;
+        d.src_id = gth.src_shard;
+        rs.gather_segs.push_back(d);
+        rs.gather_items.push_back(gth.src_item);
+        b0 = b1;
+      }
+      next += nb * dev::kBatchChunks;
     }
-    next += nb * dev::kBatchChunks;
+    rs.gather_chunks_end = next;
   }
+  for (std::size_t k = 0; k < rs.gather_segs.size(); ++k) {
+    dev::ItemDesc d = rs.gather_segs[k];
+    d.src += views[d.src_id].item_ptrs[rs.gather_items[k]];
+    d.pad = link_class(d.src_id);
+    descs.push_back(d);
+  }
+  const std::uint32_t next = rs.gather_segs.empty() ? rs.own_chunks : rs.gather_chunks_end;
   bool remote = false;
   for (std::uint32_t s = 0; s < nsrc; ++s) remote |= need[s] && src_dev[s] != sh.device;
   dev::PullParams pp{};

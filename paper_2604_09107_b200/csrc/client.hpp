@@ -341,6 +341,12 @@ class Client {
     ReshardPlan plan;                        // segments (source offsets) / gathers / copies
     std::vector<std::unique_ptr<DevBuf>> gather_bufs;  // per plan.gathers entry
     std::uint32_t own_chunks = 0;            // landing chunks of the reader's own items
+    // The gathers' landing segments (the batches slice copies read), built
+    // on the first launch: src = offset in the source item, src_id = source
+    // shard; gather_items[k] = the source item of segment k.
+    std::vector<dev::ItemDesc> gather_segs;
+    std::vector<std::uint32_t> gather_items;
+    std::uint32_t gather_chunks_end = 0;
   };
   struct Payload {
     Manifest manifest;
