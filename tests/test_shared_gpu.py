@@ -279,3 +279,97 @@ def test_tp_group_split_over_processes_via_group_transactions():
         for p in ps:
             p.join(timeout=60)
         log.close()
+
+
+def _retention_member(role, port, q, ev):
+    """role 'trainer': hosts nothing but its replica + a retention watcher;
+    parks v1 in host memory on unpublish.  role 'reader': joins later and
+    pulls v1 from the parked lane (POSIX shm mapped by name) via the log."""
+    import sys
+    sys.path.insert(0, ROOT)
+    import torch
+
+    from paper_2604_09107_b200 import ros
+    from paper_2604_09107_b200.ros import Status
+    from paper_2604_09107_b200.shared import SharedCluster
+    try:
+        dev = torch.device("cuda", 0)
+        sc = SharedCluster("127.0.0.1", port)
+        sizes = [(6 << 20) + 4096 * 3, 5000, 3 << 20]
+        if role == "trainer":
+            w = sc.create("m", "watcher", 1)
+            assert w.register_tensor(0, "w0", torch.zeros(4096, dtype=torch.uint8, device=dev)) == Status.ok
+            w.set_retention([0, 1])
+            sc.open(w)
+            t = sc.create("m", "trainer", 1, tiny_threshold=1 << 20)
+            tb = [torch.empty(n, dtype=torch.uint8, device=dev) for n in sizes]
+            for i, b in enumerate(tb):
+                ros.synth_bf16(b, 910 + i)
+                assert t.register_tensor(0, f"w{i}", b) == Status.ok
+            torch.cuda.synchronize()
+            sc.open(t)
+            assert sc.publish(t, 1).status == Status.ok
+            v1 = ros.digest_spans([b.data_ptr() for b in tb], sizes, 0)
+            r = sc.unpublish(t)
+            out = {"unpublish": int(r.status), "lanes": t.lanes(), "v1": v1}
+            for i, b in enumerate(tb):
+                ros.synth_bf16(b, 1910 + i)
+            torch.cuda.synchronize()
+            out["publish2"] = int(sc.publish(t, 2).status)
+            q.put(("trainer", out))
+            ev.wait(120)
+            sc.sync()
+            q.put(("trainer2", {"view": sc.local.view("m", "trainer+offload@1")}))
+        else:
+            r = sc.create("m", "reader", 1, tiny_threshold=1 << 20)
+            rb = [torch.zeros(n, dtype=torch.uint8, device=dev) for n in sizes]
+            for i, b in enumerate(rb):
+                assert r.register_tensor(0, f"w{i}", b) == Status.ok
+            sc.open(r)
+            res = sc.replicate(r, "1")
+            q.put(("reader", {"status": int(res.status), "v": res.version,
+                              "digests": ros.digest_spans([b.data_ptr() for b in rb], sizes, 0),
+                              "plan": [(a.replica, a.src) for a in sc.assigns()]}))
+            ev.set()
+        sc.close()
+    except Exception as e:  # pragma: no cover - surfaced by the parent
+        import traceback
+        q.put((role, {"error": repr(e) + traceback.format_exc()}))
+        ev.set()
+
+
+def test_retention_offload_through_the_op_log():
+    """The last durable copy of a retained version unpublishes: its process
+    parks it in pinned host memory (POSIX shm) and announces the lane through
+    the log; a reader process that joins afterwards replicates that version
+    from the lane (copy-engine frames verified in place by its pull kernel)
+    and, once a worker holds it again, the registry releases the offload."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import multiprocessing as mp
+    from paper_2604_09107_b200.shared import LogServer
+    log = LogServer()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    ev = ctx.Event()
+    tr = ctx.Process(target=_retention_member, args=("trainer", log.port, q, ev))
+    tr.start()
+    procs = [tr]
+    try:
+        who, out = q.get(timeout=300)
+        assert who == "trainer" and "error" not in out, out
+        assert out["unpublish"] == 0 and out["lanes"] == [1] and out["publish2"] == 0
+        rd = ctx.Process(target=_retention_member, args=("reader", log.port, q, ev))
+        rd.start()
+        procs.append(rd)
+        res = dict(q.get(timeout=300) for _ in range(2))
+        assert "error" not in res["reader"], res["reader"]
+        assert res["reader"]["status"] == 0 and res["reader"]["v"] == 1
+        assert res["reader"]["digests"] == out["v1"]
+        assert ("reader", "trainer+offload@1") in res["reader"]["plan"]
+        assert res["trainer2"]["view"] is None  # released once a worker holds v1
+    finally:
+        ev.set()
+        for p in procs:
+            p.join(timeout=60)
+        log.close()
