@@ -1909,6 +1909,7 @@ Status Client::resolve_shard(Shard& sh, const std::string& replica, std::uint32_
 
 Status Client::launch_reshard_fill(Shard& sh, const Assignment& a, bool src_complete) {
   DeviceGuard g(sh.device);
+  PhaseClock pc;
   Payload& p = *sh.holding;
   Reshard& rs = *p.reshard;
   const auto nsrc = static_cast<std::uint32_t>(rs.srcs.size());
@@ -1926,6 +1927,7 @@ Status Client::launch_reshard_fill(Shard& sh, const Assignment& a, bool src_comp
              src_complete ? nullptr : reinterpret_cast<const std::uint32_t*>(views[s].flags),
              views[s].epoch, 0};
   }
+  pc.mark("reshard fill: resolve sources");
   std::vector<int> src_dev(nsrc, sh.device);
   for (std::uint32_t s = 0; s < nsrc; ++s)
     if (need[s]) src_dev[s] = views[s].device;
@@ -2002,9 +2004,11 @@ Status Client::launch_reshard_fill(Shard& sh, const Assignment& a, bool src_comp
   bool remote = false;
   for (std::uint32_t s = 0; s < nsrc; ++s) remote |= need[s] && src_dev[s] != sh.device;
   dev::PullParams pp{};
+  pc.mark("reshard fill: segments");
   RS_CUDA(dev::upload_pull_plan(sh.device, sh.stream, descs.data(),
                                 static_cast<std::uint32_t>(descs.size()), sd.data(), nsrc, next,
                                 &sh.plan, &pp));
+  pc.mark("reshard fill: plan upload");
   stats_.h2d_bytes += sh.plan.h2d_bytes;
   pp.dst_digests = static_cast<std::uint64_t*>(p.digests.p);
   pp.dst_flags = static_cast<std::uint32_t*>(p.flags.p);
@@ -2016,11 +2020,14 @@ Status Client::launch_reshard_fill(Shard& sh, const Assignment& a, bool src_comp
   RS_CUDA(dev::launch_pull(pp, grid(sh), sh.stream));
   stats_.kernel_launches += dev::pull_has_work(pp) ? 1 : 0;
   RS_CUDA(cudaEventRecord(sh.ev1, sh.stream));
+  pc.mark("reshard fill: launched");
   p.landed_some = true;
   // the follow-up (slice copies, packing, re-digests) queued right behind the
   // fill, skipped on the device if it fails: no host round trip in between
   auto* code = &reinterpret_cast<dev::PullStatus*>(static_cast<std::uint8_t*>(sh.plan.scratch) + 64)->code;
-  return finish_reshard(sh, code);
+  Status fs = finish_reshard(sh, code);
+  pc.mark("reshard fill: follow-up queued");
+  return fs;
 }
 
 Status Client::finish_reshard(Shard& sh, const std::uint32_t* guard) {
@@ -2224,6 +2231,7 @@ Status Client::replicate(const VersionSpec& spec, VersionId* out, double wait_s)
   if (!opened_) {
     if (Status s = open(); !ok(s)) return s;
   }
+  PhaseClock pc;
   apply_releases();
   OpOutcome o;
   Status s = reg_->replicate(model_, replica_, spec, &o);
@@ -2231,6 +2239,7 @@ Status Client::replicate(const VersionSpec& spec, VersionId* out, double wait_s)
   if (!o.done) o = reg_->wait_op(model_, replica_, wait_s);
   if (!o.done) return Status::timeout;
   if (!ok(o.status)) return o.status;
+  pc.mark("replicate: registry");
   s = run_replicate_loop(o, *o.version);
   if (ok(s) && out) *out = *o.version;
   return s;
