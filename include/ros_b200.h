@@ -25,7 +25,7 @@
 extern "C" {
 #endif
 
-#define RS_ABI_VERSION 2
+#define RS_ABI_VERSION 3
 
 typedef struct rs_cluster rs_cluster; /* ServerCore + ServeRegistry of this process */
 typedef struct rs_handle rs_handle;   /* ClientCore: one replica's shard handles   */
@@ -51,6 +51,11 @@ typedef struct {
                             * readers pull meanwhile.  The committed manifest is the
                             * reference's, byte for byte (rs_publish_finalize waits
                             * for it).  Default 0: the reference order.            */
+  int offload_seed;        /* ClientConfig.offload_seed (config.hpp): an update whose
+                            * source is in another datacenter fills the version into
+                            * pinned host memory in the background (replica
+                            * "<replica>+seed@<v>") and reports no change; a later
+                            * update consumes that seed locally.  Default 0.       */
 } rs_config;
 
 /* Assignment (reference messages.hpp:40-52) minus the manifest bytes, which
@@ -106,6 +111,8 @@ int rs_cluster_view(rs_cluster* c, const char* model, const char* replica, char*
 /* ReplicaView.min_progress (server_core.hpp:48): the fewest verified items
  * over the replica's shards, as its fills report them (ProgressMsg,
  * client_core.cpp:1414-1439) -- it advances while a fill runs. */
+/* ReplicaView.seeding: the replica fills from another datacenter */
+int rs_cluster_seeding(rs_cluster* c, const char* model, const char* replica, int* seeding);
 int rs_cluster_progress(rs_cluster* c, const char* model, const char* replica,
                         uint64_t* min_progress);
 /* The source replica a replicating replica currently pulls from ("" if none). */
@@ -307,6 +314,30 @@ int rs_server_take_releases(rs_cluster* c, const char* model, const char* owner,
                             uint64_t* versions, size_t cap, size_t* n);
 int rs_cluster_kind(rs_cluster* c, const char* model, const char* replica, char* buf, size_t cap,
                     size_t* len);  /* "worker" | "offload" */
+
+/* ---- cross-link seed buffers (client_core.cpp:1720-1812; server_core.cpp
+ * 88-99, 915-970, 1124-1204) ------------------------------------------------
+ * With rs_config.offload_seed, rs_update against a source in another
+ * datacenter returns changed = 0 and starts a background fill of the version
+ * into pinned host memory (the pull kernel lands it over PCIe, verifying
+ * every chunk); the registry masks the version for this datacenter until the
+ * seed completes, then plans same-datacenter readers onto it, and the
+ * owner's next rs_update consumes it locally (local_seed_consume).  The seed
+ * is released once consumed and drained (rs_poll frees it). */
+int rs_seed_lanes(rs_handle* h, uint64_t* versions, size_t cap, size_t* n);  /* after the fill */
+int rs_seed_wait(rs_handle* h);  /* wait for a running seed fill (and its report) */
+int rs_server_set_offload_seed(rs_cluster* c, const char* model, const char* replica, int on);
+/* the shard's assignment in the replica's last replicate/update outcome */
+int rs_server_assignment(rs_cluster* c, const char* model, const char* replica, uint32_t shard,
+                         rs_assignment* out);
+/* 1 (and the shard's seed assignment) when the replica's last update started a seed */
+int rs_server_seed_start(rs_cluster* c, const char* model, const char* replica, uint32_t shard,
+                         rs_assignment* out);
+/* ProgressMsg / CompleteMsg with TransferRole::seed for the seed of `version` */
+int rs_server_seed_progress(rs_cluster* c, const char* model, const char* replica, uint32_t shard,
+                            uint64_t items, uint64_t version);
+int rs_server_seed_complete(rs_cluster* c, const char* model, const char* replica, uint32_t shard,
+                            int outcome, uint64_t version);
 
 /* ---- off-box data plane (transport_stream.hpp:36-76)
  * Serve this process's serve states over TCP (port 0: any free port).  A

@@ -87,6 +87,7 @@ def ref():
         lib.ref_cluster_new.restype = C.c_void_p
         lib.ref_cluster_new.argtypes = [C.c_int, C.c_int, C.c_int, C.c_uint64]
         lib.ref_cluster_add.argtypes = [C.c_void_p, C.c_char_p, C.c_uint32, C.c_uint64, C.c_uint64]
+        lib.ref_cluster_add_dc.argtypes = [C.c_void_p, C.c_char_p, C.c_uint32, C.c_char_p, C.c_int]
         lib.ref_cluster_register.argtypes = [C.c_void_p, C.c_char_p, C.c_uint32, C.c_char_p, C.c_void_p,
                                              C.c_uint64]
         lib.ref_cluster_register_modeled.argtypes = [C.c_void_p, C.c_char_p, C.c_uint32, C.c_char_p,
@@ -302,6 +303,10 @@ class RefCluster:
 
     def add(self, replica, shards=1, tiny=0, target=0):
         self.lib.ref_cluster_add(self.h, replica.encode(), shards, tiny, target)
+
+    def add_dc(self, replica, shards=1, dc="dc0", offload_seed=False):
+        """A replica with ClientConfig.datacenter / offload_seed set."""
+        self.lib.ref_cluster_add_dc(self.h, replica.encode(), shards, dc.encode(), int(offload_seed))
 
     def register(self, replica, shard, name, arr: np.ndarray):
         assert arr.flags.c_contiguous

@@ -261,6 +261,24 @@ int ref_cluster_add(void* h, const char* replica, std::uint32_t shards,
   return 0;
 }
 
+// ref_cluster_add with ClientConfig.datacenter and ClientConfig.offload_seed
+// (the cross-link seeding scenario, test_client_core.cpp:460-503).
+int ref_cluster_add_dc(void* h, const char* replica, std::uint32_t shards, const char* dc,
+                       int offload_seed) {
+  auto* c = static_cast<Cluster*>(h);
+  ref_cluster_add(h, replica, shards, 0, 0);
+  auto& n = *c->nodes.at(replica);
+  ClientConfig cfg = c->base_cfg;
+  cfg.data_endpoint = std::string("ep:") + replica;
+  cfg.datacenter = dc;
+  cfg.offload_seed = offload_seed != 0;
+  Executor* ex = &c->sim;
+  if (c->threaded) ex = n.texec.get();
+  n.core = std::make_unique<ClientCore>("m", replica, shards, cfg, ex, &c->log, &c->net, &c->net,
+                                        &n.serves);
+  return 0;
+}
+
 int ref_cluster_register(void* h, const char* replica, std::uint32_t shard,
                          const char* name, void* ptr, std::uint64_t len) {
   auto* c = static_cast<Cluster*>(h);

@@ -26,7 +26,7 @@ class RsConfig(C.Structure):
     _fields_ = [("chunk_bytes", u64), ("tiny_threshold", u64), ("group_target", u64),
                 ("pipeline", i32), ("checksum_retries", i32), ("pull_timeout_s", dbl),
                 ("datacenter", C.c_char * 32), ("reshard_align", u32),
-                ("grid_sms", u32), ("early_publish", i32)]
+                ("grid_sms", u32), ("early_publish", i32), ("offload_seed", i32)]
 
 
 class RsAssignment(C.Structure):
@@ -56,6 +56,7 @@ _SIGS = {
     "rs_cluster_set_silent": (i32, [vp, cstr, cstr, i32]),
     "rs_cluster_set_topology": (i32, [vp, u32, vp, vp]),
     "rs_cluster_progress": (i32, [vp, cstr, cstr, C.POINTER(u64)]),
+    "rs_cluster_seeding": (i32, [vp, cstr, cstr, C.POINTER(i32)]),
     "rs_cluster_source": (i32, [vp, cstr, cstr, vp, sz, C.POINTER(sz)]),
     "rs_open": (i32, [vp, cstr, cstr, u32, C.POINTER(RsConfig), C.POINTER(vp)]),
     "rs_register": (i32, [vp, u32, cstr, vp, u64]),
@@ -73,6 +74,13 @@ _SIGS = {
     "rs_offload_release": (i32, [vp, u64]),
     "rs_poll": (i32, [vp]),
     "rs_lanes": (i32, [vp, vp, sz, C.POINTER(sz)]),
+    "rs_seed_lanes": (i32, [vp, vp, sz, C.POINTER(sz)]),
+    "rs_seed_wait": (i32, [vp]),
+    "rs_server_set_offload_seed": (i32, [vp, cstr, cstr, i32]),
+    "rs_server_assignment": (i32, [vp, cstr, cstr, u32, C.POINTER(RsAssignment)]),
+    "rs_server_seed_start": (i32, [vp, cstr, cstr, u32, C.POINTER(RsAssignment)]),
+    "rs_server_seed_progress": (i32, [vp, cstr, cstr, u32, u64, u64]),
+    "rs_server_seed_complete": (i32, [vp, cstr, cstr, u32, i32, u64]),
     "rs_server_set_retention": (i32, [vp, cstr, cstr, vp, sz]),
     "rs_server_offload_pending": (i32, [vp, cstr, cstr, C.POINTER(u64)]),
     "rs_server_offload_confirm": (i32, [vp, cstr, cstr, u32, u64, i32, cstr]),

@@ -63,6 +63,7 @@ rsb::ClientConfig to_cfg(const rs_config* c) {
   if (c->reshard_align) cfg.reshard_align = c->reshard_align;
   cfg.grid_sms = c->grid_sms;
   cfg.early_publish = c->early_publish != 0;
+  cfg.offload_seed = c->offload_seed != 0;
   return cfg;
 }
 
@@ -114,6 +115,7 @@ void rs_config_default(rs_config* cfg) {
   cfg->reshard_align = d.reshard_align;
   cfg->grid_sms = d.grid_sms;
   cfg->early_publish = d.early_publish ? 1 : 0;
+  cfg->offload_seed = d.offload_seed ? 1 : 0;
 }
 
 int rs_cluster_create(int pipeline, int smart_skipping, rs_cluster** out) {
@@ -157,6 +159,14 @@ int rs_cluster_view(rs_cluster* c, const char* model, const char* replica, char*
   if (version) *version = v->version.value_or(0);
   if (serving) *serving = v->serving;
   if (visible) *visible = v->visible;
+  return 0;
+}
+
+int rs_cluster_seeding(rs_cluster* c, const char* model, const char* replica, int* seeding) {
+  if (!c || !model || !replica || !seeding) return st(rsb::Status::invalid_argument);
+  auto v = c->reg.view(model, replica);
+  if (!v) return st(rsb::Status::not_found);
+  *seeding = v->seeding;
   return 0;
 }
 
@@ -548,6 +558,59 @@ int rs_server_complete(rs_cluster* c, const char* model, const char* replica, ui
                        int outcome) {
   if (!c || !model || !replica) return st(rsb::Status::invalid_argument);
   c->reg.complete(model, replica, shard, static_cast<rsb::Status>(outcome));
+  return 0;
+}
+
+int rs_server_set_offload_seed(rs_cluster* c, const char* model, const char* replica, int on) {
+  if (!c || !model || !replica) return st(rsb::Status::invalid_argument);
+  return st(c->reg.set_offload_seed(model, replica, on != 0));
+}
+
+int rs_server_assignment(rs_cluster* c, const char* model, const char* replica, uint32_t shard,
+                         rs_assignment* out) {
+  if (!c || !model || !replica || !out) return st(rsb::Status::invalid_argument);
+  auto o = c->reg.op_result(model, replica);
+  if (!o.done || shard >= o.assignments.size()) return st(rsb::Status::not_found);
+  fill_assignment(o.assignments[shard], out);
+  return 0;
+}
+
+int rs_server_seed_start(rs_cluster* c, const char* model, const char* replica, uint32_t shard,
+                         rs_assignment* out) {
+  if (!c || !model || !replica) return 0;
+  auto o = c->reg.op_result(model, replica);
+  if (!o.done || !o.seed || shard >= o.seed->assignments.size()) return 0;
+  if (out) fill_assignment(o.seed->assignments[shard], out);
+  return 1;
+}
+
+int rs_server_seed_progress(rs_cluster* c, const char* model, const char* replica, uint32_t shard,
+                            uint64_t items, uint64_t version) {
+  if (!c || !model || !replica) return st(rsb::Status::invalid_argument);
+  c->reg.progress(model, replica, shard, items, true, version);
+  return 0;
+}
+
+int rs_server_seed_complete(rs_cluster* c, const char* model, const char* replica, uint32_t shard,
+                            int outcome, uint64_t version) {
+  if (!c || !model || !replica) return st(rsb::Status::invalid_argument);
+  c->reg.complete(model, replica, shard, static_cast<rsb::Status>(outcome), true, version);
+  return 0;
+}
+
+int rs_seed_lanes(rs_handle* h, uint64_t* versions, size_t cap, size_t* n) {
+  if (!h) return st(rsb::Status::invalid_argument);
+  h->client->join_seed();
+  auto vs = h->client->seed_lanes();
+  if (n) *n = vs.size();
+  if (versions)
+    for (size_t i = 0; i < vs.size() && i < cap; ++i) versions[i] = vs[i];
+  return 0;
+}
+
+int rs_seed_wait(rs_handle* h) {
+  if (!h) return st(rsb::Status::invalid_argument);
+  h->client->join_seed();
   return 0;
 }
 

@@ -584,6 +584,7 @@ Client::Client(Registry* reg, ServeRegistry* serves, std::string model, std::str
 
 Client::~Client() {
   if (fin_thread_.joinable()) fin_thread_.join();
+  join_seed();
   stop_serving();
   for (auto& sh : shards_) {
     if (sh.device < 0) continue;
@@ -600,6 +601,10 @@ Client::~Client() {
     dev::free_pull_plan(sh.device, &sh.plan);
     dev::free_pull_plan(sh.device, &sh.hash_plan);
     dev::free_pull_plan(sh.device, &sh.fuse_plan);
+    dev::free_pull_plan(sh.device, &sh.seed_plan);
+    if (sh.seed_ev) cudaEventDestroy(sh.seed_ev);
+    if (sh.seed_stream) cudaStreamDestroy(sh.seed_stream);
+    for (auto& [v, lane] : sh.seed_lanes) serves_->erase(lane.key);
   }
 }
 
@@ -730,6 +735,7 @@ Status Client::open() {
   if (Status s = derived_blobs(&dman, &dlay); !ok(s)) return s;
   Status s = reg_->open(model_, replica_, num_shards_, cfg_.dc, eps, layout_key(), dman, dlay);
   if (ok(s) && !retain_.empty()) s = reg_->set_retention(model_, replica_, retain_);
+  if (ok(s) && cfg_.offload_seed) s = reg_->set_offload_seed(model_, replica_, true);
   if (ok(s)) opened_ = true;
   return s;
 }
@@ -1806,7 +1812,15 @@ std::vector<Client::FillOutcome> Client::wait_shards(const std::vector<std::uint
     stats_.fill_sum_ms += ms;
     stats_.fill_bytes += st[i].bytes;
     stats_.last_pull_launches = 1;
-    stats_.bytes_pulled += st[i].bytes;
+    // Stats (client_core.hpp:44-52): a local seed consumption is a local
+    // copy, not a pull; a pull over the cross-datacenter link counts twice
+    const auto& la = i < launch_as_.size() ? launch_as_[i] : std::optional<Assignment>{};
+    if (la && la->local_seed_consume) {
+      stats_.bytes_copied_local += st[i].bytes;
+    } else {
+      stats_.bytes_pulled += st[i].bytes;
+      if (la && la->cross_dc) stats_.bytes_pulled_cross_dc += st[i].bytes;
+    }
     stats_.checksum_failures += st[i].retried_batches;
     switch (st[i].code) {
       case dev::kPullOk:
@@ -2260,6 +2274,9 @@ Status Client::update(const VersionSpec& spec, bool* changed, VersionId* out, do
   if (changed) *changed = o.changed;
   if (!o.changed) {
     if (out && o.version) *out = *o.version;
+    // still on what we hold; the reply may start a background seed fill
+    // (client_core.cpp:1331-1337)
+    if (o.seed) return start_seed(*o.seed);
     return Status::ok;
   }
   s = run_replicate_loop(o, *o.version);
@@ -2269,6 +2286,7 @@ Status Client::update(const VersionSpec& spec, bool* changed, VersionId* out, do
 
 Status Client::close() {
   join_finalize();
+  join_seed();
   closed_ = true;
   stop_serving();
   for (auto& sh : shards_) serves_->erase(ServeRegistry::key(model_, replica_, sh.idx));
@@ -2421,13 +2439,226 @@ void Client::release_lane(VersionId v) {
 }
 
 void Client::apply_releases() {
-  for (const auto& r : reg_->take_releases(model_, replica_)) release_lane(r.version);
+  for (const auto& r : reg_->take_releases(model_, replica_)) {
+    if (r.seed) release_seed_lane(r.version);
+    else release_lane(r.version);
+  }
 }
 
 std::vector<VersionId> Client::lanes() const {
   std::set<VersionId> vs;
   for (const auto& sh : shards_)
     for (const auto& [v, lane] : sh.lanes) vs.insert(v);
+  return {vs.begin(), vs.end()};
+}
+
+// ---- cross-link seed buffers ----------------------------------------------
+
+Status Client::launch_seed(Shard& sh, const Assignment& a) {
+  // start_seed_fill (client_core.cpp:1720-1770): the lane is this replica's
+  // serve state "<replica>+seed@<v>", items in pinned host memory (POSIX
+  // shm, device-mapped) with its chunk-digest table beside them.  The pull
+  // kernel lands the source's bytes there over PCIe, verifying every chunk
+  // against the source's table and writing the lane's own.
+  if (a.reshard) return Status::invalid_argument;  // seeds hold the source's slicing
+  auto mr = Manifest::decode(a.manifest);
+  if (!mr) return Status::protocol_error;
+  const VersionId v = a.version;
+  if (sh.seed_lanes.count(v)) return Status::ok;  // already seeded (start ignored)
+  if (Status s = ensure_stream(sh); !ok(s)) return s;
+  DeviceGuard g(sh.device);
+  const auto& items = mr->items();
+  ChunkMap cm = ChunkMap::uniform(*mr, cfg_.chunk_bytes);
+  if (!a.layout.empty()) {
+    auto lay = ShardLayout::decode(a.layout);
+    if (!lay || lay->chunk_len.size() != items.size()) return Status::protocol_error;
+    cm = ChunkMap::from_lens(*mr, lay->chunk_len);
+  }
+  std::vector<std::uint64_t> off(items.size());
+  std::uint64_t tot = 0, bytes = 0;
+  for (std::size_t i = 0; i < items.size(); ++i) {
+    off[i] = tot;
+    tot += (items[i].length + 255) / 256 * 256;
+    bytes += items[i].length;
+  }
+  const std::uint64_t dig_off = tot;
+  tot += std::uint64_t(cm.n_chunks()) * 8;
+  Shard::SeedLane lane;
+  for (auto it = host_pool_.begin(); it != host_pool_.end(); ++it)
+    if ((*it)->n >= tot) {
+      lane.buf = std::move(*it);
+      host_pool_.erase(it);
+      break;
+    }
+  if (!lane.buf) {
+    lane.buf = std::make_unique<HostBuf>();
+    if (Status s = lane.buf->alloc(tot); !ok(s)) return s;
+  }
+  auto* base = static_cast<std::uint8_t*>(lane.buf->p);
+  // the source: a serve state in this process (or imported), or off-box
+  SourceView view;
+  if (a.source_endpoint.rfind("tcp:", 0) == 0) {
+    lane.tcp = std::make_shared<StreamSource>();
+    Status s = lane.tcp->open(a.source_endpoint, ServeRegistry::key(model_, a.source_replica, sh.idx),
+                              v, cfg_.pull_timeout_s, &host_pool_);
+    if (!ok(s)) {
+      lane.tcp->release(&host_pool_);
+      return s;
+    }
+    view = lane.tcp->view();
+  } else if (Status s = resolve_source(sh, a, v, &view, cfg_.pull_timeout_s); !ok(s)) {
+    return s;
+  }
+  if (!(view.cmap == cm)) {
+    if (lane.tcp) lane.tcp->release(&host_pool_);
+    return Status::protocol_error;
+  }
+  std::vector<dev::ItemDesc> descs(items.size());
+  for (std::size_t i = 0; i < items.size(); ++i) {
+    descs[i] = identity_segment(view.item_ptrs[i], reinterpret_cast<std::uint64_t>(base + off[i]),
+                                items[i].length, cm, i);
+    descs[i].pad = 1;  // host-memory landing: no tensor maps (generic bulk stores)
+  }
+  const bool src_complete = a.source_complete && !lane.tcp;
+  dev::SrcDesc sdesc{reinterpret_cast<const std::uint64_t*>(view.digests),
+                     src_complete ? nullptr : reinterpret_cast<const std::uint32_t*>(view.flags),
+                     view.epoch, 0};
+  if (!sh.seed_stream) RS_CUDA(cudaStreamCreateWithFlags(&sh.seed_stream, cudaStreamNonBlocking));
+  if (!sh.seed_ev) RS_CUDA(cudaEventCreateWithFlags(&sh.seed_ev, cudaEventDisableTiming));
+  dev::PullParams pp{};
+  RS_CUDA(dev::upload_pull_plan(sh.device, sh.seed_stream, descs.data(),
+                                static_cast<std::uint32_t>(descs.size()), &sdesc, 1, cm.n_chunks(),
+                                &sh.seed_plan, &pp));
+  stats_.h2d_bytes += sh.seed_plan.h2d_bytes;
+  pp.dst_digests = reinterpret_cast<std::uint64_t*>(base + dig_off);
+  pp.dst_flags = nullptr;  // not served while it fills (seeding copies are never chased)
+  pp.dst_epoch = 1;
+  pp.timeout_ns = static_cast<std::uint64_t>(cfg_.pull_timeout_s * 1e9);
+  pp.remote = view.device >= 0 && view.device != sh.device ? 1u : 0u;
+  // A PCIe-bound background fill: a few SMs, beside whatever else runs.
+  RS_CUDA(dev::launch_pull(pp, std::min(grid(sh), 16), sh.seed_stream));
+  stats_.kernel_launches += dev::pull_has_work(pp) ? 1 : 0;
+  RS_CUDA(cudaEventRecord(sh.seed_ev, sh.seed_stream));
+  lane.key = ServeRegistry::key(model_, replica_ + "+seed@" + std::to_string(v), sh.idx);
+  lane.serve = serves_->ensure(lane.key);
+  {
+    std::vector<std::uint64_t> ends, ptrs;
+    for (std::size_t i = 0; i < items.size(); ++i) {
+      ends.push_back(items[i].stream_offset + items[i].length);
+      ptrs.push_back(reinterpret_cast<std::uint64_t>(base + off[i]));
+    }
+    std::lock_guard lk(lane.serve->m);
+    lane.serve->serving = false;  // until the fill verified every chunk
+    lane.serve->imported = false;
+    lane.serve->version = v;
+    lane.serve->complete = false;
+    lane.serve->progress = 0;
+    lane.serve->device = -1;
+    lane.serve->pid = static_cast<int>(getpid());
+    lane.serve->item_ends = std::move(ends);
+    lane.serve->item_ptrs = std::move(ptrs);
+    lane.serve->cmap = cm;
+    lane.serve->digests = reinterpret_cast<std::uint64_t>(base + dig_off);
+    lane.serve->flags = 0;
+    lane.serve->epoch = 1;
+    lane.serve->host_name = lane.buf->name;
+    lane.serve->host_size = lane.buf->n;
+    lane.serve->host_base = reinterpret_cast<std::uint64_t>(base);
+  }
+  sh.seed_lanes.emplace(v, std::move(lane));
+  (void)bytes;
+  return Status::ok;
+}
+
+Status Client::start_seed(const SeedStart& ss) {
+  join_seed();  // a fill of a stale target ends first (its report is ignored)
+  struct Job {
+    std::uint32_t shard;
+    int device;
+    cudaEvent_t ev;
+    const dev::PullStatus* status;
+    std::shared_ptr<ServeState> serve;
+    std::shared_ptr<StreamSource> tcp;
+    std::uint64_t bytes, items;
+  };
+  std::vector<Job> jobs;
+  for (auto& sh : shards_) {
+    if (sh.device < 0 || sh.idx >= ss.assignments.size()) continue;
+    const bool had = sh.seed_lanes.count(ss.version) != 0;
+    Status s = launch_seed(sh, ss.assignments[sh.idx]);
+    if (!ok(s)) {
+      reg_->complete(model_, replica_, sh.idx, s, true, ss.version);
+      continue;
+    }
+    if (had) continue;
+    auto& lane = sh.seed_lanes.at(ss.version);
+    std::uint64_t bytes = 0;
+    for (std::size_t i = 0; i < lane.serve->item_ends.size(); ++i)
+      bytes += lane.serve->item_ends[i] - (i ? lane.serve->item_ends[i - 1] : 0);
+    jobs.push_back({sh.idx, sh.device, sh.seed_ev,
+                    reinterpret_cast<const dev::PullStatus*>(
+                        static_cast<std::uint8_t*>(sh.seed_plan.scratch) + 64),
+                    lane.serve, lane.tcp, bytes, lane.serve->item_ends.size()});
+  }
+  if (jobs.empty()) return Status::ok;
+  // The waiter touches only what it was handed (events, status words, the
+  // lanes' serve states) and the registry (its own lock).
+  seed_thread_ = std::thread([this, jobs = std::move(jobs), v = ss.version] {
+    for (const auto& j : jobs) {
+      DeviceGuard g(j.device);
+      cudaError_t e = cudaEventSynchronize(j.ev);
+      dev::PullStatus st{};
+      if (e == cudaSuccess) e = cudaMemcpy(&st, j.status, sizeof(st), cudaMemcpyDeviceToHost);
+      bool good = e == cudaSuccess && st.code == dev::kPullOk;
+      if (j.tcp) good = ok(j.tcp->finish(good)) && good;
+      if (good) {
+        std::lock_guard lk(j.serve->m);
+        j.serve->serving = true;
+        j.serve->complete = true;
+        j.serve->progress = j.items;
+        seed_cross_dc_ += j.bytes;
+      }
+      const Status out = good ? Status::ok
+                         : e != cudaSuccess ? Status::transfer_failed
+                         : st.code == dev::kPullChecksum ? Status::checksum_mismatch
+                         : Status::timeout;
+      if (good) reg_->progress(model_, replica_, j.shard, j.items, true, v);
+      reg_->complete(model_, replica_, j.shard, out, true, v);
+    }
+  });
+  return Status::ok;
+}
+
+void Client::join_seed() {
+  if (seed_thread_.joinable()) seed_thread_.join();
+  for (auto& sh : shards_)  // off-box sources' pinned buffers back to the pool
+    for (auto& [v, lane] : sh.seed_lanes)
+      if (lane.tcp) {
+        lane.tcp->release(&host_pool_);
+        lane.tcp.reset();
+      }
+}
+
+void Client::release_seed_lane(VersionId v) {
+  // DirectiveKind::offload_release, purpose seed (client_core.cpp:1773-1794)
+  join_seed();
+  for (auto& sh : shards_) {
+    auto it = sh.seed_lanes.find(v);
+    if (it == sh.seed_lanes.end()) continue;
+    {
+      std::lock_guard lk(it->second.serve->m);
+      it->second.serve->serving = false;
+    }
+    serves_->erase(it->second.key);
+    if (host_pool_.size() < 2) host_pool_.push_back(std::move(it->second.buf));
+    sh.seed_lanes.erase(it);
+  }
+}
+
+std::vector<VersionId> Client::seed_lanes() const {
+  std::set<VersionId> vs;
+  for (const auto& sh : shards_)
+    for (const auto& [v, lane] : sh.seed_lanes) vs.insert(v);
   return {vs.begin(), vs.end()};
 }
 

@@ -55,6 +55,11 @@ struct ClientConfig {
   // 1.05 GB Llama-3-8B embedding -- when they are done.  The committed
   // manifest is the reference's, byte for byte; only its arrival is later.
   bool early_publish = false;
+  // Host-memory seeding (ClientConfig.offload_seed, config.hpp): an update
+  // whose source is in another datacenter fills "<replica>+seed@<v>" in
+  // pinned host memory in the background and stays on its version; a later
+  // update consumes the seed locally (PCIe, no cross-link traffic).
+  bool offload_seed = false;
 };
 
 // Owned device allocation.
@@ -295,7 +300,13 @@ class Client {
 
   std::optional<VersionId> current_version() const { return current_; }
   bool is_published() const { return published_; }
-  const ClientStats& stats() const { return stats_; }
+  ClientStats stats() const {
+    ClientStats s = stats_;
+    const std::uint64_t seeded = seed_cross_dc_.load();  // background seed fills
+    s.bytes_pulled += seeded;
+    s.bytes_pulled_cross_dc += seeded;
+    return s;
+  }
   const std::string& model() const { return model_; }
   const std::string& replica() const { return replica_; }
   std::uint32_t num_shards() const { return num_shards_; }
@@ -323,6 +334,15 @@ class Client {
   // Free the lanes the registry released (DirectiveKind::offload_release).
   void apply_releases();
   std::vector<VersionId> lanes() const;
+  // --- cross-link seed buffers (client_core.cpp:1720-1812) ---------------
+  // Starts the background fill of every local shard's seed lane (an update's
+  // SeedStart); its completion is reported to the registry by a waiter
+  // thread (role seed).  The split phase calls it with the outcome of
+  // Registry::update.
+  Status start_seed(const SeedStart& ss);
+  // Waits for a running seed fill (its registry report included).
+  void join_seed();
+  std::vector<VersionId> seed_lanes() const;
   std::string endpoint(std::uint32_t shard) const { return shards_[shard].endpoint; }
 
  private:
@@ -403,12 +423,24 @@ class Client {
       std::string endpoint;
     };
     std::map<VersionId, Lane> lanes;  // retention offloads held for the registry
+    struct SeedLane {
+      std::string key;
+      std::shared_ptr<ServeState> serve;
+      std::unique_ptr<HostBuf> buf;
+      std::shared_ptr<StreamSource> tcp;  // the fill's off-box source
+    };
+    std::map<VersionId, SeedLane> seed_lanes;  // seed buffers (filling or complete)
+    cudaStream_t seed_stream = nullptr;
+    cudaEvent_t seed_ev = nullptr;
+    dev::PlanUpload seed_plan;
     std::shared_ptr<StreamSource> tcp;  // the fill's source when it is off-box (tcp:)
     // early publish: K6 over the big entries on its own stream
     cudaStream_t k6 = nullptr;
     DevBuf k6_tables;
   };
   Status make_retention_lane(Shard& sh, VersionId v, std::string* endpoint);
+  Status launch_seed(Shard& sh, const Assignment& a);
+  void release_seed_lane(VersionId v);
   Status settle_offload(OpOutcome* o, double wait_s);
 
   Status ensure_stream(Shard& sh);
@@ -475,6 +507,9 @@ class Client {
   VersionId fin_v_ = 0;
   std::vector<std::string> fin_manifests_;  // per shard ("" for a non-local shard)
   std::vector<bool> launched_;
+  // seed fill waiter (reports role-seed completion to the registry)
+  std::thread seed_thread_;
+  std::atomic<std::uint64_t> seed_cross_dc_{0};
   std::vector<std::optional<Assignment>> launch_as_;  // per shard: the latest launch's assignment
   bool published_ = false;
   bool opened_ = false;

@@ -115,7 +115,7 @@ Status Registry::close(const std::string& model, const std::string& replica) {
     if (o->kind == Kind::offload && o->owner == replica) owned.push_back(name);
   for (const auto& name : owned) {
     auto it = m.reps.find(name);
-    const VersionId v = *it->second->version;
+    const VersionId v = it->second->offload_v;
     trace("offload_dropped", {{"model", model}, {"replica", name}, {"reason", "owner_closed"}});
     m.reps.erase(it);
     prune_version(m, v);
@@ -185,7 +185,8 @@ Registry::Rep* Registry::pick_source(ModelState& m, VersionId v,
   // the box is uniform: same slicing first, then topology cost.
   auto key = [&](const Rep* c) {
     const std::string& ep0 = c->endpoints.empty() ? c->name : c->endpoints[0];
-    return std::make_tuple(1 /* no own seed buffers */, c->dc == reader.dc ? 0 : 1,
+    const bool own_seed = c->kind == Kind::offload && c->seed && c->owner == reader.name;
+    return std::make_tuple(own_seed ? 0 : 1, c->dc == reader.dc ? 0 : 1,
                            c->layout == slicing(reader.layout) ? 0 : 1, topo_(rep0, ep0), c->serving,
                            c->last_assigned, std::cref(c->name));
   };
@@ -481,6 +482,53 @@ void Registry::start_update(Rep& r) {
   if (!servable(m, *target, r)) return finish_op(r, Status::invalid_argument);
   Rep* src = pick_source(m, *target, r);
   if (!src) return no_change();
+  // A change over the cross-datacenter link with host seeding on: fill a
+  // seed buffer in the background and stay on the current version until it
+  // lands (server_core.cpp:915-970).
+  if (src->dc != r.dc && r.offload_seed) {
+    Rep* seed = find_seed(r);
+    if (seed && seed->life == Life::replicating) {
+      if (seed->version && *seed->version >= *target) return no_change();  // already under way
+      void_replication(*seed, "stale_seed");  // it chases a stale version: restart
+      release_offload(*seed);
+    } else if (seed) {
+      release_offload(*seed);  // a completed seed of another version: drop and refill
+    }
+    const std::string name = r.name + "+seed@" + n2s(*target);
+    if (m.reps.count(name)) return no_change();  // the same buffer still draining
+    auto rec = std::make_unique<Rep>();
+    rec->model = r.model;
+    rec->name = name;
+    rec->kind = Kind::offload;
+    rec->seed = true;
+    rec->owner = r.name;
+    rec->num_shards = r.num_shards;
+    rec->dc = r.dc;
+    rec->layout = r.layout;
+    rec->endpoints = r.endpoints;
+    rec->life = Life::replicating;
+    rec->version = target;
+    rec->offload_v = *target;
+    rec->source = src->name;
+    rec->seeding = true;
+    rec->shards.assign(r.num_shards, {});
+    src->serving++;
+    src->last_assigned = ++tick_;
+    SeedStart ss;
+    ss.version = *target;
+    ss.source = src->name;
+    for (std::uint32_t s = 0; s < r.num_shards; ++s) {
+      Assignment a = make_assignment(m, *src, *target, s, *rec);
+      a.seeding = true;
+      ss.assignments.push_back(std::move(a));
+    }
+    m.reps.emplace(name, std::move(rec));
+    trace("seed_start", {{"model", r.model}, {"replica", r.name}, {"v", n2s(*target)},
+                         {"src", src->name}});
+    no_change();
+    r.last.seed = std::move(ss);
+    return;
+  }
   t.resolved = true;
   t.changed = true;
   t.target = target;
@@ -615,6 +663,8 @@ void Registry::settle_ok(Rep& r) {
     for (std::uint32_t s = 0; s < r.num_shards; ++s) {
       Assignment a = make_assignment(m, *sit->second, *t.target, s, r);
       a.seeding = r.seeding;
+      const Rep& src = *sit->second;
+      a.local_seed_consume = src.kind == Kind::offload && src.seed && src.owner == r.name;
       o.assignments.push_back(std::move(a));
     }
   }
@@ -646,33 +696,48 @@ void Registry::wake_blocked(const std::string& model) {
 // ----------------------------------------------------- progress / complete
 
 void Registry::progress(const std::string& model, const std::string& replica,
-                        std::uint32_t shard, std::uint64_t items) {
+                        std::uint32_t shard, std::uint64_t items, bool seed,
+                        VersionId seed_version) {
   std::lock_guard lk(mu_);
   Rep* r = find(model, replica);
+  if (r && seed) r = find_seed(*r);
+  if (r && seed && seed_version && r->offload_v != seed_version) return;
   if (!r || r->life != Life::replicating || shard >= r->num_shards) return;
   auto& sx = r->shards[shard];
   if (items > sx.progress) sx.progress = items;
 }
 
 void Registry::complete(const std::string& model, const std::string& replica,
-                        std::uint32_t shard, Status outcome) {
+                        std::uint32_t shard, Status outcome, bool seed,
+                        VersionId seed_version) {
   std::lock_guard lk(mu_);
   Rep* r = find(model, replica);
+  if (r && seed) r = find_seed(*r);
+  if (r && seed && seed_version && r->offload_v != seed_version) return;
   if (!r || r->life != Life::replicating || shard >= r->num_shards) return;
   if (!ok(outcome)) {
-    trace("shard_failed", {{"model", model}, {"replica", replica},
+    trace("shard_failed", {{"model", model}, {"replica", r->name},
                            {"shard", n2s(shard)}, {"status", status_name(outcome)}});
-    void_replication(*r, status_name(outcome));
+    if (r->kind == Kind::offload && r->seed) {
+      void_replication(*r, "seed_failed");
+      release_offload(*r);
+    } else {
+      void_replication(*r, status_name(outcome));
+    }
     cv_.notify_all();
     return;
   }
   r->shards[shard].complete = true;
-  trace("shard_complete", {{"model", model}, {"replica", replica}, {"shard", n2s(shard)}});
+  trace("shard_complete", {{"model", model}, {"replica", r->name}, {"shard", n2s(shard)}});
   if (r->complete_all()) finish_replication(*r);
   cv_.notify_all();
 }
 
 void Registry::finish_replication(Rep& r) {
+  std::string consumed_seed;  // the owner consumed its own seed buffer
+  if (Rep* src = find(r.model, r.source);
+      src && src->kind == Kind::offload && src->seed && src->owner == r.name)
+    consumed_seed = src->name;
   release_source(r);
   r.life = Life::published;
   r.visible = true;
@@ -680,6 +745,12 @@ void Registry::finish_replication(Rep& r) {
   r.seeding = false;
   trace("replica_complete", {{"model", r.model}, {"replica", r.name},
                              {"v", n2s(*r.version)}, {"seeded", was_seeding ? "1" : "0"}});
+  if (!consumed_seed.empty()) {
+    if (Rep* sd = find(r.model, consumed_seed)) {
+      trace("seed_consumed", {{"model", r.model}, {"replica", r.name}});
+      release_offload(*sd);
+    }
+  }
   wake_blocked(r.model);
   eval_offload_releases(r.model);
 }
@@ -743,6 +814,22 @@ Status Registry::set_retention(const std::string& model, const std::string& repl
   if (!r || r->kind != Kind::worker) return Status::not_found;
   r->retain = lags;
   return Status::ok;
+}
+
+Status Registry::set_offload_seed(const std::string& model, const std::string& replica, bool on) {
+  std::lock_guard lk(mu_);
+  Rep* r = find(model, replica);
+  if (!r || r->kind != Kind::worker) return Status::not_found;
+  r->offload_seed = on;
+  return Status::ok;
+}
+
+Registry::Rep* Registry::find_seed(const Rep& owner) {
+  // the owner's live seed buffer: at most one not already draining
+  for (auto& [name, r] : ms(owner.model).reps)
+    if (r->kind == Kind::offload && r->seed && r->owner == owner.name && !r->releasing)
+      return r.get();
+  return nullptr;
 }
 
 std::set<VersionId> Registry::retained_versions(ModelState& m) {
@@ -843,6 +930,7 @@ void Registry::create_offload_replica(Rep& owner, VersionId v,
   rec->life = Life::published;
   rec->visible = true;
   rec->version = v;
+  rec->offload_v = v;
   rec->shards.assign(owner.num_shards, ShardState{0, true});
   m.reps.emplace(name, std::move(rec));
   trace("offload_replica", {{"model", owner.model}, {"replica", name}, {"v", n2s(v)},
@@ -855,7 +943,8 @@ void Registry::eval_offload_releases(const std::string& model) {
   const auto retained = retained_versions(m);
   std::vector<Rep*> drop;
   for (auto& [name, r] : m.reps) {
-    if (r->kind != Kind::offload || r->releasing || r->life != Life::published) continue;
+    // retention buffers only: a seed is released when its owner consumes it
+    if (r->kind != Kind::offload || r->seed || r->releasing || r->life != Life::published) continue;
     const VersionId v = *r->version;
     bool replaced = false;
     for (const auto& [oname, other] : m.reps)
@@ -872,17 +961,17 @@ void Registry::release_offload(Rep& off) {
   off.releasing = true;
   off.visible = false;
   trace("offload_release_start", {{"model", off.model}, {"replica", off.name},
-                                  {"v", off.version ? n2s(*off.version) : "none"},
+                                  {"v", n2s(off.offload_v)},
                                   {"serving", n2s(off.serving)}});
   if (off.serving == 0) finish_offload_release(off);
 }
 
 void Registry::finish_offload_release(Rep& off) {
   const std::string model = off.model, name = off.name;
-  releases_[model].push_back({off.owner, *off.version});
+  releases_[model].push_back({off.owner, off.offload_v, off.seed});
   trace("offload_released", {{"model", model}, {"replica", name}});
   auto& m = ms(model);
-  const VersionId v = *off.version;
+  const VersionId v = off.offload_v;
   m.reps.erase(name);
   prune_version(m, v);
 }

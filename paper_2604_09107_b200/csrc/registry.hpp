@@ -21,8 +21,12 @@
 //    paper_2604_09107_b200/ros.py Cluster) yields the same plan everywhere.
 //  * Retention offloads follow the reference (unpublish_needs_offload
 //    1606-1618, on_offload_confirm 1387-1437, create_offload_replica
-//    1439-1485, eval_offload_releases 1620-1645); cross-DC seed lanes are not
-//    modelled (one box, one datacenter).
+//    1439-1485, eval_offload_releases 1620-1645), and so do cross-link seed
+//    buffers (update's seed start 915-970, role-seed progress/complete
+//    1124-1175, consumption and release 1177-1204; find_seed_replica 88-99):
+//    a replica opened with offload_seed whose update source sits in another
+//    datacenter fills "<replica>+seed@<v>" in host memory in the background,
+//    stays on its version, and consumes the seed locally on a later update.
 //  * pick_source's key gains a topology cost between dc and serving; on a
 //    uniform NVSwitch box every cost is equal and the order is exactly the
 //    reference's (own_seed, same_dc, serving, last_assigned, name).
@@ -72,6 +76,14 @@ struct Assignment {
 
 enum class OpKind : std::uint8_t { none, publish, unpublish, replicate, update };
 
+// SeedStart (messages.hpp): a background host-memory fill the client starts
+// for every shard while its update reports no change.
+struct SeedStart {
+  VersionId version = 0;
+  std::string source;
+  std::vector<Assignment> assignments;  // per shard, seeding = true
+};
+
 struct OpOutcome {
   bool done = false;
   Status status = Status::ok;
@@ -82,12 +94,15 @@ struct OpOutcome {
   // in host memory first (ResponseKind::offload_first, server_core.cpp:428-440):
   // the client answers with offload_confirm for every shard.
   std::optional<VersionId> offload_first;
+  // update without change: the seed fill to start (server_core.cpp:483-494)
+  std::optional<SeedStart> seed;
 };
 
 // A retention offload the owner may now free (DirectiveKind::offload_release).
 struct OffloadRelease {
   std::string owner;
   VersionId version = 0;
+  bool seed = false;  // OffloadPurpose::seed (else retention)
 };
 
 struct ReplicaView {
@@ -142,6 +157,8 @@ class Registry {
   // version is parked in host memory (an offload replica) before it goes.
   Status set_retention(const std::string& model, const std::string& replica,
                        const std::set<std::uint64_t>& lags);
+  // ClientConfig.offload_seed (OpenReq.offload_seed, server_core.cpp:230).
+  Status set_offload_seed(const std::string& model, const std::string& replica, bool on);
   // OffloadConfirmMsg (server_core.cpp:1387-1437): the shard parked
   // `version` in host memory (ok) and serves it at `endpoint`.
   Status offload_confirm(const std::string& model, const std::string& replica,
@@ -187,10 +204,14 @@ class Registry {
                 OpOutcome* out);
 
   // Transfer lifecycle reports from the reader (ProgressMsg / CompleteMsg).
+  // seed = TransferRole::seed: the report is about the replica's seed fill
+  // of `seed_version` (ignored when its seed moved on to another version).
   void progress(const std::string& model, const std::string& replica,
-                std::uint32_t shard, std::uint64_t items);
+                std::uint32_t shard, std::uint64_t items, bool seed = false,
+                VersionId seed_version = 0);
   void complete(const std::string& model, const std::string& replica,
-                std::uint32_t shard, Status outcome);
+                std::uint32_t shard, Status outcome, bool seed = false,
+                VersionId seed_version = 0);
   // FailureReportMsg: reason 0 = timeout, 1 = checksum.  On success returns
   // the replacement assignment for `shard`.
   Result<Assignment> failure_report(const std::string& model,
@@ -246,6 +267,9 @@ class Registry {
     Kind kind = Kind::worker;
     std::string owner;        // offload: the worker whose buffer this is
     bool releasing = false;   // offload: released, draining its readers
+    bool seed = false;        // offload: OffloadPurpose::seed (else retention)
+    VersionId offload_v = 0;  // offload: the version the buffer holds
+    bool offload_seed = false;  // worker: ClientConfig.offload_seed
     std::set<std::uint64_t> retain;  // retention lags requested by this replica
     std::string model, name, dc;
     std::string layout;  // slicing key ("" plain)
@@ -315,6 +339,7 @@ class Registry {
   void eval_offload_releases(const std::string& model);
   void release_offload(Rep& off);
   void finish_offload_release(Rep& off);
+  Rep* find_seed(const Rep& owner);
 
   std::map<std::string, std::vector<OffloadRelease>> releases_;  // model -> pending directives
   Config cfg_;

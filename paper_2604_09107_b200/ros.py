@@ -108,7 +108,7 @@ def _read_bytes(fn, *args) -> bytes:
 
 def make_config(chunk_bytes=4096, tiny_threshold=2 << 20, group_target=64 << 20, pipeline=True,
                 checksum_retries=3, pull_timeout_s=4.0, datacenter="dc0",
-                reshard_align=2, grid_sms=0, early_publish=False) -> RsConfig:
+                reshard_align=2, grid_sms=0, early_publish=False, offload_seed=False) -> RsConfig:
     cfg = RsConfig()
     lib.rs_config_default(C.byref(cfg))
     cfg.chunk_bytes = chunk_bytes
@@ -121,6 +121,7 @@ def make_config(chunk_bytes=4096, tiny_threshold=2 << 20, group_target=64 << 20,
     cfg.reshard_align = reshard_align
     cfg.grid_sms = grid_sms
     cfg.early_publish = int(early_publish)
+    cfg.offload_seed = int(offload_seed)
     return cfg
 
 
@@ -208,8 +209,10 @@ class Cluster:
             return None
         check(rc)
         kind = _read_bytes(lib.rs_cluster_kind, self.h, _b(model), _b(replica)).decode()
+        seeding = C.c_int()
+        check(lib.rs_cluster_seeding(self.h, _b(model), _b(replica), C.byref(seeding)))
         return {"kind": kind, "lifecycle": life.value.decode(), "version": v.value,
-                "serving": s.value, "visible": bool(vis.value)}
+                "serving": s.value, "visible": bool(vis.value), "seeding": bool(seeding.value)}
 
     def progress(self, model: str, replica: str) -> int:
         """The replica's verified items (min over shards), as its fills report."""
@@ -325,8 +328,20 @@ class Handle:
         return [int(buf[i]) for i in range(min(n.value, 64))]
 
     def poll(self) -> None:
-        """Free the retention offloads the registry released."""
+        """Free the retention offloads and seed buffers the registry released."""
         check(lib.rs_poll(self.h))
+
+    def seed_lanes(self) -> list[int]:
+        """Versions this handle holds as cross-link seed buffers in host
+        memory (waits for a running seed fill first)."""
+        n = C.c_size_t(0)
+        buf = (C.c_uint64 * 64)()
+        check(lib.rs_seed_lanes(self.h, C.cast(buf, C.c_void_p), 64, C.byref(n)))
+        return [int(buf[i]) for i in range(min(n.value, 64))]
+
+    def seed_wait(self) -> None:
+        """Wait for a running seed fill (and its report to the registry)."""
+        check(lib.rs_seed_wait(self.h))
 
     def local_shards(self) -> list[int]:
         """Shards whose regions this process registered (a replica may span

@@ -32,7 +32,7 @@ def test_library_exports_every_declared_symbol():
 def test_abi_and_status_names():
     from paper_2604_09107_b200._lib import lib
     from paper_2604_09107_b200.ros import Status
-    assert lib.rs_abi_version() == 2
+    assert lib.rs_abi_version() == 3
     for s in Status:
         assert lib.rs_status_name(int(s)).decode() == s.name  # types.cpp:7-29
     assert lib.rs_status_name(99).decode() == "unknown"
