@@ -747,6 +747,7 @@ Status Client::build_payload(Shard& sh, VersionId v, std::shared_ptr<Payload>* o
   DeviceGuard g(sh.device);
   const std::size_t n = sh.regs.size();
   auto p = std::make_shared<Payload>();
+  PhaseClock pc;
   RS_CUDA(cudaEventRecord(sh.ev0, sh.stream));
 
   // Entry digests (K6).
@@ -761,10 +762,13 @@ Status Client::build_payload(Shard& sh, VersionId v, std::shared_ptr<Payload>* o
   std::vector<std::uint32_t> now, later;
   for (std::uint32_t i = 0; i < n; ++i)
     (cfg_.early_publish && lens[i] >= cfg_.limits.tiny_threshold ? later : now).push_back(i);
-  if (!later.empty()) {
-    if (!sh.k6) RS_CUDA(cudaStreamCreateWithFlags(&sh.k6, cudaStreamNonBlocking));
-    if (Status s = sh.k6_tables.alloc(sh.device, 3 * later.size() * 8); !ok(s)) return s;
-  }
+  // The background digest stream and its tables exist from the first
+  // publish in either mode (sized for every entry), so an early publish --
+  // the latency-critical one -- creates and allocates nothing: stream
+  // creation + cudaMalloc were measured at 0.8-52 ms there.
+  if (!sh.k6) RS_CUDA(cudaStreamCreateWithFlags(&sh.k6, cudaStreamNonBlocking));
+  if (Status s = sh.k6_tables.alloc(sh.device, std::max<std::size_t>(3 * n, 1) * 8); !ok(s)) return s;
+  pc.mark("build_payload: k6 stream + tables");
   // Library buffers of a publish are reused across publishes (a cudaFree
   // synchronizes the device and was measured taking up to 0.44 s here).
   DevBuf& tab = sh.dig_tables;
@@ -782,11 +786,13 @@ Status Client::build_payload(Shard& sh, VersionId v, std::shared_ptr<Payload>* o
     RS_CUDA(dev::launch_span_digests(d, d + nn, d + 2 * nn, static_cast<int>(nn), sh.stream));
     ++stats_.kernel_launches;
     RS_CUDA(cudaMemcpyAsync(nd.data(), d + 2 * nn, nn * 8, cudaMemcpyDeviceToHost, sh.stream));
+    pc.mark("build_payload: small-entry digests queued");
     RS_CUDA(cudaStreamSynchronize(sh.stream));
     for (std::size_t k = 0; k < nn; ++k) dig[now[k]] = nd[k];
     stats_.h2d_bytes += 16 * nn;
     stats_.d2h_bytes += 8 * nn;
   }
+  pc.mark("build_payload: entry digests");
   std::vector<EntryInfo> infos(n);
   for (std::size_t i = 0; i < n; ++i) infos[i] = {sh.regs[i].name, lens[i], dig[i]};
   auto mr = assemble(infos, cfg_.limits);
@@ -833,6 +839,7 @@ Status Client::build_payload(Shard& sh, VersionId v, std::shared_ptr<Payload>* o
       p->manifest.set_group_digest(static_cast<std::uint32_t>(gi), gd[gi]);
   }
 
+  pc.mark("build_payload: groups");
   // Serving addresses per item, chunk map, chunk digest table + watermarks.
   const auto& items = p->manifest.items();
   p->item_ptrs.resize(items.size());
@@ -847,6 +854,7 @@ Status Client::build_payload(Shard& sh, VersionId v, std::shared_ptr<Payload>* o
   p->cmap = ChunkMap::from_lens(p->manifest, lay.chunk_len);
   p->layout = lay.encode();
   if (Status s = alloc_tables(sh, *p, 0); !ok(s)) return s;
+  pc.mark("build_payload: tables");
   p->epoch = ++sh.epoch_ctr;
   // Chunk digest table of the published bytes (hash-only pull), and every
   // watermark set: a complete source.
@@ -854,10 +862,14 @@ Status Client::build_payload(Shard& sh, VersionId v, std::shared_ptr<Payload>* o
   for (std::size_t i = 0; i < items.size(); ++i) all[i] = static_cast<std::uint32_t>(i);
   if (Status s = hash_items(sh, *p, all); !ok(s)) return s;
   RS_CUDA(cudaEventRecord(sh.ev1, sh.stream));
+  pc.mark("build_payload: hash pass queued");
   if (!later.empty()) {
     // launched only now, after every allocation of this publish (the hash
     // pass's plan included): a device allocation issued while it runs would
-    // serialise the rest behind it; it runs beside the hash pass
+    // serialise the rest behind it.  It starts behind the hash pass: its
+    // CTAs (one per entry, hundreds of ms each) dispatched first would hold
+    // the SMs' shared memory and keep the persistent hash pass from
+    // launching until they drain (seen: publish 4 ms -> 89 ms, one run in two)
     const std::size_t nl = later.size();
     std::vector<std::uint64_t> lp(nl), ll(nl);
     for (std::size_t k = 0; k < nl; ++k) {
@@ -865,7 +877,7 @@ Status Client::build_payload(Shard& sh, VersionId v, std::shared_ptr<Payload>* o
       ll[k] = lens[later[k]];
     }
     auto* kd = static_cast<std::uint64_t*>(sh.k6_tables.p);
-    RS_CUDA(cudaStreamWaitEvent(sh.k6, sh.ev0, 0));  // behind the caller's prior work on sh.stream
+    RS_CUDA(cudaStreamWaitEvent(sh.k6, sh.ev1, 0));  // behind the hash pass (and all prior work)
     RS_CUDA(cudaMemcpyAsync(kd, lp.data(), nl * 8, cudaMemcpyHostToDevice, sh.k6));
     RS_CUDA(cudaMemcpyAsync(kd + nl, ll.data(), nl * 8, cudaMemcpyHostToDevice, sh.k6));
     RS_CUDA(dev::launch_span_digests(kd, kd + nl, kd + 2 * nl, static_cast<int>(nl), sh.k6));
@@ -873,7 +885,9 @@ Status Client::build_payload(Shard& sh, VersionId v, std::shared_ptr<Payload>* o
     stats_.h2d_bytes += 16 * nl;
   }
 
+  pc.mark("build_payload: K6 queued");
   RS_CUDA(cudaStreamSynchronize(sh.stream));
+  pc.mark("build_payload: hash pass done");
   float ms = 0;
   cudaEventElapsedTime(&ms, sh.ev0, sh.ev1);
   stats_.last_publish_ms = ms;
