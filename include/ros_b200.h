@@ -326,6 +326,15 @@ int rs_cluster_kind(rs_cluster* c, const char* model, const char* replica, char*
  * is released once consumed and drained (rs_poll frees it). */
 int rs_seed_lanes(rs_handle* h, uint64_t* versions, size_t cap, size_t* n);  /* after the fill */
 int rs_seed_wait(rs_handle* h);  /* wait for a running seed fill (and its report) */
+/* Split phase (the registry replicated through an operation log): start the
+ * seed fill the replica's last update outcome carries, without reporting it
+ * to the local registry; after the fill, rs_seed_status gives each local
+ * shard's outcome (to append as a role-seed completion) and rs_seed_export
+ * the lane's serve state for other processes (rs_serve_import). */
+int rs_seed_fill(rs_handle* h);
+int rs_seed_status(rs_handle* h, uint32_t shard);
+int rs_seed_export(rs_handle* h, uint32_t shard, uint64_t version, void* buf, size_t cap,
+                   size_t* len);
 int rs_server_set_offload_seed(rs_cluster* c, const char* model, const char* replica, int on);
 /* the shard's assignment in the replica's last replicate/update outcome */
 int rs_server_assignment(rs_cluster* c, const char* model, const char* replica, uint32_t shard,

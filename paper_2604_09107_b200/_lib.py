@@ -76,6 +76,9 @@ _SIGS = {
     "rs_lanes": (i32, [vp, vp, sz, C.POINTER(sz)]),
     "rs_seed_lanes": (i32, [vp, vp, sz, C.POINTER(sz)]),
     "rs_seed_wait": (i32, [vp]),
+    "rs_seed_fill": (i32, [vp]),
+    "rs_seed_status": (i32, [vp, u32]),
+    "rs_seed_export": (i32, [vp, u32, u64, vp, sz, C.POINTER(sz)]),
     "rs_server_set_offload_seed": (i32, [vp, cstr, cstr, i32]),
     "rs_server_assignment": (i32, [vp, cstr, cstr, u32, C.POINTER(RsAssignment)]),
     "rs_server_seed_start": (i32, [vp, cstr, cstr, u32, C.POINTER(RsAssignment)]),

@@ -608,6 +608,28 @@ int rs_seed_lanes(rs_handle* h, uint64_t* versions, size_t cap, size_t* n) {
   return 0;
 }
 
+int rs_seed_fill(rs_handle* h) {
+  if (!h) return st(rsb::Status::invalid_argument);
+  auto& cl = *h->client;
+  auto o = h->cluster->reg.op_result(cl.model(), cl.replica());
+  if (!o.done || !o.seed) return st(rsb::Status::not_found);
+  cl.set_seed_report(false);
+  return st(cl.start_seed(*o.seed));
+}
+
+int rs_seed_status(rs_handle* h, uint32_t shard) {
+  if (!h) return st(rsb::Status::invalid_argument);
+  return st(h->client->seed_status(shard));
+}
+
+int rs_seed_export(rs_handle* h, uint32_t shard, uint64_t version, void* buf, size_t cap,
+                   size_t* len) {
+  if (!h) return st(rsb::Status::invalid_argument);
+  auto r = h->client->export_seed(shard, version);
+  if (!r) return st(r.status());
+  return put_bytes(*r, static_cast<char*>(buf), cap, len);
+}
+
 int rs_seed_wait(rs_handle* h) {
   if (!h) return st(rsb::Status::invalid_argument);
   h->client->join_seed();

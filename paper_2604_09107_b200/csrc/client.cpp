@@ -2586,6 +2586,7 @@ Status Client::launch_seed(Shard& sh, const Assignment& a) {
 
 Status Client::start_seed(const SeedStart& ss) {
   join_seed();  // a fill of a stale target ends first (its report is ignored)
+  seed_status_.assign(num_shards_, Status::not_found);
   struct Job {
     std::uint32_t shard;
     int device;
@@ -2601,11 +2602,16 @@ Status Client::start_seed(const SeedStart& ss) {
     const bool had = sh.seed_lanes.count(ss.version) != 0;
     Status s = launch_seed(sh, ss.assignments[sh.idx]);
     if (!ok(s)) {
-      reg_->complete(model_, replica_, sh.idx, s, true, ss.version);
+      seed_status_[sh.idx] = s;
+      if (seed_report_) reg_->complete(model_, replica_, sh.idx, s, true, ss.version);
       continue;
     }
-    if (had) continue;
     auto& lane = sh.seed_lanes.at(ss.version);
+    if (had) {  // filled by an earlier start (join_seed above: not running)
+      std::lock_guard lk(lane.serve->m);
+      seed_status_[sh.idx] = lane.serve->complete ? Status::ok : Status::transfer_failed;
+      continue;
+    }
     std::uint64_t bytes = 0;
     for (std::size_t i = 0; i < lane.serve->item_ends.size(); ++i)
       bytes += lane.serve->item_ends[i] - (i ? lane.serve->item_ends[i - 1] : 0);
@@ -2616,8 +2622,8 @@ Status Client::start_seed(const SeedStart& ss) {
   }
   if (jobs.empty()) return Status::ok;
   // The waiter touches only what it was handed (events, status words, the
-  // lanes' serve states) and the registry (its own lock).
-  seed_thread_ = std::thread([this, jobs = std::move(jobs), v = ss.version] {
+  // lanes' serve states), its own status slots and the registry (its own lock).
+  seed_thread_ = std::thread([this, jobs = std::move(jobs), v = ss.version, report = seed_report_] {
     for (const auto& j : jobs) {
       DeviceGuard g(j.device);
       cudaError_t e = cudaEventSynchronize(j.ev);
@@ -2636,11 +2642,26 @@ Status Client::start_seed(const SeedStart& ss) {
                          : e != cudaSuccess ? Status::transfer_failed
                          : st.code == dev::kPullChecksum ? Status::checksum_mismatch
                          : Status::timeout;
+      seed_status_[j.shard] = out;
+      if (!report) continue;  // the caller reports through its operation log
       if (good) reg_->progress(model_, replica_, j.shard, j.items, true, v);
       reg_->complete(model_, replica_, j.shard, out, true, v);
     }
   });
   return Status::ok;
+}
+
+Status Client::seed_status(std::uint32_t shard) {
+  join_seed();
+  return shard < seed_status_.size() ? seed_status_[shard] : Status::not_found;
+}
+
+Result<std::string> Client::export_seed(std::uint32_t shard, VersionId v) {
+  if (shard >= num_shards_) return Status::invalid_argument;
+  join_seed();
+  auto it = shards_[shard].seed_lanes.find(v);
+  if (it == shards_[shard].seed_lanes.end()) return Status::not_found;
+  return serves_->export_state(it->second.key);
 }
 
 void Client::join_seed() {

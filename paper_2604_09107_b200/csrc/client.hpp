@@ -343,6 +343,12 @@ class Client {
   // Waits for a running seed fill (its registry report included).
   void join_seed();
   std::vector<VersionId> seed_lanes() const;
+  // Split phase (a registry replicated through an operation log): the
+  // waiter records each shard's outcome instead of reporting it, and the
+  // caller appends the role-seed completions to the log.
+  void set_seed_report(bool on) { seed_report_ = on; }
+  Status seed_status(std::uint32_t shard);  // after join_seed
+  Result<std::string> export_seed(std::uint32_t shard, VersionId v);
   std::string endpoint(std::uint32_t shard) const { return shards_[shard].endpoint; }
 
  private:
@@ -510,6 +516,8 @@ class Client {
   // seed fill waiter (reports role-seed completion to the registry)
   std::thread seed_thread_;
   std::atomic<std::uint64_t> seed_cross_dc_{0};
+  bool seed_report_ = true;
+  std::vector<Status> seed_status_;  // per shard, the last seed fill's outcome
   std::vector<std::optional<Assignment>> launch_as_;  // per shard: the latest launch's assignment
   bool published_ = false;
   bool opened_ = false;

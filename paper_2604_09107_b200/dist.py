@@ -95,6 +95,11 @@ def apply_op(c, o) -> int:
         return lib.rs_server_update(c, _b(m), _b(r), _b(sp), int(cur is not None), cur or 0)
     if kind == "complete":
         return lib.rs_server_complete(c, _b(o[1]), _b(o[2]), o[3], o[4])
+    if kind == "seed_on":  # ClientConfig.offload_seed (OpenReq.offload_seed)
+        return lib.rs_server_set_offload_seed(c, _b(o[1]), _b(o[2]), 1)
+    if kind == "seed_complete":  # CompleteMsg, TransferRole::seed
+        _, m, r, shard, outcome, v = o
+        return lib.rs_server_seed_complete(c, _b(m), _b(r), shard, outcome, v)
     if kind == "report":
         return lib.rs_server_failure_report(c, _b(o[1]), _b(o[2]), o[3], _b(o[4]), o[5])
     if kind == "close":

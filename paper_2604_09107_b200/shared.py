@@ -102,6 +102,8 @@ class SharedCluster:
         self.me = f"{os.getpid()}-{uuid.uuid4().hex[:8]}"
         self._w = _Conn(host, port, timeout_s)  # appends (caller's thread)
         self._w2 = _Conn(host, port, timeout_s)  # appends of the early-publish finalizer
+        self._w3 = _Conn(host, port, timeout_s)  # appends of the seed-fill waiter
+        self._seed = None
         self._r = _Conn(host, port, timeout_s)  # the follower's tail
         self._fin = None
         self._cv = threading.Condition()
@@ -183,8 +185,11 @@ class SharedCluster:
     def close(self):
         if self._fin is not None:
             self._fin.join(60)
+        if self._seed is not None:
+            self._seed.join(120)
         self._stop = True
         self._t.join(timeout=5)
+        self._w3.close()
         self._w2.close()
         self._w.close()
         self._r.close()
@@ -255,6 +260,8 @@ class SharedCluster:
             rc = apply_op(c, ("open", m, r, n, meta["dc"], eps, lk, dman, dlay))
             if rc == 0 and meta.get("retain"):
                 rc = apply_op(c, ("retain", m, r, list(meta["retain"])))
+            if rc == 0 and meta.get("seed"):
+                rc = apply_op(c, ("seed_on", m, r))
             return rc
         if kind == "publish":
             return apply_op(c, ("publish", m, r, meta["v"], [parts[i][0] for i in range(n)],
@@ -292,7 +299,9 @@ class SharedCluster:
     # ---- ops -------------------------------------------------------------------
     def create(self, model: str, replica: str, num_shards: int = 1, **cfg) -> Handle:
         """Local: a handle to register tensors on, before open()."""
-        return self.local.open(model, replica, num_shards, **cfg)
+        h = self.local.open(model, replica, num_shards, **cfg)
+        h.offload_seed = bool(cfg.get("offload_seed", False))
+        return h
 
     def open(self, h: Handle, endpoints=None, datacenter: str = "dc0", timeout: float = 120.0) -> None:
         """Announces the replica (ClientCore::open): endpoints, slicing key,
@@ -314,7 +323,8 @@ class SharedCluster:
             hs = h.shard_hash(sh)
             parts[sh] = {"ep": eps[sh], "hash": hs,
                          "dm": h.derived(sh, 0) if hs[1] else b"", "dl": h.derived(sh, 1) if hs[1] else b""}
-        meta = {"dc": datacenter, "retain": list(getattr(h, "retain", []) or [])}
+        meta = {"dc": datacenter, "retain": list(getattr(h, "retain", []) or []),
+                "seed": bool(getattr(h, "offload_seed", False))}
         rc = self._group(h, "open", parts, meta, timeout)
         if rc:
             raise RuntimeError(f"open {h.replica}: {Status(rc).name}")
@@ -400,6 +410,7 @@ class SharedCluster:
         if s != Status.ok:
             return OpResult(s)
         if update and not ch:
+            self._start_seed(h)
             return OpResult(Status.ok, v or cur, False)
         rc = lib.rs_transfer_bind(h.h, v)
         if rc:
@@ -445,6 +456,42 @@ class SharedCluster:
                 final = Status.transfer_failed
         lib.rs_transfer_finish(h.h, v, int(final == Status.ok))
         return OpResult(final, v if final == Status.ok else None, changed)
+
+    # ---- cross-link seed buffers (client_core.cpp:1720-1812) -----------------
+    def _start_seed(self, h: Handle) -> None:
+        """An update without change whose outcome starts a seed fill: fill this
+        member's shards into pinned host memory in the background; when done,
+        announce the lanes (other members import them) and append the
+        role-seed completions, so every registry replica publishes the seed."""
+        from ._lib import RsAssignment
+        a = RsAssignment()
+        loc = h.local_shards()
+        if not loc or lib.rs_server_seed_start(self.local.h, _b(h.model), _b(h.replica), loc[0],
+                                               C.byref(a)) != 1:
+            return
+        v = a.version
+        if self._seed is not None:
+            self._seed.join()
+        rc = lib.rs_seed_fill(h.h)
+
+        def wait():
+            lib.rs_seed_wait(h.h)
+            sts = {s: (lib.rs_seed_status(h.h, s) if rc == 0 else rc) for s in loc}
+            blobs = [_read_bytes(lib.rs_seed_export, h.h, s, v) for s in loc if sts[s] == 0]
+            if blobs:
+                self._w3.append(pickle.dumps((self.me, ("import", blobs))))
+            for s in loc:
+                self._w3.append(pickle.dumps((self.me, ("seed_complete", h.model, h.replica, s,
+                                                        int(sts[s]), v))))
+        self._seed = threading.Thread(target=wait, daemon=True)
+        self._seed.start()
+
+    def seed_wait(self, h: Handle, timeout: float = 120.0) -> None:
+        """Wait until this member's seed fill is reported to the log."""
+        if self._seed is not None:
+            self._seed.join(timeout)
+            self._seed = None
+        self.sync()
 
     def update(self, h: Handle, spec: str = "latest", wait_s: float = 60.0) -> OpResult:
         return self.replicate(h, spec, update=True, wait_s=wait_s)

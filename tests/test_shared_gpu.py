@@ -373,3 +373,111 @@ def test_retention_offload_through_the_op_log():
         for p in procs:
             p.join(timeout=60)
         log.close()
+
+
+def _seed_member(role, port, q, evs):
+    """T (dc1) publishes v1; F (dc2, offload_seed) updates -> background seed
+    fill into host memory, reported through the log; N (dc2, another
+    process) is planned onto F's seed and pulls it from F's host lane; F's
+    next update consumes its seed locally; the registry then releases it."""
+    import sys
+    sys.path.insert(0, ROOT)
+    import torch
+
+    from paper_2604_09107_b200 import ros
+    from paper_2604_09107_b200.ros import Status
+    from paper_2604_09107_b200.shared import SharedCluster
+    try:
+        dev = torch.device("cuda", 0)
+        sc = SharedCluster("127.0.0.1", port)
+        sizes = [(6 << 20) + 4096 * 3, 5000, 3 << 20]
+        bufs = [torch.zeros(n, dtype=torch.uint8, device=dev) for n in sizes]
+        dc = "dc1" if role == "T" else "dc2"
+        h = sc.create("m", role, 1, tiny_threshold=1 << 20, offload_seed=(role == "F"))
+        if role == "T":
+            for i, b in enumerate(bufs):
+                ros.synth_bf16(b, 710 + i)
+        for i, b in enumerate(bufs):
+            assert h.register_tensor(0, f"w{i}", b) == Status.ok
+        torch.cuda.synchronize()
+        sc.open(h, datacenter=dc)
+        digests = lambda: ros.digest_spans([b.data_ptr() for b in bufs], sizes, 0)  # noqa: E731
+        out = {}
+        if role == "T":
+            assert sc.publish(h, 1).status == Status.ok
+            q.put(("T", {"v1": digests()}))
+            evs["done"].wait(300)
+        elif role == "F":
+            evs["published"].wait(120)
+            r = sc.update(h)
+            out["first"] = (int(r.status), r.changed)
+            sc.seed_wait(h)
+            v = sc.local.view("m", "F+seed@1")
+            out["seed_view"] = v and (v["lifecycle"], v["kind"])
+            out["untouched"] = not any(b.any() for b in bufs)
+            q.put(("F1", out))
+            evs["neighbour_done"].wait(300)
+            r = sc.update(h)
+            out = {"second": (int(r.status), r.changed, r.version), "digests": digests(),
+                   "src": [(a.replica, a.src) for a in sc.assigns() if a.replica == "F"]}
+            sc.sync()
+            h.poll()
+            out["after_view"] = sc.local.view("m", "F+seed@1")
+            out["lanes"] = h.seed_lanes()
+            q.put(("F2", out))
+        else:  # N
+            evs["seeded"].wait(300)
+            r = sc.replicate(h)
+            q.put(("N", {"status": int(r.status), "v": r.version, "digests": digests(),
+                         "src": [(a.replica, a.src) for a in sc.assigns() if a.replica == "N"]}))
+            evs["done"].wait(300)
+        sc.close()
+    except Exception as e:  # pragma: no cover - surfaced by the parent
+        import traceback
+        q.put((role, {"error": repr(e) + traceback.format_exc()}))
+
+
+def test_cross_link_seed_through_the_op_log():
+    """Seed buffers across processes (client_core.cpp:1720-1812 with the
+    op log as the control plane): the seed fill is started by F's update,
+    reported with role seed through the log, its host lane announced; a
+    same-datacenter reader in a third process pulls the seed; F consumes it
+    locally; every byte equals the trainer's."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import multiprocessing as mp
+    from paper_2604_09107_b200.shared import LogServer
+    log = LogServer()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    evs = {k: ctx.Event() for k in ("published", "seeded", "neighbour_done", "done")}
+    procs = [ctx.Process(target=_seed_member, args=(r, log.port, q, evs)) for r in ("T", "F", "N")]
+    try:
+        for p in procs:
+            p.start()
+        got = {}
+        who, out = q.get(timeout=300)
+        assert who == "T" and "error" not in out, out
+        got["T"] = out
+        evs["published"].set()
+        who, out = q.get(timeout=300)
+        assert who == "F1" and "error" not in out, (who, out)
+        assert out["first"] == (0, False)
+        assert out["seed_view"] == ("published", "offload") and out["untouched"]
+        evs["seeded"].set()
+        who, out = q.get(timeout=300)
+        assert who == "N" and "error" not in out, (who, out)
+        assert out["status"] == 0 and out["v"] == 1 and out["src"] == [("N", "F+seed@1")]
+        assert out["digests"] == got["T"]["v1"]
+        evs["neighbour_done"].set()
+        who, out = q.get(timeout=300)
+        assert who == "F2" and "error" not in out, (who, out)
+        assert out["second"] == (0, True, 1)
+        assert out["src"] == [("F", "F+seed@1")]
+        assert out["digests"] == got["T"]["v1"]
+        assert out["after_view"] is None and out["lanes"] == []
+    finally:
+        evs["done"].set()
+        for p in procs:
+            p.join(timeout=60)
+        log.close()
