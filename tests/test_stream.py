@@ -340,3 +340,32 @@ def test_reference_wire_serves_only_the_verified_prefix_of_a_filling_replica():
         assert got == want
         a.transfer_finish(1, True)
         c.close()
+
+
+def test_cross_datacenter_seed_over_tcp():
+    """The realistic seeding case: the other datacenter's source is reached
+    over the wire.  The seed fill receives its frames into pinned host
+    memory and the pull kernel verifies them into the seed lane (host to
+    host through the SM path); the owner then consumes the seed locally."""
+    dev = torch.device("cuda:0")
+    with Cluster() as cl:
+        port = cl.listen()
+        ep = f"tcp:127.0.0.1:{port}"
+        tb = _bufs(dev, seed=31)
+        t = _open(cl, "trainer", tb, ep, datacenter="dc1")
+        assert t.publish(1).status == Status.ok
+        fb = _bufs(dev)
+        f = _open(cl, "far", fb, ep, datacenter="dc2", offload_seed=True)
+        res = f.update()
+        assert res.status == Status.ok and not res.changed, res
+        assert f.seed_lanes() == [1]
+        assert cl.view("m", "far+seed@1")["lifecycle"] == "published"
+        res = f.update()
+        assert res.status == Status.ok and res.changed and res.version == 1, res
+        torch.cuda.synchronize()
+        for a, b in zip(tb, fb):
+            assert torch.equal(a, b)
+        assert np.array_equal(f.chunk_digests(0), t.chunk_digests(0))
+        st = f.stats()
+        total = sum(b.numel() for b in tb)
+        assert st.bytes_pulled_cross_dc == total and st.bytes_copied_local == total
