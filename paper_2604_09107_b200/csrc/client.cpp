@@ -1370,8 +1370,12 @@ Status Client::bind_reshard(Shard& sh, const Assignment& a, VersionId v) {
   // assemble, digests not computed); its chunks follow the chunk rule on its
   // own geometry; the plan maps them onto the source shards' chunks.
   if (Status s = ensure_stream(sh); !ok(s)) return s;
-  if (sh.holding && sh.holding->reshard && sh.holding->reshard->src_manifests == a.all_manifests &&
-      sh.holding->reshard->src_layouts == a.all_layouts) {
+  if (!a.all_manifests || !a.all_layouts) return Status::protocol_error;
+  auto same = [](const Assignment::Blobs& x, const Assignment::Blobs& y) {
+    return x == y || (x && y && *x == *y);  // shared snapshot, or equal bytes
+  };
+  if (sh.holding && sh.holding->reshard && same(sh.holding->reshard->src_manifests, a.all_manifests) &&
+      same(sh.holding->reshard->src_layouts, a.all_layouts)) {
     // Same source slicing and bytes' manifests: keep the plan and the tables;
     // a new fill epoch unless this resumes the same version's fill.
     bool resume = (current_ && *current_ == v) || (sh.partial_version && *sh.partial_version == v);
@@ -1404,13 +1408,15 @@ Status Client::bind_reshard(Shard& sh, const Assignment& a, VersionId v) {
   rs->endpoints = a.all_endpoints;
   rs->src_manifests = a.all_manifests;
   rs->src_layouts = a.all_layouts;
-  for (std::size_t s = 0; s < a.all_manifests.size(); ++s) {
+  const auto& all_man = *a.all_manifests;
+  const auto& all_lay = *a.all_layouts;
+  for (std::size_t s = 0; s < all_man.size(); ++s) {
     SourceShard ss;
-    auto sm = Manifest::decode(a.all_manifests[s]);
+    auto sm = Manifest::decode(all_man[s]);
     if (!sm) return Status::protocol_error;
     ss.manifest = std::move(*sm);
-    if (s < a.all_layouts.size() && !a.all_layouts[s].empty()) {
-      auto sl = ShardLayout::decode(a.all_layouts[s]);
+    if (s < all_lay.size() && !all_lay[s].empty()) {
+      auto sl = ShardLayout::decode(all_lay[s]);
       if (!sl) return Status::protocol_error;
       ss.layout = std::move(*sl);
     } else {

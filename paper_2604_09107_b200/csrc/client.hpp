@@ -363,7 +363,7 @@ class Client {
   struct Reshard {
     std::vector<SourceShard> srcs;           // manifests/layouts/chunk0 of the source shards
     std::vector<std::string> endpoints;      // per source shard
-    std::vector<std::string> src_manifests, src_layouts;  // what the plan was built from
+    Assignment::Blobs src_manifests, src_layouts;  // what the plan was built from
     ReshardPlan plan;                        // segments (source offsets) / gathers / copies
     std::vector<std::unique_ptr<DevBuf>> gather_bufs;  // per plan.gathers entry
     std::uint32_t own_chunks = 0;            // landing chunks of the reader's own items

@@ -210,15 +210,17 @@ Assignment Registry::make_assignment(ModelState& m, Rep& src, VersionId v,
   a.source_endpoint = shard < src.endpoints.size() ? src.endpoints[shard] : "";
   a.source_complete = src.life == Life::published && src.complete_all();
   a.cross_dc = src.dc != reader.dc;
-  const LayoutInfo& li = m.versions[v].by_layout[src.layout];
+  LayoutInfo& li = m.versions[v].by_layout[src.layout];
   a.provisional = li.provisional;
   if (src.layout == slicing(reader.layout)) {
     a.manifest = shard < li.manifests.size() ? li.manifests[shard] : "";
     a.layout = shard < li.layouts.size() ? li.layouts[shard] : "";
   } else {
     a.reshard = true;
-    a.all_manifests = li.manifests;
-    a.all_layouts = li.layouts;
+    if (!li.man_sp) li.man_sp = std::make_shared<const std::vector<std::string>>(li.manifests);
+    if (!li.lay_sp) li.lay_sp = std::make_shared<const std::vector<std::string>>(li.layouts);
+    a.all_manifests = li.man_sp;
+    a.all_layouts = li.lay_sp;
     a.all_endpoints = src.endpoints;
   }
   return a;
@@ -272,6 +274,7 @@ Status Registry::publish(const std::string& model, const std::string& replica,
     if (lit->second.provisional && !provisional) {
       lit->second.manifests = manifests;  // this publisher brings the final bytes
       lit->second.provisional = false;
+      lit->second.man_sp.reset();
     }
   } else {
     LayoutInfo li{r->num_shards, manifests, layouts, provisional};
@@ -312,6 +315,7 @@ Status Registry::finalize_manifests(const std::string& model, const std::string&
   }
   li.manifests = manifests;
   li.provisional = false;
+  li.man_sp.reset();
   trace("manifest_final", {{"model", model}, {"replica", replica}, {"v", n2s(v)}});
   cv_.notify_all();
   return Status::ok;

@@ -69,9 +69,13 @@ struct Assignment {
   // the publisher commits them later (Registry::finalize_manifests).
   bool provisional = false;
   // Reshard (the source's slicing differs from the reader's): every source
-  // shard's manifest, layout and endpoint.
+  // shard's manifest, layout and endpoint.  The blobs are shared with the
+  // registry (tens of KB per shard: an outcome is copied several times on its
+  // way to the client, and a rebind compares them).
   bool reshard = false;
-  std::vector<std::string> all_manifests, all_layouts, all_endpoints;
+  using Blobs = std::shared_ptr<const std::vector<std::string>>;
+  Blobs all_manifests, all_layouts;
+  std::vector<std::string> all_endpoints;
 };
 
 enum class OpKind : std::uint8_t { none, publish, unpublish, replicate, update };
@@ -296,6 +300,9 @@ class Registry {
     std::vector<std::string> manifests;
     std::vector<std::string> layouts;
     bool provisional = false;  // early publish: big-entry digests still pending
+    // shared snapshots handed to reshard assignments (reset when the
+    // manifests change)
+    Assignment::Blobs man_sp, lay_sp;
   };
   struct VersionInfo {
     std::map<std::string, LayoutInfo> by_layout;  // slicing key -> per-shard metadata
