@@ -13,6 +13,7 @@
 // Scenarios (tests/unit/test_client_core.cpp):
 //   replicate pulls bytes that verify against the manifest  :163-202
 //   corrupt source: quiet retry, report, re-pick             :346-377
+//   cross-link update fills a host seed, consumes it locally :460-503
 //
 // Prints one "PASS <level> <scenario> k=v ..." or "FAIL ..." line per
 // scenario; exit status 0 iff every scenario passed.  --list prints the
@@ -287,6 +288,48 @@ void level_a_update() {
   report(ok, "A", "update_no_change_then_newer", counters(rd.stats()));
 }
 
+void level_a_seed() {
+  // test_client_core.cpp:460-503: a cross-link update fills a host seed,
+  // then consumes it locally (ClientConfig.datacenter / offload_seed)
+  B200Cluster cl;
+  DevBufs tb, fb;
+  const Tensor w{0, "w", 200000, 44}, x{1, "x", 100000, 45};
+  ClientConfig c1;
+  c1.datacenter = "dc1";
+  B200Client t(cl, "m", "T", 2, c1);
+  t.register_tensor(0, w.name, tb.make(w, w.salt));
+  t.register_tensor(1, x.name, tb.make(x, x.salt));
+  std::optional<ClientCore::OpResult> r;
+  t.publish(1, [&](ClientCore::OpResult o) { r = o; });
+  bool ok = r && r->status == Status::ok;
+  ClientConfig c2;
+  c2.datacenter = "dc2";
+  c2.offload_seed = true;
+  B200Client f(cl, "m", "F", 2, c2);
+  f.register_tensor(0, w.name, fb.make(w, 46));
+  f.register_tensor(1, x.name, fb.make(x, 47));
+  // first poll: the version is masked for dc2, a background fill starts
+  f.update(VersionSpec::latest(), [&](ClientCore::OpResult o) { r = o; });
+  ok &= r->status == Status::ok && !r->changed && !r->version.has_value();
+  f.poll();  // the fill's report is in
+  auto sv = cl.replica_view("m", "F+seed@1");
+  ok &= sv && sv->lifecycle == "published";
+  ok &= f.stats().bytes_pulled_cross_dc == 200000 + 100000;
+  // second poll: the change lands by consuming the local seed buffer
+  f.update(VersionSpec::latest(), [&](ClientCore::OpResult o) { r = o; });
+  ok &= r->status == Status::ok && r->changed && r->version == VersionId{1};
+  ok &= f.current_version() == VersionId{1};
+  ok &= fb.host(w) == pattern(w.len, w.salt) && fb.host(x) == pattern(x.len, x.salt);
+  const auto s = f.stats();
+  ok &= s.bytes_copied_local == 200000 + 100000 && s.bytes_pulled_cross_dc == 200000 + 100000;
+  // consumed and drained: handed back, the lane vanishes
+  f.poll();
+  ok &= !cl.replica_view("m", "F+seed@1").has_value();
+  report(ok, "A", "cross_link_update_fills_a_host_seed_then_consumes_it",
+         "bytes_pulled_cross_dc=" + std::to_string(s.bytes_pulled_cross_dc) +
+             " bytes_copied_local=" + std::to_string(s.bytes_copied_local));
+}
+
 void level_b_update() {
   RefFix fx;
   const Tensor w{0, "w", 200000, 1};
@@ -443,6 +486,7 @@ int main(int argc, char** argv) {
       {"B silent_source_reported_and_pull_moves", level_b_silent_source},
       {"B transport_equivalence_mem_vs_b200", level_b_equivalence},
       {"C rsdp_reference_reader_pulls_and_verifies", level_c_rsdp_reader},
+      {"A cross_link_update_fills_a_host_seed_then_consumes_it", level_a_seed},
   };
   if (argc > 1 && std::strcmp(argv[1], "--list") == 0) {
     for (const auto& [name, fn] : scenarios) std::printf("%s\n", name);

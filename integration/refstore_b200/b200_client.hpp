@@ -14,6 +14,8 @@
 #include <cstdint>
 #include <span>
 #include <stdexcept>
+#include <chrono>
+#include <cstdio>
 #include <string>
 
 #include "refstore/client_core.hpp"
@@ -97,9 +99,22 @@ class B200Client {
 
   B200Client(B200Cluster& cluster, std::string model, std::string replica,
              std::uint32_t num_shards)
+      : B200Client(cluster, std::move(model), std::move(replica), num_shards, ClientConfig{}) {}
+  // The ClientCore constructor's ClientConfig (config.hpp:23-47): the knobs
+  // that shape the read path carry over; chunk_bytes (the reference's pull
+  // window) does not -- the device path digests 4 KiB chunks.
+  B200Client(B200Cluster& cluster, std::string model, std::string replica,
+             std::uint32_t num_shards, const ClientConfig& rc)
       : cluster_(cluster), model_(std::move(model)), replica_(std::move(replica)) {
     rs_config cfg;
     rs_config_default(&cfg);
+    cfg.tiny_threshold = rc.manifest.tiny_threshold;
+    cfg.group_target = rc.manifest.group_target;
+    cfg.pipeline = rc.pipeline ? 1 : 0;
+    cfg.checksum_retries = rc.checksum_retries;
+    cfg.pull_timeout_s = std::chrono::duration<double>(rc.pull_timeout).count();
+    std::snprintf(cfg.datacenter, sizeof(cfg.datacenter), "%s", rc.datacenter.c_str());
+    cfg.offload_seed = rc.offload_seed ? 1 : 0;
     B200Cluster::check(rs_open(cluster.get(), model_.c_str(), replica_.c_str(), num_shards, &cfg, &h_));
   }
   ~B200Client() {
@@ -167,6 +182,14 @@ class B200Client {
     return out;
   }
   rs_handle* handle() const { return h_; }
+  // The reference client reacts to offload_release directives on its
+  // executor; a blocking handle applies them here (and waits for a running
+  // seed fill's report first).
+  void poll() {
+    if (!h_) return;
+    rs_seed_wait(h_);
+    rs_poll(h_);
+  }
 
  private:
   static OpResult result(int st) {

@@ -25,7 +25,8 @@ BIN = os.path.join(ROOT, "integration", "_build", "ref_scenarios")
 SCENARIOS = ["A replicate_pulls_bytes_that_verify", "B replicate_pulls_bytes_that_verify",
              "B corrupt_source_quiet_retry_report_repick", "A update_no_change_then_newer",
              "B update_no_change_then_newer", "B silent_source_reported_and_pull_moves",
-             "B transport_equivalence_mem_vs_b200", "C rsdp_reference_reader_pulls_and_verifies"]
+             "B transport_equivalence_mem_vs_b200", "C rsdp_reference_reader_pulls_and_verifies",
+             "A cross_link_update_fills_a_host_seed_then_consumes_it"]
 
 
 def _binary():
@@ -65,3 +66,6 @@ def test_reference_scenarios_through_the_b200_path():
     assert kv[SCENARIOS[7]]["bytes_pulled"] == str((3 << 20) + 1000 + 2000 + 4096)
     assert int(kv[SCENARIOS[5]]["failure_reports"]) >= 1
     assert int(kv[SCENARIOS[6]]["device_bytes"]) > 0
+    # test_client_core.cpp:460-503 through B200Client: only the seed fill
+    # crossed the link, the consumption was a local copy
+    assert kv[SCENARIOS[8]] == {"bytes_pulled_cross_dc": "300000", "bytes_copied_local": "300000"}
