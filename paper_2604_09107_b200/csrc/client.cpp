@@ -1623,7 +1623,15 @@ Status Client::launch_fill(Shard& sh, const SourceView& src, bool src_complete) 
   // releases every verified batch at once, so a chaser downstream sees it sooner
   pp.remote = dma || !remote ? 0u : (src.device >= 0 && !any_cast) ? 2u : 1u;
   sh.t_launch = std::chrono::steady_clock::now();
-  RS_CUDA(dev::launch_pull(pp, grid(sh), sh.stream));
+  int ctas = grid(sh);
+  if (pp.remote == 2) {  // A/B knob: CTAs of a plain peer pull (chain hop)
+    static const int peer_grid = [] {
+      const char* e = std::getenv("RSB_PEER_GRID");
+      return e ? std::atoi(e) : 0;
+    }();
+    if (peer_grid > 0) ctas = std::min(ctas, peer_grid);
+  }
+  RS_CUDA(dev::launch_pull(pp, ctas, sh.stream));
   stats_.kernel_launches += dev::pull_has_work(pp) ? 1 : 0;
   // A fill fed over TCP waits on progress that may need this GPU's copy
   // engines (a StreamServer in this process staging a frame D2H).  Nothing
