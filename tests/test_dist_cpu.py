@@ -85,6 +85,31 @@ def test_replicated_registry_two_ranks_same_plan():
     assert res[0][3] == res[1][3]  # byte-identical registry traces on both ranks
 
 
+def test_replicated_registry_eight_ranks_same_plan():
+    """The driver's 8-GPU scaling run in miniature: eight gloo ranks, one
+    replica each (trainer + 7 readers replicating at once), every rank ends
+    with the reference's chain plan and byte-identical registry traces."""
+    import multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    world = 8
+    ps = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in ps:
+        p.start()
+    res = {}
+    for _ in range(world):
+        r = q.get(timeout=300)
+        res[r[0]] = r
+    for p in ps:
+        p.join(timeout=60)
+    assert all(res[r][1] != "error" for r in res), res
+    plan = json.load(open(golden("plans.json")))["chain7"]
+    want = [(a["replica"], a["version"], a["src"], a["src_serving"]) for a in plan["assigns"]]
+    assert all(res[r][1] == want for r in range(world))
+    assert len({res[r][3] for r in range(world)}) == 1
+
+
 class _FakeHandle:
     """The parts of ros.Handle DistCluster.open reads, for a replica whose
     shards are split across ranks (no device registrations on CPU)."""
