@@ -373,7 +373,7 @@ def cpu_reference_run(shapes, readers: int = 1, steps: int = 1, warmup: int = 0,
                          "landing buffers" if shared else "")}
 
 
-def reference_parity(workload, t, r, rviews, cast: bool, soft: bool = False):
+def reference_parity(workload, t, r, rviews, cast: bool, soft: bool = False, chunk: int = 4096):
     """Pre-timing parity against the reference at full scale
     (tests/golden/scale.json, made by tests/golden/make_scale_golden.py from
     oracle/_ref): the trainer's manifest bytes (build_publish_payload), the
@@ -395,11 +395,12 @@ def reference_parity(workload, t, r, rviews, cast: bool, soft: bool = False):
                               rviews[0][1].device.index or 0)
     want = g["cast_digests"] if cast else g["tensor_digests"]
     out = {"manifest": hashlib.sha256(t.manifest(0)).hexdigest() == g["manifest_sha256"],
-           "chunk_table": sha(r.chunk_digests(0)) == g["chunk_table_sha256"],
+           # the fixture's chunk table is over 4096-byte chunks
+           "chunk_table": sha(r.chunk_digests(0)) == g["chunk_table_sha256"] if chunk == 4096 else None,
            "landed_tensors": ["%016X" % x for x in landed] == want,
            "against": "tests/golden/scale.json (reference digest64 / build_publish_payload)"}
     if not soft:
-        assert out["manifest"] and out["chunk_table"] and out["landed_tensors"], out
+        assert out["manifest"] and out["chunk_table"] is not False and out["landed_tensors"], out
     return out
 
 
@@ -518,7 +519,7 @@ def run_single(args):
     if not args.no_verify:
         verify()
         if not reshard:
-            parity = reference_parity(args.workload, t, r, rviews, cast)
+            parity = reference_parity(args.workload, t, r, rviews, cast, chunk=args.chunk)
     clk = ClockSampler(0)
     torch.cuda.synchronize()
     clk.start()

@@ -103,7 +103,7 @@ def run(args):
     # every rank (trainer and readers) against the reference at full scale
     # (tests/golden/scale.json): manifest bytes, chunk table, landed tensors
     parity = dc.gather(None if args.no_verify else
-                       B.reference_parity(args.workload, h, h, views, False, soft=True))
+                       B.reference_parity(args.workload, h, h, views, False, soft=True, chunk=args.chunk))
     clk = B.ClockSampler(local)
     nvc = B.NvlinkCounters(local)
     dist.barrier(group=dc.pg)
