@@ -350,10 +350,12 @@ class DistCluster:
                 else:
                     txn["active"] = True
         blobs = [h.serve_export(s) for s in txn["loc"]] if txn["active"] else None
-        self._import_all(self.gather(blobs))
-        # a replica whose bind failed on one rank fails on all of its ranks
-        bind = self.gather((h.model, h.replica, txn["active"], txn["result"] is not None)
-                           if h is not None else None)
+        # one all-gather: the serve states to import, and every part's bind
+        # outcome (a replica whose bind failed on one rank fails on all of its ranks)
+        got = self.gather((blobs, (h.model, h.replica, txn["active"], txn["result"] is not None)
+                           if h is not None else None))
+        self._import_all([g[0] for g in got])
+        bind = [g[1] for g in got]
         broken = {(b[0], b[1]) for b in bind if b is not None and b[3] and not b[2]}
         if txn["active"] and (h.model, h.replica) in broken:
             lib.rs_transfer_finish(h.h, txn["version"], 0)
@@ -374,14 +376,21 @@ class DistCluster:
     def replicate_finish(self, h: Optional[Handle], max_rounds: int = 8) -> Optional[OpResult]:
         """Collective second half: wait for the launched fills, report
         failures (re-filling from the re-picked source while allowed) and
-        complete every shard."""
+        complete every shard.  One all-gather per round: every rank derives
+        every replica's decision (final or retry) from the same gathered
+        outcomes, so the loop ends everywhere together and the completions
+        are applied in the same (rank) order on every registry replica."""
         txn = self._txn.pop(id(h), None) if h is not None else None
         active = bool(txn and txn["active"])
         result = txn["result"] if txn else None
         version = txn["version"] if txn else None
         loc = txn["loc"] if txn else []
+        # a part that failed before launching (its bind) completes with the rest
+        pending_done = None
+        if h is not None and not active and result is not None and version is not None:
+            pending_done = (h.model, h.replica, loc, int(result.status))
         rounds = 0
-        final = None  # this replica's outcome once decided
+        done_by_rank = {}
         while True:
             outcome = None
             if active:
@@ -390,39 +399,47 @@ class DistCluster:
                 step = lib.rs_transfer_wait if txn["launched"] else lib.rs_transfer_fill
                 txn["launched"] = False
                 step(h.h, C.cast(sts, C.c_void_p), C.cast(rsn, C.c_void_p))
-                outcome = {"model": h.model, "replica": h.replica,
+                outcome = {"model": h.model, "replica": h.replica, "loc": loc,
                            "failed": {i: (int(sts[i]), int(rsn[i])) for i in loc if sts[i] != 0},
                            "src": self._source(h.model, h.replica)}
+            elif pending_done is not None:
+                outcome = {"done": pending_done}
+                pending_done = None
+            got = self.gather(outcome)
             reps = {}
-            for o in self.gather(outcome):
-                if o is None:
+            for o in got:
+                if o is None or "done" in o:
                     continue
                 st = reps.setdefault((o["model"], o["replica"]), {"failed": {}, "retry": True})
                 for i, (code, reason) in o["failed"].items():
                     st["failed"][i] = code
                     st["retry"] &= self._apply(("report", o["model"], o["replica"], i, o["src"],
                                                 reason)) == 0
-            if active:
-                st = reps.get((h.model, h.replica), {"failed": {}, "retry": True})
+            any_active = False
+            for rk, o in enumerate(got):
+                if o is None:
+                    continue
+                if "done" in o:
+                    done_by_rank[rk] = o["done"]
+                    continue
+                st = reps[(o["model"], o["replica"])]
                 if not st["failed"]:
-                    final = Status.ok
+                    fin = Status.ok
                 elif not (st["retry"] and rounds + 1 < max_rounds):
-                    final = Status(next(iter(st["failed"].values())))
-                if final is not None:
-                    lib.rs_transfer_finish(h.h, version, int(final == Status.ok))
-                    result = OpResult(final, version if final == Status.ok else None,
-                                      txn["changed"])
+                    fin = Status(next(iter(st["failed"].values())))
+                else:
+                    any_active = True  # this part refills from the re-picked source
+                    continue
+                done_by_rank[rk] = (o["model"], o["replica"], o["loc"], int(fin))
+                if rk == self.rank:
+                    lib.rs_transfer_finish(h.h, version, int(fin == Status.ok))
+                    result = OpResult(fin, version if fin == Status.ok else None, txn["changed"])
                     active = False
-            if not any(self.gather(active)):
+            if not any_active:
                 break
             rounds += 1
-        done = None
-        if h is not None and result is not None and version is not None:
-            done = (h.model, h.replica, loc, int(result.status))
-        for o in self.gather(done):
-            if o is None:
-                continue
-            m, r, shards, st = o
+        for rk in sorted(done_by_rank):
+            m, r, shards, st = done_by_rank[rk]
             for i in shards:
                 self._apply(("complete", m, r, i, st))
         return result
