@@ -7,7 +7,9 @@ a planner change that would cost bandwidth shows up on a CPU.
 Model (per GPU, one NVSwitch port):
   * a GPU that only sends or only receives moves `nvlink_one_way` bytes/s in
     that direction; a GPU doing both moves `nvlink_both_ways` each way
-    (tools/nvlink_dir_probe.py: SM pulls 770-785 one way, ~672 both);
+    (tools/nvlink_dir_probe.py: SM pulls 770-785 one way, ~672 both;
+    tools/bidir_counters.sh: with both directions busy the receive lane
+    carries 874-887 of 900 GB/s and the pull lands 679-691 of user data);
   * concurrent flows through one GPU port share it equally;
   * a reader chasing a source that is still filling cannot run ahead of it;
   * a GPU-local source is bound by HBM (read + write of every byte);
