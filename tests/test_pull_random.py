@@ -79,3 +79,36 @@ def test_random_publish_pull_matches_reference(oracle, seed):
         table = oracle.chunk_digests(items, chunk)
         assert np.array_equal(t.chunk_digests(0), table), seed
         assert np.array_equal(r.chunk_digests(0), table), seed
+
+
+def test_many_tiny_tensors_match_reference(oracle):
+    """3,000 tiny tensors (1 B - 5 KB) and two big ones: many packed groups,
+    thousands of pack/unpack spans and K6 spans in one publish and pull."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    rng = np.random.default_rng(77)
+    sizes = [int(x) for x in rng.integers(1, 5000, 3000)] + [5 << 20, (3 << 20) + 7]
+    rng.shuffle(sizes)
+    host = [rng.integers(0, 256, n, dtype=np.uint8) for n in sizes]
+    names = [f"p{i}" for i in range(len(sizes))]
+    tiny, target = 64 << 10, 1 << 20
+    dev = torch.device("cuda:0")
+    with Cluster() as cl:
+        t = cl.open("m", "trainer", 1, tiny_threshold=tiny, group_target=target)
+        r = cl.open("m", "reader", 1, tiny_threshold=tiny, group_target=target)
+        tb, rb = [], []
+        for n, a in zip(names, host):
+            x = torch.from_numpy(a).to(dev)
+            y = torch.zeros_like(x)
+            tb.append(x)
+            rb.append(y)
+            assert t.register_tensor(0, n, x) == Status.ok
+            assert r.register_tensor(0, n, y) == Status.ok
+        assert t.publish(1).status == Status.ok
+        assert r.replicate().status == Status.ok
+        torch.cuda.synchronize()
+        assert all(torch.equal(x, y) for x, y in zip(tb, rb))
+        want = (oracle.ref_build_manifest(names, host, tiny, target) if oracle.ref_available()
+                else oracle.publish_manifest(names, host, tiny, target))
+        assert t.manifest(0) == want and r.manifest(0) == want
+        assert np.array_equal(r.chunk_digests(0), t.chunk_digests(0))
