@@ -2110,6 +2110,17 @@ Status Client::finish_reshard(Shard& sh, const std::uint32_t* guard) {
       if (at == items[i].length) fused_items.insert(i);  // copies cover the item exactly
     }
   }
+  // region address of each of this reader's packed members -> (region end,
+  // the member's address in its group staging)
+  std::map<std::uint64_t, std::pair<std::uint64_t, std::uint64_t>> member_at;
+  for (std::uint32_t i = 0; i < items.size(); ++i) {
+    if (!items[i].is_group) continue;
+    for (const auto& mem : p.manifest.groups[items[i].index].members) {
+      const auto ptr = reinterpret_cast<std::uint64_t>(sh.regs[mem.entry].ptr);
+      member_at[ptr] = {ptr + sh.regs[mem.entry].len,
+                        reinterpret_cast<std::uint64_t>(p.group_bufs[items[i].index]->p) + mem.offset};
+    }
+  }
   std::vector<std::uint64_t> srcs, dsts, lens;
   for (const auto& c : rs.plan.copies) {
     const auto base = reinterpret_cast<std::uint64_t>(rs.gather_bufs[gidx.at({c.src_shard, c.src_item})]->p);
@@ -2132,36 +2143,38 @@ Status Client::finish_reshard(Shard& sh, const std::uint32_t* guard) {
       }
     }
     const std::uint64_t flag = c.cast ? dev::kSpanCastE4M3 : 0;
+    // 2) a slice of one of this reader's own packed members lands in its
+    //    group staging too (the group re-served by this copy), copied from
+    //    the same source bytes in the same launch: members are only ever
+    //    filled by copies (plan_reshard), so no separate packing pass
+    std::uint64_t also = 0;  // staging address of c.dst, or 0
+    if (!terminal()) {
+      auto mt = member_at.upper_bound(c.dst);
+      if (mt != member_at.begin() && c.dst < (--mt)->second.first)
+        also = mt->second.second + (c.dst - mt->first);
+    }
+    auto add = [&](std::uint64_t src, std::uint64_t dst, std::uint64_t len) {
+      srcs.push_back(src);
+      dsts.push_back(dst);
+      lens.push_back(len | flag);
+      if (also) {
+        srcs.push_back(src);
+        dsts.push_back(also + (dst - c.dst));
+        lens.push_back(len);
+      }
+    };
     if (c.src_stride == c.nc && c.dst_stride * (c.cast ? 2 : 1) == c.nc) {
-      // whole rows on both sides: one contiguous span
-      srcs.push_back(base + c.src_off);
-      dsts.push_back(c.dst);
-      lens.push_back((c.rows * c.nc) | flag);
+      add(base + c.src_off, c.dst, c.rows * c.nc);  // whole rows on both sides: one contiguous span
       continue;
     }
-    for (std::uint64_t r = 0; r < c.rows; ++r) {
-      srcs.push_back(base + c.src_off + r * c.src_stride);
-      dsts.push_back(c.dst + r * c.dst_stride);
-      lens.push_back(c.nc | flag);
-    }
+    for (std::uint64_t r = 0; r < c.rows; ++r)
+      add(base + c.src_off + r * c.src_stride, c.dst + r * c.dst_stride, c.nc);
   }
   if (Status s = copy_spans(sh, srcs, dsts, lens, guard); !ok(s)) return s;
   if (terminal()) return Status::ok;  // a cast copy never re-serves: nothing to pack or digest
-  // 2) pack this reader's own groups (its tiny slices) for re-serving
-  srcs.clear();
-  dsts.clear();
-  lens.clear();
   std::vector<std::uint32_t> group_items;
-  for (std::uint32_t i = 0; i < items.size(); ++i) {
-    if (!items[i].is_group) continue;
-    group_items.push_back(i);
-    for (const auto& mem : p.manifest.groups[items[i].index].members) {
-      srcs.push_back(reinterpret_cast<std::uint64_t>(sh.regs[mem.entry].ptr));
-      dsts.push_back(reinterpret_cast<std::uint64_t>(p.group_bufs[items[i].index]->p) + mem.offset);
-      lens.push_back(sh.regs[mem.entry].len);
-    }
-  }
-  if (Status s = copy_spans(sh, srcs, dsts, lens, guard); !ok(s)) return s;
+  for (std::uint32_t i = 0; i < items.size(); ++i)
+    if (items[i].is_group) group_items.push_back(i);
   // 3) digest + release the items whose bytes arrived by copy: the groups and
   //    big items sliced out of gathered source items (own chunk table and
   //    watermarks)
