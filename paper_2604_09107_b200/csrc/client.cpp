@@ -298,15 +298,32 @@ ChunkMap ChunkMap::uniform(const Manifest& m, std::uint64_t chunk_bytes) {
                                                  static_cast<std::uint32_t>(chunk_bytes)));
 }
 
-ChunkMap ChunkMap::from_lens(const Manifest& m, const std::vector<std::uint32_t>& lens) {
+ChunkMap ChunkMap::from_lens(const Manifest& m, const std::vector<std::uint32_t>& lens,
+                             const std::vector<std::uint32_t>& member_lens) {
   ChunkMap c;
   std::uint32_t next = 0;
   const auto& items = m.items();
+  c.parts.resize(items.size());
   for (std::size_t i = 0; i < items.size(); ++i) {
-    const std::uint64_t cl = i < lens.size() && lens[i] ? lens[i] : 4096;
-    const auto n = static_cast<std::uint32_t>((items[i].length + cl - 1) / cl);
+    std::uint32_t n = 0, cl32 = 0;
+    if (i < lens.size() && lens[i] == 0 && items[i].is_group && !member_lens.empty()) {
+      // member-cut group: one run per member, in packing order
+      std::vector<GroupMember> mem = m.groups[items[i].index].members;
+      std::sort(mem.begin(), mem.end(),
+                [](const GroupMember& a, const GroupMember& b) { return a.offset < b.offset; });
+      for (const auto& g : mem) {
+        const std::uint64_t len = m.entries[g.entry].length;
+        const std::uint64_t cl = g.entry < member_lens.size() && member_lens[g.entry] ? member_lens[g.entry] : 4096;
+        c.parts[i].push_back(ChunkPart{g.offset, len, static_cast<std::uint32_t>(cl), n});
+        n += static_cast<std::uint32_t>((len + cl - 1) / cl);
+      }
+    } else {
+      const std::uint64_t cl = i < lens.size() && lens[i] ? lens[i] : 4096;
+      n = static_cast<std::uint32_t>((items[i].length + cl - 1) / cl);
+      cl32 = static_cast<std::uint32_t>(cl);
+    }
     c.chunk0.push_back(next);
-    c.chunk_len.push_back(static_cast<std::uint32_t>(cl));
+    c.chunk_len.push_back(cl32);
     c.count.push_back(n);
     next += (n + dev::kBatchChunks - 1) / dev::kBatchChunks * dev::kBatchChunks;
   }
@@ -314,19 +331,27 @@ ChunkMap ChunkMap::from_lens(const Manifest& m, const std::vector<std::uint32_t>
   return c;
 }
 
-dev::ItemDesc identity_segment(std::uint64_t src, std::uint64_t dst, std::uint64_t len,
-                               const ChunkMap& cm, std::size_t item) {
-  dev::ItemDesc d{};
-  d.src = src;
-  d.dst = dst;
-  d.len = len;
-  d.chunk0 = cm.chunk0[item];
-  d.chunk_len = cm.chunk_len[item];
-  d.src_chunk0 = cm.chunk0[item];
-  d.q = 1;
-  d.m = 1;
-  d.src_id = 0;
-  return d;
+ChunkMap ChunkMap::from_layout(const Manifest& m, const ShardLayout& lay, std::uint64_t chunk_bytes,
+                               std::uint32_t align) {
+  return from_lens(m, lay.chunk_len, member_chunk_lens(m, lay.geo, chunk_bytes, align));
+}
+
+// Item-for-item segments of item `item` (one per chunk run); dst 0: hash only.
+void append_identity(std::vector<dev::ItemDesc>* out, std::uint64_t src, std::uint64_t dst,
+                     std::uint64_t len, const ChunkMap& cm, std::size_t item) {
+  for (const ChunkPart& r : cm.runs(item, len)) {
+    dev::ItemDesc d{};
+    d.src = src + r.off;
+    d.dst = dst ? dst + r.off : 0;
+    d.len = r.len;
+    d.chunk0 = cm.chunk0[item] + r.first;
+    d.chunk_len = r.chunk_len;
+    d.src_chunk0 = d.chunk0;
+    d.q = 1;
+    d.m = 1;
+    d.src_id = 0;
+    out->push_back(d);
+  }
 }
 
 // ----------------------------------------------------------- ServeRegistry
@@ -851,7 +876,7 @@ Status Client::build_payload(Shard& sh, VersionId v, std::shared_ptr<Payload>* o
   ShardLayout lay;
   for (const auto& r : sh.regs) lay.geo.push_back(r.geo);
   lay.chunk_len = item_chunk_lens(p->manifest, lay.geo, cfg_.chunk_bytes, cfg_.reshard_align);
-  p->cmap = ChunkMap::from_lens(p->manifest, lay.chunk_len);
+  p->cmap = ChunkMap::from_layout(p->manifest, lay, cfg_.chunk_bytes, cfg_.reshard_align);
   p->layout = lay.encode();
   if (Status s = alloc_tables(sh, *p, 0); !ok(s)) return s;
   pc.mark("build_payload: tables");
@@ -1040,8 +1065,7 @@ Status Client::hash_items(Shard& sh, Payload& p, const std::vector<std::uint32_t
   DeviceGuard g(sh.device);
   const auto& items = p.manifest.items();
   std::vector<dev::ItemDesc> descs;
-  for (std::uint32_t i : which)
-    descs.push_back(identity_segment(p.item_ptrs[i], 0, items[i].length, p.cmap, i));
+  for (std::uint32_t i : which) append_identity(&descs, p.item_ptrs[i], 0, items[i].length, p.cmap, i);
   const dev::SrcDesc self{nullptr, nullptr, 0, 0};
   dev::PullParams pp{};
   RS_CUDA(dev::upload_pull_plan(sh.device, sh.stream, descs.data(),
@@ -1276,7 +1300,7 @@ Status Client::bind(Shard& sh, const Assignment& a, VersionId v) {
   if (!a.layout.empty()) {
     auto lay = ShardLayout::decode(a.layout);
     if (!lay || lay->chunk_len.size() != items.size()) return Status::protocol_error;
-    p->cmap = ChunkMap::from_lens(p->manifest, lay->chunk_len);
+    p->cmap = ChunkMap::from_layout(p->manifest, *lay, cfg_.chunk_bytes, cfg_.reshard_align);
     p->layout = a.layout;
   } else {
     p->cmap = ChunkMap::uniform(p->manifest, cfg_.chunk_bytes);
@@ -1391,7 +1415,11 @@ Status Client::bind_reshard(Shard& sh, const Assignment& a, VersionId v) {
   auto p = std::make_shared<Payload>();
   std::vector<std::uint32_t> lens;
   if (Status s = derive(sh, &p->manifest, &p->encoded, &p->layout, &lens); !ok(s)) return s;
-  p->cmap = ChunkMap::from_lens(p->manifest, lens);
+  {
+    auto own = ShardLayout::decode(p->layout);
+    if (!own) return Status::protocol_error;
+    p->cmap = ChunkMap::from_layout(p->manifest, *own, cfg_.chunk_bytes, cfg_.reshard_align);
+  }
   for (const auto& grp : p->manifest.groups) {
     auto buf = std::make_unique<DevBuf>();
     if (Status s = buf->alloc(sh.device, grp.packed_length); !ok(s)) return s;
@@ -1423,7 +1451,11 @@ Status Client::bind_reshard(Shard& sh, const Assignment& a, VersionId v) {
       ss.layout.chunk_len.assign(ss.manifest.items().size(),
                                  static_cast<std::uint32_t>(cfg_.chunk_bytes));
     }
-    ss.chunk0 = ChunkMap::from_lens(ss.manifest, ss.layout.chunk_len).chunk0;
+    {
+      ChunkMap scm = ChunkMap::from_layout(ss.manifest, ss.layout, cfg_.chunk_bytes, cfg_.reshard_align);
+      ss.chunk0 = std::move(scm.chunk0);
+      ss.parts = std::move(scm.parts);
+    }
     rs->srcs.push_back(std::move(ss));
   }
   std::vector<ReaderEntry> rd;
@@ -1455,8 +1487,15 @@ Status Client::bind_reshard(Shard& sh, const Assignment& a, VersionId v) {
     auto buf = std::make_unique<DevBuf>();
     if (Status s = buf->alloc(sh.device, it.length); !ok(s)) return s;
     rs->gather_bufs.push_back(std::move(buf));
-    const std::uint64_t cl = rs->srcs[gth.src_shard].layout.chunk_len[gth.src_item];
-    const auto n = static_cast<std::uint32_t>((it.length + cl - 1) / cl);
+    const SourceShard& gss = rs->srcs[gth.src_shard];
+    std::uint32_t n = 0;
+    if (gth.src_item < gss.parts.size() && !gss.parts[gth.src_item].empty()) {
+      for (const auto& r : gss.parts[gth.src_item])
+        n += static_cast<std::uint32_t>((r.len + r.chunk_len - 1) / r.chunk_len);
+    } else {
+      const std::uint64_t cl = gss.layout.chunk_len[gth.src_item];
+      n = static_cast<std::uint32_t>((it.length + cl - 1) / cl);
+    }
     extra += (n + dev::kBatchChunks - 1) / dev::kBatchChunks * dev::kBatchChunks;
   }
   if (Status s = alloc_tables(sh, *p, extra); !ok(s)) return s;
@@ -1564,13 +1603,14 @@ Status Client::launch_fill(Shard& sh, const SourceView& src, bool src_complete) 
   DeviceGuard g(sh.device);
   const auto& p = *sh.holding;
   const auto& items = p.manifest.items();
-  std::vector<dev::ItemDesc> descs(items.size());
+  std::vector<dev::ItemDesc> descs;
   bool any_cast = false;
   for (std::size_t i = 0; i < items.size(); ++i) {
-    descs[i] = identity_segment(src.item_ptrs[i], p.item_ptrs[i], items[i].length, p.cmap, i);
+    const std::size_t at = descs.size();
+    append_identity(&descs, src.item_ptrs[i], p.item_ptrs[i], items[i].length, p.cmap, i);
     if (!items[i].is_group &&
         sh.regs[sh.by_name.at(p.manifest.entries[items[i].index].name)].cast) {
-      descs[i].chunk_len |= dev::kCastE4M3;
+      descs[at].chunk_len |= dev::kCastE4M3;  // a big item: one run
       any_cast = true;
     }
   }
@@ -1583,8 +1623,10 @@ Status Client::launch_fill(Shard& sh, const SourceView& src, bool src_complete) 
   // A resumed epoch (landed_some: an earlier attempt verified some batches)
   // takes the SM path, which skips the landed batches: the engine would copy
   // every frame again, over bytes already verified, and nothing re-checks them.
+  // (Copy-engine frames cut items at uniform chunk boundaries: a member-cut
+  // group takes the SM path too.)
   const bool dma = src.device < 0 && src_complete && !any_cast && !p.landed_some &&
-                   host_dma_enabled() && write_value32();
+                   !p.cmap.any_cut() && host_dma_enabled() && write_value32();
   if (dma) {
     for (std::size_t i = 0; i < items.size(); ++i) {
       descs[i].src = p.item_ptrs[i];
@@ -1998,17 +2040,33 @@ Status Client::launch_reshard_fill(Shard& sh, const Assignment& a, bool src_comp
       const auto& gth = rs.plan.gathers[gi];
       const SourceShard& ss = rs.srcs[gth.src_shard];
       const auto& it = ss.manifest.items()[gth.src_item];
-      const std::uint64_t cl = ss.layout.chunk_len[gth.src_item];
-      const auto n = static_cast<std::uint32_t>((it.length + cl - 1) / cl);
+      // the item's chunk runs (one for a uniform item; one per member of a
+      // member-cut group)
+      std::vector<ChunkPart> runs;
+      if (gth.src_item < ss.parts.size() && !ss.parts[gth.src_item].empty())
+        runs = ss.parts[gth.src_item];
+      else
+        runs.push_back(ChunkPart{0, it.length, ss.layout.chunk_len[gth.src_item], 0});
+      auto run_chunks = [](const ChunkPart& r) {
+        return static_cast<std::uint32_t>((r.len + r.chunk_len - 1) / r.chunk_len);
+      };
+      const std::uint32_t n = runs.back().first + run_chunks(runs.back());
       const std::uint32_t nb = (n + dev::kBatchChunks - 1) / dev::kBatchChunks;
+      auto chunk_at = [&](std::uint64_t x) {  // the chunk holding byte x of the item
+        auto r = std::upper_bound(runs.begin(), runs.end(), x,
+                                  [](std::uint64_t v, const ChunkPart& p) { return v < p.off; });
+        --r;
+        return r->first + static_cast<std::uint32_t>((x - r->off) / r->chunk_len);
+      };
       std::vector<char> want(nb, 0);
       auto nit = need_bytes.find({gth.src_shard, gth.src_item});
       if (nit == need_bytes.end()) {
         std::fill(want.begin(), want.end(), 1);
       } else {
-        const std::uint64_t per = cl * dev::kBatchChunks;
         for (const auto& [lo, hi] : nit->second)
-          for (std::uint64_t b = lo / per; b <= (hi - 1) / per && b < nb; ++b) want[b] = 1;
+          for (std::uint32_t b = chunk_at(lo) / dev::kBatchChunks;
+               b <= chunk_at(hi - 1) / dev::kBatchChunks && b < nb; ++b)
+            want[b] = 1;
       }
       for (std::uint32_t b0 = 0; b0 < nb;) {
         if (!want[b0]) {
@@ -2017,19 +2075,25 @@ Status Client::launch_reshard_fill(Shard& sh, const Assignment& a, bool src_comp
         }
         std::uint32_t b1 = b0;
         while (b1 < nb && want[b1]) ++b1;
-        const std::uint64_t off = std::uint64_t(b0) * dev::kBatchChunks * cl;
-        const std::uint64_t end = std::min<std::uint64_t>(it.length, std::uint64_t(b1) * dev::kBatchChunks * cl);
-        dev::ItemDesc d{};
-        d.src = off;  // + the source item's address at launch
-        d.dst = reinterpret_cast<std::uint64_t>(rs.gather_bufs[gi]->p) + off;
-        d.len = end - off;
-        d.chunk0 = next + b0 * dev::kBatchChunks;
-        d.chunk_len = static_cast<std::uint32_t>(cl);
-        d.src_chunk0 = ss.chunk0[gth.src_item] + b0 * dev::kBatchChunks;
-        d.q = d.m = 1;
-        d.src_id = gth.src_shard;
-        rs.gather_segs.push_back(d);
-        rs.gather_items.push_back(gth.src_item);
+        const std::uint32_t k0 = b0 * dev::kBatchChunks, k1 = std::min(n, b1 * dev::kBatchChunks);
+        for (const ChunkPart& r : runs) {  // whole batches, cut at run boundaries
+          const std::uint32_t rk0 = std::max(k0, r.first), rk1 = std::min(k1, r.first + run_chunks(r));
+          if (rk0 >= rk1) continue;
+          const std::uint64_t off = r.off + std::uint64_t(rk0 - r.first) * r.chunk_len;
+          const std::uint64_t end = std::min<std::uint64_t>(r.off + r.len,
+                                                            r.off + std::uint64_t(rk1 - r.first) * r.chunk_len);
+          dev::ItemDesc d{};
+          d.src = off;  // + the source item's address at launch
+          d.dst = reinterpret_cast<std::uint64_t>(rs.gather_bufs[gi]->p) + off;
+          d.len = end - off;
+          d.chunk0 = next + rk0;
+          d.chunk_len = r.chunk_len;
+          d.src_chunk0 = ss.chunk0[gth.src_item] + rk0;
+          d.q = d.m = 1;
+          d.src_id = gth.src_shard;
+          rs.gather_segs.push_back(d);
+          rs.gather_items.push_back(gth.src_item);
+        }
         b0 = b1;
       }
       next += nb * dev::kBatchChunks;
@@ -2513,7 +2577,7 @@ Status Client::launch_seed(Shard& sh, const Assignment& a) {
   if (!a.layout.empty()) {
     auto lay = ShardLayout::decode(a.layout);
     if (!lay || lay->chunk_len.size() != items.size()) return Status::protocol_error;
-    cm = ChunkMap::from_lens(*mr, lay->chunk_len);
+    cm = ChunkMap::from_layout(*mr, *lay, cfg_.chunk_bytes, cfg_.reshard_align);
   }
   std::vector<std::uint64_t> off(items.size());
   std::uint64_t tot = 0, bytes = 0;
@@ -2554,12 +2618,11 @@ Status Client::launch_seed(Shard& sh, const Assignment& a) {
     if (lane.tcp) lane.tcp->release(&host_pool_);
     return Status::protocol_error;
   }
-  std::vector<dev::ItemDesc> descs(items.size());
-  for (std::size_t i = 0; i < items.size(); ++i) {
-    descs[i] = identity_segment(view.item_ptrs[i], reinterpret_cast<std::uint64_t>(base + off[i]),
-                                items[i].length, cm, i);
-    descs[i].pad = 1;  // host-memory landing: no tensor maps (generic bulk stores)
-  }
+  std::vector<dev::ItemDesc> descs;
+  for (std::size_t i = 0; i < items.size(); ++i)
+    append_identity(&descs, view.item_ptrs[i], reinterpret_cast<std::uint64_t>(base + off[i]),
+                    items[i].length, cm, i);
+  for (auto& d : descs) d.pad = 1;  // host-memory landing: no tensor maps (generic bulk stores)
   const bool src_complete = a.source_complete && !lane.tcp;
   dev::SrcDesc sdesc{reinterpret_cast<const std::uint64_t*>(view.digests),
                      src_complete ? nullptr : reinterpret_cast<const std::uint32_t*>(view.flags),

@@ -93,8 +93,11 @@ struct DevBuf {
 // items are holes (no bytes, no digest).
 struct ChunkMap {
   std::vector<std::uint32_t> chunk0;     // n_items + 1 prefix (batch aligned)
-  std::vector<std::uint32_t> chunk_len;  // per item
+  std::vector<std::uint32_t> chunk_len;  // per item (0: member-cut, see parts)
   std::vector<std::uint32_t> count;      // real chunks per item
+  // Per item: its runs when member-cut (layout.hpp member rule), else empty.
+  // Derived from the manifest and the layout, so not compared.
+  std::vector<std::vector<ChunkPart>> parts;
   std::uint32_t n_chunks() const { return chunk0.empty() ? 0 : chunk0.back(); }
   std::uint32_t n_batches() const {
     return (n_chunks() + dev::kBatchChunks - 1) / dev::kBatchChunks;
@@ -105,7 +108,22 @@ struct ChunkMap {
     return n;
   }
   static ChunkMap uniform(const Manifest& m, std::uint64_t chunk_bytes);
-  static ChunkMap from_lens(const Manifest& m, const std::vector<std::uint32_t>& lens);
+  // lens: per item (0: member-cut, with member_lens per entry).
+  static ChunkMap from_lens(const Manifest& m, const std::vector<std::uint32_t>& lens,
+                            const std::vector<std::uint32_t>& member_lens = {});
+  static ChunkMap from_layout(const Manifest& m, const ShardLayout& lay, std::uint64_t chunk_bytes,
+                              std::uint32_t align);
+  bool cut(std::size_t i) const { return i < parts.size() && !parts[i].empty(); }
+  bool any_cut() const {
+    for (const auto& p : parts)
+      if (!p.empty()) return true;
+    return false;
+  }
+  // The runs of item i (a single run for a uniform item).
+  std::vector<ChunkPart> runs(std::size_t i, std::uint64_t item_len) const {
+    if (cut(i)) return parts[i];
+    return {ChunkPart{0, item_len, chunk_len[i], 0}};
+  }
   bool operator==(const ChunkMap& o) const {
     return chunk0 == o.chunk0 && chunk_len == o.chunk_len && count == o.count;
   }

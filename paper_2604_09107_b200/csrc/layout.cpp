@@ -61,11 +61,25 @@ std::vector<std::uint32_t> item_chunk_lens(const Manifest& m, const std::vector<
                                            std::uint64_t chunk_bytes, std::uint32_t align) {
   std::vector<std::uint32_t> out;
   for (const auto& it : m.items()) {
-    if (!it.is_group && it.index < geo.size())
+    if (!it.is_group && it.index < geo.size()) {
       out.push_back(chunk_len_for(geo[it.index], chunk_bytes, align));
-    else
+    } else if (it.is_group) {
+      bool cut = false;  // member rule: some member carries a geometry
+      for (const auto& mem : m.groups[it.index].members)
+        cut |= mem.entry < geo.size() && geo[mem.entry].has();
+      out.push_back(cut ? 0u : static_cast<std::uint32_t>(chunk_bytes));
+    } else {
       out.push_back(static_cast<std::uint32_t>(chunk_bytes));
+    }
   }
+  return out;
+}
+
+std::vector<std::uint32_t> member_chunk_lens(const Manifest& m, const std::vector<Geometry>& geo,
+                                             std::uint64_t chunk_bytes, std::uint32_t align) {
+  std::vector<std::uint32_t> out(m.entries.size(), static_cast<std::uint32_t>(chunk_bytes));
+  for (std::size_t e = 0; e < out.size() && e < geo.size(); ++e)
+    if (geo[e].has()) out[e] = chunk_len_for(geo[e], chunk_bytes, align);
   return out;
 }
 
@@ -139,19 +153,31 @@ Status plan_reshard(const std::vector<ReaderEntry>& reader, const std::vector<So
       covered += (b - a) * (c1 - c0);
       const auto [item, ioff] = item_of(ss.manifest, static_cast<std::uint32_t>(e));
       const bool src_big = !ss.manifest.items()[item].is_group;
-      const std::uint32_t c = item < ss.layout.chunk_len.size() ? ss.layout.chunk_len[item] : 0;
-      const bool aligned = !r.in_group && src_big && c != 0 && c == r.chunk_len &&
+      std::uint32_t c = item < ss.layout.chunk_len.size() ? ss.layout.chunk_len[item] : 0;
+      // a member of a member-cut group: its own run of chunks inside the item
+      std::uint32_t run_first = 0;
+      bool member_run = false;
+      if (!src_big && item < ss.parts.size())
+        for (const ChunkPart& p : ss.parts[item])
+          if (p.off == ioff) {
+            c = p.chunk_len;
+            run_first = p.first;
+            member_run = true;
+          }
+      const bool aligned = !r.in_group && (src_big || member_run) && c != 0 && c == r.chunk_len &&
                            (c0 - sg.c0) % c == 0 && (c1 - c0) % c == 0 && sg.nc % c == 0 &&
                            (c1 - c0) == rg.nc && sg.nc / c <= 0xffff;
       if (aligned) {
         dev::ItemDesc d{};
-        d.src = ((a - sg.r0) * sg.nc + (c0 - sg.c0));  // offset; base added by the caller
+        // offset in the source item; its base address is added by the caller
+        d.src = ioff + ((a - sg.r0) * sg.nc + (c0 - sg.c0));
         d.dst = r.ptr + (a - rg.r0) * rg.nc / (r.cast ? 2 : 1);
         d.len = (b - a) * (c1 - c0);
         const std::uint64_t m = sg.nc / c, q = (c1 - c0) / c;
         d.chunk0 = r.chunk0 + static_cast<std::uint32_t>((a - rg.r0) * q);
         d.chunk_len = c | (r.cast ? dev::kCastE4M3 : 0u);
-        d.src_chunk0 = ss.chunk0[item] + static_cast<std::uint32_t>((a - sg.r0) * m + (c0 - sg.c0) / c);
+        d.src_chunk0 = ss.chunk0[item] + run_first +
+                       static_cast<std::uint32_t>((a - sg.r0) * m + (c0 - sg.c0) / c);
         d.q = static_cast<std::uint16_t>(q);
         d.m = static_cast<std::uint16_t>(m);
         d.src_id = si;

@@ -12,8 +12,16 @@
 //     c = the largest multiple of 128 <= chunk_bytes that divides
 //         gcd(nc, W / align)                           (align = 2 by default)
 // so every TP <= align split along either dimension is a union of whole
-// chunks on both sides (no over-read to verify).  Items without geometry,
-// groups, and geometries the rule cannot serve use chunk_bytes.
+// chunks on both sides (no over-read to verify).  Items without geometry and
+// geometries the rule cannot serve use chunk_bytes.
+//
+// Member rule (packed groups): a group with a member that carries a geometry
+// is cut member by member -- each member starts a run of chunks of its own
+// length (the chunk rule on its geometry, else chunk_bytes), so a region that
+// is a whole member, or a chunk-aligned slice of one, maps chunk-for-chunk
+// onto the group (an FSDP k/v slice packed by the reference's tiny rule
+// lands straight into a TP reader's region, verified).  Its layout records
+// chunk length 0; plain groups keep one run of chunk_bytes.
 #pragma once
 
 #include <cstdint>
@@ -38,6 +46,14 @@ struct Geometry {
 
 std::uint32_t chunk_len_for(const Geometry& g, std::uint64_t chunk_bytes, std::uint32_t align);
 
+// A run of equal chunks inside an item (a member of a member-cut group).
+struct ChunkPart {
+  std::uint64_t off = 0;        // bytes into the item
+  std::uint64_t len = 0;
+  std::uint32_t chunk_len = 0;
+  std::uint32_t first = 0;      // its first chunk, relative to the item's chunk0
+};
+
 // Per shard of a published (or derived) layout: geometry per manifest entry
 // and the chunk length per transfer item.
 struct ShardLayout {
@@ -47,9 +63,13 @@ struct ShardLayout {
   static Result<ShardLayout> decode(std::string_view s);
 };
 
-// Chunk lengths of a shard's items from its entries' geometries.
+// Chunk lengths of a shard's items from its entries' geometries (0: a
+// member-cut group).
 std::vector<std::uint32_t> item_chunk_lens(const Manifest& m, const std::vector<Geometry>& geo,
                                            std::uint64_t chunk_bytes, std::uint32_t align);
+// Per entry: the chunk length of its run inside a member-cut group.
+std::vector<std::uint32_t> member_chunk_lens(const Manifest& m, const std::vector<Geometry>& geo,
+                                             std::uint64_t chunk_bytes, std::uint32_t align);
 
 // One source shard as the reshard planner sees it.
 struct SourceShard {
@@ -57,6 +77,7 @@ struct SourceShard {
   ShardLayout layout;
   std::vector<std::uint64_t> item_ptrs;  // reader-VA address per item (0: not mapped yet)
   std::vector<std::uint32_t> chunk0;     // source chunk index per item (batch aligned)
+  std::vector<std::vector<ChunkPart>> parts;  // per item: its runs when member-cut
 };
 
 // A reader entry the segments cannot serve directly (it lives in a source

@@ -271,6 +271,10 @@ void StreamServer::serve_conn(int fd) {
     device = st->device;
   }
   if (device >= 0) cudaSetDevice(device);
+  // a member-cut group's chunks are not uniform in its item: not streamed
+  // (the reader's header check would refuse it; fail the request instead)
+  for (auto c : cm.chunk_len)
+    if (c == 0) return finish(static_cast<std::uint32_t>(Status::invalid_argument));
   const auto spans = batch_spans(cm, lens);
   for (const auto& sp : spans)
     if (sp.len > kStageBytes) return finish(static_cast<std::uint32_t>(Status::invalid_argument));

@@ -138,9 +138,14 @@ def _reader_items(oracle, tensors, shard_geos, full_host, tiny, chunk=4096, alig
             geo = shard_geos[names[e]]
             clens.append(oracle.chunk_len_for(geo[1], geo[5], chunk, align))
         elif g[e] not in seen:
+            # a packed group of regions with geometry is cut member by member
+            # (layout.hpp member rule): each member is its own run of chunks
             seen.add(g[e])
-            items.append(np.concatenate([data[k] for k in range(len(names)) if g[k] == g[e]]))
-            clens.append(chunk)
+            members = sorted((int(off[k]), k) for k in range(len(names)) if g[k] == g[e])
+            for _, k in members:
+                geo = shard_geos[names[k]]
+                items.append(data[k])
+                clens.append(oracle.chunk_len_for(geo[1], geo[5], chunk, align))
     enc = bytearray(oracle.manifest_encode(names, lens, [0] * len(names), g, off, ng, [0] * ng))
     enc[19] = 2  # derived-layout digest algorithm tag (field 2)
     return data, items, clens, bytes(enc)

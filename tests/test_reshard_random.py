@@ -55,9 +55,14 @@ def _expected_items(oracle, tensors, geos, full_host, tiny, chunk=4096, align=2)
             geo = geos[names[e]]
             clens.append(oracle.chunk_len_for(geo[1], geo[5], chunk, align))
         elif g[e] not in seen:
+            # a packed group of regions with geometry is cut member by member
+            # (layout.hpp member rule): each member is its own run of chunks
             seen.add(g[e])
-            items.append(np.concatenate([data[k] for k in range(len(names)) if g[k] == g[e]]))
-            clens.append(chunk)
+            members = sorted((int(off[k]), k) for k in range(len(names)) if g[k] == g[e])
+            for _, k in members:
+                geo = geos[names[k]]
+                items.append(data[k])
+                clens.append(oracle.chunk_len_for(geo[1], geo[5], chunk, align))
     return data, items, clens
 
 
