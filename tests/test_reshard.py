@@ -245,3 +245,45 @@ def test_reshard_detects_corrupt_source(oracle):
         res = r.replicate(wait_s=5)
         assert res.status == Status.checksum_mismatch
         assert r.stats().checksum_failures >= 2
+
+
+@pytest.mark.gpu
+def test_member_cut_version_parked_in_host_memory(oracle):
+    """A TP/FSDP trainer's packed groups are cut member by member (layout.hpp
+    member rule).  When its version is parked in pinned host memory (a
+    retention offload) a same-slicing reader pulls it from there: the
+    member-cut items take the SM path (copy-engine frames assume uniform
+    chunks) and land bit-exact with the trainer's chunk table."""
+    _need_gpu()
+    dev = torch.device("cuda:0")
+    tiny = 64 << 10
+    tensors = mini_llama(1)
+    full = _trainer_tensors(dev, tensors, seed0=900)
+    split = lambda shape, dim, s: tp_slice(shape, 2, 0, 2, s)  # noqa: E731  FSDP-2 row blocks
+    with Cluster() as cl:
+        w = cl.open("m", "watcher", 1)
+        wt = torch.zeros(4096, dtype=torch.uint8, device=dev)
+        assert w.register_tensor(0, "w0", wt) == Status.ok
+        w.set_retention([0])
+        assert w.connect() == Status.ok
+        t, keep = _publish_sharded(cl, "trainer", dev, tensors, full, 2, split, tiny)
+        assert t.publish(1).status == Status.ok
+        tables = [t.chunk_digests(s) for s in range(2)]
+        assert t.unpublish().status == Status.ok  # parks v1 in host memory
+        assert t.lanes() == [1]
+        r = cl.open("m", "reader", 2, tiny_threshold=tiny)
+        bufs = {}
+        for s in range(2):
+            for n, shape, dim in tensors:
+                geo = split(shape, dim, s)
+                b = torch.zeros(geo[3] * geo[5], dtype=torch.uint8, device=dev)
+                bufs[(s, n)] = (b, geo)
+                assert r.register_slice(s, n, b, geo) == Status.ok
+        res = r.replicate("1")
+        assert res.status == Status.ok, res
+        assert [(a.replica, a.src) for a in cl.assigns()][-1] == ("reader", "trainer+offload@1")
+        torch.cuda.synchronize()
+        for (s, n), (b, geo) in bufs.items():
+            assert np.array_equal(b.cpu().numpy(), oracle.slice_bytes(full[n].cpu().numpy(), geo)), (s, n)
+        for s in range(2):
+            assert np.array_equal(r.chunk_digests(s), tables[s]), s
