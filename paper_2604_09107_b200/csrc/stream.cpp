@@ -107,19 +107,42 @@ struct BatchSpan {
   std::uint64_t off = 0, len = 0;
 };
 
+// Byte offset inside item i of its item-relative chunk c (the item's length
+// at or past its last chunk): uniform chunks, or the item's runs when it is
+// a member-cut group.
+std::uint64_t chunk_offset(const ChunkMap& cm, std::uint32_t i, std::uint64_t c, std::uint64_t item_len) {
+  if (!cm.cut(i)) return std::min<std::uint64_t>(c * cm.chunk_len[i], item_len);
+  for (const ChunkPart& r : cm.parts[i]) {
+    const std::uint64_t n = (r.len + r.chunk_len - 1) / r.chunk_len;
+    if (c < r.first + n) return r.off + std::min<std::uint64_t>((c - r.first) * r.chunk_len, r.len);
+  }
+  return item_len;
+}
+
 std::vector<BatchSpan> batch_spans(const ChunkMap& cm, const std::vector<std::uint64_t>& item_len) {
   std::vector<BatchSpan> out(cm.n_batches());
   for (std::uint32_t i = 0; i + 1 < cm.chunk0.size(); ++i) {
     const std::uint32_t b0 = cm.chunk0[i] / dev::kBatchChunks;
     const std::uint32_t nb = (cm.count[i] + dev::kBatchChunks - 1) / dev::kBatchChunks;
     for (std::uint32_t k = 0; k < nb; ++k) {
-      const std::uint64_t off = std::uint64_t(k) * dev::kBatchChunks * cm.chunk_len[i];
-      const std::uint64_t end =
-          std::min<std::uint64_t>(off + std::uint64_t(dev::kBatchChunks) * cm.chunk_len[i], item_len[i]);
+      const std::uint64_t off = chunk_offset(cm, i, std::uint64_t(k) * dev::kBatchChunks, item_len[i]);
+      const std::uint64_t end = chunk_offset(cm, i, std::uint64_t(k + 1) * dev::kBatchChunks, item_len[i]);
       out[b0 + k] = {i, off, end > off ? end - off : 0};
     }
   }
   return out;
+}
+
+// A member-cut item's runs on the wire: per item a run count, then every
+// run as (offset, length, chunk length, first chunk).
+void flatten_runs(const ChunkMap& cm, std::vector<std::uint32_t>* nruns, std::vector<std::uint64_t>* runs) {
+  nruns->assign(cm.chunk_len.size(), 0);
+  runs->clear();
+  for (std::size_t i = 0; i < cm.chunk_len.size(); ++i) {
+    if (!cm.cut(i)) continue;
+    (*nruns)[i] = static_cast<std::uint32_t>(cm.parts[i].size());
+    for (const ChunkPart& r : cm.parts[i]) runs->insert(runs->end(), {r.off, r.len, r.chunk_len, r.first});
+  }
 }
 
 }  // namespace
@@ -271,10 +294,10 @@ void StreamServer::serve_conn(int fd) {
     device = st->device;
   }
   if (device >= 0) cudaSetDevice(device);
-  // a member-cut group's chunks are not uniform in its item: not streamed
-  // (the reader's header check would refuse it; fail the request instead)
-  for (auto c : cm.chunk_len)
-    if (c == 0) return finish(static_cast<std::uint32_t>(Status::invalid_argument));
+  // a member-cut item streams by its runs, which an imported state (another
+  // process's replica) does not carry: such an item is not served from here
+  for (std::size_t i = 0; i < cm.chunk_len.size(); ++i)
+    if (cm.chunk_len[i] == 0 && !cm.cut(i)) return finish(static_cast<std::uint32_t>(Status::invalid_argument));
   const auto spans = batch_spans(cm, lens);
   for (const auto& sp : spans)
     if (sp.len > kStageBytes) return finish(static_cast<std::uint32_t>(Status::invalid_argument));
@@ -285,8 +308,12 @@ void StreamServer::serve_conn(int fd) {
     if (!dig.empty() && cudaMemcpy(dig.data(), reinterpret_cast<const void*>(digests), dig.size() * 8,
                                    cudaMemcpyDefault) != cudaSuccess)
       return finish(static_cast<std::uint32_t>(Status::transfer_failed));
+    std::vector<std::uint32_t> nruns;
+    std::vector<std::uint64_t> runs;
+    flatten_runs(cm, &nruns, &runs);
     if (!send_pod(fd, std::uint32_t{0}) || !send_vec(fd, cm.chunk0) || !send_vec(fd, cm.chunk_len) ||
-        !send_vec(fd, cm.count) || !send_vec(fd, lens) || !send_vec(fd, dig))
+        !send_vec(fd, cm.count) || !send_vec(fd, lens) || !send_vec(fd, nruns) || !send_vec(fd, runs) ||
+        !send_vec(fd, dig))
       return (void)::close(fd);
   } else if (!send_pod(fd, std::uint32_t{0})) {
     return (void)::close(fd);
@@ -430,10 +457,28 @@ Status StreamSource::open(const std::string& endpoint, const std::string& key, V
   ChunkMap cm;
   std::vector<std::uint64_t> lens, dig;
   const int fd0 = fds_[0];
+  std::vector<std::uint32_t> nruns;
+  std::vector<std::uint64_t> runs;
   if (!recv_vec(fd0, &cm.chunk0) || !recv_vec(fd0, &cm.chunk_len) || !recv_vec(fd0, &cm.count) ||
-      !recv_vec(fd0, &lens) || !recv_vec(fd0, &dig) || !valid_header(cm, lens) ||
-      dig.size() != cm.n_chunks())
+      !recv_vec(fd0, &lens) || !recv_vec(fd0, &nruns) || !recv_vec(fd0, &runs) || !recv_vec(fd0, &dig))
     return Status::protocol_error;
+  // the runs of member-cut items, as the header states them
+  if (nruns.size() != cm.chunk_len.size()) return Status::protocol_error;
+  {
+    std::uint64_t total = 0;
+    for (auto n : nruns) total += n;
+    if (runs.size() != 4 * total) return Status::protocol_error;
+    cm.parts.assign(nruns.size(), {});
+    std::size_t at = 0;
+    for (std::size_t i = 0; i < nruns.size(); ++i)
+      for (std::uint32_t k = 0; k < nruns[i]; ++k, at += 4) {
+        if (runs[at + 2] == 0 || runs[at + 2] > (1u << 30) || runs[at + 3] > (1u << 30))
+          return Status::protocol_error;
+        cm.parts[i].push_back(ChunkPart{runs[at], runs[at + 1], static_cast<std::uint32_t>(runs[at + 2]),
+                                        static_cast<std::uint32_t>(runs[at + 3])});
+      }
+  }
+  if (!valid_header(cm, lens) || dig.size() != cm.n_chunks()) return Status::protocol_error;
   // every stripe's socket gives up when its source stays silent well past
   // the pull timeout (the kernel has failed by then; finish() shuts it too)
   const double rx_s = 2 * timeout_s + 1;
@@ -489,10 +534,25 @@ bool StreamSource::valid_header(const ChunkMap& cm, const std::vector<std::uint6
   if (cm.chunk0.size() != n + 1 || cm.chunk_len.size() != n || cm.count.size() != n ||
       cm.chunk0[0] != 0 || cm.chunk0.back() > (1u << 30))
     return false;
+  if (!cm.parts.empty() && cm.parts.size() != n) return false;
   for (std::size_t i = 0; i < n; ++i) {
     const std::uint32_t cl = cm.chunk_len[i];
-    if (cl == 0 || cm.chunk0[i] % dev::kBatchChunks != 0) return false;
-    if (cm.count[i] != (lens[i] + cl - 1) / cl) return false;
+    if (cm.chunk0[i] % dev::kBatchChunks != 0) return false;
+    if (cl == 0) {
+      // member-cut: runs back to back from byte 0, covering the item, their
+      // chunks numbered consecutively from 0
+      if (!cm.cut(i)) return false;
+      std::uint64_t off = 0, first = 0;
+      for (const ChunkPart& r : cm.parts[i]) {
+        if (r.off != off || r.first != first || r.chunk_len == 0 || r.len == 0) return false;
+        off += r.len;
+        first += (r.len + r.chunk_len - 1) / r.chunk_len;
+      }
+      if (off != lens[i] || first != cm.count[i]) return false;
+    } else {
+      if (cm.cut(i)) return false;
+      if (cm.count[i] != (lens[i] + cl - 1) / cl) return false;
+    }
     if (std::uint64_t(cm.chunk0[i]) + cm.count[i] > cm.chunk0[i + 1]) return false;
   }
   return true;
@@ -508,7 +568,7 @@ void StreamSource::receive_loop(int fd) {
     const std::uint32_t nb = (cm.count[i] + dev::kBatchChunks - 1) / dev::kBatchChunks;
     for (std::uint32_t k = 0; k < nb; ++k) {
       item_of[b0 + k] = i;
-      off_of[b0 + k] = std::uint64_t(k) * dev::kBatchChunks * cm.chunk_len[i];
+      off_of[b0 + k] = chunk_offset(cm, i, std::uint64_t(k) * dev::kBatchChunks, item_len_[i]);
     }
   }
   auto* flags = reinterpret_cast<std::uint32_t*>(view_.flags);
@@ -529,8 +589,8 @@ void StreamSource::receive_loop(int fd) {
     if (item_of[b0 + nb - 1] != i || (b0 + nb - 1) * std::uint64_t(dev::kBatchChunks) >=
                                          std::uint64_t(cm.chunk0[i]) + cm.count[i])
       return fail(Status::protocol_error);
-    const std::uint64_t end = std::min<std::uint64_t>(
-        item_len_[i], off_of[b0] + std::uint64_t(nb) * dev::kBatchChunks * cm.chunk_len[i]);
+    const std::uint64_t end = chunk_offset(
+        cm, i, std::uint64_t(b0 + nb) * dev::kBatchChunks - cm.chunk0[i], item_len_[i]);
     if (off_of[b0] >= end && item_len_[i] != 0) return fail(Status::protocol_error);
     if (len != end - off_of[b0]) return fail(Status::protocol_error);
     if (!recv_all(fd, base + item_off_[i] + off_of[b0], len)) return fail(Status::transfer_failed);

@@ -194,8 +194,9 @@ def test_hostile_tcp_source_is_rejected(case):
         if stripe != 0:
             return
         count = [n // 4096 + (1 if case == "bad_header" else 0)]
+        # chunk0, chunk_len, count, item lengths, member-cut runs (none), digests
         c.sendall(_vec("I", [0, 256]) + _vec("I", [4096]) + _vec("I", count) + _vec("Q", [n]) +
-                  _vec("Q", [0] * 256))
+                  _vec("I", [0]) + _vec("Q", []) + _vec("Q", [0] * 256))
         if case == "oversized_frame":
             c.sendall(struct.pack("<IIQ", 0, 1, 1 << 30) + b"\0" * 4096)
 
@@ -369,3 +370,36 @@ def test_cross_datacenter_seed_over_tcp():
         st = f.stats()
         total = sum(b.numel() for b in tb)
         assert st.bytes_pulled_cross_dc == total and st.bytes_copied_local == total
+
+
+def test_member_cut_groups_stream_over_tcp():
+    """A replica whose packed groups are cut member by member (regions with
+    slice geometry; layout.hpp member rule) streams over the B200 TCP plane:
+    the header carries each member-cut item's runs, frames are cut at its
+    batch boundaries, and the reader lands the bytes and the chunk table."""
+    dev = torch.device("cuda:0")
+    with Cluster() as cl:
+        port = cl.listen()
+        ep = f"tcp:127.0.0.1:{port}"
+        sizes = [(1 << 20) + 4096 * 7, 6000, 4096, 333, 70000]
+        t = cl.open("m", "trainer", 1, tiny_threshold=64 << 10)
+        r = cl.open("m", "reader", 1, tiny_threshold=64 << 10)
+        tb, rb = [], []
+        from paper_2604_09107_b200 import ros
+        for i, n in enumerate(sizes):
+            a = torch.zeros(n, dtype=torch.uint8, device=dev)
+            ros.synth_bf16(a[: n // 2 * 2], 40 + i)
+            b = torch.zeros(n, dtype=torch.uint8, device=dev)
+            tb.append(a)
+            rb.append(b)
+            g = (1, n, 0, 1, 0, n)  # a [1 x n] tensor held whole
+            assert t.register_slice(0, f"w{i}", a, g) == Status.ok
+            assert r.register_slice(0, f"w{i}", b, g) == Status.ok
+        t.set_endpoint(0, ep)
+        assert t.publish(1).status == Status.ok
+        res = r.replicate(wait_s=20.0)
+        assert res.status == Status.ok, res
+        torch.cuda.synchronize()
+        for a, b in zip(tb, rb):
+            assert torch.equal(a, b)
+        assert np.array_equal(r.chunk_digests(0), t.chunk_digests(0))
