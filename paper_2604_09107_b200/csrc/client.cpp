@@ -1481,23 +1481,8 @@ Status Client::bind_reshard(Shard& sh, const Assignment& a, VersionId v) {
   // Gathered source items land in library staging, behind the reader's own
   // chunk range (batch aligned), verified against the source chunk digests.
   rs->own_chunks = p->cmap.n_chunks();
-  std::uint32_t extra = 0;
-  for (const auto& gth : rs->plan.gathers) {
-    const auto& it = rs->srcs[gth.src_shard].manifest.items()[gth.src_item];
-    auto buf = std::make_unique<DevBuf>();
-    if (Status s = buf->alloc(sh.device, it.length); !ok(s)) return s;
-    rs->gather_bufs.push_back(std::move(buf));
-    const SourceShard& gss = rs->srcs[gth.src_shard];
-    std::uint32_t n = 0;
-    if (gth.src_item < gss.parts.size() && !gss.parts[gth.src_item].empty()) {
-      for (const auto& r : gss.parts[gth.src_item])
-        n += static_cast<std::uint32_t>((r.len + r.chunk_len - 1) / r.chunk_len);
-    } else {
-      const std::uint64_t cl = gss.layout.chunk_len[gth.src_item];
-      n = static_cast<std::uint32_t>((it.length + cl - 1) / cl);
-    }
-    extra += (n + dev::kBatchChunks - 1) / dev::kBatchChunks * dev::kBatchChunks;
-  }
+  if (Status s = build_gathers(sh, *rs); !ok(s)) return s;
+  const std::uint32_t extra = rs->gather_chunks_end - rs->own_chunks;
   if (Status s = alloc_tables(sh, *p, extra); !ok(s)) return s;
   RS_CUDA(cudaStreamSynchronize(sh.stream));
   p->reshard = std::move(rs);
@@ -1991,6 +1976,111 @@ Status Client::resolve_shard(Shard& sh, const std::string& replica, std::uint32_
   }
 }
 
+Status Client::build_gathers(Shard& sh, Reshard& rs) {
+  // Gathered source items (groups, unaligned slices) land in staging, but
+  // only the watermark batches that hold bytes some slice copy reads: a
+  // reader shard that needs a few members of a packed group does not pull
+  // (and verify) the rest of it.  Each range is whole batches of the item
+  // (cut at chunk-run boundaries), and the staging holds only those ranges,
+  // packed: a window per run of adjacent ranges (item offset -> staging
+  // offset), so a 64 MiB group whose biases and norms are needed costs
+  // their batches, not 64 MiB.  A function of the plan: built once per bind,
+  // re-addressed onto the sources' mappings per launch.
+  rs.gather_segs.clear();
+  rs.gather_items.clear();
+  rs.gather_windows.assign(rs.plan.gathers.size(), {});
+  rs.gather_bufs.clear();
+  std::map<std::pair<std::uint32_t, std::uint32_t>, std::vector<std::pair<std::uint64_t, std::uint64_t>>> need_bytes;
+  for (const auto& c : rs.plan.copies)
+    need_bytes[{c.src_shard, c.src_item}].emplace_back(c.src_off,
+                                                      c.src_off + (c.rows - 1) * c.src_stride + c.nc);
+  std::uint32_t next = rs.own_chunks;
+  for (std::size_t gi = 0; gi < rs.plan.gathers.size(); ++gi) {
+    const auto& gth = rs.plan.gathers[gi];
+    const SourceShard& ss = rs.srcs[gth.src_shard];
+    const auto& it = ss.manifest.items()[gth.src_item];
+    // the item's chunk runs (one for a uniform item; one per member of a
+    // member-cut group)
+    std::vector<ChunkPart> runs;
+    if (gth.src_item < ss.parts.size() && !ss.parts[gth.src_item].empty())
+      runs = ss.parts[gth.src_item];
+    else
+      runs.push_back(ChunkPart{0, it.length, ss.layout.chunk_len[gth.src_item], 0});
+    auto run_chunks = [](const ChunkPart& r) {
+      return static_cast<std::uint32_t>((r.len + r.chunk_len - 1) / r.chunk_len);
+    };
+    const std::uint32_t n = runs.back().first + run_chunks(runs.back());
+    const std::uint32_t nb = (n + dev::kBatchChunks - 1) / dev::kBatchChunks;
+    auto chunk_at = [&](std::uint64_t x) {  // the chunk holding byte x of the item
+      auto r = std::upper_bound(runs.begin(), runs.end(), x,
+                                [](std::uint64_t v, const ChunkPart& p) { return v < p.off; });
+      --r;
+      return r->first + static_cast<std::uint32_t>((x - r->off) / r->chunk_len);
+    };
+    std::vector<char> want(nb, 0);
+    auto nit = need_bytes.find({gth.src_shard, gth.src_item});
+    if (nit == need_bytes.end()) {
+      std::fill(want.begin(), want.end(), 1);
+    } else {
+      for (const auto& [lo, hi] : nit->second)
+        for (std::uint32_t b = chunk_at(lo) / dev::kBatchChunks;
+             b <= chunk_at(hi - 1) / dev::kBatchChunks && b < nb; ++b)
+          want[b] = 1;
+    }
+    std::uint64_t packed = 0;  // staging bytes so far
+    const std::size_t seg0 = rs.gather_segs.size();
+    for (std::uint32_t b0 = 0; b0 < nb;) {
+      if (!want[b0]) {
+        ++b0;
+        continue;
+      }
+      std::uint32_t b1 = b0;
+      while (b1 < nb && want[b1]) ++b1;
+      const std::uint32_t k0 = b0 * dev::kBatchChunks, k1 = std::min(n, b1 * dev::kBatchChunks);
+      // one window per run of wanted batches: its ranges are adjacent in the item
+      std::uint64_t win_lo = ~0ull, win_base = (packed + 255) / 256 * 256;
+      for (const ChunkPart& r : runs) {  // whole batches, cut at run boundaries
+        const std::uint32_t rk0 = std::max(k0, r.first), rk1 = std::min(k1, r.first + run_chunks(r));
+        if (rk0 >= rk1) continue;
+        const std::uint64_t off = r.off + std::uint64_t(rk0 - r.first) * r.chunk_len;
+        const std::uint64_t end = std::min<std::uint64_t>(r.off + r.len,
+                                                          r.off + std::uint64_t(rk1 - r.first) * r.chunk_len);
+        if (win_lo == ~0ull) win_lo = off;
+        dev::ItemDesc d{};
+        d.src = off;                         // + the source item's address at launch
+        d.dst = win_base + (off - win_lo);   // + the staging's address below
+        d.len = end - off;
+        d.chunk0 = next + rk0;
+        d.chunk_len = r.chunk_len;
+        d.src_chunk0 = ss.chunk0[gth.src_item] + rk0;
+        d.q = d.m = 1;
+        d.src_id = gth.src_shard;
+        rs.gather_segs.push_back(d);
+        rs.gather_items.push_back(gth.src_item);
+        packed = win_base + (end - win_lo);
+      }
+      if (win_lo != ~0ull) rs.gather_windows[gi].push_back({win_lo, win_lo + (packed - win_base), win_base});
+      b0 = b1;
+    }
+    auto buf = std::make_unique<DevBuf>();
+    if (Status s = buf->alloc(sh.device, std::max<std::uint64_t>(packed, 256)); !ok(s)) return s;
+    for (std::size_t k = seg0; k < rs.gather_segs.size(); ++k)
+      rs.gather_segs[k].dst += reinterpret_cast<std::uint64_t>(buf->p);
+    rs.gather_bufs.push_back(std::move(buf));
+    next += nb * dev::kBatchChunks;
+  }
+  rs.gather_chunks_end = next;
+  return Status::ok;
+}
+
+std::uint64_t Client::Reshard::staged(std::size_t gi, std::uint64_t item_off) const {
+  // the staging address of byte item_off of gather gi's source item
+  for (const auto& w : gather_windows[gi])
+    if (item_off >= w[0] && item_off < w[1])
+      return reinterpret_cast<std::uint64_t>(gather_bufs[gi]->p) + w[2] + (item_off - w[0]);
+  return 0;  // not landed: the plan never reads it
+}
+
 Status Client::launch_reshard_fill(Shard& sh, const Assignment& a, bool src_complete) {
   DeviceGuard g(sh.device);
   PhaseClock pc;
@@ -2024,82 +2114,8 @@ Status Client::launch_reshard_fill(Shard& sh, const Assignment& a, bool src_comp
     d.src = views[d.src_id].item_ptrs[d.pad] + d.src;
     d.pad = link_class(d.src_id);
   }
-  // Gathered source items (groups, unaligned slices) land in staging, but
-  // only the watermark batches that hold bytes some slice copy reads: a
-  // reader shard that needs a few members of a packed group does not pull
-  // (and verify) the rest of it.  Each range is whole batches of the item,
-  // so the kernel's batch -> segment mapping is unchanged.  The ranges are a
-  // function of the plan: built once per bind, re-addressed per launch.
-  if (rs.gather_segs.empty() && !rs.plan.gathers.empty()) {
-    std::map<std::pair<std::uint32_t, std::uint32_t>, std::vector<std::pair<std::uint64_t, std::uint64_t>>> need_bytes;
-    for (const auto& c : rs.plan.copies)
-      need_bytes[{c.src_shard, c.src_item}].emplace_back(c.src_off,
-                                                        c.src_off + (c.rows - 1) * c.src_stride + c.nc);
-    std::uint32_t next = rs.own_chunks;
-    for (std::size_t gi = 0; gi < rs.plan.gathers.size(); ++gi) {
-      const auto& gth = rs.plan.gathers[gi];
-      const SourceShard& ss = rs.srcs[gth.src_shard];
-      const auto& it = ss.manifest.items()[gth.src_item];
-      // the item's chunk runs (one for a uniform item; one per member of a
-      // member-cut group)
-      std::vector<ChunkPart> runs;
-      if (gth.src_item < ss.parts.size() && !ss.parts[gth.src_item].empty())
-        runs = ss.parts[gth.src_item];
-      else
-        runs.push_back(ChunkPart{0, it.length, ss.layout.chunk_len[gth.src_item], 0});
-      auto run_chunks = [](const ChunkPart& r) {
-        return static_cast<std::uint32_t>((r.len + r.chunk_len - 1) / r.chunk_len);
-      };
-      const std::uint32_t n = runs.back().first + run_chunks(runs.back());
-      const std::uint32_t nb = (n + dev::kBatchChunks - 1) / dev::kBatchChunks;
-      auto chunk_at = [&](std::uint64_t x) {  // the chunk holding byte x of the item
-        auto r = std::upper_bound(runs.begin(), runs.end(), x,
-                                  [](std::uint64_t v, const ChunkPart& p) { return v < p.off; });
-        --r;
-        return r->first + static_cast<std::uint32_t>((x - r->off) / r->chunk_len);
-      };
-      std::vector<char> want(nb, 0);
-      auto nit = need_bytes.find({gth.src_shard, gth.src_item});
-      if (nit == need_bytes.end()) {
-        std::fill(want.begin(), want.end(), 1);
-      } else {
-        for (const auto& [lo, hi] : nit->second)
-          for (std::uint32_t b = chunk_at(lo) / dev::kBatchChunks;
-               b <= chunk_at(hi - 1) / dev::kBatchChunks && b < nb; ++b)
-            want[b] = 1;
-      }
-      for (std::uint32_t b0 = 0; b0 < nb;) {
-        if (!want[b0]) {
-          ++b0;
-          continue;
-        }
-        std::uint32_t b1 = b0;
-        while (b1 < nb && want[b1]) ++b1;
-        const std::uint32_t k0 = b0 * dev::kBatchChunks, k1 = std::min(n, b1 * dev::kBatchChunks);
-        for (const ChunkPart& r : runs) {  // whole batches, cut at run boundaries
-          const std::uint32_t rk0 = std::max(k0, r.first), rk1 = std::min(k1, r.first + run_chunks(r));
-          if (rk0 >= rk1) continue;
-          const std::uint64_t off = r.off + std::uint64_t(rk0 - r.first) * r.chunk_len;
-          const std::uint64_t end = std::min<std::uint64_t>(r.off + r.len,
-                                                            r.off + std::uint64_t(rk1 - r.first) * r.chunk_len);
-          dev::ItemDesc d{};
-          d.src = off;  // + the source item's address at launch
-          d.dst = reinterpret_cast<std::uint64_t>(rs.gather_bufs[gi]->p) + off;
-          d.len = end - off;
-          d.chunk0 = next + rk0;
-          d.chunk_len = r.chunk_len;
-          d.src_chunk0 = ss.chunk0[gth.src_item] + rk0;
-          d.q = d.m = 1;
-          d.src_id = gth.src_shard;
-          rs.gather_segs.push_back(d);
-          rs.gather_items.push_back(gth.src_item);
-        }
-        b0 = b1;
-      }
-      next += nb * dev::kBatchChunks;
-    }
-    rs.gather_chunks_end = next;
-  }
+  // the gather segments (built at bind, build_gathers) re-addressed onto
+  // the sources' current mappings
   for (std::size_t k = 0; k < rs.gather_segs.size(); ++k) {
     dev::ItemDesc d = rs.gather_segs[k];
     d.src += views[d.src_id].item_ptrs[rs.gather_items[k]];
@@ -2187,7 +2203,10 @@ Status Client::finish_reshard(Shard& sh, const std::uint32_t* guard) {
   }
   std::vector<std::uint64_t> srcs, dsts, lens;
   for (const auto& c : rs.plan.copies) {
-    const auto base = reinterpret_cast<std::uint64_t>(rs.gather_bufs[gidx.at({c.src_shard, c.src_item})]->p);
+    const std::size_t gi = gidx.at({c.src_shard, c.src_item});
+    const std::uint64_t at = rs.staged(gi, c.src_off);  // the copy's first byte in staging
+    if (!at) return Status::protocol_error;
+    const std::uint64_t base = at - c.src_off;  // item offsets inside this copy's window
     if (!fused_items.empty()) {
       auto it = std::find_if(fused_items.begin(), fused_items.end(), [&](std::uint32_t i) {
         return c.dst >= p.item_ptrs[i] && c.dst < p.item_ptrs[i] + items[i].length;

@@ -18,6 +18,7 @@
 
 #include <cuda_runtime.h>
 
+#include <array>
 #include <atomic>
 #include <chrono>
 #include <cstdint>
@@ -391,6 +392,9 @@ class Client {
     std::vector<dev::ItemDesc> gather_segs;
     std::vector<std::uint32_t> gather_items;
     std::uint32_t gather_chunks_end = 0;
+    // per gather: the staging windows (item offset lo, hi, staging offset)
+    std::vector<std::vector<std::array<std::uint64_t, 3>>> gather_windows;
+    std::uint64_t staged(std::size_t gi, std::uint64_t item_off) const;
   };
   struct Payload {
     Manifest manifest;
@@ -483,6 +487,7 @@ class Client {
                 std::vector<std::uint32_t>* lens) const;
   Status alloc_tables(Shard& sh, Payload& p, std::uint32_t extra_chunks);
   Status launch_reshard_fill(Shard& sh, const Assignment& a, bool src_complete);
+  Status build_gathers(Shard& sh, Reshard& rs);
   // Queues the reshard's follow-up work behind its pull kernel on sh.stream
   // (slice copies, group packing, re-digests), skipped on the device when the
   // fill failed (guard = the fill's status code word).
