@@ -636,7 +636,7 @@ def run_single(args):
         line["e2e_device_resident"] = {"value": round(e2e, 2), "unit": UNIT,
                                        "what": "rs_replicate wall clock, version in the trainer's HBM"}
     if not args.no_cpu:
-        cb = cpu_reference_run(shapes, readers=1, steps=args.cpu_reps, warmup=0, verify=False)
+        cb = cpu_reference_run(shapes, readers=1, steps=args.cpu_reps, warmup=1, verify=False)  # the warm-up takes the landing buffers' first-touch page faults
         line["cpu_baseline"] = cb and {k: cb[k] for k in ("value", "unit", "cores", "nproc", "kind",
                                                           "sample")}
     print(json.dumps(line), flush=True)
