@@ -1474,6 +1474,23 @@ Status Client::bind_reshard(Shard& sh, const Assignment& a, VersionId v) {
           re.chunk0 = p->cmap.chunk0[i];
           re.chunk_len = p->cmap.chunk_len[i];
         }
+    } else if (!re.cast) {
+      // a member of a member-cut group of this reader: its place in the
+      // group's staging and its own run of chunks
+      const auto g = static_cast<std::uint32_t>(p->manifest.group_of(e));
+      for (std::uint32_t i = 0; i < items.size(); ++i) {
+        if (!items[i].is_group || items[i].index != g || !p->cmap.cut(i)) continue;
+        for (const auto& mem : p->manifest.groups[g].members) {
+          if (mem.entry != e) continue;
+          for (const ChunkPart& run : p->cmap.parts[i])
+            if (run.off == mem.offset) {
+              re.stage_ptr = reinterpret_cast<std::uint64_t>(p->group_bufs[g]->p) + mem.offset;
+              re.stage_chunk0 = p->cmap.chunk0[i] + run.first;
+              re.stage_chunk_len = run.chunk_len;
+              re.group_item = i;
+            }
+        }
+      }
     }
     rd.push_back(std::move(re));
   }
@@ -2253,11 +2270,19 @@ Status Client::finish_reshard(Shard& sh, const std::uint32_t* guard) {
     for (std::uint64_t r = 0; r < c.rows; ++r)
       add(base + c.src_off + r * c.src_stride, c.dst + r * c.dst_stride, c.nc);
   }
+  // groups the fill landed straight into their staging: unpack to the regions
+  const std::set<std::uint32_t> direct(rs.plan.direct_groups.begin(), rs.plan.direct_groups.end());
+  for (std::uint32_t i : direct)
+    for (const auto& mem : p.manifest.groups[items[i].index].members) {
+      srcs.push_back(reinterpret_cast<std::uint64_t>(p.group_bufs[items[i].index]->p) + mem.offset);
+      dsts.push_back(reinterpret_cast<std::uint64_t>(sh.regs[mem.entry].ptr));
+      lens.push_back(sh.regs[mem.entry].len);
+    }
   if (Status s = copy_spans(sh, srcs, dsts, lens, guard); !ok(s)) return s;
   if (terminal()) return Status::ok;  // a cast copy never re-serves: nothing to pack or digest
-  std::vector<std::uint32_t> group_items;
+  std::vector<std::uint32_t> group_items;  // re-digested: filled by copies
   for (std::uint32_t i = 0; i < items.size(); ++i)
-    if (items[i].is_group) group_items.push_back(i);
+    if (items[i].is_group && !direct.count(i)) group_items.push_back(i);
   // 3) digest + release the items whose bytes arrived by copy: the groups and
   //    big items sliced out of gathered source items (own chunk table and
   //    watermarks)

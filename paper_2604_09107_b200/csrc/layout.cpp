@@ -116,8 +116,12 @@ Status plan_reshard(const std::vector<ReaderEntry>& reader, const std::vector<So
   out->gathers.clear();
   out->copies.clear();
   out->rehash.clear();
+  out->direct_groups.clear();
   std::map<std::pair<std::uint32_t, std::uint32_t>, bool> gathered;
-  for (const auto& r : reader) {
+  // One reader entry's pieces, appended to `into`.  staged: the entry is a
+  // member of the reader's member-cut group and may land straight in the
+  // group's staging.
+  auto plan_one = [&](const ReaderEntry& r, ReshardPlan* into, bool staged) -> Status {
     const Geometry rg = r.geo.has() ? r.geo : full_geometry(r.len);
     std::uint64_t covered = 0;
     // Source slices already taken for this region.  Replicated tensors (a
@@ -164,17 +168,20 @@ Status plan_reshard(const std::vector<ReaderEntry>& reader, const std::vector<So
             run_first = p.first;
             member_run = true;
           }
-      const bool aligned = !r.in_group && (src_big || member_run) && c != 0 && c == r.chunk_len &&
+      // a member of this reader's own member-cut group lands in its group
+      // staging (staged), else the region itself
+      const std::uint32_t want_c = staged ? r.stage_chunk_len : r.chunk_len;
+      const bool aligned = (!r.in_group || staged) && (src_big || member_run) && c != 0 && c == want_c &&
                            (c0 - sg.c0) % c == 0 && (c1 - c0) % c == 0 && sg.nc % c == 0 &&
                            (c1 - c0) == rg.nc && sg.nc / c <= 0xffff;
       if (aligned) {
         dev::ItemDesc d{};
         // offset in the source item; its base address is added by the caller
         d.src = ioff + ((a - sg.r0) * sg.nc + (c0 - sg.c0));
-        d.dst = r.ptr + (a - rg.r0) * rg.nc / (r.cast ? 2 : 1);
+        d.dst = (staged ? r.stage_ptr : r.ptr) + (a - rg.r0) * rg.nc / (r.cast ? 2 : 1);
         d.len = (b - a) * (c1 - c0);
         const std::uint64_t m = sg.nc / c, q = (c1 - c0) / c;
-        d.chunk0 = r.chunk0 + static_cast<std::uint32_t>((a - rg.r0) * q);
+        d.chunk0 = (staged ? r.stage_chunk0 : r.chunk0) + static_cast<std::uint32_t>((a - rg.r0) * q);
         d.chunk_len = c | (r.cast ? dev::kCastE4M3 : 0u);
         d.src_chunk0 = ss.chunk0[item] + run_first +
                        static_cast<std::uint32_t>((a - sg.r0) * m + (c0 - sg.c0) / c);
@@ -182,11 +189,11 @@ Status plan_reshard(const std::vector<ReaderEntry>& reader, const std::vector<So
         d.m = static_cast<std::uint16_t>(m);
         d.src_id = si;
         d.pad = item;  // source item (base address looked up by the caller)
-        out->segs.push_back(d);
+        into->segs.push_back(d);
       } else {
         if (!gathered[{si, item}]) {
           gathered[{si, item}] = true;
-          out->gathers.push_back({si, item});
+          into->gathers.push_back({si, item});
         }
         SliceCopy cp;
         cp.src_shard = si;
@@ -199,13 +206,46 @@ Status plan_reshard(const std::vector<ReaderEntry>& reader, const std::vector<So
         cp.rows = b - a;
         cp.nc = c1 - c0;
         cp.cast = r.cast;
-        out->copies.push_back(cp);
+        into->copies.push_back(cp);
         if (!r.in_group && !r.cast &&
-            std::find(out->rehash.begin(), out->rehash.end(), r.item) == out->rehash.end())
-          out->rehash.push_back(r.item);
+            std::find(into->rehash.begin(), into->rehash.end(), r.item) == into->rehash.end())
+          into->rehash.push_back(r.item);
       }
     }
     if (covered != rg.nr * rg.nc || rg.nr * rg.nc != r.len) return Status::version_unavailable;
+    return Status::ok;
+  };
+  std::map<std::uint32_t, std::vector<const ReaderEntry*>> groups;  // reader group item -> members
+  for (const auto& r : reader) {
+    if (r.in_group && r.stage_ptr) {
+      groups[r.group_item].push_back(&r);
+      continue;
+    }
+    if (Status st = plan_one(r, out, false); !ok(st)) return st;
+  }
+  // A reader group lands straight from the sources only when every member
+  // does: its watermarks are released by the fill, so no member may still
+  // be on its way by copy.  Otherwise the whole group is copied and
+  // re-digested as before.
+  for (const auto& [gitem, members] : groups) {
+    ReshardPlan trial;
+    auto gathered_before = gathered;
+    bool direct = true;
+    for (const ReaderEntry* r : members) {
+      if (Status st = plan_one(*r, &trial, true); !ok(st)) return st;
+      if (!trial.copies.empty()) {
+        direct = false;
+        break;
+      }
+    }
+    if (direct) {
+      out->segs.insert(out->segs.end(), trial.segs.begin(), trial.segs.end());
+      out->direct_groups.push_back(gitem);
+      continue;
+    }
+    gathered = std::move(gathered_before);
+    for (const ReaderEntry* r : members)
+      if (Status st = plan_one(*r, out, false); !ok(st)) return st;
   }
   std::sort(out->segs.begin(), out->segs.end(),
             [](const dev::ItemDesc& x, const dev::ItemDesc& y) { return x.chunk0 < y.chunk0; });

@@ -99,6 +99,9 @@ struct ReshardPlan {
   std::vector<GatherNeed> gathers;  // whole source items to land in staging
   std::vector<SliceCopy> copies;    // staging -> reader regions
   std::vector<std::uint32_t> rehash;  // reader big items (partly) filled by copies
+  // reader groups landed straight into their staging by the fill (every
+  // member direct): unpacked to the regions, not re-digested
+  std::vector<std::uint32_t> direct_groups;
 };
 
 // Reader entry e (name, region address, geometry, own item index + chunk0 +
@@ -113,6 +116,12 @@ struct ReaderEntry {
   std::uint32_t item = 0;       // reader item (big entries)
   std::uint32_t chunk0 = 0;     // reader landing chunk index of the item
   std::uint32_t chunk_len = 0;  // reader chunk length of the item
+  // a member of the reader's own member-cut group: where it sits in the
+  // group's staging and its run of chunks (stage_ptr 0: not eligible)
+  std::uint64_t stage_ptr = 0;
+  std::uint32_t stage_chunk0 = 0;
+  std::uint32_t stage_chunk_len = 0;
+  std::uint32_t group_item = 0;
 };
 
 Status plan_reshard(const std::vector<ReaderEntry>& reader, const std::vector<SourceShard>& srcs,
