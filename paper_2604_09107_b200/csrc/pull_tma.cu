@@ -608,9 +608,10 @@ cudaError_t launch_variant(const PullParams& p, int sms, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-// The two shapes the product path launches.
+// The three shapes the product path launches.
 using V13 = Cfg<512, 2, 1, 320, 4, 4, true>;  // 4 two-stage pipelines per SM, dynamic batch claiming
 using V16 = Cfg<512, 2, 1, 320, 4, 1, true>;  // V13 releasing every batch at once (chain hops)
+using V15 = Cfg<512, 3, 1, 0, 4, 4, true>;    // 3 stages, segments in global: fused-cast pulls
 #ifdef RSB_ALL_VARIANTS
 // Diagnostic shapes from the round-1 sweeps (profiles/r1/variants*.txt);
 // built only with RSB_ALL_VARIANTS=1 (python -m paper_2604_09107_b200.build).
@@ -628,7 +629,6 @@ using V10 = Cfg<256, 5, 1, 128, 4>;
 using V11 = Cfg<512, 2, 1, 320, 4, 8>;   // V8, releasing 8 batches per fence
 using V12 = Cfg<512, 2, 1, 320, 4, 16>;  // V8, releasing 16 batches per fence
 using V14 = Cfg<256, 4, 1, 320, 4, 4, true>;  // V9 (4 stages of 256 B) with dynamic claiming
-using V15 = Cfg<512, 3, 1, 0, 4, 4, true>;    // V7 (3 stages, segments in global), dynamic
 using V17 = Cfg<512, 2, 1, 320, 4, 8, true>;  // V13 releasing 8 batches per fence
 #endif
 
@@ -654,11 +654,16 @@ cudaError_t launch_pull_tma(const PullParams& p, int sms, cudaStream_t s) {
   // 91-92%, its fastest pipelines idling at the tail; V0, 3 two-warp CTAs:
   // 88-90%), FSDP-8 -> TP-2 reshard 97.5% (V8: 91%); over NVLink equal to V8
   // (785 GB/s one way, 672 with both directions busy).
+  // A pull that lands e4m3 (has_cast) takes V15, a third stage per
+  // pipeline: the consumers also convert every value into the stage before
+  // the tensor store, and the deeper ring hides it (config 5 N=1: 4.17 ->
+  // 3.95 ms; V17, releasing 8 batches per fence: 4.08).
   int v = variant();
-  if (v < 0) v = p.remote == 2 ? 16 : 13;
+  if (v < 0) v = p.remote == 2 ? 16 : p.has_cast ? 15 : 13;
   switch (v) {
     case 13: return launch_variant<V13>(p, sms, s);
     case 16: return launch_variant<V16>(p, sms, s);
+    case 15: return launch_variant<V15>(p, sms, s);
 #ifdef RSB_ALL_VARIANTS
     case 0: return launch_variant<V0>(p, sms, s);
     case 1: return launch_variant<V1>(p, sms, s);
@@ -674,7 +679,6 @@ cudaError_t launch_pull_tma(const PullParams& p, int sms, cudaStream_t s) {
     case 11: return launch_variant<V11>(p, sms, s);
     case 12: return launch_variant<V12>(p, sms, s);
     case 14: return launch_variant<V14>(p, sms, s);
-    case 15: return launch_variant<V15>(p, sms, s);
     case 17: return launch_variant<V17>(p, sms, s);
 #endif
     default: return cudaErrorNotSupported;  // a shape this build does not carry: fail loudly
