@@ -112,3 +112,35 @@ def test_many_tiny_tensors_match_reference(oracle):
                 else oracle.publish_manifest(names, host, tiny, target))
         assert t.manifest(0) == want and r.manifest(0) == want
         assert np.array_equal(r.chunk_digests(0), t.chunk_digests(0))
+
+
+@pytest.mark.parametrize("seed", range(10))
+def test_random_cast_pull_matches_oracle(oracle, seed):
+    """Fused bf16 -> e4m3 landing (the three-stage V15 shape) over random
+    bf16 tensor sets: odd element counts, tensors that straddle the tiny
+    threshold (packed members land as e4m3 through the group path)."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    rng = np.random.default_rng(40_000 + seed)
+    tiny = int([64 << 10, 1 << 20][int(rng.integers(0, 2))])
+    elems = [int(rng.integers(1, 3 << 20)) if rng.random() < 0.5 else int(rng.integers(1, tiny // 2))
+             for _ in range(int(rng.integers(2, 10)))]
+    host = [oracle.synth_bf16(900 * seed + i, n) for i, n in enumerate(elems)]
+    dev = torch.device("cuda:0")
+    with Cluster() as cl:
+        t = cl.open("m", "trainer", 1, tiny_threshold=tiny)
+        r = cl.open("m", "fp8", 1, tiny_threshold=tiny)
+        outs = []
+        for i, a in enumerate(host):
+            x = torch.from_numpy(a.view(np.int16).copy()).to(dev)
+            y = torch.zeros(a.size, dtype=torch.uint8, device=dev)
+            outs.append(y)
+            assert t.register_tensor(0, f"w{i}", x) == Status.ok
+            assert r.register_cast(0, f"w{i}", y, a.nbytes) == Status.ok
+        assert t.publish(1).status == Status.ok
+        res = r.replicate()
+        assert res.status == Status.ok, (seed, res)
+        torch.cuda.synchronize()
+        for a, y in zip(host, outs):
+            assert np.array_equal(y.cpu().numpy(), oracle.bf16_to_e4m3(a)), seed
+        assert np.array_equal(r.chunk_digests(0), t.chunk_digests(0))
